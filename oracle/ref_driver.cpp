@@ -1,0 +1,355 @@
+// ref_driver.cpp — C entry points into the UNMODIFIED reference library
+// (/root/reference/proj/core, compiled from its own sources by oracle/Makefile
+// into oracle/_ref/).  TEST INFRASTRUCTURE: used to generate the golden
+// fixtures, to pin the C restatement (pcal_oracle.c), and as bench.py's
+// `--impl reference` CPU arm.  Nothing of the product links this.
+//
+// The grid models of configs 3–5 do not exist in the reference; they are
+// plugged into the reference solve() as ObjectiveModel subclasses whose
+// evaluate() calls the restatement in pcal_oracle.c.
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "orthopt/diagnostics.hpp"
+#include "orthopt/kernels.hpp"
+#include "orthopt/problems.hpp"
+#include "orthopt/rng.hpp"
+#include "orthopt/solver.hpp"
+#include "pcal_oracle.h"
+
+using namespace orthopt;
+
+namespace {
+
+thread_local std::string g_err;
+
+// Grid model adapter: reference ObjectiveModel backed by the oracle restatement.
+class GridModel : public ObjectiveModel {
+ public:
+  GridModel(const orc_model& m, std::vector<double> v)
+      : ObjectiveModel(m.n, m.p, m.kind == ORC_MODEL_STENCIL ? ProblemKind::P3 : ProblemKind::P6,
+                       m.s),
+        m_(m),
+        v_(std::move(v)) {
+    m_.v = v_.data();
+    m_.work = nullptr;
+    orc_model_prepare(&m_);
+  }
+  ~GridModel() override { orc_model_release(&m_); }
+  Evaluation evaluate(const DenseMatrix& x, int threads) const override {
+    if (x.rows() != n_ || x.cols() != p_) throw dimension_error("evaluate: iterate shape mismatch");
+    Evaluation ev;
+    ev.gradient = DenseMatrix(n_, p_);
+    const int rc = orc_evaluate(&m_, x.data(), &ev.value, ev.gradient.data(), threads);
+    if (rc) throw evaluation_error("GridModel: non-finite objective or gradient");
+    return ev;
+  }
+  void save(std::ostream&) const override { throw io_error("GridModel: not serializable"); }
+
+ private:
+  orc_model m_;
+  std::vector<double> v_;
+};
+
+DenseMatrix from_ptr(const double* p, std::int64_t r, std::int64_t c) {
+  DenseMatrix m(r, c);
+  std::memcpy(m.data(), p, sizeof(double) * static_cast<size_t>(r * c));
+  return m;
+}
+
+SquareSymmetric sym_from_ptr(const double* p, std::int64_t n) {
+  SquareSymmetric s(n);
+  for (std::int64_t j = 0; j < n; ++j)
+    for (std::int64_t i = 0; i <= j; ++i) s.set_mirrored(i, j, p[i + j * n]);
+  return s;
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    return f();
+  } catch (const parameter_error& e) {
+    g_err = e.what();
+    return ORC_E_PARAM;
+  } catch (const dimension_error& e) {
+    g_err = e.what();
+    return ORC_E_DIM;
+  } catch (const rank_error& e) {
+    g_err = e.what();
+    return ORC_E_RANK;
+  } catch (const evaluation_error& e) {
+    g_err = e.what();
+    return ORC_E_EVAL;
+  } catch (const divergence_error& e) {
+    g_err = e.what();
+    return ORC_E_DIVERGE;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -99;
+  }
+}
+
+SolverConfig to_config(const orc_config* c) {
+  SolverConfig cfg;
+  cfg.algorithm = Algorithm::Pcal;
+  cfg.beta = c->beta;
+  cfg.eta_rule.kind = static_cast<StepsizeRule::Kind>(c->eta_kind);
+  cfg.eta_rule.gamma = c->gamma;
+  cfg.eta_rule.eta_min = c->eta_min;
+  cfg.eta_rule.eta_max = c->eta_max;
+  cfg.eta_rule.eta0 = c->eta0;
+  cfg.multiplier_rule =
+      c->multiplier_rule == ORC_MULT_PCAL ? MultiplierRule::PcalFormula : MultiplierRule::PlamFormula;
+  cfg.tol_rel_kkt = c->tol_rel_kkt;
+  cfg.max_iter = c->max_iter;
+  cfg.threads = c->threads;
+  cfg.final_orth = c->final_orth != 0;
+  return cfg;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+// --- problem construction (problems.cpp) --------------------------------
+// Dense trace minimization of configs 1–2: A = sym_part(random_normal(n,n,Rng(seed)))
+// (problems.cpp:45-48 via gen_problem1(α=0, RandomSym)); s from
+// spectral_norm_estimate(A, seed ^ 0x73706563) (problems.cpp:215) unless s_in >= 0.
+void* ref_make_dense_trace_min(std::int64_t n, std::int64_t p, std::uint64_t seed, double s_in,
+                               int threads, double* a_out, double* s_out) {
+  void* out = nullptr;
+  guarded([&] {
+    Rng rng(seed);
+    SquareSymmetric a = sym_part(random_normal(n, n, rng));
+    const double s = s_in >= 0.0 ? s_in : spectral_norm_estimate(a, seed ^ 0x73706563u, threads);
+    if (a_out) std::memcpy(a_out, a.matrix().data(), sizeof(double) * static_cast<size_t>(n * n));
+    if (s_out) *s_out = s;
+    out = make_quadratic(std::move(a), DenseMatrix(n, p), ProblemKind::P3, s, threads).release();
+    return 0;
+  });
+  return out;
+}
+
+void* ref_make_quadratic(const double* a, const double* g0, std::int64_t n, std::int64_t p,
+                         double s) {
+  void* out = nullptr;
+  guarded([&] {
+    DenseMatrix g = g0 ? from_ptr(g0, n, p) : DenseMatrix(n, p);
+    out = make_quadratic(sym_from_ptr(a, n), std::move(g), g0 ? ProblemKind::P2 : ProblemKind::P3,
+                         s)
+              .release();
+    return 0;
+  });
+  return out;
+}
+
+void* ref_make_grid_model(int kind, std::int64_t nx, std::int64_t ny, std::int64_t nz,
+                          std::int64_t p, const double* v, double s) {
+  void* out = nullptr;
+  guarded([&] {
+    orc_model m{};
+    m.kind = kind;
+    m.nx = nx;
+    m.ny = ny;
+    m.nz = nz;
+    m.n = nx * ny * nz;
+    m.p = p;
+    m.s = s;
+    out = new GridModel(m, std::vector<double>(v, v + m.n));
+    return 0;
+  });
+  return out;
+}
+
+void ref_free_model(void* m) { delete static_cast<ObjectiveModel*>(m); }
+
+int ref_evaluate(void* model, const double* x, double* f, double* g) {
+  return guarded([&] {
+    auto* m = static_cast<ObjectiveModel*>(model);
+    Evaluation ev = m->evaluate(from_ptr(x, m->n(), m->p()), 1);
+    *f = ev.value;
+    std::memcpy(g, ev.gradient.data(), sizeof(double) * ev.gradient.size());
+    return 0;
+  });
+}
+
+double ref_fd_gradient_check(void* model, const double* x, double h, std::uint64_t seed) {
+  double r = -1.0;
+  guarded([&] {
+    auto* m = static_cast<ObjectiveModel*>(model);
+    r = fd_gradient_check(*m, from_ptr(x, m->n(), m->p()), h, seed);
+    return 0;
+  });
+  return r;
+}
+
+// --- kernels / setup -------------------------------------------------------
+int ref_random_normal(std::int64_t rows, std::int64_t cols, std::uint64_t seed, double* out) {
+  return guarded([&] {
+    Rng rng(seed);
+    DenseMatrix m = random_normal(rows, cols, rng);
+    std::memcpy(out, m.data(), sizeof(double) * m.size());
+    return 0;
+  });
+}
+
+int ref_initial_point(int mode, double sigma, std::uint64_t seed, std::int64_t n, std::int64_t p,
+                      double* out) {
+  return guarded([&] {
+    DenseMatrix x = initial_point({static_cast<InitMode>(mode), sigma, seed}, n, p);
+    std::memcpy(out, x.data(), sizeof(double) * x.size());
+    return 0;
+  });
+}
+
+double ref_spectral_norm_estimate(const double* a, std::int64_t n, std::uint64_t seed, int threads) {
+  double r = -1.0;
+  guarded([&] {
+    r = spectral_norm_estimate(sym_from_ptr(a, n), seed, threads);
+    return 0;
+  });
+  return r;
+}
+
+int ref_orthonormalize(const double* x, std::int64_t n, std::int64_t p, double* q) {
+  return guarded([&] {
+    DenseMatrix r = orthonormalize(from_ptr(x, n, p));
+    std::memcpy(q, r.data(), sizeof(double) * r.size());
+    return 0;
+  });
+}
+
+int ref_gram(const double* x, std::int64_t n, std::int64_t p, double* g) {
+  return guarded([&] {
+    SquareSymmetric s = gram(from_ptr(x, n, p), 1);
+    std::memcpy(g, s.matrix().data(), sizeof(double) * static_cast<size_t>(p * p));
+    return 0;
+  });
+}
+
+int ref_matmul_at_b(const double* a, const double* b, std::int64_t n, std::int64_t pa,
+                    std::int64_t pb, double* c) {
+  return guarded([&] {
+    DenseMatrix r = matmul_at_b(from_ptr(a, n, pa), from_ptr(b, n, pb), 1);
+    std::memcpy(c, r.data(), sizeof(double) * r.size());
+    return 0;
+  });
+}
+
+int ref_matmul(const double* a, const double* b, std::int64_t m, std::int64_t k, std::int64_t nc,
+               double* c, int threads) {
+  return guarded([&] {
+    DenseMatrix r = matmul(from_ptr(a, m, k), from_ptr(b, k, nc), threads);
+    std::memcpy(c, r.data(), sizeof(double) * r.size());
+    return 0;
+  });
+}
+
+int ref_pcal_step(const double* x, const double* gl, std::int64_t n, std::int64_t p, double eta,
+                  double* out, std::int64_t* degenerate) {
+  return guarded([&] {
+    PcalStepResult r = pcal_step(from_ptr(x, n, p), from_ptr(gl, n, p), eta, 1);
+    std::memcpy(out, r.x.data(), sizeof(double) * r.x.size());
+    *degenerate = r.degenerate_columns;
+    return 0;
+  });
+}
+
+double ref_stepsize_select(const orc_config* c, std::int64_t iter, double eta_prev, double eta0,
+                           const double* x, const double* xp, const double* gl,
+                           const double* glp, std::int64_t n, std::int64_t p) {
+  double r = -1.0;
+  guarded([&] {
+    SolverState st;
+    st.x = from_ptr(x, n, p);
+    st.grad_l = from_ptr(gl, n, p);
+    if (xp) st.prev_x = from_ptr(xp, n, p);
+    if (glp) st.prev_grad_l = from_ptr(glp, n, p);
+    st.iter = iter;
+    st.eta = eta_prev;
+    st.eta0 = eta0;
+    r = stepsize_select(to_config(c).eta_rule, st);
+    return 0;
+  });
+  return r;
+}
+
+double ref_kkt_violation(void* model, const double* x) {
+  double r = -1.0;
+  guarded([&] {
+    auto* m = static_cast<ObjectiveModel*>(model);
+    r = kkt_violation(*m, from_ptr(x, m->n(), m->p()), 1);
+    return 0;
+  });
+  return r;
+}
+
+double ref_feasibility_violation(const double* x, std::int64_t n, std::int64_t p) {
+  return feasibility_violation(from_ptr(x, n, p), 1);
+}
+
+double ref_flops_estimate_pcal(std::int64_t n, std::int64_t p) {
+  return flops_estimate(Algorithm::Pcal, n, p);
+}
+
+// --- solve() ---------------------------------------------------------------
+// Fills the same orc_report layout as the restatement.  Returns a negative
+// ORC_E_* code when solve() throws (parameter/dimension errors).
+int ref_solve(void* model, const orc_config* c, const double* x0, orc_report* r,
+              double* timers /* blas3, func, orth or NULL */) {
+  return guarded([&] {
+    auto* m = static_cast<ObjectiveModel*>(model);
+    CategoryTimers t;
+    RunReport rep = solve(*m, to_config(c), from_ptr(x0, m->n(), m->p()), timers ? &t : nullptr);
+    r->trace_len = static_cast<std::int64_t>(rep.trace.size());
+    for (size_t i = 0; i < rep.trace.size(); ++i) {
+      double* row = r->trace + i * ORC_TRACE_COLS;
+      const MetricSample& s = rep.trace[i];
+      row[0] = static_cast<double>(s.iter);
+      row[1] = s.fval;
+      row[2] = s.kkt_abs;
+      row[3] = s.kkt_rel;
+      row[4] = s.feas;
+      row[5] = s.eta;
+      row[6] = s.elapsed;
+    }
+    r->final_pre[0] = rep.final_pre_orth.fval;
+    r->final_pre[1] = rep.final_pre_orth.kkt_abs;
+    r->final_pre[2] = rep.final_pre_orth.kkt_rel;
+    r->final_pre[3] = rep.final_pre_orth.feas;
+    r->has_post = rep.final_post_orth.has_value();
+    if (r->has_post) {
+      r->final_post[0] = rep.final_post_orth->fval;
+      r->final_post[1] = rep.final_post_orth->kkt_abs;
+      r->final_post[2] = rep.final_post_orth->kkt_rel;
+      r->final_post[3] = rep.final_post_orth->feas;
+    }
+    r->has_x = !rep.stop_iterate.empty();
+    if (r->has_x && r->stop_x)
+      std::memcpy(r->stop_x, rep.stop_iterate.data(), sizeof(double) * rep.stop_iterate.size());
+    if (r->has_x && r->final_x)
+      std::memcpy(r->final_x, rep.final_x.data(), sizeof(double) * rep.final_x.size());
+    r->iterations = rep.iterations;
+    r->degenerate_steps = rep.degenerate_steps;
+    r->wall_time = rep.wall_time;
+    r->status = rep.status == RunStatus::Converged ? ORC_CONVERGED
+                : rep.status == RunStatus::MaxIter ? ORC_MAXITER
+                                                    : ORC_DIVERGED;
+    r->beta_used = rep.config.beta;
+    r->eta0_used = rep.trace.empty() ? 0.0 : rep.trace.front().eta;
+    if (timers) {
+      timers[0] = t.blas3;
+      timers[1] = t.func;
+      timers[2] = t.orth;
+    }
+    return 0;
+  });
+}
+
+}  // extern "C"
