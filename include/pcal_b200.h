@@ -1,0 +1,200 @@
+/*
+ * pcal_b200.h — C ABI of the B200-native PCAL iteration (libpcal_b200.so).
+ *
+ * This is the drop-in boundary for the reference's solver entry point
+ *   orthopt::RunReport orthopt::solve(const ObjectiveModel&, const SolverConfig&,
+ *                                      const DenseMatrix& x0, CategoryTimers*)
+ *   (/root/reference/proj/core/include/orthopt/solver.hpp:120-121)
+ * restated with plain pointers and sizes.  Matrices are FP64, column-major
+ * (element (i,j) at data[i + j*rows]) exactly like orthopt::DenseMatrix
+ * (matrix.hpp:38-45), so host buffers round-trip without transposes.
+ *
+ * The reference's virtual gradient callback ObjectiveModel::evaluate
+ * (problems.hpp:39) cannot be a host callback here (X lives in HBM), so the
+ * model is a descriptor of a device-evaluated objective (pcal_model_desc):
+ * dense quadratic (QuadraticModel, problems.hpp:53-69), 7-point periodic
+ * stencil + diagonal potential, or the Kohn–Sham-like density model.  An
+ * unsupported model is an error; there is no CPU fallback.
+ *
+ * Errors the reference throws out of solve() (parameter_error, dimension_error,
+ * solver.cpp:106-118,628-630) are returned as negative codes with a message in
+ * pcal_last_error().  In-run failures (divergence_error / evaluation_error /
+ * rank_error, solver.cpp:460-471) are NOT errors: the report carries
+ * status = PCAL_STATUS_DIVERGED and a partial trace, as in the reference.
+ */
+#ifndef PCAL_B200_H
+#define PCAL_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* return codes */
+#define PCAL_OK 0
+#define PCAL_E_PARAMETER (-1)   /* orthopt::parameter_error   (errors.hpp:24-28) */
+#define PCAL_E_DIMENSION (-2)   /* orthopt::dimension_error   (errors.hpp:9-13)  */
+#define PCAL_E_RANK (-3)        /* orthopt::rank_error        (errors.hpp:15-19) */
+#define PCAL_E_UNSUPPORTED (-4) /* model/algorithm not provided by this library   */
+#define PCAL_E_CUDA (-5)        /* CUDA runtime failure / no device               */
+#define PCAL_E_STATE (-6)       /* API misuse (e.g. reading an unfinished run)     */
+#define PCAL_E_DIVERGENCE (-7)  /* building blocks only: orthopt::divergence_error (errors.hpp:33-45) */
+#define PCAL_E_EVALUATION (-8)  /* building blocks only: orthopt::evaluation_error (errors.hpp:27-31) */
+
+/* run status — orthopt::RunStatus (report.hpp:37) */
+#define PCAL_STATUS_CONVERGED 0
+#define PCAL_STATUS_MAX_ITER 1
+#define PCAL_STATUS_DIVERGED 2
+
+/* model kinds */
+#define PCAL_MODEL_DENSE 1      /* f = ½tr(XᵀAX) + tr(G0ᵀX), A n×n symmetric (problems.cpp:130-141) */
+#define PCAL_MODEL_STENCIL 2    /* f = ½tr(XᵀLX) + ½tr(XᵀVX), L = −Δ_h 7-point periodic */
+#define PCAL_MODEL_KOHN_SHAM 3  /* E = ¼tr(XᵀLX)+½tr(XᵀV_ionX)+¼ρᵀL†ρ+½ρᵀε_xc(ρ) */
+
+/* pointer location for model data / x0 */
+#define PCAL_HOST 0
+#define PCAL_DEVICE 1
+
+/* StepsizeRule::Kind (solver.hpp:13-20), same order */
+#define PCAL_ETA_CONSTANT 0
+#define PCAL_ETA_DIFFERENTIAL 1
+#define PCAL_ETA_BB1 2
+#define PCAL_ETA_BB2 3
+#define PCAL_ETA_ABB 4
+
+/* MultiplierRule (solver.hpp:22) */
+#define PCAL_MULT_PLAM_FORMULA 0
+#define PCAL_MULT_PCAL_FORMULA 1
+
+/* Algorithm (diagnostics.hpp:10): this library implements PCAL only. */
+#define PCAL_ALG_PCAL 1
+
+typedef struct pcal_model_desc {
+  int32_t kind;          /* PCAL_MODEL_* */
+  int32_t location;      /* PCAL_HOST / PCAL_DEVICE for a, g0, v */
+  int64_t n, p;          /* ObjectiveModel::n(), p() */
+  double s;              /* ObjectiveModel::curvature_scale() (sets eta0 = s + 2β) */
+  const double* a;       /* dense: n×n column-major, symmetric */
+  const double* g0;      /* dense: n×p linear term or NULL (zero) */
+  int64_t nx, ny, nz;    /* grid models: n = nx·ny·nz, row i = x + nx·(y + ny·z) */
+  const double* v;       /* stencil: V (n); Kohn–Sham: V_ion (n) */
+} pcal_model_desc;
+
+typedef struct pcal_config {  /* orthopt::SolverConfig (solver.hpp:30-42) */
+  int32_t algorithm;          /* PCAL_ALG_PCAL */
+  double beta;                /* < 0: PCAL default 1.0 (solver.cpp:120-125) */
+  int32_t eta_kind;           /* PCAL_ETA_* */
+  double gamma;               /* Constant rule only */
+  double eta_min, eta_max;    /* safeguard interval */
+  double eta0;                /* <= 0: s + 2β */
+  int32_t multiplier_rule;    /* PCAL_MULT_* */
+  double tol_rel_kkt;
+  int64_t max_iter;
+  int32_t final_orth;
+  int32_t device;             /* CUDA device ordinal ("threads" is never ambient, SPEC §) */
+} pcal_config;
+
+#define PCAL_TRACE_COLS 7     /* iter, fval, kkt_abs, kkt_rel, feas, eta, elapsed (report.hpp:13-21) */
+
+typedef struct pcal_report {  /* orthopt::RunReport (report.hpp:51-64) */
+  double* trace;              /* caller buffer: trace_capacity × PCAL_TRACE_COLS (row-major) */
+  int64_t trace_capacity;     /* >= max_iter + 1 */
+  int64_t trace_len;
+  double final_pre[4];        /* fval, kkt_abs, kkt_rel, feas */
+  double final_post[4];
+  int32_t has_post;
+  double* stop_x;             /* caller buffer n×p, or NULL */
+  double* final_x;            /* caller buffer n×p, or NULL */
+  int32_t has_x;              /* 0 when the run diverged (reference leaves them empty) */
+  int64_t iterations;
+  int64_t degenerate_steps;
+  double wall_time;           /* seconds */
+  int32_t status;             /* PCAL_STATUS_* */
+  double beta;                /* resolved penalty */
+  double eta0;                /* resolved first stepsize */
+} pcal_report;
+
+typedef struct pcal_category_timers { /* orthopt::CategoryTimers (report.hpp:66-72), seconds */
+  double blas3, func, orth;
+} pcal_category_timers;
+
+/* Defaults of SolverConfig (PCAL, β auto, ABB, PcalFormula, tol 1e-8, 3000 iters). */
+void pcal_config_default(pcal_config* c);
+
+/* orthopt::solve — the drop-in entry point (host buffers; copies in/out inside). */
+int pcal_solve(const pcal_model_desc* model, const pcal_config* config, const double* x0,
+               int32_t x0_location, pcal_report* report, pcal_category_timers* timers);
+
+/* Thread-local message for the last failing call. */
+const char* pcal_last_error(void);
+
+/* ---- device-resident session (the same solver, split into its phases) -----
+ * create uploads/adopts the model and x0 and evaluates the start point (trace
+ * row 0); run enqueues iterations on the session stream without a host sync;
+ * finish performs the final orthonormalization and fills the report. */
+typedef struct pcal_session pcal_session;
+
+int pcal_session_create(const pcal_model_desc* model, const pcal_config* config,
+                        const double* x0, int32_t x0_location, pcal_session** out);
+/* Enqueue up to `iters` more iterations (stops early once converged/diverged). */
+int pcal_session_run(pcal_session* s, int64_t iters);
+int pcal_session_sync(pcal_session* s);
+/* cudaStream_t of the session, as void*, for event timing by the caller. */
+void* pcal_session_stream(pcal_session* s);
+int pcal_session_finish(pcal_session* s, pcal_report* report);
+void pcal_session_destroy(pcal_session* s);
+/* Teacher forcing: replace the state by (X_{k-1}, X_k) at iteration k with the
+ * previous stepsize eta_prev (k = 0: x_prev ignored).  Host buffers. */
+int pcal_session_set_state(pcal_session* s, const double* x_prev, const double* x, int64_t k,
+                           double eta_prev);
+/* Copy the current iterate X_k (host buffer n×p) and the last stepsize. */
+int pcal_session_get_x(pcal_session* s, double* x_out, double* eta_out, int64_t* k_out);
+/* Device pointer of the current iterate (column-major, leading dimension *ld). */
+int pcal_session_device_x(pcal_session* s, const double** x, int64_t* ld);
+/* Number of kernels this library launched since session creation. */
+int64_t pcal_session_kernel_launches(pcal_session* s);
+/* Per-iteration launch count of the captured iteration graph. */
+int64_t pcal_session_kernels_per_iteration(pcal_session* s);
+
+/* ---- building blocks (host buffers; for parity tests and tools) ---------- */
+/* C = Aᵀ·B for n×pa and n×pb (kernels.cpp:124-137 matmul_at_b). */
+int pcal_matmul_at_b(const double* a, const double* b, int64_t n, int64_t pa, int64_t pb,
+                     double* c, int32_t device);
+/* C = A·B, m×k times k×nc (kernels.cpp:105-122 matmul). */
+int pcal_matmul(const double* a, const double* b, int64_t m, int64_t k, int64_t nc, double* c,
+                int32_t device);
+/* XᵀX, exactly symmetric (kernels.cpp:139-153 gram). */
+int pcal_gram(const double* x, int64_t n, int64_t p, double* g, int32_t device);
+/* CholeskyQR2 with MGS2 fallback (kernels.cpp:250-265 orthonormalize);
+ * PCAL_E_RANK when rank-deficient. */
+int pcal_orthonormalize(const double* x, int64_t n, int64_t p, double* q, int32_t device);
+/* ObjectiveModel::evaluate on the device (f and G = ∇f at x). */
+int pcal_evaluate(const pcal_model_desc* model, const double* x, double* f, double* g,
+                  int32_t device);
+/* pcal_step (solver.cpp:264-307): per-column normalized proximal step. */
+int pcal_pcal_step(const double* x, const double* grad_l, int64_t n, int64_t p, double eta,
+                   double* out, int64_t* degenerate_columns, int32_t device);
+/* Power iteration on A² (kernels.cpp:267-293 spectral_norm_estimate), device matvecs,
+ * start vector from the reference Rng(seed). */
+int pcal_spectral_norm_estimate(const double* a, int64_t n, uint64_t seed, double* s,
+                                int32_t device);
+/* flops_estimate(Pcal, n, p) (diagnostics.cpp:100-114). */
+double pcal_flops_estimate(int64_t n, int64_t p);
+
+/* ---- problem setup on the host (reference generators, problems.cpp) ------ */
+/* random_normal(rows, cols, Rng(seed)) (kernels.cpp:49-55), bitwise equal;
+ * `threads` host threads (checkpointed generator states). */
+int pcal_random_normal(int64_t rows, int64_t cols, uint64_t seed, double* out, int32_t threads);
+int pcal_random_uniform(int64_t count, uint64_t seed, double* out);
+/* sym_part(random_normal(n, n, Rng(seed))) — the dense operator of configs 1–2
+ * (problems.cpp:45-48). */
+int pcal_gen_dense_operator(int64_t n, uint64_t seed, double* a, int32_t threads);
+/* initial_point({Qr}, n, p) on the device: orthonormalize(random_normal(n,p,Rng(seed)))
+ * (solver.cpp:136-142). */
+int pcal_initial_point_qr(int64_t n, int64_t p, uint64_t seed, double* x0, int32_t device);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PCAL_B200_H */

@@ -1,0 +1,165 @@
+"""Generate tests/golden/*.npz from the UNMODIFIED reference (oracle/_ref).
+
+Run in the build container (where /root/reference exists):
+    python -m oracle.make_golden            # small fixtures (seconds)
+    python -m oracle.make_golden --cfg2     # + config-2 prefix (several minutes)
+
+The fixtures pin the C restatement (tests/test_oracle_golden.py, CPU) and are
+the parity anchors of the GPU tests.  Large matrices are stored as SHA-256 of
+their little-endian bytes plus small slices.
+"""
+from __future__ import annotations
+
+import hashlib
+import os
+import sys
+
+import numpy as np
+
+from oracle.oracle import Config, Model, Reference, MODEL_DENSE, MODEL_STENCIL, MODEL_KOHN_SHAM
+
+OUT = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden")
+TINY = np.finfo(float).tiny
+INIT_SALT = 0x1235713      # harness.cpp:18
+SPECTRAL_SALT = 0x73706563  # problems.cpp:19
+
+
+def sha(a: np.ndarray) -> str:
+    return hashlib.sha256(np.asfortranarray(a, dtype="<f8").tobytes(order="F")).hexdigest()
+
+
+def run_case(R: Reference, model: Model, x0, **cfg) -> dict:
+    rep = R.solve(model, Config(**cfg), x0)
+    out = {"trace": rep.trace[:, :6], "final_pre": rep.final_pre, "iterations": rep.iterations,
+           "degenerate_steps": rep.degenerate_steps, "status": rep.status,
+           "beta": rep.beta, "eta0": rep.eta0}
+    out["final_post"] = rep.final_post if rep.final_post is not None else np.full(4, np.nan)
+    if rep.final_x is not None:
+        out["final_x_sha"] = sha(rep.final_x)
+        out["stop_x_sha"] = sha(rep.stop_x)
+    return out, rep
+
+
+def small(R: Reference) -> None:
+    os.makedirs(OUT, exist_ok=True)
+    g = {}
+    # --- RNG stream (rng.hpp, kernels.cpp:49-78)
+    g["normal_seed1"] = R.random_normal(1001, 1, 1)[:, 0]
+    g["normal_seed_init1"] = R.random_normal(21, 1, 1 ^ INIT_SALT)[:, 0]
+    # --- kernels (kernels.cpp)
+    a = R.random_normal(37, 5, 3)
+    b = R.random_normal(37, 4, 4)
+    g["k_a"], g["k_b"] = a, b
+    g["k_matmul_at_b"] = R.matmul_at_b(a, b)
+    g["k_gram"] = R.gram(a)
+    c = R.random_normal(5, 6, 5)
+    g["k_c"] = c
+    g["k_matmul"] = R.matmul(a, c)
+    x = R.random_normal(30, 4, 6)
+    g["k_orth_x"] = x
+    g["k_orth_q"] = R.orthonormalize(x)
+    s50 = R.random_normal(50, 50, 7)
+    sym = 0.5 * (s50 + s50.T)
+    g["k_spec_a"] = np.asfortranarray(sym)
+    g["k_spec_s"] = R.spectral_norm_estimate(sym, 11)
+    # --- pcal_step known answers (test_solver.cpp:244-272 shapes)
+    xs = R.random_normal(30, 5, 15)
+    gs = R.random_normal(30, 5, 16)
+    g["ps_x"], g["ps_g"] = xs, gs
+    g["ps_out"], _ = R.pcal_step(xs, gs, 2.0)
+    # --- stepsize_select closed forms (test_solver.cpp:167-224)
+    X = np.array([[1.0], [1.0]]); Xp = np.zeros((2, 1)); G = np.array([[1.0], [3.0]]); Gp = np.zeros((2, 1))
+    etas = []
+    for kind, it in [(2, 1), (3, 1), (4, 1), (4, 2), (1, 2)]:
+        etas.append(R.stepsize_select(Config(eta_kind=kind), it, 0.5, 0.25, X, Xp, G, Gp))
+    g["ss_etas"] = np.array(etas)
+    # --- cfg1 (n=1000, p=20, seed 1): the north-star CPU-runnable config
+    m1 = R.dense_trace_min(1000, 20, 1)
+    x01 = R.initial_point_qr(1000, 20, 1 ^ INIT_SALT)
+    g["cfg1_s"] = m1.s
+    g["cfg1_a_sha"] = sha(m1.a)
+    g["cfg1_x0_sha"] = sha(x01)
+    case, rep = run_case(R, m1, x01, tol_rel_kkt=TINY, max_iter=200, threads=8)
+    for k, v in case.items():
+        g["cfg1_" + k] = v
+    g["cfg1_final_x_rows"] = rep.final_x[:8]
+    g["cfg1_stop_x_rows"] = rep.stop_x[:8]
+    # --- small dense cases from the reference's own tests
+    cases = [("c40", 40, 5, 24, 25, {}), ("c12", 12, 2, 57, 58, {}),
+             ("c20", 20, 4, 22, 23, {"max_iter": 40, "final_orth": False}),
+             ("c14plam", 14, 3, 59, 60, {"multiplier_rule": 0}),
+             ("c200", 200, 10, 101, 102, {})]
+    for name, n, p, sa, sx, kw in cases:
+        r = R.random_normal(n, n, sa)
+        A = np.asfortranarray(0.5 * (r + r.T))
+        s = R.spectral_norm_estimate(A, SPECTRAL_SALT)  # make_quadratic default (problems.cpp:292)
+        mod = Model(MODEL_DENSE, n, p, s, a=A)
+        x0 = R.initial_point_qr(n, p, sx)
+        cfg = {"threads": 1}
+        cfg.update(kw)
+        case, rep = run_case(R, mod, x0, **cfg)
+        g[name + "_a_seed"] = sa
+        g[name + "_x0_seed"] = sx
+        g[name + "_s"] = s
+        for k, v in case.items():
+            g[name + "_" + k] = v
+        if rep.final_x is not None:
+            g[name + "_final_x"] = rep.final_x
+            g[name + "_stop_x"] = rep.stop_x
+    # stationary start: A = Diag(1,2,3,4), X = [e1 e2] (test_solver.cpp:318-331)
+    A4 = np.diag([1.0, 2.0, 3.0, 4.0])
+    X4 = np.zeros((4, 2)); X4[0, 0] = 1.0; X4[1, 1] = 1.0
+    case, _ = run_case(R, Model(MODEL_DENSE, 4, 2, 4.0, a=np.asfortranarray(A4)), X4)
+    for k, v in case.items():
+        g["stat_" + k] = v
+    np.savez_compressed(os.path.join(OUT, "reference_small.npz"), **g)
+    print("wrote", os.path.join(OUT, "reference_small.npz"), len(g), "arrays")
+
+
+def grid_cases(R: Reference) -> None:
+    """Grid models (no reference implementation): the reference solve() driving
+    the restated operator — pins the PCAL loop around it, not the operator."""
+    g = {}
+    for name, kind, grid, p in [("st6", MODEL_STENCIL, (6, 5, 4), 4),
+                                ("ks6", MODEL_KOHN_SHAM, (6, 6, 6), 4)]:
+        n = grid[0] * grid[1] * grid[2]
+        from oracle.oracle import Restatement
+        O = Restatement()
+        v = O.random_uniform(n, 3) if kind == MODEL_STENCIL else -O.random_uniform(n, 3)
+        s = 12.0 + float(np.max(np.abs(v)))
+        mod = Model(kind, n, p, s, grid=grid, v=v)
+        x0 = R.initial_point_qr(n, p, 3 ^ INIT_SALT)
+        case, rep = run_case(R, mod, x0, tol_rel_kkt=TINY, max_iter=60)
+        g[name + "_v"] = v
+        g[name + "_s"] = s
+        for k, val in case.items():
+            g[name + "_" + k] = val
+        g[name + "_final_x"] = rep.final_x
+    np.savez_compressed(os.path.join(OUT, "reference_grid.npz"), **g)
+    print("wrote reference_grid.npz")
+
+
+def cfg2(R: Reference) -> None:
+    """Config 2 (n=16384, p=128, seed 1): s and the first iterations."""
+    import time
+    t = time.time()
+    m = R.dense_trace_min(16384, 128, 1, threads=16)
+    print("cfg2 gen + s:", time.time() - t, m.s, flush=True)
+    x0 = R.initial_point_qr(16384, 128, 1 ^ INIT_SALT)
+    t = time.time()
+    case, rep = run_case(R, m, x0, tol_rel_kkt=TINY, max_iter=3, threads=16, final_orth=False)
+    print("cfg2 3 iters:", time.time() - t, flush=True)
+    g = {"cfg2_s": m.s, "cfg2_a_sha": sha(m.a), "cfg2_x0_sha": sha(x0)}
+    for k, v in case.items():
+        g["cfg2_" + k] = v
+    g["cfg2_stop_x_rows"] = rep.stop_x[:8]
+    np.savez_compressed(os.path.join(OUT, "reference_cfg2.npz"), **g)
+    print("wrote reference_cfg2.npz")
+
+
+if __name__ == "__main__":
+    R = Reference()
+    small(R)
+    grid_cases(R)
+    if "--cfg2" in sys.argv:
+        cfg2(R)

@@ -1,0 +1,100 @@
+// common.cuh — shared definitions for the B200 PCAL library (sm_100a, FP64).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+
+namespace pcal {
+
+// Thrown inside the library, converted to PCAL_E_* at the C ABI.
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define PCAL_CUDA(call)                                                               \
+  do {                                                                                \
+    cudaError_t e_ = (call);                                                          \
+    if (e_ != cudaSuccess)                                                            \
+      throw ::pcal::Error(-5, std::string(#call) + ": " + cudaGetErrorString(e_) +    \
+                                  " (" + __FILE__ + ":" + std::to_string(__LINE__) + ")"); \
+  } while (0)
+
+// Launch-count bookkeeping: every kernel this library launches goes through
+// count_launch() so sessions can report how many native kernels ran.
+extern thread_local int64_t* g_launch_counter;
+inline void count_launch(int64_t k = 1) {
+  if (g_launch_counter) *g_launch_counter += k;
+}
+
+inline int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+inline int64_t ceil_div(int64_t v, int64_t m) { return (v + m - 1) / m; }
+
+// Leading dimension of every internal n×p buffer: rows padded to a multiple
+// of 16 doubles (128 B) with zeros, so GEMM tiles load aligned 16-byte chunks
+// and padded rows contribute nothing to Grams or norms.
+inline int64_t padded_ld(int64_t n) { return round_up(n, 16); }
+
+constexpr int kTraceCols = 7;
+
+// Device-resident control block of one PCAL run.  Every iteration kernel
+// reads `done` first and exits when the run has stopped, so iteration graphs
+// can be launched ahead of the stopping decision without a host round trip.
+struct Ctl {
+  // run state
+  int64_t iter;        // index k of the current iterate X_k (trace row k recorded)
+  int64_t trace_len;   // rows recorded
+  int64_t degenerate;  // pcal_step degenerate columns (accumulated)
+  int32_t done;        // 0 running, 1 converged, 2 diverged
+  int32_t have_prev;   // X_{k-1}, GL_{k-1} available (stepsize memory)
+  int32_t eval_bad;    // evaluation produced non-finite f/G
+  int32_t step_bad;    // pcal_step produced a non-finite iterate
+  int32_t step_param;  // pcal_step got eta <= 0 (parameter_error)
+  int32_t step_deg;    // degenerate columns of the current step
+  // scalars
+  double eta;          // stepsize of the current step (η_k)
+  double eta_prev;     // SolverState::eta (last stepsize used), 0 before the first step
+  double eta0;
+  double beta;
+  double kkt_den;      // kkt_abs at X_0
+  double f, kkt_abs, feas, rel;
+  uint64_t t0_ns;      // %globaltimer at session start
+  // configuration
+  double tol, gamma, eta_min, eta_max;
+  int32_t eta_kind;
+  int32_t mult_rule;
+};
+
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide sum in a fixed order (deterministic); result valid in thread 0.
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double* sm /* NT/32 */) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sm[w] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int i = 0; i < NT / 32; ++i) r += sm[i];
+  }
+  return r;
+}
+
+}  // namespace pcal

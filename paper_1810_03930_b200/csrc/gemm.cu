@@ -1,0 +1,167 @@
+// gemm.cu — stream-K DMMA GEMM: configurations, schedules, launches.
+#include <algorithm>
+#include <vector>
+
+#include "../../include/pcal_b200.h"
+#include "gemm_dmma.cuh"
+
+namespace pcal {
+
+// ------------------------------------------------------------------------------
+// GEMM configurations and launch plumbing
+// ------------------------------------------------------------------------------
+
+template <int AM>
+using CfgBig = GemmCfg<128, 128, 2, 4, 3, AM>;
+template <int AM>
+using CfgMid = GemmCfg<64, 64, 2, 2, 4, AM>;
+template <int AM>
+using CfgSmall = GemmCfg<64, 32, 2, 2, 4, AM>;
+
+int num_sms(int device) {
+  int v = 0;
+  PCAL_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device));
+  return v;
+}
+
+CfgInfo cfg_info(int size) {
+  switch (size) {
+    case CFG_BIG: return {128, 128, 64};
+    case CFG_MID: return {64, 64, 32};
+    default: return {64, 32, 32};
+  }
+}
+
+void GemmPlan::release() {
+  if (d_tiles) cudaFree(d_tiles);
+  if (d_split) cudaFree(d_split);
+  if (d_tasks) cudaFree(d_tasks);
+  if (ws) cudaFree(ws);
+  d_tiles = nullptr;
+  d_split = nullptr;
+  d_tasks = nullptr;
+  ws = nullptr;
+}
+
+int pick_size(int64_t N) {
+  if (N >= 128) return CFG_BIG;
+  if (N > 32) return CFG_MID;
+  return CFG_SMALL;
+}
+
+void plan_gemm(GemmPlan& pl, int device, int size, int amode, int epi, int64_t M,
+                      int64_t N, int64_t K, int64_t sym_row0, int grid_override) {
+  pl.release();
+  pl.size = size;
+  pl.amode = amode;
+  pl.epi = epi;
+  const CfgInfo ci = cfg_info(size);
+  const int BK = 16;
+  if (K % BK) throw Error(PCAL_E_DIMENSION, "gemm: K must be a multiple of 16");
+  const int64_t tm_n = ceil_div(M, ci.BM), tn_n = ceil_div(N, ci.BN);
+  std::vector<int2> tiles;
+  for (int64_t tn = 0; tn < tn_n; ++tn)
+    for (int64_t tm = 0; tm < tm_n; ++tm) {
+      if (sym_row0 >= 0) {
+        const int64_t r0 = tm * ci.BM;
+        const int64_t c1 = (tn + 1) * ci.BN - 1;
+        if (r0 >= sym_row0 && (r0 - sym_row0) > c1) continue;  // strictly below diagonal
+      }
+      tiles.push_back(make_int2((int)tm, (int)tn));
+    }
+  const int ntiles = (int)tiles.size();
+  const int ki = (int)(K / BK);
+  const int64_t units = (int64_t)ntiles * ki;
+  int grid = grid_override > 0 ? grid_override : num_sms(device);
+  if (units < grid) grid = (int)std::max<int64_t>(1, units);
+  std::vector<int32_t> split(ntiles, -1);
+  std::vector<FixupTask> tasks;
+  int qmax = 1;
+  for (int t = 0; t < ntiles; ++t) {
+    const int32_t cf = cta_of_unit((int64_t)t * ki, units, grid);
+    const int32_t cl = cta_of_unit((int64_t)(t + 1) * ki - 1, units, grid);
+    if (cf != cl) {
+      split[t] = (int32_t)tasks.size();
+      tasks.push_back({t, (int32_t)tasks.size(), cl - cf + 1});
+      qmax = std::max(qmax, cl - cf + 1);
+    }
+  }
+  PCAL_CUDA(cudaMalloc(&pl.d_tiles, sizeof(int2) * ntiles));
+  PCAL_CUDA(cudaMemcpy(pl.d_tiles, tiles.data(), sizeof(int2) * ntiles, cudaMemcpyHostToDevice));
+  PCAL_CUDA(cudaMalloc(&pl.d_split, sizeof(int32_t) * ntiles));
+  PCAL_CUDA(cudaMemcpy(pl.d_split, split.data(), sizeof(int32_t) * ntiles, cudaMemcpyHostToDevice));
+  pl.ntasks = (int)tasks.size();
+  if (pl.ntasks) {
+    PCAL_CUDA(cudaMalloc(&pl.d_tasks, sizeof(FixupTask) * pl.ntasks));
+    PCAL_CUDA(cudaMemcpy(pl.d_tasks, tasks.data(), sizeof(FixupTask) * pl.ntasks,
+                         cudaMemcpyHostToDevice));
+    pl.ws_doubles = (size_t)pl.ntasks * qmax * ci.BM * ci.BN;
+    PCAL_CUDA(cudaMalloc(&pl.ws, sizeof(double) * pl.ws_doubles));
+  }
+  // heavily split plain-store tiles (Gram) spread their fixup over 8 CTAs each
+  pl.sub = (epi == EPI_STORE && qmax > 8) ? 8 : 1;
+  GemmArgs& g = pl.args;
+  g = GemmArgs{};
+  g.M = M;
+  g.N = N;
+  g.K = K;
+  g.tiles = pl.d_tiles;
+  g.split_slot = pl.d_split;
+  g.ntiles = ntiles;
+  g.ki = ki;
+  g.units = units;
+  g.grid = grid;
+  g.ws = pl.ws;
+  g.qmax = qmax;
+}
+
+template <class Cfg, int EPI>
+static void launch_cfg(const GemmPlan& pl, cudaStream_t st) {
+  auto kern = gemm_streamk<Cfg, EPI>;
+  static bool attr_set = false;  // per instantiation
+  if (!attr_set) {
+    PCAL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   Cfg::SMEM_BYTES));
+    attr_set = true;
+  }
+  kern<<<pl.args.grid, Cfg::THREADS, Cfg::SMEM_BYTES, st>>>(pl.args);
+  PCAL_CUDA(cudaGetLastError());
+  count_launch();
+  if (pl.ntasks) {
+    if (pl.sub > 1) {
+      if constexpr (EPI == EPI_STORE) {
+        gemm_fixup<Cfg, EPI, 8><<<dim3(pl.ntasks, 8), Cfg::THREADS, 0, st>>>(pl.args, pl.d_tasks);
+      }
+    } else {
+      gemm_fixup<Cfg, EPI, 1><<<dim3(pl.ntasks, 1), Cfg::THREADS, 0, st>>>(pl.args, pl.d_tasks);
+    }
+    PCAL_CUDA(cudaGetLastError());
+    count_launch();
+  }
+}
+
+template <int AM, int EPI>
+static void launch_sized(const GemmPlan& pl, cudaStream_t st) {
+  switch (pl.size) {
+    case CFG_BIG: launch_cfg<CfgBig<AM>, EPI>(pl, st); break;
+    case CFG_MID: launch_cfg<CfgMid<AM>, EPI>(pl, st); break;
+    default: launch_cfg<CfgSmall<AM>, EPI>(pl, st); break;
+  }
+}
+
+void launch_gemm(const GemmPlan& pl, cudaStream_t st) {
+  if (pl.amode == A_MCONTIG) {
+    switch (pl.epi) {
+      case EPI_STORE: launch_sized<A_MCONTIG, EPI_STORE>(pl, st); break;
+      case EPI_GRAD: launch_sized<A_MCONTIG, EPI_GRAD>(pl, st); break;
+      default: launch_sized<A_MCONTIG, EPI_XM>(pl, st); break;
+    }
+  } else {
+    if (pl.epi != EPI_STORE) throw Error(PCAL_E_STATE, "gemm: K-contiguous A only with stores");
+    launch_sized<A_KCONTIG, EPI_STORE>(pl, st);
+  }
+  (void)0;
+}
+
+
+}  // namespace pcal

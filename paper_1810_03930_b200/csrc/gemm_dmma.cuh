@@ -1,0 +1,350 @@
+// gemm_dmma.cuh — FP64 tensor-core GEMM for sm_100a with stream-K scheduling
+// and fused PCAL epilogues.
+//
+// Blackwell has no FP64 tcgen05 kind (ptxas rejects kind::f64),
+// so FP64 tensor math is the warp-level mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4,
+// measured 37.1 TFLOP/s peak on B200: profiles/fp64_peaks_r01.txt).  Tiles are
+// staged global→shared with 16-byte cp.async in a STAGES-deep ring; the
+// schedule is stream-K: the linearised (tile, k-iteration) space is cut into
+// `grid` equal contiguous ranges, one per CTA (grid = SM count), so the
+// tall-skinny contractions of PCAL (K = n up to 2M, M·N = p×p) and the dense
+// gradient (M = n, N = p, K = n) both fill all 148 SMs.  A tile completed by
+// one CTA gets its epilogue in-kernel; a tile shared by several CTAs has its
+// partial accumulators written to a workspace and summed in a FIXED order
+// (CTA order) by gemm_fixup — results never depend on timing, and the
+// direct and fixup paths run the same epilogue code.
+//
+// Operands (FP64, column-major device buffers):
+//   A_MCONTIG: A(m,k) = A[m + k·lda]     (dense operator A; X in X·M)
+//   A_KCONTIG: A(m,k) = A[k + m·lda]     (Xᵀ / [G|X]ᵀ in the Grams)
+//   B        : B(k,n) = B[k + n·ldb]     (X, Y, or the p×2p multiplier block)
+#pragma once
+
+#include "gemm_types.h"
+
+namespace pcal {
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const int sz = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+template <int BM_, int BN_, int WARPS_M_, int WARPS_N_, int STAGES_, int AMODE_>
+struct GemmCfg {
+  static constexpr int BM = BM_, BN = BN_, BK = 16;
+  static constexpr int WARPS_M = WARPS_M_, WARPS_N = WARPS_N_;
+  static constexpr int WARPS = WARPS_M * WARPS_N, THREADS = WARPS * 32;
+  static constexpr int STAGES = STAGES_;
+  static constexpr int AMODE = AMODE_;
+  static constexpr int WM = BM / WARPS_M, WN = BN / WARPS_N;  // warp tile
+  static constexpr int MT = WM / 8, NT = WN / 8;              // 8×8 mma tiles per warp
+  static constexpr int FRAG = MT * NT * 2;                    // accumulators per thread
+  // shared layouts (doubles); +4 padding makes the 16 lanes of a 64-bit
+  // fragment wavefront hit 16 distinct bank pairs
+  static constexpr int SA_M = BM + 4;       // A_MCONTIG: As[k][m]
+  static constexpr int SA_K = BK + 4;       // A_KCONTIG: As[m][k]
+  static constexpr int A_STAGE = AMODE == A_MCONTIG ? BK * SA_M : BM * SA_K;
+  static constexpr int SB_K = BK + 4;       // Bs[n][k]
+  static constexpr int B_STAGE = BN * SB_K;
+  static constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) * 8;
+  static_assert(WM % 8 == 0 && WN % 8 == 0, "warp tile must be a multiple of 8");
+};
+
+// ---- tile loads -------------------------------------------------------------
+template <class Cfg>
+__device__ __forceinline__ void load_stage(const GemmArgs& g, double* As, double* Bs, int tm,
+                                           int tn, int kk) {
+  constexpr int BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK, T = Cfg::THREADS;
+  const int64_t m0 = (int64_t)tm * BM, n0 = (int64_t)tn * BN, k0 = (int64_t)kk * BK;
+  if constexpr (Cfg::AMODE == A_MCONTIG) {
+    // BK columns of BM contiguous doubles; 16-byte chunks of 2 doubles
+    constexpr int CH = BK * BM / 2;
+#pragma unroll
+    for (int c = threadIdx.x; c < CH; c += T) {
+      const int kr = c / (BM / 2), mc = (c % (BM / 2)) * 2;
+      const int64_t m = m0 + mc;
+      const bool ok = m < g.M;
+      const double* src = g.A + (ok ? m + (k0 + kr) * g.lda : 0);
+      cp_async16(As + kr * Cfg::SA_M + mc, src, ok);
+    }
+  } else {
+    // BM rows (columns of the stored matrix) of BK contiguous doubles
+    constexpr int CH = BM * BK / 2;
+#pragma unroll
+    for (int c = threadIdx.x; c < CH; c += T) {
+      const int mr = c / (BK / 2), kc = (c % (BK / 2)) * 2;
+      const int64_t m = m0 + mr;
+      const bool ok = m < g.M;
+      const double* src = g.A + (ok ? (k0 + kc) + m * g.lda : 0);
+      cp_async16(As + mr * Cfg::SA_K + kc, src, ok);
+    }
+  }
+  {
+    constexpr int CH = BN * BK / 2;
+#pragma unroll
+    for (int c = threadIdx.x; c < CH; c += T) {
+      const int nr = c / (BK / 2), kc = (c % (BK / 2)) * 2;
+      const int64_t nn = n0 + nr;
+      const bool ok = nn < g.N;
+      const double* src = g.B + (ok ? (k0 + kc) + nn * g.ldb : 0);
+      cp_async16(Bs + nr * Cfg::SB_K + kc, src, ok);
+    }
+  }
+}
+
+// ---- one BK slice of MMAs ------------------------------------------------------
+template <class Cfg>
+__device__ __forceinline__ void mma_stage(const double* As, const double* Bs, int wm, int wn,
+                                          int lane, double (&acc)[Cfg::MT][Cfg::NT][2]) {
+  const int r = lane >> 2, q = lane & 3;
+#pragma unroll
+  for (int k4 = 0; k4 < Cfg::BK; k4 += 4) {
+    double a[Cfg::MT], b[Cfg::NT];
+#pragma unroll
+    for (int mt = 0; mt < Cfg::MT; ++mt) {
+      const int m = wm * Cfg::WM + mt * 8 + r;
+      if constexpr (Cfg::AMODE == A_MCONTIG)
+        a[mt] = As[(k4 + q) * Cfg::SA_M + m];
+      else
+        a[mt] = As[m * Cfg::SA_K + k4 + q];
+    }
+#pragma unroll
+    for (int nt = 0; nt < Cfg::NT; ++nt) {
+      const int n = wn * Cfg::WN + nt * 8 + r;
+      b[nt] = Bs[n * Cfg::SB_K + k4 + q];
+    }
+#pragma unroll
+    for (int mt = 0; mt < Cfg::MT; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < Cfg::NT; ++nt) dmma_8x8x4(acc[mt][nt][0], acc[mt][nt][1], a[mt], b[nt]);
+  }
+}
+
+// ---- epilogues ---------------------------------------------------------------
+// Fragment (mt, nt, e) of lane `lane` in warp (wm, wn) is output element
+//   row = m0 + wm·WM + mt·8 + lane/4,   col = n0 + wn·WN + nt·8 + 2·(lane%4) + e.
+// Column partial sums are reduced over the warp's WM rows (fixed shuffle
+// order) and stored per row-block rb = (m0 + wm·WM)/WM.
+template <class Cfg, int EPI>
+__device__ __forceinline__ void epilogue(const GemmArgs& g, int tm, int tn, int wm, int wn,
+                                         int lane, double (&acc)[Cfg::MT][Cfg::NT][2]) {
+  const EpiParams& e = g.ep;
+  const int r = lane >> 2, q = lane & 3;
+  const int64_t mw0 = (int64_t)tm * Cfg::BM + wm * Cfg::WM;
+  const int64_t nw0 = (int64_t)tn * Cfg::BN + wn * Cfg::WN;
+  if constexpr (EPI == EPI_STORE) {
+#pragma unroll
+    for (int mt = 0; mt < Cfg::MT; ++mt) {
+      const int64_t row = mw0 + mt * 8 + r;
+#pragma unroll
+      for (int nt = 0; nt < Cfg::NT; ++nt)
+#pragma unroll
+        for (int x = 0; x < 2; ++x) {
+          const int64_t col = nw0 + nt * 8 + 2 * q + x;
+          if (row < e.m_store && col < e.n_store) e.C[row + col * e.ldc] = acc[mt][nt][x];
+        }
+    }
+  } else if constexpr (EPI == EPI_GRAD) {
+    const int64_t rb = mw0 / Cfg::WM;
+    bool bad = false;
+#pragma unroll
+    for (int nt = 0; nt < Cfg::NT; ++nt)
+#pragma unroll
+      for (int x = 0; x < 2; ++x) {
+        const int64_t col = nw0 + nt * 8 + 2 * q + x;
+        double fs = 0.0;
+#pragma unroll
+        for (int mt = 0; mt < Cfg::MT; ++mt) {
+          const int64_t row = mw0 + mt * 8 + r;
+          if (row < e.n && col < e.p) {
+            double gv = acc[mt][nt][x];
+            if (e.g0) gv += e.g0[row + col * e.ld];
+            e.G[row + col * e.ld] = gv;
+            fs += e.X[row + col * e.ld] * gv;
+            bad |= !isfinite(gv);
+          }
+        }
+        fs += __shfl_xor_sync(0xffffffffu, fs, 4);
+        fs += __shfl_xor_sync(0xffffffffu, fs, 8);
+        fs += __shfl_xor_sync(0xffffffffu, fs, 16);
+        if (r == 0 && col < e.p) e.fpart[rb * e.p + col] = fs;
+      }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) *e.bad = 1;
+  } else {  // EPI_XM
+    const int64_t rb = mw0 / Cfg::WM;
+#pragma unroll
+    for (int nt = 0; nt < Cfg::NT; ++nt) {
+      const int64_t j = (nw0 + nt * 8 + 2 * q) >> 1;  // output column
+      double ks = 0.0, ds = 0.0;
+#pragma unroll
+      for (int mt = 0; mt < Cfg::MT; ++mt) {
+        const int64_t row = mw0 + mt * 8 + r;
+        if (row < e.n && j < e.p) {
+          const int64_t idx = row + j * e.ld;
+          const double kkt = e.G[idx] - acc[mt][nt][0];
+          const double pv = kkt + e.beta * acc[mt][nt][1];
+          e.G[idx] = pv;
+          ks += kkt * kkt;
+          ds += e.X[idx] * pv;
+        }
+      }
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1) {
+        ks += __shfl_xor_sync(0xffffffffu, ks, o);
+        ds += __shfl_xor_sync(0xffffffffu, ds, o);
+      }
+      if (r == 0 && j < e.p) {
+        e.kpart[rb * e.p + j] = ks;
+        e.dpart[rb * e.p + j] = ds;
+      }
+    }
+  }
+}
+
+template <class Cfg>
+__device__ __forceinline__ size_t frag_index(int warp, int mt, int nt, int x, int lane) {
+  return ((((size_t)warp * Cfg::MT + mt) * Cfg::NT + nt) * 2 + x) * 32 + lane;
+}
+
+// ---- main kernel ----------------------------------------------------------------
+template <class Cfg, int EPI>
+__global__ void __launch_bounds__(Cfg::THREADS, 1) gemm_streamk(GemmArgs g) {
+  if (g.ctl && g.ctl->done) return;
+  extern __shared__ __align__(16) double smem[];
+  double* As = smem;
+  double* Bs = smem + Cfg::STAGES * Cfg::A_STAGE;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wm = warp / Cfg::WARPS_N, wn = warp % Cfg::WARPS_N;
+  const int32_t cta = blockIdx.x;
+  const int64_t u0 = cta_unit_begin(cta, g.units, g.grid);
+  const int64_t u1 = cta_unit_begin(cta + 1, g.units, g.grid);
+  if (u0 >= u1) return;
+
+  // prologue: fill STAGES-1 stages
+#pragma unroll
+  for (int s = 0; s < Cfg::STAGES - 1; ++s) {
+    const int64_t u = u0 + s;
+    if (u < u1) {
+      const int t = (int)(u / g.ki);
+      const int2 tc = g.tiles[t];
+      load_stage<Cfg>(g, As + s * Cfg::A_STAGE, Bs + s * Cfg::B_STAGE, tc.x, tc.y, (int)(u % g.ki));
+    }
+    cp_async_commit();
+  }
+
+  double acc[Cfg::MT][Cfg::NT][2];
+#pragma unroll
+  for (int mt = 0; mt < Cfg::MT; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < Cfg::NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+
+  int64_t seg_begin = u0;  // first unit of the current tile segment
+  for (int64_t u = u0; u < u1; ++u) {
+    const int64_t i = u - u0;
+    cp_async_wait<Cfg::STAGES - 2>();
+    __syncthreads();
+    {
+      const int64_t un = u + Cfg::STAGES - 1;
+      if (un < u1) {
+        const int s = (int)(un - u0) % Cfg::STAGES;
+        const int t = (int)(un / g.ki);
+        const int2 tc = g.tiles[t];
+        load_stage<Cfg>(g, As + s * Cfg::A_STAGE, Bs + s * Cfg::B_STAGE, tc.x, tc.y,
+                        (int)(un % g.ki));
+      }
+      cp_async_commit();
+    }
+    const int s = (int)(i % Cfg::STAGES);
+    mma_stage<Cfg>(As + s * Cfg::A_STAGE, Bs + s * Cfg::B_STAGE, wm, wn, lane, acc);
+
+    const int t = (int)(u / g.ki);
+    const int kk = (int)(u % g.ki);
+    if (kk == g.ki - 1 || u == u1 - 1) {
+      const int2 tc = g.tiles[t];
+      const bool whole = (seg_begin % g.ki == 0) && kk == g.ki - 1;
+      if (whole) {
+        epilogue<Cfg, EPI>(g, tc.x, tc.y, wm, wn, lane, acc);
+      } else {
+        const int slot = g.split_slot[t];
+        const int q = cta - cta_of_unit((int64_t)t * g.ki, g.units, g.grid);
+        double* w = g.ws + ((size_t)slot * g.qmax + q) * (size_t)(Cfg::BM * Cfg::BN);
+#pragma unroll
+        for (int mt = 0; mt < Cfg::MT; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < Cfg::NT; ++nt)
+#pragma unroll
+            for (int x = 0; x < 2; ++x) w[frag_index<Cfg>(warp, mt, nt, x, lane)] = acc[mt][nt][x];
+      }
+#pragma unroll
+      for (int mt = 0; mt < Cfg::MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < Cfg::NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+      seg_begin = u + 1;
+    }
+  }
+  cp_async_wait<0>();
+}
+
+// Sums the partials of split tiles in CTA order and applies the epilogue.
+// grid = (#split tiles, SUB): for EPI_STORE the fragment is additionally
+// divided into SUB slices across CTAs (heavily split Gram tiles).
+template <class Cfg, int EPI, int SUB>
+__global__ void __launch_bounds__(Cfg::THREADS) gemm_fixup(GemmArgs g, const FixupTask* tasks) {
+  if (g.ctl && g.ctl->done) return;
+  const FixupTask tk = tasks[blockIdx.x];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wm = warp / Cfg::WARPS_N, wn = warp % Cfg::WARPS_N;
+  double acc[Cfg::MT][Cfg::NT][2];
+  const double* base = g.ws + (size_t)tk.slot * g.qmax * (size_t)(Cfg::BM * Cfg::BN);
+  constexpr int PER = (Cfg::MT + SUB - 1) / SUB;
+  const int mt_lo = (SUB == 1) ? 0 : blockIdx.y * PER;
+#pragma unroll
+  for (int mt = 0; mt < Cfg::MT; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < Cfg::NT; ++nt)
+#pragma unroll
+      for (int x = 0; x < 2; ++x) {
+        double s = 0.0;
+        if (SUB == 1 || (mt >= mt_lo && mt < mt_lo + PER)) {
+          for (int q = 0; q < tk.nq; ++q)
+            s += base[(size_t)q * (Cfg::BM * Cfg::BN) + frag_index<Cfg>(warp, mt, nt, x, lane)];
+        }
+        acc[mt][nt][x] = s;
+      }
+  const int2 tc = g.tiles[tk.tile];
+  if constexpr (SUB == 1) {
+    epilogue<Cfg, EPI>(g, tc.x, tc.y, wm, wn, lane, acc);
+  } else {
+    static_assert(EPI == EPI_STORE, "sliced fixup only for plain stores");
+    const EpiParams& e = g.ep;
+    const int r = lane >> 2, qq = lane & 3;
+    const int64_t mw0 = (int64_t)tc.x * Cfg::BM + wm * Cfg::WM;
+    const int64_t nw0 = (int64_t)tc.y * Cfg::BN + wn * Cfg::WN;
+#pragma unroll
+    for (int mt = 0; mt < Cfg::MT; ++mt) {
+      if (mt < mt_lo || mt >= mt_lo + PER) continue;
+      const int64_t row = mw0 + mt * 8 + r;
+#pragma unroll
+      for (int nt = 0; nt < Cfg::NT; ++nt)
+#pragma unroll
+        for (int x = 0; x < 2; ++x) {
+          const int64_t col = nw0 + nt * 8 + 2 * qq + x;
+          if (row < e.m_store && col < e.n_store) e.C[row + col * e.ldc] = acc[mt][nt][x];
+        }
+    }
+  }
+}
+
+}  // namespace pcal

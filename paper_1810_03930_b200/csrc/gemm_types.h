@@ -1,0 +1,100 @@
+// gemm_types.h — host/device shared types of the stream-K DMMA GEMM.
+#pragma once
+
+#include "common.cuh"
+
+namespace pcal {
+
+enum AMode { A_MCONTIG = 0, A_KCONTIG = 1 };
+enum EpiKind { EPI_STORE = 0, EPI_GRAD = 1, EPI_XM = 2 };
+
+struct EpiParams {
+  // EPI_STORE: C[row + col·ldc] = acc for row < m_store, col < n_store
+  double* C;
+  int64_t ldc, m_store, n_store;
+  // EPI_GRAD: G = acc (+g0); fpart[rb·p + col] = Σ_rows X∘G over a warp row-block
+  // EPI_XM:   acc columns interleave (X·W, X·C) per output column j:
+  //           kkt = G − XW; P = kkt + β·XC (written over G);
+  //           kpart[rb·p + j] = Σ kkt², dpart[rb·p + j] = Σ X∘P
+  double* G;
+  const double* X;
+  const double* g0;
+  int64_t ld;        // leading dimension of G, X, g0
+  double* fpart;
+  double* kpart;
+  double* dpart;
+  int32_t* bad;      // set to 1 if a non-finite value is produced (GRAD)
+  double beta;
+  int64_t n, p;
+};
+
+struct GemmArgs {
+  const double* A;
+  int64_t lda;
+  const double* B;
+  int64_t ldb;
+  int64_t M, N;       // logical extents (loads beyond are zero-filled)
+  int64_t K;          // multiple of BK (operands zero-padded)
+  const int2* tiles;  // (tm, tn) per tile
+  const int32_t* split_slot;  // per tile: workspace slot or -1 (owned by one CTA)
+  int32_t ntiles;
+  int32_t ki;         // k-iterations per tile
+  int64_t units;      // ntiles · ki
+  int32_t grid;
+  double* ws;         // [slot][q][BM·BN] partials, fragment-native layout
+  int32_t qmax;
+  EpiParams ep;
+  const Ctl* ctl;     // early exit when ctl->done (may be null)
+};
+
+struct FixupTask {   // one split tile
+  int32_t tile;
+  int32_t slot;
+  int32_t nq;
+};
+
+// CTA whose contiguous unit range contains unit x: max c with ⌊c·U/G⌋ ≤ x.
+__host__ __device__ inline int32_t cta_of_unit(int64_t x, int64_t U, int32_t G) {
+  int64_t c = ((x + 1) * (int64_t)G + U - 1) / U - 1;
+  return (int32_t)(c < 0 ? 0 : (c >= G ? G - 1 : c));
+}
+__host__ __device__ inline int64_t cta_unit_begin(int32_t c, int64_t U, int32_t G) {
+  return (int64_t)c * U / G;
+}
+
+
+// ---- host-side plans -----------------------------------------------------------
+enum CfgSize { CFG_BIG = 0, CFG_MID = 1, CFG_SMALL = 2 };
+
+struct CfgInfo {
+  int BM, BN, WM;
+};
+CfgInfo cfg_info(int size);
+int pick_size(int64_t N);
+
+// A GEMM with a static stream-K schedule (tile list, split tiles, workspace).
+struct GemmPlan {
+  int size = CFG_BIG, amode = A_MCONTIG, epi = EPI_STORE;
+  GemmArgs args{};
+  int2* d_tiles = nullptr;
+  int32_t* d_split = nullptr;
+  FixupTask* d_tasks = nullptr;
+  int ntasks = 0;
+  int sub = 1;
+  double* ws = nullptr;
+  size_t ws_doubles = 0;
+  GemmPlan() = default;
+  GemmPlan(const GemmPlan&) = delete;
+  GemmPlan& operator=(const GemmPlan&) = delete;
+  ~GemmPlan() { release(); }
+  void release();
+};
+
+// Build a plan.  `sym_row0` >= 0 skips tiles lying strictly below the diagonal
+// of the block starting at row sym_row0 (the XᵀX half of the Gram).
+void plan_gemm(GemmPlan& pl, int device, int size, int amode, int epi, int64_t M, int64_t N,
+               int64_t K, int64_t sym_row0 = -1, int grid_override = 0);
+void launch_gemm(const GemmPlan& pl, cudaStream_t st);
+int num_sms(int device);
+
+}  // namespace pcal

@@ -1,0 +1,166 @@
+// host_setup.cpp — problem setup on the host: the reference's documented
+// random stream (rng.hpp:13-55, kernels.cpp:65-78: xoshiro256++ seeded by
+// splitmix64, uniforms from the top 53 bits, Box–Muller normals with a cached
+// spare) and the periodic Fourier basis of the Kohn–Sham model.  The stream is
+// part of the reference's data contract (same seed ⇒ same instance), so the
+// draws here are bitwise identical to the reference; the Box–Muller work is
+// spread over threads from checkpointed generator states.
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <thread>
+#include <vector>
+
+#include "../../include/pcal_b200.h"
+#include "host_setup.h"
+
+namespace {
+
+struct Rng {
+  uint64_t s[4];
+  explicit Rng(uint64_t seed) {
+    uint64_t x = seed;
+    for (auto& w : s) w = splitmix64(x);
+  }
+  static uint64_t splitmix64(uint64_t& x) {
+    x += 0x9e3779b97f4a7c15ULL;
+    uint64_t z = x;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+  }
+  static uint64_t rotl(uint64_t v, int k) { return (v << k) | (v >> (64 - k)); }
+  uint64_t next() {
+    const uint64_t result = rotl(s[0] + s[3], 23) + s[0];
+    const uint64_t t = s[1] << 17;
+    s[2] ^= s[0];
+    s[3] ^= s[1];
+    s[1] ^= s[2];
+    s[0] ^= s[3];
+    s[2] ^= t;
+    s[3] = rotl(s[3], 45);
+    return result;
+  }
+  double uniform() { return static_cast<double>(next() >> 11) * 0x1.0p-53; }
+  // One Box–Muller pair: the first value is returned by normal(), the second
+  // is the cached spare (kernels.cpp:65-78).
+  void pair(double& c, double& sn) {
+    const double u1 = 1.0 - uniform();
+    const double u2 = uniform();
+    const double r = std::sqrt(-2.0 * std::log(u1));
+    const double t = 6.283185307179586476925286766559 * u2;
+    sn = r * std::sin(t);
+    c = r * std::cos(t);
+  }
+};
+
+}  // namespace
+
+namespace pcal {
+
+void host_random_normal(int64_t count, uint64_t seed, double* out, int threads) {
+  Rng r(seed);
+  const int64_t npairs = (count + 1) / 2;
+  const int64_t chunk = int64_t(1) << 16;
+  const int64_t nchunks = (npairs + chunk - 1) / chunk;
+  if (threads <= 1 || nchunks < 2) {
+    for (int64_t m = 0; m < npairs; ++m) {
+      double c, s;
+      r.pair(c, s);
+      out[2 * m] = c;
+      if (2 * m + 1 < count) out[2 * m + 1] = s;
+    }
+    return;
+  }
+  std::vector<Rng> cps;
+  cps.reserve(static_cast<size_t>(nchunks));
+  for (int64_t c = 0; c < nchunks; ++c) {
+    cps.push_back(r);
+    const int64_t pairs = (c + 1 < nchunks) ? chunk : npairs - c * chunk;
+    for (int64_t q = 0; q < 2 * pairs; ++q) (void)r.next();
+  }
+  std::vector<std::thread> pool;
+  for (int t = 0; t < threads; ++t)
+    pool.emplace_back([&, t] {
+      for (int64_t c = t; c < nchunks; c += threads) {
+        Rng g = cps[static_cast<size_t>(c)];
+        const int64_t p0 = c * chunk, p1 = (c + 1 < nchunks) ? p0 + chunk : npairs;
+        for (int64_t m = p0; m < p1; ++m) {
+          double cv, sv;
+          g.pair(cv, sv);
+          out[2 * m] = cv;
+          if (2 * m + 1 < count) out[2 * m + 1] = sv;
+        }
+      }
+    });
+  for (auto& th : pool) th.join();
+}
+
+void host_random_uniform(int64_t count, uint64_t seed, double* out) {
+  Rng r(seed);
+  for (int64_t k = 0; k < count; ++k) out[k] = r.uniform();
+}
+
+}  // namespace pcal
+
+// Real orthonormal eigenbasis of the periodic N-point second difference
+// (DESIGN.md §3): column m of q (q[i + N·m]) is mode m; lam[m] its eigenvalue.
+void pcal_fourier_basis(int64_t N, double* q, double* lam) {
+  const double two_pi = 6.283185307179586476925286766559;
+  const double c0 = 1.0 / std::sqrt(static_cast<double>(N));
+  const double c1 = std::sqrt(2.0 / static_cast<double>(N));
+  for (int64_t i = 0; i < N; ++i) q[i] = c0;
+  lam[0] = 0.0;
+  int64_t m = 1;
+  for (int64_t k = 1; 2 * k < N; ++k) {
+    const double th = two_pi * static_cast<double>(k) / static_cast<double>(N);
+    for (int64_t i = 0; i < N; ++i) {
+      const double ang = two_pi * static_cast<double>((k * i) % N) / static_cast<double>(N);
+      q[i + N * m] = c1 * std::cos(ang);
+      q[i + N * (m + 1)] = c1 * std::sin(ang);
+    }
+    lam[m] = 2.0 - 2.0 * std::cos(th);
+    lam[m + 1] = lam[m];
+    m += 2;
+  }
+  if (N % 2 == 0) {
+    for (int64_t i = 0; i < N; ++i) q[i + N * m] = (i % 2 == 0) ? c0 : -c0;
+    lam[m] = 4.0;
+  }
+}
+
+extern "C" {
+
+int pcal_random_normal(int64_t rows, int64_t cols, uint64_t seed, double* out, int32_t threads) {
+  if (!out || rows < 1 || cols < 1) return PCAL_E_PARAMETER;
+  pcal::host_random_normal(rows * cols, seed, out, threads);
+  return PCAL_OK;
+}
+
+int pcal_random_uniform(int64_t count, uint64_t seed, double* out) {
+  if (!out || count < 0) return PCAL_E_PARAMETER;
+  pcal::host_random_uniform(count, seed, out);
+  return PCAL_OK;
+}
+
+// sym_part(random_normal(n,n,Rng(seed))) (problems.cpp:45-48, kernels.cpp:28-36).
+int pcal_gen_dense_operator(int64_t n, uint64_t seed, double* a, int32_t threads) {
+  if (!a || n < 1) return PCAL_E_PARAMETER;
+  pcal::host_random_normal(n * n, seed, a, threads);
+  // in place: a(i,j) = a(j,i) = 0.5·(b(i,j) + b(j,i)) for i ≤ j (same value both sides)
+  const int nt = threads > 1 ? threads : 1;
+  std::vector<std::thread> pool;
+  for (int t = 0; t < nt; ++t)
+    pool.emplace_back([=] {
+      for (int64_t j = t; j < n; j += nt)
+        for (int64_t i = 0; i <= j; ++i) {
+          const double v = 0.5 * (a[i + j * n] + a[j + i * n]);
+          a[i + j * n] = v;
+          a[j + i * n] = v;
+        }
+    });
+  for (auto& th : pool) th.join();
+  return PCAL_OK;
+}
+
+}  // extern "C"

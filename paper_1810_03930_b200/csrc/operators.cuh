@@ -1,0 +1,146 @@
+// operators.cuh — device gradient evaluation for the grid models (the
+// ObjectiveModel::evaluate callback of problems.hpp:39, restated for the
+// configs without a reference implementation; definitions in DESIGN.md §3).
+//
+// Arithmetic uses explicit round-to-nearest intrinsics (no FMA contraction) in
+// the same left-to-right order as the oracle (oracle/pcal_oracle.c
+// orc_laplacian_apply / orc_evaluate), so the stencil gradient is bitwise equal
+// to the oracle's; only the objective's reduction order differs.
+#pragma once
+
+#include "common.cuh"
+
+namespace pcal {
+
+constexpr int kStencilThreads = 256;
+constexpr int kStreamThreadsOps = 256;
+
+// G = L X + V∘X with L = −Δ_h (7-point, periodic, h = 1) and, for the
+// Kohn–Sham model, G = ½ L X + u∘X (scale_l = 0.5, u = V + L†ρ − c ρ^{1/3}).
+// fpart[chunk·p + j] = Σ_{rows of chunk} X∘(LX) (the Laplacian quadratic form).
+// Grid: (n / chunk, p); one thread per row element, x-fastest for coalescing.
+template <bool KS>
+__global__ void __launch_bounds__(kStencilThreads)
+    k_stencil_grad(const double* __restrict__ x, const double* __restrict__ u,
+                   double* __restrict__ g, int64_t nx, int64_t ny, int64_t nz, int64_t ld,
+                   int64_t p, int64_t chunk, double* __restrict__ fpart, int32_t* bad,
+                   const Ctl* ctl) {
+  if (ctl && ctl->done) return;
+  __shared__ double sm[kStencilThreads / 32];
+  const int64_t n = nx * ny * nz;
+  const int64_t j = blockIdx.y;
+  const int64_t r0 = (int64_t)blockIdx.x * chunk;
+  const int64_t r1 = min(n, r0 + chunk);
+  const double* xj = x + j * ld;
+  double* gj = g + j * ld;
+  const int64_t nxy = nx * ny;
+  double acc = 0.0;
+  bool nonfinite = false;
+  for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+    const int64_t xx = i % nx;
+    const int64_t y = (i / nx) % ny;
+    const int64_t z = i / nxy;
+    const int64_t xm = i + (xx == 0 ? nx - 1 : -1);
+    const int64_t xp = i + (xx == nx - 1 ? 1 - nx : 1);
+    const int64_t ym = i + (y == 0 ? (ny - 1) * nx : -nx);
+    const int64_t yp = i + (y == ny - 1 ? (1 - ny) * nx : nx);
+    const int64_t zm = i + (z == 0 ? (nz - 1) * nxy : -nxy);
+    const int64_t zp = i + (z == nz - 1 ? (1 - nz) * nxy : nxy);
+    const double xv = __ldg(xj + i);
+    double lx = __dmul_rn(6.0, xv);
+    lx = __dsub_rn(lx, __ldg(xj + xm));
+    lx = __dsub_rn(lx, __ldg(xj + xp));
+    lx = __dsub_rn(lx, __ldg(xj + ym));
+    lx = __dsub_rn(lx, __ldg(xj + yp));
+    lx = __dsub_rn(lx, __ldg(xj + zm));
+    lx = __dsub_rn(lx, __ldg(xj + zp));
+    double gv;
+    if (KS) gv = __dadd_rn(__dmul_rn(0.5, lx), __dmul_rn(__ldg(u + i), xv));
+    else gv = __dadd_rn(lx, __dmul_rn(__ldg(u + i), xv));
+    gj[i] = gv;
+    acc += KS ? xv * lx : xv * gv;
+    nonfinite |= !isfinite(gv);
+  }
+  const double s = block_sum<kStencilThreads>(acc, sm);
+  if (threadIdx.x == 0) fpart[blockIdx.x * p + j] = s;
+  if (__syncthreads_or(nonfinite) && threadIdx.x == 0) *bad = 1;
+}
+
+// ρ_i = Σ_j X_ij² (row_sq_norms, kernels.cpp:295-303 order: column-outer).
+__global__ void k_row_sq_norms(const double* __restrict__ x, int64_t n, int64_t ld, int64_t p,
+                               double* __restrict__ rho, const Ctl* ctl) {
+  if (ctl && ctl->done) return;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double s = 0.0;
+  for (int64_t j = 0; j < p; ++j) {
+    const double v = x[i + j * ld];
+    s = __dadd_rn(s, __dmul_rn(v, v));
+  }
+  rho[i] = s;
+}
+
+// One axis of the separable real Fourier transform of an n-vector on the grid
+// (oracle axis_transform): forward out[..o..] = Σ_i Q[i,o]·in[..i..],
+// inverse out[..o..] = Σ_m Q[o,m]·in[..m..], index order, no contraction.
+__global__ void k_axis_transform(const double* __restrict__ in, double* __restrict__ out,
+                                 const double* __restrict__ q, int64_t N, int64_t nx, int64_t ny,
+                                 int64_t nz, int axis, int forward, const Ctl* ctl) {
+  if (ctl && ctl->done) return;
+  const int64_t n = nx * ny * nz;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  const int64_t stride = axis == 0 ? 1 : (axis == 1 ? nx : nx * ny);
+  const int64_t o = (e / stride) % N;
+  const int64_t base = e - o * stride;
+  double s = 0.0;
+  for (int64_t i = 0; i < N; ++i) {
+    const double qv = forward ? q[i + N * o] : q[o + N * i];
+    s = __dadd_rn(s, __dmul_rn(qv, in[base + i * stride]));
+  }
+  out[e] = s;
+}
+
+// Spectral division by λx+λy+λz with the constant mode removed (L† of the
+// periodic Laplacian), then (after the inverse transform, separate launch)
+// the KS potential.  Also accumulates the density scalars per block:
+//   spart[b·3 + {0,1,2}] = {Σ V ρ, Σ ρ h, Σ ρ^{4/3}}.
+__global__ void k_spectral_divide(double* __restrict__ a, const double* __restrict__ lx,
+                                  const double* __restrict__ ly, const double* __restrict__ lz,
+                                  int64_t nx, int64_t ny, int64_t nz, const Ctl* ctl) {
+  if (ctl && ctl->done) return;
+  const int64_t n = nx * ny * nz;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t x = i % nx, y = (i / nx) % ny, z = i / (nx * ny);
+  const double lam = __dadd_rn(__dadd_rn(lx[x], ly[y]), lz[z]);
+  a[i] = (i == 0) ? 0.0 : __ddiv_rn(a[i], lam);
+}
+
+__global__ void k_ks_potential(const double* __restrict__ v, const double* __restrict__ rho,
+                               const double* __restrict__ h, double* __restrict__ u, int64_t n,
+                               double c /* (3/π)^{1/3} */, double* __restrict__ spart,
+                               const Ctl* ctl) {
+  if (ctl && ctl->done) return;
+  __shared__ double sm[kStreamThreadsOps / 32];
+  double vr = 0.0, rh = 0.0, ex = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double r = rho[i];
+    const double cr = cbrt(r);
+    vr += v[i] * r;
+    rh += r * h[i];
+    ex += r * cr;
+    u[i] = __dsub_rn(__dadd_rn(v[i], h[i]), __dmul_rn(c, cr));
+  }
+  const double a = block_sum<kStreamThreadsOps>(vr, sm);
+  const double b = block_sum<kStreamThreadsOps>(rh, sm);
+  const double d = block_sum<kStreamThreadsOps>(ex, sm);
+  if (threadIdx.x == 0) {
+    spart[blockIdx.x * 3 + 0] = a;
+    spart[blockIdx.x * 3 + 1] = b;
+    spart[blockIdx.x * 3 + 2] = d;
+  }
+}
+
+}  // namespace pcal

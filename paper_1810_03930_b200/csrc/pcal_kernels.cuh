@@ -1,0 +1,226 @@
+// pcal_kernels.cuh — streaming / small-matrix / reduction kernels of one PCAL
+// iteration (solver.cpp:385-438 restated for HBM).  All reductions are
+// deterministic: per-block partials in fixed slots, summed in index order.
+#pragma once
+
+#include "common.cuh"
+
+namespace pcal {
+
+constexpr int kStreamThreads = 256;
+
+// out[c·ncols + col] = Σ_{r in chunk c} in[r·ncols + col]   (in: nrows × ncols row-major)
+__global__ void k_sum_rows(const double* __restrict__ in, int64_t nrows, int64_t ncols,
+                           int64_t rows_per_chunk, double* __restrict__ out, const Ctl* ctl) {
+  if (ctl && ctl->done) return;
+  const int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t c = blockIdx.y;
+  if (col >= ncols) return;
+  const int64_t r0 = c * rows_per_chunk;
+  const int64_t r1 = min(nrows, r0 + rows_per_chunk);
+  double s = 0.0;
+  for (int64_t r = r0; r < r1; ++r) s += in[r * ncols + col];
+  out[c * ncols + col] = s;
+}
+
+// W = Ψ(GᵀX) = ½(M1 + M1ᵀ), C = XᵀX − I (exactly symmetric, from the computed
+// upper triangle), written interleaved as the B operand of the X·[W|C] GEMM:
+//   mcat[k + (2j)·ldk] = W[k,j],  mcat[k + (2j+1)·ldk] = C[k,j]
+// (eval_iterate, solver.cpp:79-84).  fpart2[block] = Σ C² over the block.
+// gr: (2·pp) × pp column-major; rows [0,pp) = GᵀX, rows [pp,2pp) = XᵀX.
+__global__ void k_small_pxp(const double* __restrict__ gr, int64_t pp, int64_t p,
+                            double* __restrict__ mcat, int64_t ldk, double* __restrict__ cpart,
+                            const Ctl* ctl) {
+  if (ctl && ctl->done) return;
+  __shared__ double sm[kStreamThreads / 32];
+  const int64_t total = p * p;
+  const int64_t ldg = 2 * pp;
+  double acc = 0.0;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = e % p, j = e / p;
+    const double w = 0.5 * (gr[k + j * ldg] + gr[j + k * ldg]);
+    const int64_t a = min(k, j), b = max(k, j);
+    double c = gr[pp + a + b * ldg];
+    if (k == j) c += -1.0;
+    mcat[k + (2 * j) * ldk] = w;
+    mcat[k + (2 * j + 1) * ldk] = c;
+    acc += c * c;
+  }
+  const double s = block_sum<kStreamThreads>(acc, sm);
+  if (threadIdx.x == 0) cpart[blockIdx.x] = s;
+}
+
+// Stepsize inner products (stepsize_select, solver.cpp:218-222) with the
+// PCAL diagonal correction recomputed in registers (solver.cpp:397-405):
+//   GL = P − d∘X,  S = X − X_prev,  Y = GL − GL_prev.
+// part[block·3 + {0,1,2}] = partial {⟨S,S⟩, ⟨S,Y⟩, ⟨Y,Y⟩}.
+__global__ void k_bb_partials(const double* __restrict__ x, const double* __restrict__ pg,
+                              const double* __restrict__ xp, const double* __restrict__ pgp,
+                              const double* __restrict__ d, const double* __restrict__ dp,
+                              int64_t ld, int64_t p, double* __restrict__ part, const Ctl* ctl) {
+  if (ctl->done || ctl->iter == 0 || !ctl->have_prev) return;
+  __shared__ double sm[kStreamThreads / 32];
+  double ss = 0.0, sy = 0.0, yy = 0.0;
+  const int64_t half = ld / 2;  // ld is a multiple of 16: double2 vectors never straddle columns
+  const int64_t total = half * p;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e / half;
+    const double2 xv = reinterpret_cast<const double2*>(x)[e];
+    const double2 xpv = reinterpret_cast<const double2*>(xp)[e];
+    const double2 pv = reinterpret_cast<const double2*>(pg)[e];
+    const double2 ppv = reinterpret_cast<const double2*>(pgp)[e];
+    const double dj = d[j], dpj = dp[j];
+    {
+      const double s = xv.x - xpv.x;
+      const double y = (pv.x - dj * xv.x) - (ppv.x - dpj * xpv.x);
+      ss += s * s;
+      sy += s * y;
+      yy += y * y;
+    }
+    {
+      const double s = xv.y - xpv.y;
+      const double y = (pv.y - dj * xv.y) - (ppv.y - dpj * xpv.y);
+      ss += s * s;
+      sy += s * y;
+      yy += y * y;
+    }
+  }
+  const double a = block_sum<kStreamThreads>(ss, sm);
+  const double b = block_sum<kStreamThreads>(sy, sm);
+  const double c = block_sum<kStreamThreads>(yy, sm);
+  if (threadIdx.x == 0) {
+    part[blockIdx.x * 3 + 0] = a;
+    part[blockIdx.x * 3 + 1] = b;
+    part[blockIdx.x * 3 + 2] = c;
+  }
+}
+
+__device__ __forceinline__ double clamp_eta(const Ctl* c, double v) {
+  const double r = v > c->eta_min ? v : c->eta_min;
+  return r < c->eta_max ? r : c->eta_max;
+}
+
+// stepsize_select (solver.cpp:212-251) on the device; one thread.
+__global__ void k_eta(Ctl* ctl, const double* __restrict__ part, int nblocks) {
+  if (ctl->done) return;
+  if (threadIdx.x != 0) return;
+  Ctl* c = ctl;
+  double eta;
+  if (c->eta_kind == 0) {
+    eta = clamp_eta(c, c->gamma);
+  } else {
+    const double fallback = c->eta_prev > 0.0 ? c->eta_prev : c->eta0;
+    if (!c->have_prev || c->iter == 0) {
+      eta = clamp_eta(c, c->eta0 > 0.0 ? c->eta0 : fallback);
+    } else {
+      double ss = 0.0, sy = 0.0, yy = 0.0;
+      for (int b = 0; b < nblocks; ++b) {
+        ss += part[3 * b + 0];
+        sy += part[3 * b + 1];
+        yy += part[3 * b + 2];
+      }
+      const double bb1 = (ss == 0.0 || sy == 0.0) ? fallback : fabs(sy) / ss;
+      const double bb2 = (sy == 0.0) ? fallback : yy / fabs(sy);
+      double v = fallback;
+      switch (c->eta_kind) {
+        case 2: v = bb1; break;
+        case 3: v = bb2; break;
+        case 4: v = (c->iter % 2 == 1) ? bb1 : bb2; break;
+        case 1: v = (ss == 0.0) ? fallback : sqrt(yy) / sqrt(ss); break;
+        default: break;
+      }
+      eta = clamp_eta(c, v);
+    }
+  }
+  c->eta = eta;
+  c->step_deg = 0;
+  if (!(eta > 0.0)) {  // pcal_step: parameter_error (solver.cpp:266)
+    c->step_param = 1;
+    c->done = 3;
+  }
+}
+
+// pcal_step part 1 (solver.cpp:278-282): Z = X − (1/η)·GL with GL = P − d∘X,
+// written over the X_{k-1} buffer; npart[chunk·p + j] = Σ_{chunk rows} z².
+__global__ void k_update(const double* __restrict__ x, const double* __restrict__ pg,
+                         const double* __restrict__ d, double* __restrict__ z, int64_t n,
+                         int64_t ld, int64_t p, int64_t chunk, double* __restrict__ npart,
+                         const Ctl* ctl) {
+  if (ctl->done) return;
+  __shared__ double sm[kStreamThreads / 32];
+  const int64_t j = blockIdx.y;
+  const int64_t r0 = (int64_t)blockIdx.x * chunk;
+  const int64_t r1 = min(n, r0 + chunk);
+  const double inv_eta = 1.0 / ctl->eta;
+  const double dj = d[j];
+  double acc = 0.0;
+  const double* xj = x + j * ld;
+  const double* pj = pg + j * ld;
+  double* zj = z + j * ld;
+  for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+    const double xv = xj[i];
+    const double gl = pj[i] - dj * xv;
+    const double v = xv - inv_eta * gl;
+    zj[i] = v;
+    acc += v * v;
+  }
+  const double s = block_sum<kStreamThreads>(acc, sm);
+  if (threadIdx.x == 0) npart[blockIdx.x * p + j] = s;
+}
+
+// pcal_step part 2 (solver.cpp:283-305): z ·= 1/‖z‖; a column with ‖z‖ < 1e-14
+// keeps the previous column renormalized (or e_{j mod n}); non-finite ⇒ diverged.
+__global__ void k_normalize(const double* __restrict__ x, double* __restrict__ z, int64_t n,
+                            int64_t ld, int64_t p, int64_t chunk, int64_t nchunks,
+                            const double* __restrict__ npart, Ctl* ctl) {
+  if (ctl->done) return;
+  __shared__ double sm[kStreamThreads / 32];
+  __shared__ double s_inv;
+  __shared__ int s_deg;
+  const int64_t j = blockIdx.y;
+  const int64_t r0 = (int64_t)blockIdx.x * chunk;
+  const int64_t r1 = min(n, r0 + chunk);
+  if (threadIdx.x == 0) {
+    double nrm2 = 0.0;
+    for (int64_t c = 0; c < nchunks; ++c) nrm2 += npart[c * p + j];
+    const double nrm = sqrt(nrm2);
+    s_deg = nrm < 1e-14;
+    s_inv = 1.0 / nrm;
+  }
+  __syncthreads();
+  double* zj = z + j * ld;
+  bool bad = false;
+  if (!s_deg) {
+    const double inv = s_inv;
+    for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+      const double v = zj[i] * inv;
+      zj[i] = v;
+      bad |= !isfinite(v);
+    }
+  } else {
+    // degenerate column: whole-column norm of the previous iterate (rare path)
+    const double* xj = x + j * ld;
+    double acc = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) acc += xj[i] * xj[i];
+    const double pn2 = block_sum<kStreamThreads>(acc, sm);
+    if (threadIdx.x == 0) sm[0] = sqrt(pn2);
+    __syncthreads();
+    const double pn = sm[0];
+    for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+      double v;
+      if (pn > 0.0) v = xj[i] * (1.0 / pn);
+      else v = (i == (j % n)) ? 1.0 : 0.0;
+      zj[i] = v;
+      bad |= !isfinite(v);
+    }
+  }
+  if (s_deg && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&ctl->step_deg, 1);
+  if (__syncthreads_or(bad) && threadIdx.x == 0) {
+    ctl->step_bad = 1;
+    ctl->done = 2;
+  }
+}
+
+}  // namespace pcal

@@ -1,0 +1,159 @@
+"""GPU parity of the building blocks against the oracle / reference golden vectors.
+
+Tolerances (FP64): the DMMA contractions sum in a blocked order instead of the
+reference's sequential order, so products agree to a few ulps of the operand
+norms: ‖Δ‖ ≤ 1e-13·‖ref‖ (kernels); the 7-point stencil gradient uses
+round-to-nearest intrinsics in the oracle's order and must be BITWISE equal.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import rel
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden", "reference_small.npz")
+
+
+@pytest.fixture(scope="module")
+def gold():
+    return np.load(GOLD)
+
+
+@pytest.mark.parametrize("shape", [(37, 5, 4), (1000, 20, 20), (333, 7, 13), (4096, 128, 128),
+                                   (2048, 256, 200), (16, 1, 1)])
+def test_matmul_at_b(pcal, orc, shape):
+    n, pa, pb = shape
+    a = orc.random_normal(n, pa, 11)
+    b = orc.random_normal(n, pb, 12)
+    got = pcal.matmul_at_b(a, b)
+    want = orc.matmul_at_b(a, b)
+    assert got.shape == want.shape
+    assert rel(got, want) <= 1e-13
+
+
+@pytest.mark.parametrize("shape", [(37, 5), (1000, 20), (1001, 33), (8192, 64), (2048, 256)])
+def test_gram_exactly_symmetric(pcal, orc, shape):
+    n, p = shape
+    x = orc.random_normal(n, p, 21)
+    g = pcal.gram(x)
+    assert np.array_equal(g, g.T)  # gram mirrors the upper triangle (kernels.cpp:150-151)
+    assert rel(g, orc.gram(x)) <= 1e-13
+
+
+@pytest.mark.parametrize("shape", [(37, 5, 6), (1000, 20, 40), (513, 17, 3), (4096, 128, 256)])
+def test_matmul(pcal, orc, shape):
+    m, k, nc = shape
+    a = orc.random_normal(m, k, 31)
+    b = orc.random_normal(k, nc, 32)
+    assert rel(pcal.matmul(a, b), orc.matmul(a, b)) <= 1e-13
+
+
+def test_kernels_vs_reference_golden(pcal, gold):
+    assert rel(pcal.matmul_at_b(gold["k_a"], gold["k_b"]), gold["k_matmul_at_b"]) <= 1e-14
+    assert rel(pcal.gram(gold["k_a"]), gold["k_gram"]) <= 1e-14
+    assert rel(pcal.matmul(gold["k_a"], gold["k_c"]), gold["k_matmul"]) <= 1e-14
+
+
+def test_orthonormalize(pcal, orc, gold):
+    q = pcal.orthonormalize(gold["k_orth_x"])
+    assert np.abs(q - gold["k_orth_q"]).max() <= 1e-13
+    x = orc.random_normal(5000, 64, 41)
+    q = pcal.orthonormalize(x)
+    assert np.linalg.norm(q.T @ q - np.eye(64)) <= 1e-12  # acceptance_main.cpp:101
+    assert rel(q, orc.orthonormalize(x)) <= 1e-12
+    # X = Q·R with R = QᵀX upper triangular (span preserved)
+    r = q.T @ x
+    assert np.abs(np.tril(r, -1)).max() <= 1e-10 * np.abs(r).max()
+
+
+def test_orthonormalize_rank_deficient(pcal, orc):
+    x = orc.random_normal(40, 4, 42)
+    x[:, 3] = x[:, 0] + x[:, 1]  # exactly dependent column (test_kernels.cpp:150-181)
+    with pytest.raises(pcal.RankError):
+        pcal.orthonormalize(x)
+    with pytest.raises(np.linalg.LinAlgError):
+        orc.orthonormalize(x)
+
+
+def test_orthonormalize_fixed_point(pcal):
+    x = np.zeros((6, 3), order="F")
+    x[0, 0] = x[1, 1] = x[2, 2] = 1.0
+    assert np.abs(pcal.orthonormalize(x) - x).max() <= 1e-15
+
+
+def test_pcal_step_known_answers(pcal, orc, gold):
+    col = np.array([[3.0], [4.0]])
+    out, deg = pcal.pcal_step(col, np.zeros((2, 1)), 5.0)  # (3,4) → (0.6,0.8)
+    assert deg == 0 and abs(out[0, 0] - 0.6) < 1e-15 and abs(out[1, 0] - 0.8) < 1e-15
+    out, _ = pcal.pcal_step(gold["ps_x"], gold["ps_g"], 2.0)
+    assert np.abs(out - gold["ps_out"]).max() <= 1e-15
+    assert np.abs(np.linalg.norm(out, axis=0) - 1.0).max() <= 1e-14
+    # grad_l = eta·X ⇒ zero update ⇒ every column degenerate, previous column kept
+    x = gold["ps_x"]
+    out, deg = pcal.pcal_step(x, 2.0 * x, 2.0)
+    assert deg == 5
+    assert np.abs(out - x / np.linalg.norm(x, axis=0)).max() <= 1e-15
+    with pytest.raises(pcal.ParameterError):
+        pcal.pcal_step(x, x, 0.0)
+
+
+def test_pcal_step_divergence(pcal):
+    x = np.ones((8, 2), order="F")
+    g = np.zeros((8, 2), order="F")
+    g[0, 0] = np.inf
+    with pytest.raises(pcal.DivergenceError):
+        pcal.pcal_step(x, g, 1.0)
+
+
+def test_spectral_norm(pcal, orc, gold):
+    s = pcal.spectral_norm_estimate(gold["k_spec_a"], 11)
+    assert abs(s - gold["k_spec_s"]) <= 1e-9 * gold["k_spec_s"]
+
+
+def test_dense_gradient(pcal, orc):
+    n, p = 1000, 20
+    m = orc.dense_trace_min(n, p, 5, s=10.0)
+    x = orc.initial_point_qr(n, p, 6)
+    f_ref, g_ref = orc.evaluate(m, x)
+    f, g = pcal.evaluate(pcal.QuadraticModel(m.a, p, m.s), x)
+    assert rel(g, g_ref) <= 1e-13
+    assert abs(f - f_ref) <= 1e-12 * abs(f_ref)
+
+
+def test_dense_gradient_with_linear_term(pcal, orc):
+    from oracle.oracle import Model, MODEL_DENSE
+    n, p = 300, 7
+    a = orc.sym_part(orc.random_normal(n, n, 8))
+    g0 = orc.random_normal(n, p, 9)
+    x = orc.random_normal(n, p, 10)
+    f_ref, g_ref = orc.evaluate(Model(MODEL_DENSE, n, p, 1.0, a=a, g0=g0), x)
+    f, g = pcal.evaluate(pcal.QuadraticModel(a, p, 1.0, g0=g0), x)
+    assert rel(g, g_ref) <= 1e-13
+    assert abs(f - f_ref) <= 1e-12 * abs(f_ref)
+
+
+@pytest.mark.parametrize("grid,p", [((6, 5, 4), 3), ((64, 64, 64), 4), ((16, 16, 16), 33)])
+def test_stencil_gradient_bitwise(pcal, orc, grid, p):
+    from oracle.oracle import Model, MODEL_STENCIL
+    n = grid[0] * grid[1] * grid[2]
+    v = orc.random_uniform(n, 3)
+    x = orc.random_normal(n, p, 4)
+    f_ref, g_ref = orc.evaluate(Model(MODEL_STENCIL, n, p, 13.0, grid=grid, v=v), x)
+    f, g = pcal.evaluate(pcal.StencilModel(grid, v, p, 13.0), x)
+    assert np.array_equal(g, g_ref)  # same op order, no contraction
+    assert abs(f - f_ref) <= 1e-12 * abs(f_ref)
+
+
+@pytest.mark.parametrize("grid,p", [((6, 6, 6), 4), ((48, 48, 48), 3), ((8, 6, 10), 5)])
+def test_kohn_sham_gradient(pcal, orc, grid, p):
+    from oracle.oracle import Model, MODEL_KOHN_SHAM
+    n = grid[0] * grid[1] * grid[2]
+    v = -orc.random_uniform(n, 5)
+    x = orc.initial_point_qr(n, p, 6)
+    mo = Model(MODEL_KOHN_SHAM, n, p, 12.0, grid=grid, v=v)
+    f_ref, g_ref = orc.evaluate(mo, x)
+    f, g = pcal.evaluate(pcal.KohnShamModel(grid, v, p, 12.0), x)
+    assert rel(g, g_ref) <= 1e-14  # only the device cbrt may differ by an ulp
+    assert abs(f - f_ref) <= 1e-12 * abs(f_ref)
