@@ -170,9 +170,14 @@ __device__ __forceinline__ void epilogue(const GemmArgs& g, int tm, int tn, int 
           const int64_t row = mw0 + mt * 8 + r;
           if (row < e.n && col < e.p) {
             double gv = acc[mt][nt][x];
-            if (e.g0) gv += e.g0[row + col * e.ld];
+            double fv = gv;  // f = ½⟨X, AX + 2·G0⟩ = ½⟨X,AX⟩ + ⟨G0,X⟩
+            if (e.g0) {
+              const double g0v = e.g0[row + col * e.ld];
+              gv += g0v;
+              fv = gv + g0v;
+            }
             e.G[row + col * e.ld] = gv;
-            fs += e.X[row + col * e.ld] * gv;
+            fs += e.X[row + col * e.ld] * fv;
             bad |= !isfinite(gv);
           }
         }

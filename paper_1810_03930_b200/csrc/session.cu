@@ -889,7 +889,14 @@ void session_finish(pcal_session* s, pcal_report* r) {
         s->timers->orth +=
             std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
       if (ok) {
+        // the iteration kernels skip work once `done` is set: clear it for the
+        // post-orth evaluation (solver.cpp:452) and restore it afterwards
+        const int32_t zero = 0;
+        PCAL_CUDA(cudaMemcpyAsync(&s->ctl->done, &zero, sizeof(int32_t), cudaMemcpyHostToDevice,
+                                  s->stream));
         launch_eval(s, nb, 2, s->ctl);
+        PCAL_CUDA(cudaMemcpyAsync(&s->ctl->done, &s->h_ctl->done, sizeof(int32_t),
+                                  cudaMemcpyHostToDevice, s->stream));
         double post[8];
         PCAL_CUDA(cudaMemcpyAsync(post, s->post.p, sizeof(double) * 5, cudaMemcpyDeviceToHost,
                                   s->stream));
