@@ -1,0 +1,348 @@
+#!/usr/bin/env python
+"""PCAL iterations/s on B200 (BASELINE.json metric), one JSON line on rank 0.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl reference]
+
+A "step" is one PCAL iteration (solver.cpp:369-439) of config C (default 2:
+dense trace minimization, n=16384, p=128, FP64 — BASELINE configs[1]).
+  value : iterations/s with the instance resident in HBM, K iterations timed
+          with CUDA events on the session stream (graphs, no host sync), max
+          over ranks; the operator A (2 GiB) is larger than L2, so every
+          iteration streams it from HBM (no L2 flush needed).
+  e2e   : the public drop-in call pcal_solve() (host buffers: H2D of A and X0
+          from pinned memory, D2H of the report) for the config's full
+          iteration count + final orthonormalization, wall clock.
+  roofline : dominant kernel, achieved = algorithmic flops (or bytes) per launch
+          ÷ its mean CUDA-event duration measured in this run; peak = measured
+          FP64 DMMA rate (profiles/fp64_peaks_r01.json; MEASURED_PEAKS.json has
+          no FP64 entry) or MEASURED_PEAKS.json hbm_gbs for HBM-bound kernels.
+  cpu_baseline : the UNMODIFIED reference solve() (oracle/_ref) on the host
+          cores, per-iteration time from its own trace clock, bounded sample.
+--impl reference times that CPU implementation alone (rank 0; others exit 0).
+N > 1: one process per GPU (torchrun), independent replicas of the instance
+(row sharding with NCCL is the next step); value = N·K / max time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+TINY = float(np.finfo(float).tiny)
+INIT_SALT = 0x1235713
+
+
+def load_peaks() -> dict:
+    peaks = {"fp64_tflops": 37.15, "fp64_src": "fallback (DMMA microbenchmark, round 1)",
+             "hbm_gbs": 6544.3, "hbm_src": "fallback"}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        peaks["hbm_gbs"] = float(m["hbm_gbs"])
+        peaks["hbm_src"] = "MEASURED_PEAKS.json hbm_gbs"
+    except Exception:
+        pass
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_peaks_r01.json")) as f:
+            m = json.load(f)
+        peaks["fp64_tflops"] = float(m["dmma_tflops"])
+        peaks["fp64_src"] = "measured DMMA.8x8x4 peak, profiles/fp64_peaks_r01.json"
+    except Exception:
+        pass
+    return peaks
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+    NAMES = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+             0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+             0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, device: int):
+        self.samples, self.reasons, self.ok = [], 0, False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max = None
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self) -> dict:
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max, "reasons": ["unavailable"]}
+        names = [n for bit, n in self.NAMES.items() if self.reasons & bit and bit != 0x1]
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max,
+                "reasons": names, "samples": len(self.samples)}
+
+
+def dist_setup(ngpus: int):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+def max_over_ranks(v: float, world: int) -> float:
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world: int):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def pinned_f64(n_rows: int, n_cols: int):
+    """Column-major FP64 host matrix in pinned memory (for the e2e H2D copies)."""
+    import torch
+    t = torch.empty(n_rows * n_cols, dtype=torch.float64, pin_memory=True)
+    arr = t.numpy().reshape((n_cols, n_rows)).T  # Fortran-ordered view
+    return t, arr
+
+
+def cpu_reference_rate(inst, x0, budget_s: float = 15.0, threads: int = None, min_iters=1):
+    """Time the reference CPU solve() on a bounded sample; returns (iters/s, info)."""
+    from oracle.oracle import Config, Model, MODEL_DENSE, MODEL_KOHN_SHAM, MODEL_STENCIL
+    from oracle.oracle import Reference, Restatement, available_reference
+    threads = threads or os.cpu_count() or 1
+    R = Reference() if available_reference() else Restatement()
+    kind = {"dense": MODEL_DENSE, "stencil": MODEL_STENCIL, "kohn_sham": MODEL_KOHN_SHAM}[inst.kind]
+    m = Model(kind, inst.n, inst.p, inst.s, a=inst.a, grid=inst.grid or (0, 0, 0), v=inst.v)
+    # probe: one iteration, per-iteration time from the reference's own trace clock
+    probe = R.solve(m, Config(tol_rel_kkt=TINY, max_iter=1, threads=threads, final_orth=False), x0)
+    t_it = max(probe.trace[1, 6] - probe.trace[0, 6], 1e-6)
+    iters = int(max(min_iters, min(inst.iters, budget_s / t_it)))
+    rep = R.solve(m, Config(tol_rel_kkt=TINY, max_iter=iters, threads=threads, final_orth=False), x0)
+    per = (rep.trace[iters, 6] - rep.trace[0, 6]) / iters
+    what = "reference solve() (oracle/_ref)" if R.kind == "reference" else "C restatement (oracle)"
+    if inst.kind != "dense":
+        what += " driving the restated grid operator (no reference operator exists)"
+    info = {"kind": R.kind, "cores": threads, "iters": iters,
+            "sample": f"{what}: {iters} PCAL iteration(s) of config {inst.cfg} "
+                      f"(n={inst.n}, p={inst.p}), timed by its trace clock, setup excluded"}
+    return 1.0 / per, info
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import paper_1810_03930_b200 as P
+    from paper_1810_03930_b200.problems import make_instance
+    from oracle.oracle import Restatement
+    inst = make_instance(args.config, P, threads=os.cpu_count() or 8)
+    x0 = Restatement().initial_point_qr(inst.n, inst.p, inst.seed ^ INIT_SALT,
+                                        threads=os.cpu_count() or 8)
+    budget = float(os.environ.get("PCAL_REF_BUDGET_S", "60"))
+    rate, info = cpu_reference_rate(inst, x0, budget_s=budget, min_iters=1)
+    line = {"metric": "PCAL iterations/sec", "impl": "reference", "value": rate,
+            "unit": "iterations/s", "n_gpus": args.gpus, "steps": info["iters"],
+            "warmup": 1, "ms_per_step": 1e3 / rate, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"config {inst.cfg}", "n": inst.n, "p": inst.p,
+                       "kind": inst.kind},
+            "cpu_baseline": {"value": rate, "unit": "iterations/s", "cores": info["cores"],
+                             "kind": info["kind"], "sample": info["sample"]},
+            "e2e": {"value": rate, "unit": "iterations/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    import torch
+    import paper_1810_03930_b200 as P
+    from paper_1810_03930_b200.problems import make_instance
+
+    rank, world, local = dist_setup(args.gpus)
+    torch.cuda.set_device(local)
+    dev = local
+    K, W = args.steps, max(args.warmup, 3)
+    peaks = load_peaks()
+    hostthreads = max(1, (os.cpu_count() or 8) // world)
+
+    # ---- setup (not timed): instance in pinned host memory, X0 on the device
+    a_pin = None
+    if args.config in (1, 2):
+        n = {1: 1000, 2: 16384}[args.config]
+        a_t, a_pin = pinned_f64(n, n)
+    inst = make_instance(args.config, P, threads=hostthreads, a_out=a_pin, device=dev)
+    x0 = P.initial_point(inst.n, inst.p, inst.seed ^ INIT_SALT, device=dev)
+    model = inst.model(P)
+    prof_iters = 10
+    cfg = P.SolverConfig(tol_rel_kkt=TINY, max_iter=W + K + prof_iters + 2, final_orth=False,
+                         device=dev)
+
+    # ---- value: device-resident iterations, CUDA events on the session stream
+    ses = P.Session(model, cfg, x0)
+    stream = torch.cuda.ExternalStream(ses.stream, device=dev)
+    ses.run(W)
+    ses.sync()
+    barrier(world)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = ses.kernel_launches
+    with ClockSampler(dev) as clk:
+        e0.record(stream)
+        ses.run(K)
+        e1.record(stream)
+        e1.synchronize()
+    launches = ses.kernel_launches - l0
+    kpi = ses.kernels_per_iteration
+    ms = e0.elapsed_time(e1)
+    torch.cuda.synchronize()
+    ms = max_over_ranks(ms, world)
+    barrier(world)
+    phases = ses.profile(prof_iters)      # per-phase CUDA-event durations (same session)
+    rep = ses.finish(want_x=False)
+    ses.close()
+    assert rep.status == "max_iter", rep.status
+    ms_per = ms / K
+    value = world * K / (ms * 1e-3)
+
+    # ---- roofline of the dominant kernel + whole-iteration roofline
+    n, p = inst.n, inst.p
+    P64 = peaks["fp64_tflops"] * 1e12
+    BW = peaks["hbm_gbs"] * 1e9
+    work = {"gradient": (inst.grad_flops(), "tensor") if inst.kind == "dense"
+            else ((16.0 * n * p + inst.op_bytes()), "hbm"),
+            "gram": (3.0 * n * p * p, "tensor"), "xm": (4.0 * n * p * p, "tensor")}
+    dom = max(("gradient", "gram", "xm"), key=lambda k: phases[k])
+    amount, bound = work[dom]
+    t = phases[dom] * 1e-3
+    if bound == "tensor":
+        ach, peak, unit = amount / t / 1e12, peaks["fp64_tflops"], "TFLOP/s"
+        src = peaks["fp64_src"]
+    else:
+        ach, peak, unit = amount / t / 1e9, peaks["hbm_gbs"], "GB/s"
+        src = peaks["hbm_src"]
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", f"ncu_cfg{args.config}_summary.json")) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch", {}).get(dom)
+    except Exception:
+        pass
+    F = 7.0 * n * p * p + inst.grad_flops()
+    B = 80.0 * n * p + inst.op_bytes()
+    t_star = max(F / P64, B / BW)
+    roof = {"bound": bound, "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak,
+            "traffic": traffic, "kernel": dom, "kernel_ms": phases[dom], "peak_src": src}
+    iter_roof = {"flops": F, "bytes": B, "t_star_ms": t_star * 1e3, "frac": t_star * 1e3 / ms_per,
+                 "bound": "fp64" if F / P64 >= B / BW else "hbm",
+                 "phase_ms": {k: round(v, 5) for k, v in phases.items()}}
+
+    # ---- e2e: the public drop-in call with host buffers
+    e2e = None
+    if not args.no_e2e:
+        iters = inst.iters
+        x0h = np.asfortranarray(x0)
+        a_host = inst.a if inst.kind == "dense" else None
+        m_host = inst.model(P, a=a_host)
+        barrier(world)
+        t0 = time.perf_counter()
+        r = P.solve(m_host, P.SolverConfig(tol_rel_kkt=TINY, max_iter=iters, device=dev), x0h)
+        wall = time.perf_counter() - t0
+        wall = max_over_ranks(wall, world)
+        h2d = inst.op_bytes() + 8 * n * p
+        d2h = 8 * 2 * n * p + 8 * 7 * (iters + 1)
+        e2e = {"value": world * r.iterations / wall, "unit": "iterations/s",
+               "h2d_bytes_per_step": h2d / r.iterations, "d2h_bytes_per_step": d2h / r.iterations,
+               "iterations": r.iterations, "wall_s": wall, "status": r.status,
+               "final_post_feas": r.final_post_orth.feas if r.final_post_orth else None,
+               "includes": "H2D A+X0 (pinned), all iterations, final CholeskyQR2, D2H trace+X"}
+
+    # ---- CPU baseline (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            rate, info = cpu_reference_rate(inst, np.asfortranarray(x0), budget_s=15.0)
+            cpu = {"value": rate, "unit": "iterations/s", "cores": info["cores"],
+                   "kind": info["kind"], "sample": info["sample"]}
+        except Exception as e:  # reported, never silently substituted
+            cpu = {"value": None, "unit": "iterations/s", "cores": 0, "kind": "unavailable",
+                   "sample": f"failed: {e}"}
+
+    if rank == 0:
+        wl = {1: "config 1: dense trace-min n=1000 p=20 (A=sym(randn), seed 1)",
+              2: "config 2: dense trace-min n=16384 p=128 (A=sym(randn), seed 1)",
+              3: "config 3: 7-pt periodic Laplacian + diag V, 64^3, p=256, seed 1",
+              4: "config 4: Kohn-Sham-like 48^3, p=512, seed 1",
+              5: "config 5: 7-pt Laplacian + diag V, 128^3, p=1024, seed 1"}[args.config]
+        line = {
+            "metric": "PCAL iterations/sec", "value": value, "unit": "iterations/s",
+            "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": ms_per,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference RNG stream, seed 1; no dataset)",
+            "config": {"workload": wl, "n": n, "p": p, "kind": inst.kind, "s": inst.s,
+                       "parallelism": "single-gpu" if world == 1 else f"replicas x{world}",
+                       "l2": ("inputs larger than L2: A = %.1f GiB streamed every iteration"
+                              % (inst.op_bytes() / 2 ** 30)) if inst.kind == "dense"
+                       else "working set (X, P, X_prev, P_prev) larger than L2",
+                       "iteration_graph_kernels": kpi},
+            "roofline": roof, "iteration_roofline": iter_roof, "cpu_baseline": cpu,
+            "e2e": e2e, "clocks": clk.summary(), "gpu_launches": launches,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

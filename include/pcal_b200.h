@@ -154,6 +154,10 @@ int pcal_session_get_x(pcal_session* s, double* x_out, double* eta_out, int64_t*
 int pcal_session_device_x(pcal_session* s, const double** x, int64_t* ld);
 /* Number of kernels this library launched since session creation. */
 int64_t pcal_session_kernel_launches(pcal_session* s);
+/* Run `iters` iterations WITHOUT graphs, timing each phase with CUDA events on
+ * the session stream; ms_out[4] = mean ms per iteration of {streaming step
+ * (stepsize + pcal_step), gradient, Gram + p×p, X·[W|C] + reductions}. */
+int pcal_session_profile(pcal_session* s, int64_t iters, double* ms_out);
 /* Per-iteration launch count of the captured iteration graph. */
 int64_t pcal_session_kernels_per_iteration(pcal_session* s);
 

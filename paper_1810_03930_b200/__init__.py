@@ -129,6 +129,7 @@ def lib() -> C.CDLL:
     L.pcal_session_device_x.argtypes = [vp, C.POINTER(vp), C.POINTER(i64)]
     L.pcal_session_kernel_launches.argtypes = [vp]
     L.pcal_session_kernel_launches.restype = i64
+    L.pcal_session_profile.argtypes = [vp, i64, _dp]
     L.pcal_session_kernels_per_iteration.argtypes = [vp]
     L.pcal_session_kernels_per_iteration.restype = i64
     L.pcal_matmul_at_b.argtypes = [vp, vp, i64, i64, i64, vp, i32]
@@ -416,6 +417,12 @@ class Session:
                                                   self.config.max_iter, want_x)
         _check(self._L.pcal_session_finish(self._h, C.byref(rep)))
         return _report_from(rep, trace, stop_x, final_x)
+
+    def profile(self, iters: int) -> dict:
+        """Mean ms per iteration of each phase (CUDA events, no graphs)."""
+        out = (C.c_double * 4)()
+        _check(self._L.pcal_session_profile(self._h, iters, C.cast(out, _dp)))
+        return {"step": out[0], "gradient": out[1], "gram": out[2], "xm": out[3]}
 
     @property
     def kernel_launches(self) -> int:

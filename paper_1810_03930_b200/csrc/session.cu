@@ -286,7 +286,10 @@ struct pcal_session {
   bool use_graphs = true;
   std::chrono::steady_clock::time_point t_start;
   pcal_category_timers* timers = nullptr;
-  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t pev[6] = {};   // phase events (timers / profiling; never inside graphs)
+  bool pev_on = false;
+  double prof_ms[4] = {0, 0, 0, 0};  // stream, gradient, gram+pxp, xm+reductions
+  int64_t prof_iters = 0;
   ~pcal_session();
 };
 
@@ -294,6 +297,10 @@ namespace pcal {
 
 static double* Xof(pcal_session* s, int b) { return s->pair[b].p + s->ld * s->pp; }
 static double* Pof(pcal_session* s, int b) { return s->pair[b].p; }
+
+static void mark(pcal_session* s, int i) {
+  if (s->pev_on) PCAL_CUDA(cudaEventRecord(s->pev[i], s->stream));
+}
 
 struct LaunchScope {
   int64_t* prev;
@@ -377,18 +384,17 @@ static void launch_eval(pcal_session* s, int b, int mode, const Ctl* ctl_guard) 
   cudaStream_t st = s->stream;
   k_zero_i32<<<1, 1, 0, st>>>(s->bad, ctl_guard);
   count_launch();
-  cudaEvent_t* ev = s->timers ? s->ev : nullptr;
-  if (ev) PCAL_CUDA(cudaEventRecord(ev[0], st));
+  mark(s, 1);
   launch_gradient(s, b, ctl_guard);
-  if (ev) PCAL_CUDA(cudaEventRecord(ev[1], st));
+  mark(s, 2);
   launch_gemm(s->gram[b], st);
   k_small_pxp<<<s->cp_blocks, kStreamThreads, 0, st>>>(s->gr.p, s->pp, s->p, s->mcat.p, s->pp,
                                                        s->cpart.p, ctl_guard);
   count_launch();
+  mark(s, 3);
   launch_gemm(s->xm[b], st);
   launch_colsums(s, s->fpart.p, s->nrb_f, s->kpart.p, s->dpart.p, s->nrb_xm, s->fcol.p,
                  s->kcol.p, s->dvec[b].p, ctl_guard);
-  if (ev) PCAL_CUDA(cudaEventRecord(ev[2], st));
   FinishArgs fa{};
   fa.fcol = s->fcol.p;
   fa.kcol = s->kcol.p;
@@ -404,13 +410,20 @@ static void launch_eval(pcal_session* s, int b, int mode, const Ctl* ctl_guard) 
   fa.c_xc = s->c_xc;
   k_finish_eval<<<1, 32, 0, st>>>(fa, s->ctl, s->post.p);
   count_launch();
-  if (ev) {
-    PCAL_CUDA(cudaEventSynchronize(ev[2]));
-    float a = 0, c = 0;
-    PCAL_CUDA(cudaEventElapsedTime(&a, ev[0], ev[1]));
-    PCAL_CUDA(cudaEventElapsedTime(&c, ev[1], ev[2]));
-    s->timers->func += a * 1e-3;
-    s->timers->blas3 += c * 1e-3;
+  mark(s, 4);
+  if (s->pev_on) {
+    PCAL_CUDA(cudaEventSynchronize(s->pev[4]));
+    float g = 0, gm = 0, xm = 0;
+    PCAL_CUDA(cudaEventElapsedTime(&g, s->pev[1], s->pev[2]));
+    PCAL_CUDA(cudaEventElapsedTime(&gm, s->pev[2], s->pev[3]));
+    PCAL_CUDA(cudaEventElapsedTime(&xm, s->pev[3], s->pev[4]));
+    if (s->timers) {  // CategoryTimers: products inside evaluate count as func (report.hpp:66-72)
+      s->timers->func += g * 1e-3;
+      s->timers->blas3 += (gm + xm) * 1e-3;
+    }
+    s->prof_ms[1] += g;
+    s->prof_ms[2] += gm;
+    s->prof_ms[3] += xm;
   }
 }
 
@@ -418,6 +431,7 @@ static void launch_eval(pcal_session* s, int b, int mode, const Ctl* ctl_guard) 
 static void launch_iteration(pcal_session* s, int b) {
   cudaStream_t st = s->stream;
   const int nb = 1 - b;
+  mark(s, 0);
   k_bb_partials<<<s->bb_blocks, kStreamThreads, 0, st>>>(Xof(s, b), Pof(s, b), Xof(s, nb),
                                                          Pof(s, nb), s->dvec[b].p, s->dvec[nb].p,
                                                          s->ld, s->p, s->bbpart.p, s->ctl);
@@ -429,8 +443,15 @@ static void launch_iteration(pcal_session* s, int b) {
                                              s->up_chunk, s->up_nchunks, s->npart.p, s->ctl);
   count_launch(4);
   PCAL_CUDA(cudaGetLastError());
+  mark(s, 5);
   launch_eval(s, nb, 0, s->ctl);
   PCAL_CUDA(cudaGetLastError());
+  if (s->pev_on) {
+    float a = 0;
+    PCAL_CUDA(cudaEventElapsedTime(&a, s->pev[0], s->pev[5]));
+    s->prof_ms[0] += a;
+    s->prof_iters += 1;
+  }
 }
 
 static void build_plans(pcal_session* s) {
@@ -662,7 +683,7 @@ static void capture_graphs(pcal_session* s) {
 pcal_session::~pcal_session() {
   for (auto& g : graph)
     if (g) cudaGraphExecDestroy(g);
-  for (auto& e : ev)
+  for (auto& e : pev)
     if (e) cudaEventDestroy(e);
   if (bad) cudaFree(bad);
   if (ctl) cudaFree(ctl);
@@ -716,8 +737,8 @@ void session_create(const pcal_model_desc* model, const pcal_config* config, con
                                : clamp_eta_h(config, model->s + 2.0 * s->beta);
   LaunchScope ls(&s->launches);
   PCAL_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
-  if (timers)
-    for (auto& e : s->ev) PCAL_CUDA(cudaEventCreate(&e));
+  for (auto& e : s->pev) PCAL_CUDA(cudaEventCreate(&e));
+  s->pev_on = timers != nullptr;
   alloc_state(s.get());
   upload_model(s.get());
   build_plans(s.get());
@@ -984,6 +1005,25 @@ void pcal_session_destroy(pcal_session* s) {
 }
 
 int64_t pcal_session_kernel_launches(pcal_session* s) { return s ? s->launches : 0; }
+
+int pcal_session_profile(pcal_session* s, int64_t iters, double* ms_out) {
+  return guarded([&] {
+    PCAL_CUDA(cudaSetDevice(s->device));
+    LaunchScope ls(&s->launches);
+    s->pev_on = true;
+    for (double& v : s->prof_ms) v = 0.0;
+    s->prof_iters = 0;
+    iters = std::min<int64_t>(iters, s->cfg.max_iter - s->launched);  // trace capacity
+    for (int64_t i = 0; i < iters; ++i) {
+      launch_iteration(s, (int)(s->next_k % 2));
+      s->next_k++;
+      s->launched++;
+    }
+    s->pev_on = s->timers != nullptr;
+    PCAL_CUDA(cudaStreamSynchronize(s->stream));
+    for (int i = 0; i < 4; ++i) ms_out[i] = s->prof_iters ? s->prof_ms[i] / s->prof_iters : 0.0;
+  });
+}
 int64_t pcal_session_kernels_per_iteration(pcal_session* s) { return s ? s->kernels_per_iter : 0; }
 
 int pcal_session_set_state(pcal_session* s, const double* x_prev, const double* x, int64_t k,
