@@ -170,12 +170,23 @@ def run_reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    import paper_1810_03930_b200 as P
-    from paper_1810_03930_b200.problems import make_instance
+    # the instance comes from the oracle's restatement of the reference RNG
+    # (bitwise the reference's data): nothing of the B200 library on this path
+    from paper_1810_03930_b200.problems import CONFIGS, REFERENCE_S, Instance, ks_potential
     from oracle.oracle import Restatement
-    inst = make_instance(args.config, P, threads=os.cpu_count() or 8)
-    x0 = Restatement().initial_point_qr(inst.n, inst.p, inst.seed ^ INIT_SALT,
-                                        threads=os.cpu_count() or 8)
+    O = Restatement()
+    c = CONFIGS[args.config]
+    th = os.cpu_count() or 8
+    if c["kind"] == "dense":
+        m = O.dense_trace_min(c["n"], c["p"], 1, s=REFERENCE_S.get((c["n"], 1)), threads=th)
+        inst = Instance(args.config, "dense", m.n, m.p, c["iters"], m.s, a=m.a)
+    else:
+        g = c["grid"]
+        nn = g[0] * g[1] * g[2]
+        v = O.random_uniform(nn, 1) if c["kind"] == "stencil" else ks_potential(g, 1, O)
+        s = 12.0 + float(v.max()) if c["kind"] == "stencil" else 6.0 + float(np.abs(v).max())
+        inst = Instance(args.config, c["kind"], nn, c["p"], c["iters"], s, v=v, grid=g)
+    x0 = O.initial_point_qr(inst.n, inst.p, inst.seed ^ INIT_SALT, threads=th)
     budget = float(os.environ.get("PCAL_REF_BUDGET_S", "60"))
     rate, info = cpu_reference_rate(inst, x0, budget_s=budget, min_iters=1)
     line = {"metric": "PCAL iterations/sec", "impl": "reference", "value": rate,

@@ -70,9 +70,10 @@ class Instance:
         return 12.0 * n * p + 6.0 * 48 * n
 
 
-def ks_potential(grid, seed: int, pcal) -> np.ndarray:
+def ks_potential(grid, seed: int, gen) -> np.ndarray:
+    """`gen.random_uniform(count, seed)` must be the reference stream."""
     nx, ny, nz = grid
-    u = pcal.random_uniform(3 * 32, seed)
+    u = gen.random_uniform(3 * 32, seed)
     centres = (u.reshape(32, 3) * np.array([nx, ny, nz], dtype=float))  # a-major
     x = np.arange(nx, dtype=float)
     y = np.arange(ny, dtype=float)
