@@ -12,7 +12,7 @@ namespace pcal {
 // ------------------------------------------------------------------------------
 
 template <int AM>
-using CfgBig = GemmCfg<128, 128, 2, 4, 3, AM>;
+using CfgBig = GemmCfg<128, 128, 2, 4, 4, AM>;
 template <int AM>
 using CfgMid = GemmCfg<64, 64, 2, 2, 4, AM>;
 template <int AM>
@@ -124,7 +124,7 @@ static void launch_cfg(const GemmPlan& pl, cudaStream_t st) {
                                    Cfg::SMEM_BYTES));
     attr_set = true;
   }
-  kern<<<pl.args.grid, Cfg::THREADS, Cfg::SMEM_BYTES, st>>>(pl.args);
+  kern<<<pl.args.grid, Cfg::THREADS + 128, Cfg::SMEM_BYTES, st>>>(pl.args);
   PCAL_CUDA(cudaGetLastError());
   count_launch();
   if (pl.ntasks) {

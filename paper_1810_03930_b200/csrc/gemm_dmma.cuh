@@ -58,7 +58,7 @@ struct GemmCfg {
   static constexpr int A_STAGE = AMODE == A_MCONTIG ? BK * SA_M : BM * SA_K;
   static constexpr int SB_K = BK + 4;       // Bs[n][k]
   static constexpr int B_STAGE = BN * SB_K;
-  static constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) * 8;
+  static constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) * 8 + 2 * STAGES * 8;
   static_assert(WM % 8 == 0 && WN % 8 == 0, "warp tile must be a multiple of 8");
 };
 
@@ -223,31 +223,150 @@ __device__ __forceinline__ size_t frag_index(int warp, int mt, int nt, int x, in
   return ((((size_t)warp * Cfg::MT + mt) * Cfg::NT + nt) * 2 + x) * 32 + lane;
 }
 
+// ---- mbarrier helpers ------------------------------------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)));
+}
+// arrives on `bar` once all prior cp.async of this thread have landed
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)));
+}
+
+// ---- producer: one warp streams the CTA's unit range into the smem ring ---------
+// Per-lane source pointers are set up once per tile and advanced by one k-slice
+// per unit, so the copy loop is pure LDGSTS + pointer increments.
+template <class Cfg>
+__device__ __forceinline__ void produce(const GemmArgs& g, double* As, double* Bs,
+                                        uint64_t* full, uint64_t* empty, int64_t u0, int64_t u1,
+                                        int lane) {
+  constexpr int BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK, S = Cfg::STAGES;
+  // A_MCONTIG: lane owns m-chunks {2·lane + 64·h}; A_KCONTIG / B: lane owns
+  // rows {lane/8 + 4·j} at k-chunk lane%8.  One base pointer per operand is
+  // advanced by one k-slice per unit (the producer runs on 40 registers).
+  constexpr int AH = Cfg::AMODE == A_MCONTIG ? BM / 64 : BM / 4;
+  constexpr int BJ = BN / 4;
+  static_assert(Cfg::AMODE != A_MCONTIG || BM % 64 == 0, "MCONTIG producer needs BM % 64 == 0");
+  static_assert(BK == 16 && AH <= 32 && BJ <= 32, "producer layout");
+  const double* pa = g.A;
+  const double* pb = g.B;
+  unsigned amask = 0, bmask = 0;
+  int cur_tile = -1;
+  const int64_t a_step = Cfg::AMODE == A_MCONTIG ? (int64_t)BK * g.lda : BK;
+  const int64_t a_rows = Cfg::AMODE == A_MCONTIG ? 64 : 4 * g.lda;  // stride between lane chunks
+  const int64_t b_rows = 4 * g.ldb;
+  for (int64_t u = u0; u < u1; ++u) {
+    const int64_t i = u - u0;
+    const int s = (int)(i % S);
+    const unsigned ph = (unsigned)((i / S) & 1);
+    const int t = (int)(u / g.ki);
+    if (t != cur_tile) {  // (re)base on this tile at k-iteration u % ki
+      cur_tile = t;
+      const int2 tc = g.tiles[t];
+      const int64_t m0 = (int64_t)tc.x * BM, n0 = (int64_t)tc.y * BN;
+      const int64_t k0 = (u % g.ki) * BK;
+      amask = 0;
+      bmask = 0;
+      if constexpr (Cfg::AMODE == A_MCONTIG) {
+        pa = g.A + (m0 + 2 * lane) + k0 * g.lda;
+#pragma unroll
+        for (int h = 0; h < AH; ++h)
+          if (m0 + 2 * lane + 64 * h < g.M) amask |= 1u << h;
+      } else {
+        pa = g.A + (k0 + 2 * (lane & 7)) + (m0 + (lane >> 3)) * g.lda;
+#pragma unroll
+        for (int h = 0; h < AH; ++h)
+          if (m0 + (lane >> 3) + 4 * h < g.M) amask |= 1u << h;
+      }
+      pb = g.B + (k0 + 2 * (lane & 7)) + (n0 + (lane >> 3)) * g.ldb;
+#pragma unroll
+      for (int j = 0; j < BJ; ++j)
+        if (n0 + (lane >> 3) + 4 * j < g.N) bmask |= 1u << j;
+    }
+    mbar_wait(&empty[s], ph ^ 1u);
+    double* as = As + s * Cfg::A_STAGE;
+    double* bs = Bs + s * Cfg::B_STAGE;
+    if constexpr (Cfg::AMODE == A_MCONTIG) {
+#pragma unroll
+      for (int h = 0; h < AH; ++h) {
+        const bool ok = (amask >> h) & 1u;
+#pragma unroll
+        for (int kr = 0; kr < BK; ++kr)
+          cp_async16(as + kr * Cfg::SA_M + 2 * lane + 64 * h, ok ? pa + h * a_rows + kr * g.lda : g.A,
+                     ok);
+      }
+    } else {
+#pragma unroll
+      for (int h = 0; h < AH; ++h) {
+        const bool ok = (amask >> h) & 1u;
+        cp_async16(as + ((lane >> 3) + 4 * h) * Cfg::SA_K + 2 * (lane & 7),
+                   ok ? pa + h * a_rows : g.A, ok);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < BJ; ++j) {
+      const bool ok = (bmask >> j) & 1u;
+      cp_async16(bs + ((lane >> 3) + 4 * j) * Cfg::SB_K + 2 * (lane & 7), ok ? pb + j * b_rows : g.B,
+                 ok);
+    }
+    cp_async_mbar_arrive(&full[s]);
+    pa += a_step;
+    pb += BK;
+  }
+}
+
 // ---- main kernel ----------------------------------------------------------------
+// Warp-specialized: warps [0, WARPS) consume (LDS + DMMA + epilogue), warp
+// WARPS produces (cp.async ring, one mbarrier pair per stage); the rest of
+// the producer warpgroup only donates its registers.
 template <class Cfg, int EPI>
-__global__ void __launch_bounds__(Cfg::THREADS, 1) gemm_streamk(GemmArgs g) {
+__global__ void __launch_bounds__(Cfg::THREADS + 128, 1) gemm_streamk(GemmArgs g) {
   if (g.ctl && g.ctl->done) return;
   extern __shared__ __align__(16) double smem[];
   double* As = smem;
   double* Bs = smem + Cfg::STAGES * Cfg::A_STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(Bs + Cfg::STAGES * Cfg::B_STAGE);
+  uint64_t* empty = full + Cfg::STAGES;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int wm = warp / Cfg::WARPS_N, wn = warp % Cfg::WARPS_N;
   const int32_t cta = blockIdx.x;
   const int64_t u0 = cta_unit_begin(cta, g.units, g.grid);
   const int64_t u1 = cta_unit_begin(cta + 1, g.units, g.grid);
   if (u0 >= u1) return;
-
-  // prologue: fill STAGES-1 stages
-#pragma unroll
-  for (int s = 0; s < Cfg::STAGES - 1; ++s) {
-    const int64_t u = u0 + s;
-    if (u < u1) {
-      const int t = (int)(u / g.ki);
-      const int2 tc = g.tiles[t];
-      load_stage<Cfg>(g, As + s * Cfg::A_STAGE, Bs + s * Cfg::B_STAGE, tc.x, tc.y, (int)(u % g.ki));
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < Cfg::STAGES; ++s) {
+      mbar_init(&full[s], 32);
+      mbar_init(&empty[s], Cfg::WARPS);
     }
-    cp_async_commit();
   }
+  __syncthreads();
+  // The producer owns a whole warpgroup (setmaxnreg is warpgroup-collective):
+  // with 8 consumer warps, consumers take 232 registers and the producer
+  // group 40 (8·32·232 + 4·32·40 ≤ 64K).
+  if (warp >= Cfg::WARPS) {
+    if constexpr (Cfg::WARPS == 8) asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::);
+    if (warp == Cfg::WARPS) {
+      produce<Cfg>(g, As, Bs, full, empty, u0, u1, lane);
+      cp_async_wait<0>();
+    }
+    return;
+  }
+  if constexpr (Cfg::WARPS == 8) asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::);
+  const int wm = warp / Cfg::WARPS_N, wn = warp % Cfg::WARPS_N;
 
   double acc[Cfg::MT][Cfg::NT][2];
 #pragma unroll
@@ -258,21 +377,11 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) gemm_streamk(GemmArgs g) {
   int64_t seg_begin = u0;  // first unit of the current tile segment
   for (int64_t u = u0; u < u1; ++u) {
     const int64_t i = u - u0;
-    cp_async_wait<Cfg::STAGES - 2>();
-    __syncthreads();
-    {
-      const int64_t un = u + Cfg::STAGES - 1;
-      if (un < u1) {
-        const int s = (int)(un - u0) % Cfg::STAGES;
-        const int t = (int)(un / g.ki);
-        const int2 tc = g.tiles[t];
-        load_stage<Cfg>(g, As + s * Cfg::A_STAGE, Bs + s * Cfg::B_STAGE, tc.x, tc.y,
-                        (int)(un % g.ki));
-      }
-      cp_async_commit();
-    }
     const int s = (int)(i % Cfg::STAGES);
+    mbar_wait(&full[s], (unsigned)((i / Cfg::STAGES) & 1));
     mma_stage<Cfg>(As + s * Cfg::A_STAGE, Bs + s * Cfg::B_STAGE, wm, wn, lane, acc);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
 
     const int t = (int)(u / g.ki);
     const int kk = (int)(u % g.ki);
@@ -299,7 +408,6 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) gemm_streamk(GemmArgs g) {
       seg_begin = u + 1;
     }
   }
-  cp_async_wait<0>();
 }
 
 // Sums the partials of split tiles in CTA order and applies the epilogue.
