@@ -1,0 +1,46 @@
+// pcal_cpp_example.cpp — the reference's Rayleigh–Ritz acceptance check
+// (acceptance_main.cpp:50-73 shape: n=200, p=10, PCAL defaults) written against
+// the C++ mirror (include/orthopt_b200/solver.hpp).  Exit code 0 on success.
+//   usage: pcal_cpp_example [n p]
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "orthopt_b200/solver.hpp"
+
+int main(int argc, char** argv) {
+  using namespace orthopt_b200;
+  const std::int64_t n = argc > 2 ? std::atoll(argv[1]) : 200;
+  const std::int64_t p = argc > 2 ? std::atoll(argv[2]) : 10;
+  try {
+    DenseMatrix a(n, n);
+    check(pcal_gen_dense_operator(n, 101, a.data(), 4));  // sym_part(random_normal(n,n,Rng(101)))
+    double s = 0.0;
+    check(pcal_spectral_norm_estimate(a.data(), n, 0x73706563, &s, 0));
+    QuadraticModel model(a, p, s);
+    SolverConfig cfg;
+    const DenseMatrix x0 = initial_point_qr(n, p, 102);
+    CategoryTimers timers;
+    const RunReport rep = solve(model, cfg, x0, &timers);
+    std::printf("status=%d iterations=%lld f_post=%.12f feas_post=%.3e blas3=%.4fs func=%.4fs orth=%.4fs\n",
+                static_cast<int>(rep.status), static_cast<long long>(rep.iterations),
+                rep.final_post_orth ? rep.final_post_orth->fval : NAN,
+                rep.final_post_orth ? rep.final_post_orth->feas : NAN, timers.blas3, timers.func,
+                timers.orth);
+    if (rep.status != RunStatus::Converged || !rep.final_post_orth ||
+        rep.final_post_orth->feas > 1e-12)
+      return 1;
+    // parameter errors are thrown before iterating (solver.cpp:106-118)
+    cfg.tol_rel_kkt = 0.0;
+    try {
+      solve(model, cfg, x0);
+      return 2;
+    } catch (const parameter_error&) {
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    std::fprintf(stderr, "error: %s\n", e.what());
+    return 3;
+  }
+}

@@ -1,0 +1,248 @@
+// orthopt_b200/solver.hpp — header-only C++ mirror of the reference solver API
+// (/root/reference/proj/core/include/orthopt/solver.hpp, report.hpp, errors.hpp,
+// problems.hpp), implemented over the C ABI of libpcal_b200.so
+// (include/pcal_b200.h).  A caller of orthopt::solve() switches by changing the
+// namespace and constructing a device-evaluated model descriptor instead of a
+// virtual ObjectiveModel subclass:
+//
+//   orthopt_b200::QuadraticModel model(a, p, s);           // problems.hpp:53-69
+//   orthopt_b200::SolverConfig cfg;                        // solver.hpp:30-42
+//   orthopt_b200::RunReport rep = orthopt_b200::solve(model, cfg, x0);
+//
+// Errors mirror errors.hpp: parameter_error / dimension_error are thrown before
+// iterating; divergence inside the run is reported via RunStatus::Diverged.
+#pragma once
+
+#include <cstdint>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../pcal_b200.h"
+
+namespace orthopt_b200 {
+
+// ---- errors (errors.hpp:9-50) -------------------------------------------------
+struct dimension_error : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+struct parameter_error : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+struct rank_error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct device_error : std::runtime_error {  // CUDA failure / no B200: no CPU fallback
+  using std::runtime_error::runtime_error;
+};
+
+inline void check(int rc) {
+  if (rc == PCAL_OK) return;
+  const std::string msg = pcal_last_error();
+  switch (rc) {
+    case PCAL_E_PARAMETER: throw parameter_error(msg);
+    case PCAL_E_DIMENSION: throw dimension_error(msg);
+    case PCAL_E_RANK: throw rank_error(msg);
+    default: throw device_error(msg);
+  }
+}
+
+// ---- DenseMatrix (matrix.hpp:16-67): column-major FP64 -----------------------
+class DenseMatrix {
+ public:
+  DenseMatrix() = default;
+  DenseMatrix(std::int64_t rows, std::int64_t cols) : rows_(rows), cols_(cols) {
+    if (rows < 1 || cols < 1) throw dimension_error("DenseMatrix: dimensions must be positive");
+    data_.assign(static_cast<size_t>(rows * cols), 0.0);
+  }
+  std::int64_t rows() const { return rows_; }
+  std::int64_t cols() const { return cols_; }
+  bool empty() const { return data_.empty(); }
+  double& operator()(std::int64_t i, std::int64_t j) { return data_[i + j * rows_]; }
+  double operator()(std::int64_t i, std::int64_t j) const { return data_[i + j * rows_]; }
+  double* data() { return data_.data(); }
+  const double* data() const { return data_.data(); }
+  std::size_t size() const { return data_.size(); }
+
+ private:
+  std::int64_t rows_ = 0, cols_ = 0;
+  std::vector<double> data_;
+};
+
+// ---- configuration (solver.hpp:13-42) -----------------------------------------
+struct StepsizeRule {
+  enum class Kind { Constant, Differential, Bb1, Bb2, Abb };
+  Kind kind = Kind::Abb;
+  double gamma = 1.0;
+  double eta_min = 1e-10;
+  double eta_max = 1e10;
+  double eta0 = 0.0;
+};
+enum class MultiplierRule { PlamFormula, PcalFormula };
+
+struct SolverConfig {
+  double beta = -1.0;
+  StepsizeRule eta_rule{};
+  MultiplierRule multiplier_rule = MultiplierRule::PcalFormula;
+  double tol_rel_kkt = 1e-8;
+  std::int64_t max_iter = 3000;
+  int device = 0;  // replaces the explicit thread count: an explicit GPU ordinal
+  bool final_orth = true;
+};
+
+// ---- results (report.hpp:13-72) --------------------------------------------------
+struct MetricSample {
+  std::int64_t iter = 0;
+  double fval = 0, kkt_abs = 0, kkt_rel = 0, feas = 0, eta = 0, elapsed = 0;
+};
+enum class RunStatus { Converged, MaxIter, Diverged };
+struct FinalMetrics {
+  double fval = 0, kkt_abs = 0, kkt_rel = 0, feas = 0;
+};
+struct CategoryTimers {
+  double blas3 = 0, func = 0, orth = 0;
+};
+struct RunReport {
+  std::vector<MetricSample> trace;
+  FinalMetrics final_pre_orth;
+  std::optional<FinalMetrics> final_post_orth;
+  DenseMatrix stop_iterate;
+  DenseMatrix final_x;
+  std::int64_t iterations = 0;
+  std::int64_t degenerate_steps = 0;
+  double wall_time = 0.0;
+  RunStatus status = RunStatus::MaxIter;
+  double beta = 0.0;
+};
+
+// ---- models: device-evaluated descriptors of ObjectiveModel (problems.hpp:28-111)
+class ObjectiveModel {
+ public:
+  virtual ~ObjectiveModel() = default;
+  std::int64_t n() const { return desc_.n; }
+  std::int64_t p() const { return desc_.p; }
+  double curvature_scale() const { return desc_.s; }
+  const pcal_model_desc& desc() const { return desc_; }
+
+ protected:
+  pcal_model_desc desc_{};
+};
+
+// f(X) = ½tr(XᵀAX) + tr(GᵀX); A and G are host matrices owned by the caller.
+class QuadraticModel : public ObjectiveModel {
+ public:
+  QuadraticModel(const DenseMatrix& a, std::int64_t p, double s, const DenseMatrix* g = nullptr) {
+    if (a.rows() != a.cols()) throw dimension_error("QuadraticModel: A must be square");
+    if (g && (g->rows() != a.rows() || g->cols() != p))
+      throw dimension_error("QuadraticModel: G row count must equal n");
+    desc_.kind = PCAL_MODEL_DENSE;
+    desc_.location = PCAL_HOST;
+    desc_.n = a.rows();
+    desc_.p = p;
+    desc_.s = s;
+    desc_.a = a.data();
+    desc_.g0 = g ? g->data() : nullptr;
+  }
+};
+
+// f(X) = ½tr(XᵀLX) + ½tr(XᵀVX), L = −Δ_h 7-point periodic.
+class StencilModel : public ObjectiveModel {
+ public:
+  StencilModel(std::int64_t nx, std::int64_t ny, std::int64_t nz, const std::vector<double>& v,
+               std::int64_t p, double s, int32_t kind = PCAL_MODEL_STENCIL) {
+    if (static_cast<std::int64_t>(v.size()) != nx * ny * nz)
+      throw dimension_error("StencilModel: |V| must equal nx*ny*nz");
+    desc_.kind = kind;
+    desc_.location = PCAL_HOST;
+    desc_.n = nx * ny * nz;
+    desc_.p = p;
+    desc_.s = s;
+    desc_.nx = nx;
+    desc_.ny = ny;
+    desc_.nz = nz;
+    desc_.v = v.data();
+  }
+};
+
+// E(X) = ¼tr(XᵀLX) + ½tr(XᵀV_ion X) + ¼ρᵀL†ρ + ½ρᵀε_xc(ρ).
+class KohnShamModel : public StencilModel {
+ public:
+  KohnShamModel(std::int64_t nx, std::int64_t ny, std::int64_t nz, const std::vector<double>& v_ion,
+                std::int64_t p, double s)
+      : StencilModel(nx, ny, nz, v_ion, p, s, PCAL_MODEL_KOHN_SHAM) {}
+};
+
+// ---- solve (solver.hpp:120-121) ------------------------------------------------
+inline RunReport solve(const ObjectiveModel& model, const SolverConfig& config,
+                       const DenseMatrix& x0, CategoryTimers* timers = nullptr) {
+  if (x0.rows() != model.n() || x0.cols() != model.p())
+    throw dimension_error("solve: start point shape mismatch");
+  pcal_config c;
+  pcal_config_default(&c);
+  c.beta = config.beta;
+  c.eta_kind = static_cast<int32_t>(config.eta_rule.kind);
+  c.gamma = config.eta_rule.gamma;
+  c.eta_min = config.eta_rule.eta_min;
+  c.eta_max = config.eta_rule.eta_max;
+  c.eta0 = config.eta_rule.eta0;
+  c.multiplier_rule = config.multiplier_rule == MultiplierRule::PcalFormula
+                          ? PCAL_MULT_PCAL_FORMULA
+                          : PCAL_MULT_PLAM_FORMULA;
+  c.tol_rel_kkt = config.tol_rel_kkt;
+  c.max_iter = config.max_iter;
+  c.final_orth = config.final_orth ? 1 : 0;
+  c.device = config.device;
+  if (config.max_iter < 1) throw parameter_error("SolverConfig: max_iter must be at least 1");
+  RunReport rep;
+  std::vector<double> trace(static_cast<size_t>(config.max_iter + 1) * PCAL_TRACE_COLS);
+  rep.stop_iterate = DenseMatrix(model.n(), model.p());
+  rep.final_x = DenseMatrix(model.n(), model.p());
+  pcal_report r{};
+  r.trace = trace.data();
+  r.trace_capacity = config.max_iter + 1;
+  r.stop_x = rep.stop_iterate.data();
+  r.final_x = rep.final_x.data();
+  pcal_category_timers t{};
+  check(pcal_solve(&model.desc(), &c, x0.data(), PCAL_HOST, &r, timers ? &t : nullptr));
+  if (timers) {
+    timers->blas3 += t.blas3;
+    timers->func += t.func;
+    timers->orth += t.orth;
+  }
+  rep.trace.resize(static_cast<size_t>(r.trace_len));
+  for (std::int64_t k = 0; k < r.trace_len; ++k) {
+    const double* row = trace.data() + k * PCAL_TRACE_COLS;
+    rep.trace[k] = {static_cast<std::int64_t>(row[0]), row[1], row[2], row[3], row[4], row[5],
+                    row[6]};
+  }
+  rep.final_pre_orth = {r.final_pre[0], r.final_pre[1], r.final_pre[2], r.final_pre[3]};
+  if (r.has_post)
+    rep.final_post_orth = FinalMetrics{r.final_post[0], r.final_post[1], r.final_post[2],
+                                       r.final_post[3]};
+  if (!r.has_x) {
+    rep.stop_iterate = DenseMatrix();
+    rep.final_x = DenseMatrix();
+  }
+  rep.iterations = r.iterations;
+  rep.degenerate_steps = r.degenerate_steps;
+  rep.wall_time = r.wall_time;
+  rep.status = r.status == PCAL_STATUS_CONVERGED ? RunStatus::Converged
+               : r.status == PCAL_STATUS_MAX_ITER ? RunStatus::MaxIter
+                                                  : RunStatus::Diverged;
+  rep.beta = r.beta;
+  return rep;
+}
+
+// initial_point({Qr}, n, p) with Rng(seed) (solver.cpp:136-142)
+inline DenseMatrix initial_point_qr(std::int64_t n, std::int64_t p, std::uint64_t seed,
+                                    int device = 0) {
+  DenseMatrix x(n, p);
+  check(pcal_initial_point_qr(n, p, seed, x.data(), device));
+  return x;
+}
+
+// flops_estimate(Pcal, n, p) (diagnostics.cpp:100-114)
+inline double flops_estimate(std::int64_t n, std::int64_t p) { return pcal_flops_estimate(n, p); }
+
+}  // namespace orthopt_b200
