@@ -158,6 +158,9 @@ int64_t pcal_session_kernel_launches(pcal_session* s);
  * the session stream; ms_out[4] = mean ms per iteration of {streaming step
  * (stepsize + pcal_step), gradient, Gram + p×p, X·[W|C] + reductions}. */
 int pcal_session_profile(pcal_session* s, int64_t iters, double* ms_out);
+/* Same, per kernel: an event after every launch; writes "name mean_ms\n" lines
+ * (mean ms per iteration, kernels of one name summed) into buf (cap bytes). */
+int pcal_session_profile_kernels(pcal_session* s, int64_t iters, char* buf, int64_t cap);
 /* Per-iteration launch count of the captured iteration graph. */
 int64_t pcal_session_kernels_per_iteration(pcal_session* s);
 

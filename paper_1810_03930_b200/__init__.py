@@ -130,6 +130,7 @@ def lib() -> C.CDLL:
     L.pcal_session_kernel_launches.argtypes = [vp]
     L.pcal_session_kernel_launches.restype = i64
     L.pcal_session_profile.argtypes = [vp, i64, _dp]
+    L.pcal_session_profile_kernels.argtypes = [vp, i64, C.c_char_p, i64]
     L.pcal_session_kernels_per_iteration.argtypes = [vp]
     L.pcal_session_kernels_per_iteration.restype = i64
     L.pcal_matmul_at_b.argtypes = [vp, vp, i64, i64, i64, vp, i32]
@@ -423,6 +424,16 @@ class Session:
         out = (C.c_double * 4)()
         _check(self._L.pcal_session_profile(self._h, iters, C.cast(out, _dp)))
         return {"step": out[0], "gradient": out[1], "gram": out[2], "xm": out[3]}
+
+    def profile_kernels(self, iters: int) -> dict:
+        """Mean ms per iteration of every kernel (event after each launch, no graphs)."""
+        buf = C.create_string_buffer(1 << 16)
+        _check(self._L.pcal_session_profile_kernels(self._h, iters, buf, len(buf)))
+        out = {}
+        for line in buf.value.decode().splitlines():
+            name, ms = line.split()
+            out[name] = float(ms)
+        return out
 
     @property
     def kernel_launches(self) -> int:

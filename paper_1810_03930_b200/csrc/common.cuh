@@ -24,9 +24,30 @@ struct Error : std::runtime_error {
                                   " (" + __FILE__ + ":" + std::to_string(__LINE__) + ")"); \
   } while (0)
 
-// Launch-count bookkeeping: every kernel this library launches goes through
-// count_launch() so sessions can report how many native kernels ran.
+// Launch bookkeeping: every kernel this library launches is followed by
+// launched(name), so sessions can report how many native kernels ran and the
+// per-kernel profiler (pcal_session_profile_kernels) can time each one with an
+// event recorded right after it on the same stream.
+struct KernelProfiler {
+  cudaStream_t stream = nullptr;
+  bool active = false;
+  struct Mark {
+    const char* name;
+    cudaEvent_t ev;
+  };
+  Mark marks[512];
+  int n = 0;
+};
 extern thread_local int64_t* g_launch_counter;
+extern thread_local KernelProfiler* g_kprof;
+inline void launched(const char* name, int64_t k = 1) {
+  if (g_launch_counter) *g_launch_counter += k;
+  if (g_kprof && g_kprof->active && g_kprof->n < 512) {
+    auto& m = g_kprof->marks[g_kprof->n++];
+    m.name = name;
+    cudaEventRecord(m.ev, g_kprof->stream);
+  }
+}
 inline void count_launch(int64_t k = 1) {
   if (g_launch_counter) *g_launch_counter += k;
 }
@@ -34,10 +55,13 @@ inline void count_launch(int64_t k = 1) {
 inline int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 inline int64_t ceil_div(int64_t v, int64_t m) { return (v + m - 1) / m; }
 
-// Leading dimension of every internal n×p buffer: rows padded to a multiple
-// of 16 doubles (128 B) with zeros, so GEMM tiles load aligned 16-byte chunks
-// and padded rows contribute nothing to Grams or norms.
-inline int64_t padded_ld(int64_t n) { return round_up(n, 16); }
+// Padding of every internal dimension that a GEMM contracts over: a multiple
+// of the largest k-slice (32 doubles = 256 B).  Rows/columns are zero padded,
+// so 16-byte cp.async chunks are aligned and padding contributes nothing to
+// Grams or norms.
+constexpr int64_t kPad = 32;
+inline int64_t padded_ld(int64_t n) { return round_up(n, kPad); }
+inline int64_t padded_p(int64_t p) { return round_up(p, kPad); }
 
 constexpr int kTraceCols = 7;
 

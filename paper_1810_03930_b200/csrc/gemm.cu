@@ -12,7 +12,7 @@ namespace pcal {
 // ------------------------------------------------------------------------------
 
 template <int AM>
-using CfgBig = GemmCfg<128, 128, 2, 4, 4, AM>;
+using CfgBig = GemmCfg<128, 128, 2, 4, 3, AM, 32>;  // BK = 32: 3 × 70 KB stages
 template <int AM>
 using CfgMid = GemmCfg<64, 64, 2, 2, 4, AM>;
 template <int AM>
@@ -26,9 +26,9 @@ int num_sms(int device) {
 
 CfgInfo cfg_info(int size) {
   switch (size) {
-    case CFG_BIG: return {128, 128, 64};
-    case CFG_MID: return {64, 64, 32};
-    default: return {64, 32, 32};
+    case CFG_BIG: return {128, 128, 64, CfgBig<A_MCONTIG>::BK};
+    case CFG_MID: return {64, 64, 32, CfgMid<A_MCONTIG>::BK};
+    default: return {64, 32, 32, CfgSmall<A_MCONTIG>::BK};
   }
 }
 
@@ -56,8 +56,8 @@ void plan_gemm(GemmPlan& pl, int device, int size, int amode, int epi, int64_t M
   pl.amode = amode;
   pl.epi = epi;
   const CfgInfo ci = cfg_info(size);
-  const int BK = 16;
-  if (K % BK) throw Error(PCAL_E_DIMENSION, "gemm: K must be a multiple of 16");
+  const int BK = ci.BK;
+  if (K % BK) throw Error(PCAL_E_DIMENSION, "gemm: K must be a multiple of the k-slice");
   const int64_t tm_n = ceil_div(M, ci.BM), tn_n = ceil_div(N, ci.BN);
   std::vector<int2> tiles;
   for (int64_t tn = 0; tn < tn_n; ++tn)
@@ -74,10 +74,18 @@ void plan_gemm(GemmPlan& pl, int device, int size, int amode, int epi, int64_t M
   const int64_t units = (int64_t)ntiles * ki;
   int grid = grid_override > 0 ? grid_override : num_sms(device);
   if (units < grid) grid = (int)std::max<int64_t>(1, units);
+  // Enough tiles for every SM: data-parallel whole tiles (no partials, no
+  // fixup); otherwise stream-K so tall-skinny / few-tile products fill the chip.
+  int64_t upc = 0;
+  if (ntiles >= grid) {
+    const int64_t w = ceil_div(ntiles, grid);
+    upc = w * ki;
+    grid = (int)ceil_div(ntiles, w);
+  }
   std::vector<int32_t> split(ntiles, -1);
   std::vector<FixupTask> tasks;
   int qmax = 1;
-  for (int t = 0; t < ntiles; ++t) {
+  for (int t = 0; t < ntiles && upc == 0; ++t) {
     const int32_t cf = cta_of_unit((int64_t)t * ki, units, grid);
     const int32_t cl = cta_of_unit((int64_t)(t + 1) * ki - 1, units, grid);
     if (cf != cl) {
@@ -98,8 +106,6 @@ void plan_gemm(GemmPlan& pl, int device, int size, int amode, int epi, int64_t M
     pl.ws_doubles = (size_t)pl.ntasks * qmax * ci.BM * ci.BN;
     PCAL_CUDA(cudaMalloc(&pl.ws, sizeof(double) * pl.ws_doubles));
   }
-  // heavily split plain-store tiles (Gram) spread their fixup over 8 CTAs each
-  pl.sub = (epi == EPI_STORE && qmax > 8) ? 8 : 1;
   GemmArgs& g = pl.args;
   g = GemmArgs{};
   g.M = M;
@@ -111,6 +117,7 @@ void plan_gemm(GemmPlan& pl, int device, int size, int amode, int epi, int64_t M
   g.ki = ki;
   g.units = units;
   g.grid = grid;
+  g.upc = upc;
   g.ws = pl.ws;
   g.qmax = qmax;
 }
@@ -125,18 +132,19 @@ static void launch_cfg(const GemmPlan& pl, cudaStream_t st) {
     attr_set = true;
   }
   kern<<<pl.args.grid, Cfg::THREADS + 128, Cfg::SMEM_BYTES, st>>>(pl.args);
+  launched(EPI == EPI_GRAD ? "gemm_grad" : EPI == EPI_XM ? "gemm_xm" : Cfg::AMODE == A_KCONTIG ? "gemm_gram" : "gemm_store");
   PCAL_CUDA(cudaGetLastError());
-  count_launch();
   if (pl.ntasks) {
-    if (pl.sub > 1) {
-      if constexpr (EPI == EPI_STORE) {
-        gemm_fixup<Cfg, EPI, 8><<<dim3(pl.ntasks, 8), Cfg::THREADS, 0, st>>>(pl.args, pl.d_tasks);
-      }
+    if (EPI == EPI_STORE) {
+      const int64_t total = (int64_t)pl.ntasks * Cfg::BM * Cfg::BN;
+      gemm_fixup_store<Cfg><<<(unsigned)((total + 255) / 256), 256, 0, st>>>(pl.args, pl.d_tasks,
+                                                                            pl.ntasks);
+      launched(Cfg::AMODE == A_KCONTIG ? "fixup_gram" : "fixup_store");
     } else {
-      gemm_fixup<Cfg, EPI, 1><<<dim3(pl.ntasks, 1), Cfg::THREADS, 0, st>>>(pl.args, pl.d_tasks);
+      gemm_fixup<Cfg, EPI><<<pl.ntasks, Cfg::THREADS, 0, st>>>(pl.args, pl.d_tasks);
+      launched(EPI == EPI_GRAD ? "fixup_grad" : "fixup_xm");
     }
     PCAL_CUDA(cudaGetLastError());
-    count_launch();
   }
 }
 

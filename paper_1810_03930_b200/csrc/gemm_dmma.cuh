@@ -41,9 +41,9 @@ __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, dou
                : "d"(a), "d"(b));
 }
 
-template <int BM_, int BN_, int WARPS_M_, int WARPS_N_, int STAGES_, int AMODE_>
+template <int BM_, int BN_, int WARPS_M_, int WARPS_N_, int STAGES_, int AMODE_, int BK_ = 16>
 struct GemmCfg {
-  static constexpr int BM = BM_, BN = BN_, BK = 16;
+  static constexpr int BM = BM_, BN = BN_, BK = BK_;
   static constexpr int WARPS_M = WARPS_M_, WARPS_N = WARPS_N_;
   static constexpr int WARPS = WARPS_M * WARPS_N, THREADS = WARPS * 32;
   static constexpr int STAGES = STAGES_;
@@ -184,7 +184,7 @@ __device__ __forceinline__ void epilogue(const GemmArgs& g, int tm, int tn, int 
         fs += __shfl_xor_sync(0xffffffffu, fs, 4);
         fs += __shfl_xor_sync(0xffffffffu, fs, 8);
         fs += __shfl_xor_sync(0xffffffffu, fs, 16);
-        if (r == 0 && col < e.p) e.fpart[rb * e.p + col] = fs;
+        if (r == 0 && col < e.p) e.fpart[col * e.pstride + rb] = fs;
       }
     if (__any_sync(0xffffffffu, bad) && lane == 0) *e.bad = 1;
   } else {  // EPI_XM
@@ -211,8 +211,8 @@ __device__ __forceinline__ void epilogue(const GemmArgs& g, int tm, int tn, int 
         ds += __shfl_xor_sync(0xffffffffu, ds, o);
       }
       if (r == 0 && j < e.p) {
-        e.kpart[rb * e.p + j] = ks;
-        e.dpart[rb * e.p + j] = ds;
+        e.kpart[j * e.pstride + rb] = ks;
+        e.dpart[j * e.pstride + rb] = ds;
       }
     }
   }
@@ -257,19 +257,22 @@ __device__ __forceinline__ void produce(const GemmArgs& g, double* As, double* B
                                         int lane) {
   constexpr int BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK, S = Cfg::STAGES;
   // A_MCONTIG: lane owns m-chunks {2·lane + 64·h}; A_KCONTIG / B: lane owns
-  // rows {lane/8 + 4·j} at k-chunk lane%8.  One base pointer per operand is
-  // advanced by one k-slice per unit (the producer runs on 40 registers).
-  constexpr int AH = Cfg::AMODE == A_MCONTIG ? BM / 64 : BM / 4;
-  constexpr int BJ = BN / 4;
+  // rows {lane/CPR + RPP·j} at k-chunk lane%CPR (CPR = BK/2 chunks per row).
+  // One base pointer per operand advances one k-slice per unit (the producer
+  // runs on 40 registers).
+  constexpr int CPR = BK / 2, RPP = 32 / CPR;
+  constexpr int AH = Cfg::AMODE == A_MCONTIG ? BM / 64 : BM / RPP;
+  constexpr int BJ = BN / RPP;
   static_assert(Cfg::AMODE != A_MCONTIG || BM % 64 == 0, "MCONTIG producer needs BM % 64 == 0");
-  static_assert(BK == 16 && AH <= 32 && BJ <= 32, "producer layout");
+  static_assert((BK == 16 || BK == 32) && AH <= 64 && BJ <= 64, "producer layout");
   const double* pa = g.A;
   const double* pb = g.B;
-  unsigned amask = 0, bmask = 0;
+  uint64_t amask = 0, bmask = 0;
   int cur_tile = -1;
   const int64_t a_step = Cfg::AMODE == A_MCONTIG ? (int64_t)BK * g.lda : BK;
-  const int64_t a_rows = Cfg::AMODE == A_MCONTIG ? 64 : 4 * g.lda;  // stride between lane chunks
-  const int64_t b_rows = 4 * g.ldb;
+  const int64_t a_rows = Cfg::AMODE == A_MCONTIG ? 64 : RPP * g.lda;  // stride between lane chunks
+  const int64_t b_rows = RPP * g.ldb;
+  const int lr = lane / CPR, lc = 2 * (lane % CPR);
   for (int64_t u = u0; u < u1; ++u) {
     const int64_t i = u - u0;
     const int s = (int)(i % S);
@@ -286,17 +289,17 @@ __device__ __forceinline__ void produce(const GemmArgs& g, double* As, double* B
         pa = g.A + (m0 + 2 * lane) + k0 * g.lda;
 #pragma unroll
         for (int h = 0; h < AH; ++h)
-          if (m0 + 2 * lane + 64 * h < g.M) amask |= 1u << h;
+          if (m0 + 2 * lane + 64 * h < g.M) amask |= 1ull << h;
       } else {
-        pa = g.A + (k0 + 2 * (lane & 7)) + (m0 + (lane >> 3)) * g.lda;
+        pa = g.A + (k0 + lc) + (m0 + lr) * g.lda;
 #pragma unroll
         for (int h = 0; h < AH; ++h)
-          if (m0 + (lane >> 3) + 4 * h < g.M) amask |= 1u << h;
+          if (m0 + lr + RPP * h < g.M) amask |= 1ull << h;
       }
-      pb = g.B + (k0 + 2 * (lane & 7)) + (n0 + (lane >> 3)) * g.ldb;
+      pb = g.B + (k0 + lc) + (n0 + lr) * g.ldb;
 #pragma unroll
       for (int j = 0; j < BJ; ++j)
-        if (n0 + (lane >> 3) + 4 * j < g.N) bmask |= 1u << j;
+        if (n0 + lr + RPP * j < g.N) bmask |= 1ull << j;
     }
     mbar_wait(&empty[s], ph ^ 1u);
     double* as = As + s * Cfg::A_STAGE;
@@ -304,7 +307,7 @@ __device__ __forceinline__ void produce(const GemmArgs& g, double* As, double* B
     if constexpr (Cfg::AMODE == A_MCONTIG) {
 #pragma unroll
       for (int h = 0; h < AH; ++h) {
-        const bool ok = (amask >> h) & 1u;
+        const bool ok = (amask >> h) & 1ull;
 #pragma unroll
         for (int kr = 0; kr < BK; ++kr)
           cp_async16(as + kr * Cfg::SA_M + 2 * lane + 64 * h, ok ? pa + h * a_rows + kr * g.lda : g.A,
@@ -313,16 +316,14 @@ __device__ __forceinline__ void produce(const GemmArgs& g, double* As, double* B
     } else {
 #pragma unroll
       for (int h = 0; h < AH; ++h) {
-        const bool ok = (amask >> h) & 1u;
-        cp_async16(as + ((lane >> 3) + 4 * h) * Cfg::SA_K + 2 * (lane & 7),
-                   ok ? pa + h * a_rows : g.A, ok);
+        const bool ok = (amask >> h) & 1ull;
+        cp_async16(as + (lr + RPP * h) * Cfg::SA_K + lc, ok ? pa + h * a_rows : g.A, ok);
       }
     }
 #pragma unroll
     for (int j = 0; j < BJ; ++j) {
-      const bool ok = (bmask >> j) & 1u;
-      cp_async16(bs + ((lane >> 3) + 4 * j) * Cfg::SB_K + 2 * (lane & 7), ok ? pb + j * b_rows : g.B,
-                 ok);
+      const bool ok = (bmask >> j) & 1ull;
+      cp_async16(bs + (lr + RPP * j) * Cfg::SB_K + lc, ok ? pb + j * b_rows : g.B, ok);
     }
     cp_async_mbar_arrive(&full[s]);
     pa += a_step;
@@ -344,8 +345,8 @@ __global__ void __launch_bounds__(Cfg::THREADS + 128, 1) gemm_streamk(GemmArgs g
   uint64_t* empty = full + Cfg::STAGES;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int32_t cta = blockIdx.x;
-  const int64_t u0 = cta_unit_begin(cta, g.units, g.grid);
-  const int64_t u1 = cta_unit_begin(cta + 1, g.units, g.grid);
+  const int64_t u0 = cta_unit_begin(cta, g.units, g.grid, g.upc);
+  const int64_t u1 = cta_unit_begin(cta + 1, g.units, g.grid, g.upc);
   if (u0 >= u1) return;
   if (threadIdx.x == 0) {
     for (int s = 0; s < Cfg::STAGES; ++s) {
@@ -410,54 +411,64 @@ __global__ void __launch_bounds__(Cfg::THREADS + 128, 1) gemm_streamk(GemmArgs g
   }
 }
 
-// Sums the partials of split tiles in CTA order and applies the epilogue.
-// grid = (#split tiles, SUB): for EPI_STORE the fragment is additionally
-// divided into SUB slices across CTAs (heavily split Gram tiles).
-template <class Cfg, int EPI, int SUB>
+// Sums the partials of split tiles in CTA order (q = 0, 1, …) and applies the
+// epilogue with the consumer-warp geometry of the main kernel.  q-outer loop:
+// every partial contributes FRAG independent coalesced loads per thread.
+template <class Cfg, int EPI>
 __global__ void __launch_bounds__(Cfg::THREADS) gemm_fixup(GemmArgs g, const FixupTask* tasks) {
   if (g.ctl && g.ctl->done) return;
   const FixupTask tk = tasks[blockIdx.x];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wm = warp / Cfg::WARPS_N, wn = warp % Cfg::WARPS_N;
   double acc[Cfg::MT][Cfg::NT][2];
-  const double* base = g.ws + (size_t)tk.slot * g.qmax * (size_t)(Cfg::BM * Cfg::BN);
-  constexpr int PER = (Cfg::MT + SUB - 1) / SUB;
-  const int mt_lo = (SUB == 1) ? 0 : blockIdx.y * PER;
 #pragma unroll
   for (int mt = 0; mt < Cfg::MT; ++mt)
 #pragma unroll
-    for (int nt = 0; nt < Cfg::NT; ++nt)
+    for (int nt = 0; nt < Cfg::NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+  const double* base = g.ws + (size_t)tk.slot * g.qmax * (size_t)(Cfg::BM * Cfg::BN);
+  for (int q = 0; q < tk.nq; ++q) {
+    const double* w = base + (size_t)q * (Cfg::BM * Cfg::BN);
 #pragma unroll
-      for (int x = 0; x < 2; ++x) {
-        double s = 0.0;
-        if (SUB == 1 || (mt >= mt_lo && mt < mt_lo + PER)) {
-          for (int q = 0; q < tk.nq; ++q)
-            s += base[(size_t)q * (Cfg::BM * Cfg::BN) + frag_index<Cfg>(warp, mt, nt, x, lane)];
-        }
-        acc[mt][nt][x] = s;
-      }
-  const int2 tc = g.tiles[tk.tile];
-  if constexpr (SUB == 1) {
-    epilogue<Cfg, EPI>(g, tc.x, tc.y, wm, wn, lane, acc);
-  } else {
-    static_assert(EPI == EPI_STORE, "sliced fixup only for plain stores");
-    const EpiParams& e = g.ep;
-    const int r = lane >> 2, qq = lane & 3;
-    const int64_t mw0 = (int64_t)tc.x * Cfg::BM + wm * Cfg::WM;
-    const int64_t nw0 = (int64_t)tc.y * Cfg::BN + wn * Cfg::WN;
-#pragma unroll
-    for (int mt = 0; mt < Cfg::MT; ++mt) {
-      if (mt < mt_lo || mt >= mt_lo + PER) continue;
-      const int64_t row = mw0 + mt * 8 + r;
+    for (int mt = 0; mt < Cfg::MT; ++mt)
 #pragma unroll
       for (int nt = 0; nt < Cfg::NT; ++nt)
 #pragma unroll
-        for (int x = 0; x < 2; ++x) {
-          const int64_t col = nw0 + nt * 8 + 2 * qq + x;
-          if (row < e.m_store && col < e.n_store) e.C[row + col * e.ldc] = acc[mt][nt][x];
-        }
-    }
+        for (int x = 0; x < 2; ++x) acc[mt][nt][x] += w[frag_index<Cfg>(warp, mt, nt, x, lane)];
   }
+  const int2 tc = g.tiles[tk.tile];
+  epilogue<Cfg, EPI>(g, tc.x, tc.y, wm, wn, lane, acc);
+}
+
+// Plain-store fixup spread over the whole chip: one thread per output element
+// of every split tile (heavily split tall-skinny Grams have ~70 partials per tile).
+template <class Cfg>
+__global__ void __launch_bounds__(256) gemm_fixup_store(GemmArgs g, const FixupTask* tasks,
+                                                        int ntasks) {
+  if (g.ctl && g.ctl->done) return;
+  constexpr int TILE = Cfg::BM * Cfg::BN;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)ntasks * TILE) return;
+  const int task = (int)(e / TILE);
+  const int f = (int)(e % TILE);
+  const FixupTask tk = tasks[task];
+  const double* base = g.ws + (size_t)tk.slot * g.qmax * (size_t)TILE + f;
+  double s = 0.0;
+  for (int q = 0; q < tk.nq; ++q) s += base[(size_t)q * TILE];
+  // decode the fragment-native index (frag_index)
+  const int lane = f & 31;
+  int r = f >> 5;
+  const int x = r & 1;
+  r >>= 1;
+  const int nt = r % Cfg::NT;
+  r /= Cfg::NT;
+  const int mt = r % Cfg::MT;
+  const int warp = r / Cfg::MT;
+  const int wm = warp / Cfg::WARPS_N, wn = warp % Cfg::WARPS_N;
+  const int2 tc = g.tiles[tk.tile];
+  const int64_t row = (int64_t)tc.x * Cfg::BM + wm * Cfg::WM + mt * 8 + (lane >> 2);
+  const int64_t col = (int64_t)tc.y * Cfg::BN + wn * Cfg::WN + nt * 8 + 2 * (lane & 3) + x;
+  const EpiParams& ep = g.ep;
+  if (row < ep.m_store && col < ep.n_store) ep.C[row + col * ep.ldc] = s;
 }
 
 }  // namespace pcal

@@ -26,6 +26,7 @@ struct EpiParams {
   int32_t* bad;      // set to 1 if a non-finite value is produced (GRAD)
   double beta;
   int64_t n, p;
+  int64_t pstride;   // column stride of the partial arrays: part[col·pstride + rb]
 };
 
 struct GemmArgs {
@@ -41,6 +42,7 @@ struct GemmArgs {
   int32_t ki;         // k-iterations per tile
   int64_t units;      // ntiles · ki
   int32_t grid;
+  int64_t upc;        // > 0: data-parallel (whole tiles per CTA), 0: stream-K
   double* ws;         // [slot][q][BM·BN] partials, fragment-native layout
   int32_t qmax;
   EpiParams ep;
@@ -58,7 +60,9 @@ __host__ __device__ inline int32_t cta_of_unit(int64_t x, int64_t U, int32_t G) 
   int64_t c = ((x + 1) * (int64_t)G + U - 1) / U - 1;
   return (int32_t)(c < 0 ? 0 : (c >= G ? G - 1 : c));
 }
-__host__ __device__ inline int64_t cta_unit_begin(int32_t c, int64_t U, int32_t G) {
+// upc > 0: data-parallel schedule, each CTA owns upc consecutive units (whole tiles)
+__host__ __device__ inline int64_t cta_unit_begin(int32_t c, int64_t U, int32_t G, int64_t upc) {
+  if (upc > 0) return (int64_t)c * upc < U ? (int64_t)c * upc : U;
   return (int64_t)c * U / G;
 }
 
@@ -67,7 +71,7 @@ __host__ __device__ inline int64_t cta_unit_begin(int32_t c, int64_t U, int32_t 
 enum CfgSize { CFG_BIG = 0, CFG_MID = 1, CFG_SMALL = 2 };
 
 struct CfgInfo {
-  int BM, BN, WM;
+  int BM, BN, WM, BK;
 };
 CfgInfo cfg_info(int size);
 int pick_size(int64_t N);
@@ -80,7 +84,6 @@ struct GemmPlan {
   int32_t* d_split = nullptr;
   FixupTask* d_tasks = nullptr;
   int ntasks = 0;
-  int sub = 1;
   double* ws = nullptr;
   size_t ws_doubles = 0;
   GemmPlan() = default;

@@ -17,14 +17,14 @@ constexpr int kStreamThreadsOps = 256;
 
 // G = L X + V∘X with L = −Δ_h (7-point, periodic, h = 1) and, for the
 // Kohn–Sham model, G = ½ L X + u∘X (scale_l = 0.5, u = V + L†ρ − c ρ^{1/3}).
-// fpart[chunk·p + j] = Σ_{rows of chunk} X∘(LX) (the Laplacian quadratic form).
+// fpart[j·pstride + chunk] = Σ_{rows of chunk} X∘G (X∘LX for the KS model).
 // Grid: (n / chunk, p); one thread per row element, x-fastest for coalescing.
 template <bool KS>
 __global__ void __launch_bounds__(kStencilThreads)
     k_stencil_grad(const double* __restrict__ x, const double* __restrict__ u,
                    double* __restrict__ g, int64_t nx, int64_t ny, int64_t nz, int64_t ld,
-                   int64_t p, int64_t chunk, double* __restrict__ fpart, int32_t* bad,
-                   const Ctl* ctl) {
+                   int64_t p, int64_t chunk, double* __restrict__ fpart, int64_t pstride,
+                   int32_t* bad, const Ctl* ctl) {
   if (ctl && ctl->done) return;
   __shared__ double sm[kStencilThreads / 32];
   const int64_t n = nx * ny * nz;
@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(kStencilThreads)
     nonfinite |= !isfinite(gv);
   }
   const double s = block_sum<kStencilThreads>(acc, sm);
-  if (threadIdx.x == 0) fpart[blockIdx.x * p + j] = s;
+  if (threadIdx.x == 0) fpart[j * pstride + blockIdx.x] = s;
   if (__syncthreads_or(nonfinite) && threadIdx.x == 0) *bad = 1;
 }
 

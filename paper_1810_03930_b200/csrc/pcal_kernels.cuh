@@ -9,18 +9,26 @@ namespace pcal {
 
 constexpr int kStreamThreads = 256;
 
-// out[c·ncols + col] = Σ_{r in chunk c} in[r·ncols + col]   (in: nrows × ncols row-major)
-__global__ void k_sum_rows(const double* __restrict__ in, int64_t nrows, int64_t ncols,
-                           int64_t rows_per_chunk, double* __restrict__ out, const Ctl* ctl) {
+// Column sums of the row-block partial arrays (part[col·stride + rb]), one
+// block per (column, array), fixed-order block reduction:
+//   out_a[col] = Σ_{rb < nrows_a} part_a[col·stride_a + rb].
+struct ColSumArgs {
+  const double* in[3];
+  int64_t nrows[3];
+  int64_t stride[3];
+  double* out[3];
+};
+__global__ void __launch_bounds__(kStreamThreads) k_colsum3(ColSumArgs a, const Ctl* ctl) {
   if (ctl && ctl->done) return;
-  const int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t c = blockIdx.y;
-  if (col >= ncols) return;
-  const int64_t r0 = c * rows_per_chunk;
-  const int64_t r1 = min(nrows, r0 + rows_per_chunk);
-  double s = 0.0;
-  for (int64_t r = r0; r < r1; ++r) s += in[r * ncols + col];
-  out[c * ncols + col] = s;
+  __shared__ double sm[kStreamThreads / 32];
+  const int which = blockIdx.y;
+  if (!a.in[which]) return;
+  const int64_t col = blockIdx.x;
+  const double* src = a.in[which] + col * a.stride[which];
+  double acc = 0.0;
+  for (int64_t r = threadIdx.x; r < a.nrows[which]; r += blockDim.x) acc += src[r];
+  const double s = block_sum<kStreamThreads>(acc, sm);
+  if (threadIdx.x == 0) a.out[which][col] = s;
 }
 
 // W = Ψ(GᵀX) = ½(M1 + M1ᵀ), C = XᵀX − I (exactly symmetric, from the computed
@@ -102,25 +110,35 @@ __device__ __forceinline__ double clamp_eta(const Ctl* c, double v) {
   return r < c->eta_max ? r : c->eta_max;
 }
 
-// stepsize_select (solver.cpp:212-251) on the device; one thread.
-__global__ void k_eta(Ctl* ctl, const double* __restrict__ part, int nblocks) {
+// stepsize_select (solver.cpp:212-251) on the device: one block reduces the
+// k_bb_partials slots in a fixed order, thread 0 applies the rule.
+__global__ void __launch_bounds__(kStreamThreads) k_eta(Ctl* ctl, const double* __restrict__ part,
+                                                         int nblocks) {
   if (ctl->done) return;
-  if (threadIdx.x != 0) return;
+  __shared__ double sm[kStreamThreads / 32];
   Ctl* c = ctl;
+  const bool need = c->eta_kind != 0 && c->have_prev && c->iter != 0;
+  double ss = 0.0, sy = 0.0, yy = 0.0;
+  if (need) {
+    double a = 0.0, b = 0.0, d = 0.0;
+    for (int i = threadIdx.x; i < nblocks; i += blockDim.x) {
+      a += part[3 * i + 0];
+      b += part[3 * i + 1];
+      d += part[3 * i + 2];
+    }
+    ss = block_sum<kStreamThreads>(a, sm);
+    sy = block_sum<kStreamThreads>(b, sm);
+    yy = block_sum<kStreamThreads>(d, sm);
+  }
+  if (threadIdx.x != 0) return;
   double eta;
   if (c->eta_kind == 0) {
     eta = clamp_eta(c, c->gamma);
   } else {
     const double fallback = c->eta_prev > 0.0 ? c->eta_prev : c->eta0;
-    if (!c->have_prev || c->iter == 0) {
+    if (!need) {
       eta = clamp_eta(c, c->eta0 > 0.0 ? c->eta0 : fallback);
     } else {
-      double ss = 0.0, sy = 0.0, yy = 0.0;
-      for (int b = 0; b < nblocks; ++b) {
-        ss += part[3 * b + 0];
-        sy += part[3 * b + 1];
-        yy += part[3 * b + 2];
-      }
       const double bb1 = (ss == 0.0 || sy == 0.0) ? fallback : fabs(sy) / ss;
       const double bb2 = (sy == 0.0) ? fallback : yy / fabs(sy);
       double v = fallback;

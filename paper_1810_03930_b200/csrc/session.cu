@@ -7,7 +7,7 @@
 // `done` flag asynchronously, so the iteration never waits on the host.
 //
 // Memory layout (HBM): every n×p matrix is column-major with leading dimension
-// ld = round_up(n,16) and pp = round_up(p,16) columns, zero padded.  The
+// ld = round_up(n,32) and pp = round_up(p,32) columns, zero padded.  The
 // iterate X_k and the PCAL gradient buffer P_k (∇f(X_k), then overwritten in
 // place by g_plam = ∇f − XW + βXC) are stored side by side as a pair
 // [P_k | X_k] so the Gram GEMM reads [P|X]ᵀX as ONE operand; two pairs
@@ -34,6 +34,7 @@
 namespace pcal {
 
 thread_local int64_t* g_launch_counter = nullptr;
+thread_local KernelProfiler* g_kprof = nullptr;
 thread_local std::string g_last_error;
 
 // ------------------------------------------------------------------------------
@@ -154,29 +155,39 @@ struct FinishArgs {
   double c_xc;          // (3/π)^{1/3}
 };
 
-__global__ void k_finish_eval(FinishArgs a, Ctl* ctl, double* post /* 4 */) {
+__global__ void __launch_bounds__(256) k_finish_eval(FinishArgs a, Ctl* ctl,
+                                                     double* post /* 5 */) {
   if (a.mode != 2 && ctl->done) return;
-  if (threadIdx.x != 0) return;
-  double f1 = 0.0, k2 = 0.0, c2 = 0.0;
-  for (int64_t j = 0; j < a.p; ++j) {
-    f1 += a.fcol[j];
-    k2 += a.kcol[j];
+  __shared__ double sm[8];
+  double pf = 0.0, pk = 0.0, pc = 0.0, pv = 0.0, pr = 0.0, pe = 0.0;
+  for (int64_t j = threadIdx.x; j < a.p; j += blockDim.x) {
+    pf += a.fcol[j];
+    pk += a.kcol[j];
   }
-  for (int i = 0; i < a.ncp; ++i) c2 += a.cpart[i];
+  for (int i = threadIdx.x; i < a.ncp; i += blockDim.x) pc += a.cpart[i];
+  if (a.model == PCAL_MODEL_KOHN_SHAM)
+    for (int i = threadIdx.x; i < a.nsp; i += blockDim.x) {
+      pv += a.spart[3 * i];
+      pr += a.spart[3 * i + 1];
+      pe += a.spart[3 * i + 2];
+    }
+  const double f1 = block_sum<256>(pf, sm);
+  const double k2 = block_sum<256>(pk, sm);
+  const double c2 = block_sum<256>(pc, sm);
+  const double vr = block_sum<256>(pv, sm);
+  const double rh = block_sum<256>(pr, sm);
+  const double ex = block_sum<256>(pe, sm);
+  if (threadIdx.x != 0) return;
+  const bool bad_flag = *a.bad != 0;
+  *a.bad = 0;  // reset for the next evaluation
   double f;
   if (a.model == PCAL_MODEL_KOHN_SHAM) {
-    double vr = 0.0, rh = 0.0, ex = 0.0;
-    for (int i = 0; i < a.nsp; ++i) {
-      vr += a.spart[3 * i];
-      rh += a.spart[3 * i + 1];
-      ex += a.spart[3 * i + 2];
-    }
     f = 0.25 * f1 + 0.5 * vr + 0.25 * rh - 0.375 * a.c_xc * ex;
   } else {
     f = 0.5 * f1;
   }
   const double kkt = sqrt(k2), feas = sqrt(c2);
-  const bool bad = *a.bad || !isfinite(f);
+  const bool bad = bad_flag || !isfinite(f);
   if (a.mode == 2) {  // post-orth metrics (solver.cpp:452-455)
     post[0] = f;
     post[1] = kkt;
@@ -263,7 +274,7 @@ struct pcal_session {
   int64_t ldA = 0;
   // iteration state
   pcal::DevBuf pair[2], dvec[2];
-  pcal::DevBuf gr, mcat, fpart, kpart, dpart, lvl1, fcol, kcol, cpart, bbpart, npart, post;
+  pcal::DevBuf gr, mcat, fpart, kpart, dpart, fcol, kcol, cpart, bbpart, npart, post;
   pcal::DevBuf orth_b, orth_l, orth_t, orth_f2;
   int32_t* bad = nullptr;
   int32_t* orth_status = nullptr;
@@ -274,6 +285,7 @@ struct pcal_session {
   // plans
   pcal::GemmPlan grad[2], gram[2], xm[2], orth_gram, orth_mul;
   int64_t nrb_grad = 0, nrb_xm = 0, nrb_f = 0;  // row-blocks of f/k/d partials
+  int64_t pstride_f = 0, pstride_xm = 0;        // column strides of the partial arrays
   int64_t up_chunk = 0, up_nchunks = 0;
   int bb_blocks = 0, cp_blocks = 0, sp_blocks = 0;
   int64_t st_chunk = 0, st_nchunks = 0;
@@ -308,26 +320,26 @@ struct LaunchScope {
   ~LaunchScope() { g_launch_counter = prev; }
 };
 
-// Column sums of the three partial arrays (f, kkt², d) in a fixed two-level order.
+// Column sums of the three partial arrays (f, kkt², d), one launch.
 static void launch_colsums(pcal_session* s, const double* fp, int64_t nrb_f, const double* kp,
                            const double* dp, int64_t nrb_kd, double* fcol, double* kcol,
                            double* dcol, const Ctl* ctl) {
-  const int64_t p = s->p;
-  const int64_t NCH = 32;
-  auto two_level = [&](const double* in, int64_t nrows, double* out, double* lvl) {
-    const int64_t rpc = ceil_div(nrows, NCH);
-    const int64_t nch = ceil_div(nrows, rpc);
-    dim3 g1((unsigned)ceil_div(p, 128), (unsigned)nch);
-    k_sum_rows<<<g1, 128, 0, s->stream>>>(in, nrows, p, rpc, lvl, ctl);
-    dim3 g2((unsigned)ceil_div(p, 128), 1);
-    k_sum_rows<<<g2, 128, 0, s->stream>>>(lvl, nch, p, nch, out, ctl);
-    count_launch(2);
-  };
-  if (fp) two_level(fp, nrb_f, fcol, s->lvl1.p);
-  if (kp) two_level(kp, nrb_kd, kcol, s->lvl1.p + NCH * p);
+  ColSumArgs a{};
+  a.in[0] = fp;
+  a.nrows[0] = nrb_f;
+  a.stride[0] = s->pstride_f;
+  a.out[0] = fcol;
+  a.in[1] = kp;
+  a.nrows[1] = nrb_kd;
+  a.stride[1] = s->pstride_xm;
+  a.out[1] = kcol;
   // PlamFormula: no diagonal correction, d stays 0 (solver.cpp:406-408)
-  if (dp && s->cfg.multiplier_rule == PCAL_MULT_PCAL_FORMULA)
-    two_level(dp, nrb_kd, dcol, s->lvl1.p + 2 * NCH * p);
+  a.in[2] = (dp && s->cfg.multiplier_rule == PCAL_MULT_PCAL_FORMULA) ? dp : nullptr;
+  a.nrows[2] = nrb_kd;
+  a.stride[2] = s->pstride_xm;
+  a.out[2] = dcol;
+  k_colsum3<<<dim3((unsigned)s->p, 3), kStreamThreads, 0, s->stream>>>(a, ctl);
+  launched("k_colsum3");
 }
 
 // Gradient of the model at X (pair b): G into P(b), f partials into fpart.
@@ -341,8 +353,8 @@ static void launch_gradient(pcal_session* s, int b, const Ctl* ctl) {
       dim3 g((unsigned)s->st_nchunks, (unsigned)p);
       k_stencil_grad<false><<<g, kStencilThreads, 0, s->stream>>>(
           Xof(s, b), s->V.p, Pof(s, b), s->model.nx, s->model.ny, s->model.nz, s->ld, p,
-          s->st_chunk, s->fpart.p, s->bad, ctl);
-      count_launch();
+          s->st_chunk, s->fpart.p, s->pstride_f, s->bad, ctl);
+      launched("k_stencil_grad");
       break;
     }
     case PCAL_MODEL_KOHN_SHAM: {
@@ -350,27 +362,36 @@ static void launch_gradient(pcal_session* s, int b, const Ctl* ctl) {
       const unsigned nb = (unsigned)ceil_div(n, 256);
       const auto& m = s->model;
       k_row_sq_norms<<<nb, 256, 0, s->stream>>>(Xof(s, b), n, s->ld, p, s->rho.p, ctl);
+      launched("k_row_sq_norms");
       k_axis_transform<<<nb, 256, 0, s->stream>>>(s->rho.p, s->tmpa.p, s->qx.p, m.nx, m.nx, m.ny,
                                                   m.nz, 0, 1, ctl);
+      launched("k_axis_transform");
       k_axis_transform<<<nb, 256, 0, s->stream>>>(s->tmpa.p, s->tmpb.p, s->qy.p, m.ny, m.nx, m.ny,
                                                   m.nz, 1, 1, ctl);
+      launched("k_axis_transform");
       k_axis_transform<<<nb, 256, 0, s->stream>>>(s->tmpb.p, s->tmpa.p, s->qz.p, m.nz, m.nx, m.ny,
                                                   m.nz, 2, 1, ctl);
+      launched("k_axis_transform");
       k_spectral_divide<<<nb, 256, 0, s->stream>>>(s->tmpa.p, s->lx.p, s->ly.p, s->lz.p, m.nx,
                                                    m.ny, m.nz, ctl);
+      launched("k_spectral_divide");
       k_axis_transform<<<nb, 256, 0, s->stream>>>(s->tmpa.p, s->tmpb.p, s->qz.p, m.nz, m.nx, m.ny,
                                                   m.nz, 2, 0, ctl);
+      launched("k_axis_transform");
       k_axis_transform<<<nb, 256, 0, s->stream>>>(s->tmpb.p, s->tmpa.p, s->qy.p, m.ny, m.nx, m.ny,
                                                   m.nz, 1, 0, ctl);
+      launched("k_axis_transform");
       k_axis_transform<<<nb, 256, 0, s->stream>>>(s->tmpa.p, s->h.p, s->qx.p, m.nx, m.nx, m.ny,
                                                   m.nz, 0, 0, ctl);
+      launched("k_axis_transform");
       k_ks_potential<<<s->sp_blocks, 256, 0, s->stream>>>(s->V.p, s->rho.p, s->h.p, s->u.p, n,
                                                           s->c_xc, s->spart.p, ctl);
+      launched("k_ks_potential");
       dim3 g((unsigned)s->st_nchunks, (unsigned)p);
       k_stencil_grad<true><<<g, kStencilThreads, 0, s->stream>>>(
           Xof(s, b), s->u.p, Pof(s, b), m.nx, m.ny, m.nz, s->ld, p, s->st_chunk, s->fpart.p,
-          s->bad, ctl);
-      count_launch(10);
+          s->pstride_f, s->bad, ctl);
+      launched("k_stencil_grad");
       break;
     }
     default:
@@ -382,15 +403,13 @@ static void launch_gradient(pcal_session* s, int b, const Ctl* ctl) {
 // G, [GᵀX; XᵀX], W, C, g_plam = G − XW + βXC (into P), d, kkt, feas, f.
 static void launch_eval(pcal_session* s, int b, int mode, const Ctl* ctl_guard) {
   cudaStream_t st = s->stream;
-  k_zero_i32<<<1, 1, 0, st>>>(s->bad, ctl_guard);
-  count_launch();
   mark(s, 1);
   launch_gradient(s, b, ctl_guard);
   mark(s, 2);
   launch_gemm(s->gram[b], st);
   k_small_pxp<<<s->cp_blocks, kStreamThreads, 0, st>>>(s->gr.p, s->pp, s->p, s->mcat.p, s->pp,
                                                        s->cpart.p, ctl_guard);
-  count_launch();
+  launched("k_small_pxp");
   mark(s, 3);
   launch_gemm(s->xm[b], st);
   launch_colsums(s, s->fpart.p, s->nrb_f, s->kpart.p, s->dpart.p, s->nrb_xm, s->fcol.p,
@@ -408,8 +427,8 @@ static void launch_eval(pcal_session* s, int b, int mode, const Ctl* ctl_guard) 
   fa.trace = s->trace.p;
   fa.bad = s->bad;
   fa.c_xc = s->c_xc;
-  k_finish_eval<<<1, 32, 0, st>>>(fa, s->ctl, s->post.p);
-  count_launch();
+  k_finish_eval<<<1, 256, 0, st>>>(fa, s->ctl, s->post.p);
+  launched("k_finish_eval");
   mark(s, 4);
   if (s->pev_on) {
     PCAL_CUDA(cudaEventSynchronize(s->pev[4]));
@@ -435,13 +454,16 @@ static void launch_iteration(pcal_session* s, int b) {
   k_bb_partials<<<s->bb_blocks, kStreamThreads, 0, st>>>(Xof(s, b), Pof(s, b), Xof(s, nb),
                                                          Pof(s, nb), s->dvec[b].p, s->dvec[nb].p,
                                                          s->ld, s->p, s->bbpart.p, s->ctl);
-  k_eta<<<1, 32, 0, st>>>(s->ctl, s->bbpart.p, s->bb_blocks);
+  launched("k_bb_partials");
+  k_eta<<<1, kStreamThreads, 0, st>>>(s->ctl, s->bbpart.p, s->bb_blocks);
+  launched("k_eta");
   dim3 gu((unsigned)s->up_nchunks, (unsigned)s->p);
   k_update<<<gu, kStreamThreads, 0, st>>>(Xof(s, b), Pof(s, b), s->dvec[b].p, Xof(s, nb), s->n,
                                           s->ld, s->p, s->up_chunk, s->npart.p, s->ctl);
+  launched("k_update");
   k_normalize<<<gu, kStreamThreads, 0, st>>>(Xof(s, b), Xof(s, nb), s->n, s->ld, s->p,
                                              s->up_chunk, s->up_nchunks, s->npart.p, s->ctl);
-  count_launch(4);
+  launched("k_normalize");
   PCAL_CUDA(cudaGetLastError());
   mark(s, 5);
   launch_eval(s, nb, 0, s->ctl);
@@ -473,6 +495,7 @@ static void build_plans(pcal_session* s) {
       e.g0 = s->g0.p;
       e.ld = ld;
       e.fpart = s->fpart.p;
+      e.pstride = s->pstride_f;
       e.bad = s->bad;
       e.n = n;
       e.p = s->p;
@@ -506,6 +529,7 @@ static void build_plans(pcal_session* s) {
       e.ld = ld;
       e.kpart = s->kpart.p;
       e.dpart = s->dpart.p;
+      e.pstride = s->pstride_xm;
       e.beta = s->beta;
       e.n = n;
       e.p = s->p;
@@ -534,13 +558,14 @@ static void alloc_state(pcal_session* s) {
   s->st_nchunks = ceil_div(n, s->st_chunk);
   s->nrb_f = s->model.kind == PCAL_MODEL_DENSE ? ceil_div(n, wm_grad) : s->st_nchunks;
   s->nrb_xm = ceil_div(n, wm_xm);
-  s->fpart.alloc((size_t)(s->nrb_f + 1) * p);
+  s->pstride_f = s->nrb_f + 2;
+  s->pstride_xm = s->nrb_xm + 2;
+  s->fpart.alloc((size_t)s->pstride_f * p);
   s->fpart.zero(st);
-  s->kpart.alloc((size_t)(s->nrb_xm + 1) * p);
+  s->kpart.alloc((size_t)s->pstride_xm * p);
   s->kpart.zero(st);
-  s->dpart.alloc((size_t)(s->nrb_xm + 1) * p);
+  s->dpart.alloc((size_t)s->pstride_xm * p);
   s->dpart.zero(st);
-  s->lvl1.alloc((size_t)3 * 32 * p);
   s->fcol.alloc(p);
   s->kcol.alloc(p);
   s->cp_blocks = (int)std::min<int64_t>(ceil_div(p * p, kStreamThreads), 256);
@@ -730,7 +755,7 @@ void session_create(const pcal_model_desc* model, const pcal_config* config, con
   s->timers = timers;
   s->n = model->n;
   s->p = model->p;
-  s->pp = round_up(s->p, 16);
+  s->pp = padded_p(s->p);
   s->ld = padded_ld(s->n);
   s->beta = config->beta >= 0.0 ? config->beta : 1.0;                  // solver.cpp:120-125
   s->eta0 = config->eta0 > 0.0 ? clamp_eta_h(config, config->eta0)     // solver.cpp:99-102
@@ -745,7 +770,7 @@ void session_create(const pcal_model_desc* model, const pcal_config* config, con
   init_ctl(s.get());
   upload_matrix(x0, x0_loc, s->n, s->p, Xof(s.get(), 0), s->ld, s->stream);
   k_set_t0<<<1, 1, 0, s->stream>>>(s->ctl);
-  count_launch();
+  launched("k_set_t0");
   launch_eval(s.get(), 0, 1, s->ctl);  // eval_iterate(X0) + record(0) (solver.cpp:363-365)
   PCAL_CUDA(cudaGetLastError());
   s->next_k = 0;
@@ -832,11 +857,13 @@ bool orthonormalize_dev(pcal_session* s, const double* x, double* q, double* scr
   int32_t ok = 0;
   gram_of(x);
   k_sym_fro2<<<1, 1024, 0, st>>>(s->orth_b.p, pp, p, s->orth_f2.p);
+  launched("k_sym_fro2");
   k_cholesky<<<1, 1024, 0, st>>>(s->orth_b.p, pp, p, s->orth_f2.p, s->orth_l.p, pp,
                                  s->orth_status);
+  launched("k_cholesky");
   k_trinv_t<<<(unsigned)ceil_div(p, 128), 128, 0, st>>>(s->orth_l.p, pp, p, s->orth_t.p, pp,
                                                         s->orth_status);
-  count_launch(3);
+  launched("k_trinv_t");
   PCAL_CUDA(cudaMemcpyAsync(&ok, s->orth_status, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   PCAL_CUDA(cudaStreamSynchronize(st));
   bool chol_ok = ok != 0;
@@ -845,9 +872,10 @@ bool orthonormalize_dev(pcal_session* s, const double* x, double* q, double* scr
     gram_of(scratch);
     k_cholesky<<<1, 1024, 0, st>>>(s->orth_b.p, pp, p, s->orth_f2.p, s->orth_l.p, pp,
                                    s->orth_status);
+    launched("k_cholesky");
     k_trinv_t<<<(unsigned)ceil_div(p, 128), 128, 0, st>>>(s->orth_l.p, pp, p, s->orth_t.p, pp,
                                                           s->orth_status);
-    count_launch(2);
+    launched("k_trinv_t");
     PCAL_CUDA(cudaMemcpyAsync(&ok, s->orth_status, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     PCAL_CUDA(cudaStreamSynchronize(st));
     chol_ok = ok != 0;
@@ -857,7 +885,7 @@ bool orthonormalize_dev(pcal_session* s, const double* x, double* q, double* scr
     PCAL_CUDA(cudaMemcpy2DAsync(q, sizeof(double) * ld, x, sizeof(double) * ld,
                                 sizeof(double) * ld, p, cudaMemcpyDeviceToDevice, st));
     k_mgs2<<<1, 1024, 0, st>>>(q, n, ld, p, s->orth_f2.p, s->orth_status);
-    count_launch();
+    launched("k_mgs2");
     PCAL_CUDA(cudaMemcpyAsync(&ok, s->orth_status, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     PCAL_CUDA(cudaStreamSynchronize(st));
     if (!ok) return false;
@@ -1006,6 +1034,53 @@ void pcal_session_destroy(pcal_session* s) {
 
 int64_t pcal_session_kernel_launches(pcal_session* s) { return s ? s->launches : 0; }
 
+// Per-kernel timing: iterations launched without graphs, an event after every
+// kernel; writes "name mean_ms count\n" lines (means per iteration) into buf.
+int pcal_session_profile_kernels(pcal_session* s, int64_t iters, char* buf, int64_t cap) {
+  return guarded([&] {
+    PCAL_CUDA(cudaSetDevice(s->device));
+    LaunchScope ls(&s->launches);
+    auto prof = std::make_unique<KernelProfiler>();
+    prof->stream = s->stream;
+    for (auto& m : prof->marks) PCAL_CUDA(cudaEventCreate(&m.ev));
+    cudaEvent_t start;
+    PCAL_CUDA(cudaEventCreate(&start));
+    std::vector<std::pair<std::string, double>> acc;
+    iters = std::min<int64_t>(iters, s->cfg.max_iter - s->launched);
+    g_kprof = prof.get();
+    for (int64_t i = 0; i < iters; ++i) {
+      prof->n = 0;
+      prof->active = true;
+      PCAL_CUDA(cudaEventRecord(start, s->stream));
+      launch_iteration(s, (int)(s->next_k % 2));
+      prof->active = false;
+      s->next_k++;
+      s->launched++;
+      PCAL_CUDA(cudaStreamSynchronize(s->stream));
+      cudaEvent_t prev = start;
+      for (int k = 0; k < prof->n; ++k) {
+        float ms = 0;
+        PCAL_CUDA(cudaEventElapsedTime(&ms, prev, prof->marks[k].ev));
+        prev = prof->marks[k].ev;
+        bool found = false;
+        for (auto& a : acc)
+          if (a.first == prof->marks[k].name) {
+            a.second += ms;
+            found = true;
+          }
+        if (!found) acc.emplace_back(prof->marks[k].name, ms);
+      }
+    }
+    g_kprof = nullptr;
+    std::string out;
+    for (auto& a : acc) out += a.first + " " + std::to_string(a.second / std::max<int64_t>(1, iters)) + "\n";
+    for (auto& m : prof->marks) cudaEventDestroy(m.ev);
+    cudaEventDestroy(start);
+    if ((int64_t)out.size() + 1 > cap) throw Error(PCAL_E_PARAMETER, "profile buffer too small");
+    std::memcpy(buf, out.c_str(), out.size() + 1);
+  });
+}
+
 int pcal_session_profile(pcal_session* s, int64_t iters, double* ms_out) {
   return guarded([&] {
     PCAL_CUDA(cudaSetDevice(s->device));
@@ -1123,7 +1198,7 @@ std::unique_ptr<pcal_session> make_aux(int64_t n, int64_t p, int device) {
   s->model.p = p;
   s->n = n;
   s->p = p;
-  s->pp = round_up(p, 16);
+  s->pp = padded_p(p);
   s->ld = padded_ld(n);
   alloc_state(s.get());
   init_ctl(s.get());
@@ -1151,6 +1226,16 @@ __global__ void k_matvec_part(const double* __restrict__ a, int64_t lda, int64_t
   part[kc * n + i] = s;
 }
 
+// out[i] = Σ_{c < nchunks} part[c·n + i] (fixed order)
+__global__ void k_sum_chunks(const double* __restrict__ part, int64_t nchunks, int64_t n,
+                             double* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double s = 0.0;
+  for (int64_t c = 0; c < nchunks; ++c) s += part[c * n + i];
+  out[i] = s;
+}
+
 __global__ void k_dot_part(const double* __restrict__ a, const double* __restrict__ b, int64_t n,
                            double* __restrict__ part) {
   __shared__ double sm[32];
@@ -1176,8 +1261,8 @@ int pcal_matmul_at_b(const double* a, const double* b, int64_t n, int64_t pa, in
   return guarded([&] {
     auto s = make_aux(n, std::max(pa, pb), device);
     DevBuf A, B, C;
-    upload_padded(A, a, n, pa, s->ld, round_up(pa, 16), s->stream);
-    upload_padded(B, b, n, pb, s->ld, round_up(pb, 16), s->stream);
+    upload_padded(A, a, n, pa, s->ld, padded_p(pa), s->stream);
+    upload_padded(B, b, n, pb, s->ld, padded_p(pb), s->stream);
     C.alloc((size_t)pa * pb);
     GemmPlan pl;
     plan_gemm(pl, device, pick_size(pb), A_KCONTIG, EPI_STORE, pa, pb, s->ld);
@@ -1199,7 +1284,7 @@ int pcal_matmul(const double* a, const double* b, int64_t m, int64_t k, int64_t 
                 int32_t device) {
   return guarded([&] {
     auto s = make_aux(m, 1, device);
-    const int64_t kp = round_up(k, 16), ldm = padded_ld(m);
+    const int64_t kp = padded_p(k), ldm = padded_ld(m);
     DevBuf A, B, C;
     upload_padded(A, a, m, k, ldm, kp, s->stream);
     upload_padded(B, b, k, nc, kp, nc, s->stream);
@@ -1259,8 +1344,8 @@ int pcal_initial_point_qr(int64_t n, int64_t p, uint64_t seed, double* x0, int32
       throw Error(PCAL_E_PARAMETER, "initial_point: dimensions must satisfy 2p <= n");
     std::vector<double> h((size_t)n * p);
     host_random_normal(n * p, seed, h.data(), (int)std::min<unsigned>(16, std::thread::hardware_concurrency()));
-    if (pcal_orthonormalize(h.data(), n, p, x0, device) != PCAL_OK)
-      throw Error(PCAL_E_RANK, g_last_error);
+    const int rc = pcal_orthonormalize(h.data(), n, p, x0, device);
+    if (rc != PCAL_OK) throw Error(rc, g_last_error);
   });
 }
 
@@ -1277,6 +1362,7 @@ int pcal_evaluate(const pcal_model_desc* model, const double* x, double* f, doub
     std::unique_ptr<pcal_session> s(raw);
     LaunchScope ls(&s->launches);
     k_zero_i32<<<1, 1, 0, s->stream>>>(s->bad, nullptr);
+    launched("k_zero_i32");
     launch_gradient(s.get(), 0, nullptr);
     launch_colsums(s.get(), s->fpart.p, s->nrb_f, nullptr, nullptr, 0, s->fcol.p, nullptr, nullptr,
                    nullptr);
@@ -1293,7 +1379,8 @@ int pcal_evaluate(const pcal_model_desc* model, const double* x, double* f, doub
     fa.trace = s->trace.p;
     fa.bad = s->bad;
     fa.c_xc = s->c_xc;
-    k_finish_eval<<<1, 32, 0, s->stream>>>(fa, s->ctl, s->post.p);
+    k_finish_eval<<<1, 256, 0, s->stream>>>(fa, s->ctl, s->post.p);
+    launched("k_finish_eval");
     double post[8];
     PCAL_CUDA(cudaMemcpyAsync(post, s->post.p, sizeof(double) * 5, cudaMemcpyDeviceToHost,
                               s->stream));
@@ -1318,9 +1405,11 @@ int pcal_pcal_step(const double* x, const double* grad_l, int64_t n, int64_t p, 
     k_update<<<gu, kStreamThreads, 0, s->stream>>>(Xof(s.get(), 0), Pof(s.get(), 0), s->dvec[0].p,
                                                    Xof(s.get(), 1), n, s->ld, p, s->up_chunk,
                                                    s->npart.p, s->ctl);
+    launched("k_update");
     k_normalize<<<gu, kStreamThreads, 0, s->stream>>>(Xof(s.get(), 0), Xof(s.get(), 1), n, s->ld,
                                                       p, s->up_chunk, s->up_nchunks, s->npart.p,
                                                       s->ctl);
+    launched("k_normalize");
     PCAL_CUDA(cudaGetLastError());
     copy_out(s.get(), Xof(s.get(), 1), out);
     read_ctl(s.get());
@@ -1357,11 +1446,13 @@ int pcal_spectral_norm_estimate(const double* a, int64_t n, uint64_t seed, doubl
     auto matvec = [&](const double* in, double* o) {
       k_matvec_part<<<dim3((unsigned)ceil_div(n, 256), (unsigned)nkc), 256, 0, s->stream>>>(
           A.p, lda, n, in, kchunk, part.p);
-      k_sum_rows<<<dim3((unsigned)ceil_div(n, 128), 1), 128, 0, s->stream>>>(part.p, nkc, n, nkc, o,
-                                                                            nullptr);
+      launched("k_matvec_part");
+      k_sum_chunks<<<(unsigned)ceil_div(n, 256), 256, 0, s->stream>>>(part.p, nkc, n, o);
+      launched("k_sum_chunks");
     };
     auto norm = [&](const double* x) {
       k_dot_part<<<nblk, 256, 0, s->stream>>>(x, x, n, dots.p);
+      launched("k_dot_part");
       PCAL_CUDA(cudaMemcpyAsync(hd.data(), dots.p, sizeof(double) * nblk, cudaMemcpyDeviceToHost,
                                 s->stream));
       PCAL_CUDA(cudaStreamSynchronize(s->stream));
@@ -1380,6 +1471,7 @@ int pcal_spectral_norm_estimate(const double* a, int64_t n, uint64_t seed, doubl
       }
       // A padded columns are contiguous with lda ≥ n: sum over the whole buffer (pads are 0)
       k_dot_part<<<nblk, 256, 0, s->stream>>>(A.p, A.p, lda * n, fp.p);
+      launched("k_dot_part");
       PCAL_CUDA(cudaMemcpyAsync(hd.data(), fp.p, sizeof(double) * nblk, cudaMemcpyDeviceToHost,
                                 s->stream));
       PCAL_CUDA(cudaStreamSynchronize(s->stream));
@@ -1398,6 +1490,7 @@ int pcal_spectral_norm_estimate(const double* a, int64_t n, uint64_t seed, doubl
       const double nt = norm(t.p);
       if (nt == 0.0) break;
       k_scale_div<<<(unsigned)ceil_div(n, 256), 256, 0, s->stream>>>(t.p, n, nt);
+      launched("k_scale_div");
       std::swap(v.p, t.p);
       if (prev >= 0.0 && std::abs(est - prev) <= 1e-6 * std::max(est, 1e-300)) break;
       prev = est;
