@@ -60,8 +60,9 @@ void plan_gemm(GemmPlan& pl, int device, int size, int amode, int epi, int64_t M
   if (K % BK) throw Error(PCAL_E_DIMENSION, "gemm: K must be a multiple of the k-slice");
   const int64_t tm_n = ceil_div(M, ci.BM), tn_n = ceil_div(N, ci.BN);
   std::vector<int2> tiles;
-  for (int64_t tn = 0; tn < tn_n; ++tn)
-    for (int64_t tm = 0; tm < tm_n; ++tm) {
+  // tm-major: consecutive tiles share the A row-block (L2 reuse across tn)
+  for (int64_t tm = 0; tm < tm_n; ++tm)
+    for (int64_t tn = 0; tn < tn_n; ++tn) {
       if (sym_row0 >= 0) {
         const int64_t r0 = tm * ci.BM;
         const int64_t c1 = (tn + 1) * ci.BN - 1;

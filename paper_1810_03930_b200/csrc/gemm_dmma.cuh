@@ -158,9 +158,18 @@ __device__ __forceinline__ void epilogue(const GemmArgs& g, int tm, int tn, int 
     }
   } else if constexpr (EPI == EPI_GRAD) {
     const int64_t rb = mw0 / Cfg::WM;
+    const bool interior = (mw0 + Cfg::WM <= e.n) && (nw0 + Cfg::WN <= e.p) && !e.g0;
     bool bad = false;
 #pragma unroll
-    for (int nt = 0; nt < Cfg::NT; ++nt)
+    for (int nt = 0; nt < Cfg::NT; ++nt) {
+      double xv[2][Cfg::MT];
+      if (interior) {  // batch the X loads of this column pair
+#pragma unroll
+        for (int x = 0; x < 2; ++x)
+#pragma unroll
+          for (int mt = 0; mt < Cfg::MT; ++mt)
+            xv[x][mt] = e.X[mw0 + mt * 8 + r + (nw0 + nt * 8 + 2 * q + x) * e.ld];
+      }
 #pragma unroll
       for (int x = 0; x < 2; ++x) {
         const int64_t col = nw0 + nt * 8 + 2 * q + x;
@@ -168,7 +177,12 @@ __device__ __forceinline__ void epilogue(const GemmArgs& g, int tm, int tn, int 
 #pragma unroll
         for (int mt = 0; mt < Cfg::MT; ++mt) {
           const int64_t row = mw0 + mt * 8 + r;
-          if (row < e.n && col < e.p) {
+          if (interior) {
+            const double gv = acc[mt][nt][x];
+            e.G[row + col * e.ld] = gv;
+            fs += xv[x][mt] * gv;
+            bad |= !isfinite(gv);
+          } else if (row < e.n && col < e.p) {
             double gv = acc[mt][nt][x];
             double fv = gv;  // f = ½⟨X, AX + 2·G0⟩ = ½⟨X,AX⟩ + ⟨G0,X⟩
             if (e.g0) {
@@ -186,33 +200,61 @@ __device__ __forceinline__ void epilogue(const GemmArgs& g, int tm, int tn, int 
         fs += __shfl_xor_sync(0xffffffffu, fs, 16);
         if (r == 0 && col < e.p) e.fpart[col * e.pstride + rb] = fs;
       }
+    }
     if (__any_sync(0xffffffffu, bad) && lane == 0) *e.bad = 1;
   } else {  // EPI_XM
     const int64_t rb = mw0 / Cfg::WM;
+    // interior warp tiles: issue every G/X load of a batch of NB column groups
+    // before any use (one memory round trip per batch instead of one per element)
+    const bool interior = (mw0 + Cfg::WM <= e.n) && (((nw0 + Cfg::WN) >> 1) <= e.p);
+    constexpr int NB = Cfg::NT >= 2 ? 2 : 1;
 #pragma unroll
-    for (int nt = 0; nt < Cfg::NT; ++nt) {
-      const int64_t j = (nw0 + nt * 8 + 2 * q) >> 1;  // output column
-      double ks = 0.0, ds = 0.0;
+    for (int nb0 = 0; nb0 < Cfg::NT; nb0 += NB) {
+      double gv[NB][Cfg::MT], xv[NB][Cfg::MT];
+      if (interior) {
 #pragma unroll
-      for (int mt = 0; mt < Cfg::MT; ++mt) {
-        const int64_t row = mw0 + mt * 8 + r;
-        if (row < e.n && j < e.p) {
-          const int64_t idx = row + j * e.ld;
-          const double kkt = e.G[idx] - acc[mt][nt][0];
-          const double pv = kkt + e.beta * acc[mt][nt][1];
-          e.G[idx] = pv;
-          ks += kkt * kkt;
-          ds += e.X[idx] * pv;
+        for (int b = 0; b < NB; ++b) {
+          const int64_t j = (nw0 + (nb0 + b) * 8 + 2 * q) >> 1;
+#pragma unroll
+          for (int mt = 0; mt < Cfg::MT; ++mt) {
+            const int64_t idx = mw0 + mt * 8 + r + j * e.ld;
+            gv[b][mt] = e.G[idx];
+            xv[b][mt] = e.X[idx];
+          }
         }
       }
 #pragma unroll
-      for (int o = 4; o < 32; o <<= 1) {
-        ks += __shfl_xor_sync(0xffffffffu, ks, o);
-        ds += __shfl_xor_sync(0xffffffffu, ds, o);
-      }
-      if (r == 0 && j < e.p) {
-        e.kpart[j * e.pstride + rb] = ks;
-        e.dpart[j * e.pstride + rb] = ds;
+      for (int b = 0; b < NB; ++b) {
+        const int nt = nb0 + b;
+        const int64_t j = (nw0 + nt * 8 + 2 * q) >> 1;  // output column
+        double ks = 0.0, ds = 0.0;
+#pragma unroll
+        for (int mt = 0; mt < Cfg::MT; ++mt) {
+          const int64_t row = mw0 + mt * 8 + r;
+          const int64_t idx = row + j * e.ld;
+          if (interior) {
+            const double kkt = gv[b][mt] - acc[mt][nt][0];
+            const double pv = kkt + e.beta * acc[mt][nt][1];
+            e.G[idx] = pv;
+            ks += kkt * kkt;
+            ds += xv[b][mt] * pv;
+          } else if (row < e.n && j < e.p) {
+            const double kkt = e.G[idx] - acc[mt][nt][0];
+            const double pv = kkt + e.beta * acc[mt][nt][1];
+            e.G[idx] = pv;
+            ks += kkt * kkt;
+            ds += e.X[idx] * pv;
+          }
+        }
+#pragma unroll
+        for (int o = 4; o < 32; o <<= 1) {
+          ks += __shfl_xor_sync(0xffffffffu, ks, o);
+          ds += __shfl_xor_sync(0xffffffffu, ds, o);
+        }
+        if (r == 0 && j < e.p) {
+          e.kpart[j * e.pstride + rb] = ks;
+          e.dpart[j * e.pstride + rb] = ds;
+        }
       }
     }
   }
