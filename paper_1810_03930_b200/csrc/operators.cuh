@@ -66,6 +66,114 @@ __global__ void __launch_bounds__(kStencilThreads)
   if (__syncthreads_or(nonfinite) && threadIdx.x == 0) *bad = 1;
 }
 
+// z-marching 2.5D stencil for grids with nx ≤ 32·XP and ny % TY == 0: a block
+// owns an nx × TY tile of the xy-plane of one column j and walks a z-range;
+// each thread keeps its points of planes z−1, z, z+1 in registers and the
+// current plane (+ periodic y-halo rows) in shared memory, so every X value is
+// read from HBM once (halo rows: 2/TY extra, mostly L2 hits).  Same operation
+// order as k_stencil_grad (bitwise identical results).
+template <bool KS, int XP, int TY>
+__global__ void __launch_bounds__(32 * TY)
+    k_stencil_march(const double* __restrict__ x, const double* __restrict__ u,
+                    double* __restrict__ g, int nx, int ny, int nz, int64_t ld, int zchunk,
+                    double* __restrict__ fpart, int64_t pstride, int32_t* bad, const Ctl* ctl) {
+  if (ctl && ctl->done) return;
+  constexpr int W = 32 * XP;  // smem row width (≥ nx)
+  __shared__ double pl[TY + 2][W];
+  __shared__ double sm[TY];
+  const int lane = threadIdx.x, ty = threadIdx.y;
+  const int y0 = blockIdx.x * TY;
+  const int zc = blockIdx.y;
+  const int64_t j = blockIdx.z;
+  const int z0 = zc * zchunk;
+  const int z1 = min(nz, z0 + zchunk);
+  const int y = y0 + ty;
+  const int64_t nxy = (int64_t)nx * ny;
+  const double* xj = x + j * ld;
+  double* gj = g + j * ld;
+  const int yh = ty == 0 ? (y0 == 0 ? ny - 1 : y0 - 1) : (y0 + TY == ny ? 0 : y0 + TY);
+  // all global loads run one z-step ahead: planes z+1 (interior), the y-halo
+  // rows of plane z+1 and the potential u of plane z+1 are fetched while
+  // plane z is computed
+  double below[XP], cur[XP], above[XP], halo[XP], uc[XP];
+  auto plane = [&](int z) { return (int64_t)((z % nz + nz) % nz) * nxy; };
+  const bool hrow = ty == 0 || ty == TY - 1;
+#pragma unroll
+  for (int k = 0; k < XP; ++k) {
+    const int xx = lane + 32 * k;
+    const bool ok = xx < nx;
+    below[k] = ok ? __ldg(xj + plane(z0 - 1) + (int64_t)y * nx + xx) : 0.0;
+    cur[k] = ok ? __ldg(xj + plane(z0) + (int64_t)y * nx + xx) : 0.0;
+    above[k] = ok ? __ldg(xj + plane(z0 + 1) + (int64_t)y * nx + xx) : 0.0;
+    halo[k] = (ok && hrow) ? __ldg(xj + plane(z0) + (int64_t)yh * nx + xx) : 0.0;
+    uc[k] = ok ? __ldg(u + plane(z0) + (int64_t)y * nx + xx) : 0.0;
+  }
+  double acc = 0.0;
+  bool nonfinite = false;
+  for (int z = z0; z < z1; ++z) {
+    const int64_t pz = plane(z), pn = plane(z + 1), pa = plane(z + 2);
+#pragma unroll
+    for (int k = 0; k < XP; ++k) {
+      const int xx = lane + 32 * k;
+      if (xx < nx) {
+        pl[ty + 1][xx] = cur[k];
+        if (hrow) pl[ty == 0 ? 0 : TY + 1][xx] = halo[k];
+      }
+    }
+    __syncthreads();
+    double above2[XP], halo_n[XP], u_n[XP];
+    const bool more = z + 1 < z1;
+#pragma unroll
+    for (int k = 0; k < XP; ++k) {
+      const int xx = lane + 32 * k;
+      const bool ok = xx < nx && more;
+      above2[k] = ok ? __ldg(xj + pa + (int64_t)y * nx + xx) : 0.0;
+      halo_n[k] = (ok && hrow) ? __ldg(xj + pn + (int64_t)yh * nx + xx) : 0.0;
+      u_n[k] = ok ? __ldg(u + pn + (int64_t)y * nx + xx) : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < XP; ++k) {
+      const int xx = lane + 32 * k;
+      if (xx < nx) {
+        const int xm = xx == 0 ? nx - 1 : xx - 1;
+        const int xp = xx == nx - 1 ? 0 : xx + 1;
+        const double xv = cur[k];
+        double lx = __dmul_rn(6.0, xv);
+        lx = __dsub_rn(lx, pl[ty + 1][xm]);
+        lx = __dsub_rn(lx, pl[ty + 1][xp]);
+        lx = __dsub_rn(lx, pl[ty][xx]);
+        lx = __dsub_rn(lx, pl[ty + 2][xx]);
+        lx = __dsub_rn(lx, below[k]);
+        lx = __dsub_rn(lx, above[k]);
+        const int64_t i = pz + (int64_t)y * nx + xx;
+        double gv;
+        if (KS) gv = __dadd_rn(__dmul_rn(0.5, lx), __dmul_rn(uc[k], xv));
+        else gv = __dadd_rn(lx, __dmul_rn(uc[k], xv));
+        gj[i] = gv;
+        acc += KS ? xv * lx : xv * gv;
+        nonfinite |= !isfinite(gv);
+      }
+      below[k] = cur[k];
+      cur[k] = above[k];
+      above[k] = above2[k];
+      halo[k] = halo_n[k];
+      uc[k] = u_n[k];
+    }
+    __syncthreads();
+  }
+  // block reduction (fixed order) → one partial per (tile, z-chunk)
+  double v = warp_sum(acc);
+  if (lane == 0) sm[ty] = v;
+  __syncthreads();
+  if (lane == 0 && ty == 0) {
+    double s = 0.0;
+#pragma unroll
+    for (int t = 0; t < TY; ++t) s += sm[t];
+    fpart[j * pstride + blockIdx.x + (int64_t)gridDim.x * zc] = s;
+  }
+  if (__syncthreads_or(nonfinite) && lane == 0 && ty == 0) *bad = 1;
+}
+
 // ρ_i = Σ_j X_ij² (row_sq_norms, kernels.cpp:295-303 order: column-outer).
 __global__ void k_row_sq_norms(const double* __restrict__ x, int64_t n, int64_t ld, int64_t p,
                                double* __restrict__ rho, const Ctl* ctl) {

@@ -289,6 +289,8 @@ struct pcal_session {
   int64_t up_chunk = 0, up_nchunks = 0;
   int bb_blocks = 0, cp_blocks = 0, sp_blocks = 0;
   int64_t st_chunk = 0, st_nchunks = 0;
+  bool st_march = false;
+  int64_t st_zchunk = 0, st_nzc = 0;
   // graphs
   cudaGraphExec_t graph[2] = {nullptr, nullptr};
   int64_t kernels_per_iter = 0;
@@ -343,6 +345,43 @@ static void launch_colsums(pcal_session* s, const double* fp, int64_t nrb_f, con
 }
 
 // Gradient of the model at X (pair b): G into P(b), f partials into fpart.
+// 7-point stencil part of the grid models: z-marching kernel when the grid
+// allows it (nx ≤ 128, ny % 8 == 0), else the generic element kernel.
+static void launch_stencil(pcal_session* s, int b, const double* u, bool ks, const Ctl* ctl) {
+  const auto& m = s->model;
+  const int64_t p = s->p;
+  if (s->st_march) {
+    const int TY = 8;
+    dim3 grid((unsigned)(m.ny / TY), (unsigned)s->st_nzc, (unsigned)p);
+    dim3 block(32, TY);
+    const int xp = (int)ceil_div(m.nx, 32);
+#define PCAL_MARCH(KSV, XPV)                                                                   \
+  k_stencil_march<KSV, XPV, 8><<<grid, block, 0, s->stream>>>(                               \
+      Xof(s, b), u, Pof(s, b), (int)m.nx, (int)m.ny, (int)m.nz, s->ld, (int)s->st_zchunk,     \
+      s->fpart.p, s->pstride_f, s->bad, ctl)
+    if (ks) {
+      if (xp == 1) PCAL_MARCH(true, 1); else if (xp == 2) PCAL_MARCH(true, 2);
+      else if (xp == 3) PCAL_MARCH(true, 3); else PCAL_MARCH(true, 4);
+    } else {
+      if (xp == 1) PCAL_MARCH(false, 1); else if (xp == 2) PCAL_MARCH(false, 2);
+      else if (xp == 3) PCAL_MARCH(false, 3); else PCAL_MARCH(false, 4);
+    }
+#undef PCAL_MARCH
+    launched("k_stencil_march");
+  } else {
+    dim3 g((unsigned)s->st_nchunks, (unsigned)p);
+    if (ks)
+      k_stencil_grad<true><<<g, kStencilThreads, 0, s->stream>>>(
+          Xof(s, b), u, Pof(s, b), m.nx, m.ny, m.nz, s->ld, p, s->st_chunk, s->fpart.p,
+          s->pstride_f, s->bad, ctl);
+    else
+      k_stencil_grad<false><<<g, kStencilThreads, 0, s->stream>>>(
+          Xof(s, b), u, Pof(s, b), m.nx, m.ny, m.nz, s->ld, p, s->st_chunk, s->fpart.p,
+          s->pstride_f, s->bad, ctl);
+    launched("k_stencil_grad");
+  }
+}
+
 static void launch_gradient(pcal_session* s, int b, const Ctl* ctl) {
   const int64_t p = s->p;
   switch (s->model.kind) {
@@ -350,11 +389,7 @@ static void launch_gradient(pcal_session* s, int b, const Ctl* ctl) {
       launch_gemm(s->grad[b], s->stream);
       break;
     case PCAL_MODEL_STENCIL: {
-      dim3 g((unsigned)s->st_nchunks, (unsigned)p);
-      k_stencil_grad<false><<<g, kStencilThreads, 0, s->stream>>>(
-          Xof(s, b), s->V.p, Pof(s, b), s->model.nx, s->model.ny, s->model.nz, s->ld, p,
-          s->st_chunk, s->fpart.p, s->pstride_f, s->bad, ctl);
-      launched("k_stencil_grad");
+      launch_stencil(s, b, s->V.p, false, ctl);
       break;
     }
     case PCAL_MODEL_KOHN_SHAM: {
@@ -387,11 +422,7 @@ static void launch_gradient(pcal_session* s, int b, const Ctl* ctl) {
       k_ks_potential<<<s->sp_blocks, 256, 0, s->stream>>>(s->V.p, s->rho.p, s->h.p, s->u.p, n,
                                                           s->c_xc, s->spart.p, ctl);
       launched("k_ks_potential");
-      dim3 g((unsigned)s->st_nchunks, (unsigned)p);
-      k_stencil_grad<true><<<g, kStencilThreads, 0, s->stream>>>(
-          Xof(s, b), s->u.p, Pof(s, b), m.nx, m.ny, m.nz, s->ld, p, s->st_chunk, s->fpart.p,
-          s->pstride_f, s->bad, ctl);
-      launched("k_stencil_grad");
+      launch_stencil(s, b, s->u.p, true, ctl);
       break;
     }
     default:
@@ -556,7 +587,20 @@ static void alloc_state(pcal_session* s) {
   const int64_t wm_xm = cfg_info(pick_size(2 * pp)).WM;
   s->st_chunk = 2048;
   s->st_nchunks = ceil_div(n, s->st_chunk);
-  s->nrb_f = s->model.kind == PCAL_MODEL_DENSE ? ceil_div(n, wm_grad) : s->st_nchunks;
+  {
+    const auto& m = s->model;
+    s->st_march = m.kind != PCAL_MODEL_DENSE && m.nx <= 128 && m.ny % 8 == 0 && m.ny >= 8 &&
+                  m.nz >= 1;
+    if (s->st_march) {  // enough blocks for ≈ 8 per SM
+      const int64_t tiles = (m.ny / 8) * p;
+      int64_t nzc = std::max<int64_t>(1, std::min<int64_t>(m.nz, ceil_div(8 * 148, tiles)));
+      s->st_zchunk = ceil_div(m.nz, nzc);
+      s->st_nzc = ceil_div(m.nz, s->st_zchunk);
+    }
+  }
+  s->nrb_f = s->model.kind == PCAL_MODEL_DENSE ? ceil_div(n, wm_grad)
+             : s->st_march ? (s->model.ny / 8) * s->st_nzc
+                           : s->st_nchunks;
   s->nrb_xm = ceil_div(n, wm_xm);
   s->pstride_f = s->nrb_f + 2;
   s->pstride_xm = s->nrb_xm + 2;

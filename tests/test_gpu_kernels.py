@@ -157,3 +157,17 @@ def test_kohn_sham_gradient(pcal, orc, grid, p):
     f, g = pcal.evaluate(pcal.KohnShamModel(grid, v, p, 12.0), x)
     assert rel(g, g_ref) <= 1e-14  # only the device cbrt may differ by an ulp
     assert abs(f - f_ref) <= 1e-12 * abs(f_ref)
+
+
+@pytest.mark.parametrize("grid,p", [((32, 8, 5), 3), ((48, 16, 7), 2), ((128, 16, 4), 2),
+                                    ((64, 64, 64), 2), ((40, 24, 3), 5)])
+def test_stencil_march_bitwise(pcal, orc, grid, p):
+    """z-marching kernel (nx ≤ 128, ny % 8 == 0): same bits as the oracle."""
+    from oracle.oracle import Model, MODEL_STENCIL
+    n = grid[0] * grid[1] * grid[2]
+    v = orc.random_uniform(n, 13)
+    x = orc.random_normal(n, p, 14)
+    f_ref, g_ref = orc.evaluate(Model(MODEL_STENCIL, n, p, 13.0, grid=grid, v=v), x)
+    f, g = pcal.evaluate(pcal.StencilModel(grid, v, p, 13.0), x)
+    assert np.array_equal(g, g_ref)
+    assert abs(f - f_ref) <= 1e-12 * abs(f_ref)
