@@ -164,6 +164,35 @@ int pcal_session_profile_kernels(pcal_session* s, int64_t iters, char* buf, int6
 /* Per-iteration launch count of the captured iteration graph. */
 int64_t pcal_session_kernels_per_iteration(pcal_session* s);
 
+/* ---- row-sharded multi-GPU solve (one process per GPU, NCCL) -------------
+ * Rows are split by z-slabs (grid models) or row blocks (dense); every n×p
+ * object is row-local, p×p objects are replicated, and per iteration the ranks
+ * exchange the Gram partials, per-column sums, stepsize partials, column norms
+ * and the halo planes / X allgather.  A sharded session takes
+ * the GLOBAL sizes in `model` (n, p, nx, ny, nz) but LOCAL data: dense `a` =
+ * rows [row0, row0+nrows) of A for all n columns (ld = nrows), `g0`, `v` and
+ * x0 = the owned rows.  pcal_partition tells each rank its rows. */
+typedef struct pcal_comm pcal_comm;
+int pcal_partition(const pcal_model_desc* model, int32_t nranks, int32_t rank, int64_t* row0,
+                   int64_t* nrows);
+/* 128-byte NCCL unique id (rank 0 creates it, the caller broadcasts it). */
+int pcal_nccl_unique_id(void* out);
+int pcal_comm_create_nccl(int32_t nranks, int32_t rank, const void* unique_id, int32_t device,
+                          pcal_comm** out);
+void pcal_comm_destroy(pcal_comm* comm);
+int pcal_session_create_sharded(const pcal_model_desc* local_model, const pcal_config* config,
+                                const double* x0_local, int32_t x0_location, pcal_comm* comm,
+                                pcal_session** out);
+/* report rows (stop_x / final_x) are the local rows (nrows × p). */
+int pcal_solve_sharded(const pcal_model_desc* local_model, const pcal_config* config,
+                       const double* x0_local, int32_t x0_location, pcal_comm* comm,
+                       pcal_report* report);
+/* The sharded algorithm with `nranks` emulated ranks on ONE GPU (host threads,
+ * loopback collectives): validates the multi-GPU path where one GPU exists.
+ * Global host data in, global report out. */
+int pcal_solve_emulated(const pcal_model_desc* model, const pcal_config* config, const double* x0,
+                        int32_t nranks, pcal_report* report);
+
 /* ---- building blocks (host buffers; for parity tests and tools) ---------- */
 /* C = Aᵀ·B for n×pa and n×pb (kernels.cpp:124-137 matmul_at_b). */
 int pcal_matmul_at_b(const double* a, const double* b, int64_t n, int64_t pa, int64_t pb,

@@ -146,6 +146,16 @@ def lib() -> C.CDLL:
     L.pcal_random_uniform.argtypes = [i64, u64, vp]
     L.pcal_gen_dense_operator.argtypes = [i64, u64, vp, i32]
     L.pcal_initial_point_qr.argtypes = [i64, i64, u64, vp, i32]
+    L.pcal_partition.argtypes = [C.POINTER(_Model), i32, i32, C.POINTER(i64), C.POINTER(i64)]
+    L.pcal_nccl_unique_id.argtypes = [vp]
+    L.pcal_comm_create_nccl.argtypes = [i32, i32, vp, i32, C.POINTER(vp)]
+    L.pcal_comm_destroy.argtypes = [vp]
+    L.pcal_session_create_sharded.argtypes = [C.POINTER(_Model), C.POINTER(_Config), vp, i32, vp,
+                                              C.POINTER(vp)]
+    L.pcal_solve_sharded.argtypes = [C.POINTER(_Model), C.POINTER(_Config), vp, i32, vp,
+                                     C.POINTER(_Report)]
+    L.pcal_solve_emulated.argtypes = [C.POINTER(_Model), C.POINTER(_Config), vp, i32,
+                                      C.POINTER(_Report)]
     _lib = L
     return L
 
@@ -275,13 +285,14 @@ class QuadraticModel(_ModelBase):
     """f(X) = ½tr(XᵀAX) + tr(G0ᵀX) with dense symmetric A (problems.cpp:125-141).
     ``a`` may be a host numpy array or a CUDA torch tensor (column-major)."""
 
-    def __init__(self, a, p: int, s: float, g0=None):
+    def __init__(self, a, p: int, s: float, g0=None, n: Optional[int] = None):
         self.kind = MODEL_DENSE
         on_dev = hasattr(a, "data_ptr") and not isinstance(a, np.ndarray)
         self.a = a if on_dev else _f64(a)
         self.g0 = None if g0 is None else (g0 if on_dev else _f64(g0))
         self.location = DEVICE if on_dev else HOST
-        self.n = int(a.shape[0])
+        # n: global size (a may be the local row slab of a sharded session)
+        self.n = int(a.shape[1]) if n is None else int(n)
         self.p = int(p)
         self.s = float(s)
 
@@ -291,7 +302,8 @@ class QuadraticModel(_ModelBase):
 
 
 class StencilModel(_ModelBase):
-    """f(X) = ½tr(XᵀLX) + ½tr(XᵀVX), L = −Δ_h 7-point periodic (configs 3 and 5)."""
+    """f(X) = ½tr(XᵀLX) + ½tr(XᵀVX), L = −Δ_h 7-point periodic (configs 3 and 5).
+    ``v`` is the potential of the owned rows (all rows on a single GPU)."""
 
     def __init__(self, grid, v, p: int, s: float):
         self.kind = MODEL_STENCIL
@@ -554,3 +566,81 @@ def gen_dense_operator(n: int, seed: int, threads: int = 8) -> np.ndarray:
 
 def flops_estimate(n: int, p: int) -> float:
     return lib().pcal_flops_estimate(n, p)
+
+
+# --------------------------------------------------------------------------- #
+# row-sharded multi-GPU
+# --------------------------------------------------------------------------- #
+def partition(model: _ModelBase, nranks: int, rank: int) -> tuple:
+    """(row0, nrows) owned by `rank` of `nranks` (z-slabs / row blocks)."""
+    cm, keep = model._c()
+    r0, nr = C.c_int64(), C.c_int64()
+    _check(lib().pcal_partition(C.byref(cm), nranks, rank, C.byref(r0), C.byref(nr)))
+    return r0.value, nr.value
+
+
+def solve_emulated(model: _ModelBase, config: SolverConfig, x0, nranks: int) -> RunReport:
+    """The sharded algorithm with `nranks` emulated ranks on one GPU (loopback
+    collectives); global host data in, global report out."""
+    cm, keep = model._c()
+    cc = config._c()
+    x0 = _f64(x0)
+    rep, trace, stop_x, final_x = _new_report(model.n, model.p, config.max_iter)
+    _check(lib().pcal_solve_emulated(C.byref(cm), C.byref(cc), _ptr(x0), nranks, C.byref(rep)))
+    return _report_from(rep, trace, stop_x, final_x)
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(lib().pcal_nccl_unique_id(buf))
+    return buf.raw
+
+
+class Comm:
+    """NCCL communicator of one rank (one process per GPU)."""
+
+    def __init__(self, nranks: int, rank: int, unique_id: bytes, device: int):
+        self.nranks, self.rank = nranks, rank
+        h = C.c_void_p()
+        uid = C.create_string_buffer(bytes(unique_id), 128)
+        _check(lib().pcal_comm_create_nccl(nranks, rank, uid, device, C.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().pcal_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class ShardedSession(Session):
+    """Session over the local rows of a row-sharded problem (model carries the
+    global sizes and the LOCAL slabs; x0 = owned rows)."""
+
+    def __init__(self, model: _ModelBase, config: SolverConfig, x0_local, comm: Comm,
+                 n_local: int):
+        self._L = lib()
+        self.model, self.config = model, config
+        self.n_local = n_local
+        cm, self._keep = model._c()
+        cc = config._c()
+        on_dev = hasattr(x0_local, "data_ptr") and not isinstance(x0_local, np.ndarray)
+        if not on_dev:
+            x0_local = _f64(x0_local)
+        self._x0 = x0_local
+        h = C.c_void_p()
+        _check(self._L.pcal_session_create_sharded(C.byref(cm), C.byref(cc), _ptr(x0_local),
+                                                   DEVICE if on_dev else HOST, comm._h,
+                                                   C.byref(h)))
+        self._h = h
+
+    def finish(self, want_x: bool = True) -> RunReport:
+        rep, trace, stop_x, final_x = _new_report(self.n_local, self.model.p,
+                                                  self.config.max_iter, want_x)
+        _check(self._L.pcal_session_finish(self._h, C.byref(rep)))
+        return _report_from(rep, trace, stop_x, final_x)

@@ -76,7 +76,8 @@ template <bool KS, int XP, int TY>
 __global__ void __launch_bounds__(32 * TY)
     k_stencil_march(const double* __restrict__ x, const double* __restrict__ u,
                     double* __restrict__ g, int nx, int ny, int nz, int64_t ld, int zchunk,
-                    double* __restrict__ fpart, int64_t pstride, int32_t* bad, const Ctl* ctl) {
+                    double* __restrict__ fpart, int64_t pstride, int32_t* bad, const Ctl* ctl,
+                    const double* __restrict__ hlo, const double* __restrict__ hhi) {
   if (ctl && ctl->done) return;
   constexpr int W = 32 * XP;  // smem row width (≥ nx)
   __shared__ double pl[TY + 2][W];
@@ -96,22 +97,33 @@ __global__ void __launch_bounds__(32 * TY)
   // rows of plane z+1 and the potential u of plane z+1 are fetched while
   // plane z is computed
   double below[XP], cur[XP], above[XP], halo[XP], uc[XP];
-  auto plane = [&](int z) { return (int64_t)((z % nz + nz) % nz) * nxy; };
+  // plane z of column j: periodic wrap on a single GPU; on a z-slab of a
+  // sharded grid, planes −1 and nz come from the neighbours' halo planes
+  auto src = [&](int z) -> const double* {
+    if (hlo) {
+      if (z < 0) return hlo + j * nxy;
+      if (z >= nz) return hhi + j * nxy;
+      return xj + (int64_t)z * nxy;
+    }
+    return xj + (int64_t)((z % nz + nz) % nz) * nxy;
+  };
   const bool hrow = ty == 0 || ty == TY - 1;
 #pragma unroll
   for (int k = 0; k < XP; ++k) {
     const int xx = lane + 32 * k;
     const bool ok = xx < nx;
-    below[k] = ok ? __ldg(xj + plane(z0 - 1) + (int64_t)y * nx + xx) : 0.0;
-    cur[k] = ok ? __ldg(xj + plane(z0) + (int64_t)y * nx + xx) : 0.0;
-    above[k] = ok ? __ldg(xj + plane(z0 + 1) + (int64_t)y * nx + xx) : 0.0;
-    halo[k] = (ok && hrow) ? __ldg(xj + plane(z0) + (int64_t)yh * nx + xx) : 0.0;
-    uc[k] = ok ? __ldg(u + plane(z0) + (int64_t)y * nx + xx) : 0.0;
+    below[k] = ok ? __ldg(src(z0 - 1) + (int64_t)y * nx + xx) : 0.0;
+    cur[k] = ok ? __ldg(src(z0) + (int64_t)y * nx + xx) : 0.0;
+    above[k] = ok ? __ldg(src(z0 + 1) + (int64_t)y * nx + xx) : 0.0;
+    halo[k] = (ok && hrow) ? __ldg(src(z0) + (int64_t)yh * nx + xx) : 0.0;
+    uc[k] = ok ? __ldg(u + (int64_t)z0 * nxy + (int64_t)y * nx + xx) : 0.0;
   }
   double acc = 0.0;
   bool nonfinite = false;
   for (int z = z0; z < z1; ++z) {
-    const int64_t pz = plane(z), pn = plane(z + 1), pa = plane(z + 2);
+    const double* sn = src(z + 1);
+    const double* sa = src(z + 2);
+    const int64_t pz = (int64_t)z * nxy, pn = pz + nxy;
 #pragma unroll
     for (int k = 0; k < XP; ++k) {
       const int xx = lane + 32 * k;
@@ -127,8 +139,8 @@ __global__ void __launch_bounds__(32 * TY)
     for (int k = 0; k < XP; ++k) {
       const int xx = lane + 32 * k;
       const bool ok = xx < nx && more;
-      above2[k] = ok ? __ldg(xj + pa + (int64_t)y * nx + xx) : 0.0;
-      halo_n[k] = (ok && hrow) ? __ldg(xj + pn + (int64_t)yh * nx + xx) : 0.0;
+      above2[k] = ok ? __ldg(sa + (int64_t)y * nx + xx) : 0.0;
+      halo_n[k] = (ok && hrow) ? __ldg(sn + (int64_t)yh * nx + xx) : 0.0;
       u_n[k] = ok ? __ldg(u + pn + (int64_t)y * nx + xx) : 0.0;
     }
 #pragma unroll
@@ -172,6 +184,30 @@ __global__ void __launch_bounds__(32 * TY)
     fpart[j * pstride + blockIdx.x + (int64_t)gridDim.x * zc] = s;
   }
   if (__syncthreads_or(nonfinite) && lane == 0 && ty == 0) *bad = 1;
+}
+
+// Halo send planes of a z-slab: lo = plane 0, hi = plane nzl−1 of every column.
+__global__ void k_pack_planes(const double* __restrict__ x, int64_t ld, int64_t nxy, int64_t nzl,
+                              double* __restrict__ lo, double* __restrict__ hi, const Ctl* ctl) {
+  if (ctl && ctl->done) return;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t j = blockIdx.y;
+  if (e >= nxy) return;
+  lo[j * nxy + e] = x[j * ld + e];
+  hi[j * nxy + e] = x[j * ld + (nzl - 1) * nxy + e];
+}
+
+// Gathered rank blocks (R × [ld_blk × cols]) → global row order (ld_out × cols):
+// out[row0_r + i + c·ld_out] = in[r·ld_blk·cols + c·ld_blk + i], i < rows_r.
+__global__ void k_unpack_rows(const double* __restrict__ in, int64_t ld_blk, int64_t cols,
+                              const int64_t* __restrict__ rr /* row0[R], rows[R] */, int R,
+                              double* __restrict__ out, int64_t ld_out, const Ctl* ctl) {
+  if (ctl && ctl->done) return;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t c = blockIdx.y;
+  const int r = blockIdx.z;
+  if (i >= rr[R + r]) return;
+  out[rr[r] + i + c * ld_out] = in[(int64_t)r * ld_blk * cols + c * ld_blk + i];
 }
 
 // ρ_i = Σ_j X_ij² (row_sq_norms, kernels.cpp:295-303 order: column-outer).

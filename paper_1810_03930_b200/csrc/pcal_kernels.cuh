@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(kStreamThreads) k_eta(Ctl* ctl, const double* 
 __global__ void k_update(const double* __restrict__ x, const double* __restrict__ pg,
                          const double* __restrict__ d, double* __restrict__ z, int64_t n,
                          int64_t ld, int64_t p, int64_t chunk, double* __restrict__ npart,
-                         const Ctl* ctl) {
+                         double* __restrict__ xpart, const Ctl* ctl) {
   if (ctl->done) return;
   __shared__ double sm[kStreamThreads / 32];
   const int64_t j = blockIdx.y;
@@ -173,7 +173,7 @@ __global__ void k_update(const double* __restrict__ x, const double* __restrict_
   const int64_t r1 = min(n, r0 + chunk);
   const double inv_eta = 1.0 / ctl->eta;
   const double dj = d[j];
-  double acc = 0.0;
+  double acc = 0.0, xacc = 0.0;
   const double* xj = x + j * ld;
   const double* pj = pg + j * ld;
   double* zj = z + j * ld;
@@ -183,16 +183,38 @@ __global__ void k_update(const double* __restrict__ x, const double* __restrict_
     const double v = xv - inv_eta * gl;
     zj[i] = v;
     acc += v * v;
+    xacc += xv * xv;
   }
   const double s = block_sum<kStreamThreads>(acc, sm);
   if (threadIdx.x == 0) npart[blockIdx.x * p + j] = s;
+  if (xpart) {  // sharded: ‖x_j‖² partials for the degenerate-column rule
+    const double t = block_sum<kStreamThreads>(xacc, sm);
+    if (threadIdx.x == 0) xpart[blockIdx.x * p + j] = t;
+  }
+}
+
+// sharded: local column sums of the z² / x² chunk partials → nrm[0:p], nrm[p:2p]
+__global__ void k_norm_reduce(const double* __restrict__ npart, const double* __restrict__ xpart,
+                              int64_t nchunks, int64_t p, double* __restrict__ nrm,
+                              const Ctl* ctl) {
+  if (ctl->done) return;
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= p) return;
+  double a = 0.0, b = 0.0;
+  for (int64_t c = 0; c < nchunks; ++c) {
+    a += npart[c * p + j];
+    b += xpart[c * p + j];
+  }
+  nrm[j] = a;
+  nrm[p + j] = b;
 }
 
 // pcal_step part 2 (solver.cpp:283-305): z ·= 1/‖z‖; a column with ‖z‖ < 1e-14
 // keeps the previous column renormalized (or e_{j mod n}); non-finite ⇒ diverged.
 __global__ void k_normalize(const double* __restrict__ x, double* __restrict__ z, int64_t n,
                             int64_t ld, int64_t p, int64_t chunk, int64_t nchunks,
-                            const double* __restrict__ npart, Ctl* ctl) {
+                            const double* __restrict__ npart, const double* __restrict__ nrm,
+                            int64_t row0, int64_t n_glob, Ctl* ctl) {
   if (ctl->done) return;
   __shared__ double sm[kStreamThreads / 32];
   __shared__ double s_inv;
@@ -202,10 +224,14 @@ __global__ void k_normalize(const double* __restrict__ x, double* __restrict__ z
   const int64_t r1 = min(n, r0 + chunk);
   if (threadIdx.x == 0) {
     double nrm2 = 0.0;
-    for (int64_t c = 0; c < nchunks; ++c) nrm2 += npart[c * p + j];
-    const double nrm = sqrt(nrm2);
-    s_deg = nrm < 1e-14;
-    s_inv = 1.0 / nrm;
+    if (nrm) {
+      nrm2 = nrm[j];  // sharded: global column norm (allreduced)
+    } else {
+      for (int64_t c = 0; c < nchunks; ++c) nrm2 += npart[c * p + j];
+    }
+    const double nz = sqrt(nrm2);
+    s_deg = nz < 1e-14;
+    s_inv = 1.0 / nz;
   }
   __syncthreads();
   double* zj = z + j * ld;
@@ -220,16 +246,21 @@ __global__ void k_normalize(const double* __restrict__ x, double* __restrict__ z
   } else {
     // degenerate column: whole-column norm of the previous iterate (rare path)
     const double* xj = x + j * ld;
-    double acc = 0.0;
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) acc += xj[i] * xj[i];
-    const double pn2 = block_sum<kStreamThreads>(acc, sm);
+    double pn2;
+    if (nrm) {
+      pn2 = nrm[p + j];
+    } else {
+      double acc = 0.0;
+      for (int64_t i = threadIdx.x; i < n; i += blockDim.x) acc += xj[i] * xj[i];
+      pn2 = block_sum<kStreamThreads>(acc, sm);
+    }
     if (threadIdx.x == 0) sm[0] = sqrt(pn2);
     __syncthreads();
     const double pn = sm[0];
     for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
       double v;
       if (pn > 0.0) v = xj[i] * (1.0 / pn);
-      else v = (i == (j % n)) ? 1.0 : 0.0;
+      else v = (row0 + i == (j % n_glob)) ? 1.0 : 0.0;
       zj[i] = v;
       bad |= !isfinite(v);
     }
@@ -237,8 +268,16 @@ __global__ void k_normalize(const double* __restrict__ x, double* __restrict__ z
   if (s_deg && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&ctl->step_deg, 1);
   if (__syncthreads_or(bad) && threadIdx.x == 0) {
     ctl->step_bad = 1;
-    ctl->done = 2;
+    if (!nrm) ctl->done = 2;  // sharded: decided collectively in k_finish_eval
   }
 }
 
+}  // namespace pcal
+
+namespace pcal {
+// sharded: local failure flags appended to the allreduced column sums
+__global__ void k_flags(const Ctl* ctl, const int32_t* bad, double* out) {
+  out[0] = ctl->step_bad ? 1.0 : 0.0;
+  out[1] = *bad ? 1.0 : 0.0;
+}
 }  // namespace pcal

@@ -25,6 +25,7 @@
 #include <vector>
 
 #include "../../include/pcal_b200.h"
+#include "comm.h"
 #include "common.cuh"
 #include "gemm_types.h"
 #include "host_setup.h"
@@ -150,6 +151,7 @@ struct FinishArgs {
   int32_t model;
   int64_t p;
   int32_t mode;         // 0 = iteration record, 1 = start point (row 0), 2 = post-orth
+  const double* flags;  // sharded: allreduced {step_bad, eval_bad} counts (else null)
   double* trace;
   int32_t* bad;         // evaluation non-finite flag
   double c_xc;          // (3/π)^{1/3}
@@ -178,8 +180,13 @@ __global__ void __launch_bounds__(256) k_finish_eval(FinishArgs a, Ctl* ctl,
   const double rh = block_sum<256>(pr, sm);
   const double ex = block_sum<256>(pe, sm);
   if (threadIdx.x != 0) return;
-  const bool bad_flag = *a.bad != 0;
+  const bool bad_flag = a.flags ? a.flags[1] > 0.0 : *a.bad != 0;
   *a.bad = 0;  // reset for the next evaluation
+  if (a.flags && a.mode == 0 && a.flags[0] > 0.0) {  // some rank's pcal_step diverged
+    ctl->step_bad = 1;
+    ctl->done = 2;
+    return;
+  }
   double f;
   if (a.model == PCAL_MODEL_KOHN_SHAM) {
     f = 0.25 * f1 + 0.5 * vr + 0.25 * rh - 0.375 * a.c_xc * ex;
@@ -265,6 +272,15 @@ struct DevBuf {
 struct pcal_session {
   int device = 0;
   cudaStream_t stream = nullptr;
+  bool own_stream = true;
+  // row sharding (null comm: the whole problem on this GPU)
+  pcal::Comm* comm = nullptr;
+  int64_t n_glob = 0, row0 = 0;  // global row count, first owned row
+  int64_t gz = 0;                // grid models: owned z-planes (nz for a single GPU)
+  int64_t K_full = 0;            // dense: padded global row count (gradient GEMM K)
+  int64_t ld_max = 0;            // common leading dimension of every rank's buffers
+  std::vector<int64_t> rank_row0, rank_rows;
+  pcal::DevBuf xfull, xgath, halo, rho_gath, rank_rows_d, fkd[2], nrm, xpart;
   pcal_model_desc model{};
   pcal_config cfg{};
   int64_t n = 0, p = 0, pp = 0, ld = 0;
@@ -273,8 +289,8 @@ struct pcal_session {
   pcal::DevBuf A, g0, V, u, rho, h, tmpa, tmpb, qx, qy, qz, lx, ly, lz, spart;
   int64_t ldA = 0;
   // iteration state
-  pcal::DevBuf pair[2], dvec[2];
-  pcal::DevBuf gr, mcat, fpart, kpart, dpart, fcol, kcol, cpart, bbpart, npart, post;
+  pcal::DevBuf pair[2];
+  pcal::DevBuf gr, mcat, fpart, kpart, dpart, cpart, bbpart, npart, post;
   pcal::DevBuf orth_b, orth_l, orth_t, orth_f2;
   int32_t* bad = nullptr;
   int32_t* orth_status = nullptr;
@@ -311,6 +327,10 @@ namespace pcal {
 
 static double* Xof(pcal_session* s, int b) { return s->pair[b].p + s->ld * s->pp; }
 static double* Pof(pcal_session* s, int b) { return s->pair[b].p; }
+// packed per-column sums of an evaluation: [f | kkt² | d] (one allreduce when sharded)
+static double* Fcol(pcal_session* s, int b) { return s->fkd[b].p; }
+static double* Kcol(pcal_session* s, int b) { return s->fkd[b].p + s->p; }
+static double* Dvec(pcal_session* s, int b) { return s->fkd[b].p + 2 * s->p; }
 
 static void mark(pcal_session* s, int i) {
   if (s->pev_on) PCAL_CUDA(cudaEventRecord(s->pev[i], s->stream));
@@ -352,13 +372,26 @@ static void launch_stencil(pcal_session* s, int b, const double* u, bool ks, con
   const int64_t p = s->p;
   if (s->st_march) {
     const int TY = 8;
+    const double* hlo = nullptr;
+    const double* hhi = nullptr;
+    if (s->comm) {  // C5: exchange the boundary planes with the slab neighbours
+      const int64_t nxy = m.nx * m.ny;
+      double* h = s->halo.p;
+      const size_t cnt = (size_t)p * nxy;
+      k_pack_planes<<<dim3((unsigned)ceil_div(nxy, 256), (unsigned)p), 256, 0, s->stream>>>(
+          Xof(s, b), s->ld, nxy, s->gz, h, h + cnt, ctl);
+      launched("k_pack_planes");
+      s->comm->halo(h, h + cnt, h + 2 * cnt, h + 3 * cnt, cnt, s->stream);
+      hlo = h + 2 * cnt;
+      hhi = h + 3 * cnt;
+    }
     dim3 grid((unsigned)(m.ny / TY), (unsigned)s->st_nzc, (unsigned)p);
     dim3 block(32, TY);
     const int xp = (int)ceil_div(m.nx, 32);
 #define PCAL_MARCH(KSV, XPV)                                                                   \
   k_stencil_march<KSV, XPV, 8><<<grid, block, 0, s->stream>>>(                               \
-      Xof(s, b), u, Pof(s, b), (int)m.nx, (int)m.ny, (int)m.nz, s->ld, (int)s->st_zchunk,     \
-      s->fpart.p, s->pstride_f, s->bad, ctl)
+      Xof(s, b), u, Pof(s, b), (int)m.nx, (int)m.ny, (int)s->gz, s->ld, (int)s->st_zchunk,     \
+      s->fpart.p, s->pstride_f, s->bad, ctl, hlo, hhi)
     if (ks) {
       if (xp == 1) PCAL_MARCH(true, 1); else if (xp == 2) PCAL_MARCH(true, 2);
       else if (xp == 3) PCAL_MARCH(true, 3); else PCAL_MARCH(true, 4);
@@ -386,6 +419,14 @@ static void launch_gradient(pcal_session* s, int b, const Ctl* ctl) {
   const int64_t p = s->p;
   switch (s->model.kind) {
     case PCAL_MODEL_DENSE:
+      if (s->comm) {  // C5: every rank needs all rows of X for its row slab of A·X
+        const int R = s->comm->size;
+        s->comm->allgather(Xof(s, b), s->xgath.p, (size_t)s->ld * s->pp, s->stream);
+        k_unpack_rows<<<dim3((unsigned)ceil_div(s->ld, 256), (unsigned)s->pp, (unsigned)R), 256, 0,
+                        s->stream>>>(s->xgath.p, s->ld, s->pp, (const int64_t*)s->rank_rows_d.p, R,
+                                     s->xfull.p, s->K_full, ctl);
+        launched("k_unpack_rows");
+      }
       launch_gemm(s->grad[b], s->stream);
       break;
     case PCAL_MODEL_STENCIL: {
@@ -398,30 +439,41 @@ static void launch_gradient(pcal_session* s, int b, const Ctl* ctl) {
       const auto& m = s->model;
       k_row_sq_norms<<<nb, 256, 0, s->stream>>>(Xof(s, b), n, s->ld, p, s->rho.p, ctl);
       launched("k_row_sq_norms");
-      k_axis_transform<<<nb, 256, 0, s->stream>>>(s->rho.p, s->tmpa.p, s->qx.p, m.nx, m.nx, m.ny,
+      if (s->comm) {  // C5: the spectral solve needs the full density
+        const int R = s->comm->size;
+        s->comm->allgather(s->rho.p, s->rho_gath.p, (size_t)s->ld, s->stream);
+        k_unpack_rows<<<dim3((unsigned)ceil_div(s->ld, 256), 1, (unsigned)R), 256, 0, s->stream>>>(
+            s->rho_gath.p, s->ld, 1, (const int64_t*)s->rank_rows_d.p, R, s->rho.p, s->n_glob,
+            ctl);
+        launched("k_unpack_rows");
+      }
+      const unsigned ng = (unsigned)ceil_div(s->n_glob, 256);
+      k_axis_transform<<<ng, 256, 0, s->stream>>>(s->rho.p, s->tmpa.p, s->qx.p, m.nx, m.nx, m.ny,
                                                   m.nz, 0, 1, ctl);
       launched("k_axis_transform");
-      k_axis_transform<<<nb, 256, 0, s->stream>>>(s->tmpa.p, s->tmpb.p, s->qy.p, m.ny, m.nx, m.ny,
+      k_axis_transform<<<ng, 256, 0, s->stream>>>(s->tmpa.p, s->tmpb.p, s->qy.p, m.ny, m.nx, m.ny,
                                                   m.nz, 1, 1, ctl);
       launched("k_axis_transform");
-      k_axis_transform<<<nb, 256, 0, s->stream>>>(s->tmpb.p, s->tmpa.p, s->qz.p, m.nz, m.nx, m.ny,
+      k_axis_transform<<<ng, 256, 0, s->stream>>>(s->tmpb.p, s->tmpa.p, s->qz.p, m.nz, m.nx, m.ny,
                                                   m.nz, 2, 1, ctl);
       launched("k_axis_transform");
-      k_spectral_divide<<<nb, 256, 0, s->stream>>>(s->tmpa.p, s->lx.p, s->ly.p, s->lz.p, m.nx,
+      k_spectral_divide<<<ng, 256, 0, s->stream>>>(s->tmpa.p, s->lx.p, s->ly.p, s->lz.p, m.nx,
                                                    m.ny, m.nz, ctl);
       launched("k_spectral_divide");
-      k_axis_transform<<<nb, 256, 0, s->stream>>>(s->tmpa.p, s->tmpb.p, s->qz.p, m.nz, m.nx, m.ny,
+      k_axis_transform<<<ng, 256, 0, s->stream>>>(s->tmpa.p, s->tmpb.p, s->qz.p, m.nz, m.nx, m.ny,
                                                   m.nz, 2, 0, ctl);
       launched("k_axis_transform");
-      k_axis_transform<<<nb, 256, 0, s->stream>>>(s->tmpb.p, s->tmpa.p, s->qy.p, m.ny, m.nx, m.ny,
+      k_axis_transform<<<ng, 256, 0, s->stream>>>(s->tmpb.p, s->tmpa.p, s->qy.p, m.ny, m.nx, m.ny,
                                                   m.nz, 1, 0, ctl);
       launched("k_axis_transform");
-      k_axis_transform<<<nb, 256, 0, s->stream>>>(s->tmpa.p, s->h.p, s->qx.p, m.nx, m.nx, m.ny,
+      k_axis_transform<<<ng, 256, 0, s->stream>>>(s->tmpa.p, s->h.p, s->qx.p, m.nx, m.nx, m.ny,
                                                   m.nz, 0, 0, ctl);
       launched("k_axis_transform");
-      k_ks_potential<<<s->sp_blocks, 256, 0, s->stream>>>(s->V.p, s->rho.p, s->h.p, s->u.p, n,
-                                                          s->c_xc, s->spart.p, ctl);
+      k_ks_potential<<<s->sp_blocks, 256, 0, s->stream>>>(s->V.p, s->rho.p + s->row0,
+                                                          s->h.p + s->row0, s->u.p, n, s->c_xc,
+                                                          s->spart.p, ctl);
       launched("k_ks_potential");
+      if (s->comm) s->comm->allreduce(s->spart.p, (size_t)3 * s->sp_blocks, s->stream);
       launch_stencil(s, b, s->u.p, true, ctl);
       break;
     }
@@ -438,16 +490,23 @@ static void launch_eval(pcal_session* s, int b, int mode, const Ctl* ctl_guard) 
   launch_gradient(s, b, ctl_guard);
   mark(s, 2);
   launch_gemm(s->gram[b], st);
+  if (s->comm) s->comm->allreduce(s->gr.p, (size_t)2 * s->pp * s->pp, st);  // C1
   k_small_pxp<<<s->cp_blocks, kStreamThreads, 0, st>>>(s->gr.p, s->pp, s->p, s->mcat.p, s->pp,
                                                        s->cpart.p, ctl_guard);
   launched("k_small_pxp");
   mark(s, 3);
   launch_gemm(s->xm[b], st);
-  launch_colsums(s, s->fpart.p, s->nrb_f, s->kpart.p, s->dpart.p, s->nrb_xm, s->fcol.p,
-                 s->kcol.p, s->dvec[b].p, ctl_guard);
+  launch_colsums(s, s->fpart.p, s->nrb_f, s->kpart.p, s->dpart.p, s->nrb_xm, Fcol(s, b),
+                 Kcol(s, b), Dvec(s, b), ctl_guard);
+  if (s->comm) {  // C2 (+ the ranks' failure flags, so every rank stops together)
+    k_flags<<<1, 1, 0, st>>>(s->ctl, s->bad, s->fkd[b].p + 3 * s->p);
+    launched("k_flags");
+    s->comm->allreduce(s->fkd[b].p, (size_t)3 * s->p + 2, st);
+  }
   FinishArgs fa{};
-  fa.fcol = s->fcol.p;
-  fa.kcol = s->kcol.p;
+  fa.fcol = Fcol(s, b);
+  fa.kcol = Kcol(s, b);
+  fa.flags = s->comm ? s->fkd[b].p + 3 * s->p : nullptr;
   fa.cpart = s->cpart.p;
   fa.ncp = s->cp_blocks;
   fa.spart = s->spart.p;
@@ -483,17 +542,29 @@ static void launch_iteration(pcal_session* s, int b) {
   const int nb = 1 - b;
   mark(s, 0);
   k_bb_partials<<<s->bb_blocks, kStreamThreads, 0, st>>>(Xof(s, b), Pof(s, b), Xof(s, nb),
-                                                         Pof(s, nb), s->dvec[b].p, s->dvec[nb].p,
+                                                         Pof(s, nb), Dvec(s, b), Dvec(s, nb),
                                                          s->ld, s->p, s->bbpart.p, s->ctl);
   launched("k_bb_partials");
+  if (s->comm) s->comm->allreduce(s->bbpart.p, (size_t)3 * s->bb_blocks, st);  // C3
   k_eta<<<1, kStreamThreads, 0, st>>>(s->ctl, s->bbpart.p, s->bb_blocks);
   launched("k_eta");
   dim3 gu((unsigned)s->up_nchunks, (unsigned)s->p);
-  k_update<<<gu, kStreamThreads, 0, st>>>(Xof(s, b), Pof(s, b), s->dvec[b].p, Xof(s, nb), s->n,
-                                          s->ld, s->p, s->up_chunk, s->npart.p, s->ctl);
+  k_update<<<gu, kStreamThreads, 0, st>>>(Xof(s, b), Pof(s, b), Dvec(s, b), Xof(s, nb), s->n,
+                                          s->ld, s->p, s->up_chunk, s->npart.p,
+                                          s->comm ? s->xpart.p : nullptr, s->ctl);
   launched("k_update");
+  const double* nrm = nullptr;
+  if (s->comm) {  // C4: global column norms
+    k_norm_reduce<<<(unsigned)ceil_div(s->p, 128), 128, 0, st>>>(s->npart.p, s->xpart.p,
+                                                                 s->up_nchunks, s->p, s->nrm.p,
+                                                                 s->ctl);
+    launched("k_norm_reduce");
+    s->comm->allreduce(s->nrm.p, (size_t)2 * s->p, st);
+    nrm = s->nrm.p;
+  }
   k_normalize<<<gu, kStreamThreads, 0, st>>>(Xof(s, b), Xof(s, nb), s->n, s->ld, s->p,
-                                             s->up_chunk, s->up_nchunks, s->npart.p, s->ctl);
+                                             s->up_chunk, s->up_nchunks, s->npart.p, nrm, s->row0,
+                                             s->n_glob, s->ctl);
   launched("k_normalize");
   PCAL_CUDA(cudaGetLastError());
   mark(s, 5);
@@ -515,11 +586,11 @@ static void build_plans(pcal_session* s) {
     if (s->model.kind == PCAL_MODEL_DENSE) {
       GemmPlan& g = s->grad[b];
       const int sz = pick_size(pp);
-      plan_gemm(g, dev, sz, A_MCONTIG, EPI_GRAD, n, pp, s->ldA);
+      plan_gemm(g, dev, sz, A_MCONTIG, EPI_GRAD, n, pp, s->K_full);
       g.args.A = s->A.p;
       g.args.lda = s->ldA;
-      g.args.B = Xof(s, b);
-      g.args.ldb = ld;
+      g.args.B = s->comm ? s->xfull.p : Xof(s, b);
+      g.args.ldb = s->comm ? s->K_full : ld;
       EpiParams& e = g.args.ep;
       e.G = Pof(s, b);
       e.X = Xof(s, b);
@@ -569,14 +640,34 @@ static void build_plans(pcal_session* s) {
   }
 }
 
+// Row partition of the sharded path: grid models by z-slabs (contiguous plane
+// ranges, the first nz % R ranks get one extra plane), dense models by row
+// blocks of ⌈n/R⌉.
+static void partition(const pcal_model_desc& m, int R, int r, int64_t* row0, int64_t* rows,
+                      int64_t* z0, int64_t* nzl) {
+  if (m.kind == PCAL_MODEL_DENSE) {
+    const int64_t base = m.n / R, rem = m.n % R;
+    *row0 = r * base + std::min<int64_t>(r, rem);
+    *rows = base + (r < rem ? 1 : 0);
+    *z0 = 0;
+    *nzl = 0;
+  } else {
+    const int64_t base = m.nz / R, rem = m.nz % R;
+    *z0 = r * base + std::min<int64_t>(r, rem);
+    *nzl = base + (r < rem ? 1 : 0);
+    *row0 = *z0 * m.nx * m.ny;
+    *rows = *nzl * m.nx * m.ny;
+  }
+}
+
 static void alloc_state(pcal_session* s) {
   cudaStream_t st = s->stream;
   const int64_t n = s->n, p = s->p, pp = s->pp, ld = s->ld;
   for (int b = 0; b < 2; ++b) {
     s->pair[b].alloc((size_t)2 * ld * pp);
     s->pair[b].zero(st);
-    s->dvec[b].alloc(pp);
-    s->dvec[b].zero(st);
+    s->fkd[b].alloc((size_t)3 * p + 2);  // [f | kkt² | d | step_bad, eval_bad]
+    s->fkd[b].zero(st);
   }
   s->gr.alloc((size_t)2 * pp * pp);
   s->gr.zero(st);
@@ -590,13 +681,35 @@ static void alloc_state(pcal_session* s) {
   {
     const auto& m = s->model;
     s->st_march = m.kind != PCAL_MODEL_DENSE && m.nx <= 128 && m.ny % 8 == 0 && m.ny >= 8 &&
-                  m.nz >= 1;
+                  s->gz >= 1;
+    if (s->comm && m.kind != PCAL_MODEL_DENSE && !s->st_march)
+      throw Error(PCAL_E_UNSUPPORTED, "sharded grid models need nx <= 128 and ny % 8 == 0");
     if (s->st_march) {  // enough blocks for ≈ 8 per SM
       const int64_t tiles = (m.ny / 8) * p;
-      int64_t nzc = std::max<int64_t>(1, std::min<int64_t>(m.nz, ceil_div(8 * 148, tiles)));
-      s->st_zchunk = ceil_div(m.nz, nzc);
-      s->st_nzc = ceil_div(m.nz, s->st_zchunk);
+      int64_t nzc = std::max<int64_t>(1, std::min<int64_t>(s->gz, ceil_div(8 * 148, tiles)));
+      s->st_zchunk = ceil_div(s->gz, nzc);
+      s->st_nzc = ceil_div(s->gz, s->st_zchunk);
     }
+  }
+  if (s->comm) {
+    const int R = s->comm->size;
+    const auto& m = s->model;
+    if (m.kind == PCAL_MODEL_DENSE) {  // C5: X allgather, unpacked into global row order
+      s->xgath.alloc((size_t)R * ld * pp);
+      s->xfull.alloc((size_t)s->K_full * pp);
+      s->xfull.zero(st);
+    } else {  // C5: z-halo planes [send_lo | send_hi | recv_lo | recv_hi], p·nx·ny each
+      s->halo.alloc((size_t)4 * p * m.nx * m.ny);
+      if (m.kind == PCAL_MODEL_KOHN_SHAM) s->rho_gath.alloc((size_t)R * ld);
+    }
+    std::vector<int64_t> rr(2 * R);
+    for (int r = 0; r < R; ++r) {
+      rr[r] = s->rank_row0[r];
+      rr[R + r] = s->rank_rows[r];
+    }
+    s->rank_rows_d.alloc((size_t)2 * R);
+    PCAL_CUDA(cudaMemcpy(s->rank_rows_d.p, rr.data(), sizeof(int64_t) * 2 * R,
+                         cudaMemcpyHostToDevice));
   }
   s->nrb_f = s->model.kind == PCAL_MODEL_DENSE ? ceil_div(n, wm_grad)
              : s->st_march ? (s->model.ny / 8) * s->st_nzc
@@ -610,8 +723,6 @@ static void alloc_state(pcal_session* s) {
   s->kpart.zero(st);
   s->dpart.alloc((size_t)s->pstride_xm * p);
   s->dpart.zero(st);
-  s->fcol.alloc(p);
-  s->kcol.alloc(p);
   s->cp_blocks = (int)std::min<int64_t>(ceil_div(p * p, kStreamThreads), 256);
   s->cpart.alloc(s->cp_blocks);
   s->bb_blocks = 4 * num_sms(s->device);
@@ -620,6 +731,8 @@ static void alloc_state(pcal_session* s) {
   s->up_chunk = std::min<int64_t>(s->up_chunk, round_up(n, 256));
   s->up_nchunks = ceil_div(n, s->up_chunk);
   s->npart.alloc((size_t)s->up_nchunks * p);
+  s->xpart.alloc((size_t)s->up_nchunks * p);
+  s->nrm.alloc((size_t)2 * p);
   s->post.alloc(8);
   s->orth_b.alloc((size_t)pp * pp);
   s->orth_l.alloc((size_t)pp * pp);
@@ -643,35 +756,41 @@ static void upload_matrix(const double* src, int32_t loc, int64_t rows, int64_t 
                               st));
 }
 
+// Model data of the rows this session owns.  Sharded sessions receive the
+// LOCAL slabs: dense A rows [row0, row0+n) of all n_glob columns (ld = n),
+// G0 / V rows of the slab.
 static void upload_model(pcal_session* s) {
   const pcal_model_desc& m = s->model;
   cudaStream_t st = s->stream;
+  const int64_t n = s->n;
   if (m.kind == PCAL_MODEL_DENSE) {
     if (!m.a) throw Error(PCAL_E_PARAMETER, "dense model: a is NULL");
-    s->ldA = padded_ld(s->n);
-    s->A.alloc((size_t)s->ldA * s->ldA);
+    s->ldA = s->ld;
+    s->A.alloc((size_t)s->ldA * s->K_full);
     s->A.zero(st);
-    upload_matrix(m.a, m.location, s->n, s->n, s->A.p, s->ldA, st);
+    upload_matrix(m.a, m.location, n, s->n_glob, s->A.p, s->ldA, st);
     if (m.g0) {
       s->g0.alloc((size_t)s->ld * s->pp);
       s->g0.zero(st);
-      upload_matrix(m.g0, m.location, s->n, s->p, s->g0.p, s->ld, st);
+      upload_matrix(m.g0, m.location, n, s->p, s->g0.p, s->ld, st);
     }
   } else if (m.kind == PCAL_MODEL_STENCIL || m.kind == PCAL_MODEL_KOHN_SHAM) {
-    if (m.nx < 1 || m.ny < 1 || m.nz < 1 || m.nx * m.ny * m.nz != s->n)
+    if (m.nx < 1 || m.ny < 1 || m.nz < 1 || m.nx * m.ny * m.nz != s->n_glob)
       throw Error(PCAL_E_DIMENSION, "grid model: n must equal nx*ny*nz");
     if (!m.v) throw Error(PCAL_E_PARAMETER, "grid model: v is NULL");
-    s->V.alloc(s->n);
-    PCAL_CUDA(cudaMemcpyAsync(s->V.p, m.v, sizeof(double) * s->n,
+    s->V.alloc(s->ld);
+    s->V.zero(st);
+    PCAL_CUDA(cudaMemcpyAsync(s->V.p, m.v, sizeof(double) * n,
                               m.location == PCAL_DEVICE ? cudaMemcpyDeviceToDevice
                                                         : cudaMemcpyHostToDevice,
                               st));
     if (m.kind == PCAL_MODEL_KOHN_SHAM) {
-      s->u.alloc(s->n);
-      s->rho.alloc(s->n);
-      s->h.alloc(s->n);
-      s->tmpa.alloc(s->n);
-      s->tmpb.alloc(s->n);
+      const int64_t ng = s->n_glob;
+      s->u.alloc(s->ld);
+      s->rho.alloc(std::max(ng, s->ld));  // local ρ, then the full ρ (sharded)
+      s->h.alloc(ng);
+      s->tmpa.alloc(ng);
+      s->tmpb.alloc(ng);
       auto basis = [&](int64_t N, DevBuf& q, DevBuf& lam) {
         std::vector<double> hq((size_t)N * N), hl((size_t)N);
         pcal_fourier_basis(N, hq.data(), hl.data());
@@ -683,7 +802,7 @@ static void upload_model(pcal_session* s) {
       basis(m.nx, s->qx, s->lx);
       basis(m.ny, s->qy, s->ly);
       basis(m.nz, s->qz, s->lz);
-      s->sp_blocks = (int)std::min<int64_t>(ceil_div(s->n, 256), 4 * 148);
+      s->sp_blocks = 4 * 148;  // fixed: the partial array is allreduced elementwise
       s->spart.alloc((size_t)3 * s->sp_blocks);
       s->c_xc = std::cbrt(3.0 / 3.14159265358979323846);
     } else {
@@ -757,7 +876,7 @@ pcal_session::~pcal_session() {
   if (bad) cudaFree(bad);
   if (ctl) cudaFree(ctl);
   if (h_ctl) cudaFreeHost(h_ctl);
-  if (stream) cudaStreamDestroy(stream);
+  if (stream && own_stream) cudaStreamDestroy(stream);
 }
 
 using namespace pcal;
@@ -782,7 +901,8 @@ int guarded(F&& f) {
 }
 
 void session_create(const pcal_model_desc* model, const pcal_config* config, const double* x0,
-                    int32_t x0_loc, pcal_session** out, pcal_category_timers* timers) {
+                    int32_t x0_loc, pcal_session** out, pcal_category_timers* timers,
+                    Comm* comm = nullptr, cudaStream_t shared_stream = nullptr) {
   if (!model || !config || !x0 || !out) throw Error(PCAL_E_PARAMETER, "NULL argument");
   validate(config);
   if (model->n < 1 || model->p < 1) throw Error(PCAL_E_DIMENSION, "model: n, p must be positive");
@@ -797,15 +917,40 @@ void session_create(const pcal_model_desc* model, const pcal_config* config, con
   s->model = *model;
   s->cfg = *config;
   s->timers = timers;
-  s->n = model->n;
+  s->comm = comm;
+  s->n_glob = model->n;
   s->p = model->p;
   s->pp = padded_p(s->p);
-  s->ld = padded_ld(s->n);
+  const int R = comm ? comm->size : 1;
+  const int rk = comm ? comm->rank : 0;
+  if (model->kind != PCAL_MODEL_DENSE && (model->nz < R))
+    throw Error(PCAL_E_PARAMETER, "fewer z-planes than ranks");
+  if (model->kind == PCAL_MODEL_DENSE && model->n < R)
+    throw Error(PCAL_E_PARAMETER, "fewer rows than ranks");
+  int64_t maxrows = 0;
+  s->rank_row0.resize(R);
+  s->rank_rows.resize(R);
+  for (int r = 0; r < R; ++r) {
+    int64_t z0, nzl;
+    partition(*model, R, r, &s->rank_row0[r], &s->rank_rows[r], &z0, &nzl);
+    maxrows = std::max(maxrows, s->rank_rows[r]);
+    if (r == rk) s->gz = nzl ? nzl : model->nz;
+  }
+  s->row0 = s->rank_row0[rk];
+  s->n = s->rank_rows[rk];
+  s->ld_max = padded_ld(maxrows);
+  s->ld = comm ? s->ld_max : padded_ld(s->n);
+  s->K_full = padded_ld(s->n_glob);
   s->beta = config->beta >= 0.0 ? config->beta : 1.0;                  // solver.cpp:120-125
   s->eta0 = config->eta0 > 0.0 ? clamp_eta_h(config, config->eta0)     // solver.cpp:99-102
                                : clamp_eta_h(config, model->s + 2.0 * s->beta);
   LaunchScope ls(&s->launches);
-  PCAL_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+  if (shared_stream) {
+    s->stream = shared_stream;
+    s->own_stream = false;
+  } else {
+    PCAL_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+  }
   for (auto& e : s->pev) PCAL_CUDA(cudaEventCreate(&e));
   s->pev_on = timers != nullptr;
   alloc_state(s.get());
@@ -818,7 +963,8 @@ void session_create(const pcal_model_desc* model, const pcal_config* config, con
   launch_eval(s.get(), 0, 1, s->ctl);  // eval_iterate(X0) + record(0) (solver.cpp:363-365)
   PCAL_CUDA(cudaGetLastError());
   s->next_k = 0;
-  s->use_graphs = timers == nullptr;
+  // graphs: not for timers (events between kernels) nor emulated ranks (host barriers)
+  s->use_graphs = timers == nullptr && !(comm && comm->emulated());
   if (s->use_graphs) capture_graphs(s.get());
   *out = s.release();
 }
@@ -845,6 +991,13 @@ void session_run(pcal_session* s, int64_t iters) {
       s->launched++;
     }
     remaining -= nb;
+    if (s->comm) {  // sharded: every rank must stop after the same batch (collectives)
+      PCAL_CUDA(cudaMemcpyAsync(&s->h_ctl->done, &s->ctl->done, sizeof(int32_t),
+                                cudaMemcpyDeviceToHost, s->stream));
+      PCAL_CUDA(cudaStreamSynchronize(s->stream));
+      if (s->h_ctl->done) break;
+      continue;
+    }
     // poll `done` of the previous batch without stalling the device queue
     if (pending) {
       PCAL_CUDA(cudaEventSynchronize(polled));
@@ -885,6 +1038,7 @@ bool orthonormalize_dev(pcal_session* s, const double* x, double* q, double* scr
     gp.args.ep.n_store = pp;
     gp.args.ctl = nullptr;
     launch_gemm(gp, st);
+    if (s->comm) s->comm->allreduce(s->orth_b.p, (size_t)pp * pp, st);  // sharded Gram
   };
   auto mul_t = [&](const double* a, double* out) {  // out = a · T
     mp.args.A = a;
@@ -926,10 +1080,29 @@ bool orthonormalize_dev(pcal_session* s, const double* x, double* q, double* scr
     if (chol_ok) mul_t(scratch, q);  // Q = Q1·L2⁻ᵀ
   }
   if (!chol_ok) {  // mgs2(x) fallback (kernels.cpp:254,258)
-    PCAL_CUDA(cudaMemcpy2DAsync(q, sizeof(double) * ld, x, sizeof(double) * ld,
-                                sizeof(double) * ld, p, cudaMemcpyDeviceToDevice, st));
-    k_mgs2<<<1, 1024, 0, st>>>(q, n, ld, p, s->orth_f2.p, s->orth_status);
-    launched("k_mgs2");
+    if (s->comm) {
+      // sharded: MGS2 is inherently sequential over columns — gather X, run it
+      // redundantly on every rank, keep the local rows (rank-deficient path only)
+      const int R = s->comm->size;
+      const int64_t kf = s->K_full;
+      DevBuf gath, full;
+      gath.alloc((size_t)R * ld * s->pp);
+      full.alloc((size_t)kf * s->pp);
+      full.zero(st);
+      s->comm->allgather(x, gath.p, (size_t)ld * s->pp, st);
+      k_unpack_rows<<<dim3((unsigned)ceil_div(ld, 256), (unsigned)s->pp, (unsigned)R), 256, 0, st>>>(
+          gath.p, ld, s->pp, (const int64_t*)s->rank_rows_d.p, R, full.p, kf, nullptr);
+      launched("k_unpack_rows");
+      k_mgs2<<<1, 1024, 0, st>>>(full.p, s->n_glob, kf, p, s->orth_f2.p, s->orth_status);
+      launched("k_mgs2");
+      PCAL_CUDA(cudaMemcpy2DAsync(q, sizeof(double) * ld, full.p + s->row0, sizeof(double) * kf,
+                                  sizeof(double) * n, p, cudaMemcpyDeviceToDevice, st));
+    } else {
+      PCAL_CUDA(cudaMemcpy2DAsync(q, sizeof(double) * ld, x, sizeof(double) * ld,
+                                  sizeof(double) * ld, p, cudaMemcpyDeviceToDevice, st));
+      k_mgs2<<<1, 1024, 0, st>>>(q, n, ld, p, s->orth_f2.p, s->orth_status);
+      launched("k_mgs2");
+    }
     PCAL_CUDA(cudaMemcpyAsync(&ok, s->orth_status, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     PCAL_CUDA(cudaStreamSynchronize(st));
     if (!ok) return false;
@@ -1244,6 +1417,8 @@ std::unique_ptr<pcal_session> make_aux(int64_t n, int64_t p, int device) {
   s->p = p;
   s->pp = padded_p(p);
   s->ld = padded_ld(n);
+  s->n_glob = n;
+  s->K_full = s->ld;
   alloc_state(s.get());
   init_ctl(s.get());
   return s;
@@ -1408,11 +1583,11 @@ int pcal_evaluate(const pcal_model_desc* model, const double* x, double* f, doub
     k_zero_i32<<<1, 1, 0, s->stream>>>(s->bad, nullptr);
     launched("k_zero_i32");
     launch_gradient(s.get(), 0, nullptr);
-    launch_colsums(s.get(), s->fpart.p, s->nrb_f, nullptr, nullptr, 0, s->fcol.p, nullptr, nullptr,
+    launch_colsums(s.get(), s->fpart.p, s->nrb_f, nullptr, nullptr, 0, Fcol(s.get(), 0), nullptr, nullptr,
                    nullptr);
     FinishArgs fa{};
-    fa.fcol = s->fcol.p;
-    fa.kcol = s->kcol.p;
+    fa.fcol = Fcol(s.get(), 0);
+    fa.kcol = Kcol(s.get(), 0);
     fa.cpart = s->cpart.p;
     fa.ncp = 0;
     fa.spart = s->spart.p;
@@ -1446,13 +1621,13 @@ int pcal_pcal_step(const double* x, const double* grad_l, int64_t n, int64_t p, 
     s->h_ctl->done = 0;
     PCAL_CUDA(cudaMemcpyAsync(s->ctl, s->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, s->stream));
     dim3 gu((unsigned)s->up_nchunks, (unsigned)p);
-    k_update<<<gu, kStreamThreads, 0, s->stream>>>(Xof(s.get(), 0), Pof(s.get(), 0), s->dvec[0].p,
+    k_update<<<gu, kStreamThreads, 0, s->stream>>>(Xof(s.get(), 0), Pof(s.get(), 0), Dvec(s.get(), 0),
                                                    Xof(s.get(), 1), n, s->ld, p, s->up_chunk,
-                                                   s->npart.p, s->ctl);
+                                                   s->npart.p, nullptr, s->ctl);
     launched("k_update");
     k_normalize<<<gu, kStreamThreads, 0, s->stream>>>(Xof(s.get(), 0), Xof(s.get(), 1), n, s->ld,
                                                       p, s->up_chunk, s->up_nchunks, s->npart.p,
-                                                      s->ctl);
+                                                      nullptr, 0, n, s->ctl);
     launched("k_normalize");
     PCAL_CUDA(cudaGetLastError());
     copy_out(s.get(), Xof(s.get(), 1), out);
@@ -1541,6 +1716,162 @@ int pcal_spectral_norm_estimate(const double* a, int64_t n, uint64_t seed, doubl
     }
     PCAL_CUDA(cudaGetLastError());
     *out = std::min(est, fro);
+  });
+}
+
+}  // extern "C"
+
+// ==============================================================================
+// Row-sharded sessions (multi-GPU) and the single-GPU loopback emulation
+// ==============================================================================
+struct pcal_comm {
+  pcal::Comm* c = nullptr;
+  ~pcal_comm() { delete c; }
+};
+
+extern "C" {
+
+int pcal_partition(const pcal_model_desc* m, int32_t nranks, int32_t rank, int64_t* row0,
+                   int64_t* nrows) {
+  return guarded([&] {
+    if (!m || nranks < 1 || rank < 0 || rank >= nranks) throw Error(PCAL_E_PARAMETER, "bad rank");
+    int64_t z0, nzl;
+    partition(*m, nranks, rank, row0, nrows, &z0, &nzl);
+  });
+}
+
+int pcal_nccl_unique_id(void* out) {
+  return guarded([&] { nccl_unique_id(out); });
+}
+
+int pcal_comm_create_nccl(int32_t nranks, int32_t rank, const void* uid, int32_t device,
+                          pcal_comm** out) {
+  return guarded([&] {
+    auto c = std::make_unique<pcal_comm>();
+    c->c = make_nccl_comm(nranks, rank, uid, device);
+    *out = c.release();
+  });
+}
+
+void pcal_comm_destroy(pcal_comm* c) { delete c; }
+
+int pcal_session_create_sharded(const pcal_model_desc* local_model, const pcal_config* config,
+                                const double* x0_local, int32_t x0_location, pcal_comm* comm,
+                                pcal_session** out) {
+  return guarded([&] {
+    session_create(local_model, config, x0_local, x0_location, out, nullptr,
+                   comm ? comm->c : nullptr);
+  });
+}
+
+int pcal_solve_sharded(const pcal_model_desc* local_model, const pcal_config* config,
+                       const double* x0_local, int32_t x0_location, pcal_comm* comm,
+                       pcal_report* report) {
+  return guarded([&] {
+    pcal_session* s = nullptr;
+    session_create(local_model, config, x0_local, x0_location, &s, nullptr,
+                   comm ? comm->c : nullptr);
+    std::unique_ptr<pcal_session> guard(s);
+    session_run(s, config->max_iter);
+    session_finish(s, report);
+  });
+}
+
+// R emulated ranks on ONE GPU: each rank is a host thread with its own session
+// on the group's shared stream; the collectives meet at host barriers.  The
+// global report gets rank 0's trace and scalars and every rank's rows of X.
+int pcal_solve_emulated(const pcal_model_desc* model, const pcal_config* config, const double* x0,
+                        int32_t nranks, pcal_report* report) {
+  return guarded([&] {
+    if (!model || !config || !x0 || !report) throw Error(PCAL_E_PARAMETER, "NULL argument");
+    if (model->location != PCAL_HOST) throw Error(PCAL_E_PARAMETER, "emulation takes host data");
+    if (nranks < 1) throw Error(PCAL_E_PARAMETER, "nranks must be >= 1");
+    validate(config);
+    PCAL_CUDA(cudaSetDevice(config->device));
+    const int R = nranks;
+    const int64_t n = model->n, p = model->p;
+    LoopbackGroup group(R);
+    std::vector<std::unique_ptr<LoopbackComm>> comms;
+    std::vector<int64_t> r0(R), rows(R);
+    for (int r = 0; r < R; ++r) {
+      comms.emplace_back(new LoopbackComm(&group, r));
+      int64_t z0, nzl;
+      partition(*model, R, r, &r0[r], &rows[r], &z0, &nzl);
+      if (rows[r] < 1) throw Error(PCAL_E_PARAMETER, "a rank would own no rows");
+    }
+    std::vector<std::vector<double>> a_loc(R), g_loc(R), x_loc(R), stop_loc(R), fin_loc(R);
+    std::vector<pcal_report> reps(R);
+    std::vector<std::vector<double>> traces(R);
+    std::vector<int> rcs(R, PCAL_OK);
+    std::vector<std::string> errs(R);
+    auto slice = [&](const double* src, int64_t ld_src, int64_t r, int64_t cols,
+                     std::vector<double>& dst) {
+      dst.resize((size_t)rows[r] * cols);
+      for (int64_t c = 0; c < cols; ++c)
+        std::memcpy(dst.data() + c * rows[r], src + r0[r] + c * ld_src, sizeof(double) * rows[r]);
+    };
+    for (int r = 0; r < R; ++r) {
+      if (model->kind == PCAL_MODEL_DENSE) {
+        slice(model->a, n, r, n, a_loc[r]);
+        if (model->g0) slice(model->g0, n, r, p, g_loc[r]);
+      }
+      slice(x0, n, r, p, x_loc[r]);
+      stop_loc[r].resize((size_t)rows[r] * p);
+      fin_loc[r].resize((size_t)rows[r] * p);
+      traces[r].resize((size_t)(config->max_iter + 1) * kTraceCols);
+      reps[r] = pcal_report{};
+      reps[r].trace = traces[r].data();
+      reps[r].trace_capacity = config->max_iter + 1;
+      reps[r].stop_x = stop_loc[r].data();
+      reps[r].final_x = fin_loc[r].data();
+    }
+    std::vector<std::thread> th;
+    for (int r = 0; r < R; ++r)
+      th.emplace_back([&, r] {
+        rcs[r] = guarded([&] {
+          PCAL_CUDA(cudaSetDevice(config->device));
+          pcal_model_desc m = *model;
+          if (m.kind == PCAL_MODEL_DENSE) {
+            m.a = a_loc[r].data();
+            m.g0 = model->g0 ? g_loc[r].data() : nullptr;
+          } else {
+            m.v = model->v + r0[r];
+          }
+          pcal_session* s = nullptr;
+          session_create(&m, config, x_loc[r].data(), PCAL_HOST, &s, nullptr, comms[r].get(),
+                         group.stream);
+          std::unique_ptr<pcal_session> guard(s);
+          session_run(s, config->max_iter);
+          session_finish(s, &reps[r]);
+        });
+        if (rcs[r] != PCAL_OK) errs[r] = g_last_error;
+      });
+    for (auto& t : th) t.join();
+    for (int r = 0; r < R; ++r)
+      if (rcs[r] != PCAL_OK) throw Error(rcs[r], "rank " + std::to_string(r) + ": " + errs[r]);
+    // merge: replicated scalars from rank 0, rows from every rank
+    double* trace = report->trace;
+    const int64_t cap = report->trace_capacity;
+    double* stop_x = report->stop_x;
+    double* final_x = report->final_x;
+    *report = reps[0];
+    report->trace = trace;
+    report->trace_capacity = cap;
+    report->stop_x = stop_x;
+    report->final_x = final_x;
+    if (trace) {
+      if (cap < reps[0].trace_len) throw Error(PCAL_E_PARAMETER, "report trace capacity too small");
+      std::memcpy(trace, traces[0].data(), sizeof(double) * reps[0].trace_len * kTraceCols);
+    }
+    for (int r = 0; r < R; ++r)
+      for (int64_t c = 0; c < p; ++c) {
+        if (stop_x && reps[0].has_x)
+          std::memcpy(stop_x + r0[r] + c * n, stop_loc[r].data() + c * rows[r],
+                      sizeof(double) * rows[r]);
+        if (final_x && reps[0].has_x)
+          std::memcpy(final_x + r0[r] + c * n, fin_loc[r].data() + c * rows[r],
+                      sizeof(double) * rows[r]);
+      }
   });
 }
 

@@ -1,0 +1,95 @@
+"""GPU: the row-sharded multi-GPU algorithm, with R ranks
+emulated on the one available GPU (loopback collectives, host barriers).
+Every rank runs exactly the kernels and collectives of the NCCL path; results
+must match the single-GPU solve to the parity tolerances (only the summation
+order of the allreduced partials differs)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+TINY = np.finfo(float).tiny
+INIT_SALT = 0x1235713
+
+
+def close(a, b, tol, floor=0.0):
+    a, b = np.asarray(a, float), np.asarray(b, float)
+    return np.all(np.abs(a - b) <= tol * np.abs(b) + floor)
+
+
+def check_pair(r1, rr, window=25):
+    assert rr.status == r1.status
+    assert rr.trace.shape[0] == r1.trace.shape[0]
+    w = min(window, r1.trace.shape[0])
+    assert close(rr.trace[:w, 1], r1.trace[:w, 1], 1e-9)
+    assert close(rr.trace[:w, 2], r1.trace[:w, 2], 1e-9)
+    assert close(rr.trace[:w, 4], r1.trace[:w, 4], 1e-9, 1e-14)
+    assert close(rr.trace[:w, 5], r1.trace[:w, 5], 1e-9)
+    if r1.final_post_orth is not None:
+        assert rr.final_post_orth is not None
+        assert abs(rr.final_post_orth.fval - r1.final_post_orth.fval) <= 1e-9 * abs(r1.final_post_orth.fval)
+        assert rr.final_post_orth.feas <= 1e-12
+        assert np.abs(np.linalg.norm(rr.final_x, axis=0) - 1.0).max() <= 1e-12
+
+
+@pytest.mark.parametrize("R", [1, 2, 3, 4])
+def test_dense_sharded_matches_single_gpu(pcal, orc, R):
+    n, p = 1000, 20
+    a = pcal.gen_dense_operator(n, 1)
+    x0 = orc.initial_point_qr(n, p, 1 ^ INIT_SALT)
+    m = pcal.QuadraticModel(a, p, 44.26282919872377)
+    cfg = pcal.SolverConfig(tol_rel_kkt=TINY, max_iter=60)
+    r1 = pcal.solve(m, cfg, x0)
+    rr = pcal.solve_emulated(m, cfg, x0, R)
+    check_pair(r1, rr, window=40)
+
+
+@pytest.mark.parametrize("R", [2, 3, 4])
+def test_stencil_sharded_matches_single_gpu(pcal, orc, R):
+    grid = (16, 16, 12)
+    n, p = 16 * 16 * 12, 8
+    v = orc.random_uniform(n, 1)
+    x0 = orc.initial_point_qr(n, p, 7)
+    m = pcal.StencilModel(grid, v, p, 12.0 + v.max())
+    cfg = pcal.SolverConfig(tol_rel_kkt=TINY, max_iter=50)
+    check_pair(pcal.solve(m, cfg, x0), pcal.solve_emulated(m, cfg, x0, R))
+
+
+@pytest.mark.parametrize("R", [2, 3])
+def test_kohn_sham_sharded_matches_single_gpu(pcal, orc, R):
+    grid = (16, 8, 10)
+    n, p = 16 * 8 * 10, 6
+    v = -orc.random_uniform(n, 2)
+    x0 = orc.initial_point_qr(n, p, 9)
+    m = pcal.KohnShamModel(grid, v, p, 6.0 + np.abs(v).max())
+    cfg = pcal.SolverConfig(tol_rel_kkt=TINY, max_iter=40)
+    check_pair(pcal.solve(m, cfg, x0), pcal.solve_emulated(m, cfg, x0, R))
+
+
+def test_sharded_convergence_stops_every_rank_together(pcal, orc):
+    r = orc.random_normal(40, 40, 24)
+    a = np.asfortranarray(0.5 * (r + r.T))
+    x0 = orc.initial_point_qr(40, 5, 25)
+    m = pcal.QuadraticModel(a, 5, orc.spectral_norm_estimate(a, 0x73706563))
+    r1 = pcal.solve(m, pcal.SolverConfig(), x0)
+    r3 = pcal.solve_emulated(m, pcal.SolverConfig(), x0, 3)
+    assert r1.status == r3.status == "converged"
+    assert abs(r1.iterations - r3.iterations) <= 3
+    assert abs(r3.final_post_orth.fval - r1.final_post_orth.fval) <= 1e-9 * abs(r1.final_post_orth.fval)
+
+
+def test_sharded_evaluation_error_is_collective(pcal):
+    a = np.eye(64)
+    a[40, 40] = np.inf  # only rank 1 of 2 sees the bad row
+    x = np.zeros((64, 2)); x[0, 0] = x[1, 1] = 1.0
+    rep = pcal.solve_emulated(pcal.QuadraticModel(a, 2, 1.0), pcal.SolverConfig(), x, 2)
+    assert rep.status == "diverged" and rep.trace.shape[0] == 0
+
+
+def test_partition_tiles_rows(pcal):
+    m = pcal.StencilModel((16, 16, 12), np.zeros(16 * 16 * 12), 4, 1.0)
+    for R in (1, 2, 3, 5, 12):
+        parts = [pcal.partition(m, R, r) for r in range(R)]
+        assert parts[0][0] == 0
+        for (a0, an), (b0, _) in zip(parts, parts[1:]):
+            assert a0 + an == b0 and an % 256 == 0  # whole z-planes
+        assert parts[-1][0] + parts[-1][1] == m.n
