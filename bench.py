@@ -19,8 +19,9 @@ dense trace minimization, n=16384, p=128, FP64 — BASELINE configs[1]).
   cpu_baseline : the UNMODIFIED reference solve() (oracle/_ref) on the host
           cores, per-iteration time from its own trace clock, bounded sample.
 --impl reference times that CPU implementation alone (rank 0; others exit 0).
-N > 1: one process per GPU (torchrun), independent replicas of the instance
-(row sharding with NCCL is the next step); value = N·K / max time.
+N > 1: one process per GPU (torchrun); the instance is ROW-SHARDED over the
+ranks (z-slabs / row blocks, NCCL collectives): strong scaling,
+value = K / max-over-ranks time.
 """
 from __future__ import annotations
 
@@ -192,7 +193,7 @@ def run_reference_arm(args):
     line = {"metric": "PCAL iterations/sec", "impl": "reference", "value": rate,
             "unit": "iterations/s", "n_gpus": args.gpus, "steps": info["iters"],
             "warmup": 1, "ms_per_step": 1e3 / rate, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"config {inst.cfg}", "n": inst.n, "p": inst.p,
                        "kind": inst.kind},
             "cpu_baseline": {"value": rate, "unit": "iterations/s", "cores": info["cores"],
@@ -212,6 +213,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the NCCL row-sharded path even on one GPU (testing)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
@@ -234,13 +237,33 @@ def main():
         a_t, a_pin = pinned_f64(n, n)
     inst = make_instance(args.config, P, threads=hostthreads, a_out=a_pin, device=dev)
     x0 = P.initial_point(inst.n, inst.p, inst.seed ^ INIT_SALT, device=dev)
-    model = inst.model(P)
     prof_iters = 10
     cfg = P.SolverConfig(tol_rel_kkt=TINY, max_iter=W + K + prof_iters + 2, final_orth=False,
                          device=dev)
+    comm = None
+    if world > 1 or args.sharded:
+        # row sharding over NCCL: this rank's slab of the instance
+        obj = [P.nccl_unique_id() if rank == 0 else None]
+        if world > 1:
+            import torch.distributed as dist
+            dist.broadcast_object_list(obj, src=0)
+        comm = P.Comm(world, rank, obj[0], dev)
+        gm = inst.model(P)
+        r0, nr = P.partition(gm, world, rank)
+        x0_loc = np.asfortranarray(x0[r0:r0 + nr])
+        if inst.kind == "dense":
+            a_loc = np.asfortranarray(inst.a[r0:r0 + nr, :])
+            model = P.QuadraticModel(a_loc, inst.p, inst.s, n=inst.n)
+        elif inst.kind == "stencil":
+            model = P.StencilModel(inst.grid, inst.v[r0:r0 + nr], inst.p, inst.s)
+        else:
+            model = P.KohnShamModel(inst.grid, inst.v[r0:r0 + nr], inst.p, inst.s)
+        ses = P.ShardedSession(model, cfg, x0_loc, comm, nr)
+    else:
+        model = inst.model(P)
+        ses = P.Session(model, cfg, x0)
 
     # ---- value: device-resident iterations, CUDA events on the session stream
-    ses = P.Session(model, cfg, x0)
     stream = torch.cuda.ExternalStream(ses.stream, device=dev)
     ses.run(W)
     ses.sync()
@@ -264,7 +287,9 @@ def main():
     ses.close()
     assert rep.status == "max_iter", rep.status
     ms_per = ms / K
-    value = world * K / (ms * 1e-3)
+    # sharded: the ranks advance ONE iteration of the problem together (strong
+    # scaling); N = 1 is the same formula
+    value = K / (ms * 1e-3)
 
     # ---- roofline of the dominant kernel + whole-iteration roofline
     n, p = inst.n, inst.p
@@ -302,16 +327,20 @@ def main():
     if not args.no_e2e:
         iters = inst.iters
         x0h = np.asfortranarray(x0)
-        a_host = inst.a if inst.kind == "dense" else None
-        m_host = inst.model(P, a=a_host)
         barrier(world)
         t0 = time.perf_counter()
-        r = P.solve(m_host, P.SolverConfig(tol_rel_kkt=TINY, max_iter=iters, device=dev), x0h)
+        if comm is not None:
+            r = P.solve_sharded(model, P.SolverConfig(tol_rel_kkt=TINY, max_iter=iters, device=dev),
+                                x0_loc, comm, nr)
+        else:
+            a_host = inst.a if inst.kind == "dense" else None
+            r = P.solve(inst.model(P, a=a_host),
+                        P.SolverConfig(tol_rel_kkt=TINY, max_iter=iters, device=dev), x0h)
         wall = time.perf_counter() - t0
         wall = max_over_ranks(wall, world)
         h2d = inst.op_bytes() + 8 * n * p
         d2h = 8 * 2 * n * p + 8 * 7 * (iters + 1)
-        e2e = {"value": world * r.iterations / wall, "unit": "iterations/s",
+        e2e = {"value": r.iterations / wall, "unit": "iterations/s",
                "h2d_bytes_per_step": h2d / r.iterations, "d2h_bytes_per_step": d2h / r.iterations,
                "iterations": r.iterations, "wall_s": wall, "status": r.status,
                "final_post_feas": r.final_post_orth.feas if r.final_post_orth else None,
@@ -337,10 +366,12 @@ def main():
         line = {
             "metric": "PCAL iterations/sec", "value": value, "unit": "iterations/s",
             "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": ms_per,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reference RNG stream, seed 1; no dataset)",
             "config": {"workload": wl, "n": n, "p": p, "kind": inst.kind, "s": inst.s,
-                       "parallelism": "single-gpu" if world == 1 else f"replicas x{world}",
+                       "parallelism": "single-gpu" if comm is None
+                       else f"row-sharded x{world} (NCCL: Gram/partials allreduce, "
+                            f"{'X allgather' if inst.kind == 'dense' else 'z-halo planes'})",
                        "l2": ("inputs larger than L2: A = %.1f GiB streamed every iteration"
                               % (inst.op_bytes() / 2 ** 30)) if inst.kind == "dense"
                        else "working set (X, P, X_prev, P_prev) larger than L2",
@@ -349,6 +380,8 @@ def main():
             "e2e": e2e, "clocks": clk.summary(), "gpu_launches": launches,
         }
         print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()

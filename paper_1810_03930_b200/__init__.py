@@ -590,6 +590,18 @@ def solve_emulated(model: _ModelBase, config: SolverConfig, x0, nranks: int) -> 
     return _report_from(rep, trace, stop_x, final_x)
 
 
+def solve_sharded(model: _ModelBase, config: SolverConfig, x0_local, comm: "Comm",
+                  n_local: int) -> RunReport:
+    """Row-sharded pcal_solve on this rank (host buffers: local slabs in, local rows out)."""
+    cm, keep = model._c()
+    cc = config._c()
+    x0_local = _f64(x0_local)
+    rep, trace, stop_x, final_x = _new_report(n_local, model.p, config.max_iter)
+    _check(lib().pcal_solve_sharded(C.byref(cm), C.byref(cc), _ptr(x0_local), HOST, comm._h,
+                                    C.byref(rep)))
+    return _report_from(rep, trace, stop_x, final_x)
+
+
 def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     _check(lib().pcal_nccl_unique_id(buf))

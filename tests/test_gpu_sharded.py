@@ -93,3 +93,30 @@ def test_partition_tiles_rows(pcal):
         for (a0, an), (b0, _) in zip(parts, parts[1:]):
             assert a0 + an == b0 and an % 256 == 0  # whole z-planes
         assert parts[-1][0] + parts[-1][1] == m.n
+
+
+@pytest.mark.parametrize("kind", ["dense", "stencil"])
+def test_nccl_single_rank_session(pcal, orc, kind):
+    """The NCCL communicator path (graph-captured ncclAllReduce / AllGather /
+    Send-Recv halos) with one rank must reproduce the single-GPU solve."""
+    try:
+        uid = pcal.nccl_unique_id()
+    except Exception as e:  # pragma: no cover
+        pytest.skip(f"NCCL unavailable: {e}")
+    comm = pcal.Comm(1, 0, uid, 0)
+    if kind == "dense":
+        n, p = 1000, 20
+        a = pcal.gen_dense_operator(n, 1)
+        m = pcal.QuadraticModel(a, p, 44.26282919872377)
+    else:
+        n, p = 16 * 16 * 12, 8
+        m = pcal.StencilModel((16, 16, 12), orc.random_uniform(n, 1), p, 13.0)
+    x0 = orc.initial_point_qr(n, p, 5)
+    cfg = pcal.SolverConfig(tol_rel_kkt=TINY, max_iter=40)
+    r1 = pcal.solve(m, cfg, x0)
+    with pcal.ShardedSession(m, cfg, x0, comm, n) as ses:
+        assert ses.kernels_per_iteration > 0  # graph captured with NCCL calls inside
+        ses.run(40)
+        rs = ses.finish()
+    comm.close()
+    check_pair(r1, rs, window=40)
