@@ -26,7 +26,7 @@ int num_sms(int device) {
 
 CfgInfo cfg_info(int size) {
   switch (size) {
-    case CFG_BIG: return {128, 128, 64, CfgBig<A_MCONTIG>::BK};
+    case CFG_BIG: return {128, 128, CfgBig<A_MCONTIG>::WM, CfgBig<A_MCONTIG>::BK};
     case CFG_MID: return {64, 64, 32, CfgMid<A_MCONTIG>::BK};
     default: return {64, 32, 32, CfgSmall<A_MCONTIG>::BK};
   }

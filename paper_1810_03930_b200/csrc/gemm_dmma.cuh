@@ -401,14 +401,20 @@ __global__ void __launch_bounds__(Cfg::THREADS + 128, 1) gemm_streamk(GemmArgs g
   // with 8 consumer warps, consumers take 232 registers and the producer
   // group 40 (8·32·232 + 4·32·40 ≤ 64K).
   if (warp >= Cfg::WARPS) {
-    if constexpr (Cfg::WARPS == 8) asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::);
+    if constexpr (Cfg::WARPS >= 8) asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::);
     if (warp == Cfg::WARPS) {
       produce<Cfg>(g, As, Bs, full, empty, u0, u1, lane);
       cp_async_wait<0>();
     }
     return;
   }
-  if constexpr (Cfg::WARPS == 8) asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::);
+  if constexpr (Cfg::WARPS >= 8) {
+    // (64K − 128·40) / consumer threads, rounded down to a multiple of 8, ≤ 232
+    constexpr int R = (65536 - 128 * 40) / Cfg::THREADS / 8 * 8 > 232
+                          ? 232
+                          : (65536 - 128 * 40) / Cfg::THREADS / 8 * 8;
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(R));
+  }
   const int wm = warp / Cfg::WARPS_N, wn = warp % Cfg::WARPS_N;
 
   double acc[Cfg::MT][Cfg::NT][2];
