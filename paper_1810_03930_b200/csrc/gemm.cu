@@ -77,11 +77,22 @@ void plan_gemm(GemmPlan& pl, int device, int size, int amode, int epi, int64_t M
   if (units < grid) grid = (int)std::max<int64_t>(1, units);
   // Enough tiles for every SM: data-parallel whole tiles (no partials, no
   // fixup); otherwise stream-K so tall-skinny / few-tile products fill the chip.
+  // Cost model in k-iterations on the busiest CTA: data-parallel costs
+  // ⌈T/G⌉·ki; stream-K costs ⌈T·ki/G⌉ plus ≈4 k-iterations of fixup (partial
+  // stores, the extra launch, the re-read).
   int64_t upc = 0;
-  if (ntiles >= grid) {
-    const int64_t w = ceil_div(ntiles, grid);
-    upc = w * ki;
-    grid = (int)ceil_div(ntiles, w);
+  {
+    const int64_t g0 = grid;
+    const int64_t dp_cost = ceil_div(ntiles, g0) * ki;
+    const int64_t sk_cost = ceil_div(units, g0) + 4;
+    if (dp_cost <= sk_cost) {
+      const int64_t w = ceil_div(ntiles, g0);
+      upc = w * ki;
+      grid = (int)ceil_div(ntiles, w);
+    } else if (epi != EPI_STORE && grid > 4 * (int64_t)ntiles) {
+      // fused epilogues are fixed up one tile per CTA: keep ≤ 4 partials per tile
+      grid = (int)(4 * (int64_t)ntiles);
+    }
   }
   std::vector<int32_t> split(ntiles, -1);
   std::vector<FixupTask> tasks;

@@ -474,6 +474,7 @@ __global__ void __launch_bounds__(Cfg::THREADS) gemm_fixup(GemmArgs g, const Fix
 #pragma unroll
     for (int nt = 0; nt < Cfg::NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
   const double* base = g.ws + (size_t)tk.slot * g.qmax * (size_t)(Cfg::BM * Cfg::BN);
+#pragma unroll 2
   for (int q = 0; q < tk.nq; ++q) {
     const double* w = base + (size_t)q * (Cfg::BM * Cfg::BN);
 #pragma unroll

@@ -281,3 +281,190 @@ __global__ void k_flags(const Ctl* ctl, const int32_t* bad, double* out) {
   out[1] = *bad ? 1.0 : 0.0;
 }
 }  // namespace pcal
+
+#include <cooperative_groups.h>
+
+namespace pcal {
+
+// The whole pcal_step phase of one iteration (stepsize_select + pcal_step,
+// solver.cpp:212-307) as ONE cooperative kernel (single GPU): bb partials →
+// grid sync → η (every block reduces the partials in the same fixed order;
+// block 0 publishes it) → Z = X − GL/η with column-norm partials → grid sync →
+// normalisation.  Same arithmetic and reduction order as the separate kernels
+// k_bb_partials / k_eta / k_update / k_normalize (bitwise identical results);
+// saves three launches and the host-visible gaps between them.
+struct StepArgs {
+  const double *x, *pg, *xp, *pgp, *d, *dp;
+  double* z;
+  double* bbpart;
+  double* npart;
+  int64_t n, ld, p, chunk, nchunks, n_glob;
+};
+
+__global__ void __launch_bounds__(kStreamThreads) k_step_fused(StepArgs a, Ctl* ctl) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double sm[kStreamThreads / 32];
+  __shared__ double s_eta;
+  __shared__ double s_inv;
+  __shared__ int s_deg;
+  if (ctl->done) return;  // uniform: nothing writes `done` before this kernel ends
+  const bool need = ctl->eta_kind != 0 && ctl->have_prev && ctl->iter != 0;
+  // ---- phase 1: stepsize inner products (k_bb_partials)
+  if (need) {
+    double ss = 0.0, sy = 0.0, yy = 0.0;
+    const int64_t half = a.ld / 2;
+    const int64_t total = half * a.p;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t j = e / half;
+      const double2 xv = reinterpret_cast<const double2*>(a.x)[e];
+      const double2 xpv = reinterpret_cast<const double2*>(a.xp)[e];
+      const double2 pv = reinterpret_cast<const double2*>(a.pg)[e];
+      const double2 ppv = reinterpret_cast<const double2*>(a.pgp)[e];
+      const double dj = a.d[j], dpj = a.dp[j];
+      {
+        const double s = xv.x - xpv.x;
+        const double y = (pv.x - dj * xv.x) - (ppv.x - dpj * xpv.x);
+        ss += s * s;
+        sy += s * y;
+        yy += y * y;
+      }
+      {
+        const double s = xv.y - xpv.y;
+        const double y = (pv.y - dj * xv.y) - (ppv.y - dpj * xpv.y);
+        ss += s * s;
+        sy += s * y;
+        yy += y * y;
+      }
+    }
+    const double bs = block_sum<kStreamThreads>(ss, sm);
+    const double by = block_sum<kStreamThreads>(sy, sm);
+    const double bc = block_sum<kStreamThreads>(yy, sm);
+    if (threadIdx.x == 0) {
+      a.bbpart[blockIdx.x * 3 + 0] = bs;
+      a.bbpart[blockIdx.x * 3 + 1] = by;
+      a.bbpart[blockIdx.x * 3 + 2] = bc;
+    }
+  }
+  grid.sync();
+  // ---- phase 2: η (k_eta), redundantly in every block
+  {
+    double ss = 0.0, sy = 0.0, yy = 0.0;
+    if (need) {
+      double s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) {
+        s1 += a.bbpart[3 * i + 0];
+        s2 += a.bbpart[3 * i + 1];
+        s3 += a.bbpart[3 * i + 2];
+      }
+      ss = block_sum<kStreamThreads>(s1, sm);
+      sy = block_sum<kStreamThreads>(s2, sm);
+      yy = block_sum<kStreamThreads>(s3, sm);
+    }
+    if (threadIdx.x == 0) {
+      const Ctl* c = ctl;
+      double eta;
+      if (c->eta_kind == 0) {
+        eta = clamp_eta(c, c->gamma);
+      } else {
+        const double fallback = c->eta_prev > 0.0 ? c->eta_prev : c->eta0;
+        if (!need) {
+          eta = clamp_eta(c, c->eta0 > 0.0 ? c->eta0 : fallback);
+        } else {
+          const double bb1 = (ss == 0.0 || sy == 0.0) ? fallback : fabs(sy) / ss;
+          const double bb2 = (sy == 0.0) ? fallback : yy / fabs(sy);
+          double v = fallback;
+          switch (c->eta_kind) {
+            case 2: v = bb1; break;
+            case 3: v = bb2; break;
+            case 4: v = (c->iter % 2 == 1) ? bb1 : bb2; break;
+            case 1: v = (ss == 0.0) ? fallback : sqrt(yy) / sqrt(ss); break;
+            default: break;
+          }
+          eta = clamp_eta(c, v);
+        }
+      }
+      s_eta = eta;
+    }
+    __syncthreads();
+  }
+  const double eta = s_eta;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    ctl->eta = eta;
+    ctl->step_deg = 0;
+    if (!(eta > 0.0)) {
+      ctl->step_param = 1;
+      ctl->done = 3;
+    }
+  }
+  if (!(eta > 0.0)) return;  // uniform
+  // ---- phase 3: Z = X − (1/η)(P − d∘X), column-norm partials (k_update)
+  const double inv_eta = 1.0 / eta;
+  const int64_t items = a.nchunks * a.p;
+  for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+    const int64_t c = it % a.nchunks, j = it / a.nchunks;
+    const int64_t r0 = c * a.chunk, r1 = min(a.n, r0 + a.chunk);
+    const double dj = a.d[j];
+    const double* xj = a.x + j * a.ld;
+    const double* pj = a.pg + j * a.ld;
+    double* zj = a.z + j * a.ld;
+    double acc = 0.0;
+    for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+      const double xv = xj[i];
+      const double gl = pj[i] - dj * xv;
+      const double v = xv - inv_eta * gl;
+      zj[i] = v;
+      acc += v * v;
+    }
+    const double s = block_sum<kStreamThreads>(acc, sm);
+    if (threadIdx.x == 0) a.npart[c * a.p + j] = s;
+  }
+  grid.sync();
+  // ---- phase 4: normalisation + degenerate columns + finiteness (k_normalize)
+  bool bad = false;
+  for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+    const int64_t c = it % a.nchunks, j = it / a.nchunks;
+    const int64_t r0 = c * a.chunk, r1 = min(a.n, r0 + a.chunk);
+    if (threadIdx.x == 0) {
+      double nrm2 = 0.0;
+      for (int64_t q = 0; q < a.nchunks; ++q) nrm2 += a.npart[q * a.p + j];
+      const double nz = sqrt(nrm2);
+      s_deg = nz < 1e-14;
+      s_inv = 1.0 / nz;
+    }
+    __syncthreads();
+    double* zj = a.z + j * a.ld;
+    if (!s_deg) {
+      const double inv = s_inv;
+      for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+        const double v = zj[i] * inv;
+        zj[i] = v;
+        bad |= !isfinite(v);
+      }
+    } else {
+      const double* xj = a.x + j * a.ld;
+      double acc = 0.0;
+      for (int64_t i = threadIdx.x; i < a.n; i += blockDim.x) acc += xj[i] * xj[i];
+      const double pn2 = block_sum<kStreamThreads>(acc, sm);
+      if (threadIdx.x == 0) sm[0] = sqrt(pn2);
+      __syncthreads();
+      const double pn = sm[0];
+      for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+        double v;
+        if (pn > 0.0) v = xj[i] * (1.0 / pn);
+        else v = (i == (j % a.n_glob)) ? 1.0 : 0.0;
+        zj[i] = v;
+        bad |= !isfinite(v);
+      }
+      if (c == 0 && threadIdx.x == 0) atomicAdd(&ctl->step_deg, 1);
+    }
+    __syncthreads();
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) {
+    ctl->step_bad = 1;
+    ctl->done = 2;
+  }
+}
+
+}  // namespace pcal

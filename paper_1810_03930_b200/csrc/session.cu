@@ -306,6 +306,7 @@ struct pcal_session {
   int bb_blocks = 0, cp_blocks = 0, sp_blocks = 0;
   int64_t st_chunk = 0, st_nchunks = 0;
   bool st_march = false;
+  bool fused_step = false;  // cooperative k_step_fused fits co-resident on the device
   int64_t st_zchunk = 0, st_nzc = 0;
   // graphs
   cudaGraphExec_t graph[2] = {nullptr, nullptr};
@@ -541,6 +542,34 @@ static void launch_iteration(pcal_session* s, int b) {
   cudaStream_t st = s->stream;
   const int nb = 1 - b;
   mark(s, 0);
+  if (!s->comm && s->fused_step) {  // one cooperative kernel for the whole step phase
+    StepArgs a{Xof(s, b), Pof(s, b), Xof(s, nb), Pof(s, nb), Dvec(s, b), Dvec(s, nb),
+               Xof(s, nb), s->bbpart.p, s->npart.p, s->n, s->ld, s->p, s->up_chunk,
+               s->up_nchunks, s->n_glob};
+    Ctl* c = s->ctl;
+    void* args[] = {&a, &c};
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3((unsigned)s->bb_blocks);
+    lc.blockDim = dim3(kStreamThreads);
+    lc.stream = st;
+    cudaLaunchAttribute attr{};
+    attr.id = cudaLaunchAttributeCooperative;
+    attr.val.cooperative = 1;
+    lc.attrs = &attr;
+    lc.numAttrs = 1;
+    PCAL_CUDA(cudaLaunchKernelExC(&lc, (const void*)k_step_fused, args));
+    launched("k_step_fused");
+    mark(s, 5);
+    launch_eval(s, nb, 0, s->ctl);
+    PCAL_CUDA(cudaGetLastError());
+    if (s->pev_on) {
+      float t = 0;
+      PCAL_CUDA(cudaEventElapsedTime(&t, s->pev[0], s->pev[5]));
+      s->prof_ms[0] += t;
+      s->prof_iters += 1;
+    }
+    return;
+  }
   k_bb_partials<<<s->bb_blocks, kStreamThreads, 0, st>>>(Xof(s, b), Pof(s, b), Xof(s, nb),
                                                          Pof(s, nb), Dvec(s, b), Dvec(s, nb),
                                                          s->ld, s->p, s->bbpart.p, s->ctl);
@@ -726,6 +755,15 @@ static void alloc_state(pcal_session* s) {
   s->cp_blocks = (int)std::min<int64_t>(ceil_div(p * p, kStreamThreads), 256);
   s->cpart.alloc(s->cp_blocks);
   s->bb_blocks = 4 * num_sms(s->device);
+  {
+    int per_sm = 0;
+    PCAL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step_fused, kStreamThreads, 0));
+    int coop = 0;
+    PCAL_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, s->device));
+    // the cooperative kernel wins while launch gaps dominate (≤ 8M elements);
+    // beyond that the separate kernels stream better
+    s->fused_step = coop && per_sm >= 4 && n * p <= (int64_t)8 << 20;
+  }
   s->bbpart.alloc((size_t)3 * s->bb_blocks);
   s->up_chunk = std::max<int64_t>(1024, round_up(ceil_div(n * p, 8 * 148 * 4), 256));
   s->up_chunk = std::min<int64_t>(s->up_chunk, round_up(n, 256));
