@@ -144,7 +144,8 @@ def pinned_f64(n_rows: int, n_cols: int):
     return t, arr
 
 
-def cpu_reference_rate(inst, x0, budget_s: float = 15.0, threads: int = None, min_iters=1):
+def cpu_reference_rate(inst, x0, budget_s: float = 15.0, threads: int = None, min_iters=1,
+                       max_iters=None):
     """Time the reference CPU solve() on a bounded sample; returns (iters/s, info)."""
     from oracle.oracle import Config, Model, MODEL_DENSE, MODEL_KOHN_SHAM, MODEL_STENCIL
     from oracle.oracle import Reference, Restatement, available_reference
@@ -155,7 +156,7 @@ def cpu_reference_rate(inst, x0, budget_s: float = 15.0, threads: int = None, mi
     # probe: one iteration, per-iteration time from the reference's own trace clock
     probe = R.solve(m, Config(tol_rel_kkt=TINY, max_iter=1, threads=threads, final_orth=False), x0)
     t_it = max(probe.trace[1, 6] - probe.trace[0, 6], 1e-6)
-    iters = int(max(min_iters, min(inst.iters, budget_s / t_it)))
+    iters = int(max(min_iters, min(inst.iters, max_iters or inst.iters, budget_s / t_it)))
     rep = R.solve(m, Config(tol_rel_kkt=TINY, max_iter=iters, threads=threads, final_orth=False), x0)
     per = (rep.trace[iters, 6] - rep.trace[0, 6]) / iters
     what = "reference solve() (oracle/_ref)" if R.kind == "reference" else "C restatement (oracle)"
@@ -189,7 +190,7 @@ def run_reference_arm(args):
         inst = Instance(args.config, c["kind"], nn, c["p"], c["iters"], s, v=v, grid=g)
     x0 = O.initial_point_qr(inst.n, inst.p, inst.seed ^ INIT_SALT, threads=th)
     budget = float(os.environ.get("PCAL_REF_BUDGET_S", "60"))
-    rate, info = cpu_reference_rate(inst, x0, budget_s=budget, min_iters=1)
+    rate, info = cpu_reference_rate(inst, x0, budget_s=budget, min_iters=1, max_iters=args.steps)
     line = {"metric": "PCAL iterations/sec", "impl": "reference", "value": rate,
             "unit": "iterations/s", "n_gpus": args.gpus, "steps": info["iters"],
             "warmup": 1, "ms_per_step": 1e3 / rate, "higher_is_better": True,
