@@ -18,9 +18,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def short(name: str) -> str:
     nm = name.replace("pcal::", "").replace("(int)", "")
-    m = re.search(r"gemm_(streamk|fixup)<GemmCfg<(\d+), (\d+), \d+, \d+, \d+, (\d)>, (\d)", nm)
+    m = re.search(r"gemm_(streamk|fixup|fixup_store)<GemmCfg<(\d+), (\d+), \d+, \d+, \d+, (\d)(?:, \d+)?>(?:, (\d))?", nm)
     if m:
-        kind = {"0": "STORE", "1": "GRAD", "2": "XM"}[m.group(5)]
+        kind = {"0": "STORE", "1": "GRAD", "2": "XM", None: "STORE"}[m.group(5)]
         mode = "MC" if m.group(4) == "0" else "KC"
         return f"gemm_{m.group(1)}<{m.group(2)}x{m.group(3)},{mode},{kind}>"
     m = re.search(r"(k_[a-z0-9_]+)", name)
