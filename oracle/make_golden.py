@@ -116,6 +116,32 @@ def small(R: Reference) -> None:
     print("wrote", os.path.join(OUT, "reference_small.npz"), len(g), "arrays")
 
 
+def algorithm_cases(R: Reference) -> None:
+    """PLAM, PLAM-DA, PCAL-DA, MOptQR and PCAL with the PLAM multiplier formula
+    (solver.cpp:320-474) on the config-1 instance and a small converging case."""
+    from oracle.oracle import ALG_PLAM, ALG_PCAL, ALG_MOPTQR, ALG_PLAMDA, ALG_PCALDA
+    g = {}
+    m1 = R.dense_trace_min(1000, 20, 1, s=44.26282919872377)
+    x01 = R.initial_point_qr(1000, 20, 1 ^ INIT_SALT)
+    r = R.random_normal(40, 40, 24)
+    a40 = np.asfortranarray(0.5 * (r + r.T))
+    s40 = R.spectral_norm_estimate(a40, SPECTRAL_SALT)
+    m40 = Model(MODEL_DENSE, 40, 5, s40, a=a40)
+    x040 = R.initial_point_qr(40, 5, 25)
+    algs = {"plam": (ALG_PLAM, 1), "plamda": (ALG_PLAMDA, 1), "pcalda": (ALG_PCALDA, 1),
+            "moptqr": (ALG_MOPTQR, 1), "pcalplamf": (ALG_PCAL, 0)}
+    for name, (alg, mult) in algs.items():
+        case, rep = run_case(R, m1, x01, tol_rel_kkt=TINY, max_iter=60, threads=8, algorithm=alg,
+                             multiplier_rule=mult)
+        for k, v in case.items():
+            g[f"a1_{name}_{k}"] = v
+        case, rep = run_case(R, m40, x040, algorithm=alg, multiplier_rule=mult, max_iter=3000)
+        for k, v in case.items():
+            g[f"a40_{name}_{k}"] = v
+    np.savez_compressed(os.path.join(OUT, "reference_algorithms.npz"), **g)
+    print("wrote reference_algorithms.npz")
+
+
 def grid_cases(R: Reference) -> None:
     """Grid models (no reference implementation): the reference solve() driving
     the restated operator — pins the PCAL loop around it, not the operator."""
@@ -161,5 +187,6 @@ if __name__ == "__main__":
     R = Reference()
     small(R)
     grid_cases(R)
+    algorithm_cases(R)
     if "--cfg2" in sys.argv:
         cfg2(R)

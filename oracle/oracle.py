@@ -31,6 +31,7 @@ TRACE_COLS = 7
 MODEL_DENSE, MODEL_STENCIL, MODEL_KOHN_SHAM = 1, 2, 3
 ETA_CONSTANT, ETA_DIFFERENTIAL, ETA_BB1, ETA_BB2, ETA_ABB = range(5)
 MULT_PLAM, MULT_PCAL = 0, 1
+ALG_PLAM, ALG_PCAL, ALG_ALM, ALG_MOPTQR, ALG_PLAMDA, ALG_PCALDA = range(6)
 STATUS_NAMES = {0: "converged", 1: "max_iter", 2: "diverged"}
 E_PARAM, E_DIM, E_RANK, E_EVAL, E_DIVERGE = -1, -2, -3, -4, -5
 
@@ -41,7 +42,8 @@ class OrcConfig(C.Structure):
     _fields_ = [("beta", C.c_double), ("eta_kind", C.c_int), ("gamma", C.c_double),
                 ("eta_min", C.c_double), ("eta_max", C.c_double), ("eta0", C.c_double),
                 ("multiplier_rule", C.c_int), ("tol_rel_kkt", C.c_double),
-                ("max_iter", C.c_int64), ("threads", C.c_int), ("final_orth", C.c_int)]
+                ("max_iter", C.c_int64), ("threads", C.c_int), ("final_orth", C.c_int),
+                ("algorithm", C.c_int)]
 
 
 class OrcReport(C.Structure):
@@ -98,11 +100,12 @@ class Config:
     max_iter: int = 3000
     threads: int = 1
     final_orth: bool = True
+    algorithm: int = 1  # ALG_PCAL
 
     def c(self) -> OrcConfig:
         return OrcConfig(self.beta, self.eta_kind, self.gamma, self.eta_min, self.eta_max,
                          self.eta0, self.multiplier_rule, self.tol_rel_kkt, self.max_iter,
-                         self.threads, int(self.final_orth))
+                         self.threads, int(self.final_orth), self.algorithm)
 
 
 @dataclass
@@ -200,6 +203,8 @@ class Restatement(_Base):
         L.orc_fd_gradient_check.restype = dbl
         L.orc_solve_pcal.argtypes = [C.POINTER(OrcModel), C.POINTER(OrcConfig), _dp,
                                      C.POINTER(OrcReport)]
+        L.orc_solve.argtypes = [C.POINTER(OrcModel), C.POINTER(OrcConfig), _dp,
+                                C.POINTER(OrcReport)]
         L.orc_stepsize_select.argtypes = [C.POINTER(OrcConfig), i64, dbl, dbl, _dp, _dp, _dp,
                                           _dp, i64]
         L.orc_stepsize_select.restype = dbl
@@ -371,13 +376,13 @@ class Restatement(_Base):
         c = cfg.c()
         rep, keep = self._report(model, cfg, snaps)
         try:
-            rc = self.lib.orc_solve_pcal(C.byref(om), C.byref(c), _ptr(x0), C.byref(rep))
+            rc = self.lib.orc_solve(C.byref(om), C.byref(c), _ptr(x0), C.byref(rep))
         finally:
             self._release(om)
         if rc == E_PARAM:
             raise ValueError("parameter_error")
         if rc:
-            raise RuntimeError(f"orc_solve_pcal failed ({rc})")
+            raise RuntimeError(f"orc_solve failed ({rc})")
         return self._finish(rep, keep, snaps)
 
 

@@ -538,6 +538,7 @@ void orc_config_default(orc_config* c) {
   c->max_iter = 3000;
   c->threads = 1;
   c->final_orth = 1;
+  c->algorithm = ORC_ALG_PCAL;
 }
 
 static double clamp_eta(const orc_config* c, double v) { /* solver.cpp:95-97 */
@@ -721,14 +722,28 @@ static void snap(orc_report* r, int64_t k, const double* x, double eta, int64_t 
     }
 }
 
-/* iterate_main, PCAL branch (solver.cpp:320-474), and solve (:626-633). */
+/* iterate_main (solver.cpp:320-474) and solve (:626-633). */
 int orc_solve_pcal(const orc_model* m, const orc_config* c, const double* x0, orc_report* r) {
+  return orc_solve(m, c, x0, r);
+}
+
+int orc_solve(const orc_model* m, const orc_config* c, const double* x0, orc_report* r) {
   const double t0 = now_s();
   int rc = validate(c);
   if (rc) return rc;
+  const int alg = c->algorithm;
+  if (alg == ORC_ALG_ALM || alg < 0 || alg > ORC_ALG_PCALDA) return ORC_E_PARAM;
   const int64_t n = m->n, p = m->p, np = n * p;
   const int threads = c->threads;
-  const double beta = c->beta >= 0.0 ? c->beta : 1.0;                     /* :120-125 */
+  const int da = alg == ORC_ALG_PLAMDA || alg == ORC_ALG_PCALDA;                /* :326-330 */
+  const int normalized = alg == ORC_ALG_PCAL || alg == ORC_ALG_PCALDA;
+  const int retraction = alg == ORC_ALG_MOPTQR;
+  const int mult = (alg == ORC_ALG_PCAL) ? c->multiplier_rule : ORC_MULT_PLAM;
+  double beta;                                                                  /* :120-134 */
+  if (c->beta >= 0.0) beta = c->beta;
+  else if (alg == ORC_ALG_PCAL || alg == ORC_ALG_PCALDA) beta = 1.0;
+  else if (alg == ORC_ALG_MOPTQR) beta = 0.0;
+  else beta = m->s + 0.1;
   const double eta0 = c->eta0 > 0.0 ? clamp_eta(c, c->eta0)                /* :99-102 */
                                     : clamp_eta(c, m->s + 2.0 * beta);
   r->beta_used = beta;
@@ -746,6 +761,8 @@ int orc_solve_pcal(const orc_model* m, const orc_config* c, const double* x0, or
   double* glp = (double*)malloc(sizeof(double) * (size_t)np);
   double* xn = (double*)malloc(sizeof(double) * (size_t)np);
   double* tmp = (double*)malloc(sizeof(double) * (size_t)np);
+  double* lam = (double*)calloc((size_t)(p * p), sizeof(double));
+  double* mm = (double*)malloc(sizeof(double) * (size_t)(p * p));
   iterate_data d;
   idata_alloc(&d, n, p);
   memcpy(x, x0, sizeof(double) * (size_t)np);
@@ -779,13 +796,46 @@ int orc_solve_pcal(const orc_model* m, const orc_config* c, const double* x0, or
       status = ORC_CONVERGED;
     } else {
       for (int64_t k = 0; k < c->max_iter; ++k) {
-        pcal_grad_l(&d, x, n, p, beta, c->multiplier_rule, gl, tmp, threads);
+        if (retraction) {                                   /* :371-374 */
+          orc_matmul(x, n, p, d.gtx, p, tmp, threads);
+          for (int64_t q = 0; q < np; ++q) gl[q] = d.grad_f[q] + -1.0 * tmp[q];
+        } else if (da) {                                    /* :375-384 */
+          if (k == 0) {
+            memcpy(lam, d.w, sizeof(double) * (size_t)(p * p));
+          } else {
+            /* lambda.add_scaled(-beta, xtx.add_scaled(-1, I)): upper triangle, mirrored */
+            for (int64_t jj = 0; jj < p; ++jj)
+              for (int64_t ii = 0; ii <= jj; ++ii) {
+                const double cij = d.xtx[ii + jj * p] + -1.0 * (ii == jj ? 1.0 : 0.0);
+                const double v = lam[ii + jj * p] + -beta * cij;
+                lam[ii + jj * p] = v;
+                lam[jj + ii * p] = v;
+              }
+          }
+          for (int64_t q = 0; q < p * p; ++q) mm[q] = beta * d.c[q] - lam[q];
+          orc_matmul(x, n, p, mm, p, tmp, threads);
+          for (int64_t q = 0; q < np; ++q) gl[q] = d.grad_f[q] + 1.0 * tmp[q];
+        } else {                                            /* :385-409 */
+          pcal_grad_l(&d, x, n, p, beta, mult, gl, tmp, threads);
+        }
         const double eta = orc_stepsize_select(c, k, eta_state, eta0, x, have_prev ? xp : NULL,
                                                gl, have_prev ? glp : NULL, np);
         int64_t deg = 0;
-        rc = orc_pcal_step(x, gl, n, p, eta, xn, &deg, threads);
-        if (rc == ORC_E_PARAM) goto done_error;
-        if (rc == ORC_E_DIVERGE) { status = ORC_DIVERGED; rc = ORC_OK; break; }
+        if (retraction) {                                   /* :415-418 */
+          if (!(eta > 0.0)) { rc = ORC_E_PARAM; goto done_error; }
+          const double sc = -1.0 / eta;
+          for (int64_t q = 0; q < np; ++q) tmp[q] = x[q] + sc * gl[q];
+          if (orc_orthonormalize(tmp, n, p, xn) != ORC_OK) { status = ORC_DIVERGED; rc = ORC_OK; break; }
+        } else if (normalized) {                            /* :419-422 */
+          rc = orc_pcal_step(x, gl, n, p, eta, xn, &deg, threads);
+          if (rc == ORC_E_PARAM) goto done_error;
+          if (rc == ORC_E_DIVERGE) { status = ORC_DIVERGED; rc = ORC_OK; break; }
+        } else {                                            /* plam_step :253-262 */
+          if (!(eta > 0.0)) { rc = ORC_E_PARAM; goto done_error; }
+          const double sc = -1.0 / eta;
+          for (int64_t q = 0; q < np; ++q) xn[q] = x[q] + sc * gl[q];
+          if (!all_finite(xn, np)) { status = ORC_DIVERGED; rc = ORC_OK; break; }
+        }
         r->degenerate_steps += deg;
         /* rotate: prev ← current, current ← next (:427-430) */
         { double* t = xp; xp = x; x = xn; xn = t; }
@@ -837,7 +887,7 @@ int orc_solve_pcal(const orc_model* m, const orc_config* c, const double* x0, or
   rc = ORC_OK;
 done_error:
   r->wall_time = now_s() - t0;
-  free(x); free(xp); free(gl); free(glp); free(xn); free(tmp);
+  free(x); free(xp); free(gl); free(glp); free(xn); free(tmp); free(lam); free(mm);
   idata_free(&d);
 #undef RECORD
   return rc;

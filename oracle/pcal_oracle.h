@@ -90,8 +90,12 @@ enum { ORC_CONVERGED = 0, ORC_MAXITER = 1, ORC_DIVERGED = 2 };
 enum { ORC_OK = 0, ORC_E_PARAM = -1, ORC_E_DIM = -2, ORC_E_RANK = -3, ORC_E_EVAL = -4,
        ORC_E_DIVERGE = -5, ORC_E_ALLOC = -6 };
 
+/* Algorithm (diagnostics.hpp:10), reference enum order */
+enum { ORC_ALG_PLAM = 0, ORC_ALG_PCAL = 1, ORC_ALG_ALM = 2, ORC_ALG_MOPTQR = 3, ORC_ALG_PLAMDA = 4,
+       ORC_ALG_PCALDA = 5 };
+
 typedef struct {
-  double beta;            /* < 0: PCAL default 1 (solver.cpp:120-134) */
+  double beta;            /* < 0: per-algorithm default (solver.cpp:120-134) */
   int eta_kind;           /* ORC_ETA_* (StepsizeRule::Kind order) */
   double gamma, eta_min, eta_max, eta0;
   int multiplier_rule;    /* ORC_MULT_* */
@@ -99,6 +103,7 @@ typedef struct {
   int64_t max_iter;
   int threads;
   int final_orth;
+  int algorithm;          /* ORC_ALG_* (ALM is not restated: ORC_E_PARAM) */
 } orc_config;
 
 void orc_config_default(orc_config* c); /* SolverConfig defaults, solver.hpp:13-42 */
@@ -126,8 +131,10 @@ typedef struct {
   double* snap_eta;       /* eta used to produce X_k (k ≥ 1), per snapshot */
 } orc_report;
 
-/* solve() for the PCAL algorithm (solver.cpp:320-474, 626-633).  Returns 0 or a
- * negative ORC_E_* for errors the reference throws out of solve(). */
+/* solve() — iterate_main (solver.cpp:320-474, 626-633) for PLAM, PCAL,
+ * MOptQR, PLAM-DA and PCAL-DA.  Returns 0 or a negative ORC_E_* for errors the
+ * reference throws out of solve(). */
+int orc_solve(const orc_model* m, const orc_config* c, const double* x0, orc_report* r);
 int orc_solve_pcal(const orc_model* m, const orc_config* c, const double* x0, orc_report* r);
 
 /* Building blocks (solver.hpp:74-113) */

@@ -95,7 +95,7 @@ int guarded(F&& f) {
 
 SolverConfig to_config(const orc_config* c) {
   SolverConfig cfg;
-  cfg.algorithm = Algorithm::Pcal;
+  cfg.algorithm = static_cast<Algorithm>(c->algorithm);
   cfg.beta = c->beta;
   cfg.eta_rule.kind = static_cast<StepsizeRule::Kind>(c->eta_kind);
   cfg.eta_rule.gamma = c->gamma;

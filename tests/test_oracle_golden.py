@@ -234,3 +234,25 @@ def test_cfg2_instance(orc):
     assert sha(m.a) == str(g["cfg2_a_sha"])
     x0 = orc.initial_point_qr(16384, 128, 1 ^ INIT_SALT)
     assert sha(x0) == str(g["cfg2_x0_sha"])
+
+
+ALGS = {"plam": (0, 1), "plamda": (4, 1), "pcalda": (5, 1), "moptqr": (3, 1), "pcalplamf": (1, 0)}
+
+
+@pytest.mark.parametrize("name", list(ALGS))
+def test_algorithm_variants_bitwise(orc, name):
+    """PLAM / PLAM-DA / PCAL-DA / MOptQR / PCAL-PlamFormula (solver.cpp:320-474)."""
+    g = np.load(os.path.join(HERE, "golden", "reference_algorithms.npz"))
+    alg, mult = ALGS[name]
+    m1 = orc.dense_trace_min(1000, 20, 1, s=44.26282919872377, threads=8)
+    x01 = orc.initial_point_qr(1000, 20, 1 ^ INIT_SALT)
+    r = orc.solve(m1, Config(tol_rel_kkt=TINY, max_iter=60, threads=8, algorithm=alg,
+                             multiplier_rule=mult), x01)
+    assert np.array_equal(r.trace[:, :6], g[f"a1_{name}_trace"])
+    assert sha(r.final_x) == str(g[f"a1_{name}_final_x_sha"])
+    rr = orc.random_normal(40, 40, 24)
+    a40 = np.asfortranarray(0.5 * (rr + rr.T))
+    m40 = Model(MODEL_DENSE, 40, 5, orc.spectral_norm_estimate(a40, 0x73706563), a=a40)
+    r = orc.solve(m40, Config(algorithm=alg, multiplier_rule=mult), orc.initial_point_qr(40, 5, 25))
+    assert np.array_equal(r.trace[:, :6], g[f"a40_{name}_trace"])
+    assert r.status == str(g[f"a40_{name}_status"]) and r.beta == float(g[f"a40_{name}_beta"])
