@@ -67,8 +67,12 @@ extern "C" {
 #define PCAL_MULT_PLAM_FORMULA 0
 #define PCAL_MULT_PCAL_FORMULA 1
 
-/* Algorithm (diagnostics.hpp:10): this library implements PCAL only. */
+/* Algorithm (diagnostics.hpp:10), reference enum order.  ALM (2) is not provided. */
+#define PCAL_ALG_PLAM 0
 #define PCAL_ALG_PCAL 1
+#define PCAL_ALG_MOPTQR 3
+#define PCAL_ALG_PLAMDA 4
+#define PCAL_ALG_PCALDA 5
 
 typedef struct pcal_model_desc {
   int32_t kind;          /* PCAL_MODEL_* */
@@ -82,7 +86,7 @@ typedef struct pcal_model_desc {
 } pcal_model_desc;
 
 typedef struct pcal_config {  /* orthopt::SolverConfig (solver.hpp:30-42) */
-  int32_t algorithm;          /* PCAL_ALG_PCAL */
+  int32_t algorithm;          /* PCAL_ALG_* (PCAL default; PLAM, MOptQR, PLAM-DA, PCAL-DA) */
   double beta;                /* < 0: PCAL default 1.0 (solver.cpp:120-125) */
   int32_t eta_kind;           /* PCAL_ETA_* */
   double gamma;               /* Constant rule only */

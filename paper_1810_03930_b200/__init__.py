@@ -216,7 +216,8 @@ class StepsizeRule:
 
 @dataclass
 class SolverConfig:
-    """orthopt::SolverConfig; ``device`` replaces the explicit thread count."""
+    """orthopt::SolverConfig; ``device`` replaces the explicit thread count.
+    ``algorithm``: "pcal" (default), "plam", "moptqr", "plam-da", "pcal-da"."""
     beta: float = -1.0
     eta_rule: StepsizeRule = field(default_factory=StepsizeRule)
     multiplier_rule: int = MultiplierRule.PCAL_FORMULA
@@ -226,11 +227,14 @@ class SolverConfig:
     device: int = 0
     algorithm: str = "pcal"
 
+    ALGORITHMS = {"plam": 0, "pcal": 1, "moptqr": 3, "plam-da": 4, "pcal-da": 5}
+
     def _c(self) -> _Config:
-        if self.algorithm != "pcal":
-            raise ParameterError(f"algorithm {self.algorithm!r} is not provided (PCAL only)")
+        if self.algorithm not in self.ALGORITHMS:
+            raise ParameterError(f"algorithm {self.algorithm!r} is not provided "
+                                 f"({', '.join(self.ALGORITHMS)}; ALM is out of scope)")
         r = self.eta_rule
-        return _Config(1, self.beta, r.kind, r.gamma, r.eta_min, r.eta_max, r.eta0,
+        return _Config(self.ALGORITHMS[self.algorithm], self.beta, r.kind, r.gamma, r.eta_min, r.eta_max, r.eta0,
                        self.multiplier_rule, self.tol_rel_kkt, self.max_iter,
                        int(self.final_orth), self.device)
 

@@ -234,13 +234,14 @@ __device__ __forceinline__ void epilogue(const GemmArgs& g, int tm, int tn, int 
           const int64_t idx = row + j * e.ld;
           if (interior) {
             const double kkt = gv[b][mt] - acc[mt][nt][0];
-            const double pv = kkt + e.beta * acc[mt][nt][1];
+            const double pv = (e.p_from_g ? gv[b][mt] : kkt) + e.beta * acc[mt][nt][1];
             e.G[idx] = pv;
             ks += kkt * kkt;
             ds += xv[b][mt] * pv;
           } else if (row < e.n && j < e.p) {
-            const double kkt = e.G[idx] - acc[mt][nt][0];
-            const double pv = kkt + e.beta * acc[mt][nt][1];
+            const double g0 = e.G[idx];
+            const double kkt = g0 - acc[mt][nt][0];
+            const double pv = (e.p_from_g ? g0 : kkt) + e.beta * acc[mt][nt][1];
             e.G[idx] = pv;
             ks += kkt * kkt;
             ds += e.X[idx] * pv;
@@ -380,6 +381,7 @@ __device__ __forceinline__ void produce(const GemmArgs& g, double* As, double* B
 template <class Cfg, int EPI>
 __global__ void __launch_bounds__(Cfg::THREADS + 128, 1) gemm_streamk(GemmArgs g) {
   if (g.ctl && g.ctl->done) return;
+  if (g.gate && !*g.gate) return;
   extern __shared__ __align__(16) double smem[];
   double* As = smem;
   double* Bs = smem + Cfg::STAGES * Cfg::A_STAGE;
@@ -465,6 +467,7 @@ __global__ void __launch_bounds__(Cfg::THREADS + 128, 1) gemm_streamk(GemmArgs g
 template <class Cfg, int EPI>
 __global__ void __launch_bounds__(Cfg::THREADS) gemm_fixup(GemmArgs g, const FixupTask* tasks) {
   if (g.ctl && g.ctl->done) return;
+  if (g.gate && !*g.gate) return;
   const FixupTask tk = tasks[blockIdx.x];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wm = warp / Cfg::WARPS_N, wn = warp % Cfg::WARPS_N;
@@ -494,6 +497,7 @@ template <class Cfg>
 __global__ void __launch_bounds__(256) gemm_fixup_store(GemmArgs g, const FixupTask* tasks,
                                                         int ntasks) {
   if (g.ctl && g.ctl->done) return;
+  if (g.gate && !*g.gate) return;
   constexpr int TILE = Cfg::BM * Cfg::BN;
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (int64_t)ntasks * TILE) return;

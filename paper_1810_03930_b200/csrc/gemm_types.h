@@ -27,6 +27,7 @@ struct EpiParams {
   double beta;
   int64_t n, p;
   int64_t pstride;   // column stride of the partial arrays: part[col·pstride + rb]
+  int32_t p_from_g;  // EPI_XM: P = G + β·acc1 (dual-ascent / MOptQR) instead of kkt + β·acc1
 };
 
 struct GemmArgs {
@@ -47,6 +48,7 @@ struct GemmArgs {
   int32_t qmax;
   EpiParams ep;
   const Ctl* ctl;     // early exit when ctl->done (may be null)
+  const int32_t* gate;  // early exit when non-null and *gate == 0 (in-graph CholeskyQR)
 };
 
 struct FixupTask {   // one split tile

@@ -32,12 +32,19 @@ __global__ void __launch_bounds__(kStreamThreads) k_colsum3(ColSumArgs a, const 
 }
 
 // W = Ψ(GᵀX) = ½(M1 + M1ᵀ), C = XᵀX − I (exactly symmetric, from the computed
-// upper triangle), written interleaved as the B operand of the X·[W|C] GEMM:
-//   mcat[k + (2j)·ldk] = W[k,j],  mcat[k + (2j+1)·ldk] = C[k,j]
-// (eval_iterate, solver.cpp:79-84).  fpart2[block] = Σ C² over the block.
+// upper triangle), written interleaved as the B operand of the X·[W|M] GEMM:
+//   mcat[k + (2j)·ldk] = W[k,j],  mcat[k + (2j+1)·ldk] = M[k,j]
+// with the second block per algorithm (solver.cpp:371-409):
+//   PCAL / PLAM : M = C                 (epilogue: P = (G − XW) + β·XC)
+//   PCAL-DA / PLAM-DA : M = βC − Λ,  Λ ← W at the start point, Λ ← Λ − β·C after
+//                 (epilogue: P = G + XM)
+//   MOptQR      : M = −GᵀX (not symmetrised)   (epilogue: P = G + XM = G − X·GᵀX)
+// cpart[block] = Σ C² over the block (feasibility).
 // gr: (2·pp) × pp column-major; rows [0,pp) = GᵀX, rows [pp,2pp) = XᵀX.
+enum { MC_PCAL = 0, MC_DA = 1, MC_MOPTQR = 2 };
 __global__ void k_small_pxp(const double* __restrict__ gr, int64_t pp, int64_t p,
                             double* __restrict__ mcat, int64_t ldk, double* __restrict__ cpart,
+                            int mode, double beta, double* __restrict__ lam, int lam_init,
                             const Ctl* ctl) {
   if (ctl && ctl->done) return;
   __shared__ double sm[kStreamThreads / 32];
@@ -51,8 +58,20 @@ __global__ void k_small_pxp(const double* __restrict__ gr, int64_t pp, int64_t p
     const int64_t a = min(k, j), b = max(k, j);
     double c = gr[pp + a + b * ldg];
     if (k == j) c += -1.0;
+    double m;
+    if (mode == MC_PCAL) {
+      m = c;
+    } else if (mode == MC_DA) {
+      // Λ is updated elementwise from the upper triangle's value, so it stays
+      // exactly symmetric (SquareSymmetric::add_scaled, kernels.cpp:38-47)
+      double l = lam_init ? w : lam[k + j * p] + -beta * c;
+      lam[k + j * p] = l;
+      m = beta * c - l;
+    } else {
+      m = -gr[k + j * ldg];
+    }
     mcat[k + (2 * j) * ldk] = w;
-    mcat[k + (2 * j + 1) * ldk] = c;
+    mcat[k + (2 * j + 1) * ldk] = m;
     acc += c * c;
   }
   const double s = block_sum<kStreamThreads>(acc, sm);
@@ -214,8 +233,20 @@ __global__ void k_norm_reduce(const double* __restrict__ npart, const double* __
 __global__ void k_normalize(const double* __restrict__ x, double* __restrict__ z, int64_t n,
                             int64_t ld, int64_t p, int64_t chunk, int64_t nchunks,
                             const double* __restrict__ npart, const double* __restrict__ nrm,
-                            int64_t row0, int64_t n_glob, Ctl* ctl) {
+                            int64_t row0, int64_t n_glob, int plain, Ctl* ctl) {
   if (ctl->done) return;
+  if (plain) {  // plam_step (solver.cpp:253-262): no normalisation, only the finiteness check
+    const int64_t j = blockIdx.y;
+    const int64_t r0 = (int64_t)blockIdx.x * chunk;
+    const int64_t r1 = min(n, r0 + chunk);
+    bool bad = false;
+    for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) bad |= !isfinite(z[j * ld + i]);
+    if (__syncthreads_or(bad) && threadIdx.x == 0) {
+      ctl->step_bad = 1;
+      if (!nrm) ctl->done = 2;
+    }
+    return;
+  }
   __shared__ double sm[kStreamThreads / 32];
   __shared__ double s_inv;
   __shared__ int s_deg;
@@ -299,6 +330,7 @@ struct StepArgs {
   double* bbpart;
   double* npart;
   int64_t n, ld, p, chunk, nchunks, n_glob;
+  int plain;  // 1: plam_step (no normalisation)
 };
 
 __global__ void __launch_bounds__(kStreamThreads) k_step_fused(StepArgs a, Ctl* ctl) {
@@ -423,7 +455,14 @@ __global__ void __launch_bounds__(kStreamThreads) k_step_fused(StepArgs a, Ctl* 
   grid.sync();
   // ---- phase 4: normalisation + degenerate columns + finiteness (k_normalize)
   bool bad = false;
-  for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+  if (a.plain) {
+    for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+      const int64_t c = it % a.nchunks, j = it / a.nchunks;
+      const int64_t r0 = c * a.chunk, r1 = min(a.n, r0 + a.chunk);
+      for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) bad |= !isfinite(a.z[j * a.ld + i]);
+    }
+  }
+  for (int64_t it = blockIdx.x; it < items && !a.plain; it += gridDim.x) {
     const int64_t c = it % a.nchunks, j = it / a.nchunks;
     const int64_t r0 = c * a.chunk, r1 = min(a.n, r0 + a.chunk);
     if (threadIdx.x == 0) {

@@ -59,9 +59,15 @@ __global__ void k_sym_fro2(const double* __restrict__ b, int64_t ldb, int64_t p,
 // floor = 1e-14·sqrt(fro2[0]) of the FIRST Gram (kernels.cpp:252); status[0]=0 on failure.
 __global__ void k_cholesky(const double* __restrict__ b, int64_t ldb, int64_t p,
                            const double* fro2_first, double* __restrict__ l, int64_t ldl,
-                           int32_t* status) {
+                           int32_t* status, const int32_t* prev_ok = nullptr,
+                           const Ctl* ctl = nullptr) {
   __shared__ double s_ljj;
   __shared__ int s_ok;
+  if (ctl && ctl->done) return;
+  if (prev_ok && !*prev_ok) {  // first CholeskyQR pass already failed
+    if (threadIdx.x == 0) *status = 0;
+    return;
+  }
   const double floor_ = 1e-14 * sqrt(*fro2_first);
   if (threadIdx.x == 0) s_ok = 1;
   for (int64_t e = threadIdx.x; e < p * p; e += blockDim.x) l[(e % p) + (e / p) * ldl] = 0.0;
@@ -136,6 +142,50 @@ __global__ void k_mgs2(double* __restrict__ q, int64_t n, int64_t ld, int64_t p,
       __syncthreads();
     }
   if (threadIdx.x == 0) *status = 1;
+}
+
+// In-graph MGS2 fallback of the MOptQR retraction: runs only when a CholeskyQR
+// pass failed; a rank-deficient iterate is a rank_error ⇒ Diverged
+// (orthonormalize inside solve(), solver.cpp:415-418,464-465).
+__global__ void k_mgs2_gated(double* __restrict__ q, int64_t n, int64_t ld, int64_t p,
+                             const double* fro2_first, const int32_t* ok1, const int32_t* ok2,
+                             int32_t* status, Ctl* ctl) {
+  if (ctl->done) return;
+  if (*ok1 && *ok2) return;
+  __shared__ double sm[32];
+  __shared__ double s_v;
+  const double floor_ = 1e-14 * sqrt(*fro2_first);
+  for (int pass = 0; pass < 2; ++pass)
+    for (int64_t j = 0; j < p; ++j) {
+      double* qj = q + j * ld;
+      for (int64_t k = 0; k < j; ++k) {
+        const double* qk = q + k * ld;
+        double acc = 0.0;
+        for (int64_t i = threadIdx.x; i < n; i += blockDim.x) acc += qk[i] * qj[i];
+        const double s = block_sum<1024>(acc, sm);
+        if (threadIdx.x == 0) s_v = s;
+        __syncthreads();
+        const double sv = s_v;
+        for (int64_t i = threadIdx.x; i < n; i += blockDim.x) qj[i] -= sv * qk[i];
+        __syncthreads();
+      }
+      double acc = 0.0;
+      for (int64_t i = threadIdx.x; i < n; i += blockDim.x) acc += qj[i] * qj[i];
+      const double nrm2 = block_sum<1024>(acc, sm);
+      if (threadIdx.x == 0) s_v = nrm2;
+      __syncthreads();
+      if (!(s_v > floor_)) {
+        if (threadIdx.x == 0) {
+          *status = 0;
+          ctl->step_bad = 1;
+          ctl->done = 2;
+        }
+        return;
+      }
+      const double inv = 1.0 / sqrt(s_v);
+      for (int64_t i = threadIdx.x; i < n; i += blockDim.x) qj[i] *= inv;
+      __syncthreads();
+    }
 }
 
 // ------------------------------------------------------------------------------
@@ -300,6 +350,10 @@ struct pcal_session {
   int64_t trace_cap = 0;
   // plans
   pcal::GemmPlan grad[2], gram[2], xm[2], orth_gram, orth_mul;
+  // MOptQR in-graph retraction (per parity): Gram of Z, Z·T → Q1, Gram of Q1, Q1·T → Q
+  pcal::GemmPlan rq_gram_z[2], rq_mul1[2], rq_gram_q[2], rq_mul2[2];
+  pcal::DevBuf lam;  // dual-ascent multiplier Λ (p×p, replicated)
+  int alg = PCAL_ALG_PCAL;
   int64_t nrb_grad = 0, nrb_xm = 0, nrb_f = 0;  // row-blocks of f/k/d partials
   int64_t pstride_f = 0, pstride_xm = 0;        // column strides of the partial arrays
   int64_t up_chunk = 0, up_nchunks = 0;
@@ -356,8 +410,10 @@ static void launch_colsums(pcal_session* s, const double* fp, int64_t nrb_f, con
   a.nrows[1] = nrb_kd;
   a.stride[1] = s->pstride_xm;
   a.out[1] = kcol;
-  // PlamFormula: no diagonal correction, d stays 0 (solver.cpp:406-408)
-  a.in[2] = (dp && s->cfg.multiplier_rule == PCAL_MULT_PCAL_FORMULA) ? dp : nullptr;
+  // d_j only for PCAL with the PCAL formula (solver.cpp:329-330,392-408); else d stays 0
+  a.in[2] = (dp && s->alg == PCAL_ALG_PCAL && s->cfg.multiplier_rule == PCAL_MULT_PCAL_FORMULA)
+                ? dp
+                : nullptr;
   a.nrows[2] = nrb_kd;
   a.stride[2] = s->pstride_xm;
   a.out[2] = dcol;
@@ -492,8 +548,14 @@ static void launch_eval(pcal_session* s, int b, int mode, const Ctl* ctl_guard) 
   mark(s, 2);
   launch_gemm(s->gram[b], st);
   if (s->comm) s->comm->allreduce(s->gr.p, (size_t)2 * s->pp * s->pp, st);  // C1
-  k_small_pxp<<<s->cp_blocks, kStreamThreads, 0, st>>>(s->gr.p, s->pp, s->p, s->mcat.p, s->pp,
-                                                       s->cpart.p, ctl_guard);
+  {
+    const int mc = (s->alg == PCAL_ALG_PLAMDA || s->alg == PCAL_ALG_PCALDA) ? MC_DA
+                   : s->alg == PCAL_ALG_MOPTQR                               ? MC_MOPTQR
+                                                                             : MC_PCAL;
+    k_small_pxp<<<s->cp_blocks, kStreamThreads, 0, st>>>(s->gr.p, s->pp, s->p, s->mcat.p, s->pp,
+                                                         s->cpart.p, mc, s->beta, s->lam.p,
+                                                         mode == 1 ? 1 : 0, ctl_guard);
+  }
   launched("k_small_pxp");
   mark(s, 3);
   launch_gemm(s->xm[b], st);
@@ -538,14 +600,47 @@ static void launch_eval(pcal_session* s, int b, int mode, const Ctl* ctl_guard) 
 }
 
 // One PCAL iteration from X_k in pair b to X_{k+1} in pair 1−b (solver.cpp:385-438).
+// MOptQR retraction inside the iteration graph (solver.cpp:415-418): Z in
+// X(nb) → Q = orthonormalize(Z) in X(nb) by CholeskyQR2 with status-gated
+// GEMMs (Q1 scratch in P(nb), dead until the next gradient) and the MGS2
+// fallback kernel, which only runs when a Cholesky pass failed.
+static void launch_retraction(pcal_session* s, int nb) {
+  cudaStream_t st = s->stream;
+  const int64_t p = s->p, pp = s->pp;
+  int32_t* ok1 = s->orth_status;
+  int32_t* ok2 = s->orth_status + 1;
+  launch_gemm(s->rq_gram_z[nb], st);
+  k_sym_fro2<<<1, 1024, 0, st>>>(s->orth_b.p, pp, p, s->orth_f2.p);
+  launched("k_sym_fro2");
+  k_cholesky<<<1, 1024, 0, st>>>(s->orth_b.p, pp, p, s->orth_f2.p, s->orth_l.p, pp, ok1, nullptr,
+                                 s->ctl);
+  launched("k_cholesky");
+  k_trinv_t<<<(unsigned)ceil_div(p, 128), 128, 0, st>>>(s->orth_l.p, pp, p, s->orth_t.p, pp, ok1);
+  launched("k_trinv_t");
+  launch_gemm(s->rq_mul1[nb], st);
+  launch_gemm(s->rq_gram_q[nb], st);
+  k_cholesky<<<1, 1024, 0, st>>>(s->orth_b.p, pp, p, s->orth_f2.p, s->orth_l.p, pp, ok2, ok1,
+                                 s->ctl);
+  launched("k_cholesky");
+  k_trinv_t<<<(unsigned)ceil_div(p, 128), 128, 0, st>>>(s->orth_l.p, pp, p, s->orth_t.p, pp, ok2);
+  launched("k_trinv_t");
+  launch_gemm(s->rq_mul2[nb], st);
+  k_mgs2_gated<<<1, 1024, 0, st>>>(Xof(s, nb), s->n, s->ld, p, s->orth_f2.p, ok1, ok2,
+                                   s->orth_status + 2, s->ctl);
+  launched("k_mgs2_gated");
+}
+
+// One iteration from X_k in pair b to X_{k+1} in pair 1−b (solver.cpp:369-439).
 static void launch_iteration(pcal_session* s, int b) {
   cudaStream_t st = s->stream;
   const int nb = 1 - b;
+  // PLAM, PLAM-DA and the MOptQR pre-retraction step do not normalise columns
+  const int plain = !(s->alg == PCAL_ALG_PCAL || s->alg == PCAL_ALG_PCALDA);
   mark(s, 0);
   if (!s->comm && s->fused_step) {  // one cooperative kernel for the whole step phase
     StepArgs a{Xof(s, b), Pof(s, b), Xof(s, nb), Pof(s, nb), Dvec(s, b), Dvec(s, nb),
                Xof(s, nb), s->bbpart.p, s->npart.p, s->n, s->ld, s->p, s->up_chunk,
-               s->up_nchunks, s->n_glob};
+               s->up_nchunks, s->n_glob, plain};
     Ctl* c = s->ctl;
     void* args[] = {&a, &c};
     cudaLaunchConfig_t lc{};
@@ -559,43 +654,37 @@ static void launch_iteration(pcal_session* s, int b) {
     lc.numAttrs = 1;
     PCAL_CUDA(cudaLaunchKernelExC(&lc, (const void*)k_step_fused, args));
     launched("k_step_fused");
-    mark(s, 5);
-    launch_eval(s, nb, 0, s->ctl);
-    PCAL_CUDA(cudaGetLastError());
-    if (s->pev_on) {
-      float t = 0;
-      PCAL_CUDA(cudaEventElapsedTime(&t, s->pev[0], s->pev[5]));
-      s->prof_ms[0] += t;
-      s->prof_iters += 1;
+  } else {
+    k_bb_partials<<<s->bb_blocks, kStreamThreads, 0, st>>>(Xof(s, b), Pof(s, b), Xof(s, nb),
+                                                           Pof(s, nb), Dvec(s, b), Dvec(s, nb),
+                                                           s->ld, s->p, s->bbpart.p, s->ctl);
+    launched("k_bb_partials");
+    if (s->comm) s->comm->allreduce(s->bbpart.p, (size_t)3 * s->bb_blocks, st);  // C3
+    k_eta<<<1, kStreamThreads, 0, st>>>(s->ctl, s->bbpart.p, s->bb_blocks);
+    launched("k_eta");
+    dim3 gu((unsigned)s->up_nchunks, (unsigned)s->p);
+    k_update<<<gu, kStreamThreads, 0, st>>>(Xof(s, b), Pof(s, b), Dvec(s, b), Xof(s, nb), s->n,
+                                            s->ld, s->p, s->up_chunk, s->npart.p,
+                                            s->comm ? s->xpart.p : nullptr, s->ctl);
+    launched("k_update");
+    const double* nrm = nullptr;
+    if (s->comm && !plain) {  // C4: global column norms
+      k_norm_reduce<<<(unsigned)ceil_div(s->p, 128), 128, 0, st>>>(s->npart.p, s->xpart.p,
+                                                                   s->up_nchunks, s->p, s->nrm.p,
+                                                                   s->ctl);
+      launched("k_norm_reduce");
+      s->comm->allreduce(s->nrm.p, (size_t)2 * s->p, st);
+      nrm = s->nrm.p;
+    } else if (s->comm) {
+      nrm = s->nrm.p;  // plain steps: only marks the sharded (collective) divergence rule
     }
-    return;
+    k_normalize<<<gu, kStreamThreads, 0, st>>>(Xof(s, b), Xof(s, nb), s->n, s->ld, s->p,
+                                               s->up_chunk, s->up_nchunks, s->npart.p, nrm,
+                                               s->row0, s->n_glob, plain, s->ctl);
+    launched("k_normalize");
   }
-  k_bb_partials<<<s->bb_blocks, kStreamThreads, 0, st>>>(Xof(s, b), Pof(s, b), Xof(s, nb),
-                                                         Pof(s, nb), Dvec(s, b), Dvec(s, nb),
-                                                         s->ld, s->p, s->bbpart.p, s->ctl);
-  launched("k_bb_partials");
-  if (s->comm) s->comm->allreduce(s->bbpart.p, (size_t)3 * s->bb_blocks, st);  // C3
-  k_eta<<<1, kStreamThreads, 0, st>>>(s->ctl, s->bbpart.p, s->bb_blocks);
-  launched("k_eta");
-  dim3 gu((unsigned)s->up_nchunks, (unsigned)s->p);
-  k_update<<<gu, kStreamThreads, 0, st>>>(Xof(s, b), Pof(s, b), Dvec(s, b), Xof(s, nb), s->n,
-                                          s->ld, s->p, s->up_chunk, s->npart.p,
-                                          s->comm ? s->xpart.p : nullptr, s->ctl);
-  launched("k_update");
-  const double* nrm = nullptr;
-  if (s->comm) {  // C4: global column norms
-    k_norm_reduce<<<(unsigned)ceil_div(s->p, 128), 128, 0, st>>>(s->npart.p, s->xpart.p,
-                                                                 s->up_nchunks, s->p, s->nrm.p,
-                                                                 s->ctl);
-    launched("k_norm_reduce");
-    s->comm->allreduce(s->nrm.p, (size_t)2 * s->p, st);
-    nrm = s->nrm.p;
-  }
-  k_normalize<<<gu, kStreamThreads, 0, st>>>(Xof(s, b), Xof(s, nb), s->n, s->ld, s->p,
-                                             s->up_chunk, s->up_nchunks, s->npart.p, nrm, s->row0,
-                                             s->n_glob, s->ctl);
-  launched("k_normalize");
   PCAL_CUDA(cudaGetLastError());
+  if (s->alg == PCAL_ALG_MOPTQR) launch_retraction(s, nb);
   mark(s, 5);
   launch_eval(s, nb, 0, s->ctl);
   PCAL_CUDA(cudaGetLastError());
@@ -610,6 +699,37 @@ static void launch_iteration(pcal_session* s, int b) {
 static void build_plans(pcal_session* s) {
   const int dev = s->device;
   const int64_t pp = s->pp, ld = s->ld, n = s->n;
+  if (s->alg == PCAL_ALG_MOPTQR) {
+    for (int b = 0; b < 2; ++b) {
+      auto gram = [&](GemmPlan& g, const double* a) {
+        plan_gemm(g, dev, pick_size(pp), A_KCONTIG, EPI_STORE, pp, pp, ld, 0);
+        g.args.A = g.args.B = a;
+        g.args.lda = g.args.ldb = ld;
+        g.args.ep.C = s->orth_b.p;
+        g.args.ep.ldc = pp;
+        g.args.ep.m_store = g.args.ep.n_store = pp;
+        g.args.ctl = s->ctl;
+      };
+      auto mul = [&](GemmPlan& g, const double* a, double* out, const int32_t* gate) {
+        plan_gemm(g, dev, pick_size(pp), A_MCONTIG, EPI_STORE, n, pp, pp);
+        g.args.A = a;
+        g.args.lda = ld;
+        g.args.B = s->orth_t.p;
+        g.args.ldb = pp;
+        g.args.ep.C = out;
+        g.args.ep.ldc = ld;
+        g.args.ep.m_store = n;
+        g.args.ep.n_store = s->p;
+        g.args.ctl = s->ctl;
+        g.args.gate = gate;
+      };
+      gram(s->rq_gram_z[b], Xof(s, b));
+      mul(s->rq_mul1[b], Xof(s, b), Pof(s, b), s->orth_status);
+      gram(s->rq_gram_q[b], Pof(s, b));
+      s->rq_gram_q[b].args.gate = s->orth_status;
+      mul(s->rq_mul2[b], Pof(s, b), Xof(s, b), s->orth_status + 1);
+    }
+  }
   for (int b = 0; b < 2; ++b) {
     // gradient (dense): G = A·X, A ldA×ldA (MCONTIG), X ld×pp
     if (s->model.kind == PCAL_MODEL_DENSE) {
@@ -661,7 +781,10 @@ static void build_plans(pcal_session* s) {
       e.kpart = s->kpart.p;
       e.dpart = s->dpart.p;
       e.pstride = s->pstride_xm;
-      e.beta = s->beta;
+      // PCAL/PLAM: P = (G − XW) + β·XC; dual ascent / MOptQR: P = G + X·M
+      e.p_from_g = (s->alg == PCAL_ALG_PLAMDA || s->alg == PCAL_ALG_PCALDA ||
+                    s->alg == PCAL_ALG_MOPTQR);
+      e.beta = e.p_from_g ? 1.0 : s->beta;
       e.n = n;
       e.p = s->p;
       g.args.ctl = s->ctl;
@@ -777,9 +900,11 @@ static void alloc_state(pcal_session* s) {
   s->orth_t.alloc((size_t)pp * pp);
   s->orth_t.zero(st);
   s->orth_f2.alloc(1);
-  PCAL_CUDA(cudaMalloc(&s->bad, sizeof(int32_t) * 4));
-  PCAL_CUDA(cudaMemsetAsync(s->bad, 0, sizeof(int32_t) * 4, st));
-  s->orth_status = s->bad + 2;
+  s->lam.alloc((size_t)p * p);
+  s->lam.zero(st);
+  PCAL_CUDA(cudaMalloc(&s->bad, sizeof(int32_t) * 8));
+  PCAL_CUDA(cudaMemsetAsync(s->bad, 0, sizeof(int32_t) * 8, st));
+  s->orth_status = s->bad + 2;  // [pass-1 ok, pass-2 ok, mgs2 status]
   PCAL_CUDA(cudaMalloc(&s->ctl, sizeof(Ctl)));
   PCAL_CUDA(cudaMallocHost(&s->h_ctl, sizeof(Ctl)));
   s->trace_cap = s->cfg.max_iter + 1;
@@ -870,8 +995,10 @@ static void init_ctl(pcal_session* s) {
 __global__ void k_set_t0(Ctl* c) { c->t0_ns = globaltimer_ns(); }
 
 static void validate(const pcal_config* c) {  // SolverConfig::validate (solver.cpp:106-118)
-  if (c->algorithm != PCAL_ALG_PCAL)
-    throw Error(PCAL_E_UNSUPPORTED, "only the PCAL algorithm is provided");
+  if (c->algorithm != PCAL_ALG_PCAL && c->algorithm != PCAL_ALG_PLAM &&
+      c->algorithm != PCAL_ALG_MOPTQR && c->algorithm != PCAL_ALG_PLAMDA &&
+      c->algorithm != PCAL_ALG_PCALDA)
+    throw Error(PCAL_E_UNSUPPORTED, "algorithm not provided (PCAL, PLAM, MOptQR, PLAM-DA, PCAL-DA)");
   if (c->beta >= 0.0 && !std::isfinite(c->beta))
     throw Error(PCAL_E_PARAMETER, "SolverConfig: beta must be finite");
   if (!(c->tol_rel_kkt > 0.0))
@@ -979,7 +1106,14 @@ void session_create(const pcal_model_desc* model, const pcal_config* config, con
   s->ld_max = padded_ld(maxrows);
   s->ld = comm ? s->ld_max : padded_ld(s->n);
   s->K_full = padded_ld(s->n_glob);
-  s->beta = config->beta >= 0.0 ? config->beta : 1.0;                  // solver.cpp:120-125
+  s->alg = config->algorithm;
+  if (comm && s->alg == PCAL_ALG_MOPTQR)
+    throw Error(PCAL_E_UNSUPPORTED, "MOptQR is single-GPU (its MGS2 fallback is not sharded)");
+  // resolve_beta (solver.cpp:120-134)
+  s->beta = config->beta >= 0.0                                                ? config->beta
+            : (s->alg == PCAL_ALG_PCAL || s->alg == PCAL_ALG_PCALDA) ? 1.0
+            : s->alg == PCAL_ALG_MOPTQR                                       ? 0.0
+                                                                              : model->s + 0.1;
   s->eta0 = config->eta0 > 0.0 ? clamp_eta_h(config, config->eta0)     // solver.cpp:99-102
                                : clamp_eta_h(config, model->s + 2.0 * s->beta);
   LaunchScope ls(&s->launches);
@@ -1665,7 +1799,7 @@ int pcal_pcal_step(const double* x, const double* grad_l, int64_t n, int64_t p, 
     launched("k_update");
     k_normalize<<<gu, kStreamThreads, 0, s->stream>>>(Xof(s.get(), 0), Xof(s.get(), 1), n, s->ld,
                                                       p, s->up_chunk, s->up_nchunks, s->npart.p,
-                                                      nullptr, 0, n, s->ctl);
+                                                      nullptr, 0, n, 0, s->ctl);
     launched("k_normalize");
     PCAL_CUDA(cudaGetLastError());
     copy_out(s.get(), Xof(s.get(), 1), out);

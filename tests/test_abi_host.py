@@ -52,7 +52,8 @@ def test_flops_estimate(pcal, orc):
 
 def test_config_validation_is_host_side(pcal):
     with pytest.raises(pcal.ParameterError):
-        pcal.SolverConfig(algorithm="plam")._c()
+        pcal.SolverConfig(algorithm="alm")._c()
+    assert pcal.SolverConfig(algorithm="plam-da")._c().algorithm == 4
 
 
 def _has_cuda():
