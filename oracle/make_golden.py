@@ -142,6 +142,28 @@ def algorithm_cases(R: Reference) -> None:
     print("wrote reference_algorithms.npz")
 
 
+def report_io_cases(R: Reference) -> None:
+    """The reference's JSON / CSV report text and an OCPROB01 container."""
+    import ctypes as C
+    L = R.lib
+    L.ref_run_single_text.argtypes = [C.c_int64, C.c_int64, C.c_uint64, C.c_int64, C.c_char_p,
+                                      C.c_int64, C.c_char_p, C.c_int64]
+    L.ref_save_quadratic.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_double,
+                                     C.c_char_p]
+    jb, cb = C.create_string_buffer(1 << 20), C.create_string_buffer(1 << 20)
+    assert L.ref_run_single_text(60, 4, 7, 50, jb, len(jb), cb, len(cb)) == 0
+    open(os.path.join(OUT, "ref_report_p1_n60.json"), "w").write(jb.value.decode() + "\n")
+    open(os.path.join(OUT, "ref_trace_p1_n60.csv"), "w").write(cb.value.decode())
+    r = R.random_normal(40, 40, 31)
+    a = np.asfortranarray(0.5 * (r + r.T))
+    g0 = R.random_normal(40, 5, 32)
+    s = R.spectral_norm_estimate(a, 33)
+    path = os.path.join(OUT, "ref_quad40.ocprob")
+    assert L.ref_save_quadratic(a.ctypes.data, g0.ctypes.data, 40, 5, s, path.encode()) == 0
+    np.savez_compressed(os.path.join(OUT, "ref_quad40.npz"), a=a, g0=g0, s=s)
+    print("wrote report/container fixtures")
+
+
 def grid_cases(R: Reference) -> None:
     """Grid models (no reference implementation): the reference solve() driving
     the restated operator — pins the PCAL loop around it, not the operator."""
@@ -188,5 +210,6 @@ if __name__ == "__main__":
     small(R)
     grid_cases(R)
     algorithm_cases(R)
+    report_io_cases(R)
     if "--cfg2" in sys.argv:
         cfg2(R)

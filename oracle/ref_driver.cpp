@@ -353,3 +353,53 @@ int ref_solve(void* model, const orc_config* c, const double* x0, orc_report* r,
 }
 
 }  // extern "C"
+
+// --- report I/O and the problem container of the reference (report_io.cpp,
+//     problems.cpp:327-416): golden text for the product's formatter tests ----
+#include <fstream>
+#include <sstream>
+
+#include "orthopt/harness.hpp"
+#include "orthopt/report_io.hpp"
+
+extern "C" {
+
+// run_single(P1 α=0 / RandomSym, seed) with PCAL defaults and max_iter; writes
+// the reference's JSON (no timing) and trace CSV (time column zeroed) into bufs.
+int ref_run_single_text(std::int64_t n, std::int64_t p, std::uint64_t seed, std::int64_t max_iter,
+                        char* json_buf, std::int64_t json_cap, char* csv_buf,
+                        std::int64_t csv_cap) {
+  return guarded([&] {
+    ProblemSpec spec;
+    spec.kind = ProblemKind::P1;
+    spec.alpha = 0.0;
+    spec.n = n;
+    spec.p = p;
+    spec.seed = seed;
+    SolverConfig cfg;
+    cfg.max_iter = max_iter;
+    RunReport rep = run_single(spec, cfg, {InitMode::Qr, 0.5, 0});
+    for (auto& s : rep.trace) s.elapsed = 0.0;
+    const std::string js = to_json(rep, false);
+    std::ostringstream cs;
+    write_trace_csv(rep, cs);
+    if ((std::int64_t)js.size() + 1 > json_cap || (std::int64_t)cs.str().size() + 1 > csv_cap)
+      throw io_error("buffer too small");
+    std::memcpy(json_buf, js.c_str(), js.size() + 1);
+    std::memcpy(csv_buf, cs.str().c_str(), cs.str().size() + 1);
+    return 0;
+  });
+}
+
+int ref_save_quadratic(const double* a, const double* g0, std::int64_t n, std::int64_t p, double s,
+                       const char* path) {
+  return guarded([&] {
+    DenseMatrix g = g0 ? from_ptr(g0, n, p) : DenseMatrix(n, p);
+    auto m = make_quadratic(sym_from_ptr(a, n), std::move(g), g0 ? ProblemKind::P2 : ProblemKind::P3, s);
+    std::ofstream out(path, std::ios::binary);
+    save_problem(*m, out);
+    return 0;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,60 @@
+"""CPU: the report formats and the OCPROB01 container are byte-compatible with
+the reference (report_io.cpp, problems.cpp:327-416).  The golden text was
+written by the reference itself (oracle/make_golden.py)."""
+import io
+import os
+from types import SimpleNamespace
+
+import numpy as np
+
+from paper_1810_03930_b200 import report_io as R
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _report_from_reference_json(text):
+    d = R.run_report_from_json(text)
+    fin = lambda f: None if f is None else SimpleNamespace(**f)
+    return SimpleNamespace(trace=d["trace"], final_pre_orth=fin(d["final_pre_orth"]),
+                           final_post_orth=fin(d["final_post_orth"]), iterations=d["iterations"],
+                           degenerate_steps=d["degenerate_steps"], status=d["status"],
+                           wall_time=d["wall_time"], stop_iterate=None, final_x=None), d
+
+
+def test_json_report_byte_identical_to_reference():
+    ref_text = open(os.path.join(GOLD, "ref_report_p1_n60.json")).read()
+    rep, d = _report_from_reference_json(ref_text)
+    assert R.to_json(rep, d["config"]) + "\n" == ref_text
+
+
+def test_trace_csv_byte_identical_to_reference():
+    ref_text = open(os.path.join(GOLD, "ref_trace_p1_n60.csv")).read()
+    rep, _ = _report_from_reference_json(open(os.path.join(GOLD, "ref_report_p1_n60.json")).read())
+    out = io.StringIO()
+    R.write_trace_csv(rep, out)
+    assert out.getvalue() == ref_text
+
+
+def test_summary_row_and_same_numerics():
+    rep, d = _report_from_reference_json(open(os.path.join(GOLD, "ref_report_p1_n60.json")).read())
+    out = io.StringIO()
+    R.write_summary_header(out)
+    R.write_summary_row(rep, d["config"], out)
+    lines = out.getvalue().splitlines()
+    assert lines[1].startswith("p1,pcal,7,60,4,1,abb,max-iter,50,0,")
+    assert R.same_numerics(rep, rep)
+    other = SimpleNamespace(**vars(rep))
+    other.trace = rep.trace.copy()
+    other.trace[3, 1] = np.nextafter(other.trace[3, 1], 0)
+    assert not R.same_numerics(rep, other)
+
+
+def test_container_round_trip_byte_identical(pcal):
+    path = os.path.join(GOLD, "ref_quad40.ocprob")
+    ref = np.load(os.path.join(GOLD, "ref_quad40.npz"))
+    model, params = R.load_problem(path, pcal)
+    assert params["tag"] == 2 and model.n == 40 and model.p == 5 and model.s == float(ref["s"])
+    assert np.array_equal(model.a, ref["a"]) and np.array_equal(model.g0, ref["g0"])
+    out = io.BytesIO()
+    R.save_problem(model, out, **{k: params[k] for k in ("kappa", "theta", "zeta", "xi")})
+    assert out.getvalue() == open(path, "rb").read()
