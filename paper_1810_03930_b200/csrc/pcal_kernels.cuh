@@ -333,14 +333,16 @@ struct StepArgs {
   int plain;  // 1: plam_step (no normalisation)
 };
 
-__global__ void __launch_bounds__(kStreamThreads) k_step_fused(StepArgs a, Ctl* ctl) {
+// The step phase as a device function of a cooperative grid (also the first
+// phase of the small-problem iteration kernel, k_iter_small).  Returns false
+// when the step must not continue (η ≤ 0); uniform across the grid.
+__device__ __forceinline__ bool step_phase(const StepArgs& a, Ctl* ctl) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   __shared__ double sm[kStreamThreads / 32];
   __shared__ double s_eta;
   __shared__ double s_inv;
   __shared__ int s_deg;
-  if (ctl->done) return;  // uniform: nothing writes `done` before this kernel ends
   const bool need = ctl->eta_kind != 0 && ctl->have_prev && ctl->iter != 0;
   // ---- phase 1: stepsize inner products (k_bb_partials)
   if (need) {
@@ -430,7 +432,7 @@ __global__ void __launch_bounds__(kStreamThreads) k_step_fused(StepArgs a, Ctl* 
       ctl->done = 3;
     }
   }
-  if (!(eta > 0.0)) return;  // uniform
+  if (!(eta > 0.0)) return false;  // uniform
   // ---- phase 3: Z = X − (1/η)(P − d∘X), column-norm partials (k_update)
   const double inv_eta = 1.0 / eta;
   const int64_t items = a.nchunks * a.p;
@@ -504,6 +506,12 @@ __global__ void __launch_bounds__(kStreamThreads) k_step_fused(StepArgs a, Ctl* 
     ctl->step_bad = 1;
     ctl->done = 2;
   }
+  return true;
+}
+
+__global__ void __launch_bounds__(kStreamThreads) k_step_fused(StepArgs a, Ctl* ctl) {
+  if (ctl->done) return;  // uniform: nothing writes `done` before this kernel ends
+  step_phase(a, ctl);
 }
 
 }  // namespace pcal

@@ -207,29 +207,10 @@ struct FinishArgs {
   double c_xc;          // (3/π)^{1/3}
 };
 
-__global__ void __launch_bounds__(256) k_finish_eval(FinishArgs a, Ctl* ctl,
-                                                     double* post /* 5 */) {
-  if (a.mode != 2 && ctl->done) return;
-  __shared__ double sm[8];
-  double pf = 0.0, pk = 0.0, pc = 0.0, pv = 0.0, pr = 0.0, pe = 0.0;
-  for (int64_t j = threadIdx.x; j < a.p; j += blockDim.x) {
-    pf += a.fcol[j];
-    pk += a.kcol[j];
-  }
-  for (int i = threadIdx.x; i < a.ncp; i += blockDim.x) pc += a.cpart[i];
-  if (a.model == PCAL_MODEL_KOHN_SHAM)
-    for (int i = threadIdx.x; i < a.nsp; i += blockDim.x) {
-      pv += a.spart[3 * i];
-      pr += a.spart[3 * i + 1];
-      pe += a.spart[3 * i + 2];
-    }
-  const double f1 = block_sum<256>(pf, sm);
-  const double k2 = block_sum<256>(pk, sm);
-  const double c2 = block_sum<256>(pc, sm);
-  const double vr = block_sum<256>(pv, sm);
-  const double rh = block_sum<256>(pr, sm);
-  const double ex = block_sum<256>(pe, sm);
-  if (threadIdx.x != 0) return;
+// Thread-0 tail of an evaluation: objective assembly, failure flags, trace
+// row, stopping test (solver.cpp:348-359,434-438,460-471).
+__device__ void finish_record(const FinishArgs& a, Ctl* ctl, double* post, double f1, double k2,
+                              double c2, double vr, double rh, double ex) {
   const bool bad_flag = a.flags ? a.flags[1] > 0.0 : *a.bad != 0;
   *a.bad = 0;  // reset for the next evaluation
   if (a.flags && a.mode == 0 && a.flags[0] > 0.0) {  // some rank's pcal_step diverged
@@ -288,6 +269,32 @@ __global__ void __launch_bounds__(256) k_finish_eval(FinishArgs a, Ctl* ctl,
   ctl->feas = feas;
   ctl->rel = rel;
   if (rel < ctl->tol) ctl->done = 1;
+}
+
+__global__ void __launch_bounds__(256) k_finish_eval(FinishArgs a, Ctl* ctl,
+                                                     double* post /* 5 */) {
+  if (a.mode != 2 && ctl->done) return;
+  __shared__ double sm[8];
+  double pf = 0.0, pk = 0.0, pc = 0.0, pv = 0.0, pr = 0.0, pe = 0.0;
+  for (int64_t j = threadIdx.x; j < a.p; j += blockDim.x) {
+    pf += a.fcol[j];
+    pk += a.kcol[j];
+  }
+  for (int i = threadIdx.x; i < a.ncp; i += blockDim.x) pc += a.cpart[i];
+  if (a.model == PCAL_MODEL_KOHN_SHAM)
+    for (int i = threadIdx.x; i < a.nsp; i += blockDim.x) {
+      pv += a.spart[3 * i];
+      pr += a.spart[3 * i + 1];
+      pe += a.spart[3 * i + 2];
+    }
+  const double f1 = block_sum<256>(pf, sm);
+  const double k2 = block_sum<256>(pk, sm);
+  const double c2 = block_sum<256>(pc, sm);
+  const double vr = block_sum<256>(pv, sm);
+  const double rh = block_sum<256>(pr, sm);
+  const double ex = block_sum<256>(pe, sm);
+  if (threadIdx.x != 0) return;
+  finish_record(a, ctl, post, f1, k2, c2, vr, rh, ex);
 }
 
 __global__ void k_zero_i32(int32_t* p, const Ctl* ctl) {
