@@ -50,7 +50,8 @@ int pick_size(int64_t N) {
 }
 
 void plan_gemm(GemmPlan& pl, int device, int size, int amode, int epi, int64_t M,
-                      int64_t N, int64_t K, int64_t sym_row0, int grid_override) {
+                      int64_t N, int64_t K, int64_t sym_row0, int grid_override, int fixed_splits,
+                      bool chunk_partials, int qmax_min) {
   pl.release();
   pl.size = size;
   pl.amode = amode;
@@ -75,13 +76,16 @@ void plan_gemm(GemmPlan& pl, int device, int size, int amode, int epi, int64_t M
   const int64_t units = (int64_t)ntiles * ki;
   int grid = grid_override > 0 ? grid_override : num_sms(device);
   if (units < grid) grid = (int)std::max<int64_t>(1, units);
-  // Enough tiles for every SM: data-parallel whole tiles (no partials, no
-  // fixup); otherwise stream-K so tall-skinny / few-tile products fill the chip.
-  // Cost model in k-iterations on the busiest CTA: data-parallel costs
-  // ⌈T/G⌉·ki; stream-K costs ⌈T·ki/G⌉ plus ≈4 k-iterations of fixup (partial
-  // stores, the extra launch, the re-read).
   int64_t upc = 0;
-  {
+  if (fixed_splits > 0) {
+    if (fixed_splits > ki) throw Error(PCAL_E_DIMENSION, "gemm: more segments than k-slices");
+    grid = ntiles * fixed_splits;  // CTA t·S + s: tile t, k-iterations [⌊s·ki/S⌋, ⌊(s+1)·ki/S⌋)
+  } else {
+    // Enough tiles for every SM: data-parallel whole tiles (no partials, no
+    // fixup); otherwise stream-K so tall-skinny / few-tile products fill the chip.
+    // Cost model in k-iterations on the busiest CTA: data-parallel costs
+    // ⌈T/G⌉·ki; stream-K costs ⌈T·ki/G⌉ plus ≈4 k-iterations of fixup (partial
+    // stores, the extra launch, the re-read).
     const int64_t g0 = grid;
     const int64_t dp_cost = ceil_div(ntiles, g0) * ki;
     const int64_t sk_cost = ceil_div(units, g0) + 4;
@@ -100,12 +104,13 @@ void plan_gemm(GemmPlan& pl, int device, int size, int amode, int epi, int64_t M
   for (int t = 0; t < ntiles && upc == 0; ++t) {
     const int32_t cf = cta_of_unit((int64_t)t * ki, units, grid);
     const int32_t cl = cta_of_unit((int64_t)(t + 1) * ki - 1, units, grid);
-    if (cf != cl) {
+    if (cf != cl || chunk_partials) {
       split[t] = (int32_t)tasks.size();
       tasks.push_back({t, (int32_t)tasks.size(), cl - cf + 1});
       qmax = std::max(qmax, cl - cf + 1);
     }
   }
+  if (chunk_partials) qmax = std::max(qmax, qmax_min);
   PCAL_CUDA(cudaMalloc(&pl.d_tiles, sizeof(int2) * ntiles));
   PCAL_CUDA(cudaMemcpy(pl.d_tiles, tiles.data(), sizeof(int2) * ntiles, cudaMemcpyHostToDevice));
   PCAL_CUDA(cudaMalloc(&pl.d_split, sizeof(int32_t) * ntiles));
@@ -132,6 +137,8 @@ void plan_gemm(GemmPlan& pl, int device, int size, int amode, int epi, int64_t M
   g.upc = upc;
   g.ws = pl.ws;
   g.qmax = qmax;
+  g.force_ws = chunk_partials ? 1 : 0;
+  pl.no_fixup = chunk_partials;
 }
 
 template <class Cfg, int EPI>
@@ -146,7 +153,7 @@ static void launch_cfg(const GemmPlan& pl, cudaStream_t st) {
   kern<<<pl.args.grid, Cfg::THREADS + 128, Cfg::SMEM_BYTES, st>>>(pl.args);
   launched(EPI == EPI_GRAD ? "gemm_grad" : EPI == EPI_XM ? "gemm_xm" : Cfg::AMODE == A_KCONTIG ? "gemm_gram" : "gemm_store");
   PCAL_CUDA(cudaGetLastError());
-  if (pl.ntasks) {
+  if (pl.ntasks && !pl.no_fixup) {
     if (EPI == EPI_STORE) {
       const int64_t total = (int64_t)pl.ntasks * Cfg::BM * Cfg::BN;
       gemm_fixup_store<Cfg><<<(unsigned)((total + 255) / 256), 256, 0, st>>>(pl.args, pl.d_tasks,
@@ -181,6 +188,27 @@ void launch_gemm(const GemmPlan& pl, cudaStream_t st) {
     launch_sized<A_KCONTIG, EPI_STORE>(pl, st);
   }
   (void)0;
+}
+
+template <class Cfg>
+static void chunk_sum_cfg(const GemmPlan& pl, const double* buf, const int32_t* rank_nq, int R,
+                          int64_t rank_stride, cudaStream_t st) {
+  const int64_t total = (int64_t)pl.ntasks * Cfg::BM * Cfg::BN;
+  gemm_chunk_sum_store<Cfg><<<(unsigned)((total + 255) / 256), 256, 0, st>>>(
+      pl.args, pl.d_tasks, pl.ntasks, buf, rank_nq, R, rank_stride);
+  launched("gram_chunk_sum");
+  PCAL_CUDA(cudaGetLastError());
+}
+
+void launch_gemm_chunk_sum(const GemmPlan& pl, const double* buf, const int32_t* rank_nq, int R,
+                           int64_t rank_stride, cudaStream_t st) {
+  if (pl.amode != A_KCONTIG || pl.epi != EPI_STORE || !pl.no_fixup)
+    throw Error(PCAL_E_STATE, "gemm: chunk sums need a K-contiguous chunk-partial plan");
+  switch (pl.size) {
+    case CFG_BIG: chunk_sum_cfg<CfgBig<A_KCONTIG>>(pl, buf, rank_nq, R, rank_stride, st); break;
+    case CFG_MID: chunk_sum_cfg<CfgMid<A_KCONTIG>>(pl, buf, rank_nq, R, rank_stride, st); break;
+    default: chunk_sum_cfg<CfgSmall<A_KCONTIG>>(pl, buf, rank_nq, R, rank_stride, st); break;
+  }
 }
 
 

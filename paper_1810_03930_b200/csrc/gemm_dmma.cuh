@@ -438,7 +438,7 @@ __global__ void __launch_bounds__(Cfg::THREADS + 128, 1) gemm_streamk(GemmArgs g
     const int kk = (int)(u % g.ki);
     if (kk == g.ki - 1 || u == u1 - 1) {
       const int2 tc = g.tiles[t];
-      const bool whole = (seg_begin % g.ki == 0) && kk == g.ki - 1;
+      const bool whole = (seg_begin % g.ki == 0) && kk == g.ki - 1 && !g.force_ws;
       if (whole) {
         epilogue<Cfg, EPI>(g, tc.x, tc.y, wm, wn, lane, acc);
       } else {
@@ -516,6 +516,43 @@ __global__ void __launch_bounds__(256) gemm_fixup_store(GemmArgs g, const FixupT
   r /= Cfg::NT;
   const int mt = r % Cfg::MT;
   const int warp = r / Cfg::MT;
+  const int wm = warp / Cfg::WARPS_N, wn = warp % Cfg::WARPS_N;
+  const int2 tc = g.tiles[tk.tile];
+  const int64_t row = (int64_t)tc.x * Cfg::BM + wm * Cfg::WM + mt * 8 + (lane >> 2);
+  const int64_t col = (int64_t)tc.y * Cfg::BN + wn * Cfg::WN + nt * 8 + 2 * (lane & 3) + x;
+  const EpiParams& ep = g.ep;
+  if (row < ep.m_store && col < ep.n_store) ep.C[row + col * ep.ldc] = s;
+}
+
+// Ordered sum of chunk partials gathered from R ranks (reproducible Gram):
+// the per-element sequence is (rank 0 chunks, rank 1 chunks, …) = the global
+// chunk order, so the result does not depend on how chunks map to ranks.
+template <class Cfg>
+__global__ void __launch_bounds__(256) gemm_chunk_sum_store(GemmArgs g, const FixupTask* tasks,
+                                                            int ntasks, const double* buf,
+                                                            const int32_t* rank_nq, int R,
+                                                            int64_t rank_stride) {
+  if (g.ctl && g.ctl->done) return;
+  constexpr int TILE = Cfg::BM * Cfg::BN;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)ntasks * TILE) return;
+  const int task = (int)(e / TILE);
+  const int f = (int)(e % TILE);
+  const FixupTask tk = tasks[task];
+  double s = 0.0;
+  for (int r = 0; r < R; ++r) {
+    const double* base = buf + r * rank_stride + (size_t)tk.slot * g.qmax * (size_t)TILE + f;
+    const int nq = rank_nq[r];
+    for (int q = 0; q < nq; ++q) s += base[(size_t)q * TILE];
+  }
+  const int lane = f & 31;
+  int rr = f >> 5;
+  const int x = rr & 1;
+  rr >>= 1;
+  const int nt = rr % Cfg::NT;
+  rr /= Cfg::NT;
+  const int mt = rr % Cfg::MT;
+  const int warp = rr / Cfg::MT;
   const int wm = warp / Cfg::WARPS_N, wn = warp % Cfg::WARPS_N;
   const int2 tc = g.tiles[tk.tile];
   const int64_t row = (int64_t)tc.x * Cfg::BM + wm * Cfg::WM + mt * 8 + (lane >> 2);

@@ -49,6 +49,7 @@ struct GemmArgs {
   EpiParams ep;
   const Ctl* ctl;     // early exit when ctl->done (may be null)
   const int32_t* gate;  // early exit when non-null and *gate == 0 (in-graph CholeskyQR)
+  int32_t force_ws;     // chunk-partial plans: every CTA stores its partial (no epilogue)
 };
 
 struct FixupTask {   // one split tile
@@ -88,6 +89,7 @@ struct GemmPlan {
   int ntasks = 0;
   double* ws = nullptr;
   size_t ws_doubles = 0;
+  bool no_fixup = false;  // chunk-partial plans: the caller reduces ws (launch_gemm_chunk_sum)
   GemmPlan() = default;
   GemmPlan(const GemmPlan&) = delete;
   GemmPlan& operator=(const GemmPlan&) = delete;
@@ -97,9 +99,22 @@ struct GemmPlan {
 
 // Build a plan.  `sym_row0` >= 0 skips tiles lying strictly below the diagonal
 // of the block starting at row sym_row0 (the XᵀX half of the Gram).
+//
+// Reproducible schedules (the sharded path):
+//   fixed_splits = S > 0: every tile's K range is cut into the same S segments
+//     (segment boundaries ⌊s·ki/S⌋ depend only on K and S, not on the number
+//     of tiles), fixed up in segment order — per-element results independent
+//     of M, hence of the row partition.
+//   chunk_partials: S = K / chunk segments whose partials are all kept in ws
+//     ([task][q][BM·BN], q padded to qmax_min) for an ordered sum across ranks.
 void plan_gemm(GemmPlan& pl, int device, int size, int amode, int epi, int64_t M, int64_t N,
-               int64_t K, int64_t sym_row0 = -1, int grid_override = 0);
+               int64_t K, int64_t sym_row0 = -1, int grid_override = 0, int fixed_splits = 0,
+               bool chunk_partials = false, int qmax_min = 0);
 void launch_gemm(const GemmPlan& pl, cudaStream_t st);
+// Ordered sum of gathered chunk partials into ep.C: for every element,
+// Σ_r Σ_{q < rank_nq[r]} buf[r·rank_stride + (task·qmax + q)·BM·BN + f].
+void launch_gemm_chunk_sum(const GemmPlan& pl, const double* buf, const int32_t* rank_nq, int R,
+                           int64_t rank_stride, cudaStream_t st);
 int num_sms(int device);
 
 }  // namespace pcal

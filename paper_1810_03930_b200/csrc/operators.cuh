@@ -264,12 +264,17 @@ __global__ void k_spectral_divide(double* __restrict__ a, const double* __restri
 __global__ void k_ks_potential(const double* __restrict__ v, const double* __restrict__ rho,
                                const double* __restrict__ h, double* __restrict__ u, int64_t n,
                                double c /* (3/π)^{1/3} */, double* __restrict__ spart,
-                               const Ctl* ctl) {
+                               const Ctl* ctl, int64_t chunk = 0) {
   if (ctl && ctl->done) return;
   __shared__ double sm[kStreamThreadsOps / 32];
   double vr = 0.0, rh = 0.0, ex = 0.0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
+  // chunk > 0: block b owns rows [b·chunk, (b+1)·chunk) (reproducible sharded
+  // path); else a grid-stride loop
+  const int64_t i0 = chunk ? (int64_t)blockIdx.x * chunk + threadIdx.x
+                           : (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t i1 = chunk ? min(n, (int64_t)(blockIdx.x + 1) * chunk) : n;
+  const int64_t di = chunk ? (int64_t)blockDim.x : (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = i0; i < i1; i += di) {
     const double r = rho[i];
     const double cr = cbrt(r);
     vr += v[i] * r;

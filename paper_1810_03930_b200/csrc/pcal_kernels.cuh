@@ -184,7 +184,7 @@ __global__ void __launch_bounds__(kStreamThreads) k_eta(Ctl* ctl, const double* 
 __global__ void k_update(const double* __restrict__ x, const double* __restrict__ pg,
                          const double* __restrict__ d, double* __restrict__ z, int64_t n,
                          int64_t ld, int64_t p, int64_t chunk, double* __restrict__ npart,
-                         double* __restrict__ xpart, const Ctl* ctl) {
+                         double* __restrict__ xpart, const Ctl* ctl, int64_t cstride = 0) {
   if (ctl->done) return;
   __shared__ double sm[kStreamThreads / 32];
   const int64_t j = blockIdx.y;
@@ -204,11 +204,12 @@ __global__ void k_update(const double* __restrict__ x, const double* __restrict_
     acc += v * v;
     xacc += xv * xv;
   }
+  const int64_t cs = cstride ? cstride : p;  // row stride of the chunk-partial arrays
   const double s = block_sum<kStreamThreads>(acc, sm);
-  if (threadIdx.x == 0) npart[blockIdx.x * p + j] = s;
+  if (threadIdx.x == 0) npart[blockIdx.x * cs + j] = s;
   if (xpart) {  // sharded: ‖x_j‖² partials for the degenerate-column rule
     const double t = block_sum<kStreamThreads>(xacc, sm);
-    if (threadIdx.x == 0) xpart[blockIdx.x * p + j] = t;
+    if (threadIdx.x == 0) xpart[blockIdx.x * cs + j] = t;
   }
 }
 
@@ -226,6 +227,87 @@ __global__ void k_norm_reduce(const double* __restrict__ npart, const double* __
   }
   nrm[j] = a;
   nrm[p + j] = b;
+}
+
+// ---- reproducible (GPU-count invariant) reductions of the sharded path -----
+// Every row reduction is first taken per fixed global row chunk (chunk
+// boundaries depend only on the problem), the chunk partials
+// are all-gathered in rank order (= global chunk order) and summed
+// sequentially by k_chunk_sum, so the result is bitwise independent of the
+// number of ranks.
+
+// Stepsize inner products per (chunk, column): out[c·3p + 3j + {0,1,2}].
+__global__ void k_bb_chunk(const double* __restrict__ x, const double* __restrict__ pg,
+                           const double* __restrict__ xp, const double* __restrict__ pgp,
+                           const double* __restrict__ d, const double* __restrict__ dp, int64_t n,
+                           int64_t ld, int64_t p, int64_t chunk, double* __restrict__ out,
+                           const Ctl* ctl) {
+  if (ctl->done || ctl->iter == 0 || !ctl->have_prev) return;
+  __shared__ double sm[kStreamThreads / 32];
+  const int64_t j = blockIdx.y, c = blockIdx.x;
+  const int64_t r0 = c * chunk, r1 = min(n, r0 + chunk);
+  const double dj = d[j], dpj = dp[j];
+  double ss = 0.0, sy = 0.0, yy = 0.0;
+  for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+    const int64_t e = i + j * ld;
+    const double xv = x[e], xpv = xp[e];
+    const double sv = xv - xpv;
+    const double yv = (pg[e] - dj * xv) - (pgp[e] - dpj * xpv);
+    ss += sv * sv;
+    sy += sv * yv;
+    yy += yv * yv;
+  }
+  const double a = block_sum<kStreamThreads>(ss, sm);
+  const double b = block_sum<kStreamThreads>(sy, sm);
+  const double e = block_sum<kStreamThreads>(yy, sm);
+  if (threadIdx.x == 0) {
+    double* o = out + c * 3 * p + 3 * j;
+    o[0] = a;
+    o[1] = b;
+    o[2] = e;
+  }
+}
+
+// Per-chunk column sums of the three row-block partial arrays (f, kkt², d):
+// block (j, which, c) sums rows [c·rpc, (c+1)·rpc) of column j of array
+// `which` into out[c·3p + which·p + j] (0 where the array is absent).
+struct ChunkColArgs {
+  const double* in[3];
+  int64_t nrows[3];   // local row-block count
+  int64_t stride[3];  // column stride
+  int64_t rpc[3];     // row blocks per chunk
+  double* out;
+  int64_t p;
+};
+__global__ void __launch_bounds__(kStreamThreads) k_chunk_colsum3(ChunkColArgs a, const Ctl* ctl) {
+  if (ctl && ctl->done) return;
+  __shared__ double sm[kStreamThreads / 32];
+  const int which = blockIdx.y;
+  const int64_t col = blockIdx.x, c = blockIdx.z;
+  double acc = 0.0;
+  if (a.in[which]) {
+    const double* src = a.in[which] + col * a.stride[which];
+    const int64_t r1 = min(a.nrows[which], (c + 1) * a.rpc[which]);
+    for (int64_t r = c * a.rpc[which] + threadIdx.x; r < r1; r += blockDim.x) acc += src[r];
+  }
+  const double s = block_sum<kStreamThreads>(acc, sm);
+  if (threadIdx.x == 0) a.out[c * 3 * a.p + which * a.p + col] = s;
+}
+
+// out[w] = Σ_r Σ_{q < nq[r]} buf[r·rank_stride + q·W + w], in that order.
+__global__ void k_chunk_sum(const double* __restrict__ buf, int R, const int32_t* __restrict__ nq,
+                            int64_t rank_stride, int64_t W, double* __restrict__ out,
+                            const Ctl* ctl) {
+  if (ctl && ctl->done) return;
+  const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= W) return;
+  double s = 0.0;
+  for (int r = 0; r < R; ++r) {
+    const double* b = buf + r * rank_stride + w;
+    const int q1 = nq[r];
+    for (int q = 0; q < q1; ++q) s += b[(int64_t)q * W];
+  }
+  out[w] = s;
 }
 
 // pcal_step part 2 (solver.cpp:283-305): z ·= 1/‖z‖; a column with ‖z‖ < 1e-14

@@ -332,6 +332,14 @@ struct pcal_session {
   bool own_stream = true;
   // row sharding (null comm: the whole problem on this GPU)
   pcal::Comm* comm = nullptr;
+  // reproducible reductions (every sharded session): fixed global row chunks
+  bool repro = false;
+  int64_t chunk_rows = 0;                 // Q: rows per chunk
+  int64_t zc_planes = 0;                  // grid models: z-planes per chunk
+  int64_t nch = 0, nch_max = 0;           // local / largest per-rank chunk count
+  int32_t* rank_nch_d = nullptr;          // chunks per rank (device)
+  int grad_splits = 0;                    // dense gradient: fixed K segments
+  pcal::DevBuf cc, ccg, bbt, spt, gath, ogath;  // chunk partials, gathered, totals, Gram gathers
   int64_t n_glob = 0, row0 = 0;  // global row count, first owned row
   int64_t gz = 0;                // grid models: owned z-planes (nz for a single GPU)
   int64_t K_full = 0;            // dense: padded global row count (gradient GEMM K)
@@ -403,6 +411,26 @@ struct LaunchScope {
   explicit LaunchScope(int64_t* c) : prev(g_launch_counter) { g_launch_counter = c; }
   ~LaunchScope() { g_launch_counter = prev; }
 };
+
+// Reproducible sum of per-chunk partials (W values per chunk, `cc` layout
+// [nch_max][W]): all-gather in rank order, then the ordered chunk sum.
+static void chunk_reduce(pcal_session* s, const double* cc, int64_t W, double* out,
+                         const Ctl* ctl) {
+  const int R = s->comm->size;
+  const size_t cnt = (size_t)s->nch_max * W;
+  s->comm->allgather(cc, s->ccg.p, cnt, s->stream);
+  k_chunk_sum<<<(unsigned)ceil_div(W, 128), 128, 0, s->stream>>>(s->ccg.p, R, s->rank_nch_d,
+                                                                  (int64_t)cnt, W, out, ctl);
+  launched("k_chunk_sum");
+}
+
+// Reproducible Gram: chunk partials of the plan's ws gathered from every rank
+// and summed in global chunk order into the plan's output.
+static void gram_reduce(pcal_session* s, const GemmPlan& g, double* gath) {
+  const int R = s->comm->size;
+  s->comm->allgather(g.ws, gath, g.ws_doubles, s->stream);
+  launch_gemm_chunk_sum(g, gath, s->rank_nch_d, R, (int64_t)g.ws_doubles, s->stream);
+}
 
 // Column sums of the three partial arrays (f, kkt², d), one launch.
 static void launch_colsums(pcal_session* s, const double* fp, int64_t nrb_f, const double* kp,
@@ -533,11 +561,18 @@ static void launch_gradient(pcal_session* s, int b, const Ctl* ctl) {
       k_axis_transform<<<ng, 256, 0, s->stream>>>(s->tmpa.p, s->h.p, s->qx.p, m.nx, m.nx, m.ny,
                                                   m.nz, 0, 0, ctl);
       launched("k_axis_transform");
-      k_ks_potential<<<s->sp_blocks, 256, 0, s->stream>>>(s->V.p, s->rho.p + s->row0,
-                                                          s->h.p + s->row0, s->u.p, n, s->c_xc,
-                                                          s->spart.p, ctl);
-      launched("k_ks_potential");
-      if (s->comm) s->comm->allreduce(s->spart.p, (size_t)3 * s->sp_blocks, s->stream);
+      if (s->repro) {  // density scalars per row chunk, reduced in chunk order
+        k_ks_potential<<<(unsigned)s->nch, 256, 0, s->stream>>>(
+            s->V.p, s->rho.p + s->row0, s->h.p + s->row0, s->u.p, n, s->c_xc, s->cc.p, ctl,
+            s->chunk_rows);
+        launched("k_ks_potential");
+        chunk_reduce(s, s->cc.p, 3, s->spt.p, ctl);
+      } else {
+        k_ks_potential<<<s->sp_blocks, 256, 0, s->stream>>>(s->V.p, s->rho.p + s->row0,
+                                                            s->h.p + s->row0, s->u.p, n, s->c_xc,
+                                                            s->spart.p, ctl);
+        launched("k_ks_potential");
+      }
       launch_stencil(s, b, s->u.p, true, ctl);
       break;
     }
@@ -554,7 +589,7 @@ static void launch_eval(pcal_session* s, int b, int mode, const Ctl* ctl_guard) 
   launch_gradient(s, b, ctl_guard);
   mark(s, 2);
   launch_gemm(s->gram[b], st);
-  if (s->comm) s->comm->allreduce(s->gr.p, (size_t)2 * s->pp * s->pp, st);  // C1
+  if (s->repro) gram_reduce(s, s->gram[b], s->gath.p);  // C1
   {
     const int mc = (s->alg == PCAL_ALG_PLAMDA || s->alg == PCAL_ALG_PCALDA) ? MC_DA
                    : s->alg == PCAL_ALG_MOPTQR                               ? MC_MOPTQR
@@ -566,12 +601,35 @@ static void launch_eval(pcal_session* s, int b, int mode, const Ctl* ctl_guard) 
   launched("k_small_pxp");
   mark(s, 3);
   launch_gemm(s->xm[b], st);
-  launch_colsums(s, s->fpart.p, s->nrb_f, s->kpart.p, s->dpart.p, s->nrb_xm, Fcol(s, b),
-                 Kcol(s, b), Dvec(s, b), ctl_guard);
-  if (s->comm) {  // C2 (+ the ranks' failure flags, so every rank stops together)
+  if (s->repro) {  // C2: per-chunk column sums, gathered and summed in chunk order
+    const bool dform = s->alg == PCAL_ALG_PCAL && s->cfg.multiplier_rule == PCAL_MULT_PCAL_FORMULA;
+    const int64_t wm_xm = cfg_info(pick_size(2 * s->pp)).WM;
+    ChunkColArgs a{};
+    a.in[0] = s->fpart.p;
+    a.nrows[0] = s->nrb_f;
+    a.stride[0] = s->pstride_f;
+    a.rpc[0] = s->model.kind == PCAL_MODEL_DENSE ? s->chunk_rows / cfg_info(pick_size(s->pp)).WM
+                                                 : s->model.ny / 8;
+    a.in[1] = s->kpart.p;
+    a.in[2] = dform ? s->dpart.p : nullptr;
+    for (int w = 1; w < 3; ++w) {
+      a.nrows[w] = s->nrb_xm;
+      a.stride[w] = s->pstride_xm;
+      a.rpc[w] = s->chunk_rows / wm_xm;
+    }
+    a.out = s->cc.p;
+    a.p = s->p;
+    k_chunk_colsum3<<<dim3((unsigned)s->p, 3, (unsigned)s->nch), kStreamThreads, 0, st>>>(
+        a, ctl_guard);
+    launched("k_chunk_colsum3");
+    chunk_reduce(s, s->cc.p, 3 * s->p, s->fkd[b].p, ctl_guard);
+    // the ranks' failure flags, so every rank stops together (exact counts)
     k_flags<<<1, 1, 0, st>>>(s->ctl, s->bad, s->fkd[b].p + 3 * s->p);
     launched("k_flags");
-    s->comm->allreduce(s->fkd[b].p, (size_t)3 * s->p + 2, st);
+    s->comm->allreduce(s->fkd[b].p + 3 * s->p, 2, st);
+  } else {
+    launch_colsums(s, s->fpart.p, s->nrb_f, s->kpart.p, s->dpart.p, s->nrb_xm, Fcol(s, b),
+                   Kcol(s, b), Dvec(s, b), ctl_guard);
   }
   FinishArgs fa{};
   fa.fcol = Fcol(s, b);
@@ -579,8 +637,8 @@ static void launch_eval(pcal_session* s, int b, int mode, const Ctl* ctl_guard) 
   fa.flags = s->comm ? s->fkd[b].p + 3 * s->p : nullptr;
   fa.cpart = s->cpart.p;
   fa.ncp = s->cp_blocks;
-  fa.spart = s->spart.p;
-  fa.nsp = s->sp_blocks;
+  fa.spart = s->repro ? s->spt.p : s->spart.p;
+  fa.nsp = s->repro ? 1 : s->sp_blocks;
   fa.model = s->model.kind;
   fa.p = s->p;
   fa.mode = mode;
@@ -661,6 +719,25 @@ static void launch_iteration(pcal_session* s, int b) {
     lc.numAttrs = 1;
     PCAL_CUDA(cudaLaunchKernelExC(&lc, (const void*)k_step_fused, args));
     launched("k_step_fused");
+  } else if (s->repro) {  // C3/C4 with chunked, rank-count invariant reductions
+    const unsigned nc = (unsigned)s->nch;
+    k_bb_chunk<<<dim3(nc, (unsigned)s->p), kStreamThreads, 0, st>>>(
+        Xof(s, b), Pof(s, b), Xof(s, nb), Pof(s, nb), Dvec(s, b), Dvec(s, nb), s->n, s->ld, s->p,
+        s->chunk_rows, s->cc.p, s->ctl);
+    launched("k_bb_chunk");
+    chunk_reduce(s, s->cc.p, 3 * s->p, s->bbt.p, s->ctl);
+    k_eta<<<1, kStreamThreads, 0, st>>>(s->ctl, s->bbt.p, (int)s->p);
+    launched("k_eta");
+    dim3 gu(nc, (unsigned)s->p);
+    k_update<<<gu, kStreamThreads, 0, st>>>(Xof(s, b), Pof(s, b), Dvec(s, b), Xof(s, nb), s->n,
+                                            s->ld, s->p, s->chunk_rows, s->cc.p, s->cc.p + s->p,
+                                            s->ctl, 2 * s->p);
+    launched("k_update");
+    chunk_reduce(s, s->cc.p, 2 * s->p, s->nrm.p, s->ctl);
+    k_normalize<<<gu, kStreamThreads, 0, st>>>(Xof(s, b), Xof(s, nb), s->n, s->ld, s->p,
+                                               s->chunk_rows, s->nch, s->cc.p, s->nrm.p, s->row0,
+                                               s->n_glob, plain, s->ctl);
+    launched("k_normalize");
   } else {
     k_bb_partials<<<s->bb_blocks, kStreamThreads, 0, st>>>(Xof(s, b), Pof(s, b), Xof(s, nb),
                                                            Pof(s, nb), Dvec(s, b), Dvec(s, nb),
@@ -742,7 +819,18 @@ static void build_plans(pcal_session* s) {
     if (s->model.kind == PCAL_MODEL_DENSE) {
       GemmPlan& g = s->grad[b];
       const int sz = pick_size(pp);
-      plan_gemm(g, dev, sz, A_MCONTIG, EPI_GRAD, n, pp, s->K_full);
+      if (s->repro) {
+        // fixed K segments chosen from global sizes only: ≈ 8 CTAs per SM-wave
+        // of the whole job, ≤ 16 partials per tile
+        const CfgInfo ci = cfg_info(sz);
+        const int64_t tiles_glob = ceil_div(s->n_glob, ci.BM) * ceil_div(pp, ci.BN);
+        const int64_t ki = s->K_full / ci.BK;
+        s->grad_splits = (int)std::max<int64_t>(
+            1, std::min<int64_t>({ki, 16, ceil_div(8 * 148, tiles_glob)}));
+        plan_gemm(g, dev, sz, A_MCONTIG, EPI_GRAD, n, pp, s->K_full, -1, 0, s->grad_splits);
+      } else {
+        plan_gemm(g, dev, sz, A_MCONTIG, EPI_GRAD, n, pp, s->K_full);
+      }
       g.args.A = s->A.p;
       g.args.lda = s->ldA;
       g.args.B = s->comm ? s->xfull.p : Xof(s, b);
@@ -762,7 +850,11 @@ static void build_plans(pcal_session* s) {
     // Gram: [P|X]ᵀ·X — A = pair (KCONTIG, rows m < 2pp), B = X, K = ld
     {
       GemmPlan& g = s->gram[b];
-      plan_gemm(g, dev, pick_size(pp), A_KCONTIG, EPI_STORE, 2 * pp, pp, ld, pp);
+      if (s->repro)  // one partial per row chunk, summed across ranks in chunk order
+        plan_gemm(g, dev, pick_size(pp), A_KCONTIG, EPI_STORE, 2 * pp, pp,
+                  s->nch * s->chunk_rows, pp, 0, (int)s->nch, true, (int)s->nch_max);
+      else
+        plan_gemm(g, dev, pick_size(pp), A_KCONTIG, EPI_STORE, 2 * pp, pp, ld, pp);
       g.args.A = s->pair[b].p;
       g.args.lda = ld;
       g.args.B = Xof(s, b);
@@ -776,7 +868,8 @@ static void build_plans(pcal_session* s) {
     // X·[W|C] with the PCAL epilogue: A = X (MCONTIG, K = pp), B = mcat (pp × 2pp)
     {
       GemmPlan& g = s->xm[b];
-      plan_gemm(g, dev, pick_size(2 * pp), A_MCONTIG, EPI_XM, n, 2 * pp, pp);
+      plan_gemm(g, dev, pick_size(2 * pp), A_MCONTIG, EPI_XM, n, 2 * pp, pp, -1, 0,
+                s->repro ? 1 : 0);  // reproducible: whole tiles, no K split
       g.args.A = Xof(s, b);
       g.args.lda = ld;
       g.args.B = s->mcat.p;
@@ -797,23 +890,46 @@ static void build_plans(pcal_session* s) {
       g.args.ctl = s->ctl;
     }
   }
+  if (s->repro) s->gath.alloc((size_t)s->comm->size * s->gram[0].ws_doubles);
 }
 
-// Row partition of the sharded path: grid models by z-slabs (contiguous plane
-// ranges, the first nz % R ranks get one extra plane), dense models by row
-// blocks of ⌈n/R⌉.
+
+// Fixed global row chunks of the sharded path: every row
+// reduction is taken per chunk and the chunk partials are summed in global
+// chunk order, so results are bitwise independent of the number of ranks.
+//   dense: Q = ⌈n/64⌉ rounded up to the row-block size a (64 for p > 32,
+//          else 32: chunk boundaries fall on GEMM warp row-blocks);
+//   grid models: Zc = ⌈nz/32⌉ whole z-planes (Q = Zc·nx·ny rows).
+static void chunking(const pcal_model_desc& m, int64_t* Q, int64_t* NC, int64_t* Zc) {
+  if (m.kind == PCAL_MODEL_DENSE) {
+    const int64_t a = padded_p(m.p) >= 64 ? 64 : 32;
+    *Q = round_up(ceil_div(m.n, 64), a);
+    *NC = ceil_div(m.n, *Q);
+    *Zc = 0;
+  } else {
+    *Zc = ceil_div(m.nz, 32);
+    *NC = ceil_div(m.nz, *Zc);
+    *Q = *Zc * m.nx * m.ny;
+  }
+}
+
+// Row partition of the sharded path: rank r owns the chunks
+// [⌊r·NC/R⌋, ⌊(r+1)·NC/R⌋) — whole z-planes for the grid models.
 static void partition(const pcal_model_desc& m, int R, int r, int64_t* row0, int64_t* rows,
                       int64_t* z0, int64_t* nzl) {
+  int64_t Q, NC, Zc;
+  chunking(m, &Q, &NC, &Zc);
+  if (R > NC)
+    throw Error(PCAL_E_PARAMETER, "more ranks than row chunks (" + std::to_string(NC) + ")");
+  const int64_t c0 = (int64_t)r * NC / R, c1 = (int64_t)(r + 1) * NC / R;
   if (m.kind == PCAL_MODEL_DENSE) {
-    const int64_t base = m.n / R, rem = m.n % R;
-    *row0 = r * base + std::min<int64_t>(r, rem);
-    *rows = base + (r < rem ? 1 : 0);
+    *row0 = c0 * Q;
+    *rows = std::min(c1 * Q, m.n) - *row0;
     *z0 = 0;
     *nzl = 0;
   } else {
-    const int64_t base = m.nz / R, rem = m.nz % R;
-    *z0 = r * base + std::min<int64_t>(r, rem);
-    *nzl = base + (r < rem ? 1 : 0);
+    *z0 = c0 * Zc;
+    *nzl = std::min(c1 * Zc, m.nz) - *z0;
     *row0 = *z0 * m.nx * m.ny;
     *rows = *nzl * m.nx * m.ny;
   }
@@ -843,7 +959,10 @@ static void alloc_state(pcal_session* s) {
                   s->gz >= 1;
     if (s->comm && m.kind != PCAL_MODEL_DENSE && !s->st_march)
       throw Error(PCAL_E_UNSUPPORTED, "sharded grid models need nx <= 128 and ny % 8 == 0");
-    if (s->st_march) {  // enough blocks for ≈ 8 per SM
+    if (s->repro) {  // one z-chunk per row chunk: f partials per (y-tile, chunk)
+      s->st_zchunk = s->zc_planes;
+      s->st_nzc = s->nch;
+    } else if (s->st_march) {  // enough blocks for ≈ 8 per SM
       const int64_t tiles = (m.ny / 8) * p;
       int64_t nzc = std::max<int64_t>(1, std::min<int64_t>(s->gz, ceil_div(8 * 148, tiles)));
       s->st_zchunk = ceil_div(s->gz, nzc);
@@ -897,7 +1016,17 @@ static void alloc_state(pcal_session* s) {
   s->bbpart.alloc((size_t)3 * s->bb_blocks);
   s->up_chunk = std::max<int64_t>(1024, round_up(ceil_div(n * p, 8 * 148 * 4), 256));
   s->up_chunk = std::min<int64_t>(s->up_chunk, round_up(n, 256));
+  if (s->repro) s->up_chunk = s->chunk_rows;  // norm partials per row chunk
   s->up_nchunks = ceil_div(n, s->up_chunk);
+  if (s->repro) {
+    const int R = s->comm->size;
+    s->cc.alloc((size_t)s->nch_max * 3 * p);
+    s->cc.zero(st);
+    s->ccg.alloc((size_t)R * s->nch_max * 3 * p);
+    s->bbt.alloc((size_t)3 * p);
+    s->spt.alloc(3);
+    s->spt.zero(st);
+  }
   s->npart.alloc((size_t)s->up_nchunks * p);
   s->xpart.alloc((size_t)s->up_nchunks * p);
   s->nrm.alloc((size_t)2 * p);
@@ -1046,6 +1175,7 @@ pcal_session::~pcal_session() {
   for (auto& e : pev)
     if (e) cudaEventDestroy(e);
   if (bad) cudaFree(bad);
+  if (rank_nch_d) cudaFree(rank_nch_d);
   if (ctl) cudaFree(ctl);
   if (h_ctl) cudaFreeHost(h_ctl);
   if (stream && own_stream) cudaStreamDestroy(stream);
@@ -1112,6 +1242,24 @@ void session_create(const pcal_model_desc* model, const pcal_config* config, con
   s->n = s->rank_rows[rk];
   s->ld_max = padded_ld(maxrows);
   s->ld = comm ? s->ld_max : padded_ld(s->n);
+  if (comm) {  // reproducible chunked reductions
+    int64_t Q, NC, Zc;
+    chunking(*model, &Q, &NC, &Zc);
+    if (model->kind != PCAL_MODEL_DENSE && (model->nx * model->ny) % 64 != 0)
+      throw Error(PCAL_E_UNSUPPORTED, "sharded grid models need nx*ny to be a multiple of 64");
+    s->repro = true;
+    s->chunk_rows = Q;
+    s->zc_planes = Zc;
+    std::vector<int32_t> nq(R);
+    for (int r = 0; r < R; ++r) {
+      nq[r] = (int32_t)((int64_t)(r + 1) * NC / R - (int64_t)r * NC / R);
+      s->nch_max = std::max<int64_t>(s->nch_max, nq[r]);
+    }
+    s->nch = nq[rk];
+    s->ld_max = s->ld = s->nch_max * Q;  // every chunk's rows fit (zero padded)
+    PCAL_CUDA(cudaMalloc(&s->rank_nch_d, sizeof(int32_t) * R));
+    PCAL_CUDA(cudaMemcpy(s->rank_nch_d, nq.data(), sizeof(int32_t) * R, cudaMemcpyHostToDevice));
+  }
   s->K_full = padded_ld(s->n_glob);
   s->alg = config->algorithm;
   if (comm && s->alg == PCAL_ALG_MOPTQR)
@@ -1203,8 +1351,15 @@ bool orthonormalize_dev(pcal_session* s, const double* x, double* q, double* scr
   GemmPlan& gp = s->orth_gram;
   GemmPlan& mp = s->orth_mul;
   if (!gp.d_tiles) {
-    plan_gemm(gp, s->device, pick_size(pp), A_KCONTIG, EPI_STORE, pp, pp, ld, 0);
-    plan_gemm(mp, s->device, pick_size(pp), A_MCONTIG, EPI_STORE, n, pp, pp);
+    if (s->repro) {  // chunked Gram + whole-tile products (rank-count invariant)
+      plan_gemm(gp, s->device, pick_size(pp), A_KCONTIG, EPI_STORE, pp, pp,
+                s->nch * s->chunk_rows, 0, 0, (int)s->nch, true, (int)s->nch_max);
+      plan_gemm(mp, s->device, pick_size(pp), A_MCONTIG, EPI_STORE, n, pp, pp, -1, 0, 1);
+      s->ogath.alloc((size_t)s->comm->size * gp.ws_doubles);
+    } else {
+      plan_gemm(gp, s->device, pick_size(pp), A_KCONTIG, EPI_STORE, pp, pp, ld, 0);
+      plan_gemm(mp, s->device, pick_size(pp), A_MCONTIG, EPI_STORE, n, pp, pp);
+    }
   }
   auto gram_of = [&](const double* a) {
     gp.args.A = a;
@@ -1217,7 +1372,7 @@ bool orthonormalize_dev(pcal_session* s, const double* x, double* q, double* scr
     gp.args.ep.n_store = pp;
     gp.args.ctl = nullptr;
     launch_gemm(gp, st);
-    if (s->comm) s->comm->allreduce(s->orth_b.p, (size_t)pp * pp, st);  // sharded Gram
+    if (s->repro) gram_reduce(s, gp, s->ogath.p);  // sharded Gram
   };
   auto mul_t = [&](const double* a, double* out) {  // out = a · T
     mp.args.A = a;
