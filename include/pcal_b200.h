@@ -169,16 +169,26 @@ int pcal_session_profile_kernels(pcal_session* s, int64_t iters, char* buf, int6
 int64_t pcal_session_kernels_per_iteration(pcal_session* s);
 
 /* ---- row-sharded multi-GPU solve (one process per GPU, NCCL) -------------
- * Rows are split by z-slabs (grid models) or row blocks (dense); every n×p
- * object is row-local, p×p objects are replicated, and per iteration the ranks
- * exchange the Gram partials, per-column sums, stepsize partials, column norms
- * and the halo planes / X allgather.  A sharded session takes
- * the GLOBAL sizes in `model` (n, p, nx, ny, nz) but LOCAL data: dense `a` =
- * rows [row0, row0+nrows) of A for all n columns (ld = nrows), `g0`, `v` and
- * x0 = the owned rows.  pcal_partition tells each rank its rows. */
+ * Rows are split into fixed global row chunks (pcal_row_chunks: whole z-plane
+ * groups for the grid models, row blocks for dense) and rank r of R owns the
+ * chunks [⌊r·NC/R⌋, ⌊(r+1)·NC/R⌋).  Every n×p object is row-local, p×p
+ * objects are replicated, and per iteration the ranks exchange per-chunk
+ * partials of the Gram, column sums, stepsize inner products and column norms
+ * (all-gathered and summed in global chunk order, so results are bitwise
+ * identical for every rank count — the reference's thread-count invariance,
+ * harness.cpp:131-137) plus the halo planes / X allgather.  A
+ * sharded session takes the GLOBAL sizes in `model` (n, p, nx, ny, nz) but
+ * LOCAL data: dense `a` = rows [row0, row0+nrows) of A for all n columns
+ * (ld = nrows), `g0`, `v` and x0 = the owned rows.  pcal_partition tells each
+ * rank its rows. */
 typedef struct pcal_comm pcal_comm;
 int pcal_partition(const pcal_model_desc* model, int32_t nranks, int32_t rank, int64_t* row0,
                    int64_t* nrows);
+/* Number of visible CUDA devices (0 without a GPU; never fails). */
+int pcal_device_count(int32_t* count);
+/* The fixed row chunking of the sharded path: rows per chunk and chunk count
+ * (the largest usable rank count). */
+int pcal_row_chunks(const pcal_model_desc* model, int64_t* chunk_rows, int64_t* nchunks);
 /* 128-byte NCCL unique id (rank 0 creates it, the caller broadcasts it). */
 int pcal_nccl_unique_id(void* out);
 int pcal_comm_create_nccl(int32_t nranks, int32_t rank, const void* unique_id, int32_t device,
@@ -190,12 +200,13 @@ int pcal_session_create_sharded(const pcal_model_desc* local_model, const pcal_c
 /* report rows (stop_x / final_x) are the local rows (nrows × p). */
 int pcal_solve_sharded(const pcal_model_desc* local_model, const pcal_config* config,
                        const double* x0_local, int32_t x0_location, pcal_comm* comm,
-                       pcal_report* report);
+                       pcal_report* report, pcal_category_timers* timers /* nullable */);
 /* The sharded algorithm with `nranks` emulated ranks on ONE GPU (host threads,
  * loopback collectives): validates the multi-GPU path where one GPU exists.
  * Global host data in, global report out. */
 int pcal_solve_emulated(const pcal_model_desc* model, const pcal_config* config, const double* x0,
-                        int32_t nranks, pcal_report* report);
+                        int32_t nranks, pcal_report* report,
+                        pcal_category_timers* timers /* nullable: rank 0's categories */);
 
 /* ---- building blocks (host buffers; for parity tests and tools) ---------- */
 /* C = Aᵀ·B for n×pa and n×pb (kernels.cpp:124-137 matmul_at_b). */

@@ -153,9 +153,11 @@ def lib() -> C.CDLL:
     L.pcal_session_create_sharded.argtypes = [C.POINTER(_Model), C.POINTER(_Config), vp, i32, vp,
                                               C.POINTER(vp)]
     L.pcal_solve_sharded.argtypes = [C.POINTER(_Model), C.POINTER(_Config), vp, i32, vp,
-                                     C.POINTER(_Report)]
+                                     C.POINTER(_Report), C.POINTER(_Timers)]
     L.pcal_solve_emulated.argtypes = [C.POINTER(_Model), C.POINTER(_Config), vp, i32,
-                                      C.POINTER(_Report)]
+                                      C.POINTER(_Report), C.POINTER(_Timers)]
+    L.pcal_row_chunks.argtypes = [C.POINTER(_Model), C.POINTER(i64), C.POINTER(i64)]
+    L.pcal_device_count.argtypes = [C.POINTER(i32)]
     _lib = L
     return L
 
@@ -583,26 +585,53 @@ def partition(model: _ModelBase, nranks: int, rank: int) -> tuple:
     return r0.value, nr.value
 
 
-def solve_emulated(model: _ModelBase, config: SolverConfig, x0, nranks: int) -> RunReport:
+def _timed_call(timers, fn):
+    tm = _Timers() if timers is not None else None
+    fn(C.byref(tm) if tm is not None else None)
+    if timers is not None:
+        timers.blas3 += tm.blas3
+        timers.func += tm.func
+        timers.orth += tm.orth
+
+
+def device_count() -> int:
+    """Visible CUDA devices (0 without a GPU)."""
+    c = C.c_int32()
+    lib().pcal_device_count(C.byref(c))
+    return c.value
+
+
+def row_chunks(model: _ModelBase) -> tuple:
+    """(rows per chunk, chunk count) of the sharded path's fixed row chunking."""
+    cm, keep = model._c()
+    q, nc = C.c_int64(), C.c_int64()
+    _check(lib().pcal_row_chunks(C.byref(cm), C.byref(q), C.byref(nc)))
+    return q.value, nc.value
+
+
+def solve_emulated(model: _ModelBase, config: SolverConfig, x0, nranks: int,
+                   timers: Optional[CategoryTimers] = None) -> RunReport:
     """The sharded algorithm with `nranks` emulated ranks on one GPU (loopback
-    collectives); global host data in, global report out."""
+    collectives); global host data in, global report out.  `timers` receives
+    rank 0's blas3 / func / orth categories."""
     cm, keep = model._c()
     cc = config._c()
     x0 = _f64(x0)
     rep, trace, stop_x, final_x = _new_report(model.n, model.p, config.max_iter)
-    _check(lib().pcal_solve_emulated(C.byref(cm), C.byref(cc), _ptr(x0), nranks, C.byref(rep)))
+    _timed_call(timers, lambda t: _check(lib().pcal_solve_emulated(
+        C.byref(cm), C.byref(cc), _ptr(x0), nranks, C.byref(rep), t)))
     return _report_from(rep, trace, stop_x, final_x)
 
 
 def solve_sharded(model: _ModelBase, config: SolverConfig, x0_local, comm: "Comm",
-                  n_local: int) -> RunReport:
+                  n_local: int, timers: Optional[CategoryTimers] = None) -> RunReport:
     """Row-sharded pcal_solve on this rank (host buffers: local slabs in, local rows out)."""
     cm, keep = model._c()
     cc = config._c()
     x0_local = _f64(x0_local)
     rep, trace, stop_x, final_x = _new_report(n_local, model.p, config.max_iter)
-    _check(lib().pcal_solve_sharded(C.byref(cm), C.byref(cc), _ptr(x0_local), HOST, comm._h,
-                                    C.byref(rep)))
+    _timed_call(timers, lambda t: _check(lib().pcal_solve_sharded(
+        C.byref(cm), C.byref(cc), _ptr(x0_local), HOST, comm._h, C.byref(rep), t)))
     return _report_from(rep, trace, stop_x, final_x)
 
 

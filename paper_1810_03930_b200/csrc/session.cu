@@ -2074,6 +2074,24 @@ int pcal_partition(const pcal_model_desc* m, int32_t nranks, int32_t rank, int64
   });
 }
 
+int pcal_device_count(int32_t* count) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    n = 0;
+  }
+  if (count) *count = n;
+  return PCAL_OK;
+}
+
+int pcal_row_chunks(const pcal_model_desc* m, int64_t* chunk_rows, int64_t* nchunks) {
+  return guarded([&] {
+    if (!m || !chunk_rows || !nchunks) throw Error(PCAL_E_PARAMETER, "NULL argument");
+    int64_t zc;
+    chunking(*m, chunk_rows, nchunks, &zc);
+  });
+}
+
 int pcal_nccl_unique_id(void* out) {
   return guarded([&] { nccl_unique_id(out); });
 }
@@ -2100,10 +2118,10 @@ int pcal_session_create_sharded(const pcal_model_desc* local_model, const pcal_c
 
 int pcal_solve_sharded(const pcal_model_desc* local_model, const pcal_config* config,
                        const double* x0_local, int32_t x0_location, pcal_comm* comm,
-                       pcal_report* report) {
+                       pcal_report* report, pcal_category_timers* timers) {
   return guarded([&] {
     pcal_session* s = nullptr;
-    session_create(local_model, config, x0_local, x0_location, &s, nullptr,
+    session_create(local_model, config, x0_local, x0_location, &s, timers,
                    comm ? comm->c : nullptr);
     std::unique_ptr<pcal_session> guard(s);
     session_run(s, config->max_iter);
@@ -2115,7 +2133,7 @@ int pcal_solve_sharded(const pcal_model_desc* local_model, const pcal_config* co
 // on the group's shared stream; the collectives meet at host barriers.  The
 // global report gets rank 0's trace and scalars and every rank's rows of X.
 int pcal_solve_emulated(const pcal_model_desc* model, const pcal_config* config, const double* x0,
-                        int32_t nranks, pcal_report* report) {
+                        int32_t nranks, pcal_report* report, pcal_category_timers* timers) {
   return guarded([&] {
     if (!model || !config || !x0 || !report) throw Error(PCAL_E_PARAMETER, "NULL argument");
     if (model->location != PCAL_HOST) throw Error(PCAL_E_PARAMETER, "emulation takes host data");
@@ -2172,8 +2190,8 @@ int pcal_solve_emulated(const pcal_model_desc* model, const pcal_config* config,
             m.v = model->v + r0[r];
           }
           pcal_session* s = nullptr;
-          session_create(&m, config, x_loc[r].data(), PCAL_HOST, &s, nullptr, comms[r].get(),
-                         group.stream);
+          session_create(&m, config, x_loc[r].data(), PCAL_HOST, &s, r == 0 ? timers : nullptr,
+                         comms[r].get(), group.stream);
           std::unique_ptr<pcal_session> guard(s);
           session_run(s, config->max_iter);
           session_finish(s, &reps[r]);

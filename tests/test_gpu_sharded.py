@@ -157,3 +157,30 @@ def test_sharded_results_bitwise_identical_across_gpu_counts(pcal, orc, kind):
         assert report_io.same_numerics(reps[0], r)
     # and the chunked path stays within the parity tolerances of the single-GPU solve
     check_pair(pcal.solve(m, cfg, x0), reps[0], window=40)
+
+
+def test_run_scaling_emulated_reports_identical_results(pcal, orc):
+    """run_scaling (harness.cpp:106-138) over 1, 2, 4 emulated GPUs."""
+    import json
+    from paper_1810_03930_b200 import scaling
+    m, x0 = _scaling_case(pcal, orc, "stencil")
+    cfg = pcal.SolverConfig(tol_rel_kkt=TINY, max_iter=30)
+    rep = scaling.run_scaling(m, cfg, x0, gpus=[1, 2, 4], mode="emulated")
+    assert rep.identical_results and rep.hardware_oversubscribed
+    assert rep.gpus == [1, 2, 4] and rep.speedups[0] == 1.0
+    assert all(c.func > 0.0 and c.blas3 > 0.0 and c.orth > 0.0 for c in rep.categories)
+    j = json.loads(scaling.to_json(rep))
+    assert j["iterations"] == 30 and j["status"] == "max-iter" and j["threads"] == [1, 2, 4]
+
+
+def test_run_scaling_nccl_process_per_gpu(pcal, orc):
+    """The one-process-per-GPU launch (torch.distributed.run + NCCL) on the GPUs
+    present, checked bitwise against the emulated run of the same rank count."""
+    from paper_1810_03930_b200 import report_io, scaling
+    m, x0 = _scaling_case(pcal, orc, "dense")
+    cfg = pcal.SolverConfig(tol_rel_kkt=TINY, max_iter=25)
+    g = [1] + ([2] if scaling.visible_gpus() >= 2 else [])
+    rep = scaling.run_scaling(m, cfg, x0, gpus=g, mode="nccl", timeout=600)
+    assert rep.identical_results and not rep.hardware_oversubscribed
+    em = pcal.solve_emulated(m, cfg, x0, 1)
+    assert report_io.same_numerics(rep.runs[0], em)
