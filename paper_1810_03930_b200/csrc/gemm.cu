@@ -1,5 +1,6 @@
 // gemm.cu — stream-K DMMA GEMM: configurations, schedules, launches.
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "../../include/pcal_b200.h"
@@ -49,6 +50,16 @@ int pick_size(int64_t N) {
   return CFG_SMALL;
 }
 
+int64_t count_tiles(int size, int64_t M, int64_t N, int64_t sym_row0) {
+  const CfgInfo ci = cfg_info(size);
+  int64_t c = 0;
+  for (int64_t tm = 0; tm < ceil_div(M, ci.BM); ++tm)
+    for (int64_t tn = 0; tn < ceil_div(N, ci.BN); ++tn)
+      if (!(sym_row0 >= 0 && tm * ci.BM >= sym_row0 && (tm * ci.BM - sym_row0) > (tn + 1) * ci.BN - 1))
+        ++c;
+  return c;
+}
+
 void plan_gemm(GemmPlan& pl, int device, int size, int amode, int epi, int64_t M,
                       int64_t N, int64_t K, int64_t sym_row0, int grid_override, int fixed_splits,
                       bool chunk_partials, int qmax_min) {
@@ -77,9 +88,18 @@ void plan_gemm(GemmPlan& pl, int device, int size, int amode, int epi, int64_t M
   int grid = grid_override > 0 ? grid_override : num_sms(device);
   if (units < grid) grid = (int)std::max<int64_t>(1, units);
   int64_t upc = 0;
+  int segs = 0;
   if (fixed_splits > 0) {
+    // segmented schedule: S fixed K segments per tile, whole segments per CTA
     if (fixed_splits > ki) throw Error(PCAL_E_DIMENSION, "gemm: more segments than k-slices");
-    grid = ntiles * fixed_splits;  // CTA t·S + s: tile t, k-iterations [⌊s·ki/S⌋, ⌊(s+1)·ki/S⌋)
+    segs = fixed_splits;
+    const int64_t nseg = (int64_t)ntiles * segs;
+    const int g0 = grid_override > 0 ? grid_override : num_sms(device);
+    // long segments: one CTA each (the next CTA's pipeline fill overlaps this
+    // one's partial store); short segments: persistent CTAs walk several
+    const char* env = getenv("PCAL_SEG_GRID");
+    const bool one_each = env ? env[0] == 'f' : (int64_t)ki / segs >= 32;
+    grid = (int)(one_each ? nseg : std::min<int64_t>(nseg, g0));
   } else {
     // Enough tiles for every SM: data-parallel whole tiles (no partials, no
     // fixup); otherwise stream-K so tall-skinny / few-tile products fill the chip.
@@ -101,13 +121,22 @@ void plan_gemm(GemmPlan& pl, int device, int size, int amode, int epi, int64_t M
   std::vector<int32_t> split(ntiles, -1);
   std::vector<FixupTask> tasks;
   int qmax = 1;
-  for (int t = 0; t < ntiles && upc == 0; ++t) {
-    const int32_t cf = cta_of_unit((int64_t)t * ki, units, grid);
-    const int32_t cl = cta_of_unit((int64_t)(t + 1) * ki - 1, units, grid);
-    if (cf != cl || chunk_partials) {
-      split[t] = (int32_t)tasks.size();
-      tasks.push_back({t, (int32_t)tasks.size(), cl - cf + 1});
-      qmax = std::max(qmax, cl - cf + 1);
+  if (segs > 0) {
+    if (segs > 1 || chunk_partials)
+      for (int t = 0; t < ntiles; ++t) {
+        split[t] = t;
+        tasks.push_back({t, t, segs});
+      }
+    qmax = segs;
+  } else {
+    for (int t = 0; t < ntiles && upc == 0; ++t) {
+      const int32_t cf = cta_of_unit((int64_t)t * ki, units, grid);
+      const int32_t cl = cta_of_unit((int64_t)(t + 1) * ki - 1, units, grid);
+      if (cf != cl || chunk_partials) {
+        split[t] = (int32_t)tasks.size();
+        tasks.push_back({t, (int32_t)tasks.size(), cl - cf + 1});
+        qmax = std::max(qmax, cl - cf + 1);
+      }
     }
   }
   if (chunk_partials) qmax = std::max(qmax, qmax_min);
@@ -138,6 +167,7 @@ void plan_gemm(GemmPlan& pl, int device, int size, int amode, int epi, int64_t M
   g.ws = pl.ws;
   g.qmax = qmax;
   g.force_ws = chunk_partials ? 1 : 0;
+  g.segs = segs;
   pl.no_fixup = chunk_partials;
 }
 
@@ -190,26 +220,36 @@ void launch_gemm(const GemmPlan& pl, cudaStream_t st) {
   (void)0;
 }
 
-template <class Cfg>
-static void chunk_sum_cfg(const GemmPlan& pl, const double* buf, const int32_t* rank_nq, int R,
-                          int64_t rank_stride, cudaStream_t st) {
-  const int64_t total = (int64_t)pl.ntasks * Cfg::BM * Cfg::BN;
-  gemm_chunk_sum_store<Cfg><<<(unsigned)((total + 255) / 256), 256, 0, st>>>(
-      pl.args, pl.d_tasks, pl.ntasks, buf, rank_nq, R, rank_stride);
-  launched("gram_chunk_sum");
+void launch_gemm_tree_local(const GemmPlan& pl, const int2* nodes, int nnodes, int64_t leaf0,
+                            int64_t nleaves, double* out, cudaStream_t st) {
+  const CfgInfo ci = cfg_info(pl.size);
+  const int tile = ci.BM * ci.BN;
+  const int64_t total = (int64_t)pl.ntasks * tile;
+  gemm_tree_local<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(
+      pl.ws, pl.args.qmax, pl.ntasks, tile, nodes, nnodes, leaf0, nleaves, out, pl.args.ctl);
+  launched("gram_tree_local");
   PCAL_CUDA(cudaGetLastError());
 }
 
-void launch_gemm_chunk_sum(const GemmPlan& pl, const double* buf, const int32_t* rank_nq, int R,
-                           int64_t rank_stride, cudaStream_t st) {
-  if (pl.amode != A_KCONTIG || pl.epi != EPI_STORE || !pl.no_fixup)
-    throw Error(PCAL_E_STATE, "gemm: chunk sums need a K-contiguous chunk-partial plan");
-  switch (pl.size) {
-    case CFG_BIG: chunk_sum_cfg<CfgBig<A_KCONTIG>>(pl, buf, rank_nq, R, rank_stride, st); break;
-    case CFG_MID: chunk_sum_cfg<CfgMid<A_KCONTIG>>(pl, buf, rank_nq, R, rank_stride, st); break;
-    default: chunk_sum_cfg<CfgSmall<A_KCONTIG>>(pl, buf, rank_nq, R, rank_stride, st); break;
-  }
+template <class Cfg>
+static void tree_final_cfg(const GemmPlan& pl, const double* buf, const int32_t* cnt,
+                           const int2* nodes, int R, int maxn, cudaStream_t st) {
+  const int64_t total = (int64_t)pl.ntasks * Cfg::BM * Cfg::BN;
+  gemm_tree_final<Cfg><<<(unsigned)((total + 255) / 256), 256, 0, st>>>(
+      pl.args, pl.d_tasks, pl.ntasks, buf, cnt, nodes, R, maxn);
+  launched("gram_tree_final");
+  PCAL_CUDA(cudaGetLastError());
 }
 
+void launch_gemm_tree_final(const GemmPlan& pl, const double* buf, const int32_t* cnt,
+                            const int2* nodes, int R, int maxn, cudaStream_t st) {
+  if (pl.amode != A_KCONTIG || pl.epi != EPI_STORE || !pl.no_fixup)
+    throw Error(PCAL_E_STATE, "gemm: tree sums need a K-contiguous chunk-partial plan");
+  switch (pl.size) {
+    case CFG_BIG: tree_final_cfg<CfgBig<A_KCONTIG>>(pl, buf, cnt, nodes, R, maxn, st); break;
+    case CFG_MID: tree_final_cfg<CfgMid<A_KCONTIG>>(pl, buf, cnt, nodes, R, maxn, st); break;
+    default: tree_final_cfg<CfgSmall<A_KCONTIG>>(pl, buf, cnt, nodes, R, maxn, st); break;
+  }
+}
 
 }  // namespace pcal

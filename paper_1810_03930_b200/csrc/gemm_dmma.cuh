@@ -316,16 +316,15 @@ __device__ __forceinline__ void produce(const GemmArgs& g, double* As, double* B
   const int64_t a_rows = Cfg::AMODE == A_MCONTIG ? 64 : RPP * g.lda;  // stride between lane chunks
   const int64_t b_rows = RPP * g.ldb;
   const int lr = lane / CPR, lc = 2 * (lane % CPR);
+  int t = (int)(u0 / g.ki), kk = (int)(u0 % g.ki);  // advanced incrementally
+  int s = 0;
+  unsigned ph = 0;
   for (int64_t u = u0; u < u1; ++u) {
-    const int64_t i = u - u0;
-    const int s = (int)(i % S);
-    const unsigned ph = (unsigned)((i / S) & 1);
-    const int t = (int)(u / g.ki);
-    if (t != cur_tile) {  // (re)base on this tile at k-iteration u % ki
+    if (t != cur_tile) {  // (re)base on this tile at k-iteration kk
       cur_tile = t;
       const int2 tc = g.tiles[t];
       const int64_t m0 = (int64_t)tc.x * BM, n0 = (int64_t)tc.y * BN;
-      const int64_t k0 = (u % g.ki) * BK;
+      const int64_t k0 = (int64_t)kk * BK;
       amask = 0;
       bmask = 0;
       if constexpr (Cfg::AMODE == A_MCONTIG) {
@@ -371,6 +370,14 @@ __device__ __forceinline__ void produce(const GemmArgs& g, double* As, double* B
     cp_async_mbar_arrive(&full[s]);
     pa += a_step;
     pb += BK;
+    if (++s == S) {
+      s = 0;
+      ph ^= 1u;
+    }
+    if (++kk == g.ki) {
+      kk = 0;
+      ++t;
+    }
   }
 }
 
@@ -389,8 +396,10 @@ __global__ void __launch_bounds__(Cfg::THREADS + 128, 1) gemm_streamk(GemmArgs g
   uint64_t* empty = full + Cfg::STAGES;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int32_t cta = blockIdx.x;
-  const int64_t u0 = cta_unit_begin(cta, g.units, g.grid, g.upc);
-  const int64_t u1 = cta_unit_begin(cta + 1, g.units, g.grid, g.upc);
+  const int64_t u0 = g.segs ? seg_unit_begin(cta, g.ntiles, g.ki, g.segs, g.grid)
+                            : cta_unit_begin(cta, g.units, g.grid, g.upc);
+  const int64_t u1 = g.segs ? seg_unit_begin(cta + 1, g.ntiles, g.ki, g.segs, g.grid)
+                            : cta_unit_begin(cta + 1, g.units, g.grid, g.upc);
   if (u0 >= u1) return;
   if (threadIdx.x == 0) {
     for (int s = 0; s < Cfg::STAGES; ++s) {
@@ -425,25 +434,36 @@ __global__ void __launch_bounds__(Cfg::THREADS + 128, 1) gemm_streamk(GemmArgs g
 #pragma unroll
     for (int nt = 0; nt < Cfg::NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
 
-  int64_t seg_begin = u0;  // first unit of the current tile segment
+  // tile / k-iteration / segment counters advance incrementally (no 64-bit
+  // divisions on the DMMA issue path)
+  int t = (int)(u0 / g.ki);
+  int kk = (int)(u0 % g.ki);
+  const int S = g.segs;
+  int cur_seg = S > 1 ? seg_of(kk, g.ki, S) : 0;
+  int seg_stop = S > 1 ? (int)((int64_t)(cur_seg + 1) * g.ki / S) : g.ki;  // exclusive, in kk
+  bool tile_start = kk == 0;  // this CTA's current tile segment began at the tile's k = 0
+  int stage = 0;
+  unsigned phase = 0;
   for (int64_t u = u0; u < u1; ++u) {
-    const int64_t i = u - u0;
-    const int s = (int)(i % Cfg::STAGES);
-    mbar_wait(&full[s], (unsigned)((i / Cfg::STAGES) & 1));
-    mma_stage<Cfg>(As + s * Cfg::A_STAGE, Bs + s * Cfg::B_STAGE, wm, wn, lane, acc);
+    mbar_wait(&full[stage], phase);
+    mma_stage<Cfg>(As + stage * Cfg::A_STAGE, Bs + stage * Cfg::B_STAGE, wm, wn, lane, acc);
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
+    if (lane == 0) mbar_arrive(&empty[stage]);
+    if (++stage == Cfg::STAGES) {
+      stage = 0;
+      phase ^= 1u;
+    }
 
-    const int t = (int)(u / g.ki);
-    const int kk = (int)(u % g.ki);
-    if (kk == g.ki - 1 || u == u1 - 1) {
+    const bool tile_end = kk == g.ki - 1;
+    const bool seg_end = kk + 1 == seg_stop;  // == tile_end without segments
+    if (tile_end || seg_end || u == u1 - 1) {
       const int2 tc = g.tiles[t];
-      const bool whole = (seg_begin % g.ki == 0) && kk == g.ki - 1 && !g.force_ws;
+      const bool whole = tile_start && tile_end && !g.force_ws && S <= 1;
       if (whole) {
         epilogue<Cfg, EPI>(g, tc.x, tc.y, wm, wn, lane, acc);
       } else {
         const int slot = g.split_slot[t];
-        const int q = cta - cta_of_unit((int64_t)t * g.ki, g.units, g.grid);
+        const int q = S ? cur_seg : cta - cta_of_unit((int64_t)t * g.ki, g.units, g.grid);
         double* w = g.ws + ((size_t)slot * g.qmax + q) * (size_t)(Cfg::BM * Cfg::BN);
 #pragma unroll
         for (int mt = 0; mt < Cfg::MT; ++mt)
@@ -456,7 +476,19 @@ __global__ void __launch_bounds__(Cfg::THREADS + 128, 1) gemm_streamk(GemmArgs g
       for (int mt = 0; mt < Cfg::MT; ++mt)
 #pragma unroll
         for (int nt = 0; nt < Cfg::NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
-      seg_begin = u + 1;
+      tile_start = tile_end;
+    }
+    if (tile_end) {
+      kk = 0;
+      ++t;
+      cur_seg = 0;
+      seg_stop = S > 1 ? g.ki / S : g.ki;
+    } else {
+      ++kk;
+      if (seg_end) {
+        ++cur_seg;
+        seg_stop = (int)((int64_t)(cur_seg + 1) * g.ki / S);
+      }
     }
   }
 }
@@ -524,27 +556,93 @@ __global__ void __launch_bounds__(256) gemm_fixup_store(GemmArgs g, const FixupT
   if (row < ep.m_store && col < ep.n_store) ep.C[row + col * ep.ldc] = s;
 }
 
-// Ordered sum of chunk partials gathered from R ranks (reproducible Gram):
-// the per-element sequence is (rank 0 chunks, rank 1 chunks, …) = the global
-// chunk order, so the result does not depend on how chunks map to ranks.
+// ---- fixed-tree reduction of chunk partials (reproducible Gram) -------------
+// The S_glob chunk partials (leaves, in global chunk order) are summed over a
+// fixed binary tree: node (ℓ, i) covers leaves [i·2^ℓ, min((i+1)·2^ℓ, S_glob))
+// and equals left + right (left alone when the right child is empty).  Each
+// rank sums the maximal nodes inside its own leaf range (gemm_tree_local), the
+// ranks exchange only those O(log S) node sums, and every rank finishes the
+// same tree (gemm_tree_final): bitwise the same Gram for every rank count.
+
+// Sum of the n leaves of one aligned node: binary counter + right fold.
+__device__ __forceinline__ double tree_leaves(const double* leaf, int64_t stride, int n) {
+  double st[24];
+  int sp = 0;
+  int j = 0;
+  for (; j + 8 <= n; j += 8) {  // aligned 8-leaf blocks: 8 loads in flight, pairwise in registers
+    double l[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) l[q] = leaf[(int64_t)(j + q) * stride];
+    double v = ((l[0] + l[1]) + (l[2] + l[3])) + ((l[4] + l[5]) + (l[6] + l[7]));
+    for (int k = (j + 8) >> 3; (k & 1) == 0; k >>= 1) v = st[--sp] + v;
+    st[sp++] = v;
+  }
+  for (; j < n; ++j) {
+    double v = leaf[(int64_t)j * stride];
+    for (int k = j + 1; (k & 1) == 0; k >>= 1) v = st[--sp] + v;
+    st[sp++] = v;
+  }
+  double acc = st[sp - 1];
+  for (int q = sp - 2; q >= 0; --q) acc = st[q] + acc;
+  return acc;
+}
+
+// out[k][task][f] = sum of this rank's maximal node k over its leaves
+// ws[task][q][f] (q = local leaf index, leaf0 = first global leaf of the rank).
+__global__ void __launch_bounds__(256) gemm_tree_local(const double* __restrict__ ws, int qmax,
+                                                       int ntasks, int tile, const int2* nodes,
+                                                       int nnodes, int64_t leaf0, int64_t nleaves,
+                                                       double* __restrict__ out, const Ctl* ctl) {
+  if (ctl && ctl->done) return;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)ntasks * tile) return;
+  const int task = (int)(e / tile), f = (int)(e % tile);
+  for (int k = 0; k < nnodes; ++k) {
+    const int2 nd = nodes[k];
+    const int64_t a = (int64_t)nd.y << nd.x;
+    const int64_t b = min(a + ((int64_t)1 << nd.x), nleaves);
+    const double* leaf = ws + ((int64_t)task * qmax + (a - leaf0)) * tile + f;
+    out[((int64_t)k * ntasks + task) * tile + f] = tree_leaves(leaf, tile, (int)(b - a));
+  }
+}
+
+// Merges every rank's node sums (buf[r][k][task][f], labels nodes[r·maxn + k])
+// in global order into the tree root and stores it (fragment-native decode).
 template <class Cfg>
-__global__ void __launch_bounds__(256) gemm_chunk_sum_store(GemmArgs g, const FixupTask* tasks,
-                                                            int ntasks, const double* buf,
-                                                            const int32_t* rank_nq, int R,
-                                                            int64_t rank_stride) {
+__global__ void __launch_bounds__(256) gemm_tree_final(GemmArgs g, const FixupTask* tasks,
+                                                       int ntasks, const double* buf,
+                                                       const int32_t* cnt, const int2* nodes,
+                                                       int R, int maxn) {
   if (g.ctl && g.ctl->done) return;
   constexpr int TILE = Cfg::BM * Cfg::BN;
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (int64_t)ntasks * TILE) return;
   const int task = (int)(e / TILE);
   const int f = (int)(e % TILE);
-  const FixupTask tk = tasks[task];
-  double s = 0.0;
+  double sv[24];
+  int sl[24], si[24];
+  int sp = 0;
   for (int r = 0; r < R; ++r) {
-    const double* base = buf + r * rank_stride + (size_t)tk.slot * g.qmax * (size_t)TILE + f;
-    const int nq = rank_nq[r];
-    for (int q = 0; q < nq; ++q) s += base[(size_t)q * TILE];
+    const int nk = cnt[r];
+    for (int k = 0; k < nk; ++k) {
+      const int2 nd = nodes[r * maxn + k];
+      double v = buf[(((int64_t)r * maxn + k) * ntasks + task) * TILE + f];
+      int l = nd.x, i = nd.y;
+      while (sp > 0 && sl[sp - 1] == l && (si[sp - 1] & 1) == 0 && si[sp - 1] + 1 == i) {
+        v = sv[sp - 1] + v;  // left sibling + right sibling = parent
+        --sp;
+        ++l;
+        i >>= 1;
+      }
+      sv[sp] = v;
+      sl[sp] = l;
+      si[sp] = i;
+      ++sp;
+    }
   }
+  double s = sv[sp - 1];
+  for (int q = sp - 2; q >= 0; --q) s = sv[q] + s;  // truncated right spine
+  const FixupTask tk = tasks[task];
   const int lane = f & 31;
   int rr = f >> 5;
   const int x = rr & 1;

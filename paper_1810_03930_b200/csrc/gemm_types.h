@@ -50,6 +50,7 @@ struct GemmArgs {
   const Ctl* ctl;     // early exit when ctl->done (may be null)
   const int32_t* gate;  // early exit when non-null and *gate == 0 (in-graph CholeskyQR)
   int32_t force_ws;     // chunk-partial plans: every CTA stores its partial (no epilogue)
+  int32_t segs;         // > 0: segmented schedule, S fixed K segments per tile (see below)
 };
 
 struct FixupTask {   // one split tile
@@ -67,6 +68,19 @@ __host__ __device__ inline int32_t cta_of_unit(int64_t x, int64_t U, int32_t G) 
 __host__ __device__ inline int64_t cta_unit_begin(int32_t c, int64_t U, int32_t G, int64_t upc) {
   if (upc > 0) return (int64_t)c * upc < U ? (int64_t)c * upc : U;
   return (int64_t)c * U / G;
+}
+// Segmented schedule (reproducible plans): the K range of every tile is cut
+// into S segments at k-iterations ⌊s·ki/S⌋, independent of the tile count;
+// CTA c owns the whole segments [⌊c·T·S/G⌋, ⌊(c+1)·T·S/G⌋) and flushes one
+// partial per segment, so each output is (((0 + P₀) + P₁) + …) over the same
+// segments whatever the number of tiles or CTAs.
+__host__ __device__ inline int32_t seg_of(int32_t kk, int32_t ki, int32_t S) {
+  return (int32_t)(((int64_t)(kk + 1) * S - 1) / ki);
+}
+__host__ __device__ inline int64_t seg_unit_begin(int32_t c, int32_t ntiles, int32_t ki,
+                                                  int32_t S, int32_t G) {
+  const int64_t sg = (int64_t)c * ntiles * S / G;
+  return (sg / S) * ki + (sg % S) * ki / S;
 }
 
 
@@ -89,7 +103,7 @@ struct GemmPlan {
   int ntasks = 0;
   double* ws = nullptr;
   size_t ws_doubles = 0;
-  bool no_fixup = false;  // chunk-partial plans: the caller reduces ws (launch_gemm_chunk_sum)
+  bool no_fixup = false;  // chunk-partial plans: the caller reduces ws (launch_gemm_tree_*)
   GemmPlan() = default;
   GemmPlan(const GemmPlan&) = delete;
   GemmPlan& operator=(const GemmPlan&) = delete;
@@ -111,10 +125,15 @@ void plan_gemm(GemmPlan& pl, int device, int size, int amode, int epi, int64_t M
                int64_t K, int64_t sym_row0 = -1, int grid_override = 0, int fixed_splits = 0,
                bool chunk_partials = false, int qmax_min = 0);
 void launch_gemm(const GemmPlan& pl, cudaStream_t st);
-// Ordered sum of gathered chunk partials into ep.C: for every element,
-// Σ_r Σ_{q < rank_nq[r]} buf[r·rank_stride + (task·qmax + q)·BM·BN + f].
-void launch_gemm_chunk_sum(const GemmPlan& pl, const double* buf, const int32_t* rank_nq, int R,
-                           int64_t rank_stride, cudaStream_t st);
+// Tiles plan_gemm schedules for an M×N output (same skipping rule).
+int64_t count_tiles(int size, int64_t M, int64_t N, int64_t sym_row0 = -1);
+// Fixed-tree reduction of a chunk-partial plan's ws (gemm_dmma.cuh):
+// local maximal-node sums into `out` ([nnodes][ntasks][BM·BN]), then the
+// merge of every rank's node sums (buf = [R][maxn][ntasks][BM·BN]) into ep.C.
+void launch_gemm_tree_local(const GemmPlan& pl, const int2* nodes, int nnodes, int64_t leaf0,
+                            int64_t nleaves, double* out, cudaStream_t st);
+void launch_gemm_tree_final(const GemmPlan& pl, const double* buf, const int32_t* cnt,
+                            const int2* nodes, int R, int maxn, cudaStream_t st);
 int num_sms(int device);
 
 }  // namespace pcal

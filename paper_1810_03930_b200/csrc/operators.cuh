@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(32 * TY)
     k_stencil_march(const double* __restrict__ x, const double* __restrict__ u,
                     double* __restrict__ g, int nx, int ny, int nz, int64_t ld, int zchunk,
                     double* __restrict__ fpart, int64_t pstride, int32_t* bad, const Ctl* ctl,
-                    const double* __restrict__ hlo, const double* __restrict__ hhi) {
+                    const double* __restrict__ hlo, const double* __restrict__ hhi, int zpart) {
   if (ctl && ctl->done) return;
   constexpr int W = 32 * XP;  // smem row width (≥ nx)
   __shared__ double pl[TY + 2][W];
@@ -171,17 +171,21 @@ __global__ void __launch_bounds__(32 * TY)
       halo[k] = halo_n[k];
       uc[k] = u_n[k];
     }
-    __syncthreads();
-  }
-  // block reduction (fixed order) → one partial per (tile, z-chunk)
-  double v = warp_sum(acc);
-  if (lane == 0) sm[ty] = v;
-  __syncthreads();
-  if (lane == 0 && ty == 0) {
-    double s = 0.0;
+    // block reduction (fixed order) → one f partial per (tile, zpart planes):
+    // once per z-chunk (zpart = zchunk), or per row chunk on the sharded path
+    if ((z + 1) % zpart == 0 || z + 1 == z1) {
+      const double v = warp_sum(acc);
+      if (lane == 0) sm[ty] = v;
+      __syncthreads();
+      if (lane == 0 && ty == 0) {
+        double s = 0.0;
 #pragma unroll
-    for (int t = 0; t < TY; ++t) s += sm[t];
-    fpart[j * pstride + blockIdx.x + (int64_t)gridDim.x * zc] = s;
+        for (int t = 0; t < TY; ++t) s += sm[t];
+        fpart[j * pstride + blockIdx.x + (int64_t)gridDim.x * (z / zpart)] = s;
+      }
+      acc = 0.0;
+    }
+    __syncthreads();
   }
   if (__syncthreads_or(nonfinite) && lane == 0 && ty == 0) *bad = 1;
 }

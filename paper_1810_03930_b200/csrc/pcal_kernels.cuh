@@ -269,8 +269,9 @@ __global__ void k_bb_chunk(const double* __restrict__ x, const double* __restric
 }
 
 // Per-chunk column sums of the three row-block partial arrays (f, kkt², d):
-// block (j, which, c) sums rows [c·rpc, (c+1)·rpc) of column j of array
-// `which` into out[c·3p + which·p + j] (0 where the array is absent).
+// block (j, which) — thread c sums rows [c·rpc, (c+1)·rpc) of column j of
+// array `which` sequentially into out[c·3p + which·p + j] (0 where the array
+// is absent).
 struct ChunkColArgs {
   const double* in[3];
   int64_t nrows[3];   // local row-block count
@@ -278,20 +279,22 @@ struct ChunkColArgs {
   int64_t rpc[3];     // row blocks per chunk
   double* out;
   int64_t p;
+  int64_t nch;        // local chunks
 };
-__global__ void __launch_bounds__(kStreamThreads) k_chunk_colsum3(ChunkColArgs a, const Ctl* ctl) {
+__global__ void __launch_bounds__(128) k_chunk_colsum3(ChunkColArgs a, const Ctl* ctl) {
   if (ctl && ctl->done) return;
-  __shared__ double sm[kStreamThreads / 32];
   const int which = blockIdx.y;
-  const int64_t col = blockIdx.x, c = blockIdx.z;
-  double acc = 0.0;
-  if (a.in[which]) {
-    const double* src = a.in[which] + col * a.stride[which];
-    const int64_t r1 = min(a.nrows[which], (c + 1) * a.rpc[which]);
-    for (int64_t r = c * a.rpc[which] + threadIdx.x; r < r1; r += blockDim.x) acc += src[r];
+  const int64_t col = blockIdx.x;
+  const double* src = a.in[which] ? a.in[which] + col * a.stride[which] : nullptr;
+  for (int64_t c = threadIdx.x; c < a.nch; c += blockDim.x) {
+    double acc = 0.0;
+    if (src) {
+      const int64_t r1 = min(a.nrows[which], (c + 1) * a.rpc[which]);
+#pragma unroll 4
+      for (int64_t r = c * a.rpc[which]; r < r1; ++r) acc += src[r];
+    }
+    a.out[c * 3 * a.p + which * a.p + col] = acc;
   }
-  const double s = block_sum<kStreamThreads>(acc, sm);
-  if (threadIdx.x == 0) a.out[c * 3 * a.p + which * a.p + col] = s;
 }
 
 // out[w] = Σ_r Σ_{q < nq[r]} buf[r·rank_stride + q·W + w], in that order.
@@ -305,6 +308,7 @@ __global__ void k_chunk_sum(const double* __restrict__ buf, int R, const int32_t
   for (int r = 0; r < R; ++r) {
     const double* b = buf + r * rank_stride + w;
     const int q1 = nq[r];
+#pragma unroll 8
     for (int q = 0; q < q1; ++q) s += b[(int64_t)q * W];
   }
   out[w] = s;

@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <functional>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -338,8 +339,20 @@ struct pcal_session {
   int64_t zc_planes = 0;                  // grid models: z-planes per chunk
   int64_t nch = 0, nch_max = 0;           // local / largest per-rank chunk count
   int32_t* rank_nch_d = nullptr;          // chunks per rank (device)
-  int grad_splits = 0;                    // dense gradient: fixed K segments
-  pcal::DevBuf cc, ccg, bbt, spt, gath, ogath;  // chunk partials, gathered, totals, Gram gathers
+  int grad_splits = 0;                    // dense gradient: fixed K segments per tile
+  int gram_sub = 1, orth_sub = 1;         // Gram segments per row chunk (fixed globally)
+  pcal::DevBuf cc, ccg, bbt, spt;         // chunk partials, gathered, totals
+  struct Tree {                           // fixed-tree Gram reduction (0: iteration, 1: orth)
+    int maxn = 0, nloc = 0;
+    int64_t leaf0 = 0, nleaves = 0;
+    int2* nodes_d = nullptr;              // [R][maxn] (level, index)
+    int32_t* cnt_d = nullptr;             // [R]
+    pcal::DevBuf tn, gath;                // this rank's node sums, all ranks' node sums
+    ~Tree() {
+      if (nodes_d) cudaFree(nodes_d);
+      if (cnt_d) cudaFree(cnt_d);
+    }
+  } tree[2];
   int64_t n_glob = 0, row0 = 0;  // global row count, first owned row
   int64_t gz = 0;                // grid models: owned z-planes (nz for a single GPU)
   int64_t K_full = 0;            // dense: padded global row count (gradient GEMM K)
@@ -376,7 +389,7 @@ struct pcal_session {
   int64_t st_chunk = 0, st_nchunks = 0;
   bool st_march = false;
   bool fused_step = false;  // cooperative k_step_fused fits co-resident on the device
-  int64_t st_zchunk = 0, st_nzc = 0;
+  int64_t st_zchunk = 0, st_nzc = 0, st_zpart = 0;  // march z-chunk, count, planes per f partial
   // graphs
   cudaGraphExec_t graph[2] = {nullptr, nullptr};
   int64_t kernels_per_iter = 0;
@@ -418,18 +431,83 @@ static void chunk_reduce(pcal_session* s, const double* cc, int64_t W, double* o
                          const Ctl* ctl) {
   const int R = s->comm->size;
   const size_t cnt = (size_t)s->nch_max * W;
-  s->comm->allgather(cc, s->ccg.p, cnt, s->stream);
-  k_chunk_sum<<<(unsigned)ceil_div(W, 128), 128, 0, s->stream>>>(s->ccg.p, R, s->rank_nch_d,
-                                                                  (int64_t)cnt, W, out, ctl);
+  if (R > 1) s->comm->allgather(cc, s->ccg.p, cnt, s->stream);
+  k_chunk_sum<<<(unsigned)ceil_div(W, 128), 128, 0, s->stream>>>(R > 1 ? s->ccg.p : cc, R,
+                                                                  s->rank_nch_d, (int64_t)cnt, W,
+                                                                  out, ctl);
   launched("k_chunk_sum");
 }
 
-// Reproducible Gram: chunk partials of the plan's ws gathered from every rank
-// and summed in global chunk order into the plan's output.
-static void gram_reduce(pcal_session* s, const GemmPlan& g, double* gath) {
+static void chunking(const pcal_model_desc& m, int64_t* Q, int64_t* NC, int64_t* Zc);
+
+// Reproducible Gram: this rank's maximal tree nodes over its chunk partials,
+// exchanged (O(log) node sums per rank) and merged into the same fixed tree
+// on every rank (gemm_tree_local / gemm_tree_final).
+static void gram_reduce(pcal_session* s, const GemmPlan& g, int which) {
   const int R = s->comm->size;
-  s->comm->allgather(g.ws, gath, g.ws_doubles, s->stream);
-  launch_gemm_chunk_sum(g, gath, s->rank_nch_d, R, (int64_t)g.ws_doubles, s->stream);
+  auto& T = s->tree[which];
+  launch_gemm_tree_local(g, T.nodes_d + (size_t)s->comm->rank * T.maxn, T.nloc, T.leaf0,
+                         T.nleaves, T.tn.p, s->stream);
+  const double* buf = T.tn.p;
+  if (R > 1) {
+    s->comm->allgather(T.tn.p, T.gath.p, T.tn.n, s->stream);
+    buf = T.gath.p;
+  }
+  launch_gemm_tree_final(g, buf, T.cnt_d, T.nodes_d, R, T.maxn, s->stream);
+}
+
+// Maximal fixed-tree nodes inside the leaf range [l0, l1) of nleaves leaves.
+static std::vector<int2> tree_nodes(int64_t l0, int64_t l1, int64_t nleaves) {
+  int top = 0;
+  while (((int64_t)1 << top) < nleaves) ++top;
+  std::vector<int2> out;
+  for (int64_t cur = l0; cur < l1;) {
+    int best = 0;
+    for (int l = top; l >= 0; --l) {
+      if (cur % ((int64_t)1 << l)) continue;
+      if (std::min(cur + ((int64_t)1 << l), nleaves) <= l1) {
+        best = l;
+        break;
+      }
+    }
+    out.push_back(make_int2(best, (int)(cur >> best)));
+    cur = std::min(cur + ((int64_t)1 << best), nleaves);
+  }
+  return out;
+}
+
+// Tree metadata of Gram `which` (m partials per row chunk; ntiles output tiles).
+static void tree_setup(pcal_session* s, int which, int m, int64_t ntiles) {
+  const int R = s->comm->size;
+  auto& T = s->tree[which];
+  int64_t NC = 0;
+  std::vector<std::vector<int2>> nodes(R);
+  std::vector<int64_t> c0(R + 1);
+  {
+    int64_t Q, Zc;
+    chunking(s->model, &Q, &NC, &Zc);
+  }
+  T.nleaves = NC * m;
+  for (int r = 0; r < R; ++r) {
+    const int64_t a = (int64_t)r * NC / R * m, b = (int64_t)(r + 1) * NC / R * m;
+    nodes[r] = tree_nodes(a, b, T.nleaves);
+    T.maxn = std::max<int>(T.maxn, (int)nodes[r].size());
+    if (r == s->comm->rank) T.leaf0 = a;
+  }
+  T.nloc = (int)nodes[s->comm->rank].size();
+  std::vector<int2> flat((size_t)R * T.maxn, make_int2(0, 0));
+  std::vector<int32_t> cnt(R);
+  for (int r = 0; r < R; ++r) {
+    cnt[r] = (int32_t)nodes[r].size();
+    std::copy(nodes[r].begin(), nodes[r].end(), flat.begin() + (size_t)r * T.maxn);
+  }
+  PCAL_CUDA(cudaMalloc(&T.nodes_d, sizeof(int2) * flat.size()));
+  PCAL_CUDA(cudaMemcpy(T.nodes_d, flat.data(), sizeof(int2) * flat.size(), cudaMemcpyHostToDevice));
+  PCAL_CUDA(cudaMalloc(&T.cnt_d, sizeof(int32_t) * R));
+  PCAL_CUDA(cudaMemcpy(T.cnt_d, cnt.data(), sizeof(int32_t) * R, cudaMemcpyHostToDevice));
+  const CfgInfo ci = cfg_info(pick_size(s->pp));
+  T.tn.alloc((size_t)T.maxn * ntiles * ci.BM * ci.BN);
+  if (R > 1) T.gath.alloc((size_t)R * T.tn.n);
 }
 
 // Column sums of the three partial arrays (f, kkt², d), one launch.
@@ -483,7 +561,7 @@ static void launch_stencil(pcal_session* s, int b, const double* u, bool ks, con
 #define PCAL_MARCH(KSV, XPV)                                                                   \
   k_stencil_march<KSV, XPV, 8><<<grid, block, 0, s->stream>>>(                               \
       Xof(s, b), u, Pof(s, b), (int)m.nx, (int)m.ny, (int)s->gz, s->ld, (int)s->st_zchunk,     \
-      s->fpart.p, s->pstride_f, s->bad, ctl, hlo, hhi)
+      s->fpart.p, s->pstride_f, s->bad, ctl, hlo, hhi, (int)s->st_zpart)
     if (ks) {
       if (xp == 1) PCAL_MARCH(true, 1); else if (xp == 2) PCAL_MARCH(true, 2);
       else if (xp == 3) PCAL_MARCH(true, 3); else PCAL_MARCH(true, 4);
@@ -511,7 +589,7 @@ static void launch_gradient(pcal_session* s, int b, const Ctl* ctl) {
   const int64_t p = s->p;
   switch (s->model.kind) {
     case PCAL_MODEL_DENSE:
-      if (s->comm) {  // C5: every rank needs all rows of X for its row slab of A·X
+      if (s->comm && s->comm->size > 1) {  // C5: every rank needs all rows of X for A·X
         const int R = s->comm->size;
         s->comm->allgather(Xof(s, b), s->xgath.p, (size_t)s->ld * s->pp, s->stream);
         k_unpack_rows<<<dim3((unsigned)ceil_div(s->ld, 256), (unsigned)s->pp, (unsigned)R), 256, 0,
@@ -589,7 +667,7 @@ static void launch_eval(pcal_session* s, int b, int mode, const Ctl* ctl_guard) 
   launch_gradient(s, b, ctl_guard);
   mark(s, 2);
   launch_gemm(s->gram[b], st);
-  if (s->repro) gram_reduce(s, s->gram[b], s->gath.p);  // C1
+  if (s->repro) gram_reduce(s, s->gram[b], 0);  // C1
   {
     const int mc = (s->alg == PCAL_ALG_PLAMDA || s->alg == PCAL_ALG_PCALDA) ? MC_DA
                    : s->alg == PCAL_ALG_MOPTQR                               ? MC_MOPTQR
@@ -619,8 +697,8 @@ static void launch_eval(pcal_session* s, int b, int mode, const Ctl* ctl_guard) 
     }
     a.out = s->cc.p;
     a.p = s->p;
-    k_chunk_colsum3<<<dim3((unsigned)s->p, 3, (unsigned)s->nch), kStreamThreads, 0, st>>>(
-        a, ctl_guard);
+    a.nch = s->nch;
+    k_chunk_colsum3<<<dim3((unsigned)s->p, 3), 128, 0, st>>>(a, ctl_guard);
     launched("k_chunk_colsum3");
     chunk_reduce(s, s->cc.p, 3 * s->p, s->fkd[b].p, ctl_guard);
     // the ranks' failure flags, so every rank stops together (exact counts)
@@ -819,22 +897,16 @@ static void build_plans(pcal_session* s) {
     if (s->model.kind == PCAL_MODEL_DENSE) {
       GemmPlan& g = s->grad[b];
       const int sz = pick_size(pp);
-      if (s->repro) {
-        // fixed K segments chosen from global sizes only: ≈ 8 CTAs per SM-wave
-        // of the whole job, ≤ 16 partials per tile
-        const CfgInfo ci = cfg_info(sz);
-        const int64_t tiles_glob = ceil_div(s->n_glob, ci.BM) * ceil_div(pp, ci.BN);
-        const int64_t ki = s->K_full / ci.BK;
-        s->grad_splits = (int)std::max<int64_t>(
-            1, std::min<int64_t>({ki, 16, ceil_div(8 * 148, tiles_glob)}));
+      if (s->repro) {  // fixed K segments (chosen from global sizes in session_create)
         plan_gemm(g, dev, sz, A_MCONTIG, EPI_GRAD, n, pp, s->K_full, -1, 0, s->grad_splits);
       } else {
         plan_gemm(g, dev, sz, A_MCONTIG, EPI_GRAD, n, pp, s->K_full);
       }
       g.args.A = s->A.p;
       g.args.lda = s->ldA;
-      g.args.B = s->comm ? s->xfull.p : Xof(s, b);
-      g.args.ldb = s->comm ? s->K_full : ld;
+      const bool gathered = s->comm && s->comm->size > 1;
+      g.args.B = gathered ? s->xfull.p : Xof(s, b);
+      g.args.ldb = gathered ? s->K_full : ld;
       EpiParams& e = g.args.ep;
       e.G = Pof(s, b);
       e.X = Xof(s, b);
@@ -852,7 +924,8 @@ static void build_plans(pcal_session* s) {
       GemmPlan& g = s->gram[b];
       if (s->repro)  // one partial per row chunk, summed across ranks in chunk order
         plan_gemm(g, dev, pick_size(pp), A_KCONTIG, EPI_STORE, 2 * pp, pp,
-                  s->nch * s->chunk_rows, pp, 0, (int)s->nch, true, (int)s->nch_max);
+                  s->nch * s->chunk_rows, pp, 0, (int)(s->nch * s->gram_sub), true,
+                  (int)(s->nch_max * s->gram_sub));
       else
         plan_gemm(g, dev, pick_size(pp), A_KCONTIG, EPI_STORE, 2 * pp, pp, ld, pp);
       g.args.A = s->pair[b].p;
@@ -890,7 +963,7 @@ static void build_plans(pcal_session* s) {
       g.args.ctl = s->ctl;
     }
   }
-  if (s->repro) s->gath.alloc((size_t)s->comm->size * s->gram[0].ws_doubles);
+  if (s->repro) tree_setup(s, 0, s->gram_sub, s->gram[0].ntasks);
 }
 
 
@@ -899,7 +972,7 @@ static void build_plans(pcal_session* s) {
 // chunk order, so results are bitwise independent of the number of ranks.
 //   dense: Q = ⌈n/64⌉ rounded up to the row-block size a (64 for p > 32,
 //          else 32: chunk boundaries fall on GEMM warp row-blocks);
-//   grid models: Zc = ⌈nz/32⌉ whole z-planes (Q = Zc·nx·ny rows).
+//   grid models: Zc = ⌈nz/64⌉ whole z-planes (Q = Zc·nx·ny rows).
 static void chunking(const pcal_model_desc& m, int64_t* Q, int64_t* NC, int64_t* Zc) {
   if (m.kind == PCAL_MODEL_DENSE) {
     const int64_t a = padded_p(m.p) >= 64 ? 64 : 32;
@@ -907,7 +980,7 @@ static void chunking(const pcal_model_desc& m, int64_t* Q, int64_t* NC, int64_t*
     *NC = ceil_div(m.n, *Q);
     *Zc = 0;
   } else {
-    *Zc = ceil_div(m.nz, 32);
+    *Zc = ceil_div(m.nz, 64);
     *NC = ceil_div(m.nz, *Zc);
     *Q = *Zc * m.nx * m.ny;
   }
@@ -935,6 +1008,63 @@ static void partition(const pcal_model_desc& m, int R, int r, int64_t* row0, int
   }
 }
 
+// Segment counts of the reproducible GEMM schedules.  They may depend on
+// global sizes only (never on the rank count), so pick the count whose
+// modelled time exceeds the ideal (perfectly balanced, no partials) by the
+// least over R ∈ {1, 2, 4, 8}.  Model per CTA: ⌈units/148⌉ segments, each
+// costing its DMMA time (34 TF/s FP64 over 148 SMs) plus writing and
+// re-reading one BM×BN partial at the SM's share of 6.5 TB/s.
+static int best_segments(int smax, int64_t nc, int bm, int bn,
+                         const std::function<double(int, int)>& units,
+                         const std::function<double(int)>& kseg, bool always_store) {
+  const double G = 148.0, f_sm = 34e12 / G, bw_sm = 6.5e12 / G;
+  const double t_store = 2.0 * bm * bn * 8.0 / bw_sm;
+  auto tseg = [&](int S) { return 2.0 * bm * bn * kseg(S) / f_sm; };
+  int best = 1;
+  double best_excess = 1e300;
+  for (int S = 1; S <= smax; ++S) {
+    double excess = 0.0;
+    for (int R : {1, 2, 4, 8}) {
+      if (R > nc) break;
+      const double u = units(S, R);
+      const double t = std::ceil(u / G) * (tseg(S) + (S > 1 || always_store ? t_store : 0.0));
+      const double ideal = units(1, R) * tseg(1) / G;
+      excess = std::max(excess, t - ideal);
+    }
+    if (excess < best_excess * (1.0 - 1e-9)) {
+      best_excess = excess;
+      best = S;
+    }
+  }
+  return best;
+}
+
+static void choose_segments(pcal_session* s, int64_t NC) {
+  const int64_t pp = s->pp, Q = s->chunk_rows;
+  const CfgInfo ci = cfg_info(pick_size(pp));
+  auto rows_R = [&](int R) { return (double)ceil_div(NC, (int64_t)R) * Q; };  // worst rank
+  if (s->model.kind == PCAL_MODEL_DENSE) {
+    const int64_t ki = s->K_full / ci.BK;
+    const double tn = (double)ceil_div(pp, ci.BN);
+    s->grad_splits = best_segments(
+        (int)std::min<int64_t>(32, ki), NC, ci.BM, ci.BN,
+        [&](int S, int R) { return std::ceil(rows_R(R) / ci.BM) * tn * S; },
+        [&](int S) { return (double)s->K_full / S; }, false);
+  }
+  const int smax = (int)std::min<int64_t>(16, Q / ci.BK);
+  const double tg = (double)count_tiles(pick_size(pp), 2 * pp, pp, pp);
+  const double to = (double)count_tiles(pick_size(pp), pp, pp, 0);
+  // chunk partials are always stored, so even m = 1 pays the partial traffic
+  s->gram_sub = best_segments(
+      smax, NC, ci.BM, ci.BN,
+      [&](int m, int R) { return tg * (double)ceil_div(NC, (int64_t)R) * m; },
+      [&](int m) { return (double)Q / m; }, true);
+  s->orth_sub = best_segments(
+      smax, NC, ci.BM, ci.BN,
+      [&](int m, int R) { return to * (double)ceil_div(NC, (int64_t)R) * m; },
+      [&](int m) { return (double)Q / m; }, true);
+}
+
 static void alloc_state(pcal_session* s) {
   cudaStream_t st = s->stream;
   const int64_t n = s->n, p = s->p, pp = s->pp, ld = s->ld;
@@ -959,14 +1089,14 @@ static void alloc_state(pcal_session* s) {
                   s->gz >= 1;
     if (s->comm && m.kind != PCAL_MODEL_DENSE && !s->st_march)
       throw Error(PCAL_E_UNSUPPORTED, "sharded grid models need nx <= 128 and ny % 8 == 0");
-    if (s->repro) {  // one z-chunk per row chunk: f partials per (y-tile, chunk)
-      s->st_zchunk = s->zc_planes;
-      s->st_nzc = s->nch;
-    } else if (s->st_march) {  // enough blocks for ≈ 8 per SM
+    if (s->st_march) {  // enough blocks for ≈ 8 per SM
       const int64_t tiles = (m.ny / 8) * p;
       int64_t nzc = std::max<int64_t>(1, std::min<int64_t>(s->gz, ceil_div(8 * 148, tiles)));
       s->st_zchunk = ceil_div(s->gz, nzc);
+      // sharded: z-chunks of whole row chunks, one f partial per (y-tile, row chunk)
+      if (s->repro) s->st_zchunk = round_up(s->st_zchunk, s->zc_planes);
       s->st_nzc = ceil_div(s->gz, s->st_zchunk);
+      s->st_zpart = s->repro ? s->zc_planes : s->st_zchunk;
     }
   }
   if (s->comm) {
@@ -990,7 +1120,7 @@ static void alloc_state(pcal_session* s) {
                          cudaMemcpyHostToDevice));
   }
   s->nrb_f = s->model.kind == PCAL_MODEL_DENSE ? ceil_div(n, wm_grad)
-             : s->st_march ? (s->model.ny / 8) * s->st_nzc
+             : s->st_march ? (s->model.ny / 8) * ceil_div(s->gz, s->st_zpart)
                            : s->st_nchunks;
   s->nrb_xm = ceil_div(n, wm_xm);
   s->pstride_f = s->nrb_f + 2;
@@ -1242,6 +1372,7 @@ void session_create(const pcal_model_desc* model, const pcal_config* config, con
   s->n = s->rank_rows[rk];
   s->ld_max = padded_ld(maxrows);
   s->ld = comm ? s->ld_max : padded_ld(s->n);
+  s->K_full = padded_ld(s->n_glob);
   if (comm) {  // reproducible chunked reductions
     int64_t Q, NC, Zc;
     chunking(*model, &Q, &NC, &Zc);
@@ -1257,6 +1388,7 @@ void session_create(const pcal_model_desc* model, const pcal_config* config, con
     }
     s->nch = nq[rk];
     s->ld_max = s->ld = s->nch_max * Q;  // every chunk's rows fit (zero padded)
+    choose_segments(s.get(), NC);
     PCAL_CUDA(cudaMalloc(&s->rank_nch_d, sizeof(int32_t) * R));
     PCAL_CUDA(cudaMemcpy(s->rank_nch_d, nq.data(), sizeof(int32_t) * R, cudaMemcpyHostToDevice));
   }
@@ -1353,9 +1485,10 @@ bool orthonormalize_dev(pcal_session* s, const double* x, double* q, double* scr
   if (!gp.d_tiles) {
     if (s->repro) {  // chunked Gram + whole-tile products (rank-count invariant)
       plan_gemm(gp, s->device, pick_size(pp), A_KCONTIG, EPI_STORE, pp, pp,
-                s->nch * s->chunk_rows, 0, 0, (int)s->nch, true, (int)s->nch_max);
+                s->nch * s->chunk_rows, 0, 0, (int)(s->nch * s->orth_sub), true,
+                (int)(s->nch_max * s->orth_sub));
       plan_gemm(mp, s->device, pick_size(pp), A_MCONTIG, EPI_STORE, n, pp, pp, -1, 0, 1);
-      s->ogath.alloc((size_t)s->comm->size * gp.ws_doubles);
+      tree_setup(s, 1, s->orth_sub, gp.ntasks);
     } else {
       plan_gemm(gp, s->device, pick_size(pp), A_KCONTIG, EPI_STORE, pp, pp, ld, 0);
       plan_gemm(mp, s->device, pick_size(pp), A_MCONTIG, EPI_STORE, n, pp, pp);
@@ -1372,7 +1505,7 @@ bool orthonormalize_dev(pcal_session* s, const double* x, double* q, double* scr
     gp.args.ep.n_store = pp;
     gp.args.ctl = nullptr;
     launch_gemm(gp, st);
-    if (s->repro) gram_reduce(s, gp, s->ogath.p);  // sharded Gram
+    if (s->repro) gram_reduce(s, gp, 1);  // sharded Gram
   };
   auto mul_t = [&](const double* a, double* out) {  // out = a · T
     mp.args.A = a;

@@ -65,9 +65,9 @@ def test_row_chunks_cover_partition():
         assert all(r0 % q == 0 for r0, _ in parts)
     with pytest.raises(P.ParameterError):
         P.partition(m, nc + 1, 0)
-    g = P.StencilModel((16, 16, 64), np.zeros(16 * 16 * 64), 4, 1.0)
+    g = P.StencilModel((16, 16, 128), np.zeros(16 * 16 * 128), 4, 1.0)
     q, nc = P.row_chunks(g)
-    assert q == 2 * 256 and nc == 32  # ⌈64/32⌉ = 2 planes per chunk
+    assert q == 2 * 256 and nc == 64  # ⌈128/64⌉ = 2 planes per chunk
 
 
 def _free_port():

@@ -9,6 +9,7 @@ from paper_1810_03930_b200.problems import make_instance
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=2)
 ap.add_argument("--iters", type=int, default=10)
+ap.add_argument("--sharded", action="store_true", help="the row-sharded path on one NCCL rank")
 a = ap.parse_args()
 t = time.time()
 inst = make_instance(a.config, P, threads=os.cpu_count() or 8)
@@ -16,7 +17,12 @@ x0 = P.initial_point(inst.n, inst.p, inst.seed ^ 0x1235713)
 print(f"config {a.config}: n={inst.n} p={inst.p} setup {time.time()-t:.1f}s", flush=True)
 cfg = P.SolverConfig(tol_rel_kkt=float(np.finfo(float).tiny), max_iter=a.iters * 3 + 10,
                      final_orth=False)
-with P.Session(inst.model(P), cfg, x0) as s:
+if a.sharded:
+    comm = P.Comm(1, 0, P.nccl_unique_id(), 0)
+    ses = P.ShardedSession(inst.model(P), cfg, x0, comm, inst.n)
+else:
+    ses = P.Session(inst.model(P), cfg, x0)
+with ses as s:
     s.run(3); s.sync()
     prof = s.profile_kernels(a.iters)
     ph = s.profile(a.iters)
