@@ -129,6 +129,27 @@ __device__ __forceinline__ double clamp_eta(const Ctl* c, double v) {
   return r < c->eta_max ? r : c->eta_max;
 }
 
+// The stepsize rule of stepsize_select (solver.cpp:212-251) from the summed
+// ⟨S,S⟩, ⟨S,Y⟩, ⟨Y,Y⟩: BB1 / BB2 / ABB (odd k → BB1) / differential, the
+// zero-denominator fallback to the previous η (or η0), then the clamp.
+__device__ __forceinline__ double select_eta(const Ctl* c, double ss, double sy, double yy,
+                                             bool need) {
+  if (c->eta_kind == 0) return clamp_eta(c, c->gamma);
+  const double fallback = c->eta_prev > 0.0 ? c->eta_prev : c->eta0;
+  if (!need) return clamp_eta(c, c->eta0 > 0.0 ? c->eta0 : fallback);
+  const double bb1 = (ss == 0.0 || sy == 0.0) ? fallback : fabs(sy) / ss;
+  const double bb2 = (sy == 0.0) ? fallback : yy / fabs(sy);
+  double v = fallback;
+  switch (c->eta_kind) {
+    case 2: v = bb1; break;
+    case 3: v = bb2; break;
+    case 4: v = (c->iter % 2 == 1) ? bb1 : bb2; break;
+    case 1: v = (ss == 0.0) ? fallback : sqrt(yy) / sqrt(ss); break;
+    default: break;
+  }
+  return clamp_eta(c, v);
+}
+
 // stepsize_select (solver.cpp:212-251) on the device: one block reduces the
 // k_bb_partials slots in a fixed order, thread 0 applies the rule.
 __global__ void __launch_bounds__(kStreamThreads) k_eta(Ctl* ctl, const double* __restrict__ part,
@@ -150,27 +171,7 @@ __global__ void __launch_bounds__(kStreamThreads) k_eta(Ctl* ctl, const double* 
     yy = block_sum<kStreamThreads>(d, sm);
   }
   if (threadIdx.x != 0) return;
-  double eta;
-  if (c->eta_kind == 0) {
-    eta = clamp_eta(c, c->gamma);
-  } else {
-    const double fallback = c->eta_prev > 0.0 ? c->eta_prev : c->eta0;
-    if (!need) {
-      eta = clamp_eta(c, c->eta0 > 0.0 ? c->eta0 : fallback);
-    } else {
-      const double bb1 = (ss == 0.0 || sy == 0.0) ? fallback : fabs(sy) / ss;
-      const double bb2 = (sy == 0.0) ? fallback : yy / fabs(sy);
-      double v = fallback;
-      switch (c->eta_kind) {
-        case 2: v = bb1; break;
-        case 3: v = bb2; break;
-        case 4: v = (c->iter % 2 == 1) ? bb1 : bb2; break;
-        case 1: v = (ss == 0.0) ? fallback : sqrt(yy) / sqrt(ss); break;
-        default: break;
-      }
-      eta = clamp_eta(c, v);
-    }
-  }
+  const double eta = select_eta(c, ss, sy, yy, need);
   c->eta = eta;
   c->step_deg = 0;
   if (!(eta > 0.0)) {  // pcal_step: parameter_error (solver.cpp:266)
@@ -482,31 +483,7 @@ __device__ __forceinline__ bool step_phase(const StepArgs& a, Ctl* ctl) {
       sy = block_sum<kStreamThreads>(s2, sm);
       yy = block_sum<kStreamThreads>(s3, sm);
     }
-    if (threadIdx.x == 0) {
-      const Ctl* c = ctl;
-      double eta;
-      if (c->eta_kind == 0) {
-        eta = clamp_eta(c, c->gamma);
-      } else {
-        const double fallback = c->eta_prev > 0.0 ? c->eta_prev : c->eta0;
-        if (!need) {
-          eta = clamp_eta(c, c->eta0 > 0.0 ? c->eta0 : fallback);
-        } else {
-          const double bb1 = (ss == 0.0 || sy == 0.0) ? fallback : fabs(sy) / ss;
-          const double bb2 = (sy == 0.0) ? fallback : yy / fabs(sy);
-          double v = fallback;
-          switch (c->eta_kind) {
-            case 2: v = bb1; break;
-            case 3: v = bb2; break;
-            case 4: v = (c->iter % 2 == 1) ? bb1 : bb2; break;
-            case 1: v = (ss == 0.0) ? fallback : sqrt(yy) / sqrt(ss); break;
-            default: break;
-          }
-          eta = clamp_eta(c, v);
-        }
-      }
-      s_eta = eta;
-    }
+    if (threadIdx.x == 0) s_eta = select_eta(ctl, ss, sy, yy, need);
     __syncthreads();
   }
   const double eta = s_eta;

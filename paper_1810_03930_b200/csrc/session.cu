@@ -19,6 +19,7 @@
 #include <functional>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -298,6 +299,10 @@ __global__ void __launch_bounds__(256) k_finish_eval(FinishArgs a, Ctl* ctl,
   finish_record(a, ctl, post, f1, k2, c2, vr, rh, ex);
 }
 
+}  // namespace pcal
+#include "small.cuh"
+namespace pcal {
+
 __global__ void k_zero_i32(int32_t* p, const Ctl* ctl) {
   if (ctl && ctl->done) return;
   *p = 0;
@@ -389,6 +394,9 @@ struct pcal_session {
   int64_t st_chunk = 0, st_nchunks = 0;
   bool st_march = false;
   bool fused_step = false;  // cooperative k_step_fused fits co-resident on the device
+  bool mega = false;        // small dense problem: k_iter_small runs whole batches of iterations
+  int mega_grid = 0;
+  pcal::DevBuf at, mpart, mz, mnpb, mbb;  // Aᵀ, Z and the CTA partials of k_iter_small
   int64_t st_zchunk = 0, st_nzc = 0, st_zpart = 0;  // march z-chunk, count, planes per f partial
   // graphs
   cudaGraphExec_t graph[2] = {nullptr, nullptr};
@@ -1332,6 +1340,111 @@ int guarded(F&& f) {
   }
 }
 
+// k_iter_small over `iters` iterations (cooperative, one CTA per SM).
+static void launch_small(pcal_session* s, int iters) {
+  SmallArgs a{};
+  for (int b = 0; b < 2; ++b) {
+    a.pair[b] = s->pair[b].p;
+    a.fkd[b] = s->fkd[b].p;
+  }
+  a.at = s->at.p;
+  a.ldat = s->ld;
+  a.g0 = s->g0.p;
+  a.gr = s->gr.p;
+  a.lam = s->lam.p;
+  a.z = s->mz.p;
+  a.part = s->mpart.p;
+  a.npb = s->mnpb.p;
+  a.bbpart = s->mbb.p;
+  a.n = s->n;
+  a.ld = s->ld;
+  a.p = s->p;
+  a.pp = s->pp;
+  a.plain = !(s->alg == PCAL_ALG_PCAL || s->alg == PCAL_ALG_PCALDA);
+  const bool da = s->alg == PCAL_ALG_PLAMDA || s->alg == PCAL_ALG_PCALDA;
+  a.mc_mode = da ? MC_DA : MC_PCAL;
+  a.p_from_g = da;
+  a.dform = s->alg == PCAL_ALG_PCAL && s->cfg.multiplier_rule == PCAL_MULT_PCAL_FORMULA;
+  a.beta = s->beta;
+  a.beta_epi = da ? 1.0 : s->beta;
+  a.fa.model = s->model.kind;
+  a.fa.p = s->p;
+  a.fa.mode = 0;
+  a.fa.trace = s->trace.p;
+  a.fa.bad = s->bad;
+  a.fa.c_xc = s->c_xc;
+  Ctl* c = s->ctl;
+  void* args[] = {&a, &c, &iters};
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3((unsigned)s->mega_grid);
+  lc.blockDim = dim3(kSmallThreads);
+  lc.stream = s->stream;
+  cudaLaunchAttribute attr{};
+  attr.id = cudaLaunchAttributeCooperative;
+  attr.val.cooperative = 1;
+  lc.attrs = &attr;
+  lc.numAttrs = 1;
+  // PCAL_SMALL_PROF=1: per-phase %globaltimer stamps of CTA 0, printed per batch
+  static const bool prof = getenv("PCAL_SMALL_PROF") && getenv("PCAL_SMALL_PROF")[0] == '1';
+  uint64_t* dprof = nullptr;
+  if (prof) {
+    PCAL_CUDA(cudaMalloc(&dprof, sizeof(uint64_t) * 8 * iters));
+    PCAL_CUDA(cudaMemsetAsync(dprof, 0, sizeof(uint64_t) * 8 * iters, s->stream));
+    a.prof = dprof;
+  }
+  PCAL_CUDA(cudaLaunchKernelExC(&lc, (const void*)k_iter_small, args));
+  launched("k_iter_small");
+  if (prof) {
+    std::vector<uint64_t> h((size_t)8 * iters);
+    PCAL_CUDA(cudaMemcpyAsync(h.data(), dprof, sizeof(uint64_t) * h.size(), cudaMemcpyDeviceToHost,
+                              s->stream));
+    PCAL_CUDA(cudaStreamSynchronize(s->stream));
+    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    int cnt = 0;
+    for (int it = 0; it + 1 < iters; ++it) {
+      const uint64_t* r = &h[(size_t)8 * it];
+      if (!r[5] || !h[(size_t)8 * (it + 1)]) break;
+      for (int q = 0; q < 5; ++q) acc[q] += (double)(r[q + 1] - r[q]);
+      acc[5] += (double)(h[(size_t)8 * (it + 1)] - r[5]);
+      acc[6] += (double)(r[6] - r[4]);
+      acc[7] += (double)(r[7] - r[6]);
+      ++cnt;
+    }
+    if (cnt)
+      fprintf(stderr, "k_iter_small us/iter: step %.2f grad %.2f gram %.2f xm %.2f record %.2f "
+              "(colsums %.2f, c2+finish %.2f) next %.2f\n",
+              acc[0] / cnt / 1e3, acc[1] / cnt / 1e3, acc[2] / cnt / 1e3, acc[3] / cnt / 1e3,
+              acc[4] / cnt / 1e3, acc[6] / cnt / 1e3, acc[7] / cnt / 1e3, acc[5] / cnt / 1e3);
+    cudaFree(dprof);
+  }
+}
+
+// The persistent small-problem kernel applies to dense PCAL / PLAM / dual-ascent
+// runs with p ≤ 32 on one GPU (MOptQR keeps its in-graph retraction).
+static void setup_small(pcal_session* s) {
+  const char* off = getenv("PCAL_NO_SMALL_KERNEL");
+  if ((off && off[0] == '1') || s->comm || s->model.kind != PCAL_MODEL_DENSE ||
+      s->p > kSmallP || s->n > 8192 || s->alg == PCAL_ALG_MOPTQR)
+    return;
+  int coop = 0, per_sm = 0;
+  PCAL_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, s->device));
+  PCAL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_iter_small, kSmallThreads, 0));
+  if (!coop || per_sm < 1) return;
+  s->mega_grid = num_sms(s->device);
+  if (s->mega_grid > 160) return;  // the record phase sums ≤ 160 CTA partials
+  s->at.alloc((size_t)s->ld * s->n);
+  s->at.zero(s->stream);  // rows k ≥ n are read by the padded k-steps
+  dim3 g((unsigned)ceil_div(s->n, 32), (unsigned)ceil_div(s->n, 32));
+  k_transpose<<<g, dim3(32, 8), 0, s->stream>>>(s->A.p, s->ldA, s->n, s->at.p, s->ld);
+  launched("k_transpose");
+  s->mpart.alloc((size_t)s->mega_grid * 3 * kSmallP);
+  s->mnpb.alloc((size_t)s->mega_grid * kSmallP);
+  s->mbb.alloc((size_t)s->mega_grid * 3);
+  s->mz.alloc((size_t)s->ld * s->pp);
+  s->mz.zero(s->stream);  // padded rows / columns are read by the DMMA tiles
+  s->mega = true;
+}
+
 void session_create(const pcal_model_desc* model, const pcal_config* config, const double* x0,
                     int32_t x0_loc, pcal_session** out, pcal_category_timers* timers,
                     Comm* comm = nullptr, cudaStream_t shared_stream = nullptr) {
@@ -1415,6 +1528,7 @@ void session_create(const pcal_model_desc* model, const pcal_config* config, con
   alloc_state(s.get());
   upload_model(s.get());
   build_plans(s.get());
+  setup_small(s.get());
   init_ctl(s.get());
   upload_matrix(x0, x0_loc, s->n, s->p, Xof(s.get(), 0), s->ld, s->stream);
   k_set_t0<<<1, 1, 0, s->stream>>>(s->ctl);
@@ -1438,7 +1552,12 @@ void session_run(pcal_session* s, int64_t iters) {
   bool pending = false;
   while (remaining > 0) {
     const int64_t nb = std::min(batch, remaining);
-    for (int64_t i = 0; i < nb; ++i) {
+    if (s->mega && !s->pev_on) {  // one persistent launch for the whole batch
+      launch_small(s, (int)nb);
+      s->next_k += nb;
+      s->launched += nb;
+    }
+    for (int64_t i = 0; i < nb && !(s->mega && !s->pev_on); ++i) {
       const int b = (int)(s->next_k % 2);
       if (s->use_graphs) {
         PCAL_CUDA(cudaGraphLaunch(s->graph[b], s->stream));
