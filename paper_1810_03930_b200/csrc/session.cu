@@ -396,6 +396,7 @@ struct pcal_session {
   bool fused_step = false;  // cooperative k_step_fused fits co-resident on the device
   bool mega = false;        // small dense problem: k_iter_small runs whole batches of iterations
   int mega_grid = 0;
+  int64_t mega_lda_s = 0;   // > 0: k_iter_small keeps each CTA's 8 rows of A in shared memory
   pcal::DevBuf at, mpart, mz, mnpb, mbb;  // Aᵀ, Z and the CTA partials of k_iter_small
   int64_t st_zchunk = 0, st_nzc = 0, st_zpart = 0;  // march z-chunk, count, planes per f partial
   // graphs
@@ -1373,11 +1374,13 @@ static void launch_small(pcal_session* s, int iters) {
   a.fa.trace = s->trace.p;
   a.fa.bad = s->bad;
   a.fa.c_xc = s->c_xc;
+  a.lda_s = s->mega_lda_s;
   Ctl* c = s->ctl;
   void* args[] = {&a, &c, &iters};
   cudaLaunchConfig_t lc{};
   lc.gridDim = dim3((unsigned)s->mega_grid);
   lc.blockDim = dim3(kSmallThreads);
+  lc.dynamicSmemBytes = (size_t)8 * s->mega_lda_s * sizeof(double);
   lc.stream = s->stream;
   cudaLaunchAttribute attr{};
   attr.id = cudaLaunchAttributeCooperative;
@@ -1399,22 +1402,21 @@ static void launch_small(pcal_session* s, int iters) {
     PCAL_CUDA(cudaMemcpyAsync(h.data(), dprof, sizeof(uint64_t) * h.size(), cudaMemcpyDeviceToHost,
                               s->stream));
     PCAL_CUDA(cudaStreamSynchronize(s->stream));
-    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    double acc[6] = {0, 0, 0, 0, 0, 0};
     int cnt = 0;
     for (int it = 0; it + 1 < iters; ++it) {
       const uint64_t* r = &h[(size_t)8 * it];
       if (!r[5] || !h[(size_t)8 * (it + 1)]) break;
       for (int q = 0; q < 5; ++q) acc[q] += (double)(r[q + 1] - r[q]);
       acc[5] += (double)(h[(size_t)8 * (it + 1)] - r[5]);
-      acc[6] += (double)(r[6] - r[4]);
-      acc[7] += (double)(r[7] - r[6]);
       ++cnt;
     }
     if (cnt)
-      fprintf(stderr, "k_iter_small us/iter: step %.2f grad %.2f gram %.2f xm %.2f record %.2f "
-              "(colsums %.2f, c2+finish %.2f) next %.2f\n",
+      fprintf(stderr,
+              "k_iter_small us/iter: B eta+Z %.2f  C norm+grad %.2f  D gram %.2f  E xm %.2f  "
+              "A sums+record+bb %.2f  (loop %.2f)\n",
               acc[0] / cnt / 1e3, acc[1] / cnt / 1e3, acc[2] / cnt / 1e3, acc[3] / cnt / 1e3,
-              acc[4] / cnt / 1e3, acc[6] / cnt / 1e3, acc[7] / cnt / 1e3, acc[5] / cnt / 1e3);
+              acc[4] / cnt / 1e3, acc[5] / cnt / 1e3);
     cudaFree(dprof);
   }
 }
@@ -1428,9 +1430,18 @@ static void setup_small(pcal_session* s) {
     return;
   int coop = 0, per_sm = 0;
   PCAL_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, s->device));
-  PCAL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_iter_small, kSmallThreads, 0));
-  if (!coop || per_sm < 1) return;
   s->mega_grid = num_sms(s->device);
+  // one 8-row gradient tile per CTA: keep those rows of A resident in shared
+  // memory (row stride ≡ 4 mod 16 doubles: conflict-free DMMA fragment loads)
+  const int64_t lda_s = round_up(s->n, 16) + 4;
+  if (s->n <= 8 * (int64_t)s->mega_grid && 8 * lda_s * 8 <= 160 * 1024) {
+    s->mega_lda_s = lda_s;
+    PCAL_CUDA(cudaFuncSetAttribute(k_iter_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(8 * lda_s * 8)));
+  }
+  PCAL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &per_sm, k_iter_small, kSmallThreads, (size_t)8 * s->mega_lda_s * sizeof(double)));
+  if (!coop || per_sm < 1) return;
   if (s->mega_grid > 160) return;  // the record phase sums ≤ 160 CTA partials
   s->at.alloc((size_t)s->ld * s->n);
   s->at.zero(s->stream);  // rows k ≥ n are read by the padded k-steps

@@ -40,6 +40,7 @@ struct SmallArgs {
   double beta;        // β
   double beta_epi;    // β of the P update (1 for dual ascent)
   FinishArgs fa;      // trace, bad flag, model (mode 0)
+  int64_t lda_s;      // > 0: this CTA's 8 rows of A stay in shared memory (row stride)
   uint64_t* prof;     // optional: %globaltimer per phase boundary (CTA 0), [iters][8]
 };
 
@@ -128,7 +129,7 @@ __device__ __forceinline__ void bb_block(const double* x, const double* xp, cons
 __device__ __forceinline__ void gradient_tiles(const SmallArgs& a, const double* Y,
                                                const double* scale, double* Pn,
                                                double (*sG)[4 * 64], double* sF, double& fcol,
-                                               bool& bad) {
+                                               bool& bad, const double* sA) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r8 = lane >> 2, q4 = lane & 3;
   const int64_t n = a.n, ld = a.ld, p = a.p;
@@ -141,7 +142,8 @@ __device__ __forceinline__ void gradient_tiles(const SmallArgs& a, const double*
 #pragma unroll
     for (int t = 0; t < 4; ++t) c[t][0] = c[t][1] = 0.0;
     const bool rok = i0 + r8 < n;
-    const double* arow = a.at + (rok ? (i0 + r8) * a.ldat : 0);
+    // A rows: resident in shared memory (one tile per CTA) or read from Aᵀ
+    const double* arow = sA ? sA + r8 * a.lda_s : a.at + (rok ? (i0 + r8) * a.ldat : 0);
 #pragma unroll 8
     for (int64_t k4 = k4b; k4 < k4e; ++k4) {
       const int64_t k = k4 * 4 + q4;
@@ -226,7 +228,15 @@ __global__ void __launch_bounds__(kSmallThreads) k_iter_small(SmallArgs a, Ctl* 
   // this CTA's rows of the streaming phases
   const int64_t rpb = (n + gridDim.x - 1) / gridDim.x;
   const int64_t r0 = min(n, (int64_t)blockIdx.x * rpb), r1 = min(n, r0 + rpb);
+  extern __shared__ double sA[];  // [8][lda_s]: A rows of this CTA's gradient tile
   if (ctl->done) return;
+  if (a.lda_s > 0) {  // n ≤ 8·gridDim: one tile per CTA, loaded once per launch
+    const int64_t i0 = (int64_t)blockIdx.x * 8;
+    for (int64_t e = threadIdx.x; e < 8 * a.lda_s; e += blockDim.x) {
+      const int64_t r = e / a.lda_s, k = e % a.lda_s;
+      sA[e] = (i0 + r < n && k < n) ? a.at[k + (i0 + r) * a.ldat] : 0.0;
+    }
+  }
   {  // stepsize partials of the current step from the stored state (pair b = current)
     const int b = (int)(ctl->iter & 1), nb = b ^ 1;
     double* Pb = a.pair[b];
@@ -346,10 +356,11 @@ __global__ void __launch_bounds__(kSmallThreads) k_iter_small(SmallArgs a, Ctl* 
       double fcol = 0.0;
       bool gbad = false;
       if (!anydeg) {
-        gradient_tiles(a, a.z, a.plain ? nullptr : sInv, Pn, sG, sF, fcol, gbad);
+        gradient_tiles(a, a.z, a.plain ? nullptr : sInv, Pn, sG, sF, fcol, gbad,
+                       a.lda_s > 0 ? sA : nullptr);
       } else {  // rare: a degenerate column is not a scaled column of Z
         grid.sync();
-        gradient_tiles(a, Xn, nullptr, Pn, sG, sF, fcol, gbad);
+        gradient_tiles(a, Xn, nullptr, Pn, sG, sF, fcol, gbad, a.lda_s > 0 ? sA : nullptr);
       }
       if (gbad) *a.fa.bad = 1;
       if (threadIdx.x < kSmallP)
