@@ -298,14 +298,21 @@ __global__ void __launch_bounds__(128) k_chunk_colsum3(ChunkColArgs a, const Ctl
   }
 }
 
-// out[w] = Σ_r Σ_{q < nq[r]} buf[r·rank_stride + q·W + w], in that order.
+// out[w] = Σ_r Σ_{q < nq[r]} buf[r·rank_stride + q·W + w], in that order;
+// out[W + e] = Σ_r buf[r·rank_stride + extra_off + e] for e < extra (per-rank
+// values riding along in the same all-gather, e.g. the failure flags).
 __global__ void k_chunk_sum(const double* __restrict__ buf, int R, const int32_t* __restrict__ nq,
                             int64_t rank_stride, int64_t W, double* __restrict__ out,
-                            const Ctl* ctl) {
+                            const Ctl* ctl, int extra = 0, int64_t extra_off = 0) {
   if (ctl && ctl->done) return;
   const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (w >= W) return;
+  if (w >= W + extra) return;
   double s = 0.0;
+  if (w >= W) {
+    for (int r = 0; r < R; ++r) s += buf[r * rank_stride + extra_off + (w - W)];
+    out[w] = s;
+    return;
+  }
   for (int r = 0; r < R; ++r) {
     const double* b = buf + r * rank_stride + w;
     const int q1 = nq[r];

@@ -437,13 +437,13 @@ struct LaunchScope {
 // Reproducible sum of per-chunk partials (W values per chunk, `cc` layout
 // [nch_max][W]): all-gather in rank order, then the ordered chunk sum.
 static void chunk_reduce(pcal_session* s, const double* cc, int64_t W, double* out,
-                         const Ctl* ctl) {
+                         const Ctl* ctl, int extra = 0) {
   const int R = s->comm->size;
-  const size_t cnt = (size_t)s->nch_max * W;
+  const size_t off = (size_t)s->nch_max * W;  // per-rank extras follow the chunk rows
+  const size_t cnt = off + extra;
   if (R > 1) s->comm->allgather(cc, s->ccg.p, cnt, s->stream);
-  k_chunk_sum<<<(unsigned)ceil_div(W, 128), 128, 0, s->stream>>>(R > 1 ? s->ccg.p : cc, R,
-                                                                  s->rank_nch_d, (int64_t)cnt, W,
-                                                                  out, ctl);
+  k_chunk_sum<<<(unsigned)ceil_div(W + extra, 128), 128, 0, s->stream>>>(
+      R > 1 ? s->ccg.p : cc, R, s->rank_nch_d, (int64_t)cnt, W, out, ctl, extra, (int64_t)off);
   launched("k_chunk_sum");
 }
 
@@ -709,11 +709,11 @@ static void launch_eval(pcal_session* s, int b, int mode, const Ctl* ctl_guard) 
     a.nch = s->nch;
     k_chunk_colsum3<<<dim3((unsigned)s->p, 3), 128, 0, st>>>(a, ctl_guard);
     launched("k_chunk_colsum3");
-    chunk_reduce(s, s->cc.p, 3 * s->p, s->fkd[b].p, ctl_guard);
-    // the ranks' failure flags, so every rank stops together (exact counts)
-    k_flags<<<1, 1, 0, st>>>(s->ctl, s->bad, s->fkd[b].p + 3 * s->p);
+    // + the ranks' failure flags in the same all-gather, so every rank stops
+    // together (exact counts)
+    k_flags<<<1, 1, 0, st>>>(s->ctl, s->bad, s->cc.p + s->nch_max * 3 * s->p);
     launched("k_flags");
-    s->comm->allreduce(s->fkd[b].p + 3 * s->p, 2, st);
+    chunk_reduce(s, s->cc.p, 3 * s->p, s->fkd[b].p, ctl_guard, 2);
   } else {
     launch_colsums(s, s->fpart.p, s->nrb_f, s->kpart.p, s->dpart.p, s->nrb_xm, Fcol(s, b),
                    Kcol(s, b), Dvec(s, b), ctl_guard);
@@ -1159,9 +1159,9 @@ static void alloc_state(pcal_session* s) {
   s->up_nchunks = ceil_div(n, s->up_chunk);
   if (s->repro) {
     const int R = s->comm->size;
-    s->cc.alloc((size_t)s->nch_max * 3 * p);
+    s->cc.alloc((size_t)s->nch_max * 3 * p + 2);
     s->cc.zero(st);
-    s->ccg.alloc((size_t)R * s->nch_max * 3 * p);
+    s->ccg.alloc((size_t)R * (s->nch_max * 3 * p + 2));
     s->bbt.alloc((size_t)3 * p);
     s->spt.alloc(3);
     s->spt.zero(st);
