@@ -32,9 +32,9 @@ def phase_of(s: str) -> str:
         return "gradient"
     if "KC,STORE" in s or s == "k_small_pxp":
         return "gram"
-    if "XM" in s or s in ("k_sum_rows", "k_finish_eval", "k_zero_i32"):
+    if "XM" in s or s in ("k_sum_rows", "k_finish_eval", "k_zero_i32", "k_colsum3"):
         return "xm"
-    if s in ("k_bb_partials", "k_eta", "k_update", "k_normalize"):
+    if s in ("k_bb_partials", "k_eta", "k_update", "k_normalize", "k_step_fused"):
         return "step"
     return "other"
 
