@@ -29,6 +29,20 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool va
   const int sz = valid ? 16 : 0;
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
 }
+// Same with an L2 cache policy (createpolicy): the streamed dense operator is
+// marked evict-first so it does not push the reused X out of L2.
+__device__ __forceinline__ void cp_async16_pol(void* smem, const void* gmem, bool valid,
+                                               uint64_t pol) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const int sz = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;\n" ::"r"(s),
+               "l"(gmem), "r"(sz), "l"(pol));
+}
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
@@ -316,6 +330,8 @@ __device__ __forceinline__ void produce(const GemmArgs& g, double* As, double* B
   const int64_t a_rows = Cfg::AMODE == A_MCONTIG ? 64 : RPP * g.lda;  // stride between lane chunks
   const int64_t b_rows = RPP * g.ldb;
   const int lr = lane / CPR, lc = 2 * (lane % CPR);
+  const bool a_stream = Cfg::AMODE == A_MCONTIG && g.a_stream;
+  const uint64_t pol = a_stream ? l2_evict_first_policy() : 0;
   int t = (int)(u0 / g.ki), kk = (int)(u0 % g.ki);  // advanced incrementally
   int s = 0;
   unsigned ph = 0;
@@ -351,9 +367,12 @@ __device__ __forceinline__ void produce(const GemmArgs& g, double* As, double* B
       for (int h = 0; h < AH; ++h) {
         const bool ok = (amask >> h) & 1ull;
 #pragma unroll
-        for (int kr = 0; kr < BK; ++kr)
-          cp_async16(as + kr * Cfg::SA_M + 2 * lane + 64 * h, ok ? pa + h * a_rows + kr * g.lda : g.A,
-                     ok);
+        for (int kr = 0; kr < BK; ++kr) {
+          double* dst = as + kr * Cfg::SA_M + 2 * lane + 64 * h;
+          const double* src = ok ? pa + h * a_rows + kr * g.lda : g.A;
+          if (a_stream) cp_async16_pol(dst, src, ok, pol);
+          else cp_async16(dst, src, ok);
+        }
       }
     } else {
 #pragma unroll

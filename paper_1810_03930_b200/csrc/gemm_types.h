@@ -51,6 +51,7 @@ struct GemmArgs {
   const int32_t* gate;  // early exit when non-null and *gate == 0 (in-graph CholeskyQR)
   int32_t force_ws;     // chunk-partial plans: every CTA stores its partial (no epilogue)
   int32_t segs;         // > 0: segmented schedule, S fixed K segments per tile (see below)
+  int32_t a_stream;     // A is read exactly once (dense gradient): L2 evict-first loads
 };
 
 struct FixupTask {   // one split tile

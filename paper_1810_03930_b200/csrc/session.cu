@@ -913,6 +913,7 @@ static void build_plans(pcal_session* s) {
       }
       g.args.A = s->A.p;
       g.args.lda = s->ldA;
+      g.args.a_stream = 1;  // A streams through once per iteration: keep X resident in L2
       const bool gathered = s->comm && s->comm->size > 1;
       g.args.B = gathered ? s->xfull.p : Xof(s, b);
       g.args.ldb = gathered ? s->K_full : ld;
