@@ -167,17 +167,25 @@ void plan_gemm(GemmPlan& pl, int device, int size, int amode, int epi, int64_t M
   g.ws = pl.ws;
   g.qmax = qmax;
   g.force_ws = chunk_partials ? 1 : 0;
+  // long runs of k-iterations per CTA: split the copy stream over 4 producer
+  // warps; short tiles with heavy epilogues (X·[W|C]) keep a single producer
+  g.nprod = (ki >= 64 && units / std::max(grid, 1) >= 64) ? 4 : 1;
+  if (const char* e = getenv("PCAL_NPROD")) g.nprod = atoi(e) == 4 ? 4 : 1;
   g.segs = segs;
   pl.no_fixup = chunk_partials;
 }
 
 template <class Cfg, int EPI>
 static void launch_cfg(const GemmPlan& pl, cudaStream_t st) {
-  auto kern = gemm_streamk<Cfg, EPI>;
-  static bool attr_set = false;  // per instantiation
+  // separate instantiations per producer count keep the single-producer kernel
+  // (short-K tiles, heavy epilogues) free of the 4-producer code
+  auto kern = pl.args.nprod == 4 ? gemm_streamk<Cfg, EPI, 4> : gemm_streamk<Cfg, EPI, 1>;
+  static bool attr_set = false;  // per (Cfg, EPI)
   if (!attr_set) {
-    PCAL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   Cfg::SMEM_BYTES));
+    PCAL_CUDA(cudaFuncSetAttribute(gemm_streamk<Cfg, EPI, 1>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
+    PCAL_CUDA(cudaFuncSetAttribute(gemm_streamk<Cfg, EPI, 4>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
     attr_set = true;
   }
   kern<<<pl.args.grid, Cfg::THREADS + 128, Cfg::SMEM_BYTES, st>>>(pl.args);

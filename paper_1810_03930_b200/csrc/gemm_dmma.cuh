@@ -305,10 +305,14 @@ __device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)));
 }
 
-// ---- producer: one warp streams the CTA's unit range into the smem ring ---------
+// ---- producers: NP warps of the producer warpgroup stream the CTA's unit
+// range into the smem ring, each 1/NP of every stage.  Long-K products use all
+// 4 (one per SM sub-partition, so no consumer pair shares its issue slots with
+// the whole copy stream); short-K tiles with heavy epilogues use one.
 // Per-lane source pointers are set up once per tile and advanced by one k-slice
 // per unit, so the copy loop is pure LDGSTS + pointer increments.
-template <class Cfg>
+constexpr int kProducerRegs = 40;  // per producer thread after setmaxnreg
+template <class Cfg, int PW, int NP>
 __device__ __forceinline__ void produce(const GemmArgs& g, double* As, double* Bs,
                                         uint64_t* full, uint64_t* empty, int64_t u0, int64_t u1,
                                         int lane) {
@@ -367,7 +371,7 @@ __device__ __forceinline__ void produce(const GemmArgs& g, double* As, double* B
       for (int h = 0; h < AH; ++h) {
         const bool ok = (amask >> h) & 1ull;
 #pragma unroll
-        for (int kr = 0; kr < BK; ++kr) {
+        for (int kr = PW; kr < BK; kr += NP) {
           double* dst = as + kr * Cfg::SA_M + 2 * lane + 64 * h;
           const double* src = ok ? pa + h * a_rows + kr * g.lda : g.A;
           if (a_stream) cp_async16_pol(dst, src, ok, pol);
@@ -376,13 +380,13 @@ __device__ __forceinline__ void produce(const GemmArgs& g, double* As, double* B
       }
     } else {
 #pragma unroll
-      for (int h = 0; h < AH; ++h) {
+      for (int h = PW; h < AH; h += NP) {
         const bool ok = (amask >> h) & 1ull;
         cp_async16(as + (lr + RPP * h) * Cfg::SA_K + lc, ok ? pa + h * a_rows : g.A, ok);
       }
     }
 #pragma unroll
-    for (int j = 0; j < BJ; ++j) {
+    for (int j = PW; j < BJ; j += NP) {
       const bool ok = (bmask >> j) & 1ull;
       cp_async16(bs + (lr + RPP * j) * Cfg::SB_K + lc, ok ? pb + j * b_rows : g.B, ok);
     }
@@ -404,7 +408,7 @@ __device__ __forceinline__ void produce(const GemmArgs& g, double* As, double* B
 // Warp-specialized: warps [0, WARPS) consume (LDS + DMMA + epilogue), warp
 // WARPS produces (cp.async ring, one mbarrier pair per stage); the rest of
 // the producer warpgroup only donates its registers.
-template <class Cfg, int EPI>
+template <class Cfg, int EPI, int NPROD>
 __global__ void __launch_bounds__(Cfg::THREADS + 128, 1) gemm_streamk(GemmArgs g) {
   if (g.ctl && g.ctl->done) return;
   if (g.gate && !*g.gate) return;
@@ -422,27 +426,35 @@ __global__ void __launch_bounds__(Cfg::THREADS + 128, 1) gemm_streamk(GemmArgs g
   if (u0 >= u1) return;
   if (threadIdx.x == 0) {
     for (int s = 0; s < Cfg::STAGES; ++s) {
-      mbar_init(&full[s], 32);
+      mbar_init(&full[s], 32 * NPROD);
       mbar_init(&empty[s], Cfg::WARPS);
     }
   }
   __syncthreads();
   // The producer owns a whole warpgroup (setmaxnreg is warpgroup-collective):
   // with 8 consumer warps, consumers take 232 registers and the producer
-  // group 40 (8·32·232 + 4·32·40 ≤ 64K).
+  // group kProducerRegs = 40 (8·32·232 + 4·32·40 ≤ 64K).
   if (warp >= Cfg::WARPS) {
-    if constexpr (Cfg::WARPS >= 8) asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::);
-    if (warp == Cfg::WARPS) {
-      produce<Cfg>(g, As, Bs, full, empty, u0, u1, lane);
-      cp_async_wait<0>();
+    if constexpr (Cfg::WARPS >= 8) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kProducerRegs));
+    const int pw = warp - Cfg::WARPS;
+    if constexpr (NPROD == 4) {
+      switch (pw) {
+        case 0: produce<Cfg, 0, 4>(g, As, Bs, full, empty, u0, u1, lane); break;
+        case 1: produce<Cfg, 1, 4>(g, As, Bs, full, empty, u0, u1, lane); break;
+        case 2: produce<Cfg, 2, 4>(g, As, Bs, full, empty, u0, u1, lane); break;
+        default: produce<Cfg, 3, 4>(g, As, Bs, full, empty, u0, u1, lane); break;
+      }
+    } else {
+      if (pw == 0) produce<Cfg, 0, 1>(g, As, Bs, full, empty, u0, u1, lane);
     }
+    cp_async_wait<0>();
     return;
   }
   if constexpr (Cfg::WARPS >= 8) {
     // (64K − 128·40) / consumer threads, rounded down to a multiple of 8, ≤ 232
-    constexpr int R = (65536 - 128 * 40) / Cfg::THREADS / 8 * 8 > 232
+    constexpr int R = (65536 - 128 * kProducerRegs) / Cfg::THREADS / 8 * 8 > 232
                           ? 232
-                          : (65536 - 128 * 40) / Cfg::THREADS / 8 * 8;
+                          : (65536 - 128 * kProducerRegs) / Cfg::THREADS / 8 * 8;
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(R));
   }
   const int wm = warp / Cfg::WARPS_N, wn = warp % Cfg::WARPS_N;
