@@ -242,6 +242,21 @@ inline DenseMatrix initial_point_qr(std::int64_t n, std::int64_t p, std::uint64_
   return x;
 }
 
+// InitMode / InitialPointSpec / initial_point (solver.hpp:47-59, solver.cpp:136-170)
+enum class InitMode { Qr = PCAL_INIT_QR, A2TypeI = PCAL_INIT_A2_TYPE_I, A2TypeII = PCAL_INIT_A2_TYPE_II };
+struct InitialPointSpec {
+  InitMode mode = InitMode::Qr;
+  double sigma_lower = 0.5;  // a2-i only; requires sigma² <= 1/2
+  std::uint64_t seed = 0;
+};
+inline DenseMatrix initial_point(const InitialPointSpec& spec, std::int64_t n, std::int64_t p,
+                                 int device = 0) {
+  DenseMatrix x(n, p);
+  check(pcal_initial_point(n, p, static_cast<int32_t>(spec.mode), spec.sigma_lower, spec.seed,
+                           x.data(), device));
+  return x;
+}
+
 // flops_estimate(Pcal, n, p) (diagnostics.cpp:100-114)
 inline double flops_estimate(std::int64_t n, std::int64_t p) { return pcal_flops_estimate(n, p); }
 

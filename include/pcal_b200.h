@@ -244,6 +244,17 @@ int pcal_gen_dense_operator(int64_t n, uint64_t seed, double* a, int32_t threads
 /* initial_point({Qr}, n, p) on the device: orthonormalize(random_normal(n,p,Rng(seed)))
  * (solver.cpp:136-142). */
 int pcal_initial_point_qr(int64_t n, int64_t p, uint64_t seed, double* x0, int32_t device);
+/* initial_point(InitialPointSpec{mode, sigma_lower, seed}, n, p) (solver.cpp:136-170,
+ * solver.hpp:47-59): Q = orthonormalize(random_normal(n,p,Rng(seed))) on the
+ * device, then for the Assumption-A2 starts the column scaling of the
+ * reference — type I: last column ·√(1−σ²) (σ ∈ (0,1), σ² ≤ ½); type II:
+ * column j ·√(1 + b·(2u_j − 1)), b = 0.9/√p, u_j the next uniforms of the same
+ * stream, |·−1| floored at 0.1·b.  Invalid arguments: PCAL_E_PARAMETER. */
+#define PCAL_INIT_QR 0
+#define PCAL_INIT_A2_TYPE_I 1
+#define PCAL_INIT_A2_TYPE_II 2
+int pcal_initial_point(int64_t n, int64_t p, int32_t mode, double sigma_lower, uint64_t seed,
+                       double* x0, int32_t device);
 
 #ifdef __cplusplus
 }

@@ -164,6 +164,21 @@ def report_io_cases(R: Reference) -> None:
     print("wrote report/container fixtures")
 
 
+def init_cases(R: Reference) -> None:
+    """initial_point(InitialPointSpec) for the three InitMode values (solver.cpp:136-170)."""
+    import ctypes as C
+    g = {}
+    for name, mode, sigma, n, p, seed in [("qr", 0, 0.5, 30, 4, 11), ("a2i", 1, 0.6, 30, 4, 12),
+                                          ("a2ii", 2, 0.5, 31, 5, 13), ("a2ii_p1", 2, 0.5, 8, 1, 14)]:
+        out = np.zeros((n, p), order="F")
+        assert R.lib.ref_initial_point(mode, sigma, seed, n, p,
+                                       out.ctypes.data_as(C.POINTER(C.c_double))) == 0
+        g[name] = out
+        g[name + "_args"] = np.array([mode, sigma, n, p, seed], dtype=float)
+    np.savez_compressed(os.path.join(OUT, "reference_init.npz"), **g)
+    print("wrote reference_init.npz")
+
+
 def grid_cases(R: Reference) -> None:
     """Grid models (no reference implementation): the reference solve() driving
     the restated operator — pins the PCAL loop around it, not the operator."""
@@ -211,5 +226,6 @@ if __name__ == "__main__":
     grid_cases(R)
     algorithm_cases(R)
     report_io_cases(R)
+    init_cases(R)
     if "--cfg2" in sys.argv:
         cfg2(R)

@@ -146,6 +146,7 @@ def lib() -> C.CDLL:
     L.pcal_random_uniform.argtypes = [i64, u64, vp]
     L.pcal_gen_dense_operator.argtypes = [i64, u64, vp, i32]
     L.pcal_initial_point_qr.argtypes = [i64, i64, u64, vp, i32]
+    L.pcal_initial_point.argtypes = [i64, i64, i32, dbl, u64, vp, i32]
     L.pcal_partition.argtypes = [C.POINTER(_Model), i32, i32, C.POINTER(i64), C.POINTER(i64)]
     L.pcal_nccl_unique_id.argtypes = [vp]
     L.pcal_comm_create_nccl.argtypes = [i32, i32, vp, i32, C.POINTER(vp)]
@@ -544,10 +545,17 @@ def spectral_norm_estimate(a, seed: int, device: int = 0) -> float:
     return s.value
 
 
-def initial_point(n: int, p: int, seed: int, device: int = 0) -> np.ndarray:
-    """initial_point({Qr}, n, p) with Rng(seed) (solver.cpp:136-142)."""
+INIT_MODES = {"qr": 0, "a2-i": 1, "a2-ii": 2}  # InitMode (solver.hpp:47), harness names
+
+
+def initial_point(n: int, p: int, seed: int, device: int = 0, mode: str = "qr",
+                  sigma_lower: float = 0.5) -> np.ndarray:
+    """initial_point(InitialPointSpec{mode, sigma_lower, seed}, n, p)
+    (solver.cpp:136-170): "qr", or the Assumption-A2 starts "a2-i" / "a2-ii"."""
+    if mode not in INIT_MODES:
+        raise ParameterError(f"initial_point: unknown mode {mode!r}")
     x = np.zeros((n, p), order="F")
-    _check(lib().pcal_initial_point_qr(n, p, seed, _ptr(x), device))
+    _check(lib().pcal_initial_point(n, p, INIT_MODES[mode], sigma_lower, seed, _ptr(x), device))
     return x
 
 

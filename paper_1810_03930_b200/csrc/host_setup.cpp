@@ -96,6 +96,13 @@ void host_random_normal(int64_t count, uint64_t seed, double* out, int threads) 
   for (auto& th : pool) th.join();
 }
 
+void host_uniform_after_normals(int64_t nnormals, uint64_t seed, int64_t count, double* out) {
+  Rng r(seed);
+  const int64_t skip = 2 * ((nnormals + 1) / 2);
+  for (int64_t q = 0; q < skip; ++q) (void)r.next();
+  for (int64_t k = 0; k < count; ++k) out[k] = r.uniform();
+}
+
 void host_random_uniform(int64_t count, uint64_t seed, double* out) {
   Rng r(seed);
   for (int64_t k = 0; k < count; ++k) out[k] = r.uniform();

@@ -5,6 +5,9 @@
 namespace pcal {
 void host_random_normal(int64_t count, uint64_t seed, double* out, int threads);
 void host_random_uniform(int64_t count, uint64_t seed, double* out);
+// `count` uniforms of Rng(seed) drawn after `nnormals` normal() calls (each
+// Box–Muller pair consumes two raw draws; a cached spare does not).
+void host_uniform_after_normals(int64_t nnormals, uint64_t seed, int64_t count, double* out);
 }  // namespace pcal
 
 void pcal_fourier_basis(int64_t N, double* q, double* lam);

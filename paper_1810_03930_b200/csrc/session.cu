@@ -2166,6 +2166,39 @@ int pcal_initial_point_qr(int64_t n, int64_t p, uint64_t seed, double* x0, int32
   });
 }
 
+int pcal_initial_point(int64_t n, int64_t p, int32_t mode, double sigma_lower, uint64_t seed,
+                       double* x0, int32_t device) {
+  return guarded([&] {
+    if (n < 1 || p < 1 || 2 * p > n)  // solver.cpp:137-138
+      throw Error(PCAL_E_PARAMETER, "initial_point: dimensions must satisfy 2p <= n");
+    if (mode != PCAL_INIT_QR && mode != PCAL_INIT_A2_TYPE_I && mode != PCAL_INIT_A2_TYPE_II)
+      throw Error(PCAL_E_PARAMETER, "initial_point: unknown mode");
+    const double sl = sigma_lower;
+    if (mode == PCAL_INIT_A2_TYPE_I && (!(sl > 0.0 && sl < 1.0) || sl * sl > 0.5))
+      throw Error(PCAL_E_PARAMETER,
+                  "initial_point: a2-i requires sigma in (0,1) with sigma^2 <= 1/2");
+    if (!x0) throw Error(PCAL_E_PARAMETER, "NULL argument");
+    const int rc = pcal_initial_point_qr(n, p, seed, x0, device);
+    if (rc != PCAL_OK) throw Error(rc, g_last_error);
+    std::vector<double> d((size_t)p, 1.0);
+    if (mode == PCAL_INIT_A2_TYPE_I) {
+      d.back() = std::sqrt(1.0 - sl * sl);
+    } else if (mode == PCAL_INIT_A2_TYPE_II) {  // singular values inside the A2 band (solver.cpp:153-167)
+      const double band = 0.9 / std::sqrt(static_cast<double>(p));
+      std::vector<double> u((size_t)p);
+      host_uniform_after_normals(n * p, seed, p, u.data());
+      for (int64_t j = 0; j < p; ++j) {
+        double sq = 1.0 + band * (2.0 * u[j] - 1.0);
+        if (std::abs(sq - 1.0) < 0.1 * band) sq = 1.0 + 0.1 * band;
+        d[j] = std::sqrt(sq);
+      }
+    }
+    if (mode != PCAL_INIT_QR)  // scale_cols_in_place (kernels.cpp:338-346)
+      for (int64_t j = 0; j < p; ++j)
+        for (int64_t i = 0; i < n; ++i) x0[i + j * n] *= d[j];
+  });
+}
+
 int pcal_evaluate(const pcal_model_desc* model, const double* x, double* f, double* g,
                   int32_t device) {
   return guarded([&] {

@@ -72,3 +72,16 @@ def test_no_cpu_fallback(pcal):
         pcal.solve(pcal.QuadraticModel(a, 2, 1.0), pcal.SolverConfig(), x)
     with pytest.raises(pcal.NativeUnavailable):
         pcal.gram(x)
+
+
+def test_initial_point_argument_checks_are_host_side(pcal):
+    """initial_point's parameter_error cases (solver.cpp:137-138,144-146) fail
+    before any device work."""
+    with pytest.raises(pcal.ParameterError):
+        pcal.initial_point(30, 16, 1)                       # 2p > n
+    with pytest.raises(pcal.ParameterError):
+        pcal.initial_point(30, 4, 1, mode="a2-i", sigma_lower=0.8)  # σ² > 1/2
+    with pytest.raises(pcal.ParameterError):
+        pcal.initial_point(30, 4, 1, mode="a2-i", sigma_lower=0.0)
+    with pytest.raises(pcal.ParameterError):
+        pcal.initial_point(30, 4, 1, mode="a3")

@@ -171,3 +171,18 @@ def test_stencil_march_bitwise(pcal, orc, grid, p):
     f, g = pcal.evaluate(pcal.StencilModel(grid, v, p, 13.0), x)
     assert np.array_equal(g, g_ref)
     assert abs(f - f_ref) <= 1e-12 * abs(f_ref)
+
+
+@pytest.mark.parametrize("name,mode", [("qr", "qr"), ("a2i", "a2-i"), ("a2ii", "a2-ii"),
+                                       ("a2ii_p1", "a2-ii")])
+def test_initial_point_modes_match_reference(pcal, name, mode):
+    """initial_point(InitialPointSpec) for Qr / A2TypeI / A2TypeII against the
+    reference's own output (tests/golden/reference_init.npz): the column scale
+    factors come from the same random stream, the Q factor agrees to rounding."""
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "reference_init.npz"))
+    ref = g[name]
+    m, sigma, n, p, seed = g[name + "_args"]
+    x = pcal.initial_point(int(n), int(p), int(seed), mode=mode, sigma_lower=float(sigma))
+    assert x.shape == ref.shape
+    assert np.abs(x - ref).max() <= 1e-12
+    assert np.allclose(np.linalg.norm(x, axis=0), np.linalg.norm(ref, axis=0), rtol=1e-14, atol=0)
