@@ -18,11 +18,12 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def short(name: str) -> str:
     nm = name.replace("pcal::", "").replace("(int)", "")
-    m = re.search(r"gemm_(streamk|fixup|fixup_store)<GemmCfg<(\d+), (\d+), \d+, \d+, \d+, (\d)(?:, \d+)?>(?:, (\d))?", nm)
+    m = re.search(r"gemm_(streamk|fixup|fixup_store)<GemmCfg<(\d+), (\d+), \d+, \d+, \d+, (\d)(?:, \d+)?>(?:, (\d))?(?:, (\d))?", nm)
     if m:
         kind = {"0": "STORE", "1": "GRAD", "2": "XM", None: "STORE"}[m.group(5)]
         mode = "MC" if m.group(4) == "0" else "KC"
-        return f"gemm_{m.group(1)}<{m.group(2)}x{m.group(3)},{mode},{kind}>"
+        prod = f",P{m.group(6)}" if m.group(6) else ""
+        return f"gemm_{m.group(1)}<{m.group(2)}x{m.group(3)},{mode},{kind}{prod}>"
     m = re.search(r"(k_[a-z0-9_]+)", name)
     return m.group(1) if m else name[:60]
 
