@@ -50,19 +50,28 @@ int pick_size(int64_t N) {
   return CFG_SMALL;
 }
 
-int64_t count_tiles(int size, int64_t M, int64_t N, int64_t sym_row0) {
+// Tile (tm, tn) lies strictly below the diagonal of a symmetric square block:
+// the block starting at row sym_row0, and with sym_first also the one at row 0.
+static bool below_diagonal(const CfgInfo& ci, int64_t tm, int64_t tn, int64_t sym_row0,
+                           bool sym_first) {
+  if (sym_row0 < 0) return false;
+  const int64_t r0 = tm * ci.BM, c1 = (tn + 1) * ci.BN - 1;
+  if (r0 >= sym_row0) return (r0 - sym_row0) > c1;
+  return sym_first && r0 > c1;
+}
+
+int64_t count_tiles(int size, int64_t M, int64_t N, int64_t sym_row0, bool sym_first) {
   const CfgInfo ci = cfg_info(size);
   int64_t c = 0;
   for (int64_t tm = 0; tm < ceil_div(M, ci.BM); ++tm)
     for (int64_t tn = 0; tn < ceil_div(N, ci.BN); ++tn)
-      if (!(sym_row0 >= 0 && tm * ci.BM >= sym_row0 && (tm * ci.BM - sym_row0) > (tn + 1) * ci.BN - 1))
-        ++c;
+      if (!below_diagonal(ci, tm, tn, sym_row0, sym_first)) ++c;
   return c;
 }
 
 void plan_gemm(GemmPlan& pl, int device, int size, int amode, int epi, int64_t M,
                       int64_t N, int64_t K, int64_t sym_row0, int grid_override, int fixed_splits,
-                      bool chunk_partials, int qmax_min) {
+                      bool chunk_partials, int qmax_min, bool sym_first) {
   pl.release();
   pl.size = size;
   pl.amode = amode;
@@ -75,11 +84,7 @@ void plan_gemm(GemmPlan& pl, int device, int size, int amode, int epi, int64_t M
   // tm-major: consecutive tiles share the A row-block (L2 reuse across tn)
   for (int64_t tm = 0; tm < tm_n; ++tm)
     for (int64_t tn = 0; tn < tn_n; ++tn) {
-      if (sym_row0 >= 0) {
-        const int64_t r0 = tm * ci.BM;
-        const int64_t c1 = (tn + 1) * ci.BN - 1;
-        if (r0 >= sym_row0 && (r0 - sym_row0) > c1) continue;  // strictly below diagonal
-      }
+      if (below_diagonal(ci, tm, tn, sym_row0, sym_first)) continue;
       tiles.push_back(make_int2((int)tm, (int)tn));
     }
   const int ntiles = (int)tiles.size();

@@ -114,7 +114,8 @@ struct GemmPlan {
 };
 
 // Build a plan.  `sym_row0` >= 0 skips tiles lying strictly below the diagonal
-// of the block starting at row sym_row0 (the XᵀX half of the Gram).
+// of the block starting at row sym_row0 (the XᵀX half of the Gram); with
+// `sym_first` also those of the block at row 0 (GᵀX of a symmetric operator).
 //
 // Reproducible schedules (the sharded path):
 //   fixed_splits = S > 0: every tile's K range is cut into the same S segments
@@ -125,10 +126,11 @@ struct GemmPlan {
 //     ([task][q][BM·BN], q padded to qmax_min) for an ordered sum across ranks.
 void plan_gemm(GemmPlan& pl, int device, int size, int amode, int epi, int64_t M, int64_t N,
                int64_t K, int64_t sym_row0 = -1, int grid_override = 0, int fixed_splits = 0,
-               bool chunk_partials = false, int qmax_min = 0);
+               bool chunk_partials = false, int qmax_min = 0, bool sym_first = false);
 void launch_gemm(const GemmPlan& pl, cudaStream_t st);
 // Tiles plan_gemm schedules for an M×N output (same skipping rule).
-int64_t count_tiles(int size, int64_t M, int64_t N, int64_t sym_row0 = -1);
+int64_t count_tiles(int size, int64_t M, int64_t N, int64_t sym_row0 = -1,
+                    bool sym_first = false);
 // Fixed-tree reduction of a chunk-partial plan's ws (gemm_dmma.cuh):
 // local maximal-node sums into `out` ([nnodes][ntasks][BM·BN]), then the
 // merge of every rank's node sums (buf = [R][maxn][ntasks][BM·BN]) into ep.C.

@@ -45,7 +45,7 @@ enum { MC_PCAL = 0, MC_DA = 1, MC_MOPTQR = 2 };
 __global__ void k_small_pxp(const double* __restrict__ gr, int64_t pp, int64_t p,
                             double* __restrict__ mcat, int64_t ldk, double* __restrict__ cpart,
                             int mode, double beta, double* __restrict__ lam, int lam_init,
-                            const Ctl* ctl) {
+                            const Ctl* ctl, int gx_upper = 0) {
   if (ctl && ctl->done) return;
   __shared__ double sm[kStreamThreads / 32];
   const int64_t total = p * p;
@@ -54,8 +54,10 @@ __global__ void k_small_pxp(const double* __restrict__ gr, int64_t pp, int64_t p
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t k = e % p, j = e / p;
-    const double w = 0.5 * (gr[k + j * ldg] + gr[j + k * ldg]);
     const int64_t a = min(k, j), b = max(k, j);
+    // symmetric operator: GᵀX = XᵀAX is symmetric, only its upper triangle is
+    // computed and Ψ reduces to it (equal to ½(M + Mᵀ) up to rounding)
+    const double w = gx_upper ? gr[a + b * ldg] : 0.5 * (gr[k + j * ldg] + gr[j + k * ldg]);
     double c = gr[pp + a + b * ldg];
     if (k == j) c += -1.0;
     double m;

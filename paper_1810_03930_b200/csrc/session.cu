@@ -346,6 +346,7 @@ struct pcal_session {
   int32_t* rank_nch_d = nullptr;          // chunks per rank (device)
   int grad_splits = 0;                    // dense gradient: fixed K segments per tile
   int gram_sub = 1, orth_sub = 1;         // Gram segments per row chunk (fixed globally)
+  bool sym_gx = false;                    // GᵀX symmetric (grid models): upper tiles only
   pcal::DevBuf cc, ccg, bbt, spt;         // chunk partials, gathered, totals
   struct Tree {                           // fixed-tree Gram reduction (0: iteration, 1: orth)
     int maxn = 0, nloc = 0;
@@ -683,7 +684,8 @@ static void launch_eval(pcal_session* s, int b, int mode, const Ctl* ctl_guard) 
                                                                              : MC_PCAL;
     k_small_pxp<<<s->cp_blocks, kStreamThreads, 0, st>>>(s->gr.p, s->pp, s->p, s->mcat.p, s->pp,
                                                          s->cpart.p, mc, s->beta, s->lam.p,
-                                                         mode == 1 ? 1 : 0, ctl_guard);
+                                                         mode == 1 ? 1 : 0, ctl_guard,
+                                                         s->sym_gx ? 1 : 0);
   }
   launched("k_small_pxp");
   mark(s, 3);
@@ -935,9 +937,10 @@ static void build_plans(pcal_session* s) {
       if (s->repro)  // one partial per row chunk, summed across ranks in chunk order
         plan_gemm(g, dev, pick_size(pp), A_KCONTIG, EPI_STORE, 2 * pp, pp,
                   s->nch * s->chunk_rows, pp, 0, (int)(s->nch * s->gram_sub), true,
-                  (int)(s->nch_max * s->gram_sub));
+                  (int)(s->nch_max * s->gram_sub), s->sym_gx);
       else
-        plan_gemm(g, dev, pick_size(pp), A_KCONTIG, EPI_STORE, 2 * pp, pp, ld, pp);
+        plan_gemm(g, dev, pick_size(pp), A_KCONTIG, EPI_STORE, 2 * pp, pp, ld, pp, 0, 0, false,
+                  0, s->sym_gx);
       g.args.A = s->pair[b].p;
       g.args.lda = ld;
       g.args.B = Xof(s, b);
@@ -1062,7 +1065,7 @@ static void choose_segments(pcal_session* s, int64_t NC) {
         [&](int S) { return (double)s->K_full / S; }, false);
   }
   const int smax = (int)std::min<int64_t>(16, Q / ci.BK);
-  const double tg = (double)count_tiles(pick_size(pp), 2 * pp, pp, pp);
+  const double tg = (double)count_tiles(pick_size(pp), 2 * pp, pp, pp, s->sym_gx);
   const double to = (double)count_tiles(pick_size(pp), pp, pp, 0);
   // chunk partials are always stored, so even m = 1 pays the partial traffic
   s->gram_sub = best_segments(
@@ -1519,6 +1522,10 @@ void session_create(const pcal_model_desc* model, const pcal_config* config, con
   }
   s->K_full = padded_ld(s->n_glob);
   s->alg = config->algorithm;
+  // the grid models' operators are symmetric, so GᵀX = XᵀLX (+ XᵀVX) is: only its
+  // upper triangle is computed (MOptQR uses the unsymmetrised GᵀX)
+  s->sym_gx = model->kind != PCAL_MODEL_DENSE && s->alg != PCAL_ALG_MOPTQR &&
+              !getenv("PCAL_FULL_GX");
   if (comm && s->alg == PCAL_ALG_MOPTQR)
     throw Error(PCAL_E_UNSUPPORTED, "MOptQR is single-GPU (its MGS2 fallback is not sharded)");
   // resolve_beta (solver.cpp:120-134)
