@@ -220,6 +220,42 @@ def cfg2(R: Reference) -> None:
     print("wrote reference_cfg2.npz")
 
 
+def grids_full(R: Reference) -> None:
+    """Configs 3 and 4 at full size (64³×256 stencil, 48³×512 Kohn–Sham):
+    the reference solve() driving the restated operators for 3 iterations.  The
+    instances are the product's definitions (paper_1810_03930_b200/problems.py)
+    built from the reference's random stream."""
+    import time
+    from oracle.oracle import Restatement
+    from paper_1810_03930_b200.problems import ks_potential
+    O = Restatement()
+    g = {}
+    for name, kind, grid, p in [("cfg3", MODEL_STENCIL, (64, 64, 64), 256),
+                                ("cfg4", MODEL_KOHN_SHAM, (48, 48, 48), 512)]:
+        n = grid[0] * grid[1] * grid[2]
+        if kind == MODEL_STENCIL:
+            v = O.random_uniform(n, 1)
+            s = 12.0 + float(np.max(v))
+        else:
+            v = ks_potential(grid, 1, O)
+            s = 6.0 + float(np.max(np.abs(v)))
+        t = time.time()
+        x0 = O.initial_point_qr(n, p, 1 ^ INIT_SALT, threads=16)
+        print(name, "x0:", time.time() - t, flush=True)
+        t = time.time()
+        case, rep = run_case(R, Model(kind, n, p, s, grid=grid, v=v), x0, tol_rel_kkt=TINY,
+                             max_iter=3, threads=16, final_orth=False)
+        print(name, "3 iters:", time.time() - t, flush=True)
+        g[name + "_v_sha"] = sha(v)
+        g[name + "_x0_sha"] = sha(x0)
+        g[name + "_s"] = s
+        for k, val in case.items():
+            g[name + "_" + k] = val
+        g[name + "_stop_x_rows"] = rep.stop_x[:8]
+    np.savez_compressed(os.path.join(OUT, "reference_grids_full.npz"), **g)
+    print("wrote reference_grids_full.npz")
+
+
 if __name__ == "__main__":
     R = Reference()
     small(R)
@@ -229,3 +265,5 @@ if __name__ == "__main__":
     init_cases(R)
     if "--cfg2" in sys.argv:
         cfg2(R)
+    if "--grids" in sys.argv:
+        grids_full(R)
