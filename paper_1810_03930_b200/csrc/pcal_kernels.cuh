@@ -324,6 +324,31 @@ __global__ void k_chunk_sum(const double* __restrict__ buf, int R, const int32_t
   out[w] = s;
 }
 
+// z[r0:r1) ·= inv in place, 4 loads in flight per thread (an in-place
+// read-modify-write loop would otherwise serialise on possible aliasing);
+// returns whether a non-finite value was produced.
+__device__ __forceinline__ bool scale_range(double* __restrict__ zj, int64_t r0, int64_t r1,
+                                            double inv) {
+  bool bad = false;
+  const int64_t T = blockDim.x;
+  int64_t i = r0 + threadIdx.x;
+  for (; i + 3 * T < r1; i += 4 * T) {
+    const double v0 = zj[i], v1 = zj[i + T], v2 = zj[i + 2 * T], v3 = zj[i + 3 * T];
+    const double w0 = v0 * inv, w1 = v1 * inv, w2 = v2 * inv, w3 = v3 * inv;
+    zj[i] = w0;
+    zj[i + T] = w1;
+    zj[i + 2 * T] = w2;
+    zj[i + 3 * T] = w3;
+    bad |= !isfinite(w0) || !isfinite(w1) || !isfinite(w2) || !isfinite(w3);
+  }
+  for (; i < r1; i += T) {
+    const double v = zj[i] * inv;
+    zj[i] = v;
+    bad |= !isfinite(v);
+  }
+  return bad;
+}
+
 // pcal_step part 2 (solver.cpp:283-305): z ·= 1/‖z‖; a column with ‖z‖ < 1e-14
 // keeps the previous column renormalized (or e_{j mod n}); non-finite ⇒ diverged.
 __global__ void k_normalize(const double* __restrict__ x, double* __restrict__ z, int64_t n,
@@ -349,27 +374,25 @@ __global__ void k_normalize(const double* __restrict__ x, double* __restrict__ z
   const int64_t j = blockIdx.y;
   const int64_t r0 = (int64_t)blockIdx.x * chunk;
   const int64_t r1 = min(n, r0 + chunk);
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {  // ‖z_j‖² from the chunk partials: one warp, fixed order
     double nrm2 = 0.0;
     if (nrm) {
-      nrm2 = nrm[j];  // sharded: global column norm (allreduced)
+      nrm2 = threadIdx.x == 0 ? nrm[j] : 0.0;  // sharded: global column norm (all-reduced)
     } else {
-      for (int64_t c = 0; c < nchunks; ++c) nrm2 += npart[c * p + j];
+      for (int64_t c = threadIdx.x; c < nchunks; c += 32) nrm2 += npart[c * p + j];
+      nrm2 = warp_sum(nrm2);
     }
-    const double nz = sqrt(nrm2);
-    s_deg = nz < 1e-14;
-    s_inv = 1.0 / nz;
+    if (threadIdx.x == 0) {
+      const double nz = sqrt(nrm2);
+      s_deg = nz < 1e-14;
+      s_inv = 1.0 / nz;
+    }
   }
   __syncthreads();
   double* zj = z + j * ld;
   bool bad = false;
   if (!s_deg) {
-    const double inv = s_inv;
-    for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
-      const double v = zj[i] * inv;
-      zj[i] = v;
-      bad |= !isfinite(v);
-    }
+    bad = scale_range(zj, r0, r1, s_inv);
   } else {
     // degenerate column: whole-column norm of the previous iterate (rare path)
     const double* xj = x + j * ld;
@@ -539,22 +562,20 @@ __device__ __forceinline__ bool step_phase(const StepArgs& a, Ctl* ctl) {
   for (int64_t it = blockIdx.x; it < items && !a.plain; it += gridDim.x) {
     const int64_t c = it % a.nchunks, j = it / a.nchunks;
     const int64_t r0 = c * a.chunk, r1 = min(a.n, r0 + a.chunk);
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {  // same fixed order as k_normalize
       double nrm2 = 0.0;
-      for (int64_t q = 0; q < a.nchunks; ++q) nrm2 += a.npart[q * a.p + j];
-      const double nz = sqrt(nrm2);
-      s_deg = nz < 1e-14;
-      s_inv = 1.0 / nz;
+      for (int64_t q = threadIdx.x; q < a.nchunks; q += 32) nrm2 += a.npart[q * a.p + j];
+      nrm2 = warp_sum(nrm2);
+      if (threadIdx.x == 0) {
+        const double nz = sqrt(nrm2);
+        s_deg = nz < 1e-14;
+        s_inv = 1.0 / nz;
+      }
     }
     __syncthreads();
     double* zj = a.z + j * a.ld;
     if (!s_deg) {
-      const double inv = s_inv;
-      for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
-        const double v = zj[i] * inv;
-        zj[i] = v;
-        bad |= !isfinite(v);
-      }
+      bad |= scale_range(zj, r0, r1, s_inv);
     } else {
       const double* xj = a.x + j * a.ld;
       double acc = 0.0;
