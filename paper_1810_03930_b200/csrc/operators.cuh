@@ -96,7 +96,9 @@ __global__ void __launch_bounds__(32 * TY)
   // all global loads run one z-step ahead: planes z+1 (interior), the y-halo
   // rows of plane z+1 and the potential u of plane z+1 are fetched while
   // plane z is computed
-  double below[XP], cur[XP], above[XP], halo[XP], uc[XP];
+  // halo rows are consumed at the START of an iteration (smem fill), so they
+  // are fetched two planes ahead; interior planes and u one plane ahead
+  double below[XP], cur[XP], above[XP], halo[XP], halo_n[XP], uc[XP];
   // plane z of column j: periodic wrap on a single GPU; on a z-slab of a
   // sharded grid, planes −1 and nz come from the neighbours' halo planes
   auto src = [&](int z) -> const double* {
@@ -116,12 +118,12 @@ __global__ void __launch_bounds__(32 * TY)
     cur[k] = ok ? __ldg(src(z0) + (int64_t)y * nx + xx) : 0.0;
     above[k] = ok ? __ldg(src(z0 + 1) + (int64_t)y * nx + xx) : 0.0;
     halo[k] = (ok && hrow) ? __ldg(src(z0) + (int64_t)yh * nx + xx) : 0.0;
+    halo_n[k] = (ok && hrow && z0 + 1 < z1) ? __ldg(src(z0 + 1) + (int64_t)yh * nx + xx) : 0.0;
     uc[k] = ok ? __ldg(u + (int64_t)z0 * nxy + (int64_t)y * nx + xx) : 0.0;
   }
   double acc = 0.0;
   bool nonfinite = false;
   for (int z = z0; z < z1; ++z) {
-    const double* sn = src(z + 1);
     const double* sa = src(z + 2);
     const int64_t pz = (int64_t)z * nxy, pn = pz + nxy;
 #pragma unroll
@@ -133,14 +135,14 @@ __global__ void __launch_bounds__(32 * TY)
       }
     }
     __syncthreads();
-    double above2[XP], halo_n[XP], u_n[XP];
-    const bool more = z + 1 < z1;
+    double above2[XP], halo_nn[XP], u_n[XP];
+    const bool more = z + 1 < z1, more2 = z + 2 < z1;
 #pragma unroll
     for (int k = 0; k < XP; ++k) {
       const int xx = lane + 32 * k;
       const bool ok = xx < nx && more;
       above2[k] = ok ? __ldg(sa + (int64_t)y * nx + xx) : 0.0;
-      halo_n[k] = (ok && hrow) ? __ldg(sn + (int64_t)yh * nx + xx) : 0.0;
+      halo_nn[k] = (xx < nx && more2 && hrow) ? __ldg(sa + (int64_t)yh * nx + xx) : 0.0;
       u_n[k] = ok ? __ldg(u + pn + (int64_t)y * nx + xx) : 0.0;
     }
 #pragma unroll
@@ -169,6 +171,7 @@ __global__ void __launch_bounds__(32 * TY)
       cur[k] = above[k];
       above[k] = above2[k];
       halo[k] = halo_n[k];
+      halo_n[k] = halo_nn[k];
       uc[k] = u_n[k];
     }
     // block reduction (fixed order) → one f partial per (tile, zpart planes):
