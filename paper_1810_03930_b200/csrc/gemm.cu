@@ -102,8 +102,7 @@ void plan_gemm(GemmPlan& pl, int device, int size, int amode, int epi, int64_t M
     const int g0 = grid_override > 0 ? grid_override : num_sms(device);
     // long segments: one CTA each (the next CTA's pipeline fill overlaps this
     // one's partial store); short segments: persistent CTAs walk several
-    const char* env = getenv("PCAL_SEG_GRID");
-    const bool one_each = env ? env[0] == 'f' : (int64_t)ki / segs >= 32;
+    const bool one_each = (int64_t)ki / segs >= 32;
     grid = (int)(one_each ? nseg : std::min<int64_t>(nseg, g0));
   } else {
     // Enough tiles for every SM: data-parallel whole tiles (no partials, no
@@ -175,7 +174,6 @@ void plan_gemm(GemmPlan& pl, int device, int size, int amode, int epi, int64_t M
   // long runs of k-iterations per CTA: split the copy stream over 4 producer
   // warps; short tiles with heavy epilogues (X·[W|C]) keep a single producer
   g.nprod = (ki >= 64 && units / std::max(grid, 1) >= 64) ? 4 : 1;
-  if (const char* e = getenv("PCAL_NPROD")) g.nprod = atoi(e) == 4 ? 4 : 1;
   g.segs = segs;
   pl.no_fixup = chunk_partials;
 }
