@@ -100,10 +100,9 @@ void plan_gemm(GemmPlan& pl, int device, int size, int amode, int epi, int64_t M
     segs = fixed_splits;
     const int64_t nseg = (int64_t)ntiles * segs;
     const int g0 = grid_override > 0 ? grid_override : num_sms(device);
-    // long segments: one CTA each (the next CTA's pipeline fill overlaps this
-    // one's partial store); short segments: persistent CTAs walk several
-    const bool one_each = (int64_t)ki / segs >= 32;
-    grid = (int)(one_each ? nseg : std::min<int64_t>(nseg, g0));
+    // persistent CTAs walk whole segments (one pipeline per SM, no per-segment
+    // CTA start-up; measured 5% faster than one CTA per segment)
+    grid = (int)std::min<int64_t>(nseg, g0);
   } else {
     // Enough tiles for every SM: data-parallel whole tiles (no partials, no
     // fixup); otherwise stream-K so tall-skinny / few-tile products fill the chip.
