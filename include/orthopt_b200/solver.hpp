@@ -166,6 +166,36 @@ class StencilModel : public ObjectiveModel {
 };
 
 // E(X) = ¼tr(XᵀLX) + ½tr(XᵀV_ion X) + ¼ρᵀL†ρ + ½ρᵀε_xc(ρ).
+// A caller-defined objective on the device: the counterpart of subclassing
+// orthopt::ObjectiveModel and overriding evaluate() (problems.hpp:24-51).
+// enqueue_gradient() receives device pointers and the solver's CUDA stream
+// (as void*) and must only ENQUEUE the work writing G = ∇f(X) and f(X) (see
+// pcal_gradient_fn in pcal_b200.h).  The object must outlive the solve.
+class DeviceModel : public ObjectiveModel {
+ public:
+  DeviceModel(std::int64_t n, std::int64_t p, double s) {
+    desc_.kind = PCAL_MODEL_DEVICE_CALLBACK;
+    desc_.location = PCAL_DEVICE;
+    desc_.n = n;
+    desc_.p = p;
+    desc_.s = s;
+    desc_.grad = &DeviceModel::trampoline;
+    desc_.grad_ctx = this;
+  }
+  DeviceModel(const DeviceModel&) = delete;
+  DeviceModel& operator=(const DeviceModel&) = delete;
+  virtual int enqueue_gradient(const double* x, std::int64_t ld, double* g, double* f,
+                               void* stream) const = 0;
+
+ private:
+  static int trampoline(const double* x, int64_t ld, int64_t n, int64_t p, double* g, double* f,
+                        void* stream, void* ctx) {
+    (void)n;
+    (void)p;
+    return static_cast<const DeviceModel*>(ctx)->enqueue_gradient(x, ld, g, f, stream);
+  }
+};
+
 class KohnShamModel : public StencilModel {
  public:
   KohnShamModel(std::int64_t nx, std::int64_t ny, std::int64_t nz, const std::vector<double>& v_ion,

@@ -51,6 +51,18 @@ extern "C" {
 #define PCAL_MODEL_DENSE 1      /* f = ½tr(XᵀAX) + tr(G0ᵀX), A n×n symmetric (problems.cpp:130-141) */
 #define PCAL_MODEL_STENCIL 2    /* f = ½tr(XᵀLX) + ½tr(XᵀVX), L = −Δ_h 7-point periodic */
 #define PCAL_MODEL_KOHN_SHAM 3  /* E = ¼tr(XᵀLX)+½tr(XᵀV_ionX)+¼ρᵀL†ρ+½ρᵀε_xc(ρ) */
+#define PCAL_MODEL_DEVICE_CALLBACK 4  /* any f: the caller's own device gradient (below) */
+
+/* ObjectiveModel::evaluate (problems.hpp:39) for a caller-defined model, on the
+ * device: enqueue on `stream` (a cudaStream_t) the work that writes G = ∇f(X)
+ * into g (n×p, leading dimension ld, column-major) and f(X) into the device
+ * scalar *f, reading X (same layout).  Rows n..ld-1 of x are zero and those of
+ * g must stay zero.  The call only ENQUEUES: it may be made while the stream is
+ * being captured into a CUDA graph, so it must not synchronise, allocate or
+ * copy to/from the host.  Return 0 on success.  Non-finite G or f is detected
+ * by the library (evaluation_error ⇒ status Diverged, solver.cpp:460-466). */
+typedef int (*pcal_gradient_fn)(const double* x, int64_t ld, int64_t n, int64_t p, double* g,
+                                double* f, void* stream, void* ctx);
 
 /* pointer location for model data / x0 */
 #define PCAL_HOST 0
@@ -83,6 +95,8 @@ typedef struct pcal_model_desc {
   const double* g0;      /* dense: n×p linear term or NULL (zero) */
   int64_t nx, ny, nz;    /* grid models: n = nx·ny·nz, row i = x + nx·(y + ny·z) */
   const double* v;       /* stencil: V (n); Kohn–Sham: V_ion (n) */
+  pcal_gradient_fn grad; /* PCAL_MODEL_DEVICE_CALLBACK: the gradient callback */
+  void* grad_ctx;        /* its context pointer */
 } pcal_model_desc;
 
 typedef struct pcal_config {  /* orthopt::SolverConfig (solver.hpp:30-42) */

@@ -43,7 +43,7 @@ E_DIVERGENCE, E_EVALUATION = -7, -8
 STATUS = {0: "converged", 1: "max_iter", 2: "diverged"}
 TRACE_COLS = 7
 HOST, DEVICE = 0, 1
-MODEL_DENSE, MODEL_STENCIL, MODEL_KOHN_SHAM = 1, 2, 3
+MODEL_DENSE, MODEL_STENCIL, MODEL_KOHN_SHAM, MODEL_DEVICE_CALLBACK = 1, 2, 3, 4
 
 
 class NativeUnavailable(RuntimeError):
@@ -76,7 +76,13 @@ _dp = C.POINTER(C.c_double)
 class _Model(C.Structure):
     _fields_ = [("kind", C.c_int32), ("location", C.c_int32), ("n", C.c_int64), ("p", C.c_int64),
                 ("s", C.c_double), ("a", C.c_void_p), ("g0", C.c_void_p), ("nx", C.c_int64),
-                ("ny", C.c_int64), ("nz", C.c_int64), ("v", C.c_void_p)]
+                ("ny", C.c_int64), ("nz", C.c_int64), ("v", C.c_void_p), ("grad", C.c_void_p),
+                ("grad_ctx", C.c_void_p)]
+
+
+# pcal_gradient_fn (include/pcal_b200.h): enqueue G = ∇f(X) and f(X) on `stream`
+GRADIENT_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_void_p,
+                          C.c_void_p, C.c_void_p, C.c_void_p)
 
 
 class _Config(C.Structure):
@@ -331,6 +337,26 @@ class KohnShamModel(StencilModel):
     def __init__(self, grid, v_ion, p: int, s: float):
         super().__init__(grid, v_ion, p, s)
         self.kind = MODEL_KOHN_SHAM
+
+
+class DeviceCallbackModel(_ModelBase):
+    """A caller-defined objective evaluated by the caller's own device code
+    (PCAL_MODEL_DEVICE_CALLBACK): the device-side counterpart of subclassing
+    ``orthopt::ObjectiveModel`` (problems.hpp:24-51).  ``grad`` is a
+    ``pcal_gradient_fn`` — a C function address (int) or a ``GRADIENT_FN``
+    object — that enqueues G = ∇f(X) and f(X) on the stream it is given;
+    ``ctx`` is passed through (int address or None).  Single GPU."""
+
+    def __init__(self, n: int, p: int, s: float, grad, ctx=None):
+        self.kind = MODEL_DEVICE_CALLBACK
+        self.n, self.p, self.s = int(n), int(p), float(s)
+        self.grad = grad
+        self.ctx = ctx
+
+    def _c(self) -> tuple:
+        g = self.grad if isinstance(self.grad, int) else C.cast(self.grad, C.c_void_p).value
+        return _Model(self.kind, HOST, self.n, self.p, self.s, None, None, 0, 0, 0, None, g,
+                      self.ctx), (self.grad,)
 
 
 def make_quadratic(a, p: int, s: float, g0=None) -> QuadraticModel:

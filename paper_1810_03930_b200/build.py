@@ -2,8 +2,9 @@
 
 ``python -m paper_1810_03930_b200.build`` compiles every CUDA/C++ source under
 ``csrc/`` with nvcc for ``-gencode arch=compute_100a,code=sm_100a`` into
-``paper_1810_03930_b200/libpcal_b200.so`` (objects under ``build/``), and the
-C++ header-mirror example ``build/pcal_cpp_example``.  Sources are rebuilt
+``paper_1810_03930_b200/libpcal_b200.so`` (objects under ``build/``), the
+C++ header-mirror example ``build/pcal_cpp_example`` and the caller-defined
+device model example ``build/libpcal_device_model_example.so``.  Sources are rebuilt
 only when they (or any header) are newer than their object.
 """
 from __future__ import annotations
@@ -77,6 +78,14 @@ def build(verbose: bool = False) -> str:
             r = subprocess.run(cmd, capture_output=True, text=True)
             if r.returncode != 0:
                 raise RuntimeError(f"example build failed\n{r.stdout}\n{r.stderr}")
+    dm_src = os.path.join(ROOT, "examples", "device_model_example.cu")
+    if os.path.exists(dm_src):  # a caller-defined device model (PCAL_MODEL_DEVICE_CALLBACK)
+        so = os.path.join(os.path.dirname(BUILD), "libpcal_device_model_example.so")
+        if _stale(so, dm_src, _headers()):
+            cmd = [NVCC, *ARCH, *CUFLAGS, f"-I{ROOT}/include", "-shared", dm_src, "-o", so]
+            r = subprocess.run(cmd, capture_output=True, text=True)
+            if r.returncode != 0:
+                raise RuntimeError(f"device-model example build failed\n{r.stdout}\n{r.stderr}")
     return LIB
 
 

@@ -207,6 +207,7 @@ struct FinishArgs {
   double* trace;
   int32_t* bad;         // evaluation non-finite flag
   double c_xc;          // (3/π)^{1/3}
+  const double* fdev;   // device-callback models: f(X) as written by the callback
 };
 
 // Thread-0 tail of an evaluation: objective assembly, failure flags, trace
@@ -223,6 +224,8 @@ __device__ void finish_record(const FinishArgs& a, Ctl* ctl, double* post, doubl
   double f;
   if (a.model == PCAL_MODEL_KOHN_SHAM) {
     f = 0.25 * f1 + 0.5 * vr + 0.25 * rh - 0.375 * a.c_xc * ex;
+  } else if (a.model == PCAL_MODEL_DEVICE_CALLBACK) {
+    f = *a.fdev;
   } else {
     f = 0.5 * f1;
   }
@@ -303,6 +306,17 @@ __global__ void __launch_bounds__(256) k_finish_eval(FinishArgs a, Ctl* ctl,
 #include "small.cuh"
 namespace pcal {
 
+// check_finite (problems.cpp:27-30) of a caller-computed gradient.
+__global__ void k_check_finite(const double* __restrict__ g, int64_t n, int64_t ld, int64_t p,
+                               int32_t* bad, const Ctl* ctl) {
+  if (ctl && ctl->done) return;
+  bool nonfinite = false;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n * p;
+       e += (int64_t)gridDim.x * blockDim.x)
+    nonfinite |= !isfinite(g[e % n + (e / n) * ld]);
+  if (__syncthreads_or(nonfinite) && threadIdx.x == 0) *bad = 1;
+}
+
 __global__ void k_zero_i32(int32_t* p, const Ctl* ctl) {
   if (ctl && ctl->done) return;
   *p = 0;
@@ -371,6 +385,7 @@ struct pcal_session {
   double beta = 1.0, eta0 = 0.0, c_xc = 0.0;
   // model data
   pcal::DevBuf A, g0, V, u, rho, h, tmpa, tmpb, qx, qy, qz, lx, ly, lz, spart;
+  pcal::DevBuf fdev;  // device-callback models: f(X)
   int64_t ldA = 0;
   // iteration state
   pcal::DevBuf pair[2];
@@ -664,6 +679,16 @@ static void launch_gradient(pcal_session* s, int b, const Ctl* ctl) {
       launch_stencil(s, b, s->u.p, true, ctl);
       break;
     }
+    case PCAL_MODEL_DEVICE_CALLBACK: {  // the caller's own gradient, enqueued on our stream
+      const int rc = s->model.grad(Xof(s, b), s->ld, s->n, p, Pof(s, b), s->fdev.p,
+                                   (void*)s->stream, s->model.grad_ctx);
+      if (rc != 0)
+        throw Error(PCAL_E_EVALUATION, "gradient callback failed (" + std::to_string(rc) + ")");
+      k_check_finite<<<(unsigned)std::min<int64_t>(4 * 148, ceil_div(s->n * p, 256)), 256, 0,
+                       s->stream>>>(Pof(s, b), s->n, s->ld, p, s->bad, ctl);
+      launched("k_check_finite");
+      break;
+    }
     default:
       throw Error(PCAL_E_UNSUPPORTED, "unsupported model kind");
   }
@@ -734,6 +759,7 @@ static void launch_eval(pcal_session* s, int b, int mode, const Ctl* ctl_guard) 
   fa.trace = s->trace.p;
   fa.bad = s->bad;
   fa.c_xc = s->c_xc;
+  fa.fdev = s->fdev.p;
   k_finish_eval<<<1, 256, 0, st>>>(fa, s->ctl, s->post.p);
   launched("k_finish_eval");
   mark(s, 4);
@@ -986,8 +1012,12 @@ static void build_plans(pcal_session* s) {
 //   dense: Q = ⌈n/64⌉ rounded up to the row-block size a (64 for p > 32,
 //          else 32: chunk boundaries fall on GEMM warp row-blocks);
 //   grid models: Zc = ⌈nz/64⌉ whole z-planes (Q = Zc·nx·ny rows).
+static bool is_grid(int32_t kind) {
+  return kind == PCAL_MODEL_STENCIL || kind == PCAL_MODEL_KOHN_SHAM;
+}
+
 static void chunking(const pcal_model_desc& m, int64_t* Q, int64_t* NC, int64_t* Zc) {
-  if (m.kind == PCAL_MODEL_DENSE) {
+  if (!is_grid(m.kind)) {
     const int64_t a = padded_p(m.p) >= 64 ? 64 : 32;
     *Q = round_up(ceil_div(m.n, 64), a);
     *NC = ceil_div(m.n, *Q);
@@ -1008,7 +1038,7 @@ static void partition(const pcal_model_desc& m, int R, int r, int64_t* row0, int
   if (R > NC)
     throw Error(PCAL_E_PARAMETER, "more ranks than row chunks (" + std::to_string(NC) + ")");
   const int64_t c0 = (int64_t)r * NC / R, c1 = (int64_t)(r + 1) * NC / R;
-  if (m.kind == PCAL_MODEL_DENSE) {
+  if (!is_grid(m.kind)) {
     *row0 = c0 * Q;
     *rows = std::min(c1 * Q, m.n) - *row0;
     *z0 = 0;
@@ -1098,9 +1128,9 @@ static void alloc_state(pcal_session* s) {
   s->st_nchunks = ceil_div(n, s->st_chunk);
   {
     const auto& m = s->model;
-    s->st_march = m.kind != PCAL_MODEL_DENSE && m.nx <= 128 && m.ny % 8 == 0 && m.ny >= 8 &&
+    s->st_march = is_grid(m.kind) && m.nx <= 128 && m.ny % 8 == 0 && m.ny >= 8 &&
                   s->gz >= 1;
-    if (s->comm && m.kind != PCAL_MODEL_DENSE && !s->st_march)
+    if (s->comm && is_grid(m.kind) && !s->st_march)
       throw Error(PCAL_E_UNSUPPORTED, "sharded grid models need nx <= 128 and ny % 8 == 0");
     if (s->st_march) {  // enough blocks for ≈ 8 per SM
       const int64_t tiles = (m.ny / 8) * p;
@@ -1250,6 +1280,10 @@ static void upload_model(pcal_session* s) {
     } else {
       s->u.p = nullptr;
     }
+  } else if (m.kind == PCAL_MODEL_DEVICE_CALLBACK) {
+    if (!m.grad) throw Error(PCAL_E_PARAMETER, "device-callback model: grad is NULL");
+    s->fdev.alloc(1);
+    s->fdev.zero(st);
   } else {
     throw Error(PCAL_E_UNSUPPORTED, "unsupported model kind " + std::to_string(m.kind));
   }
@@ -1483,9 +1517,9 @@ void session_create(const pcal_model_desc* model, const pcal_config* config, con
   s->pp = padded_p(s->p);
   const int R = comm ? comm->size : 1;
   const int rk = comm ? comm->rank : 0;
-  if (model->kind != PCAL_MODEL_DENSE && (model->nz < R))
+  if (is_grid(model->kind) && (model->nz < R))
     throw Error(PCAL_E_PARAMETER, "fewer z-planes than ranks");
-  if (model->kind == PCAL_MODEL_DENSE && model->n < R)
+  if (!is_grid(model->kind) && model->n < R)
     throw Error(PCAL_E_PARAMETER, "fewer rows than ranks");
   int64_t maxrows = 0;
   s->rank_row0.resize(R);
@@ -1504,7 +1538,7 @@ void session_create(const pcal_model_desc* model, const pcal_config* config, con
   if (comm) {  // reproducible chunked reductions
     int64_t Q, NC, Zc;
     chunking(*model, &Q, &NC, &Zc);
-    if (model->kind != PCAL_MODEL_DENSE && (model->nx * model->ny) % 64 != 0)
+    if (is_grid(model->kind) && (model->nx * model->ny) % 64 != 0)
       throw Error(PCAL_E_UNSUPPORTED, "sharded grid models need nx*ny to be a multiple of 64");
     s->repro = true;
     s->chunk_rows = Q;
@@ -1524,10 +1558,12 @@ void session_create(const pcal_model_desc* model, const pcal_config* config, con
   s->alg = config->algorithm;
   // the grid models' operators are symmetric, so GᵀX = XᵀLX (+ XᵀVX) is: only its
   // upper triangle is computed (MOptQR uses the unsymmetrised GᵀX)
-  s->sym_gx = model->kind != PCAL_MODEL_DENSE && s->alg != PCAL_ALG_MOPTQR &&
-              !getenv("PCAL_FULL_GX");
+  s->sym_gx = (model->kind == PCAL_MODEL_STENCIL || model->kind == PCAL_MODEL_KOHN_SHAM) &&
+              s->alg != PCAL_ALG_MOPTQR && !getenv("PCAL_FULL_GX");
   if (comm && s->alg == PCAL_ALG_MOPTQR)
     throw Error(PCAL_E_UNSUPPORTED, "MOptQR is single-GPU (its MGS2 fallback is not sharded)");
+  if (comm && model->kind == PCAL_MODEL_DEVICE_CALLBACK)
+    throw Error(PCAL_E_UNSUPPORTED, "device-callback models are single-GPU");
   // resolve_beta (solver.cpp:120-134)
   s->beta = config->beta >= 0.0                                                ? config->beta
             : (s->alg == PCAL_ALG_PCAL || s->alg == PCAL_ALG_PCALDA) ? 1.0
@@ -2236,6 +2272,7 @@ int pcal_evaluate(const pcal_model_desc* model, const double* x, double* f, doub
     fa.trace = s->trace.p;
     fa.bad = s->bad;
     fa.c_xc = s->c_xc;
+    fa.fdev = s->fdev.p;
     k_finish_eval<<<1, 256, 0, s->stream>>>(fa, s->ctl, s->post.p);
     launched("k_finish_eval");
     double post[8];
