@@ -110,6 +110,85 @@ __global__ void k_trinv_t(const double* __restrict__ l, int64_t ldl, int64_t p,
   }
 }
 
+// Cholesky + T = (L⁻¹)ᵀ in ONE block for p ≤ kCholSmemP, with L resident in
+// shared memory: left-looking Cholesky (the same recurrence and pivot floor as
+// k_cholesky; d_j and the column dots are warp reductions), then forward
+// substitution for the columns of L⁻¹, one warp per column (lanes hold the
+// solution entries k ≡ lane mod 32).  Replaces k_cholesky + k_trinv_t, whose
+// global-memory recurrences are latency-bound (≈0.3 ms each at p = 128).
+constexpr int kCholSmemP = 128;
+__global__ void __launch_bounds__(1024) k_chol_trinv_small(const double* __restrict__ b,
+                                                           int64_t ldb, int p,
+                                                           const double* fro2_first,
+                                                           double* __restrict__ t, int64_t ldt,
+                                                           int32_t* status,
+                                                           const int32_t* prev_ok,
+                                                           const Ctl* ctl) {
+  extern __shared__ double sL[];  // p×p column-major: sL[i + k·p] = L(i, k), i ≥ k
+  __shared__ double s_ljj;
+  __shared__ int s_ok;
+  if (ctl && ctl->done) return;
+  if (prev_ok && !*prev_ok) {  // first CholeskyQR pass already failed
+    if (threadIdx.x == 0) *status = 0;
+    return;
+  }
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
+  const double floor_ = 1e-14 * sqrt(*fro2_first);
+  for (int e = tid; e < p * p; e += blockDim.x) {  // lower triangle of B (from its upper one)
+    const int i = e % p, j = e / p;
+    sL[e] = i >= j ? b[j + (int64_t)i * ldb] : 0.0;
+  }
+  if (tid == 0) s_ok = 1;
+  __syncthreads();
+  for (int j = 0; j < p; ++j) {
+    if (warp == 0) {
+      double d = 0.0;
+      for (int k = lane; k < j; k += 32) d += sL[j + k * p] * sL[j + k * p];
+      d = warp_sum(d);
+      if (lane == 0) {
+        d = sL[j + j * p] - d;
+        if (!(d > floor_)) s_ok = 0;
+        s_ljj = sqrt(d);
+        sL[j + j * p] = s_ljj;
+      }
+    }
+    __syncthreads();
+    if (!s_ok) break;
+    const double ljj = s_ljj;
+    for (int i = j + 1 + warp; i < p; i += nw) {
+      double acc = 0.0;
+      for (int k = lane; k < j; k += 32) acc += sL[i + k * p] * sL[j + k * p];
+      acc = warp_sum(acc);
+      if (lane == 0) sL[i + j * p] = (sL[i + j * p] - acc) / ljj;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) *status = s_ok;
+  if (!s_ok) return;
+  // columns c of L⁻¹: x_i = (δ_ic − Σ_{c≤k<i} L(i,k)·x_k) / L(i,i), T(c, i) = x_i
+  for (int c = warp; c < p; c += nw) {
+    double x[kCholSmemP / 32];
+#pragma unroll
+    for (int q = 0; q < kCholSmemP / 32; ++q) x[q] = 0.0;
+    for (int i = lane; i < c; i += 32) t[c + (int64_t)i * ldt] = 0.0;
+    for (int i = c; i < p; ++i) {
+      double acc = 0.0;
+#pragma unroll
+      for (int q = 0; q < kCholSmemP / 32; ++q) {
+        const int k = lane + 32 * q;
+        if (k >= c && k < i) acc += sL[i + k * p] * x[q];
+      }
+      acc = warp_sum(acc);
+      const double xi = ((i == c) ? 1.0 : 0.0) - acc;
+      const double v = xi / sL[i + i * p];
+#pragma unroll
+      for (int q = 0; q < kCholSmemP / 32; ++q)
+        if (lane + 32 * q == i) x[q] = v;
+      if (lane == (i & 31)) t[c + (int64_t)i * ldt] = v;
+    }
+  }
+}
+
 // mgs2 (kernels.cpp:212-246) fallback: one block, in place on q (= copy of X).
 __global__ void k_mgs2(double* __restrict__ q, int64_t n, int64_t ld, int64_t p,
                        const double* fro2_first, int32_t* status) {
@@ -779,6 +858,29 @@ static void launch_eval(pcal_session* s, int b, int mode, const Ctl* ctl_guard) 
   }
 }
 
+// L = chol(B) and T = (L⁻¹)ᵀ with the pivot floor of the first Gram; status = 0 on failure.
+static void launch_chol_trinv(cudaStream_t st, const double* b, int64_t ldb, int64_t p,
+                              const double* f2, double* l, int64_t ldl, double* t, int64_t ldt,
+                              int32_t* status, const int32_t* prev_ok, const Ctl* ctl) {
+  if (p <= kCholSmemP) {
+    const size_t smem = sizeof(double) * p * p;
+    static bool attr = false;
+    if (!attr) {
+      PCAL_CUDA(cudaFuncSetAttribute(k_chol_trinv_small,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(sizeof(double) * kCholSmemP * kCholSmemP)));
+      attr = true;
+    }
+    k_chol_trinv_small<<<1, 1024, smem, st>>>(b, ldb, (int)p, f2, t, ldt, status, prev_ok, ctl);
+    launched("k_chol_trinv_small");
+    return;
+  }
+  k_cholesky<<<1, 1024, 0, st>>>(b, ldb, p, f2, l, ldl, status, prev_ok, ctl);
+  launched("k_cholesky");
+  k_trinv_t<<<(unsigned)ceil_div(p, 128), 128, 0, st>>>(l, ldl, p, t, ldt, status);
+  launched("k_trinv_t");
+}
+
 // One PCAL iteration from X_k in pair b to X_{k+1} in pair 1−b (solver.cpp:385-438).
 // MOptQR retraction inside the iteration graph (solver.cpp:415-418): Z in
 // X(nb) → Q = orthonormalize(Z) in X(nb) by CholeskyQR2 with status-gated
@@ -792,18 +894,12 @@ static void launch_retraction(pcal_session* s, int nb) {
   launch_gemm(s->rq_gram_z[nb], st);
   k_sym_fro2<<<1, 1024, 0, st>>>(s->orth_b.p, pp, p, s->orth_f2.p);
   launched("k_sym_fro2");
-  k_cholesky<<<1, 1024, 0, st>>>(s->orth_b.p, pp, p, s->orth_f2.p, s->orth_l.p, pp, ok1, nullptr,
-                                 s->ctl);
-  launched("k_cholesky");
-  k_trinv_t<<<(unsigned)ceil_div(p, 128), 128, 0, st>>>(s->orth_l.p, pp, p, s->orth_t.p, pp, ok1);
-  launched("k_trinv_t");
+  launch_chol_trinv(st, s->orth_b.p, pp, p, s->orth_f2.p, s->orth_l.p, pp, s->orth_t.p, pp, ok1,
+                    nullptr, s->ctl);
   launch_gemm(s->rq_mul1[nb], st);
   launch_gemm(s->rq_gram_q[nb], st);
-  k_cholesky<<<1, 1024, 0, st>>>(s->orth_b.p, pp, p, s->orth_f2.p, s->orth_l.p, pp, ok2, ok1,
-                                 s->ctl);
-  launched("k_cholesky");
-  k_trinv_t<<<(unsigned)ceil_div(p, 128), 128, 0, st>>>(s->orth_l.p, pp, p, s->orth_t.p, pp, ok2);
-  launched("k_trinv_t");
+  launch_chol_trinv(st, s->orth_b.p, pp, p, s->orth_f2.p, s->orth_l.p, pp, s->orth_t.p, pp, ok2,
+                    ok1, s->ctl);
   launch_gemm(s->rq_mul2[nb], st);
   k_mgs2_gated<<<1, 1024, 0, st>>>(Xof(s, nb), s->n, s->ld, p, s->orth_f2.p, ok1, ok2,
                                    s->orth_status + 2, s->ctl);
@@ -1697,24 +1793,16 @@ bool orthonormalize_dev(pcal_session* s, const double* x, double* q, double* scr
   gram_of(x);
   k_sym_fro2<<<1, 1024, 0, st>>>(s->orth_b.p, pp, p, s->orth_f2.p);
   launched("k_sym_fro2");
-  k_cholesky<<<1, 1024, 0, st>>>(s->orth_b.p, pp, p, s->orth_f2.p, s->orth_l.p, pp,
-                                 s->orth_status);
-  launched("k_cholesky");
-  k_trinv_t<<<(unsigned)ceil_div(p, 128), 128, 0, st>>>(s->orth_l.p, pp, p, s->orth_t.p, pp,
-                                                        s->orth_status);
-  launched("k_trinv_t");
+  launch_chol_trinv(st, s->orth_b.p, pp, p, s->orth_f2.p, s->orth_l.p, pp, s->orth_t.p, pp,
+                    s->orth_status, nullptr, nullptr);
   PCAL_CUDA(cudaMemcpyAsync(&ok, s->orth_status, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   PCAL_CUDA(cudaStreamSynchronize(st));
   bool chol_ok = ok != 0;
   if (chol_ok) {
     mul_t(x, scratch);  // Q1 = X·L1⁻ᵀ
     gram_of(scratch);
-    k_cholesky<<<1, 1024, 0, st>>>(s->orth_b.p, pp, p, s->orth_f2.p, s->orth_l.p, pp,
-                                   s->orth_status);
-    launched("k_cholesky");
-    k_trinv_t<<<(unsigned)ceil_div(p, 128), 128, 0, st>>>(s->orth_l.p, pp, p, s->orth_t.p, pp,
-                                                          s->orth_status);
-    launched("k_trinv_t");
+    launch_chol_trinv(st, s->orth_b.p, pp, p, s->orth_f2.p, s->orth_l.p, pp, s->orth_t.p, pp,
+                      s->orth_status, nullptr, nullptr);
     PCAL_CUDA(cudaMemcpyAsync(&ok, s->orth_status, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     PCAL_CUDA(cudaStreamSynchronize(st));
     chol_ok = ok != 0;
@@ -1787,7 +1875,7 @@ void session_finish(pcal_session* s, pcal_report* r) {
     r->final_pre[3] = c.feas;
     r->has_x = 1;
     if (r->stop_x) copy_out(s, Xof(s, b), r->stop_x);
-    if (r->final_x) copy_out(s, Xof(s, b), r->final_x);
+    bool final_is_q = false;  // final_x = Q after a successful final orthonormalization
     if (s->cfg.final_orth) {  // solver.cpp:445-459
       auto t0 = std::chrono::steady_clock::now();
       const int nb = 1 - b;
@@ -1814,9 +1902,11 @@ void session_finish(pcal_session* s, pcal_report* r) {
           for (int i = 0; i < 4; ++i) r->final_post[i] = post[i];
           r->has_post = 1;
           if (r->final_x) copy_out(s, Xof(s, nb), r->final_x);
+          final_is_q = true;
         }
       }
     }
+    if (r->final_x && !final_is_q) copy_out(s, Xof(s, b), r->final_x);
   }
   PCAL_CUDA(cudaStreamSynchronize(s->stream));
   if (status == PCAL_STATUS_DIVERGED && tl > 0) {  // solver.cpp:467-471
