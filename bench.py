@@ -144,6 +144,16 @@ def pinned_f64(n_rows: int, n_cols: int):
     return t, arr
 
 
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_reference_rate(inst, x0, budget_s: float = 15.0, threads: int = None, min_iters=1,
                        max_iters=None):
     """Time the reference CPU solve() on a bounded sample; returns (iters/s, info)."""
@@ -162,7 +172,7 @@ def cpu_reference_rate(inst, x0, budget_s: float = 15.0, threads: int = None, mi
     what = "reference solve() (oracle/_ref)" if R.kind == "reference" else "C restatement (oracle)"
     if inst.kind != "dense":
         what += " driving the restated grid operator (no reference operator exists)"
-    info = {"kind": R.kind, "cores": threads, "iters": iters,
+    info = {"kind": R.kind, "cores": threads, "iters": iters, "cpu_model": cpu_model(),
             "sample": f"{what}: {iters} PCAL iteration(s) of config {inst.cfg} "
                       f"(n={inst.n}, p={inst.p}), timed by its trace clock, setup excluded"}
     return 1.0 / per, info
@@ -198,7 +208,8 @@ def run_reference_arm(args):
             "config": {"workload": f"config {inst.cfg}", "n": inst.n, "p": inst.p,
                        "kind": inst.kind},
             "cpu_baseline": {"value": rate, "unit": "iterations/s", "cores": info["cores"],
-                             "kind": info["kind"], "sample": info["sample"]},
+                             "kind": info["kind"], "sample": info["sample"],
+                             "cpu_model": info["cpu_model"]},
             "e2e": {"value": rate, "unit": "iterations/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -360,7 +371,7 @@ def main():
         try:
             rate, info = cpu_reference_rate(inst, np.asfortranarray(x0), budget_s=15.0)
             cpu = {"value": rate, "unit": "iterations/s", "cores": info["cores"],
-                   "kind": info["kind"], "sample": info["sample"]}
+                   "kind": info["kind"], "sample": info["sample"], "cpu_model": info["cpu_model"]}
         except Exception as e:  # reported, never silently substituted
             cpu = {"value": None, "unit": "iterations/s", "cores": 0, "kind": "unavailable",
                    "sample": f"failed: {e}"}
