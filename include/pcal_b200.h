@@ -252,6 +252,11 @@ double pcal_flops_estimate(int64_t n, int64_t p);
  * `threads` host threads (checkpointed generator states). */
 int pcal_random_normal(int64_t rows, int64_t cols, uint64_t seed, double* out, int32_t threads);
 int pcal_random_uniform(int64_t count, uint64_t seed, double* out);
+/* spectral_norm_estimate(A, seed) (kernels.cpp:267-293) on the host, bitwise equal to
+ * the reference's (problem setup of small instances; the device version is
+ * pcal_spectral_norm_estimate). */
+int pcal_spectral_norm_estimate_host(const double* a, int64_t n, uint64_t seed, int32_t threads,
+                                     double* out);
 /* sym_part(random_normal(n, n, Rng(seed))) — the dense operator of configs 1–2
  * (problems.cpp:45-48). */
 int pcal_gen_dense_operator(int64_t n, uint64_t seed, double* a, int32_t threads);

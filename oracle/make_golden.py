@@ -179,6 +179,30 @@ def init_cases(R: Reference) -> None:
     print("wrote reference_init.npz")
 
 
+HARNESS_CASES = {  # name: (kind, n, p, alpha, kappa, theta, zeta, xi, block_tridiag, seed, init, sigma, iters)
+    "p1_alpha0": (1, 80, 5, 0.0, 1.0, 1.01, 1.01, 1.0, 0, 11, 0, 0.5, 60),
+    "p1_block": (1, 60, 4, 0.0, 1.0, 1.01, 1.01, 1.0, 1, 12, 0, 0.5, 3000),
+    "p2": (2, 90, 6, 0.0, 2.0, 1.05, 1.02, 0.7, 0, 13, 0, 0.5, 3000),
+    "p3_a2i": (3, 70, 4, 0.0, 0.0, 1.08, 1.0, 0.5, 0, 14, 1, 0.6, 3000),
+}
+
+
+def harness_cases(R: Reference) -> None:
+    """run_single (harness.cpp:62-73) JSON reports for the dense problem kinds."""
+    import ctypes as C
+    L = R.lib
+    L.ref_run_single_json.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_double, C.c_double,
+                                      C.c_double, C.c_double, C.c_double, C.c_int, C.c_uint64,
+                                      C.c_int, C.c_double, C.c_int64, C.c_char_p, C.c_int64]
+    for name, (kind, n, p, alpha, kappa, theta, zeta, xi, bt, seed, init, sigma, iters) in \
+            HARNESS_CASES.items():
+        buf = C.create_string_buffer(1 << 22)
+        assert L.ref_run_single_json(kind, n, p, alpha, kappa, theta, zeta, xi, bt, seed, init,
+                                     sigma, iters, buf, len(buf)) == 0, name
+        open(os.path.join(OUT, f"ref_run_single_{name}.json"), "w").write(buf.value.decode() + "\n")
+    print("wrote run_single reports")
+
+
 def grid_cases(R: Reference) -> None:
     """Grid models (no reference implementation): the reference solve() driving
     the restated operator — pins the PCAL loop around it, not the operator."""
@@ -263,6 +287,7 @@ if __name__ == "__main__":
     algorithm_cases(R)
     report_io_cases(R)
     init_cases(R)
+    harness_cases(R)
     if "--cfg2" in sys.argv:
         cfg2(R)
     if "--grids" in sys.argv:

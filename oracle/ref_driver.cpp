@@ -391,6 +391,36 @@ int ref_run_single_text(std::int64_t n, std::int64_t p, std::uint64_t seed, std:
   });
 }
 
+// run_single(ProblemSpec, SolverConfig{max_iter}, InitialPointSpec) as the
+// reference's JSON report (elapsed times zeroed); kind 1..6 = P1..P6 names.
+int ref_run_single_json(int kind, std::int64_t n, std::int64_t p, double alpha, double kappa,
+                        double theta, double zeta, double xi, int block_tridiag,
+                        std::uint64_t seed, int init_mode, double sigma, std::int64_t max_iter,
+                        char* json_buf, std::int64_t json_cap) {
+  return guarded([&] {
+    ProblemSpec spec;
+    spec.kind = kind == 1 ? ProblemKind::P1 : kind == 2 ? ProblemKind::P2
+                : kind == 3 ? ProblemKind::P3 : kind == 4 ? ProblemKind::P4 : ProblemKind::P6;
+    spec.n = n;
+    spec.p = p;
+    spec.alpha = alpha;
+    spec.kappa = kappa;
+    spec.theta = theta;
+    spec.zeta = zeta;
+    spec.xi = xi;
+    spec.mode = block_tridiag ? OperatorMode::BlockTridiag : OperatorMode::RandomSym;
+    spec.seed = seed;
+    SolverConfig cfg;
+    cfg.max_iter = max_iter;
+    RunReport rep = run_single(spec, cfg, {static_cast<InitMode>(init_mode), sigma, 0});
+    for (auto& s : rep.trace) s.elapsed = 0.0;
+    const std::string js = to_json(rep, false);
+    if ((std::int64_t)js.size() + 1 > json_cap) throw io_error("buffer too small");
+    std::memcpy(json_buf, js.c_str(), js.size() + 1);
+    return 0;
+  });
+}
+
 int ref_save_quadratic(const double* a, const double* g0, std::int64_t n, std::int64_t p, double s,
                        const char* path) {
   return guarded([&] {

@@ -150,6 +150,7 @@ def lib() -> C.CDLL:
     L.pcal_flops_estimate.restype = dbl
     L.pcal_random_normal.argtypes = [i64, i64, u64, vp, i32]
     L.pcal_random_uniform.argtypes = [i64, u64, vp]
+    L.pcal_spectral_norm_estimate_host.argtypes = [vp, i64, u64, i32, C.POINTER(dbl)]
     L.pcal_gen_dense_operator.argtypes = [i64, u64, vp, i32]
     L.pcal_initial_point_qr.argtypes = [i64, i64, u64, vp, i32]
     L.pcal_initial_point.argtypes = [i64, i64, i32, dbl, u64, vp, i32]
@@ -589,6 +590,14 @@ def random_normal(rows: int, cols: int, seed: int, threads: int = 8) -> np.ndarr
     out = np.empty((rows, cols), order="F")
     _check(lib().pcal_random_normal(rows, cols, seed, _ptr(out), threads))
     return out
+
+
+def spectral_norm_estimate_host(a, seed: int, threads: int = 8) -> float:
+    """spectral_norm_estimate (kernels.cpp:267-293) on the host, bitwise the reference's."""
+    a = _f64(a)
+    s = C.c_double()
+    _check(lib().pcal_spectral_norm_estimate_host(_ptr(a), a.shape[0], seed, threads, C.byref(s)))
+    return s.value
 
 
 def random_uniform(count: int, seed: int) -> np.ndarray:

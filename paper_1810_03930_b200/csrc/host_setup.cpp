@@ -5,6 +5,7 @@
 // part of the reference's data contract (same seed ⇒ same instance), so the
 // draws here are bitwise identical to the reference; the Box–Muller work is
 // spread over threads from checkpointed generator states.
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -167,6 +168,63 @@ int pcal_gen_dense_operator(int64_t n, uint64_t seed, double* a, int32_t threads
         }
     });
   for (auto& th : pool) th.join();
+  return PCAL_OK;
+}
+
+// spectral_norm_estimate (kernels.cpp:267-293) on the host, bitwise: power
+// iteration on A² from a Box–Muller start vector; the column-axpy products of
+// matmul (kernels.cpp:105-122) are split over row blocks, which keeps every
+// element's k-order; norms and the Frobenius bound are sequential sums.
+int pcal_spectral_norm_estimate_host(const double* a, int64_t n, uint64_t seed, int32_t threads,
+                                     double* out) {
+  if (!a || !out || n < 1) return PCAL_E_PARAMETER;
+  auto seq_dot = [](const double* x, const double* y, int64_t m) {
+    double s = 0.0;
+    for (int64_t i = 0; i < m; ++i) s += x[i] * y[i];
+    return s;
+  };
+  const double fro = std::sqrt(seq_dot(a, a, n * n));
+  if (fro == 0.0) {
+    *out = 0.0;
+    return PCAL_OK;
+  }
+  const int nt = (int)std::max<int64_t>(1, std::min<int64_t>(threads > 0 ? threads : 1, n / 64 + 1));
+  auto matvec = [&](const double* v, double* w) {  // w = A·v, column axpy order
+    std::vector<std::thread> pool;
+    const int64_t blk = (n + nt - 1) / nt;
+    for (int t = 0; t < nt; ++t)
+      pool.emplace_back([=] {
+        const int64_t i0 = t * blk, i1 = std::min(n, i0 + blk);
+        for (int64_t i = i0; i < i1; ++i) w[i] = 0.0;
+        for (int64_t k = 0; k < n; ++k) {
+          const double s = v[k];
+          const double* ak = a + k * n;
+          for (int64_t i = i0; i < i1; ++i) w[i] += s * ak[i];
+        }
+      });
+    for (auto& th : pool) th.join();
+  };
+  std::vector<double> v((size_t)n), w((size_t)n), t((size_t)n);
+  pcal::host_random_normal(n, seed, v.data(), 1);
+  {
+    const double nv = std::sqrt(seq_dot(v.data(), v.data(), n));
+    if (nv == 0.0) v[0] = 1.0;
+    else
+      for (auto& e : v) e /= nv;
+  }
+  double prev = -1.0, est = 0.0;
+  for (int it = 0; it < 500; ++it) {
+    matvec(v.data(), w.data());
+    est = std::sqrt(seq_dot(w.data(), w.data(), n));
+    matvec(w.data(), t.data());
+    const double ntn = std::sqrt(seq_dot(t.data(), t.data(), n));
+    if (ntn == 0.0) break;
+    for (auto& e : t) e /= ntn;
+    std::swap(v, t);
+    if (prev >= 0.0 && std::abs(est - prev) <= 1e-6 * std::max(est, 1e-300)) break;
+    prev = est;
+  }
+  *out = std::min(est, fro);
   return PCAL_OK;
 }
 

@@ -6,6 +6,7 @@ import os
 from types import SimpleNamespace
 
 import numpy as np
+import pytest
 
 from paper_1810_03930_b200 import report_io as R
 
@@ -58,3 +59,35 @@ def test_container_round_trip_byte_identical(pcal):
     out = io.BytesIO()
     R.save_problem(model, out, **{k: params[k] for k in ("kappa", "theta", "zeta", "xi")})
     assert out.getvalue() == open(path, "rb").read()
+
+
+def test_harness_problem_spec_checks_are_host_side():
+    """make_problem's parameter checks (problems.cpp gen_problem*, harness.cpp:31-46)
+    and the kinds without a device model fail before any device work."""
+    from paper_1810_03930_b200 import harness as H
+    from paper_1810_03930_b200.report_io import UnsupportedModel
+    with pytest.raises(pcal_errors().ParameterError):
+        H.make_problem(H.ProblemSpec(kind="p1", n=10, p=6, alpha=0.0))      # 2p > n
+    with pytest.raises(UnsupportedModel):
+        H.make_problem(H.ProblemSpec(kind="p1", n=40, p=4, alpha=1.0))      # nonlinear density
+    with pytest.raises(UnsupportedModel):
+        H.make_problem(H.ProblemSpec(kind="p4", n=40, p=4))
+    with pytest.raises(pcal_errors().ParameterError):
+        H.make_problem(H.ProblemSpec(kind="p1", n=42, p=4, alpha=0.0, mode="block-tridiag"))
+    with pytest.raises(pcal_errors().ParameterError):
+        H.make_problem(H.ProblemSpec(kind="p2", n=40, p=4, theta=0.5))
+
+
+def test_host_spectral_norm_is_the_reference_one():
+    """spectral_norm_estimate (kernels.cpp:267-293): the host version is bitwise the
+    reference's (golden value of the reference's own run, and config 1's s)."""
+    import paper_1810_03930_b200 as P
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "reference_small.npz"))
+    assert P.spectral_norm_estimate_host(g["k_spec_a"], 11) == float(g["k_spec_s"])
+    assert P.spectral_norm_estimate_host(P.gen_dense_operator(1000, 1), 1 ^ 0x73706563) == \
+        float(g["cfg1_s"])
+
+
+def pcal_errors():
+    import paper_1810_03930_b200 as P
+    return P
