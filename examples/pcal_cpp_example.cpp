@@ -31,6 +31,16 @@ int main(int argc, char** argv) {
     if (rep.status != RunStatus::Converged || !rep.final_post_orth ||
         rep.final_post_orth->feas > 1e-12)
       return 1;
+    // the P6 density model on the same operator (problems.cpp:276-285)
+    {
+      DensityModel p6(a, p, 2.0 * std::cbrt(3.0 / 3.14159265358979323846), ProblemKind::P6, s);
+      const RunReport r6 = solve(p6, SolverConfig{}, x0);
+      std::printf("p6: status=%d iterations=%lld f_post=%.12f feas_post=%.3e\n",
+                  static_cast<int>(r6.status), static_cast<long long>(r6.iterations),
+                  r6.final_post_orth ? r6.final_post_orth->fval : NAN,
+                  r6.final_post_orth ? r6.final_post_orth->feas : NAN);
+      if (!r6.final_post_orth || r6.final_post_orth->feas > 1e-12) return 4;
+    }
     // parameter errors are thrown before iterating (solver.cpp:106-118)
     cfg.tol_rel_kkt = 0.0;
     try {

@@ -36,6 +36,9 @@ struct rank_error : std::runtime_error {
 struct device_error : std::runtime_error {  // CUDA failure / no B200: no CPU fallback
   using std::runtime_error::runtime_error;
 };
+struct generation_error : std::runtime_error {  // errors.hpp:27-31
+  using std::runtime_error::runtime_error;
+};
 
 inline void check(int rc) {
   if (rc == PCAL_OK) return;
@@ -165,7 +168,57 @@ class StencilModel : public ObjectiveModel {
   }
 };
 
-// E(X) = ¼tr(XᵀLX) + ½tr(XᵀV_ion X) + ¼ρᵀL†ρ + ½ρᵀε_xc(ρ) (DESIGN.md §3).
+// f(X) = ½tr(XᵀAXB) (BilinearModel, problems.cpp:143-156; problem P4); A n×n and
+// B p×p symmetric host matrices owned by the caller.
+class BilinearModel : public ObjectiveModel {
+ public:
+  BilinearModel(const DenseMatrix& a, const DenseMatrix& b, double s) {
+    if (a.rows() != a.cols() || b.rows() != b.cols())
+      throw dimension_error("BilinearModel: A and B must be square");
+    desc_.kind = PCAL_MODEL_BILINEAR;
+    desc_.location = PCAL_HOST;
+    desc_.n = a.rows();
+    desc_.p = b.rows();
+    desc_.s = s;
+    desc_.a = a.data();
+    desc_.b = b.data();
+  }
+};
+
+enum class ProblemKind { P1 = 1, P2 = 2, P3 = 3, P4 = 4, P6 = 6 };
+
+// DensityModel (problems.cpp:158-206): ½tr(XᵀLX) plus the density term of
+// ρ = rowsq(X) and h = L⁻¹ρ — P1: ¼·coeff·ρᵀh; P6: ½ρᵀh − ¾·coeff·Σρ^{4/3}.
+// Like the reference's constructor (which builds its LinearSolver), this forms
+// L⁻¹ and throws generation_error when L is numerically singular.
+class DensityModel : public ObjectiveModel {
+ public:
+  DensityModel(const DenseMatrix& l, std::int64_t p, double coeff, ProblemKind kind, double s)
+      : linv_(l.rows(), l.cols()) {
+    if (l.rows() != l.cols()) throw dimension_error("DensityModel: L must be square");
+    if (p < 1 || 2 * p > l.rows())
+      throw parameter_error("DensityModel: dimensions must satisfy 2p <= n");
+    if (kind != ProblemKind::P1 && kind != ProblemKind::P6)
+      throw parameter_error("DensityModel: kind must be P1 or P6");
+    if (pcal_density_inverse(l.data(), l.rows(), linv_.data(), 8) != PCAL_OK)
+      throw generation_error("LinearSolver: matrix is numerically singular");
+    desc_.kind = PCAL_MODEL_DENSITY;
+    desc_.location = PCAL_HOST;
+    desc_.n = l.rows();
+    desc_.p = p;
+    desc_.s = s;
+    desc_.a = l.data();
+    desc_.linv = linv_.data();
+    desc_.coeff = coeff;
+    desc_.density_variant = kind == ProblemKind::P6 ? PCAL_DENSITY_P6 : PCAL_DENSITY_P1;
+  }
+  DensityModel(const DensityModel&) = delete;
+  DensityModel& operator=(const DensityModel&) = delete;
+
+ private:
+  DenseMatrix linv_;
+};
+
 // A caller-defined objective on the device: the counterpart of subclassing
 // orthopt::ObjectiveModel and overriding evaluate() (problems.hpp:24-51).
 // enqueue_gradient() receives device pointers and the solver's CUDA stream
@@ -196,6 +249,7 @@ class DeviceModel : public ObjectiveModel {
   }
 };
 
+// E(X) = ¼tr(XᵀLX) + ½tr(XᵀV_ion X) + ¼ρᵀL†ρ + ½ρᵀε_xc(ρ) (DESIGN.md §3).
 class KohnShamModel : public StencilModel {
  public:
   KohnShamModel(std::int64_t nx, std::int64_t ny, std::int64_t nz, const std::vector<double>& v_ion,

@@ -52,6 +52,13 @@ extern "C" {
 #define PCAL_MODEL_STENCIL 2    /* f = ½tr(XᵀLX) + ½tr(XᵀVX), L = −Δ_h 7-point periodic */
 #define PCAL_MODEL_KOHN_SHAM 3  /* E = ¼tr(XᵀLX)+½tr(XᵀV_ionX)+¼ρᵀL†ρ+½ρᵀε_xc(ρ) */
 #define PCAL_MODEL_DEVICE_CALLBACK 4  /* any f: the caller's own device gradient (below) */
+#define PCAL_MODEL_BILINEAR 5   /* f = ½tr(XᵀAXB), A n×n, B p×p symmetric (problems.cpp:143-156, P4) */
+#define PCAL_MODEL_DENSITY 6    /* f = ½tr(XᵀLX) + density term of ρ = rowsq(X), h = L⁻¹ρ
+                                   (DensityModel, problems.cpp:158-206, P1 / P6) */
+
+/* DensityModel's two density terms (problems.cpp:179-203) */
+#define PCAL_DENSITY_P1 0       /* + ¼·coeff·ρᵀh,            G += coeff·h∘X          */
+#define PCAL_DENSITY_P6 1       /* + ½ρᵀh − ¾·coeff·Σρ^{4/3}, G += (2h − 2coeff·ρ^{1/3})∘X */
 
 /* ObjectiveModel::evaluate (problems.hpp:39) for a caller-defined model, on the
  * device: enqueue on `stream` (a cudaStream_t) the work that writes G = ∇f(X)
@@ -97,6 +104,11 @@ typedef struct pcal_model_desc {
   const double* v;       /* stencil: V (n); Kohn–Sham: V_ion (n) */
   pcal_gradient_fn grad; /* PCAL_MODEL_DEVICE_CALLBACK: the gradient callback */
   void* grad_ctx;        /* its context pointer */
+  const double* b;       /* bilinear: B p×p column-major, symmetric (location as a) */
+  const double* linv;    /* density: L⁻¹ rows (the a slab's rows, all n_glob columns; ld = rows),
+                            from pcal_density_inverse — the reference's LinearSolver */
+  double coeff;          /* density: α (P1) or γ (P6) */
+  int32_t density_variant; /* PCAL_DENSITY_P1 / PCAL_DENSITY_P6 */
 } pcal_model_desc;
 
 typedef struct pcal_config {  /* orthopt::SolverConfig (solver.hpp:30-42) */
@@ -260,6 +272,13 @@ int pcal_spectral_norm_estimate_host(const double* a, int64_t n, uint64_t seed, 
 /* sym_part(random_normal(n, n, Rng(seed))) — the dense operator of configs 1–2
  * (problems.cpp:45-48). */
 int pcal_gen_dense_operator(int64_t n, uint64_t seed, double* a, int32_t threads);
+
+/* L⁻¹ of a symmetric n×n L (column-major, host), for PCAL_MODEL_DENSITY: the
+ * reference's LinearSolver factorisation (linsolve.cpp:30-68 — Cholesky when it
+ * succeeds, else LU with partial pivoting) applied to the unit vectors with its
+ * own substitution loops (linsolve.cpp:70-102).  PCAL_E_PARAMETER (the
+ * reference's generation_error) when L is numerically singular. */
+int pcal_density_inverse(const double* l, int64_t n, double* linv, int32_t threads);
 /* initial_point({Qr}, n, p) on the device: orthonormalize(random_normal(n,p,Rng(seed)))
  * (solver.cpp:136-142). */
 int pcal_initial_point_qr(int64_t n, int64_t p, uint64_t seed, double* x0, int32_t device);

@@ -184,11 +184,17 @@ HARNESS_CASES = {  # name: (kind, n, p, alpha, kappa, theta, zeta, xi, block_tri
     "p1_block": (1, 60, 4, 0.0, 1.0, 1.01, 1.01, 1.0, 1, 12, 0, 0.5, 3000),
     "p2": (2, 90, 6, 0.0, 2.0, 1.05, 1.02, 0.7, 0, 13, 0, 0.5, 3000),
     "p3_a2i": (3, 70, 4, 0.0, 0.0, 1.08, 1.0, 0.5, 0, 14, 1, 0.6, 3000),
+    # DensityModel (P1 α > 0: LU path; block operator: Cholesky path) and P6, BilinearModel P4
+    "p1_alpha1": (1, 80, 5, 1.0, 1.0, 1.01, 1.01, 1.0, 0, 21, 0, 0.5, 3000),
+    "p1_block_alpha2": (1, 60, 4, 2.0, 1.0, 1.01, 1.01, 1.0, 1, 22, 0, 0.5, 3000),
+    "p4": (4, 60, 5, 1.0, 1.0, 1.01, 1.01, 1.0, 0, 23, 0, 0.5, 3000),
+    "p6": (6, 70, 4, 1.0, 1.0, 1.01, 1.01, 1.0, 0, 24, 0, 0.5, 3000),
+    "p6_block_a2ii": (6, 50, 3, 1.0, 1.0, 1.01, 1.01, 1.0, 1, 25, 2, 0.5, 3000),
 }
 
 
 def harness_cases(R: Reference) -> None:
-    """run_single (harness.cpp:62-73) JSON reports for the dense problem kinds."""
+    """run_single (harness.cpp:62-73) JSON reports for every problem kind."""
     import ctypes as C
     L = R.lib
     L.ref_run_single_json.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_double, C.c_double,
@@ -201,6 +207,63 @@ def harness_cases(R: Reference) -> None:
                                      sigma, iters, buf, len(buf)) == 0, name
         open(os.path.join(OUT, f"ref_run_single_{name}.json"), "w").write(buf.value.decode() + "\n")
     print("wrote run_single reports")
+
+
+def linsolve_cases(R: Reference) -> None:
+    """LinearSolver (linsolve.cpp) inverses: random symmetric (LU path), the block
+    operator (Cholesky path), a singular matrix (generation_error)."""
+    import ctypes as C
+    L = R.lib
+    dp = C.POINTER(C.c_double)
+    L.ref_linear_inverse.argtypes = [dp, C.c_int64, dp]
+    from oracle.oracle import Restatement
+    O = Restatement()
+    g = {}
+    blk = np.zeros((30, 30), order="F")
+    for b in range(0, 30, 5):
+        for i in range(5):
+            blk[b + i, b + i] = 2.0
+            if i < 4:
+                blk[b + i, b + i + 1] = blk[b + i + 1, b + i] = -1.0
+    sing = np.ones((6, 6), order="F")
+    m = O.random_normal(40, 40, 5)
+    for name, a in [("lu", 0.5 * (m + m.T)),
+                    ("chol", blk), ("singular", sing)]:
+        a = np.asfortranarray(a)
+        out = np.zeros_like(a, order="F")
+        rc = L.ref_linear_inverse(a.ctypes.data_as(dp), a.shape[0], out.ctypes.data_as(dp))
+        g[name + "_a"] = a
+        g[name + "_inv"] = out
+        g[name + "_singular"] = np.array(rc == 1)
+    np.savez_compressed(os.path.join(OUT, "reference_linsolve.npz"), **g)
+    print("wrote reference_linsolve.npz")
+
+
+MODEL_EVAL_CASES = {  # name: (kind, n, p, alpha, block_tridiag, seed) — acceptance #3's instances
+    "p1": (1, 60, 6, 1.0, 0, 31), "p6": (6, 60, 6, 1.0, 0, 32), "p4": (4, 60, 6, 1.0, 0, 35),
+    "p1_block": (1, 45, 4, 2.0, 1, 36), "p6_block": (6, 45, 4, 1.0, 1, 37),
+}
+
+
+def model_eval_cases(R: Reference) -> None:
+    """The reference's P1 (α > 0) / P4 / P6 models evaluated at seeded points."""
+    import ctypes as C
+    L = R.lib
+    dp = C.POINTER(C.c_double)
+    L.ref_evaluate_problem.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_double, C.c_int,
+                                       C.c_uint64, dp, dp, dp]
+    g = {}
+    for name, (kind, n, p, alpha, bt, seed) in MODEL_EVAL_CASES.items():
+        x = np.asfortranarray(R.random_normal(n, p, 300 + seed))
+        f = C.c_double()
+        gr = np.zeros((n, p), order="F")
+        assert L.ref_evaluate_problem(kind, n, p, alpha, bt, seed, x.ctypes.data_as(dp),
+                                      C.byref(f), gr.ctypes.data_as(dp)) == 0, name
+        g[name + "_x"] = x
+        g[name + "_f"] = f.value
+        g[name + "_g"] = gr
+    np.savez_compressed(os.path.join(OUT, "reference_models.npz"), **g)
+    print("wrote reference_models.npz")
 
 
 def grid_cases(R: Reference) -> None:
@@ -288,6 +351,8 @@ if __name__ == "__main__":
     report_io_cases(R)
     init_cases(R)
     harness_cases(R)
+    linsolve_cases(R)
+    model_eval_cases(R)
     if "--cfg2" in sys.argv:
         cfg2(R)
     if "--grids" in sys.argv:

@@ -16,6 +16,7 @@
 
 #include "orthopt/diagnostics.hpp"
 #include "orthopt/kernels.hpp"
+#include "orthopt/linsolve.hpp"
 #include "orthopt/problems.hpp"
 #include "orthopt/rng.hpp"
 #include "orthopt/solver.hpp"
@@ -428,6 +429,45 @@ int ref_save_quadratic(const double* a, const double* g0, std::int64_t n, std::i
     auto m = make_quadratic(sym_from_ptr(a, n), std::move(g), g0 ? ProblemKind::P2 : ProblemKind::P3, s);
     std::ofstream out(path, std::ios::binary);
     save_problem(*m, out);
+    return 0;
+  });
+}
+
+// LinearSolver (linsolve.cpp) of a symmetric a, solved against the identity's
+// columns: pins pcal_density_inverse.  1 when the constructor throws
+// generation_error (numerically singular).
+int ref_linear_inverse(const double* a, std::int64_t n, double* out) {
+  return guarded([&] {
+    std::unique_ptr<LinearSolver> ls;
+    try {
+      ls = std::make_unique<LinearSolver>(sym_from_ptr(a, n));
+    } catch (const generation_error&) {
+      return 1;
+    }
+    std::vector<double> e((size_t)n, 0.0);
+    for (std::int64_t c = 0; c < n; ++c) {
+      e[(size_t)c] = 1.0;
+      const std::vector<double> y = ls->solve(e);
+      e[(size_t)c] = 0.0;
+      std::memcpy(out + c * n, y.data(), sizeof(double) * (size_t)n);
+    }
+    return 0;
+  });
+}
+
+// gen_problem{1,4,6}(…, seed) evaluated at x (problems.cpp:130-206): pins the
+// device Bilinear / Density models.  kind 1 = P1 (alpha), 4 = P4, 6 = P6.
+int ref_evaluate_problem(int kind, std::int64_t n, std::int64_t p, double alpha, int block_tridiag,
+                         std::uint64_t seed, const double* x, double* f, double* g) {
+  return guarded([&] {
+    const OperatorMode mode = block_tridiag ? OperatorMode::BlockTridiag : OperatorMode::RandomSym;
+    std::unique_ptr<ObjectiveModel> m =
+        kind == 1 ? gen_problem1(n, p, alpha, mode, seed, 1)
+        : kind == 4 ? gen_problem4(n, p, seed, 1)
+                    : gen_problem6(n, p, mode, seed, 1);
+    const Evaluation ev = m->evaluate(from_ptr(x, n, p), 1);
+    *f = ev.value;
+    std::memcpy(g, ev.gradient.data(), sizeof(double) * (size_t)(n * p));
     return 0;
   });
 }

@@ -30,6 +30,7 @@ import numpy as np
 __all__ = [
     "SolverConfig", "StepsizeRule", "MultiplierRule", "RunReport", "FinalMetrics",
     "CategoryTimers", "QuadraticModel", "StencilModel", "KohnShamModel", "make_quadratic",
+    "BilinearModel", "DensityModel", "density_inverse",
     "solve", "Session", "gram", "matmul_at_b", "matmul", "orthonormalize", "pcal_step",
     "spectral_norm_estimate", "initial_point", "evaluate", "random_normal", "random_uniform",
     "gen_dense_operator", "flops_estimate", "ParameterError", "DimensionError", "RankError",
@@ -44,6 +45,8 @@ STATUS = {0: "converged", 1: "max_iter", 2: "diverged"}
 TRACE_COLS = 7
 HOST, DEVICE = 0, 1
 MODEL_DENSE, MODEL_STENCIL, MODEL_KOHN_SHAM, MODEL_DEVICE_CALLBACK = 1, 2, 3, 4
+MODEL_BILINEAR, MODEL_DENSITY = 5, 6
+DENSITY_P1, DENSITY_P6 = 0, 1
 
 
 class NativeUnavailable(RuntimeError):
@@ -77,7 +80,8 @@ class _Model(C.Structure):
     _fields_ = [("kind", C.c_int32), ("location", C.c_int32), ("n", C.c_int64), ("p", C.c_int64),
                 ("s", C.c_double), ("a", C.c_void_p), ("g0", C.c_void_p), ("nx", C.c_int64),
                 ("ny", C.c_int64), ("nz", C.c_int64), ("v", C.c_void_p), ("grad", C.c_void_p),
-                ("grad_ctx", C.c_void_p)]
+                ("grad_ctx", C.c_void_p), ("b", C.c_void_p), ("linv", C.c_void_p),
+                ("coeff", C.c_double), ("density_variant", C.c_int32)]
 
 
 # pcal_gradient_fn (include/pcal_b200.h): enqueue G = ∇f(X) and f(X) on `stream`
@@ -152,6 +156,7 @@ def lib() -> C.CDLL:
     L.pcal_random_uniform.argtypes = [i64, u64, vp]
     L.pcal_spectral_norm_estimate_host.argtypes = [vp, i64, u64, i32, C.POINTER(dbl)]
     L.pcal_gen_dense_operator.argtypes = [i64, u64, vp, i32]
+    L.pcal_density_inverse.argtypes = [vp, i64, vp, i32]
     L.pcal_initial_point_qr.argtypes = [i64, i64, u64, vp, i32]
     L.pcal_initial_point.argtypes = [i64, i64, i32, dbl, u64, vp, i32]
     L.pcal_partition.argtypes = [C.POINTER(_Model), i32, i32, C.POINTER(i64), C.POINTER(i64)]
@@ -358,6 +363,66 @@ class DeviceCallbackModel(_ModelBase):
         g = self.grad if isinstance(self.grad, int) else C.cast(self.grad, C.c_void_p).value
         return _Model(self.kind, HOST, self.n, self.p, self.s, None, None, 0, 0, 0, None, g,
                       self.ctx), (self.grad,)
+
+
+class BilinearModel(_ModelBase):
+    """f(X) = ½tr(XᵀAXB), A n×n and B p×p symmetric (BilinearModel, problems.cpp:143-156;
+    problem P4).  ``a`` may be the local row slab of a sharded session (then pass n)."""
+
+    def __init__(self, a, b, s: float, n: Optional[int] = None):
+        self.kind = MODEL_BILINEAR
+        self.a = _f64(a)
+        self.b = _f64(b)
+        if self.b.ndim != 2 or self.b.shape[0] != self.b.shape[1]:
+            raise DimensionError("BilinearModel: b must be p-by-p")
+        self.location = HOST
+        self.n = int(self.a.shape[1]) if n is None else int(n)
+        self.p = int(self.b.shape[0])
+        self.s = float(s)
+
+    def _c(self) -> tuple:
+        return _Model(self.kind, HOST, self.n, self.p, self.s, _ptr(self.a), None, 0, 0, 0, None,
+                      None, None, _ptr(self.b)), (self.a, self.b)
+
+
+def density_inverse(l, threads: int = 8) -> np.ndarray:
+    """L⁻¹ by the reference's LinearSolver (linsolve.cpp:30-102: Cholesky, else LU
+    with partial pivoting); raises ParameterError (generation_error) if singular."""
+    l = _f64(l)
+    out = np.empty_like(l, order="F")
+    rc = lib().pcal_density_inverse(_ptr(l), l.shape[0], _ptr(out), threads)
+    if rc == E_PARAMETER:
+        raise ParameterError("LinearSolver: matrix is numerically singular")
+    _check(rc)
+    return out
+
+
+class DensityModel(_ModelBase):
+    """DensityModel (problems.cpp:158-206): f = ½tr(XᵀLX) plus, with ρ = rowsq(X)
+    and h = L⁻¹ρ, ¼·coeff·ρᵀh (P1) or ½ρᵀh − ¾·coeff·Σρ^{4/3} (P6).  L⁻¹ is
+    formed at construction, as the reference builds its LinearSolver there.
+    ``l`` / ``linv`` may be the local row slabs of a sharded session (pass n)."""
+
+    def __init__(self, l, p: int, coeff: float, s: float, variant: str = "p1", linv=None,
+                 n: Optional[int] = None):
+        self.kind = MODEL_DENSITY
+        if int(p) < 1 or 2 * int(p) > (l.shape[1] if n is None else n):
+            raise ParameterError("DensityModel: dimensions must satisfy 2p <= n")
+        self.a = _f64(l)
+        self.linv = density_inverse(self.a) if linv is None else _f64(linv)
+        self.variant = variant.lower()
+        if self.variant not in ("p1", "p6"):
+            raise ParameterError(f"DensityModel: unknown variant {variant!r}")
+        self.coeff = float(coeff)
+        self.location = HOST
+        self.n = int(self.a.shape[1]) if n is None else int(n)
+        self.p = int(p)
+        self.s = float(s)
+
+    def _c(self) -> tuple:
+        return _Model(self.kind, HOST, self.n, self.p, self.s, _ptr(self.a), None, 0, 0, 0, None,
+                      None, None, None, _ptr(self.linv), self.coeff,
+                      DENSITY_P6 if self.variant == "p6" else DENSITY_P1), (self.a, self.linv)
 
 
 def make_quadratic(a, p: int, s: float, g0=None) -> QuadraticModel:

@@ -229,3 +229,99 @@ int pcal_spectral_norm_estimate_host(const double* a, int64_t n, uint64_t seed, 
 }
 
 }  // extern "C"
+
+// L⁻¹ for the density models: the reference's LinearSolver (linsolve.cpp:10-102)
+// — Cholesky when every pivot is positive and finite, else LU with partial
+// pivoting and a 1e-14·max|L| singularity floor — solved against e_j for each
+// column j with the same forward / back substitution loops.  Columns are
+// independent, so they are spread over `threads`.
+int pcal_density_inverse(const double* l, int64_t n, double* linv, int32_t threads) {
+  if (!l || !linv || n < 1) return PCAL_E_PARAMETER;
+  const size_t N = (size_t)n;
+  // factors stored row-major (F(i,j) at i·n + j): the factorisation's inner
+  // loops and the substitutions' row loops then run along memory; the
+  // arithmetic and its order are the reference's.
+  std::vector<double> f(N * N);
+  auto F = [&](int64_t i, int64_t j) -> double& { return f[(size_t)j + (size_t)i * N]; };
+  bool spd = true;
+  for (int64_t j = 0; j < n && spd; ++j) {  // try_cholesky (linsolve.cpp:10-26)
+    double d = l[j + j * n];
+    for (int64_t k = 0; k < j; ++k) d -= F(j, k) * F(j, k);
+    if (!(d > 0.0) || !std::isfinite(d)) {
+      spd = false;
+      break;
+    }
+    const double ljj = std::sqrt(d);
+    F(j, j) = ljj;
+    for (int64_t i = j + 1; i < n; ++i) {
+      double s = l[i + j * n];
+      for (int64_t k = 0; k < j; ++k) s -= F(i, k) * F(j, k);
+      F(i, j) = s / ljj;
+    }
+  }
+  std::vector<int64_t> perm;
+  if (!spd) {  // LU with partial pivoting on a dense copy (linsolve.cpp:36-67)
+    for (int64_t j = 0; j < n; ++j)
+      for (int64_t i = 0; i < n; ++i) F(i, j) = l[i + j * n];
+    perm.resize(N);
+    for (int64_t i = 0; i < n; ++i) perm[(size_t)i] = i;
+    double scale = 0.0;
+    for (double v : f) scale = std::max(scale, std::abs(v));
+    const double floor = 1e-14 * std::max(scale, 1e-300);
+    for (int64_t k = 0; k < n; ++k) {
+      int64_t piv = k;
+      double best = std::abs(F(k, k));
+      for (int64_t i = k + 1; i < n; ++i)
+        if (std::abs(F(i, k)) > best) {
+          best = std::abs(F(i, k));
+          piv = i;
+        }
+      if (!(best > floor)) return PCAL_E_PARAMETER;  // generation_error: numerically singular
+      if (piv != k) {
+        for (int64_t j = 0; j < n; ++j) std::swap(F(k, j), F(piv, j));
+        std::swap(perm[(size_t)k], perm[(size_t)piv]);
+      }
+      const double inv = 1.0 / F(k, k);
+      for (int64_t i = k + 1; i < n; ++i) {
+        const double m = F(i, k) * inv;
+        F(i, k) = m;
+        if (m != 0.0)
+          for (int64_t j = k + 1; j < n; ++j) F(i, j) -= m * F(k, j);
+      }
+    }
+  }
+  // column-major copy for the Cholesky back substitution's column loop
+  std::vector<double> fc;
+  if (spd) {
+    fc.resize(N * N);
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t j = 0; j < n; ++j) fc[(size_t)i + (size_t)j * N] = F(i, j);
+  }
+  // LinearSolver::solve(e_c) for every column c (linsolve.cpp:70-102)
+  auto solve_col = [&](int64_t c, std::vector<double>& y) {
+    for (int64_t i = 0; i < n; ++i) y[(size_t)i] = (spd ? i : perm[(size_t)i]) == c ? 1.0 : 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+      double s = y[(size_t)i];
+      for (int64_t k = 0; k < i; ++k) s -= F(i, k) * y[(size_t)k];
+      y[(size_t)i] = spd ? s / F(i, i) : s;
+    }
+    for (int64_t i = n - 1; i >= 0; --i) {
+      double s = y[(size_t)i];
+      if (spd)
+        for (int64_t k = i + 1; k < n; ++k) s -= fc[(size_t)k + (size_t)i * N] * y[(size_t)k];
+      else
+        for (int64_t k = i + 1; k < n; ++k) s -= F(i, k) * y[(size_t)k];
+      y[(size_t)i] = s / F(i, i);
+    }
+    std::memcpy(linv + c * n, y.data(), sizeof(double) * N);
+  };
+  const int nt = std::max(1, std::min<int>(threads, (int)n));
+  std::vector<std::thread> pool;
+  for (int t = 0; t < nt; ++t)
+    pool.emplace_back([&, t] {
+      std::vector<double> y(N);
+      for (int64_t c = t; c < n; c += nt) solve_col(c, y);
+    });
+  for (auto& th : pool) th.join();
+  return PCAL_OK;
+}

@@ -299,4 +299,79 @@ __global__ void k_ks_potential(const double* __restrict__ v, const double* __res
   }
 }
 
+// h = L⁻¹ρ of the density models (DensityModel::evaluate, problems.cpp:170;
+// LinearSolver::solve through the precomputed inverse): rows [0, n) of the
+// slab m (ld ldm), all nk columns.  A block covers 32 rows with 8 column
+// groups: a warp reads one 256-byte row segment per column, each thread sums
+// its columns k ≡ g (mod 8) in order and the group sums are added in group
+// order, so h is independent of the grid and of the row partition.
+__global__ void __launch_bounds__(256) k_density_hartree(const double* __restrict__ m, int64_t ldm,
+                                                         int64_t n, int64_t nk,
+                                                         const double* __restrict__ rho,
+                                                         double* __restrict__ h, const Ctl* ctl) {
+  if (ctl && ctl->done) return;
+  __shared__ double part[8][33];
+  const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int64_t i = (int64_t)blockIdx.x * 32 + lane;
+  double s = 0.0;
+  if (i < n) {
+    const double* mi = m + i;
+#pragma unroll 4
+    for (int64_t k = g; k < nk; k += 8) s = fma(__ldg(mi + k * ldm), __ldg(rho + k), s);
+  }
+  part[g][lane] = s;
+  __syncthreads();
+  if (g == 0 && i < n) {
+    double t = part[0][lane];
+#pragma unroll
+    for (int q = 1; q < 8; ++q) t += part[q][lane];
+    h[i] = t;
+  }
+}
+
+// The density term of DensityModel::evaluate (problems.cpp:179-203) on the
+// owned rows, after G = L·X: P1 G += (coeff·h)∘X, P6 G += (2h − 2coeff·ρ^{1/3})∘X;
+// block partials of ρᵀh and Σρ^{4/3} into spart[3b + 1], [3b + 2] (slot 0 = 0,
+// the Kohn–Sham layout).  Non-finite G sets *bad (check_finite, problems.cpp:27-30).
+// chunk > 0: block b owns rows [b·chunk, (b+1)·chunk) (reproducible sharded path).
+__global__ void k_density_apply(const double* __restrict__ x, double* __restrict__ g, int64_t ld,
+                                int64_t n, int64_t p, const double* __restrict__ rho,
+                                const double* __restrict__ h, double coeff, int p6,
+                                double* __restrict__ spart, int32_t* bad, const Ctl* ctl,
+                                int64_t chunk = 0) {
+  if (ctl && ctl->done) return;
+  __shared__ double sm[kStreamThreadsOps / 32];
+  double rh = 0.0, ex = 0.0;
+  bool nonfinite = false;
+  const int64_t i0 = chunk ? (int64_t)blockIdx.x * chunk + threadIdx.x
+                           : (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t i1 = chunk ? min(n, (int64_t)(blockIdx.x + 1) * chunk) : n;
+  const int64_t di = chunk ? (int64_t)blockDim.x : (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = i0; i < i1; i += di) {
+    const double r = rho[i], hi = h[i];
+    double w;
+    rh = __dadd_rn(rh, __dmul_rn(r, hi));
+    if (p6) {
+      const double cr = cbrt(r);
+      ex = __dadd_rn(ex, __dmul_rn(r, cr));
+      w = __dsub_rn(__dmul_rn(2.0, hi), __dmul_rn(__dmul_rn(2.0, coeff), cr));
+    } else {
+      w = __dmul_rn(coeff, hi);
+    }
+    for (int64_t j = 0; j < p; ++j) {
+      const double v = __dadd_rn(g[i + j * ld], __dmul_rn(w, x[i + j * ld]));
+      g[i + j * ld] = v;
+      nonfinite |= !isfinite(v);
+    }
+  }
+  if (nonfinite) *bad = 1;
+  const double b = block_sum<kStreamThreadsOps>(rh, sm);
+  const double d = block_sum<kStreamThreadsOps>(ex, sm);
+  if (threadIdx.x == 0) {
+    spart[blockIdx.x * 3 + 0] = 0.0;
+    spart[blockIdx.x * 3 + 1] = b;
+    spart[blockIdx.x * 3 + 2] = d;
+  }
+}
+
 }  // namespace pcal

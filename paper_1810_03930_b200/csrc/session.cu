@@ -287,6 +287,8 @@ struct FinishArgs {
   int32_t* bad;         // evaluation non-finite flag
   double c_xc;          // (3/π)^{1/3}
   const double* fdev;   // device-callback models: f(X) as written by the callback
+  double coeff;         // density models: α (P1) / γ (P6)
+  int32_t p6;           // density models: the P6 term
 };
 
 // Thread-0 tail of an evaluation: objective assembly, failure flags, trace
@@ -305,6 +307,8 @@ __device__ void finish_record(const FinishArgs& a, Ctl* ctl, double* post, doubl
     f = 0.25 * f1 + 0.5 * vr + 0.25 * rh - 0.375 * a.c_xc * ex;
   } else if (a.model == PCAL_MODEL_DEVICE_CALLBACK) {
     f = *a.fdev;
+  } else if (a.model == PCAL_MODEL_DENSITY) {  // problems.cpp:175-194
+    f = a.p6 ? 0.5 * f1 + 0.5 * rh - 0.75 * a.coeff * ex : 0.5 * f1 + 0.25 * a.coeff * rh;
   } else {
     f = 0.5 * f1;
   }
@@ -365,7 +369,7 @@ __global__ void __launch_bounds__(256) k_finish_eval(FinishArgs a, Ctl* ctl,
     pk += a.kcol[j];
   }
   for (int i = threadIdx.x; i < a.ncp; i += blockDim.x) pc += a.cpart[i];
-  if (a.model == PCAL_MODEL_KOHN_SHAM)
+  if (a.model == PCAL_MODEL_KOHN_SHAM || a.model == PCAL_MODEL_DENSITY)
     for (int i = threadIdx.x; i < a.nsp; i += blockDim.x) {
       pv += a.spart[3 * i];
       pr += a.spart[3 * i + 1];
@@ -464,6 +468,7 @@ struct pcal_session {
   double beta = 1.0, eta0 = 0.0, c_xc = 0.0;
   // model data
   pcal::DevBuf A, g0, V, u, rho, h, tmpa, tmpb, qx, qy, qz, lx, ly, lz, spart;
+  pcal::DevBuf Bm, tb, Minv;  // bilinear B (pp×pp) and A·X; density L⁻¹ rows
   pcal::DevBuf fdev;  // device-callback models: f(X)
   int64_t ldA = 0;
   // iteration state
@@ -477,7 +482,7 @@ struct pcal_session {
   pcal::DevBuf trace;
   int64_t trace_cap = 0;
   // plans
-  pcal::GemmPlan grad[2], gram[2], xm[2], orth_gram, orth_mul;
+  pcal::GemmPlan grad[2], grad2[2], gram[2], xm[2], orth_gram, orth_mul;
   // MOptQR in-graph retraction (per parity): Gram of Z, Z·T → Q1, Gram of Q1, Q1·T → Q
   pcal::GemmPlan rq_gram_z[2], rq_mul1[2], rq_gram_q[2], rq_mul2[2];
   pcal::DevBuf lam;  // dual-ascent multiplier Λ (p×p, replicated)
@@ -512,6 +517,10 @@ struct pcal_session {
 
 namespace pcal {
 
+// models whose gradient starts with the dense GEMM A·X (A n×n, row-sharded)
+static bool dense_family(int32_t kind) {
+  return kind == PCAL_MODEL_DENSE || kind == PCAL_MODEL_BILINEAR || kind == PCAL_MODEL_DENSITY;
+}
 static double* Xof(pcal_session* s, int b) { return s->pair[b].p + s->ld * s->pp; }
 static double* Pof(pcal_session* s, int b) { return s->pair[b].p; }
 // packed per-column sums of an evaluation: [f | kkt² | d] (one allreduce when sharded)
@@ -689,10 +698,38 @@ static void launch_stencil(pcal_session* s, int b, const double* u, bool ks, con
   }
 }
 
+// DensityModel's terms after G = L·X (problems.cpp:169-203): ρ over all rows
+// (the gathered X when sharded), h = L⁻¹ρ on the owned rows, G += w∘X.
+static void launch_density(pcal_session* s, int b, const Ctl* ctl) {
+  const bool gathered = s->comm && s->comm->size > 1;
+  const int64_t ng = s->n_glob;
+  k_row_sq_norms<<<(unsigned)ceil_div(ng, 256), 256, 0, s->stream>>>(
+      gathered ? s->xfull.p : Xof(s, b), ng, gathered ? s->K_full : s->ld, s->p, s->rho.p, ctl);
+  launched("k_row_sq_norms");
+  k_density_hartree<<<(unsigned)ceil_div(s->n, 32), 256, 0, s->stream>>>(
+      s->Minv.p, s->ld, s->n, ng, s->rho.p, s->h.p, ctl);
+  launched("k_density_hartree");
+  const int p6 = s->model.density_variant == PCAL_DENSITY_P6;
+  if (s->repro) {  // density scalars per row chunk, reduced in chunk order
+    k_density_apply<<<(unsigned)s->nch, 256, 0, s->stream>>>(
+        Xof(s, b), Pof(s, b), s->ld, s->n, s->p, s->rho.p + s->row0, s->h.p, s->model.coeff, p6,
+        s->cc.p, s->bad, ctl, s->chunk_rows);
+    launched("k_density_apply");
+    chunk_reduce(s, s->cc.p, 3, s->spt.p, ctl);
+  } else {
+    k_density_apply<<<s->sp_blocks, 256, 0, s->stream>>>(
+        Xof(s, b), Pof(s, b), s->ld, s->n, s->p, s->rho.p + s->row0, s->h.p, s->model.coeff, p6,
+        s->spart.p, s->bad, ctl);
+    launched("k_density_apply");
+  }
+}
+
 static void launch_gradient(pcal_session* s, int b, const Ctl* ctl) {
   const int64_t p = s->p;
   switch (s->model.kind) {
     case PCAL_MODEL_DENSE:
+    case PCAL_MODEL_BILINEAR:
+    case PCAL_MODEL_DENSITY:
       if (s->comm && s->comm->size > 1) {  // C5: every rank needs all rows of X for A·X
         const int R = s->comm->size;
         s->comm->allgather(Xof(s, b), s->xgath.p, (size_t)s->ld * s->pp, s->stream);
@@ -702,6 +739,8 @@ static void launch_gradient(pcal_session* s, int b, const Ctl* ctl) {
         launched("k_unpack_rows");
       }
       launch_gemm(s->grad[b], s->stream);
+      if (s->model.kind == PCAL_MODEL_BILINEAR) launch_gemm(s->grad2[b], s->stream);  // (A·X)·B
+      if (s->model.kind == PCAL_MODEL_DENSITY) launch_density(s, b, ctl);
       break;
     case PCAL_MODEL_STENCIL: {
       launch_stencil(s, b, s->V.p, false, ctl);
@@ -801,7 +840,7 @@ static void launch_eval(pcal_session* s, int b, int mode, const Ctl* ctl_guard) 
     a.in[0] = s->fpart.p;
     a.nrows[0] = s->nrb_f;
     a.stride[0] = s->pstride_f;
-    a.rpc[0] = s->model.kind == PCAL_MODEL_DENSE ? s->chunk_rows / cfg_info(pick_size(s->pp)).WM
+    a.rpc[0] = dense_family(s->model.kind) ? s->chunk_rows / cfg_info(pick_size(s->pp)).WM
                                                  : s->model.ny / 8;
     a.in[1] = s->kpart.p;
     a.in[2] = dform ? s->dpart.p : nullptr;
@@ -839,6 +878,8 @@ static void launch_eval(pcal_session* s, int b, int mode, const Ctl* ctl_guard) 
   fa.bad = s->bad;
   fa.c_xc = s->c_xc;
   fa.fdev = s->fdev.p;
+  fa.coeff = s->model.coeff;
+  fa.p6 = s->model.density_variant == PCAL_DENSITY_P6;
   k_finish_eval<<<1, 256, 0, st>>>(fa, s->ctl, s->post.p);
   launched("k_finish_eval");
   mark(s, 4);
@@ -1026,14 +1067,17 @@ static void build_plans(pcal_session* s) {
     }
   }
   for (int b = 0; b < 2; ++b) {
-    // gradient (dense): G = A·X, A ldA×ldA (MCONTIG), X ld×pp
-    if (s->model.kind == PCAL_MODEL_DENSE) {
+    // gradient (dense family): G = A·X, A ldA×ldA (MCONTIG), X ld×pp; the
+    // bilinear model stores A·X and applies B in a second GEMM with the epilogue
+    if (dense_family(s->model.kind)) {
       GemmPlan& g = s->grad[b];
       const int sz = pick_size(pp);
+      const bool bil = s->model.kind == PCAL_MODEL_BILINEAR;
+      const int epi = bil ? EPI_STORE : EPI_GRAD;
       if (s->repro) {  // fixed K segments (chosen from global sizes in session_create)
-        plan_gemm(g, dev, sz, A_MCONTIG, EPI_GRAD, n, pp, s->K_full, -1, 0, s->grad_splits);
+        plan_gemm(g, dev, sz, A_MCONTIG, epi, n, pp, s->K_full, -1, 0, s->grad_splits);
       } else {
-        plan_gemm(g, dev, sz, A_MCONTIG, EPI_GRAD, n, pp, s->K_full);
+        plan_gemm(g, dev, sz, A_MCONTIG, epi, n, pp, s->K_full);
       }
       g.args.A = s->A.p;
       g.args.lda = s->ldA;
@@ -1052,6 +1096,21 @@ static void build_plans(pcal_session* s) {
       e.n = n;
       e.p = s->p;
       g.args.ctl = s->ctl;
+      if (bil) {  // T = A·X (all pp columns: X's padding is zero), then G = T·B
+        e.C = s->tb.p;
+        e.ldc = ld;
+        e.m_store = n;
+        e.n_store = pp;
+        GemmPlan& g2 = s->grad2[b];
+        plan_gemm(g2, dev, sz, A_MCONTIG, EPI_GRAD, n, pp, pp, -1, 0, s->repro ? 1 : 0);
+        g2.args.A = s->tb.p;
+        g2.args.lda = ld;
+        g2.args.B = s->Bm.p;
+        g2.args.ldb = pp;
+        g2.args.ep = e;
+        g2.args.ep.C = nullptr;
+        g2.args.ctl = s->ctl;
+      }
     }
     // Gram: [P|X]ᵀ·X — A = pair (KCONTIG, rows m < 2pp), B = X, K = ld
     {
@@ -1182,7 +1241,7 @@ static void choose_segments(pcal_session* s, int64_t NC) {
   const int64_t pp = s->pp, Q = s->chunk_rows;
   const CfgInfo ci = cfg_info(pick_size(pp));
   auto rows_R = [&](int R) { return (double)ceil_div(NC, (int64_t)R) * Q; };  // worst rank
-  if (s->model.kind == PCAL_MODEL_DENSE) {
+  if (dense_family(s->model.kind)) {
     const int64_t ki = s->K_full / ci.BK;
     const double tn = (double)ceil_div(pp, ci.BN);
     s->grad_splits = best_segments(
@@ -1218,7 +1277,7 @@ static void alloc_state(pcal_session* s) {
   s->mcat.alloc((size_t)pp * 2 * pp);
   s->mcat.zero(st);
   // partial arrays: row-block granularities
-  const int64_t wm_grad = s->model.kind == PCAL_MODEL_DENSE ? cfg_info(pick_size(pp)).WM : 0;
+  const int64_t wm_grad = dense_family(s->model.kind) ? cfg_info(pick_size(pp)).WM : 0;
   const int64_t wm_xm = cfg_info(pick_size(2 * pp)).WM;
   s->st_chunk = 2048;
   s->st_nchunks = ceil_div(n, s->st_chunk);
@@ -1241,7 +1300,7 @@ static void alloc_state(pcal_session* s) {
   if (s->comm) {
     const int R = s->comm->size;
     const auto& m = s->model;
-    if (m.kind == PCAL_MODEL_DENSE) {  // C5: X allgather, unpacked into global row order
+    if (dense_family(m.kind)) {  // C5: X allgather, unpacked into global row order
       s->xgath.alloc((size_t)R * ld * pp);
       s->xfull.alloc((size_t)s->K_full * pp);
       s->xfull.zero(st);
@@ -1258,7 +1317,7 @@ static void alloc_state(pcal_session* s) {
     PCAL_CUDA(cudaMemcpy(s->rank_rows_d.p, rr.data(), sizeof(int64_t) * 2 * R,
                          cudaMemcpyHostToDevice));
   }
-  s->nrb_f = s->model.kind == PCAL_MODEL_DENSE ? ceil_div(n, wm_grad)
+  s->nrb_f = dense_family(s->model.kind) ? ceil_div(n, wm_grad)
              : s->st_march ? (s->model.ny / 8) * ceil_div(s->gz, s->st_zpart)
                            : s->st_nchunks;
   s->nrb_xm = ceil_div(n, wm_xm);
@@ -1331,13 +1390,35 @@ static void upload_model(pcal_session* s) {
   const pcal_model_desc& m = s->model;
   cudaStream_t st = s->stream;
   const int64_t n = s->n;
-  if (m.kind == PCAL_MODEL_DENSE) {
+  if (dense_family(m.kind)) {
     if (!m.a) throw Error(PCAL_E_PARAMETER, "dense model: a is NULL");
     s->ldA = s->ld;
     s->A.alloc((size_t)s->ldA * s->K_full);
     s->A.zero(st);
     upload_matrix(m.a, m.location, n, s->n_glob, s->A.p, s->ldA, st);
-    if (m.g0) {
+    if (m.kind == PCAL_MODEL_BILINEAR) {  // B zero-padded to pp×pp; A·X scratch
+      if (!m.b) throw Error(PCAL_E_PARAMETER, "bilinear model: b is NULL");
+      s->Bm.alloc((size_t)s->pp * s->pp);
+      s->Bm.zero(st);
+      upload_matrix(m.b, m.location, s->p, s->p, s->Bm.p, s->pp, st);
+      s->tb.alloc((size_t)s->ld * s->pp);
+      s->tb.zero(st);
+    }
+    if (m.kind == PCAL_MODEL_DENSITY) {  // L⁻¹ rows of the slab, ρ (all rows), h
+      if (!m.linv) throw Error(PCAL_E_PARAMETER, "density model: linv is NULL");
+      if (m.density_variant != PCAL_DENSITY_P1 && m.density_variant != PCAL_DENSITY_P6)
+        throw Error(PCAL_E_PARAMETER, "density model: unknown variant");
+      s->Minv.alloc((size_t)s->ld * s->n_glob);
+      s->Minv.zero(st);
+      upload_matrix(m.linv, m.location, n, s->n_glob, s->Minv.p, s->ld, st);
+      s->rho.alloc((size_t)s->n_glob);
+      s->h.alloc((size_t)s->ld);
+      s->h.zero(st);
+      s->sp_blocks = 4 * 148;
+      s->spart.alloc((size_t)3 * s->sp_blocks);
+      s->spart.zero(st);
+    }
+    if (m.kind == PCAL_MODEL_DENSE && m.g0) {
       s->g0.alloc((size_t)s->ld * s->pp);
       s->g0.zero(st);
       upload_matrix(m.g0, m.location, n, s->p, s->g0.p, s->ld, st);
@@ -2363,6 +2444,8 @@ int pcal_evaluate(const pcal_model_desc* model, const double* x, double* f, doub
     fa.bad = s->bad;
     fa.c_xc = s->c_xc;
     fa.fdev = s->fdev.p;
+    fa.coeff = s->model.coeff;
+    fa.p6 = s->model.density_variant == PCAL_DENSITY_P6;
     k_finish_eval<<<1, 256, 0, s->stream>>>(fa, s->ctl, s->post.p);
     launched("k_finish_eval");
     double post[8];
@@ -2582,7 +2665,8 @@ int pcal_solve_emulated(const pcal_model_desc* model, const pcal_config* config,
       partition(*model, R, r, &r0[r], &rows[r], &z0, &nzl);
       if (rows[r] < 1) throw Error(PCAL_E_PARAMETER, "a rank would own no rows");
     }
-    std::vector<std::vector<double>> a_loc(R), g_loc(R), x_loc(R), stop_loc(R), fin_loc(R);
+    std::vector<std::vector<double>> a_loc(R), g_loc(R), x_loc(R), stop_loc(R), fin_loc(R),
+        li_loc(R);
     std::vector<pcal_report> reps(R);
     std::vector<std::vector<double>> traces(R);
     std::vector<int> rcs(R, PCAL_OK);
@@ -2594,9 +2678,14 @@ int pcal_solve_emulated(const pcal_model_desc* model, const pcal_config* config,
         std::memcpy(dst.data() + c * rows[r], src + r0[r] + c * ld_src, sizeof(double) * rows[r]);
     };
     for (int r = 0; r < R; ++r) {
-      if (model->kind == PCAL_MODEL_DENSE) {
+      if (dense_family(model->kind)) {
+        if (!model->a) throw Error(PCAL_E_PARAMETER, "dense model: a is NULL");
         slice(model->a, n, r, n, a_loc[r]);
-        if (model->g0) slice(model->g0, n, r, p, g_loc[r]);
+        if (model->kind == PCAL_MODEL_DENSE && model->g0) slice(model->g0, n, r, p, g_loc[r]);
+        if (model->kind == PCAL_MODEL_DENSITY) {
+          if (!model->linv) throw Error(PCAL_E_PARAMETER, "density model: linv is NULL");
+          slice(model->linv, n, r, n, li_loc[r]);
+        }
       }
       slice(x0, n, r, p, x_loc[r]);
       stop_loc[r].resize((size_t)rows[r] * p);
@@ -2614,9 +2703,10 @@ int pcal_solve_emulated(const pcal_model_desc* model, const pcal_config* config,
         rcs[r] = guarded([&] {
           PCAL_CUDA(cudaSetDevice(config->device));
           pcal_model_desc m = *model;
-          if (m.kind == PCAL_MODEL_DENSE) {
+          if (dense_family(m.kind)) {
             m.a = a_loc[r].data();
-            m.g0 = model->g0 ? g_loc[r].data() : nullptr;
+            m.g0 = model->kind == PCAL_MODEL_DENSE && model->g0 ? g_loc[r].data() : nullptr;
+            if (m.kind == PCAL_MODEL_DENSITY) m.linv = li_loc[r].data();
           } else {
             m.v = model->v + r0[r];
           }

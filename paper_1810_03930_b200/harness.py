@@ -15,8 +15,13 @@ generated here with the reference's random stream and solved on the B200:
   The basis and the product are formed on the device, so the instance agrees
   with the reference's to rounding, not bitwise.
 
-P1 with α > 0, P4 (bilinear) and P6 are nonlinear / non-quadratic host models:
-they raise ``UnsupportedModel`` (run them through ``DeviceCallbackModel``).
+* P1 with α > 0 and P6 — ``DensityModel`` (problems.cpp:158-206, 208-217,
+  276-285): L = ``gen_operator``, the Hartree solve through L⁻¹ formed by the
+  reference's LinearSolver; P6 takes γ = 2·(3/π)^{1/3};
+* P4 — ``gen_problem4`` (problems.cpp:267-274): A = sym_part(random_normal(n, n)),
+  B = sym_part(random_normal(p, p)) from one stream, s = s_A·s_B.
+
+The instances of P1, P4 and P6 are bitwise the reference's.
 """
 from __future__ import annotations
 
@@ -112,11 +117,26 @@ def make_problem(spec: ProblemSpec, device: int = 0):
     if kind == "p1":
         if spec.alpha < 0.0:
             raise P.ParameterError("gen_problem1: alpha must be nonnegative")
-        if spec.alpha != 0.0:
-            raise UnsupportedModel("P1 with alpha > 0 is a nonlinear density model (use "
-                                   "DeviceCallbackModel)")
         a = _operator(spec, device)
         g0 = None
+        if spec.alpha != 0.0:  # gen_problem1 (problems.cpp:208-217)
+            s = P.spectral_norm_estimate_host(a, spec.seed ^ SPECTRAL_SALT)
+            return P.DensityModel(a, spec.p, spec.alpha, s, variant="p1")
+    elif kind == "p6":  # gen_problem6 (problems.cpp:276-285)
+        a = _operator(spec, device)
+        s = P.spectral_norm_estimate_host(a, spec.seed ^ SPECTRAL_SALT)
+        gamma = 2.0 * np.cbrt(3.0 / 3.14159265358979323846)
+        return P.DensityModel(a, spec.p, gamma, s, variant="p6")
+    elif kind == "p4":  # gen_problem4 (problems.cpp:267-274): A then B from one stream
+        n, p = spec.n, spec.p
+        z = P.random_normal(n * n + p * p, 1, spec.seed)[:, 0]
+        an = z[: n * n].reshape((n, n), order="F")
+        bn = z[n * n:].reshape((p, p), order="F")
+        a = np.asfortranarray(0.5 * (an + an.T))
+        b = np.asfortranarray(0.5 * (bn + bn.T))
+        sa = P.spectral_norm_estimate_host(a, spec.seed ^ SPECTRAL_SALT)
+        sb = P.spectral_norm_estimate_host(b, spec.seed ^ (SPECTRAL_SALT + 1))
+        return P.BilinearModel(a, b, sa * sb)
     elif kind in ("p2", "p3"):
         if kind == "p3":  # gen_problem3 = gen_problem2(κ = 0, ζ = 1)
             spec = ProblemSpec(**{**spec.__dict__, "kappa": 0.0, "zeta": 1.0})

@@ -66,15 +66,23 @@ def _save_case(path: str, model, config: P.SolverConfig, x0) -> None:
     d = {"kind": model.kind, "n": model.n, "p": model.p, "s": model.s,
          "x0": np.asfortranarray(x0, dtype=np.float64),
          "config": json.dumps(asdict(config))}
-    if model.kind == P.MODEL_DENSE:
+    if model.kind in (P.MODEL_DENSE, P.MODEL_BILINEAR, P.MODEL_DENSITY):
         if model.location != P.HOST:
             raise P.ParameterError("run_scaling: the model must live in host memory")
         d["a"] = model.a
-        if model.g0 is not None:
+        if model.kind == P.MODEL_DENSE and model.g0 is not None:
             d["g0"] = model.g0
-    else:
+        if model.kind == P.MODEL_BILINEAR:
+            d["b"] = model.b
+        if model.kind == P.MODEL_DENSITY:
+            d["linv"] = model.linv
+            d["coeff"] = model.coeff
+            d["variant"] = model.variant
+    elif model.kind in (P.MODEL_STENCIL, P.MODEL_KOHN_SHAM):
         d["grid"] = np.array(model.grid)
         d["v"] = model.v
+    else:
+        raise P.ParameterError("run_scaling: device-callback models are single-GPU")
     np.savez(path, **d)
 
 
@@ -84,6 +92,11 @@ def _load_case(path: str):
     p, s = int(z["p"]), float(z["s"])
     if kind == P.MODEL_DENSE:
         model = P.QuadraticModel(z["a"], p, s, g0=z["g0"] if "g0" in z else None)
+    elif kind == P.MODEL_BILINEAR:
+        model = P.BilinearModel(z["a"], z["b"], s)
+    elif kind == P.MODEL_DENSITY:
+        model = P.DensityModel(z["a"], p, float(z["coeff"]), s, variant=str(z["variant"]),
+                               linv=z["linv"])
     elif kind == P.MODEL_STENCIL:
         model = P.StencilModel(tuple(z["grid"]), z["v"], p, s)
     else:
@@ -99,6 +112,13 @@ def _local_model(model, r0: int, nr: int):
         g0 = None if model.g0 is None else np.asfortranarray(model.g0[r0:r0 + nr])
         return P.QuadraticModel(np.asfortranarray(model.a[r0:r0 + nr, :]), model.p, model.s,
                                 g0=g0, n=model.n)
+    if model.kind == P.MODEL_BILINEAR:
+        return P.BilinearModel(np.asfortranarray(model.a[r0:r0 + nr, :]), model.b, model.s,
+                               n=model.n)
+    if model.kind == P.MODEL_DENSITY:
+        return P.DensityModel(np.asfortranarray(model.a[r0:r0 + nr, :]), model.p, model.coeff,
+                              model.s, variant=model.variant,
+                              linv=np.asfortranarray(model.linv[r0:r0 + nr, :]), n=model.n)
     cls = P.KohnShamModel if model.kind == P.MODEL_KOHN_SHAM else P.StencilModel
     return cls(model.grid, model.v[r0:r0 + nr], model.p, model.s)
 

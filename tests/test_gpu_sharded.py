@@ -133,16 +133,23 @@ def _scaling_case(pcal, orc, kind):
         v = orc.random_uniform(n, 1)
         m = pcal.StencilModel(grid, v, p, 12.0 + v.max())
         x0 = orc.initial_point_qr(n, p, 7)
-    else:
+    elif kind == "ks":
         grid, p = (16, 8, 10), 6
         n = 16 * 8 * 10
         v = -orc.random_uniform(n, 2)
         m = pcal.KohnShamModel(grid, v, p, 6.0 + np.abs(v).max())
         x0 = orc.initial_point_qr(n, p, 9)
+    else:  # the harness's P4 / P1 (α = 1) / P6 instances
+        from paper_1810_03930_b200 import harness as H
+        spec = {"p4": dict(kind="p4", n=600, p=12, seed=31),
+                "p1": dict(kind="p1", n=640, p=10, alpha=1.0, seed=32),
+                "p6": dict(kind="p6", n=500, p=40, seed=33)}[kind]
+        m = H.make_problem(H.ProblemSpec(**spec))
+        x0 = orc.initial_point_qr(m.n, m.p, spec["seed"] ^ INIT_SALT)
     return m, x0
 
 
-@pytest.mark.parametrize("kind", ["dense", "stencil", "ks"])
+@pytest.mark.parametrize("kind", ["dense", "stencil", "ks", "p4", "p1", "p6"])
 def test_sharded_results_bitwise_identical_across_gpu_counts(pcal, orc, kind):
     """run_scaling's `identical_results` (harness.cpp:131-137, SPEC: bitwise
     identical across thread counts): every row reduction of the sharded path is

@@ -69,13 +69,43 @@ def test_harness_problem_spec_checks_are_host_side():
     with pytest.raises(pcal_errors().ParameterError):
         H.make_problem(H.ProblemSpec(kind="p1", n=10, p=6, alpha=0.0))      # 2p > n
     with pytest.raises(UnsupportedModel):
-        H.make_problem(H.ProblemSpec(kind="p1", n=40, p=4, alpha=1.0))      # nonlinear density
-    with pytest.raises(UnsupportedModel):
-        H.make_problem(H.ProblemSpec(kind="p4", n=40, p=4))
+        H.make_problem(H.ProblemSpec(kind="p5", n=40, p=4))                 # no such kind
+    with pytest.raises(pcal_errors().ParameterError):
+        H.make_problem(H.ProblemSpec(kind="p1", n=40, p=4, alpha=-1.0))
     with pytest.raises(pcal_errors().ParameterError):
         H.make_problem(H.ProblemSpec(kind="p1", n=42, p=4, alpha=0.0, mode="block-tridiag"))
     with pytest.raises(pcal_errors().ParameterError):
         H.make_problem(H.ProblemSpec(kind="p2", n=40, p=4, theta=0.5))
+
+
+def test_density_inverse_is_the_reference_linear_solver():
+    """pcal_density_inverse = LinearSolver (linsolve.cpp:30-102) against e_c, bitwise,
+    on both factorisation paths; a singular L is the reference's generation_error."""
+    import paper_1810_03930_b200 as P
+    g = np.load(os.path.join(GOLD, "reference_linsolve.npz"))
+    for name in ("lu", "chol"):
+        assert not bool(g[name + "_singular"])
+        assert np.array_equal(P.density_inverse(g[name + "_a"]), g[name + "_inv"])
+    assert bool(g["singular_singular"])
+    with pytest.raises(P.ParameterError):
+        P.density_inverse(g["singular_a"])
+
+
+@pytest.mark.parametrize("name,spec", [
+    ("p1_alpha1", dict(kind="p1", n=80, p=5, alpha=1.0, seed=21)),
+    ("p1_block_alpha2", dict(kind="p1", n=60, p=4, alpha=2.0, mode="block-tridiag", seed=22)),
+    ("p4", dict(kind="p4", n=60, p=5, seed=23)),
+    ("p6", dict(kind="p6", n=70, p=4, seed=24)),
+])
+def test_harness_instances_match_reference(name, spec):
+    """gen_problem1 (α > 0) / gen_problem4 / gen_problem6 on the host: the curvature
+    scale the reference echoes in its own run_single report, bitwise."""
+    import json
+    from paper_1810_03930_b200 import harness as H
+    ref = json.load(open(os.path.join(GOLD, f"ref_run_single_{name}.json")))
+    m = H.make_problem(H.ProblemSpec(**spec))
+    assert m.s == ref["config"]["curvature_scale"]
+    assert m.n == spec["n"] and m.p == spec["p"]
 
 
 def test_host_spectral_norm_is_the_reference_one():
