@@ -249,6 +249,12 @@ int pcal_orthonormalize(const double* x, int64_t n, int64_t p, double* q, int32_
 /* ObjectiveModel::evaluate on the device (f and G = ∇f at x). */
 int pcal_evaluate(const pcal_model_desc* model, const double* x, double* f, double* g,
                   int32_t device);
+/* fd_gradient_check (problems.hpp:148-149, problems.cpp:296-325) with the device
+ * evaluation: the worst |fd − g| / (1 + |g|) over up to 50 distinct seeded
+ * coordinates (reference default seed 0x5EEDC0DE), central differences with
+ * step h·(1 + |x_ij|).  h must be positive. */
+int pcal_fd_gradient_check(const pcal_model_desc* model, const double* x, double h, uint64_t seed,
+                           int32_t device, double* worst);
 /* pcal_step (solver.cpp:264-307): per-column normalized proximal step. */
 int pcal_pcal_step(const double* x, const double* grad_l, int64_t n, int64_t p, double eta,
                    double* out, int64_t* degenerate_columns, int32_t device);

@@ -251,17 +251,18 @@ def model_eval_cases(R: Reference) -> None:
     L = R.lib
     dp = C.POINTER(C.c_double)
     L.ref_evaluate_problem.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_double, C.c_int,
-                                       C.c_uint64, dp, dp, dp]
+                                       C.c_uint64, dp, dp, dp, dp]
     g = {}
     for name, (kind, n, p, alpha, bt, seed) in MODEL_EVAL_CASES.items():
         x = np.asfortranarray(R.random_normal(n, p, 300 + seed))
-        f = C.c_double()
+        f, fd = C.c_double(), C.c_double()
         gr = np.zeros((n, p), order="F")
         assert L.ref_evaluate_problem(kind, n, p, alpha, bt, seed, x.ctypes.data_as(dp),
-                                      C.byref(f), gr.ctypes.data_as(dp)) == 0, name
+                                      C.byref(f), gr.ctypes.data_as(dp), C.byref(fd)) == 0, name
         g[name + "_x"] = x
         g[name + "_f"] = f.value
         g[name + "_g"] = gr
+        g[name + "_fd"] = fd.value  # fd_gradient_check(model, x) with the reference defaults
     np.savez_compressed(os.path.join(OUT, "reference_models.npz"), **g)
     print("wrote reference_models.npz")
 

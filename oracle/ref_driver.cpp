@@ -458,7 +458,8 @@ int ref_linear_inverse(const double* a, std::int64_t n, double* out) {
 // gen_problem{1,4,6}(…, seed) evaluated at x (problems.cpp:130-206): pins the
 // device Bilinear / Density models.  kind 1 = P1 (alpha), 4 = P4, 6 = P6.
 int ref_evaluate_problem(int kind, std::int64_t n, std::int64_t p, double alpha, int block_tridiag,
-                         std::uint64_t seed, const double* x, double* f, double* g) {
+                         std::uint64_t seed, const double* x, double* f, double* g,
+                         double* fd) {
   return guarded([&] {
     const OperatorMode mode = block_tridiag ? OperatorMode::BlockTridiag : OperatorMode::RandomSym;
     std::unique_ptr<ObjectiveModel> m =
@@ -468,6 +469,7 @@ int ref_evaluate_problem(int kind, std::int64_t n, std::int64_t p, double alpha,
     const Evaluation ev = m->evaluate(from_ptr(x, n, p), 1);
     *f = ev.value;
     std::memcpy(g, ev.gradient.data(), sizeof(double) * (size_t)(n * p));
+    if (fd) *fd = fd_gradient_check(*m, from_ptr(x, n, p));  // defaults h = 1e-5, seed 0x5eedc0de
     return 0;
   });
 }

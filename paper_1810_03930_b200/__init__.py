@@ -32,7 +32,7 @@ __all__ = [
     "CategoryTimers", "QuadraticModel", "StencilModel", "KohnShamModel", "make_quadratic",
     "BilinearModel", "DensityModel", "density_inverse",
     "solve", "Session", "gram", "matmul_at_b", "matmul", "orthonormalize", "pcal_step",
-    "spectral_norm_estimate", "initial_point", "evaluate", "random_normal", "random_uniform",
+    "spectral_norm_estimate", "initial_point", "evaluate", "fd_gradient_check", "random_normal", "random_uniform",
     "gen_dense_operator", "flops_estimate", "ParameterError", "DimensionError", "RankError",
     "DivergenceError", "EvaluationError", "NativeUnavailable", "lib", "LIB_PATH",
 ]
@@ -148,6 +148,7 @@ def lib() -> C.CDLL:
     L.pcal_gram.argtypes = [vp, i64, i64, vp, i32]
     L.pcal_orthonormalize.argtypes = [vp, i64, i64, vp, i32]
     L.pcal_evaluate.argtypes = [C.POINTER(_Model), vp, C.POINTER(dbl), vp, i32]
+    L.pcal_fd_gradient_check.argtypes = [C.POINTER(_Model), vp, dbl, u64, i32, C.POINTER(dbl)]
     L.pcal_pcal_step.argtypes = [vp, vp, i64, i64, dbl, vp, C.POINTER(i64), i32]
     L.pcal_spectral_norm_estimate.argtypes = [vp, i64, u64, C.POINTER(dbl), i32]
     L.pcal_flops_estimate.argtypes = [i64, i64]
@@ -628,6 +629,17 @@ def evaluate(model: _ModelBase, x, device: int = 0) -> tuple:
     _check(lib().pcal_evaluate(C.byref(cm), _ptr(x), C.byref(f), _ptr(g), device))
     del keep
     return f.value, g
+
+
+def fd_gradient_check(model: _ModelBase, x, h: float = 1e-5, seed: int = 0x5EEDC0DE,
+                      device: int = 0) -> float:
+    """fd_gradient_check (problems.cpp:296-325) through the device evaluation."""
+    x = _f64(x)
+    cm, keep = model._c()
+    w = C.c_double()
+    _check(lib().pcal_fd_gradient_check(C.byref(cm), _ptr(x), h, seed, device, C.byref(w)))
+    del keep
+    return w.value
 
 
 def spectral_norm_estimate(a, seed: int, device: int = 0) -> float:

@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <set>
 #include <thread>
 #include <vector>
 
@@ -58,6 +59,14 @@ struct Rng {
 }  // namespace
 
 namespace pcal {
+
+void host_fd_coordinates(int64_t total, uint64_t seed, int64_t want, int64_t* out) {
+  Rng rng(seed);
+  std::set<int64_t> coords;
+  while ((int64_t)coords.size() < want) coords.insert((int64_t)(rng.next() % (uint64_t)total));
+  int64_t k = 0;
+  for (int64_t c : coords) out[k++] = c;
+}
 
 void host_random_normal(int64_t count, uint64_t seed, double* out, int threads) {
   Rng r(seed);

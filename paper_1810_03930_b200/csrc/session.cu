@@ -2413,48 +2413,95 @@ int pcal_initial_point(int64_t n, int64_t p, int32_t mode, double sigma_lower, u
   });
 }
 
+// One evaluation of the session's model at its pair-0 iterate: f (and G into g
+// when non-null).  Throws evaluation_error on a non-finite f or G.
+static double evaluate_pair0(pcal_session* s, double* g) {
+  LaunchScope ls(&s->launches);
+  k_zero_i32<<<1, 1, 0, s->stream>>>(s->bad, nullptr);
+  launched("k_zero_i32");
+  launch_gradient(s, 0, nullptr);
+  launch_colsums(s, s->fpart.p, s->nrb_f, nullptr, nullptr, 0, Fcol(s, 0), nullptr, nullptr,
+                 nullptr);
+  FinishArgs fa{};
+  fa.fcol = Fcol(s, 0);
+  fa.kcol = Kcol(s, 0);
+  fa.cpart = s->cpart.p;
+  fa.ncp = 0;
+  fa.spart = s->spart.p;
+  fa.nsp = s->sp_blocks;
+  fa.model = s->model.kind;
+  fa.p = s->p;
+  fa.mode = 2;
+  fa.trace = s->trace.p;
+  fa.bad = s->bad;
+  fa.c_xc = s->c_xc;
+  fa.fdev = s->fdev.p;
+  fa.coeff = s->model.coeff;
+  fa.p6 = s->model.density_variant == PCAL_DENSITY_P6;
+  k_finish_eval<<<1, 256, 0, s->stream>>>(fa, s->ctl, s->post.p);
+  launched("k_finish_eval");
+  double post[8];
+  PCAL_CUDA(cudaMemcpyAsync(post, s->post.p, sizeof(double) * 5, cudaMemcpyDeviceToHost,
+                            s->stream));
+  if (g) copy_out(s, Pof(s, 0), g);
+  PCAL_CUDA(cudaStreamSynchronize(s->stream));
+  if (post[4] != 0.0) throw Error(PCAL_E_EVALUATION, "evaluate: non-finite objective or gradient");
+  return post[0];
+}
+
+static std::unique_ptr<pcal_session> evaluation_session(const pcal_model_desc* model,
+                                                        const double* x, int32_t device) {
+  pcal_config cfg;
+  pcal_config_default(&cfg);
+  cfg.max_iter = 1;
+  cfg.final_orth = 0;
+  cfg.device = device;
+  pcal_session* raw = nullptr;
+  session_create(model, &cfg, x, PCAL_HOST, &raw, nullptr);
+  return std::unique_ptr<pcal_session>(raw);
+}
+
 int pcal_evaluate(const pcal_model_desc* model, const double* x, double* f, double* g,
                   int32_t device) {
   return guarded([&] {
-    pcal_config cfg;
-    pcal_config_default(&cfg);
-    cfg.max_iter = 1;
-    cfg.final_orth = 0;
-    cfg.device = device;
-    pcal_session* raw = nullptr;
-    session_create(model, &cfg, x, PCAL_HOST, &raw, nullptr);
-    std::unique_ptr<pcal_session> s(raw);
-    LaunchScope ls(&s->launches);
-    k_zero_i32<<<1, 1, 0, s->stream>>>(s->bad, nullptr);
-    launched("k_zero_i32");
-    launch_gradient(s.get(), 0, nullptr);
-    launch_colsums(s.get(), s->fpart.p, s->nrb_f, nullptr, nullptr, 0, Fcol(s.get(), 0), nullptr, nullptr,
-                   nullptr);
-    FinishArgs fa{};
-    fa.fcol = Fcol(s.get(), 0);
-    fa.kcol = Kcol(s.get(), 0);
-    fa.cpart = s->cpart.p;
-    fa.ncp = 0;
-    fa.spart = s->spart.p;
-    fa.nsp = s->sp_blocks;
-    fa.model = s->model.kind;
-    fa.p = s->p;
-    fa.mode = 2;
-    fa.trace = s->trace.p;
-    fa.bad = s->bad;
-    fa.c_xc = s->c_xc;
-    fa.fdev = s->fdev.p;
-    fa.coeff = s->model.coeff;
-    fa.p6 = s->model.density_variant == PCAL_DENSITY_P6;
-    k_finish_eval<<<1, 256, 0, s->stream>>>(fa, s->ctl, s->post.p);
-    launched("k_finish_eval");
-    double post[8];
-    PCAL_CUDA(cudaMemcpyAsync(post, s->post.p, sizeof(double) * 5, cudaMemcpyDeviceToHost,
-                              s->stream));
-    copy_out(s.get(), Pof(s.get(), 0), g);
-    PCAL_CUDA(cudaStreamSynchronize(s->stream));
-    *f = post[0];
-    if (post[4] != 0.0) throw Error(PCAL_E_EVALUATION, "evaluate: non-finite objective or gradient");
+    auto s = evaluation_session(model, x, device);
+    *f = evaluate_pair0(s.get(), g);
+  });
+}
+
+// fd_gradient_check (problems.cpp:296-325) with the device evaluation: up to 50
+// distinct coordinates drawn as Rng(seed).next_u64() % (n·p), visited in
+// ascending order, central differences with step h·(1 + |x_ij|); returns the
+// worst |fd − g| / (1 + |g|).  One session serves every probe.
+int pcal_fd_gradient_check(const pcal_model_desc* model, const double* x, double h, uint64_t seed,
+                           int32_t device, double* worst) {
+  return guarded([&] {
+    if (!model || !x || !worst) throw Error(PCAL_E_PARAMETER, "NULL argument");
+    if (!(h > 0.0)) throw Error(PCAL_E_PARAMETER, "fd_gradient_check: h must be positive");
+    const int64_t n = model->n, p = model->p, total = n * p;
+    auto s = evaluation_session(model, x, device);
+    std::vector<double> g((size_t)total), probe(x, x + total);
+    evaluate_pair0(s.get(), g.data());
+    const int64_t want = std::min<int64_t>(50, total);
+    std::vector<int64_t> coords((size_t)want);
+    pcal::host_fd_coordinates(total, seed, want, coords.data());
+    double w = 0.0;
+    for (int64_t c : coords) {
+      const int64_t i = c % n, j = c / n;
+      const double x0 = x[c];
+      const double hh = h * (1.0 + std::abs(x0));
+      probe[(size_t)c] = x0 + hh;
+      upload_matrix(probe.data(), PCAL_HOST, n, p, Xof(s.get(), 0), s->ld, s->stream);
+      const double fp = evaluate_pair0(s.get(), nullptr);
+      probe[(size_t)c] = x0 - hh;
+      upload_matrix(probe.data(), PCAL_HOST, n, p, Xof(s.get(), 0), s->ld, s->stream);
+      const double fm = evaluate_pair0(s.get(), nullptr);
+      probe[(size_t)c] = x0;
+      const double fd = (fp - fm) / (2.0 * hh);
+      const double gv = g[(size_t)(i + j * n)];
+      w = std::max(w, std::abs(fd - gv) / (1.0 + std::abs(gv)));
+    }
+    *worst = w;
   });
 }
 

@@ -15,7 +15,7 @@ TINY = np.finfo(float).tiny
 
 
 class _QuadCtx(C.Structure):
-    _fields_ = [("a", C.c_void_p), ("lda", C.c_int64)]
+    _fields_ = [("a", C.c_void_p), ("lda", C.c_int64), ("shift", C.c_double)]
 
 
 def _close(a, b, tol, floor=0.0):
@@ -50,6 +50,24 @@ def test_device_callback_model_follows_dense_model(pcal, orc, example):
     rr = pcal.solve(pcal.QuadraticModel(a, p, s), pcal.SolverConfig(), x0)
     assert rc.status == rr.status == "converged"
     assert abs(rc.final_post_orth.fval - rr.final_post_orth.fval) <= 1e-9 * abs(rr.final_post_orth.fval)
+    del a_dev
+
+
+def test_fd_gradient_check_flags_a_perturbed_callback(pcal, example):
+    """fd_gradient_check on a caller-defined model (problems.cpp:296-325): the exact
+    gradient passes at the quadratic tolerance, a gradient shifted by 1e-3 (the
+    reference's PerturbedModel fault injection, test_problems.cpp:27-42,187-194)
+    is flagged at ≥ 5e-4."""
+    import torch
+    n, p = 120, 5
+    a = pcal.gen_dense_operator(n, 8) / np.sqrt(n)
+    a_dev = torch.from_numpy(np.ascontiguousarray(a.T)).cuda()
+    x = pcal.initial_point(n, p, 9)
+    ctx = _QuadCtx(a_dev.data_ptr(), n, 0.0)
+    m = pcal.DeviceCallbackModel(n, p, 1.0, grad=example, ctx=C.addressof(ctx))
+    assert pcal.fd_gradient_check(m, x, 1e-4) <= 1e-9
+    ctx.shift = 1e-3
+    assert pcal.fd_gradient_check(m, x, 1e-4) >= 5e-4
     del a_dev
 
 
