@@ -123,8 +123,13 @@ __global__ void __launch_bounds__(32 * TY)
   }
   double acc = 0.0;
   bool nonfinite = false;
+  // plane z+2 (wrapped) and the f-partial counters advance incrementally: no
+  // integer division on the per-plane path (the kernel is issue-bound otherwise)
+  int zw = (z0 + 2) % nz;
+  int zp_cnt = z0 % zpart, zp_idx = z0 / zpart;
   for (int z = z0; z < z1; ++z) {
-    const double* sa = src(z + 2);
+    const double* sa = hlo ? src(z + 2) : xj + (int64_t)zw * nxy;
+    zw = zw + 1 == nz ? 0 : zw + 1;
     const int64_t pz = (int64_t)z * nxy, pn = pz + nxy;
 #pragma unroll
     for (int k = 0; k < XP; ++k) {
@@ -176,7 +181,7 @@ __global__ void __launch_bounds__(32 * TY)
     }
     // block reduction (fixed order) → one f partial per (tile, zpart planes):
     // once per z-chunk (zpart = zchunk), or per row chunk on the sharded path
-    if ((z + 1) % zpart == 0 || z + 1 == z1) {
+    if (++zp_cnt == zpart || z + 1 == z1) {
       const double v = warp_sum(acc);
       if (lane == 0) sm[ty] = v;
       __syncthreads();
@@ -184,9 +189,13 @@ __global__ void __launch_bounds__(32 * TY)
         double s = 0.0;
 #pragma unroll
         for (int t = 0; t < TY; ++t) s += sm[t];
-        fpart[j * pstride + blockIdx.x + (int64_t)gridDim.x * (z / zpart)] = s;
+        fpart[j * pstride + blockIdx.x + (int64_t)gridDim.x * zp_idx] = s;
       }
       acc = 0.0;
+      if (zp_cnt == zpart) {
+        zp_cnt = 0;
+        ++zp_idx;
+      }
     }
     __syncthreads();
   }
