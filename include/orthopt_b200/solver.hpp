@@ -83,14 +83,24 @@ struct StepsizeRule {
   double eta0 = 0.0;
 };
 enum class MultiplierRule { PlamFormula, PcalFormula };
+// Algorithm (diagnostics.hpp:10), reference order
+enum class Algorithm { Plam = PCAL_ALG_PLAM, Pcal = PCAL_ALG_PCAL, Alm = PCAL_ALG_ALM,
+                       MoptQr = PCAL_ALG_MOPTQR, PlamDa = PCAL_ALG_PLAMDA, PcalDa = PCAL_ALG_PCALDA };
+struct AlmOptions {  // solver.hpp:24-28
+  int inner_max = 500;
+  int outer_max = 50;
+  double inner_tol_scale = 0.1;
+};
 
 struct SolverConfig {
+  Algorithm algorithm = Algorithm::Pcal;
   double beta = -1.0;
   StepsizeRule eta_rule{};
   MultiplierRule multiplier_rule = MultiplierRule::PcalFormula;
   double tol_rel_kkt = 1e-8;
   std::int64_t max_iter = 3000;
   int device = 0;  // replaces the explicit thread count: an explicit GPU ordinal
+  AlmOptions alm{};
   bool final_orth = true;
 };
 
@@ -113,6 +123,8 @@ struct RunReport {
   DenseMatrix stop_iterate;
   DenseMatrix final_x;
   std::int64_t iterations = 0;
+  std::int64_t outer_iterations = 0;  // ALM multiplier updates
+  std::int64_t inner_cap_hits = 0;    // ALM inner loops stopped by a cap
   std::int64_t degenerate_steps = 0;
   double wall_time = 0.0;
   RunStatus status = RunStatus::MaxIter;
@@ -264,6 +276,10 @@ inline RunReport solve(const ObjectiveModel& model, const SolverConfig& config,
     throw dimension_error("solve: start point shape mismatch");
   pcal_config c;
   pcal_config_default(&c);
+  c.algorithm = static_cast<int32_t>(config.algorithm);
+  c.alm_inner_max = config.alm.inner_max;
+  c.alm_outer_max = config.alm.outer_max;
+  c.alm_inner_tol_scale = config.alm.inner_tol_scale;
   c.beta = config.beta;
   c.eta_kind = static_cast<int32_t>(config.eta_rule.kind);
   c.gamma = config.eta_rule.gamma;
@@ -309,6 +325,8 @@ inline RunReport solve(const ObjectiveModel& model, const SolverConfig& config,
     rep.final_x = DenseMatrix();
   }
   rep.iterations = r.iterations;
+  rep.outer_iterations = r.outer_iterations;
+  rep.inner_cap_hits = r.inner_cap_hits;
   rep.degenerate_steps = r.degenerate_steps;
   rep.wall_time = r.wall_time;
   rep.status = r.status == PCAL_STATUS_CONVERGED ? RunStatus::Converged

@@ -86,9 +86,10 @@ typedef int (*pcal_gradient_fn)(const double* x, int64_t ld, int64_t n, int64_t 
 #define PCAL_MULT_PLAM_FORMULA 0
 #define PCAL_MULT_PCAL_FORMULA 1
 
-/* Algorithm (diagnostics.hpp:10), reference enum order.  ALM (2) is not provided. */
+/* Algorithm (diagnostics.hpp:10), reference enum order. */
 #define PCAL_ALG_PLAM 0
 #define PCAL_ALG_PCAL 1
+#define PCAL_ALG_ALM 2         /* alm_outer (solver.cpp:478-624); single GPU */
 #define PCAL_ALG_MOPTQR 3
 #define PCAL_ALG_PLAMDA 4
 #define PCAL_ALG_PCALDA 5
@@ -112,7 +113,7 @@ typedef struct pcal_model_desc {
 } pcal_model_desc;
 
 typedef struct pcal_config {  /* orthopt::SolverConfig (solver.hpp:30-42) */
-  int32_t algorithm;          /* PCAL_ALG_* (PCAL default; PLAM, MOptQR, PLAM-DA, PCAL-DA) */
+  int32_t algorithm;          /* PCAL_ALG_* (PCAL default; PLAM, ALM, MOptQR, PLAM-DA, PCAL-DA) */
   double beta;                /* < 0: PCAL default 1.0 (solver.cpp:120-125) */
   int32_t eta_kind;           /* PCAL_ETA_* */
   double gamma;               /* Constant rule only */
@@ -123,6 +124,9 @@ typedef struct pcal_config {  /* orthopt::SolverConfig (solver.hpp:30-42) */
   int64_t max_iter;
   int32_t final_orth;
   int32_t device;             /* CUDA device ordinal ("threads" is never ambient, SPEC §) */
+  int32_t alm_inner_max;      /* AlmOptions (solver.hpp:24-28): gradient steps per multiplier update */
+  int32_t alm_outer_max;      /*   multiplier updates */
+  double alm_inner_tol_scale; /*   inner target max(scale·tol, scale^k)·kkt0 */
 } pcal_config;
 
 #define PCAL_TRACE_COLS 7     /* iter, fval, kkt_abs, kkt_rel, feas, eta, elapsed (report.hpp:13-21) */
@@ -143,6 +147,8 @@ typedef struct pcal_report {  /* orthopt::RunReport (report.hpp:51-64) */
   int32_t status;             /* PCAL_STATUS_* */
   double beta;                /* resolved penalty */
   double eta0;                /* resolved first stepsize */
+  int64_t outer_iterations;   /* ALM multiplier updates (report.hpp:59) */
+  int64_t inner_cap_hits;     /* ALM inner loops stopped by a cap (report.hpp:60) */
 } pcal_report;
 
 typedef struct pcal_category_timers { /* orthopt::CategoryTimers (report.hpp:66-72), seconds */

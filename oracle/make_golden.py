@@ -142,6 +142,45 @@ def algorithm_cases(R: Reference) -> None:
     print("wrote reference_algorithms.npz")
 
 
+ALM_CASES = {  # name: (instance, AlmOptions(inner_max, outer_max, scale), config overrides)
+    "a40_default": ("a40", (500, 50, 0.1), {}),
+    "a40_tight_caps": ("a40", (6, 5, 0.1), {}),                 # inner caps, outer cap ⇒ MaxIter
+    "a40_budget": ("a40", (500, 50, 0.01), {"max_iter": 25}),  # iteration budget inside a loop
+    "a40_beta0": ("a40", (500, 50, 0.1), {"beta": 0.0, "max_iter": 300}),
+    "c1_caps": ("c1", (7, 50, 0.1), {"max_iter": 60, "threads": 8}),
+}
+
+
+def alm_cases(R: Reference) -> None:
+    """ALM (alm_outer, solver.cpp:478-624) through the reference's solve(): traces,
+    finals, the outer / cap counters — including the reference unit tests'
+    instances (test_solver.cpp:463-498)."""
+    import ctypes as C
+    from oracle.oracle import ALG_ALM
+    L = R.lib
+    L.ref_set_alm.argtypes = [C.c_int, C.c_int, C.c_double]
+    L.ref_last_alm_counts.argtypes = [C.POINTER(C.c_int64)]
+    r = R.random_normal(40, 40, 24)
+    a40 = np.asfortranarray(0.5 * (r + r.T))
+    s40 = R.spectral_norm_estimate(a40, SPECTRAL_SALT)
+    inst = {"a40": (Model(MODEL_DENSE, 40, 5, s40, a=a40), R.initial_point_qr(40, 5, 25)),
+            "c1": (R.dense_trace_min(1000, 20, 1, s=44.26282919872377),
+                   R.initial_point_qr(1000, 20, 1 ^ INIT_SALT))}
+    g = {}
+    for name, (which, (imax, omax, scale), over) in ALM_CASES.items():
+        model, x0 = inst[which]
+        L.ref_set_alm(imax, omax, scale)
+        case, rep = run_case(R, model, x0, algorithm=ALG_ALM, **over)
+        cnt = (C.c_int64 * 2)()
+        L.ref_last_alm_counts(cnt)
+        for k, v in case.items():
+            g[f"{name}_{k}"] = v
+        g[f"{name}_counts"] = np.array([cnt[0], cnt[1]])
+    L.ref_set_alm(500, 50, 0.1)
+    np.savez_compressed(os.path.join(OUT, "reference_alm.npz"), **g)
+    print("wrote reference_alm.npz")
+
+
 def report_io_cases(R: Reference) -> None:
     """The reference's JSON / CSV report text and an OCPROB01 container."""
     import ctypes as C
@@ -354,6 +393,7 @@ if __name__ == "__main__":
     harness_cases(R)
     linsolve_cases(R)
     model_eval_cases(R)
+    alm_cases(R)
     if "--cfg2" in sys.argv:
         cfg2(R)
     if "--grids" in sys.argv:

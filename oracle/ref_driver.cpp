@@ -94,8 +94,14 @@ int guarded(F&& f) {
   }
 }
 
+// AlmOptions for the next solves and the ALM counters of the last one
+// (orc_config / orc_report carry neither; set through ref_set_alm).
+AlmOptions g_alm{};
+std::int64_t g_alm_counts[2] = {0, 0};
+
 SolverConfig to_config(const orc_config* c) {
   SolverConfig cfg;
+  cfg.alm = g_alm;
   cfg.algorithm = static_cast<Algorithm>(c->algorithm);
   cfg.beta = c->beta;
   cfg.eta_rule.kind = static_cast<StepsizeRule::Kind>(c->eta_kind);
@@ -308,6 +314,8 @@ int ref_solve(void* model, const orc_config* c, const double* x0, orc_report* r,
     auto* m = static_cast<ObjectiveModel*>(model);
     CategoryTimers t;
     RunReport rep = solve(*m, to_config(c), from_ptr(x0, m->n(), m->p()), timers ? &t : nullptr);
+    g_alm_counts[0] = rep.outer_iterations;
+    g_alm_counts[1] = rep.inner_cap_hits;
     r->trace_len = static_cast<std::int64_t>(rep.trace.size());
     for (size_t i = 0; i < rep.trace.size(); ++i) {
       double* row = r->trace + i * ORC_TRACE_COLS;
@@ -472,6 +480,18 @@ int ref_evaluate_problem(int kind, std::int64_t n, std::int64_t p, double alpha,
     if (fd) *fd = fd_gradient_check(*m, from_ptr(x, n, p));  // defaults h = 1e-5, seed 0x5eedc0de
     return 0;
   });
+}
+
+// AlmOptions of the following ref_solve calls (solver.hpp:24-28).
+void ref_set_alm(int inner_max, int outer_max, double inner_tol_scale) {
+  g_alm.inner_max = inner_max;
+  g_alm.outer_max = outer_max;
+  g_alm.inner_tol_scale = inner_tol_scale;
+}
+// RunReport::outer_iterations / inner_cap_hits of the last ref_solve.
+void ref_last_alm_counts(std::int64_t* out) {
+  out[0] = g_alm_counts[0];
+  out[1] = g_alm_counts[1];
 }
 
 }  // extern "C"

@@ -29,7 +29,7 @@ import numpy as np
 
 __all__ = [
     "SolverConfig", "StepsizeRule", "MultiplierRule", "RunReport", "FinalMetrics",
-    "CategoryTimers", "QuadraticModel", "StencilModel", "KohnShamModel", "make_quadratic",
+    "CategoryTimers", "AlmOptions", "QuadraticModel", "StencilModel", "KohnShamModel", "make_quadratic",
     "BilinearModel", "DensityModel", "density_inverse",
     "solve", "Session", "gram", "matmul_at_b", "matmul", "orthonormalize", "pcal_step",
     "spectral_norm_estimate", "initial_point", "evaluate", "fd_gradient_check", "random_normal", "random_uniform",
@@ -94,7 +94,9 @@ class _Config(C.Structure):
                 ("gamma", C.c_double), ("eta_min", C.c_double), ("eta_max", C.c_double),
                 ("eta0", C.c_double), ("multiplier_rule", C.c_int32),
                 ("tol_rel_kkt", C.c_double), ("max_iter", C.c_int64),
-                ("final_orth", C.c_int32), ("device", C.c_int32)]
+                ("final_orth", C.c_int32), ("device", C.c_int32),
+                ("alm_inner_max", C.c_int32), ("alm_outer_max", C.c_int32),
+                ("alm_inner_tol_scale", C.c_double)]
 
 
 class _Report(C.Structure):
@@ -103,7 +105,8 @@ class _Report(C.Structure):
                 ("has_post", C.c_int32), ("stop_x", _dp), ("final_x", _dp), ("has_x", C.c_int32),
                 ("iterations", C.c_int64), ("degenerate_steps", C.c_int64),
                 ("wall_time", C.c_double), ("status", C.c_int32), ("beta", C.c_double),
-                ("eta0", C.c_double)]
+                ("eta0", C.c_double), ("outer_iterations", C.c_int64),
+                ("inner_cap_hits", C.c_int64)]
 
 
 class _Timers(C.Structure):
@@ -231,9 +234,17 @@ class StepsizeRule:
 
 
 @dataclass
+class AlmOptions:
+    """AlmOptions (solver.hpp:24-28)."""
+    inner_max: int = 500          # gradient steps per multiplier update
+    outer_max: int = 50           # multiplier updates
+    inner_tol_scale: float = 0.1  # inner target: max(scale·tol, scale^k)·kkt0
+
+
+@dataclass
 class SolverConfig:
     """orthopt::SolverConfig; ``device`` replaces the explicit thread count.
-    ``algorithm``: "pcal" (default), "plam", "moptqr", "plam-da", "pcal-da"."""
+    ``algorithm``: "pcal" (default), "plam", "alm", "moptqr", "plam-da", "pcal-da"."""
     beta: float = -1.0
     eta_rule: StepsizeRule = field(default_factory=StepsizeRule)
     multiplier_rule: int = MultiplierRule.PCAL_FORMULA
@@ -242,17 +253,19 @@ class SolverConfig:
     final_orth: bool = True
     device: int = 0
     algorithm: str = "pcal"
+    alm: AlmOptions = field(default_factory=AlmOptions)
 
-    ALGORITHMS = {"plam": 0, "pcal": 1, "moptqr": 3, "plam-da": 4, "pcal-da": 5}
+    ALGORITHMS = {"plam": 0, "pcal": 1, "alm": 2, "moptqr": 3, "plam-da": 4, "pcal-da": 5}
 
     def _c(self) -> _Config:
         if self.algorithm not in self.ALGORITHMS:
-            raise ParameterError(f"algorithm {self.algorithm!r} is not provided "
-                                 f"({', '.join(self.ALGORITHMS)}; ALM is out of scope)")
+            raise ParameterError(f"unknown algorithm {self.algorithm!r} "
+                                 f"({', '.join(self.ALGORITHMS)})")
         r = self.eta_rule
         return _Config(self.ALGORITHMS[self.algorithm], self.beta, r.kind, r.gamma, r.eta_min, r.eta_max, r.eta0,
                        self.multiplier_rule, self.tol_rel_kkt, self.max_iter,
-                       int(self.final_orth), self.device)
+                       int(self.final_orth), self.device, int(self.alm.inner_max),
+                       int(self.alm.outer_max), float(self.alm.inner_tol_scale))
 
 
 @dataclass
@@ -283,6 +296,8 @@ class RunReport:
     status: str
     beta: float
     eta0: float
+    outer_iterations: int = 0      # ALM multiplier updates (report.hpp:59)
+    inner_cap_hits: int = 0        # ALM inner loops stopped by a cap (report.hpp:60)
 
 
 # --------------------------------------------------------------------------- #
@@ -442,7 +457,8 @@ def _report_from(rep: _Report, trace: np.ndarray, stop_x, final_x) -> RunReport:
                      stop_iterate=stop_x if rep.has_x else None,
                      final_x=final_x if rep.has_x else None, iterations=rep.iterations,
                      degenerate_steps=rep.degenerate_steps, wall_time=rep.wall_time,
-                     status=STATUS[rep.status], beta=rep.beta, eta0=rep.eta0)
+                     status=STATUS[rep.status], beta=rep.beta, eta0=rep.eta0,
+                     outer_iterations=rep.outer_iterations, inner_cap_hits=rep.inner_cap_hits)
 
 
 def _new_report(n: int, p: int, max_iter: int, want_x: bool = True) -> tuple:

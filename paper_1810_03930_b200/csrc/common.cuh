@@ -91,6 +91,21 @@ struct Ctl {
   double tol, gamma, eta_min, eta_max;
   int32_t eta_kind;
   int32_t mult_rule;
+  // stepsize memory: stepsize_select sees st.iter = iter − iter_base (0 except for
+  // ALM, whose SolverState restarts with every inner loop, solver.cpp:540-543)
+  int64_t iter_base;
+  // ALM (alm_outer, solver.cpp:478-624); alm = 0 for every other algorithm
+  int32_t alm;
+  int32_t alm_phase;   // next action: 0 = inner step, 1 = multiplier update
+  int32_t alm_met;     // the inner loop met its tolerance (else it hit a cap)
+  int32_t alm_copy;    // the iterate just evaluated is the inner loop's best so far
+  int64_t alm_inner;   // iterates tested in the current inner loop
+  int64_t alm_outer;   // multiplier updates (RunReport::outer_iterations)
+  int64_t alm_caps;    // inner loops stopped by a cap (RunReport::inner_cap_hits)
+  int64_t alm_flips;   // multiplier updates performed (each moves the iterate to the other pair)
+  int64_t alm_inner_max, alm_outer_max, max_iter;
+  double alm_best, alm_tol_scale;
+  double best_f, best_kkt, best_feas;  // data of the best iterate
 };
 
 __device__ __forceinline__ uint64_t globaltimer_ns() {

@@ -251,14 +251,14 @@ __device__ __forceinline__ void epilogue(const GemmArgs& g, int tm, int tn, int 
             const double pv = (e.p_from_g ? gv[b][mt] : kkt) + e.beta * acc[mt][nt][1];
             e.G[idx] = pv;
             ks += kkt * kkt;
-            ds += xv[b][mt] * pv;
+            ds += (e.d_sq ? pv : xv[b][mt]) * pv;
           } else if (row < e.n && j < e.p) {
             const double g0 = e.G[idx];
             const double kkt = g0 - acc[mt][nt][0];
             const double pv = (e.p_from_g ? g0 : kkt) + e.beta * acc[mt][nt][1];
             e.G[idx] = pv;
             ks += kkt * kkt;
-            ds += e.X[idx] * pv;
+            ds += (e.d_sq ? pv : e.X[idx]) * pv;
           }
         }
 #pragma unroll

@@ -28,6 +28,7 @@ struct EpiParams {
   int64_t n, p;
   int64_t pstride;   // column stride of the partial arrays: part[col·pstride + rb]
   int32_t p_from_g;  // EPI_XM: P = G + β·acc1 (dual-ascent / MOptQR) instead of kkt + β·acc1
+  int32_t d_sq;      // EPI_XM: dpart accumulates Σ P² (ALM's ‖∇L‖) instead of Σ X∘P
 };
 
 struct GemmArgs {

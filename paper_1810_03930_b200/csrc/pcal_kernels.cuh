@@ -66,7 +66,9 @@ __global__ void k_small_pxp(const double* __restrict__ gr, int64_t pp, int64_t p
     } else if (mode == MC_DA) {
       // Λ is updated elementwise from the upper triangle's value, so it stays
       // exactly symmetric (SquareSymmetric::add_scaled, kernels.cpp:38-47)
-      double l = lam_init ? w : lam[k + j * p] + -beta * c;
+      // lam_init: 1 = Λ ← W (start point), 0 = dual-ascent update, 2 = keep
+      // (ALM inner iterations: Λ changes only at the outer updates)
+      double l = lam_init == 1 ? w : lam_init == 2 ? lam[k + j * p] : lam[k + j * p] + -beta * c;
       lam[k + j * p] = l;
       m = beta * c - l;
     } else {
@@ -88,7 +90,7 @@ __global__ void k_bb_partials(const double* __restrict__ x, const double* __rest
                               const double* __restrict__ xp, const double* __restrict__ pgp,
                               const double* __restrict__ d, const double* __restrict__ dp,
                               int64_t ld, int64_t p, double* __restrict__ part, const Ctl* ctl) {
-  if (ctl->done || ctl->iter == 0 || !ctl->have_prev) return;
+  if (ctl->done || ctl->iter == ctl->iter_base || !ctl->have_prev) return;
   __shared__ double sm[kStreamThreads / 32];
   double ss = 0.0, sy = 0.0, yy = 0.0;
   const int64_t half = ld / 2;  // ld is a multiple of 16: double2 vectors never straddle columns
@@ -145,7 +147,7 @@ __device__ __forceinline__ double select_eta(const Ctl* c, double ss, double sy,
   switch (c->eta_kind) {
     case 2: v = bb1; break;
     case 3: v = bb2; break;
-    case 4: v = (c->iter % 2 == 1) ? bb1 : bb2; break;
+    case 4: v = ((c->iter - c->iter_base) % 2 == 1) ? bb1 : bb2; break;
     case 1: v = (ss == 0.0) ? fallback : sqrt(yy) / sqrt(ss); break;
     default: break;
   }
@@ -159,7 +161,7 @@ __global__ void __launch_bounds__(kStreamThreads) k_eta(Ctl* ctl, const double* 
   if (ctl->done) return;
   __shared__ double sm[kStreamThreads / 32];
   Ctl* c = ctl;
-  const bool need = c->eta_kind != 0 && c->have_prev && c->iter != 0;
+  const bool need = c->eta_kind != 0 && c->have_prev && c->iter != c->iter_base;
   double ss = 0.0, sy = 0.0, yy = 0.0;
   if (need) {
     double a = 0.0, b = 0.0, d = 0.0;
@@ -245,7 +247,7 @@ __global__ void k_bb_chunk(const double* __restrict__ x, const double* __restric
                            const double* __restrict__ d, const double* __restrict__ dp, int64_t n,
                            int64_t ld, int64_t p, int64_t chunk, double* __restrict__ out,
                            const Ctl* ctl) {
-  if (ctl->done || ctl->iter == 0 || !ctl->have_prev) return;
+  if (ctl->done || ctl->iter == ctl->iter_base || !ctl->have_prev) return;
   __shared__ double sm[kStreamThreads / 32];
   const int64_t j = blockIdx.y, c = blockIdx.x;
   const int64_t r0 = c * chunk, r1 = min(n, r0 + chunk);
@@ -462,7 +464,7 @@ __device__ __forceinline__ bool step_phase(const StepArgs& a, Ctl* ctl) {
   __shared__ double s_eta;
   __shared__ double s_inv;
   __shared__ int s_deg;
-  const bool need = ctl->eta_kind != 0 && ctl->have_prev && ctl->iter != 0;
+  const bool need = ctl->eta_kind != 0 && ctl->have_prev && ctl->iter != ctl->iter_base;
   // ---- phase 1: stepsize inner products (k_bb_partials)
   if (need) {
     double ss = 0.0, sy = 0.0, yy = 0.0;

@@ -289,12 +289,39 @@ struct FinishArgs {
   const double* fdev;   // device-callback models: f(X) as written by the callback
   double coeff;         // density models: α (P1) / γ (P6)
   int32_t p6;           // density models: the P6 term
+  const double* glcol;  // ALM: Σ_i P_ij² per column (‖∇L‖² = their sum), else null
 };
+
+// ALM inner-loop bookkeeping for the iterate just evaluated (alm_outer,
+// solver.cpp:544-561): it is tested while the inner loop and the iteration
+// budget allow — best ‖∇L‖ so far (its X is then copied to the best buffer),
+// tolerance max(scale·tol, scale^(outer+1))·kkt0 — else the loop ends at a cap.
+__device__ void alm_test(Ctl* c, double f, double kkt, double feas, double gl2) {
+  c->alm_copy = 0;
+  if (c->alm_inner < c->alm_inner_max && c->iter < c->max_iter) {
+    const double gl = sqrt(gl2);
+    if (gl < c->alm_best) {
+      c->alm_best = gl;
+      c->alm_copy = 1;
+      c->best_f = f;
+      c->best_kkt = kkt;
+      c->best_feas = feas;
+    }
+    const double sc = c->alm_tol_scale;
+    const double tk = fmax(sc * c->tol, pow(sc, (double)(c->alm_outer + 1))) *
+                      (c->kkt_den > 0.0 ? c->kkt_den : 1.0);
+    c->alm_met = gl <= tk;
+    c->alm_phase = c->alm_met ? 1 : 0;
+  } else {
+    c->alm_met = 0;
+    c->alm_phase = 1;
+  }
+}
 
 // Thread-0 tail of an evaluation: objective assembly, failure flags, trace
 // row, stopping test (solver.cpp:348-359,434-438,460-471).
 __device__ void finish_record(const FinishArgs& a, Ctl* ctl, double* post, double f1, double k2,
-                              double c2, double vr, double rh, double ex) {
+                              double c2, double vr, double rh, double ex, double gl2 = 0.0) {
   const bool bad_flag = a.flags ? a.flags[1] > 0.0 : *a.bad != 0;
   *a.bad = 0;  // reset for the next evaluation
   if (a.flags && a.mode == 0 && a.flags[0] > 0.0) {  // some rank's pcal_step diverged
@@ -328,6 +355,13 @@ __device__ void finish_record(const FinishArgs& a, Ctl* ctl, double* post, doubl
     if (a.mode == 0) ctl->degenerate += ctl->step_deg;
     return;
   }
+  if (a.mode == 3) {  // ALM multiplier update: a new inner loop starts here (no trace row)
+    ctl->f = f;
+    ctl->kkt_abs = kkt;
+    ctl->feas = feas;
+    alm_test(ctl, f, kkt, feas, gl2);
+    return;
+  }
   int64_t k;
   double eta;
   if (a.mode == 1) {
@@ -357,6 +391,32 @@ __device__ void finish_record(const FinishArgs& a, Ctl* ctl, double* post, doubl
   ctl->feas = feas;
   ctl->rel = rel;
   if (rel < ctl->tol) ctl->done = 1;
+  if (ctl->alm && !ctl->done) {
+    if (a.mode == 0) ++ctl->alm_inner;
+    alm_test(ctl, f, kkt, feas, gl2);
+  }
+}
+
+// ALM outer step (solver.cpp:562-574), before the multiplier update's
+// evaluation: the inner loop's iterate (its best one after a cap) has been
+// copied to the other pair; the stepsize memory restarts with the next loop.
+__global__ void k_alm_boundary(Ctl* c) {
+  if (c->done) return;
+  if (!c->alm_met) {
+    ++c->alm_caps;
+    c->f = c->best_f;
+    c->kkt_abs = c->best_kkt;
+    c->feas = c->best_feas;
+  }
+  ++c->alm_outer;
+  ++c->alm_flips;
+  c->alm_inner = 0;
+  c->alm_best = INFINITY;
+  c->alm_copy = 0;
+  c->have_prev = 0;
+  c->eta_prev = 0.0;
+  c->iter_base = c->iter;
+  if (c->alm_outer >= c->alm_outer_max || c->iter >= c->max_iter) c->done = 4;  // MaxIter
 }
 
 __global__ void __launch_bounds__(256) k_finish_eval(FinishArgs a, Ctl* ctl,
@@ -381,8 +441,12 @@ __global__ void __launch_bounds__(256) k_finish_eval(FinishArgs a, Ctl* ctl,
   const double vr = block_sum<256>(pv, sm);
   const double rh = block_sum<256>(pr, sm);
   const double ex = block_sum<256>(pe, sm);
+  double pg = 0.0;
+  if (a.glcol)
+    for (int64_t j = threadIdx.x; j < a.p; j += blockDim.x) pg += a.glcol[j];
+  const double gl2 = block_sum<256>(pg, sm);
   if (threadIdx.x != 0) return;
-  finish_record(a, ctl, post, f1, k2, c2, vr, rh, ex);
+  finish_record(a, ctl, post, f1, k2, c2, vr, rh, ex, gl2);
 }
 
 }  // namespace pcal
@@ -469,6 +533,7 @@ struct pcal_session {
   // model data
   pcal::DevBuf A, g0, V, u, rho, h, tmpa, tmpb, qx, qy, qz, lx, ly, lz, spart;
   pcal::DevBuf Bm, tb, Minv;  // bilinear B (pp×pp) and A·X; density L⁻¹ rows
+  pcal::DevBuf glcol, bestx;  // ALM: column sums of P², the inner loop's best X
   pcal::DevBuf fdev;  // device-callback models: f(X)
   int64_t ldA = 0;
   // iteration state
@@ -643,6 +708,10 @@ static void launch_colsums(pcal_session* s, const double* fp, int64_t nrb_f, con
   a.nrows[2] = nrb_kd;
   a.stride[2] = s->pstride_xm;
   a.out[2] = dcol;
+  if (dp && s->alg == PCAL_ALG_ALM) {  // ALM: ‖∇L‖² column sums; d stays 0
+    a.in[2] = dp;
+    a.out[2] = s->glcol.p;
+  }
   k_colsum3<<<dim3((unsigned)s->p, 3), kStreamThreads, 0, s->stream>>>(a, ctl);
   launched("k_colsum3");
 }
@@ -822,12 +891,16 @@ static void launch_eval(pcal_session* s, int b, int mode, const Ctl* ctl_guard) 
   launch_gemm(s->gram[b], st);
   if (s->repro) gram_reduce(s, s->gram[b], 0);  // C1
   {
-    const int mc = (s->alg == PCAL_ALG_PLAMDA || s->alg == PCAL_ALG_PCALDA) ? MC_DA
+    const bool alm = s->alg == PCAL_ALG_ALM;
+    // Λ: W at the start point; dual ascent updates it every evaluation, ALM only
+    // at its multiplier updates (mode 3)
+    const int lam_mode = mode == 1 ? 1 : alm ? (mode == 3 ? 0 : 2) : 0;
+    const int mc = (s->alg == PCAL_ALG_PLAMDA || s->alg == PCAL_ALG_PCALDA || alm) ? MC_DA
                    : s->alg == PCAL_ALG_MOPTQR                               ? MC_MOPTQR
                                                                              : MC_PCAL;
     k_small_pxp<<<s->cp_blocks, kStreamThreads, 0, st>>>(s->gr.p, s->pp, s->p, s->mcat.p, s->pp,
                                                          s->cpart.p, mc, s->beta, s->lam.p,
-                                                         mode == 1 ? 1 : 0, ctl_guard,
+                                                         lam_mode, ctl_guard,
                                                          s->sym_gx ? 1 : 0);
   }
   launched("k_small_pxp");
@@ -880,6 +953,7 @@ static void launch_eval(pcal_session* s, int b, int mode, const Ctl* ctl_guard) 
   fa.fdev = s->fdev.p;
   fa.coeff = s->model.coeff;
   fa.p6 = s->model.density_variant == PCAL_DENSITY_P6;
+  fa.glcol = s->alg == PCAL_ALG_ALM ? s->glcol.p : nullptr;
   k_finish_eval<<<1, 256, 0, st>>>(fa, s->ctl, s->post.p);
   launched("k_finish_eval");
   mark(s, 4);
@@ -1149,7 +1223,8 @@ static void build_plans(pcal_session* s) {
       e.dpart = s->dpart.p;
       e.pstride = s->pstride_xm;
       // PCAL/PLAM: P = (G − XW) + β·XC; dual ascent / MOptQR: P = G + X·M
-      e.p_from_g = (s->alg == PCAL_ALG_PLAMDA || s->alg == PCAL_ALG_PCALDA ||
+      e.d_sq = s->alg == PCAL_ALG_ALM;
+      e.p_from_g = (s->alg == PCAL_ALG_PLAMDA || s->alg == PCAL_ALG_PCALDA || e.d_sq ||
                     s->alg == PCAL_ALG_MOPTQR);
       e.beta = e.p_from_g ? 1.0 : s->beta;
       e.n = n;
@@ -1359,6 +1434,11 @@ static void alloc_state(pcal_session* s) {
   s->xpart.alloc((size_t)s->up_nchunks * p);
   s->nrm.alloc((size_t)2 * p);
   s->post.alloc(8);
+  if (s->alg == PCAL_ALG_ALM) {
+    s->glcol.alloc((size_t)p);
+    s->glcol.zero(st);
+    s->bestx.alloc((size_t)ld * pp);
+  }
   s->orth_b.alloc((size_t)pp * pp);
   s->orth_l.alloc((size_t)pp * pp);
   s->orth_t.alloc((size_t)pp * pp);
@@ -1478,6 +1558,12 @@ static void init_ctl(pcal_session* s) {
   c.eta_max = s->cfg.eta_max;
   c.eta_kind = s->cfg.eta_kind;
   c.mult_rule = s->cfg.multiplier_rule;
+  c.max_iter = s->cfg.max_iter;
+  c.alm = s->alg == PCAL_ALG_ALM;
+  c.alm_inner_max = s->cfg.alm_inner_max;
+  c.alm_outer_max = s->cfg.alm_outer_max;
+  c.alm_tol_scale = s->cfg.alm_inner_tol_scale;
+  c.alm_best = INFINITY;
   *s->h_ctl = c;
   PCAL_CUDA(cudaMemcpyAsync(s->ctl, s->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, s->stream));
 }
@@ -1487,8 +1573,8 @@ __global__ void k_set_t0(Ctl* c) { c->t0_ns = globaltimer_ns(); }
 static void validate(const pcal_config* c) {  // SolverConfig::validate (solver.cpp:106-118)
   if (c->algorithm != PCAL_ALG_PCAL && c->algorithm != PCAL_ALG_PLAM &&
       c->algorithm != PCAL_ALG_MOPTQR && c->algorithm != PCAL_ALG_PLAMDA &&
-      c->algorithm != PCAL_ALG_PCALDA)
-    throw Error(PCAL_E_UNSUPPORTED, "algorithm not provided (PCAL, PLAM, MOptQR, PLAM-DA, PCAL-DA)");
+      c->algorithm != PCAL_ALG_PCALDA && c->algorithm != PCAL_ALG_ALM)
+    throw Error(PCAL_E_UNSUPPORTED, "unknown algorithm");
   if (c->beta >= 0.0 && !std::isfinite(c->beta))
     throw Error(PCAL_E_PARAMETER, "SolverConfig: beta must be finite");
   if (!(c->tol_rel_kkt > 0.0))
@@ -1501,6 +1587,8 @@ static void validate(const pcal_config* c) {  // SolverConfig::validate (solver.
   if (c->eta_kind < 0 || c->eta_kind > 4) throw Error(PCAL_E_PARAMETER, "unknown stepsize rule");
   if (c->multiplier_rule != PCAL_MULT_PCAL_FORMULA && c->multiplier_rule != PCAL_MULT_PLAM_FORMULA)
     throw Error(PCAL_E_PARAMETER, "unknown multiplier rule");
+  if (c->alm_inner_max < 1 || c->alm_outer_max < 1)
+    throw Error(PCAL_E_PARAMETER, "SolverConfig: ALM iteration caps must be at least 1");
 }
 
 static double clamp_eta_h(const pcal_config* c, double v) {
@@ -1641,7 +1729,7 @@ static void launch_small(pcal_session* s, int iters) {
 static void setup_small(pcal_session* s) {
   const char* off = getenv("PCAL_NO_SMALL_KERNEL");
   if ((off && off[0] == '1') || s->comm || s->model.kind != PCAL_MODEL_DENSE ||
-      s->p > kSmallP || s->n > 8192 || s->alg == PCAL_ALG_MOPTQR)
+      s->p > kSmallP || s->n > 8192 || s->alg == PCAL_ALG_MOPTQR || s->alg == PCAL_ALG_ALM)
     return;
   int coop = 0, per_sm = 0;
   PCAL_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, s->device));
@@ -1739,6 +1827,8 @@ void session_create(const pcal_model_desc* model, const pcal_config* config, con
               s->alg != PCAL_ALG_MOPTQR && !getenv("PCAL_FULL_GX");
   if (comm && s->alg == PCAL_ALG_MOPTQR)
     throw Error(PCAL_E_UNSUPPORTED, "MOptQR is single-GPU (its MGS2 fallback is not sharded)");
+  if (comm && s->alg == PCAL_ALG_ALM)
+    throw Error(PCAL_E_UNSUPPORTED, "ALM is single-GPU (host-driven outer loop)");
   if (comm && model->kind == PCAL_MODEL_DEVICE_CALLBACK)
     throw Error(PCAL_E_UNSUPPORTED, "device-callback models are single-GPU");
   // resolve_beta (solver.cpp:120-134)
@@ -1774,9 +1864,54 @@ void session_create(const pcal_model_desc* model, const pcal_config* config, con
   *out = s.release();
 }
 
+void read_ctl(pcal_session* s) {
+  PCAL_CUDA(cudaMemcpyAsync(s->h_ctl, s->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, s->stream));
+  PCAL_CUDA(cudaStreamSynchronize(s->stream));
+}
+
+// ALM (alm_outer, solver.cpp:478-624): the inner steps are the usual iteration
+// (graph) with Λ fixed; after each evaluation the device has decided the next
+// action (Ctl::alm_phase), which the host reads: an inner step, or the
+// multiplier update — the inner loop's iterate (its best after a cap) moves to
+// the other pair, Λ ← Λ − β(XᵀX − I) in that pair's evaluation, and the
+// stepsize memory restarts.  `iters` bounds the inner steps of this call.
+static void run_alm(pcal_session* s, int64_t iters) {
+  const size_t xbytes = sizeof(double) * (size_t)s->ld * s->pp;
+  int64_t steps = 0;
+  for (;;) {
+    read_ctl(s);
+    const Ctl& c = *s->h_ctl;
+    if (c.done || (c.alm_phase == 0 && steps >= iters)) break;
+    const int b = (int)(s->next_k % 2);
+    if (c.alm_copy)
+      PCAL_CUDA(cudaMemcpyAsync(s->bestx.p, Xof(s, b), xbytes, cudaMemcpyDeviceToDevice, s->stream));
+    if (c.alm_phase == 0) {
+      if (s->use_graphs) {
+        PCAL_CUDA(cudaGraphLaunch(s->graph[b], s->stream));
+        count_launch(s->kernels_per_iter);
+      } else {
+        launch_iteration(s, b);
+      }
+      ++steps;
+      s->launched++;
+    } else {
+      PCAL_CUDA(cudaMemcpyAsync(Xof(s, 1 - b), c.alm_met ? Xof(s, b) : s->bestx.p, xbytes,
+                                cudaMemcpyDeviceToDevice, s->stream));
+      k_alm_boundary<<<1, 1, 0, s->stream>>>(s->ctl);
+      launched("k_alm_boundary");
+      launch_eval(s, 1 - b, 3, s->ctl);
+    }
+    s->next_k++;
+  }
+}
+
 void session_run(pcal_session* s, int64_t iters) {
   PCAL_CUDA(cudaSetDevice(s->device));
   LaunchScope ls(&s->launches);
+  if (s->alg == PCAL_ALG_ALM) {
+    run_alm(s, iters);
+    return;
+  }
   const int64_t batch = 32;
   int64_t remaining = std::min<int64_t>(iters, s->cfg.max_iter - s->launched);
   cudaEvent_t polled = nullptr;
@@ -1821,10 +1956,6 @@ void session_run(pcal_session* s, int64_t iters) {
   cudaEventDestroy(polled);
 }
 
-void read_ctl(pcal_session* s) {
-  PCAL_CUDA(cudaMemcpyAsync(s->h_ctl, s->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, s->stream));
-  PCAL_CUDA(cudaStreamSynchronize(s->stream));
-}
 
 // CholeskyQR2 of the n×p matrix at x (ld) into q (ld); MGS2 fallback.  Returns
 // false on rank deficiency (rank_error).  q and scratch must not alias x.
@@ -1944,12 +2075,14 @@ void session_finish(pcal_session* s, pcal_report* r) {
   r->has_x = 0;
   r->degenerate_steps = c.degenerate;
   r->iterations = tl > 0 ? tl - 1 : 0;
+  r->outer_iterations = c.alm_outer;
+  r->inner_cap_hits = c.alm_caps;
   for (int i = 0; i < 4; ++i) r->final_pre[i] = r->final_post[i] = 0.0;
   int status = c.done == 1 ? PCAL_STATUS_CONVERGED
                : c.done == 2 ? PCAL_STATUS_DIVERGED
                              : PCAL_STATUS_MAX_ITER;
   if (status != PCAL_STATUS_DIVERGED) {
-    const int b = (int)(c.iter % 2);
+    const int b = (int)((c.iter + c.alm_flips) % 2);
     r->final_pre[0] = c.f;
     r->final_pre[1] = c.kkt_abs;
     r->final_pre[2] = c.rel;
@@ -1990,6 +2123,8 @@ void session_finish(pcal_session* s, pcal_report* r) {
     if (r->final_x && !final_is_q) copy_out(s, Xof(s, b), r->final_x);
   }
   PCAL_CUDA(cudaStreamSynchronize(s->stream));
+  // alm_outer sets RunReport::iterations only on a normal exit (solver.cpp:577)
+  if (status == PCAL_STATUS_DIVERGED && s->alg == PCAL_ALG_ALM) r->iterations = 0;
   if (status == PCAL_STATUS_DIVERGED && tl > 0) {  // solver.cpp:467-471
     const double* last = r->trace ? r->trace + (tl - 1) * kTraceCols : nullptr;
     if (last) {
@@ -2014,6 +2149,9 @@ extern "C" {
 const char* pcal_last_error(void) { return g_last_error.c_str(); }
 
 void pcal_config_default(pcal_config* c) {
+  c->alm_inner_max = 500;  // AlmOptions (solver.hpp:24-28)
+  c->alm_outer_max = 50;
+  c->alm_inner_tol_scale = 0.1;
   c->algorithm = PCAL_ALG_PCAL;
   c->beta = -1.0;
   c->eta_kind = PCAL_ETA_ABB;
@@ -2172,7 +2310,7 @@ int pcal_session_get_x(pcal_session* s, double* x_out, double* eta_out, int64_t*
   return guarded([&] {
     PCAL_CUDA(cudaSetDevice(s->device));
     read_ctl(s);
-    const int b = (int)(s->h_ctl->iter % 2);
+    const int b = (int)((s->h_ctl->iter + s->h_ctl->alm_flips) % 2);
     if (x_out) copy_out(s, Xof(s, b), x_out);
     PCAL_CUDA(cudaStreamSynchronize(s->stream));
     if (eta_out) *eta_out = s->h_ctl->eta;
@@ -2183,7 +2321,7 @@ int pcal_session_get_x(pcal_session* s, double* x_out, double* eta_out, int64_t*
 int pcal_session_device_x(pcal_session* s, const double** x, int64_t* ld) {
   return guarded([&] {
     read_ctl(s);
-    *x = Xof(s, (int)(s->h_ctl->iter % 2));
+    *x = Xof(s, (int)((s->h_ctl->iter + s->h_ctl->alm_flips) % 2));
     *ld = s->ld;
   });
 }

@@ -84,9 +84,14 @@ def _final(f) -> dict:
             "kkt_abs": _num(float(f.kkt_abs)), "kkt_rel": _num(float(f.kkt_rel))}
 
 
-def to_json(report, echo: ConfigEcho, include_timing: bool = False, outer_iterations: int = 0,
-            inner_cap_hits: int = 0) -> str:
-    """to_json(RunReport) (report_io.cpp:86-106)."""
+def to_json(report, echo: ConfigEcho, include_timing: bool = False,
+            outer_iterations: Optional[int] = None, inner_cap_hits: Optional[int] = None) -> str:
+    """to_json(RunReport) (report_io.cpp:86-106).  The ALM counters default to the
+    report's own (0 for the other algorithms)."""
+    if outer_iterations is None:
+        outer_iterations = int(getattr(report, "outer_iterations", 0))
+    if inner_cap_hits is None:
+        inner_cap_hits = int(getattr(report, "inner_cap_hits", 0))
     cfg = {k: _num(v) for k, v in asdict(echo).items()}
     trace = []
     for row in report.trace:
@@ -136,8 +141,11 @@ def write_summary_header(out: IO[str]) -> None:
               "time_s\n")
 
 
-def write_summary_row(report, echo: ConfigEcho, out: IO[str], outer_iterations: int = 0) -> None:
+def write_summary_row(report, echo: ConfigEcho, out: IO[str],
+                      outer_iterations: Optional[int] = None) -> None:
     """write_summary_row (report_io.cpp:181-194)."""
+    if outer_iterations is None:
+        outer_iterations = int(getattr(report, "outer_iterations", 0))
     f = report.final_pre_orth
     out.write(f"{echo.problem},{echo.solver},{echo.seed},{echo.n},{echo.p},{_g17(echo.beta)},"
               f"{echo.eta_rule},{STATUS_TEXT[report.status]},{report.iterations},"
@@ -157,6 +165,8 @@ def same_numerics(a, b) -> bool:
         return np.array_equal(np.asarray(x, dtype=np.float64).view(np.uint64),
                               np.asarray(y, dtype=np.float64).view(np.uint64))
     if (a.status, a.iterations, a.degenerate_steps) != (b.status, b.iterations, b.degenerate_steps):
+        return False
+    if getattr(a, "outer_iterations", 0) != getattr(b, "outer_iterations", 0):
         return False
     if a.trace.shape != b.trace.shape or not beq(a.trace[:, :6], b.trace[:, :6]):
         return False

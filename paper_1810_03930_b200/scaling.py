@@ -103,6 +103,7 @@ def _load_case(path: str):
         model = P.KohnShamModel(tuple(z["grid"]), z["v"], p, s)
     c = json.loads(str(z["config"]))
     c["eta_rule"] = P.StepsizeRule(**c["eta_rule"])
+    c["alm"] = P.AlmOptions(**c["alm"])
     return model, P.SolverConfig(**c), np.asfortranarray(z["x0"])
 
 

@@ -52,8 +52,10 @@ def test_flops_estimate(pcal, orc):
 
 def test_config_validation_is_host_side(pcal):
     with pytest.raises(pcal.ParameterError):
-        pcal.SolverConfig(algorithm="alm")._c()
+        pcal.SolverConfig(algorithm="lbfgs")._c()
     assert pcal.SolverConfig(algorithm="plam-da")._c().algorithm == 4
+    c = pcal.SolverConfig(algorithm="alm", alm=pcal.AlmOptions(inner_max=7, outer_max=3))._c()
+    assert (c.algorithm, c.alm_inner_max, c.alm_outer_max, c.alm_inner_tol_scale) == (2, 7, 3, 0.1)
 
 
 def _has_cuda():
