@@ -181,6 +181,17 @@ def alm_cases(R: Reference) -> None:
     print("wrote reference_alm.npz")
 
 
+def matrix_case(R: Reference) -> None:
+    """run_matrix (harness.cpp:75-104) summary CSV of a small fixed matrix."""
+    import ctypes as C
+    L = R.lib
+    L.ref_run_matrix_csv.argtypes = [C.c_char_p, C.c_int64]
+    buf = C.create_string_buffer(1 << 20)
+    assert L.ref_run_matrix_csv(buf, len(buf)) == 0
+    open(os.path.join(OUT, "ref_matrix.csv"), "w").write(buf.value.decode())
+    print("wrote ref_matrix.csv")
+
+
 def report_io_cases(R: Reference) -> None:
     """The reference's JSON / CSV report text and an OCPROB01 container."""
     import ctypes as C
@@ -394,6 +405,7 @@ if __name__ == "__main__":
     linsolve_cases(R)
     model_eval_cases(R)
     alm_cases(R)
+    matrix_case(R)
     if "--cfg2" in sys.argv:
         cfg2(R)
     if "--grids" in sys.argv:

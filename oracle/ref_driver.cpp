@@ -494,4 +494,39 @@ void ref_last_alm_counts(std::int64_t* out) {
   out[1] = g_alm_counts[1];
 }
 
+// run_matrix (harness.cpp:75-104) over a fixed spec (tests/golden/ref_matrix.csv):
+// P2 40×4, P4 30×3, P1 (α = 1) 30×3, P6 block 30×3 and a P1 block cell with
+// n = 32 whose generation fails; PCAL, PLAM, ALM; seeds 1, 2; max_iter 500.
+int ref_run_matrix_csv(char* buf, std::int64_t cap) {
+  return guarded([&] {
+    MatrixSpec m;
+    ProblemSpec p2;
+    p2.kind = ProblemKind::P2;
+    p2.n = 40;
+    p2.p = 4;
+    ProblemSpec p4 = p2;
+    p4.kind = ProblemKind::P4;
+    p4.n = 30;
+    p4.p = 3;
+    ProblemSpec p1 = p4;
+    p1.kind = ProblemKind::P1;
+    ProblemSpec p6 = p4;
+    p6.kind = ProblemKind::P6;
+    p6.mode = OperatorMode::BlockTridiag;
+    ProblemSpec bad = p1;
+    bad.n = 32;
+    bad.mode = OperatorMode::BlockTridiag;
+    m.problems = {p2, p4, p1, p6, bad};
+    m.solvers = {Algorithm::Pcal, Algorithm::Plam, Algorithm::Alm};
+    m.seeds = {1, 2};
+    m.base.max_iter = 500;
+    std::ostringstream out;
+    run_matrix(m, out);
+    const std::string t = out.str();
+    if ((std::int64_t)t.size() + 1 > cap) throw io_error("buffer too small");
+    std::memcpy(buf, t.c_str(), t.size() + 1);
+    return 0;
+  });
+}
+
 }  // extern "C"

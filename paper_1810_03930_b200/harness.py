@@ -165,3 +165,49 @@ def run_single(problem: ProblemSpec, config: P.SolverConfig,
                       curvature_scale=model.s)
     rep.wall_time = time.perf_counter() - t0
     return rep, echo
+
+
+@dataclass
+class MatrixSpec:
+    """MatrixSpec (harness.hpp:35-43): problems × solvers × seeds."""
+    problems: list
+    solvers: list                      # algorithm names ("pcal", "plam", "alm", ...)
+    seeds: list
+    base: Optional[P.SolverConfig] = None  # algorithm overridden per cell
+    init: str = "qr"
+    sigma_lower: float = 0.5
+
+
+def run_matrix(spec: MatrixSpec, csv_out) -> None:
+    """run_matrix (harness.cpp:75-104): one summary CSV row per cell; a cell whose
+    generation fails is recorded as diverged and never aborts the matrix."""
+    import dataclasses
+    import sys
+    from paper_1810_03930_b200 import report_io as R
+    if not spec.problems or not spec.solvers or not spec.seeds:
+        raise P.ParameterError("run_matrix: empty problem/solver/seed list")
+    base = spec.base if spec.base is not None else P.SolverConfig()
+    R.write_summary_header(csv_out)
+    for prob in spec.problems:
+        for alg in spec.solvers:
+            for seed in spec.seeds:
+                cell = dataclasses.replace(prob, seed=seed)
+                cfg = dataclasses.replace(base, algorithm=alg)
+                init = InitialPointSpec(mode=spec.init, sigma_lower=spec.sigma_lower)
+                try:
+                    rep, echo = run_single(cell, cfg, init)
+                except (P.ParameterError, P.DimensionError, P.RankError, UnsupportedModel,
+                        ValueError) as e:
+                    sys.stderr.write(f"cell {cell.kind}/{alg}/{seed} failed: {e}\n")
+                    rep = P.RunReport(trace=np.zeros((0, 7)),
+                                      final_pre_orth=P.FinalMetrics(0.0, 0.0, 0.0, 0.0),
+                                      final_post_orth=None, stop_iterate=None, final_x=None,
+                                      iterations=0, degenerate_steps=0, wall_time=0.0,
+                                      status="diverged", beta=0.0, eta0=0.0)
+                    # fill_config_echo + the solver name; beta / eta_rule stay unset
+                    echo = R.ConfigEcho(problem=cell.kind.lower(), n=cell.n, p=cell.p, solver=alg,
+                                        beta=0.0, eta_rule="", tol_rel_kkt=0.0, max_iter=0,
+                                        init=spec.init, seed=seed, alpha=cell.alpha,
+                                        kappa=cell.kappa, theta=cell.theta, zeta=cell.zeta,
+                                        xi=cell.xi)
+                R.write_summary_row(rep, echo, csv_out)

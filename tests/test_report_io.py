@@ -121,3 +121,20 @@ def test_host_spectral_norm_is_the_reference_one():
 def pcal_errors():
     import paper_1810_03930_b200 as P
     return P
+
+
+def test_run_matrix_records_failed_cells_without_a_gpu():
+    """run_matrix (harness.cpp:75-104): a cell whose generation fails is a
+    'diverged' summary row (echo of the cell, no numbers) and never aborts the
+    matrix — byte-identical to the reference's rows for the same cells."""
+    import io as _io
+    from paper_1810_03930_b200 import harness as H
+    import paper_1810_03930_b200 as P
+    with pytest.raises(P.ParameterError):
+        H.run_matrix(H.MatrixSpec(problems=[], solvers=["pcal"], seeds=[1]), _io.StringIO())
+    out = _io.StringIO()
+    H.run_matrix(H.MatrixSpec(problems=[H.ProblemSpec(kind="p1", n=32, p=3, mode="block-tridiag")],
+                              solvers=["pcal", "plam", "alm"], seeds=[1, 2],
+                              base=P.SolverConfig(max_iter=500)), out)
+    ref = open(os.path.join(GOLD, "ref_matrix.csv")).read().splitlines()
+    assert out.getvalue().splitlines() == [ref[0]] + ref[-6:]
