@@ -317,6 +317,37 @@ def model_eval_cases(R: Reference) -> None:
     print("wrote reference_models.npz")
 
 
+DIAG_CASES = {  # name: (kind, n, p, alpha, block, seed, x-kind, beta)
+    "p1_near": (1, 60, 6, 1.0, 0, 31, "near", 30.0),   # near-orthonormal x: the bound applies
+    "p4_far": (4, 60, 6, 1.0, 0, 35, "randn", 1.0),    # random x: not applicable
+    "p6_near": (6, 45, 4, 1.0, 1, 37, "near", 20.0),
+}
+
+
+def diagnostics_cases(R: Reference) -> None:
+    """kkt_violation, feasibility_violation, merit_h, feasibility_bound_check
+    (diagnostics.cpp:21-98) of the reference's models at seeded points."""
+    import ctypes as C
+    L = R.lib
+    dp = C.POINTER(C.c_double)
+    L.ref_diagnostics.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_double, C.c_int, C.c_uint64,
+                                  dp, C.c_double, dp]
+    g = {}
+    for name, (kind, n, p, alpha, bt, seed, xk, beta) in DIAG_CASES.items():
+        if xk == "near":  # orthonormal start plus a small perturbation
+            x = R.initial_point_qr(n, p, seed + 100) + 1e-3 * R.random_normal(n, p, seed + 200)
+        else:
+            x = R.random_normal(n, p, seed + 300)
+        x = np.asfortranarray(x)
+        out = np.zeros(9)
+        assert L.ref_diagnostics(kind, n, p, alpha, bt, seed, x.ctypes.data_as(dp), beta,
+                                 out.ctypes.data_as(dp)) == 0, name
+        g[name + "_x"] = x
+        g[name + "_out"] = out
+    np.savez_compressed(os.path.join(OUT, "reference_diagnostics.npz"), **g)
+    print("wrote reference_diagnostics.npz")
+
+
 def grid_cases(R: Reference) -> None:
     """Grid models (no reference implementation): the reference solve() driving
     the restated operator — pins the PCAL loop around it, not the operator."""
@@ -406,6 +437,7 @@ if __name__ == "__main__":
     model_eval_cases(R)
     alm_cases(R)
     matrix_case(R)
+    diagnostics_cases(R)
     if "--cfg2" in sys.argv:
         cfg2(R)
     if "--grids" in sys.argv:

@@ -529,4 +529,29 @@ int ref_run_matrix_csv(char* buf, std::int64_t cap) {
   });
 }
 
+// diagnostics.cpp on gen_problem{1,4,6}(…, seed) at x: out = {kkt_violation,
+// feasibility_violation, merit_h(beta), bound.applicable, delta, lhs, rhs, holds, slack}.
+int ref_diagnostics(int kind, std::int64_t n, std::int64_t p, double alpha, int block_tridiag,
+                    std::uint64_t seed, const double* x, double beta, double* out) {
+  return guarded([&] {
+    const OperatorMode mode = block_tridiag ? OperatorMode::BlockTridiag : OperatorMode::RandomSym;
+    std::unique_ptr<ObjectiveModel> m =
+        kind == 1 ? gen_problem1(n, p, alpha, mode, seed, 1)
+        : kind == 4 ? gen_problem4(n, p, seed, 1)
+                    : gen_problem6(n, p, mode, seed, 1);
+    const DenseMatrix xm = from_ptr(x, n, p);
+    out[0] = kkt_violation(*m, xm);
+    out[1] = feasibility_violation(xm);
+    out[2] = merit_h(*m, xm, beta);
+    const FeasibilityBoundResult b = feasibility_bound_check(*m, xm, beta);
+    out[3] = b.applicable ? 1.0 : 0.0;
+    out[4] = b.delta;
+    out[5] = b.lhs;
+    out[6] = b.rhs;
+    out[7] = b.holds ? 1.0 : 0.0;
+    out[8] = b.slack;
+    return 0;
+  });
+}
+
 }  // extern "C"

@@ -106,3 +106,26 @@ def test_density_model_sharded_layouts(pcal):
     bad.linv = None
     with pytest.raises(pcal.ParameterError):
         pcal.evaluate(bad, np.eye(60, 6, order="F"))
+
+
+@pytest.mark.parametrize("name", ["p1_near", "p4_far", "p6_near"])
+def test_diagnostics_match_reference(pcal, name):
+    """kkt_violation, feasibility_violation, merit_h and feasibility_bound_check
+    (diagnostics.cpp:21-98) on the device against the reference's values."""
+    from paper_1810_03930_b200 import diagnostics as D
+    from paper_1810_03930_b200 import harness as H
+    spec = {"p1_near": dict(kind="p1", n=60, p=6, alpha=1.0, seed=31, beta=30.0),
+            "p4_far": dict(kind="p4", n=60, p=6, seed=35, beta=1.0),
+            "p6_near": dict(kind="p6", n=45, p=4, mode="block-tridiag", seed=37, beta=20.0)}[name]
+    beta = spec.pop("beta")
+    g = np.load(os.path.join(GOLD, "reference_diagnostics.npz"))
+    ref = g[name + "_out"]
+    x = g[name + "_x"]
+    m = H.make_problem(H.ProblemSpec(**spec))
+    assert abs(D.kkt_violation(m, x) - ref[0]) <= 1e-11 * ref[0]
+    assert abs(D.feasibility_violation(x) - ref[1]) <= 1e-11 * ref[1]
+    assert abs(D.merit_h(m, x, beta) - ref[2]) <= 1e-11 * abs(ref[2])
+    b = D.feasibility_bound_check(m, x, beta)
+    assert b.applicable == bool(ref[3]) and b.holds == bool(ref[7])
+    for v, r in ((b.delta, ref[4]), (b.lhs, ref[5]), (b.rhs, ref[6]), (b.slack, ref[8])):
+        assert abs(v - r) <= 1e-10 * abs(r) + 1e-14
