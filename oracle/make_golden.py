@@ -181,6 +181,19 @@ def alm_cases(R: Reference) -> None:
     print("wrote reference_alm.npz")
 
 
+def container_cases(R: Reference) -> None:
+    """OCPROB01 containers of the Bilinear / Density models (problems.cpp:341-416)."""
+    import ctypes as C
+    L = R.lib
+    L.ref_save_generated.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_double, C.c_int,
+                                     C.c_uint64, C.c_char_p]
+    for name, args in {"p4": (4, 12, 3, 1.0, 0, 41), "p1": (1, 10, 2, 1.5, 1, 42),
+                       "p6": (6, 11, 3, 1.0, 0, 43)}.items():
+        path = os.path.join(OUT, f"ref_{name}.ocprob")
+        assert L.ref_save_generated(*args, path.encode()) == 0, name
+    print("wrote ref_p4/p1/p6.ocprob")
+
+
 def matrix_case(R: Reference) -> None:
     """run_matrix (harness.cpp:75-104) summary CSV of a small fixed matrix."""
     import ctypes as C
@@ -438,6 +451,7 @@ if __name__ == "__main__":
     alm_cases(R)
     matrix_case(R)
     diagnostics_cases(R)
+    container_cases(R)
     if "--cfg2" in sys.argv:
         cfg2(R)
     if "--grids" in sys.argv:

@@ -554,4 +554,20 @@ int ref_diagnostics(int kind, std::int64_t n, std::int64_t p, double alpha, int 
   });
 }
 
+// save_problem of gen_problem{1,4,6}(…, seed) (problems.cpp:341-365): the
+// Bilinear / Density container forms.
+int ref_save_generated(int kind, std::int64_t n, std::int64_t p, double alpha, int block_tridiag,
+                       std::uint64_t seed, const char* path) {
+  return guarded([&] {
+    const OperatorMode mode = block_tridiag ? OperatorMode::BlockTridiag : OperatorMode::RandomSym;
+    std::unique_ptr<ObjectiveModel> m =
+        kind == 1 ? gen_problem1(n, p, alpha, mode, seed, 1)
+        : kind == 4 ? gen_problem4(n, p, seed, 1)
+                    : gen_problem6(n, p, mode, seed, 1);
+    std::ofstream out(path, std::ios::binary);
+    save_problem(*m, out);
+    return 0;
+  });
+}
+
 }  // extern "C"

@@ -420,8 +420,9 @@ class DensityModel(_ModelBase):
     ``l`` / ``linv`` may be the local row slabs of a sharded session (pass n)."""
 
     def __init__(self, l, p: int, coeff: float, s: float, variant: str = "p1", linv=None,
-                 n: Optional[int] = None):
+                 n: Optional[int] = None, mode: str = "random-sym"):
         self.kind = MODEL_DENSITY
+        self.mode = mode  # OperatorMode of L (recorded in the container form)
         if int(p) < 1 or 2 * int(p) > (l.shape[1] if n is None else n):
             raise ParameterError("DensityModel: dimensions must satisfy 2p <= n")
         self.a = _f64(l)

@@ -121,12 +121,12 @@ def make_problem(spec: ProblemSpec, device: int = 0):
         g0 = None
         if spec.alpha != 0.0:  # gen_problem1 (problems.cpp:208-217)
             s = P.spectral_norm_estimate_host(a, spec.seed ^ SPECTRAL_SALT)
-            return P.DensityModel(a, spec.p, spec.alpha, s, variant="p1")
+            return P.DensityModel(a, spec.p, spec.alpha, s, variant="p1", mode=spec.mode)
     elif kind == "p6":  # gen_problem6 (problems.cpp:276-285)
         a = _operator(spec, device)
         s = P.spectral_norm_estimate_host(a, spec.seed ^ SPECTRAL_SALT)
         gamma = 2.0 * np.cbrt(3.0 / 3.14159265358979323846)
-        return P.DensityModel(a, spec.p, gamma, s, variant="p6")
+        return P.DensityModel(a, spec.p, gamma, s, variant="p6", mode=spec.mode)
     elif kind == "p4":  # gen_problem4 (problems.cpp:267-274): A then B from one stream
         n, p = spec.n, spec.p
         z = P.random_normal(n * n + p * p, 1, spec.seed)[:, 0]

@@ -184,18 +184,40 @@ def same_numerics(a, b) -> bool:
 
 
 # ---- OCPROB01 container (problems.cpp:327-416) -----------------------------------
+def _sym_upper(raw: bytes, n: int) -> np.ndarray:
+    """get_symmetric (problems.cpp:93-99): the upper triangle mirrored."""
+    a = np.frombuffer(raw, dtype="<f8").reshape((n, n), order="F").copy(order="F")
+    iu = np.triu_indices(n)
+    a[(iu[1], iu[0])] = a[iu]  # set_mirrored(i, j, upper(i, j))
+    return a
+
+
 def save_problem(model, out, kappa: float = 0.0, theta: float = 1.0, zeta: float = 1.0,
                  xi: float = 1.0) -> None:
-    """QuadraticModel::save: magic, u32 tag (2 with a linear term, 3 without),
-    u64 n, u64 p, f64 s, kappa, theta, zeta, xi, A (n×n), G (n×p), little endian."""
-    if getattr(model, "kind", None) != 1:
-        raise UnsupportedModel("only the dense quadratic family has a container form here")
-    a = np.asfortranarray(model.a, dtype="<f8")
-    g = np.zeros((model.n, model.p), order="F") if model.g0 is None else model.g0
-    tag = 3 if model.g0 is None else 2
-    buf = MAGIC + struct.pack("<IQQd", tag, model.n, model.p, model.s)
-    buf += struct.pack("<dddd", kappa, theta, zeta, xi)
-    buf += a.tobytes(order="F") + np.asfortranarray(g, dtype="<f8").tobytes(order="F")
+    """save_problem (problems.cpp:327-366), little endian after the magic:
+    QuadraticModel — u32 tag (2 with a linear term, 3 without), u64 n, u64 p,
+    f64 s, kappa, theta, zeta, xi, A (n×n), G (n×p); BilinearModel — tag 4,
+    n, p, s, A, B (p×p); DensityModel — tag 1 / 6, n, p, s, f64 coeff,
+    u32 mode (1 = block-tridiagonal), L (n×n)."""
+    kind = getattr(model, "kind", None)
+
+    def head(tag):
+        return MAGIC + struct.pack("<IQQd", tag, model.n, model.p, model.s)
+
+    def mat(m):
+        return np.asfortranarray(m, dtype="<f8").tobytes(order="F")
+    if kind == 1:
+        g = np.zeros((model.n, model.p), order="F") if model.g0 is None else model.g0
+        buf = head(3 if model.g0 is None else 2) + struct.pack("<dddd", kappa, theta, zeta, xi)
+        buf += mat(model.a) + mat(g)
+    elif kind == 5:
+        buf = head(4) + mat(model.a) + mat(model.b)
+    elif kind == 6:
+        buf = head(6 if model.variant == "p6" else 1)
+        buf += struct.pack("<dI", model.coeff, 1 if model.mode == "block-tridiag" else 0)
+        buf += mat(model.a)
+    else:
+        raise UnsupportedModel("save_problem: grid and callback models have no container form")
     if isinstance(out, (str, bytes)):
         with open(out, "wb") as f:
             f.write(buf)
@@ -204,8 +226,9 @@ def save_problem(model, out, kappa: float = 0.0, theta: float = 1.0, zeta: float
 
 
 def load_problem(src, pcal=None):
-    """load_problem → (QuadraticModel, params dict).  A is symmetrised from its
-    upper triangle exactly like get_symmetric (problems.cpp:93-99)."""
+    """load_problem (problems.cpp:368-416) → (model, params dict): QuadraticModel
+    (tags 2 / 3), BilinearModel (4), DensityModel (1 / 6); symmetric matrices are
+    symmetrised from their upper triangle like get_symmetric."""
     if pcal is None:
         import paper_1810_03930_b200 as pcal
     data = open(src, "rb").read() if isinstance(src, (str, bytes)) else src.read()
@@ -213,16 +236,26 @@ def load_problem(src, pcal=None):
     if f.read(8) != MAGIC:
         raise ValueError("load_problem: bad magic bytes")
     tag, n, p, s = struct.unpack("<IQQd", f.read(28))
-    if tag not in (2, 3):
-        raise UnsupportedModel(f"load_problem: kind tag {tag} has no device model here")
-    kappa, theta, zeta, xi = struct.unpack("<dddd", f.read(32))
-    raw = f.read(8 * n * n)
-    graw = f.read(8 * n * p)
-    if len(raw) != 8 * n * n or len(graw) != 8 * n * p:
-        raise ValueError("load_problem: truncated stream")
-    a = np.frombuffer(raw, dtype="<f8").reshape((n, n), order="F").copy(order="F")
-    iu = np.triu_indices(n)
-    a[(iu[1], iu[0])] = a[iu]  # set_mirrored(i, j, upper(i, j))
-    g = np.frombuffer(graw, dtype="<f8").reshape((n, p), order="F").copy(order="F")
-    model = pcal.QuadraticModel(a, p, s, g0=None if tag == 3 else g)
-    return model, {"tag": tag, "kappa": kappa, "theta": theta, "zeta": zeta, "xi": xi}
+
+    def take(count):
+        raw = f.read(8 * count)
+        if len(raw) != 8 * count:
+            raise ValueError("load_problem: truncated stream")
+        return raw
+    if tag in (2, 3):
+        kappa, theta, zeta, xi = struct.unpack("<dddd", f.read(32))
+        a = _sym_upper(take(n * n), n)
+        g = np.frombuffer(take(n * p), dtype="<f8").reshape((n, p), order="F").copy(order="F")
+        model = pcal.QuadraticModel(a, p, s, g0=None if tag == 3 else g)
+        return model, {"tag": tag, "kappa": kappa, "theta": theta, "zeta": zeta, "xi": xi}
+    if tag == 4:
+        a = _sym_upper(take(n * n), n)
+        b = _sym_upper(take(p * p), p)
+        return pcal.BilinearModel(a, b, s), {"tag": tag}
+    if tag in (1, 6):
+        coeff, mode = struct.unpack("<dI", f.read(12))
+        lmat = _sym_upper(take(n * n), n)
+        model = pcal.DensityModel(lmat, p, coeff, s, variant="p6" if tag == 6 else "p1",
+                                  mode="block-tridiag" if mode == 1 else "random-sym")
+        return model, {"tag": tag, "coeff": coeff, "mode": mode}
+    raise ValueError(f"load_problem: unknown kind tag {tag}")

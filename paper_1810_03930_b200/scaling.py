@@ -78,6 +78,7 @@ def _save_case(path: str, model, config: P.SolverConfig, x0) -> None:
             d["linv"] = model.linv
             d["coeff"] = model.coeff
             d["variant"] = model.variant
+            d["mode"] = model.mode
     elif model.kind in (P.MODEL_STENCIL, P.MODEL_KOHN_SHAM):
         d["grid"] = np.array(model.grid)
         d["v"] = model.v
@@ -96,7 +97,7 @@ def _load_case(path: str):
         model = P.BilinearModel(z["a"], z["b"], s)
     elif kind == P.MODEL_DENSITY:
         model = P.DensityModel(z["a"], p, float(z["coeff"]), s, variant=str(z["variant"]),
-                               linv=z["linv"])
+                               linv=z["linv"], mode=str(z["mode"]))
     elif kind == P.MODEL_STENCIL:
         model = P.StencilModel(tuple(z["grid"]), z["v"], p, s)
     else:

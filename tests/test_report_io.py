@@ -138,3 +138,30 @@ def test_run_matrix_records_failed_cells_without_a_gpu():
                               base=P.SolverConfig(max_iter=500)), out)
     ref = open(os.path.join(GOLD, "ref_matrix.csv")).read().splitlines()
     assert out.getvalue().splitlines() == [ref[0]] + ref[-6:]
+
+
+@pytest.mark.parametrize("name,spec", [
+    ("p4", dict(kind="p4", n=12, p=3, seed=41)),
+    ("p1", dict(kind="p1", n=10, p=2, alpha=1.5, mode="block-tridiag", seed=42)),
+    ("p6", dict(kind="p6", n=11, p=3, seed=43)),
+])
+def test_bilinear_density_containers_match_reference(name, spec):
+    """save_problem of the Bilinear / Density models (problems.cpp:341-361):
+    the harness's instance saves to the reference's container byte for byte,
+    and load_problem rebuilds the same model."""
+    import io as _io
+    from paper_1810_03930_b200 import harness as H
+    from paper_1810_03930_b200 import report_io as R
+    path = os.path.join(GOLD, f"ref_{name}.ocprob")
+    m = H.make_problem(H.ProblemSpec(**spec))
+    out = _io.BytesIO()
+    R.save_problem(m, out)
+    assert out.getvalue() == open(path, "rb").read()
+    back, params = R.load_problem(path)
+    assert back.kind == m.kind and (back.n, back.p, back.s) == (m.n, m.p, m.s)
+    assert np.array_equal(back.a, m.a)
+    if name == "p4":
+        assert np.array_equal(back.b, m.b)
+    else:
+        assert back.coeff == m.coeff and back.variant == m.variant and back.mode == m.mode
+        assert np.array_equal(back.linv, m.linv)
