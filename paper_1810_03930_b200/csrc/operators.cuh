@@ -72,8 +72,11 @@ __global__ void __launch_bounds__(kStencilThreads)
 // current plane (+ periodic y-halo rows) in shared memory, so every X value is
 // read from HBM once (halo rows: 2/TY extra, mostly L2 hits).  Same operation
 // order as k_stencil_grad (bitwise identical results).
+#ifndef PCAL_STENCIL_MINB
+#define PCAL_STENCIL_MINB 4  // ≤ 64 registers: 32 resident warps per SM for the plane pipeline
+#endif
 template <bool KS, int XP, int TY>
-__global__ void __launch_bounds__(32 * TY)
+__global__ void __launch_bounds__(32 * TY, PCAL_STENCIL_MINB)
     k_stencil_march(const double* __restrict__ x, const double* __restrict__ u,
                     double* __restrict__ g, int nx, int ny, int nz, int64_t ld, int zchunk,
                     double* __restrict__ fpart, int64_t pstride, int32_t* bad, const Ctl* ctl,
@@ -170,7 +173,9 @@ __global__ void __launch_bounds__(32 * TY)
         else gv = __dadd_rn(lx, __dmul_rn(uc[k], xv));
         gj[i] = gv;
         acc += KS ? xv * lx : xv * gv;
-        nonfinite |= !isfinite(gv);
+        // stencil model: a non-finite G makes Σ X∘G non-finite (x·±inf and
+        // 0·inf are never finite), so the partial sum is checked at its flush
+        if (KS) nonfinite |= !isfinite(gv);
       }
       below[k] = cur[k];
       cur[k] = above[k];
@@ -182,6 +187,7 @@ __global__ void __launch_bounds__(32 * TY)
     // block reduction (fixed order) → one f partial per (tile, zpart planes):
     // once per z-chunk (zpart = zchunk), or per row chunk on the sharded path
     if (++zp_cnt == zpart || z + 1 == z1) {
+      if (!KS) nonfinite |= !isfinite(acc);
       const double v = warp_sum(acc);
       if (lane == 0) sm[ty] = v;
       __syncthreads();
