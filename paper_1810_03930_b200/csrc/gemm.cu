@@ -27,7 +27,8 @@ int num_sms(int device) {
 
 CfgInfo cfg_info(int size) {
   switch (size) {
-    case CFG_BIG: return {128, 128, CfgBig<A_MCONTIG>::WM, CfgBig<A_MCONTIG>::BK};
+    case CFG_BIG:
+    case CFG_XMT: return {128, 128, CfgBig<A_MCONTIG>::WM, CfgBig<A_MCONTIG>::BK};
     case CFG_MID: return {64, 64, 32, CfgMid<A_MCONTIG>::BK};
     default: return {64, 32, 32, CfgSmall<A_MCONTIG>::BK};
   }
@@ -112,7 +113,9 @@ void plan_gemm(GemmPlan& pl, int device, int size, int amode, int epi, int64_t M
     const int64_t g0 = grid;
     const int64_t dp_cost = ceil_div(ntiles, g0) * ki;
     const int64_t sk_cost = ceil_div(units, g0) + 4;
-    if (dp_cost <= sk_cost) {
+    if (size == CFG_XMT && (amode != A_MCONTIG || epi != EPI_XM))
+      throw Error(PCAL_E_STATE, "gemm: the TMEM-epilogue kernel is X·[W|C] only");
+    if (dp_cost <= sk_cost || size == CFG_XMT) {  // gemm_xm_tmem: whole tiles only
       const int64_t w = ceil_div(ntiles, g0);
       upc = w * ki;
       grid = (int)ceil_div(ntiles, w);
@@ -207,8 +210,28 @@ static void launch_cfg(const GemmPlan& pl, cudaStream_t st) {
   }
 }
 
+static void launch_xm_tmem(const GemmPlan& pl, cudaStream_t st) {
+  using Cfg = CfgBig<A_MCONTIG>;
+  constexpr int smem = Cfg::SMEM_BYTES + 4 * 8 + 16;  // + acc_full/acc_empty, TMEM slot
+  static bool attr_set = false;
+  if (!attr_set) {
+    PCAL_CUDA(cudaFuncSetAttribute(gemm_xm_tmem<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   smem));
+    attr_set = true;
+  }
+  gemm_xm_tmem<Cfg><<<pl.args.grid, Cfg::THREADS + 256, smem, st>>>(pl.args);
+  launched("gemm_xm");
+  PCAL_CUDA(cudaGetLastError());
+}
+
 template <int AM, int EPI>
 static void launch_sized(const GemmPlan& pl, cudaStream_t st) {
+  if constexpr (AM == A_MCONTIG && EPI == EPI_XM) {
+    if (pl.size == CFG_XMT) {
+      launch_xm_tmem(pl, st);
+      return;
+    }
+  }
   switch (pl.size) {
     case CFG_BIG: launch_cfg<CfgBig<AM>, EPI>(pl, st); break;
     case CFG_MID: launch_cfg<CfgMid<AM>, EPI>(pl, st); break;

@@ -524,6 +524,213 @@ __global__ void __launch_bounds__(Cfg::THREADS + 128, 1) gemm_streamk(GemmArgs g
   }
 }
 
+// ---- X·[W|C] with the epilogue off the DMMA path (TMEM-staged accumulators) ------
+// K = 2p is only 8–16 k-slices per tile, so the fused epilogue (G/X loads, P
+// stores, column partials) idles the DMMA pipe ≈20% of the time.  Here the 8
+// consumer warps hand each finished tile to tensor memory (tcgen05.st, two
+// 128 KB buffers = all 512 TMEM columns) and go straight on to the next tile,
+// while a fourth warpgroup reads the tile back (tcgen05.ld) and runs the same
+// epilogue code.  TMEM lane quarter q (= warp % 4) holds consumer warps
+// (wm, wn) = (0, q) and (1, q); epilogue warp q processes exactly their
+// fragments, so every element, partial and shuffle order is the one of
+// gemm_streamk — results are bitwise identical.  Data-parallel whole tiles.
+__device__ __forceinline__ void tmem_st32(uint32_t addr, const uint32_t (&v)[32]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};\n"
+               ::"r"(addr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31]) : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t addr, uint32_t (&v)[32]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31]) : "r"(addr) : "memory");
+}
+
+// XM epilogue of one 8-column group nt of warp tile (wm, wn): EPI_XM of
+// epilogue<> with NB = 1 (same element / partial / shuffle order).
+template <class Cfg>
+__device__ __forceinline__ void epilogue_xm_group(const GemmArgs& g, int tm, int tn, int wm, int wn,
+                                                  int lane, int nt, const double (&a)[Cfg::MT][2]) {
+  const EpiParams& e = g.ep;
+  const int r = lane >> 2, q = lane & 3;
+  const int64_t mw0 = (int64_t)tm * Cfg::BM + wm * Cfg::WM;
+  const int64_t nw0 = (int64_t)tn * Cfg::BN + wn * Cfg::WN;
+  const int64_t rb = mw0 / Cfg::WM;
+  const bool interior = (mw0 + Cfg::WM <= e.n) && (((nw0 + Cfg::WN) >> 1) <= e.p);
+  const int64_t j = (nw0 + nt * 8 + 2 * q) >> 1;
+  double gv[Cfg::MT], xv[Cfg::MT];
+  if (interior) {
+#pragma unroll
+    for (int mt = 0; mt < Cfg::MT; ++mt) {
+      const int64_t idx = mw0 + mt * 8 + r + j * e.ld;
+      gv[mt] = e.G[idx];
+      xv[mt] = e.X[idx];
+    }
+  }
+  double ks = 0.0, ds = 0.0;
+#pragma unroll
+  for (int mt = 0; mt < Cfg::MT; ++mt) {
+    const int64_t row = mw0 + mt * 8 + r;
+    const int64_t idx = row + j * e.ld;
+    if (interior) {
+      const double kkt = gv[mt] - a[mt][0];
+      const double pv = (e.p_from_g ? gv[mt] : kkt) + e.beta * a[mt][1];
+      e.G[idx] = pv;
+      ks += kkt * kkt;
+      ds += (e.d_sq ? pv : xv[mt]) * pv;
+    } else if (row < e.n && j < e.p) {
+      const double g0 = e.G[idx];
+      const double kkt = g0 - a[mt][0];
+      const double pv = (e.p_from_g ? g0 : kkt) + e.beta * a[mt][1];
+      e.G[idx] = pv;
+      ks += kkt * kkt;
+      ds += (e.d_sq ? pv : e.X[idx]) * pv;
+    }
+  }
+#pragma unroll
+  for (int o = 4; o < 32; o <<= 1) {
+    ks += __shfl_xor_sync(0xffffffffu, ks, o);
+    ds += __shfl_xor_sync(0xffffffffu, ds, o);
+  }
+  if (r == 0 && j < e.p) {
+    e.kpart[j * e.pstride + rb] = ks;
+    e.dpart[j * e.pstride + rb] = ds;
+  }
+}
+
+constexpr int kTmemEpiRegs = 104;  // epilogue warpgroup after setmaxnreg
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS + 256, 1) gemm_xm_tmem(GemmArgs g) {
+  static_assert(Cfg::WARPS == 8 && Cfg::WARPS_N == 4 && Cfg::MT * Cfg::NT * 4 == 128,
+                "TMEM staging: 8 consumer warps (2 × 4), 64 doubles each");
+  if (g.ctl && g.ctl->done) return;
+  extern __shared__ __align__(16) double smem[];
+  constexpr int S = Cfg::STAGES;
+  double* As = smem;
+  double* Bs = smem + S * Cfg::A_STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(Bs + S * Cfg::B_STAGE);
+  uint64_t* empty = full + S;
+  uint64_t* acc_full = empty + S;   // [2]
+  uint64_t* acc_empty = acc_full + 2;  // [2]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int w = (int)(g.upc / g.ki);
+  const int t0 = blockIdx.x * w, t1 = min(g.ntiles, t0 + w);
+  if (t0 >= t1) return;  // uniform over the CTA, before any TMEM allocation
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&full[i], 32 * 4);
+      mbar_init(&empty[i], Cfg::WARPS);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], Cfg::WARPS);
+      mbar_init(&acc_empty[b], 4);
+    }
+  }
+  if (warp == 0) {  // all 512 columns: two 128 × (2 × 128) accumulator buffers
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n"
+                 ::"r"(smem_u32(tslot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  const uint32_t tbase = *tslot;
+  if (warp >= Cfg::WARPS && warp < Cfg::WARPS + 4) {  // producer warpgroup
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kProducerRegs));
+    // all four warps copy: the consumers no longer pause for epilogues, so the
+    // ring must refill at the full DMMA rate
+    const int64_t u0 = (int64_t)t0 * g.ki, u1 = (int64_t)t1 * g.ki;
+    switch (warp - Cfg::WARPS) {
+      case 0: produce<Cfg, 0, 4>(g, As, Bs, full, empty, u0, u1, lane); break;
+      case 1: produce<Cfg, 1, 4>(g, As, Bs, full, empty, u0, u1, lane); break;
+      case 2: produce<Cfg, 2, 4>(g, As, Bs, full, empty, u0, u1, lane); break;
+      default: produce<Cfg, 3, 4>(g, As, Bs, full, empty, u0, u1, lane); break;
+    }
+    cp_async_wait<0>();
+    return;
+  }
+  const uint32_t quarter = (uint32_t)(warp & 3) * 32u;
+  if (warp >= Cfg::WARPS + 4) {  // epilogue warpgroup: warp q reads TMEM lanes [32q, 32q+32)
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kTmemEpiRegs));
+    const int wn = warp & 3;
+    for (int t = t0; t < t1; ++t) {
+      const int buf = (t - t0) & 1;
+      const unsigned ph = (unsigned)((t - t0) >> 1) & 1u;
+      mbar_wait(&acc_full[buf], ph);
+      asm volatile("tcgen05.fence::after_thread_sync;\n");
+      const int2 tc = g.tiles[t];
+#pragma unroll 1
+      for (int wm = 0; wm < 2; ++wm)
+#pragma unroll 1
+        for (int nt = 0; nt < Cfg::NT; ++nt) {
+          uint32_t v[32];
+          tmem_ld32(tbase + (quarter << 16) + (uint32_t)(buf * 256 + wm * 128 + nt * 32), v);
+          asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+          double a[Cfg::MT][2];
+#pragma unroll
+          for (int mt = 0; mt < Cfg::MT; ++mt)
+#pragma unroll
+            for (int x = 0; x < 2; ++x)
+              a[mt][x] = __hiloint2double((int)v[(mt * 2 + x) * 2 + 1], (int)v[(mt * 2 + x) * 2]);
+          epilogue_xm_group<Cfg>(g, tc.x, tc.y, wm, wn, lane, nt, a);
+        }
+      asm volatile("tcgen05.fence::before_thread_sync;\n");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[buf]);
+    }
+    asm volatile("bar.sync 1, %0;\n" ::"n"(Cfg::THREADS + 128));  // consumers + epilogue
+    return;
+  }
+  {  // consumers
+    constexpr int R = (65536 - 128 * kProducerRegs - 128 * kTmemEpiRegs) / Cfg::THREADS / 8 * 8;
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(R > 232 ? 232 : R));
+  }
+  const int wm = warp / Cfg::WARPS_N;
+  const int wn = warp % Cfg::WARPS_N;
+  double acc[Cfg::MT][Cfg::NT][2];
+  int stage = 0;
+  unsigned phase = 0;
+  for (int t = t0; t < t1; ++t) {
+#pragma unroll
+    for (int mt = 0; mt < Cfg::MT; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < Cfg::NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+    for (int kk = 0; kk < g.ki; ++kk) {
+      mbar_wait(&full[stage], phase);
+      mma_stage<Cfg>(As + stage * Cfg::A_STAGE, Bs + stage * Cfg::B_STAGE, wm, wn, lane, acc);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (++stage == S) {
+        stage = 0;
+        phase ^= 1u;
+      }
+    }
+    const int buf = (t - t0) & 1;
+    const unsigned ph = (unsigned)((t - t0) >> 1) & 1u;
+    mbar_wait(&acc_empty[buf], ph ^ 1u);
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+#pragma unroll
+    for (int nt = 0; nt < Cfg::NT; ++nt) {
+      uint32_t v[32];
+#pragma unroll
+      for (int mt = 0; mt < Cfg::MT; ++mt)
+#pragma unroll
+        for (int x = 0; x < 2; ++x) {
+          v[(mt * 2 + x) * 2] = (uint32_t)__double2loint(acc[mt][nt][x]);
+          v[(mt * 2 + x) * 2 + 1] = (uint32_t)__double2hiint(acc[mt][nt][x]);
+        }
+      tmem_st32(tbase + (quarter << 16) + (uint32_t)(buf * 256 + wm * 128 + nt * 32), v);
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&acc_full[buf]);
+  }
+  asm volatile("bar.sync 1, %0;\n" ::"n"(Cfg::THREADS + 128));
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tbase));
+  }
+}
+
 // Sums the partials of split tiles in CTA order (q = 0, 1, …) and applies the
 // epilogue with the consumer-warp geometry of the main kernel.  q-outer loop:
 // every partial contributes FRAG independent coalesced loads per thread.

@@ -88,7 +88,9 @@ __host__ __device__ inline int64_t seg_unit_begin(int32_t c, int32_t ntiles, int
 
 
 // ---- host-side plans -----------------------------------------------------------
-enum CfgSize { CFG_BIG = 0, CFG_MID = 1, CFG_SMALL = 2 };
+// CFG_XMT: the CFG_BIG tiles of X·[W|C] with the TMEM-staged epilogue
+// (gemm_xm_tmem; data-parallel whole tiles)
+enum CfgSize { CFG_BIG = 0, CFG_MID = 1, CFG_SMALL = 2, CFG_XMT = 3 };
 
 struct CfgInfo {
   int BM, BN, WM, BK;

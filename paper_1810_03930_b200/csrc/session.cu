@@ -1209,7 +1209,11 @@ static void build_plans(pcal_session* s) {
     // X·[W|C] with the PCAL epilogue: A = X (MCONTIG, K = pp), B = mcat (pp × 2pp)
     {
       GemmPlan& g = s->xm[b];
-      plan_gemm(g, dev, pick_size(2 * pp), A_MCONTIG, EPI_XM, n, 2 * pp, pp, -1, 0,
+      // wide outputs: the epilogue runs off the DMMA path from TMEM (gemm_xm_tmem,
+      // bitwise the same results)
+      const int xsz = pick_size(2 * pp);
+      const bool tmem = xsz == CFG_BIG && !s->repro && !getenv("PCAL_NO_TMEM_EPI");
+      plan_gemm(g, dev, tmem ? (int)CFG_XMT : xsz, A_MCONTIG, EPI_XM, n, 2 * pp, pp, -1, 0,
                 s->repro ? 1 : 0);  // reproducible: whole tiles, no K split
       g.args.A = Xof(s, b);
       g.args.lda = ld;
