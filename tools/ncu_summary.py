@@ -18,6 +18,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def short(name: str) -> str:
     nm = name.replace("pcal::", "").replace("(int)", "")
+    if "gemm_xm_tmem" in nm:
+        return "gemm_xm_tmem<128x128,MC,XM>"
     m = re.search(r"gemm_(streamk|fixup|fixup_store)<GemmCfg<(\d+), (\d+), \d+, \d+, \d+, (\d)(?:, \d+)?>(?:, (\d))?(?:, (\d))?", nm)
     if m:
         kind = {"0": "STORE", "1": "GRAD", "2": "XM", None: "STORE"}[m.group(5)]
@@ -111,7 +113,7 @@ def full(path: str, out, summary: dict):
         print(f"  dram read+write per launch: {(rb + wb) / 1e9:.4f} GB; "
               f"effective {(rb + wb) / t / 1e9:.1f} GB/s", file=out)
         ph = phase_of(name)
-        if "streamk" in name and ph in ("gradient", "gram", "xm"):
+        if ("streamk" in name or "xm_tmem" in name) and ph in ("gradient", "gram", "xm"):
             summary.setdefault(ph, rb + wb)
 
 
