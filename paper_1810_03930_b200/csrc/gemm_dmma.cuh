@@ -681,6 +681,13 @@ __global__ void __launch_bounds__(Cfg::THREADS + 256, 1) gemm_xm_tmem(GemmArgs g
   }
   {  // consumers
     constexpr int R = (65536 - 128 * kProducerRegs - 128 * kTmemEpiRegs) / Cfg::THREADS / 8 * 8;
+    // setmaxnreg only redistributes the registers the CTA was launched with
+    // (65536 / 512 threads = 128 each): an increase that the decreases do not
+    // cover blocks forever
+    constexpr int kLaunchRegs = 65536 / (Cfg::THREADS + 256) / 8 * 8;
+    static_assert(128 * kProducerRegs + 128 * kTmemEpiRegs + Cfg::THREADS * (R > 232 ? 232 : R) <=
+                      kLaunchRegs * (Cfg::THREADS + 256),
+                  "register pool of the CTA exceeded");
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(R > 232 ? 232 : R));
   }
   const int wm = warp / Cfg::WARPS_N;
