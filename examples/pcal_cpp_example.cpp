@@ -4,6 +4,7 @@
 //   usage: pcal_cpp_example [n p]
 #include <cmath>
 #include <cstdio>
+#include <algorithm>
 #include <cstdlib>
 #include <vector>
 
@@ -40,6 +41,14 @@ int main(int argc, char** argv) {
                   r6.final_post_orth ? r6.final_post_orth->fval : NAN,
                   r6.final_post_orth ? r6.final_post_orth->feas : NAN);
       if (!r6.final_post_orth || r6.final_post_orth->feas > 1e-12) return 4;
+      // the reference's diagnostics on the final iterate (diagnostics.cpp:21-47)
+      const double kkt = kkt_violation(p6, r6.final_x), feas = feasibility_violation(r6.final_x);
+      const double fd = fd_gradient_check(p6, r6.final_x);
+      std::printf("p6 diagnostics: kkt=%.3e (report %.3e) feas=%.3e fd=%.3e merit=%.12f\n", kkt,
+                  r6.final_post_orth->kkt_abs, feas, fd, merit_h(p6, r6.final_x, 1.0));
+      if (std::abs(kkt - r6.final_post_orth->kkt_abs) > 1e-6 * std::max(kkt, 1e-300) + 1e-12 ||
+          feas > 1e-12 || fd > 1e-6)
+        return 5;
     }
     // parameter errors are thrown before iterating (solver.cpp:106-118)
     cfg.tol_rel_kkt = 0.0;

@@ -17,6 +17,7 @@
 #include <optional>
 #include <stdexcept>
 #include <string>
+#include <cmath>
 #include <vector>
 
 #include "../pcal_b200.h"
@@ -361,5 +362,79 @@ inline DenseMatrix initial_point(const InitialPointSpec& spec, std::int64_t n, s
 
 // flops_estimate(Pcal, n, p) (diagnostics.cpp:100-114)
 inline double flops_estimate(std::int64_t n, std::int64_t p) { return pcal_flops_estimate(n, p); }
+
+// ---- evaluation and diagnostics (problems.hpp:39,148-149; diagnostics.hpp) ----------
+struct Evaluation {  // problems.hpp:18-22
+  double value = 0.0;
+  DenseMatrix gradient;
+};
+inline Evaluation evaluate(const ObjectiveModel& model, const DenseMatrix& x, int device = 0) {
+  Evaluation ev;
+  ev.gradient = DenseMatrix(x.rows(), x.cols());
+  check(pcal_evaluate(&model.desc(), x.data(), &ev.value, ev.gradient.data(), device));
+  return ev;
+}
+
+// fd_gradient_check with the device evaluation (problems.cpp:296-325)
+inline double fd_gradient_check(const ObjectiveModel& model, const DenseMatrix& x,
+                                double h = 1e-5, std::uint64_t seed = 0x5eedc0de,
+                                int device = 0) {
+  double w = 0.0;
+  check(pcal_fd_gradient_check(&model.desc(), x.data(), h, seed, device, &w));
+  return w;
+}
+
+namespace detail {
+inline DenseMatrix sym_at_b(const DenseMatrix& a, const DenseMatrix& b, int device) {
+  DenseMatrix m(a.cols(), b.cols());
+  check(pcal_matmul_at_b(a.data(), b.data(), a.rows(), a.cols(), b.cols(), m.data(), device));
+  DenseMatrix w(m.rows(), m.cols());
+  for (std::int64_t j = 0; j < m.cols(); ++j)
+    for (std::int64_t i = 0; i < m.rows(); ++i) w(i, j) = 0.5 * (m(i, j) + m(j, i));
+  return w;
+}
+inline DenseMatrix gram_minus_identity(const DenseMatrix& x, int device) {
+  DenseMatrix c(x.cols(), x.cols());
+  check(pcal_gram(x.data(), x.rows(), x.cols(), c.data(), device));
+  for (std::int64_t j = 0; j < c.cols(); ++j) c(j, j) -= 1.0;
+  return c;
+}
+inline double fro(const DenseMatrix& m) {
+  double s = 0.0;
+  for (std::size_t k = 0; k < m.size(); ++k) s += m.data()[k] * m.data()[k];
+  return std::sqrt(s);
+}
+}  // namespace detail
+
+// ‖G − X·Ψ(GᵀX)‖_F (diagnostics.cpp:21-30): the n×p products on the device
+inline double kkt_violation(const DenseMatrix& grad_f, const DenseMatrix& x, int device = 0) {
+  if (grad_f.rows() != x.rows() || grad_f.cols() != x.cols())
+    throw dimension_error("kkt_violation: shape mismatch");
+  const DenseMatrix w = detail::sym_at_b(grad_f, x, device);
+  DenseMatrix xw(x.rows(), x.cols());
+  check(pcal_matmul(x.data(), w.data(), x.rows(), x.cols(), x.cols(), xw.data(), device));
+  for (std::size_t k = 0; k < xw.size(); ++k) xw.data()[k] = grad_f.data()[k] - xw.data()[k];
+  return detail::fro(xw);
+}
+inline double kkt_violation(const ObjectiveModel& model, const DenseMatrix& x, int device = 0) {
+  return kkt_violation(evaluate(model, x, device).gradient, x, device);
+}
+// ‖XᵀX − I‖_F (diagnostics.cpp:32-36)
+inline double feasibility_violation(const DenseMatrix& x, int device = 0) {
+  return detail::fro(detail::gram_minus_identity(x, device));
+}
+// f(X) − ½⟨Ψ(GᵀX), XᵀX − I⟩ + β/4‖XᵀX − I‖² (diagnostics.cpp:38-47)
+inline double merit_h(const ObjectiveModel& model, const DenseMatrix& x, double beta,
+                      int device = 0) {
+  const Evaluation ev = evaluate(model, x, device);
+  const DenseMatrix w = detail::sym_at_b(ev.gradient, x, device);
+  const DenseMatrix c = detail::gram_minus_identity(x, device);
+  double cross = 0.0, feas2 = 0.0;
+  for (std::size_t k = 0; k < c.size(); ++k) {
+    cross += w.data()[k] * c.data()[k];
+    feas2 += c.data()[k] * c.data()[k];
+  }
+  return ev.value - 0.5 * cross + 0.25 * beta * feas2;
+}
 
 }  // namespace orthopt_b200
