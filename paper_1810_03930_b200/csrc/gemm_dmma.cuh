@@ -651,9 +651,22 @@ __global__ void __launch_bounds__(Cfg::THREADS + 256, 1) gemm_xm_tmem(GemmArgs g
   if (warp >= Cfg::WARPS + 4) {  // epilogue warpgroup: warp q reads TMEM lanes [32q, 32q+32)
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kTmemEpiRegs));
     const int wn = warp & 3;
+    const EpiParams& e = g.ep;
     for (int t = t0; t < t1; ++t) {
       const int buf = (t - t0) & 1;
       const unsigned ph = (unsigned)((t - t0) >> 1) & 1u;
+      {  // while the tile is still being multiplied: its G / X columns into L2
+        // (lane c: column j0 + c/2 of G or X, the tile's 128 rows, one bulk prefetch)
+        const int2 tp = g.tiles[t];
+        const int64_t m0 = (int64_t)tp.x * Cfg::BM;
+        const int64_t rows = e.n - m0 < Cfg::BM ? e.n - m0 : Cfg::BM;
+        const int64_t j = ((int64_t)tp.y * Cfg::BN + wn * Cfg::WN) / 2 + (lane >> 1);
+        if (rows > 0 && j < e.p) {
+          const double* src = ((lane & 1) ? e.X : e.G) + m0 + j * e.ld;
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src),
+                       "r"((unsigned)((rows * 8 + 15) & ~15ll)) : "memory");
+        }
+      }
       mbar_wait(&acc_full[buf], ph);
       asm volatile("tcgen05.fence::after_thread_sync;\n");
       const int2 tc = g.tiles[t];
