@@ -112,3 +112,25 @@ def test_alm_report_json_counters(pcal, orc):
     j = json.loads(R.to_json(rep, echo))
     assert (j["outer_iterations"], j["inner_cap_hits"]) == (5, 5)
     assert j["config"]["solver"] == "alm"
+
+
+@pytest.mark.parametrize("kind", ["stencil", "p4"])
+def test_alm_on_every_model_family(pcal, orc, kind):
+    """ALM runs on the grid and bilinear device models as on the dense one (the
+    engine is model-agnostic): converges, post-orth feasible, at PLAM's optimum.
+    (p = 5 on the 8×8×6 grid: the lowest Laplacian cluster, 1 + 4 modes, ends
+    at a spectral gap, so the subspace is well defined.)"""
+    from paper_1810_03930_b200 import harness as H
+    if kind == "stencil":
+        grid, n, p = (8, 8, 6), 8 * 8 * 6, 5
+        v = orc.random_uniform(n, 3)
+        m = pcal.StencilModel(grid, v, p, 12.0 + v.max())
+    else:
+        n, p = 60, 4
+        m = H.make_problem(H.ProblemSpec(kind=kind, n=n, p=p, seed=51))
+    x0 = pcal.initial_point(n, p, 52)
+    ra = pcal.solve(m, pcal.SolverConfig(algorithm="alm", max_iter=5000), x0)
+    rp = pcal.solve(m, pcal.SolverConfig(algorithm="plam", max_iter=5000), x0)
+    assert ra.status == "converged" and rp.status == "converged"
+    assert ra.final_post_orth.feas <= 1e-12 and ra.outer_iterations >= 1
+    assert abs(ra.final_post_orth.fval - rp.final_post_orth.fval) <= 1e-6 * abs(rp.final_post_orth.fval)
