@@ -178,6 +178,13 @@ def cpu_reference_rate(inst, x0, budget_s: float = 15.0, threads: int = None, mi
     return 1.0 / per, info
 
 
+WORKLOADS = {1: "config 1: dense trace-min n=1000 p=20 (A=sym(randn), seed 1)",
+             2: "config 2: dense trace-min n=16384 p=128 (A=sym(randn), seed 1)",
+             3: "config 3: 7-pt periodic Laplacian + diag V, 64^3, p=256, seed 1",
+             4: "config 4: Kohn-Sham-like 48^3, p=512, seed 1",
+             5: "config 5: 7-pt Laplacian + diag V, 128^3, p=1024, seed 1"}
+
+
 def run_reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -205,8 +212,8 @@ def run_reference_arm(args):
             "unit": "iterations/s", "n_gpus": args.gpus, "steps": info["iters"],
             "warmup": 1, "ms_per_step": 1e3 / rate, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"config {inst.cfg}", "n": inst.n, "p": inst.p,
-                       "kind": inst.kind},
+            "config": {"workload": WORKLOADS[args.config], "n": inst.n, "p": inst.p,
+                       "kind": inst.kind, "s": inst.s},
             "cpu_baseline": {"value": rate, "unit": "iterations/s", "cores": info["cores"],
                              "kind": info["kind"], "sample": info["sample"],
                              "cpu_model": info["cpu_model"]},
@@ -382,11 +389,7 @@ def main():
                    "sample": f"failed: {e}"}
 
     if rank == 0:
-        wl = {1: "config 1: dense trace-min n=1000 p=20 (A=sym(randn), seed 1)",
-              2: "config 2: dense trace-min n=16384 p=128 (A=sym(randn), seed 1)",
-              3: "config 3: 7-pt periodic Laplacian + diag V, 64^3, p=256, seed 1",
-              4: "config 4: Kohn-Sham-like 48^3, p=512, seed 1",
-              5: "config 5: 7-pt Laplacian + diag V, 128^3, p=1024, seed 1"}[args.config]
+        wl = WORKLOADS[args.config]
         line = {
             "metric": "PCAL iterations/sec", "value": value, "unit": "iterations/s",
             "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": ms_per,
