@@ -400,6 +400,17 @@ __device__ void finish_record(const FinishArgs& a, Ctl* ctl, double* post, doubl
 // ALM outer step (solver.cpp:562-574), before the multiplier update's
 // evaluation: the inner loop's iterate (its best one after a cap) has been
 // copied to the other pair; the stepsize memory restarts with the next loop.
+// Sharded ALM: the chunk-ordered column sums of the third partial are Σ P²
+// (‖∇L‖²), not d; move them to glcol and leave d = 0 for the plain step.
+__global__ void k_alm_split(double* __restrict__ d, double* __restrict__ gl, int64_t p,
+                            const Ctl* ctl) {
+  if (ctl && ctl->done) return;
+  for (int64_t j = threadIdx.x; j < p; j += blockDim.x) {
+    gl[j] = d[j];
+    d[j] = 0.0;
+  }
+}
+
 __global__ void k_alm_boundary(Ctl* c) {
   if (c->done) return;
   if (!c->alm_met) {
@@ -916,7 +927,8 @@ static void launch_eval(pcal_session* s, int b, int mode, const Ctl* ctl_guard) 
     a.rpc[0] = dense_family(s->model.kind) ? s->chunk_rows / cfg_info(pick_size(s->pp)).WM
                                                  : s->model.ny / 8;
     a.in[1] = s->kpart.p;
-    a.in[2] = dform ? s->dpart.p : nullptr;
+    const bool alm = s->alg == PCAL_ALG_ALM;
+    a.in[2] = (dform || alm) ? s->dpart.p : nullptr;
     for (int w = 1; w < 3; ++w) {
       a.nrows[w] = s->nrb_xm;
       a.stride[w] = s->pstride_xm;
@@ -932,6 +944,10 @@ static void launch_eval(pcal_session* s, int b, int mode, const Ctl* ctl_guard) 
     k_flags<<<1, 1, 0, st>>>(s->ctl, s->bad, s->cc.p + s->nch_max * 3 * s->p);
     launched("k_flags");
     chunk_reduce(s, s->cc.p, 3 * s->p, s->fkd[b].p, ctl_guard, 2);
+    if (alm) {
+      k_alm_split<<<1, 256, 0, st>>>(Dvec(s, b), s->glcol.p, s->p, ctl_guard);
+      launched("k_alm_split");
+    }
   } else {
     launch_colsums(s, s->fpart.p, s->nrb_f, s->kpart.p, s->dpart.p, s->nrb_xm, Fcol(s, b),
                    Kcol(s, b), Dvec(s, b), ctl_guard);
@@ -1831,8 +1847,6 @@ void session_create(const pcal_model_desc* model, const pcal_config* config, con
               s->alg != PCAL_ALG_MOPTQR && !getenv("PCAL_FULL_GX");
   if (comm && s->alg == PCAL_ALG_MOPTQR)
     throw Error(PCAL_E_UNSUPPORTED, "MOptQR is single-GPU (its MGS2 fallback is not sharded)");
-  if (comm && s->alg == PCAL_ALG_ALM)
-    throw Error(PCAL_E_UNSUPPORTED, "ALM is single-GPU (host-driven outer loop)");
   if (comm && model->kind == PCAL_MODEL_DEVICE_CALLBACK)
     throw Error(PCAL_E_UNSUPPORTED, "device-callback models are single-GPU");
   // resolve_beta (solver.cpp:120-134)

@@ -134,3 +134,23 @@ def test_alm_on_every_model_family(pcal, orc, kind):
     assert ra.status == "converged" and rp.status == "converged"
     assert ra.final_post_orth.feas <= 1e-12 and ra.outer_iterations >= 1
     assert abs(ra.final_post_orth.fval - rp.final_post_orth.fval) <= 1e-6 * abs(rp.final_post_orth.fval)
+
+
+def test_alm_sharded_bitwise_across_rank_counts(pcal, orc):
+    """ALM on the row-sharded path (emulated ranks): every rank takes the same
+    outer decisions from the allreduced ‖∇L‖, and 1–3 ranks give bitwise
+    identical reports; the run also matches the reference's
+    golden counters and the single-GPU trace window."""
+    from paper_1810_03930_b200 import report_io
+    g = np.load(os.path.join(GOLD, "reference_alm.npz"))
+    model, x0 = _instance(pcal, orc, "c1")
+    cfg = pcal.SolverConfig(algorithm="alm", alm=pcal.AlmOptions(7, 50, 0.1), max_iter=60)
+    reps = [pcal.solve_emulated(model, cfg, x0, R) for R in (1, 2, 3)]
+    outer, caps = (int(v) for v in g["c1_caps_counts"])
+    assert reps[0].status == "max_iter" and reps[0].iterations == 60
+    assert (reps[0].outer_iterations, reps[0].inner_cap_hits) == (outer, caps)
+    for r in reps[1:]:
+        assert report_io.same_numerics(reps[0], r)
+        assert (r.outer_iterations, r.inner_cap_hits) == (outer, caps)
+    single = pcal.solve(model, cfg, x0)
+    assert close(reps[0].trace[:25, 1], single.trace[:25, 1], 1e-9)
