@@ -208,6 +208,151 @@ __global__ void __launch_bounds__(32 * TY, PCAL_STENCIL_MINB)
   if (__syncthreads_or(nonfinite) && lane == 0 && ty == 0) *bad = 1;
 }
 
+// Full-row variant (nx = 32·XP, XP even): lane l owns the XP consecutive
+// points x = XP·l … XP·l + XP − 1, so X, u and G move as 16-byte vectors and
+// the x-neighbours come from registers and two warp shuffles (the row is
+// exactly one warp wide, so the periodic wrap is the lane wrap); shared memory
+// carries only the y-neighbour rows.  Same operands in the same order as
+// k_stencil_march: G is bitwise identical; the f partial sums its terms in a
+// different (fixed) per-thread order.
+template <bool KS, int XP, int TY>
+__global__ void __launch_bounds__(32 * TY, PCAL_STENCIL_MINB)
+    k_stencil_march_row(const double* __restrict__ x, const double* __restrict__ u,
+                        double* __restrict__ g, int nx, int ny, int nz, int64_t ld, int zchunk,
+                        double* __restrict__ fpart, int64_t pstride, int32_t* bad, const Ctl* ctl,
+                        const double* __restrict__ hlo, const double* __restrict__ hhi,
+                        int zpart) {
+  static_assert(XP % 2 == 0, "full-row march: XP even (16-byte vectors)");
+  constexpr int V = XP / 2;
+  if (ctl && ctl->done) return;
+  __shared__ __align__(16) double pl[TY + 2][32 * XP];
+  __shared__ double sm[TY];
+  const int lane = threadIdx.x, ty = threadIdx.y;
+  const int y0 = blockIdx.x * TY;
+  const int z0 = blockIdx.y * zchunk;
+  const int z1 = min(nz, z0 + zchunk);
+  const int64_t j = blockIdx.z;
+  const int y = y0 + ty;
+  const int64_t nxy = (int64_t)nx * ny;
+  const double* xj = x + j * ld;
+  double* gj = g + j * ld;
+  const int yh = ty == 0 ? (y0 == 0 ? ny - 1 : y0 - 1) : (y0 + TY == ny ? 0 : y0 + TY);
+  const bool hrow = ty == 0 || ty == TY - 1;
+  const int64_t row = (int64_t)y * nx + XP * lane, hrw = (int64_t)yh * nx + XP * lane;
+  auto src = [&](int z) -> const double* {
+    if (hlo) {
+      if (z < 0) return hlo + j * nxy;
+      if (z >= nz) return hhi + j * nxy;
+      return xj + (int64_t)z * nxy;
+    }
+    return xj + (int64_t)((z % nz + nz) % nz) * nxy;
+  };
+  auto ld2 = [](const double* p, double (&d)[XP]) {
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const double2 t = __ldg(reinterpret_cast<const double2*>(p) + v);
+      d[2 * v] = t.x;
+      d[2 * v + 1] = t.y;
+    }
+  };
+  double below[XP], cur[XP], above[XP], halo[XP], halo_n[XP], uc[XP];
+  ld2(src(z0 - 1) + row, below);
+  ld2(src(z0) + row, cur);
+  ld2(src(z0 + 1) + row, above);
+  ld2(u + (int64_t)z0 * nxy + row, uc);
+#pragma unroll
+  for (int k = 0; k < XP; ++k) halo[k] = halo_n[k] = 0.0;
+  if (hrow) {
+    ld2(src(z0) + hrw, halo);
+    if (z0 + 1 < z1) ld2(src(z0 + 1) + hrw, halo_n);
+  }
+  double acc = 0.0;
+  bool nonfinite = false;
+  int zw = (z0 + 2) % nz;
+  int zp_cnt = z0 % zpart, zp_idx = z0 / zpart;
+  double2* prow = reinterpret_cast<double2*>(&pl[ty + 1][XP * lane]);
+  double2* phal = reinterpret_cast<double2*>(&pl[ty == 0 ? 0 : TY + 1][XP * lane]);
+  const double2* pdn = reinterpret_cast<const double2*>(&pl[ty][XP * lane]);
+  const double2* pup = reinterpret_cast<const double2*>(&pl[ty + 2][XP * lane]);
+  for (int z = z0; z < z1; ++z) {
+    const double* sa = hlo ? src(z + 2) : xj + (int64_t)zw * nxy;
+    zw = zw + 1 == nz ? 0 : zw + 1;
+    const int64_t pz = (int64_t)z * nxy, pn = pz + nxy;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      prow[v] = make_double2(cur[2 * v], cur[2 * v + 1]);
+      if (hrow) phal[v] = make_double2(halo[2 * v], halo[2 * v + 1]);
+    }
+    __syncthreads();
+    double above2[XP], halo_nn[XP], u_n[XP];
+#pragma unroll
+    for (int k = 0; k < XP; ++k) above2[k] = halo_nn[k] = u_n[k] = 0.0;
+    if (z + 1 < z1) {
+      ld2(sa + row, above2);
+      ld2(u + pn + row, u_n);
+    }
+    if (hrow && z + 2 < z1) ld2(sa + hrw, halo_nn);
+    double dn[XP], up[XP];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const double2 a = pdn[v], b = pup[v];
+      dn[2 * v] = a.x;
+      dn[2 * v + 1] = a.y;
+      up[2 * v] = b.x;
+      up[2 * v + 1] = b.y;
+    }
+    const double left = __shfl_sync(0xffffffffu, cur[XP - 1], (lane + 31) & 31);
+    const double right = __shfl_sync(0xffffffffu, cur[0], (lane + 1) & 31);
+    double gv[XP];
+#pragma unroll
+    for (int k = 0; k < XP; ++k) {
+      const double xv = cur[k];
+      double lx = __dmul_rn(6.0, xv);
+      lx = __dsub_rn(lx, k == 0 ? left : cur[k - 1]);
+      lx = __dsub_rn(lx, k == XP - 1 ? right : cur[k + 1]);
+      lx = __dsub_rn(lx, dn[k]);
+      lx = __dsub_rn(lx, up[k]);
+      lx = __dsub_rn(lx, below[k]);
+      lx = __dsub_rn(lx, above[k]);
+      if (KS) gv[k] = __dadd_rn(__dmul_rn(0.5, lx), __dmul_rn(uc[k], xv));
+      else gv[k] = __dadd_rn(lx, __dmul_rn(uc[k], xv));
+      acc += KS ? xv * lx : xv * gv[k];
+      if (KS) nonfinite |= !isfinite(gv[k]);
+    }
+    double2* gout = reinterpret_cast<double2*>(gj + pz + row);
+#pragma unroll
+    for (int v = 0; v < V; ++v) gout[v] = make_double2(gv[2 * v], gv[2 * v + 1]);
+#pragma unroll
+    for (int k = 0; k < XP; ++k) {
+      below[k] = cur[k];
+      cur[k] = above[k];
+      above[k] = above2[k];
+      halo[k] = halo_n[k];
+      halo_n[k] = halo_nn[k];
+      uc[k] = u_n[k];
+    }
+    if (++zp_cnt == zpart || z + 1 == z1) {
+      if (!KS) nonfinite |= !isfinite(acc);
+      const double v = warp_sum(acc);
+      if (lane == 0) sm[ty] = v;
+      __syncthreads();
+      if (lane == 0 && ty == 0) {
+        double sacc = 0.0;
+#pragma unroll
+        for (int t = 0; t < TY; ++t) sacc += sm[t];
+        fpart[j * pstride + blockIdx.x + (int64_t)gridDim.x * zp_idx] = sacc;
+      }
+      acc = 0.0;
+      if (zp_cnt == zpart) {
+        zp_cnt = 0;
+        ++zp_idx;
+      }
+    }
+    __syncthreads();
+  }
+  if (__syncthreads_or(nonfinite) && lane == 0 && ty == 0) *bad = 1;
+}
+
 // Halo send planes of a z-slab: lo = plane 0, hi = plane nzl−1 of every column.
 __global__ void k_pack_planes(const double* __restrict__ x, int64_t ld, int64_t nxy, int64_t nzl,
                               double* __restrict__ lo, double* __restrict__ hi, const Ctl* ctl) {

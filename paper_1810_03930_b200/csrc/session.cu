@@ -755,7 +755,19 @@ static void launch_stencil(pcal_session* s, int b, const double* u, bool ks, con
   k_stencil_march<KSV, XPV, 8><<<grid, block, 0, s->stream>>>(                               \
       Xof(s, b), u, Pof(s, b), (int)m.nx, (int)m.ny, (int)s->gz, s->ld, (int)s->st_zchunk,     \
       s->fpart.p, s->pstride_f, s->bad, ctl, hlo, hhi, (int)s->st_zpart)
-    if (ks) {
+#define PCAL_MARCH_ROW(KSV, XPV)                                                               \
+  k_stencil_march_row<KSV, XPV, 8><<<grid, block, 0, s->stream>>>(                           \
+      Xof(s, b), u, Pof(s, b), (int)m.nx, (int)m.ny, (int)s->gz, s->ld, (int)s->st_zchunk,     \
+      s->fpart.p, s->pstride_f, s->bad, ctl, hlo, hhi, (int)s->st_zpart)
+    // rows of exactly 64 or 128 points: the vectorised full-row kernel
+    const bool full_row = (m.nx == 64 || m.nx == 128) && !getenv("PCAL_NO_ROW_MARCH");
+    if (full_row) {
+      if (ks) {
+        if (xp == 2) PCAL_MARCH_ROW(true, 2); else PCAL_MARCH_ROW(true, 4);
+      } else {
+        if (xp == 2) PCAL_MARCH_ROW(false, 2); else PCAL_MARCH_ROW(false, 4);
+      }
+    } else if (ks) {
       if (xp == 1) PCAL_MARCH(true, 1); else if (xp == 2) PCAL_MARCH(true, 2);
       else if (xp == 3) PCAL_MARCH(true, 3); else PCAL_MARCH(true, 4);
     } else {
@@ -763,6 +775,7 @@ static void launch_stencil(pcal_session* s, int b, const double* u, bool ks, con
       else if (xp == 3) PCAL_MARCH(false, 3); else PCAL_MARCH(false, 4);
     }
 #undef PCAL_MARCH
+#undef PCAL_MARCH_ROW
     launched("k_stencil_march");
   } else {
     dim3 g((unsigned)s->st_nchunks, (unsigned)p);
