@@ -208,11 +208,11 @@ __global__ void __launch_bounds__(32 * TY, PCAL_STENCIL_MINB)
   if (__syncthreads_or(nonfinite) && lane == 0 && ty == 0) *bad = 1;
 }
 
-// Full-row variant (nx = 32·XP, XP even): lane l owns the XP consecutive
-// points x = XP·l … XP·l + XP − 1, so X, u and G move as 16-byte vectors and
-// the x-neighbours come from registers and two warp shuffles (the row is
-// exactly one warp wide, so the periodic wrap is the lane wrap); shared memory
-// carries only the y-neighbour rows.  Same operands in the same order as
+// Full-row variant (nx = L·XP with L ≤ 32 active lanes, XP even): lane l owns
+// the XP consecutive points x = XP·l … XP·l + XP − 1, so X, u and G move as
+// 16-byte vectors and the x-neighbours come from registers and two warp
+// shuffles (one row per warp: the periodic wrap is the wrap over the L active
+// lanes); shared memory carries only the y-neighbour rows.  Same operands in the same order as
 // k_stencil_march: G is bitwise identical; the f partial sums its terms in a
 // different (fixed) per-thread order.
 template <bool KS, int XP, int TY>
@@ -228,6 +228,9 @@ __global__ void __launch_bounds__(32 * TY, PCAL_STENCIL_MINB)
   __shared__ __align__(16) double pl[TY + 2][32 * XP];
   __shared__ double sm[TY];
   const int lane = threadIdx.x, ty = threadIdx.y;
+  const int L = nx / XP;      // active lanes
+  const int ln = lane < L ? lane : L - 1;  // idle lanes shadow the last one (no stores)
+  const bool act = lane < L;
   const int y0 = blockIdx.x * TY;
   const int z0 = blockIdx.y * zchunk;
   const int z1 = min(nz, z0 + zchunk);
@@ -238,7 +241,7 @@ __global__ void __launch_bounds__(32 * TY, PCAL_STENCIL_MINB)
   double* gj = g + j * ld;
   const int yh = ty == 0 ? (y0 == 0 ? ny - 1 : y0 - 1) : (y0 + TY == ny ? 0 : y0 + TY);
   const bool hrow = ty == 0 || ty == TY - 1;
-  const int64_t row = (int64_t)y * nx + XP * lane, hrw = (int64_t)yh * nx + XP * lane;
+  const int64_t row = (int64_t)y * nx + XP * ln, hrw = (int64_t)yh * nx + XP * ln;
   auto src = [&](int z) -> const double* {
     if (hlo) {
       if (z < 0) return hlo + j * nxy;
@@ -274,6 +277,7 @@ __global__ void __launch_bounds__(32 * TY, PCAL_STENCIL_MINB)
   double2* phal = reinterpret_cast<double2*>(&pl[ty == 0 ? 0 : TY + 1][XP * lane]);
   const double2* pdn = reinterpret_cast<const double2*>(&pl[ty][XP * lane]);
   const double2* pup = reinterpret_cast<const double2*>(&pl[ty + 2][XP * lane]);
+  const int lsrc = ln == 0 ? L - 1 : ln - 1, rsrc = ln == L - 1 ? 0 : ln + 1;
   for (int z = z0; z < z1; ++z) {
     const double* sa = hlo ? src(z + 2) : xj + (int64_t)zw * nxy;
     zw = zw + 1 == nz ? 0 : zw + 1;
@@ -301,8 +305,8 @@ __global__ void __launch_bounds__(32 * TY, PCAL_STENCIL_MINB)
       up[2 * v] = b.x;
       up[2 * v + 1] = b.y;
     }
-    const double left = __shfl_sync(0xffffffffu, cur[XP - 1], (lane + 31) & 31);
-    const double right = __shfl_sync(0xffffffffu, cur[0], (lane + 1) & 31);
+    const double left = __shfl_sync(0xffffffffu, cur[XP - 1], lsrc);
+    const double right = __shfl_sync(0xffffffffu, cur[0], rsrc);
     double gv[XP];
 #pragma unroll
     for (int k = 0; k < XP; ++k) {
@@ -316,12 +320,16 @@ __global__ void __launch_bounds__(32 * TY, PCAL_STENCIL_MINB)
       lx = __dsub_rn(lx, above[k]);
       if (KS) gv[k] = __dadd_rn(__dmul_rn(0.5, lx), __dmul_rn(uc[k], xv));
       else gv[k] = __dadd_rn(lx, __dmul_rn(uc[k], xv));
-      acc += KS ? xv * lx : xv * gv[k];
-      if (KS) nonfinite |= !isfinite(gv[k]);
+      if (act) {
+        acc += KS ? xv * lx : xv * gv[k];
+        if (KS) nonfinite |= !isfinite(gv[k]);
+      }
     }
-    double2* gout = reinterpret_cast<double2*>(gj + pz + row);
+    if (act) {
+      double2* gout = reinterpret_cast<double2*>(gj + pz + row);
 #pragma unroll
-    for (int v = 0; v < V; ++v) gout[v] = make_double2(gv[2 * v], gv[2 * v + 1]);
+      for (int v = 0; v < V; ++v) gout[v] = make_double2(gv[2 * v], gv[2 * v + 1]);
+    }
 #pragma unroll
     for (int k = 0; k < XP; ++k) {
       below[k] = cur[k];

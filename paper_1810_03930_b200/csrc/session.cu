@@ -759,13 +759,14 @@ static void launch_stencil(pcal_session* s, int b, const double* u, bool ks, con
   k_stencil_march_row<KSV, XPV, 8><<<grid, block, 0, s->stream>>>(                           \
       Xof(s, b), u, Pof(s, b), (int)m.nx, (int)m.ny, (int)s->gz, s->ld, (int)s->st_zchunk,     \
       s->fpart.p, s->pstride_f, s->bad, ctl, hlo, hhi, (int)s->st_zpart)
-    // rows of exactly 64 or 128 points: the vectorised full-row kernel
-    const bool full_row = (m.nx == 64 || m.nx == 128) && !getenv("PCAL_NO_ROW_MARCH");
-    if (full_row) {
+    // rows of an even number of points ≤ 64, or a multiple of 4 ≤ 128: the
+    // vectorised full-row kernel (XP consecutive points per lane)
+    const int rxp = m.nx % 2 == 0 && m.nx <= 64 ? 2 : m.nx % 4 == 0 && m.nx <= 128 ? 4 : 0;
+    if (rxp && !getenv("PCAL_NO_ROW_MARCH")) {
       if (ks) {
-        if (xp == 2) PCAL_MARCH_ROW(true, 2); else PCAL_MARCH_ROW(true, 4);
+        if (rxp == 2) PCAL_MARCH_ROW(true, 2); else PCAL_MARCH_ROW(true, 4);
       } else {
-        if (xp == 2) PCAL_MARCH_ROW(false, 2); else PCAL_MARCH_ROW(false, 4);
+        if (rxp == 2) PCAL_MARCH_ROW(false, 2); else PCAL_MARCH_ROW(false, 4);
       }
     } else if (ks) {
       if (xp == 1) PCAL_MARCH(true, 1); else if (xp == 2) PCAL_MARCH(true, 2);
