@@ -3,25 +3,31 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl reference]
 
-A "step" is one PCAL iteration (solver.cpp:369-439) of config C (default 2:
-dense trace minimization, n=16384, p=128, FP64 — BASELINE configs[1]).
+A "step" is one PCAL iteration (solver.cpp:369-439) of config C (default 5:
+the 7-point Laplacian + diagonal potential on a 128³ periodic grid, p = 1024,
+FP64 — BASELINE configs[4], the 1/2/4/8-GPU sweep the metric is quoted on and
+the largest configuration that fits one GPU).
   value : iterations/s with the instance resident in HBM, K iterations timed
           with CUDA events on the session stream (graphs, no host sync), max
-          over ranks; the operator A (2 GiB) is larger than L2, so every
+          over ranks; the working set (X, P, X_prev, P_prev: 64 GiB at config 5;
+          the 2 GiB dense A at config 2) is far larger than L2, so every
           iteration streams it from HBM (no L2 flush needed).
-  e2e   : the public drop-in call pcal_solve() (host buffers: H2D of A and X0
-          from pinned memory, D2H of the report) for the config's full
-          iteration count + final orthonormalization, wall clock.
+  e2e   : the public drop-in call pcal_solve() (host buffers: H2D of the operator
+          and X0 from pinned memory, D2H of the report and X) for the config's
+          full iteration count + final orthonormalization, wall clock.
   roofline : dominant kernel, achieved = algorithmic flops (or bytes) per launch
           ÷ its mean CUDA-event duration measured in this run; peak = measured
           FP64 DMMA rate (profiles/fp64_peaks_r01.json; MEASURED_PEAKS.json has
           no FP64 entry) or MEASURED_PEAKS.json hbm_gbs for HBM-bound kernels.
   cpu_baseline : the UNMODIFIED reference solve() (oracle/_ref) on the host
-          cores, per-iteration time from its own trace clock, bounded sample.
+          cores, per-iteration time from its own trace clock, bounded sample
+          (config 5: a z-slab of the grid, time scaled by n / n_slab — the
+          reference needs ≈190 GiB and ≈30 min per full-size iteration).
 --impl reference times that CPU implementation alone (rank 0; others exit 0).
-N > 1: one process per GPU (torchrun); the instance is ROW-SHARDED over the
-ranks (z-slabs / row blocks, NCCL collectives): strong scaling,
-value = K / max-over-ranks time.
+N > 1: one process per GPU (torchrun; `--gpus N` without torchrun spawns the N
+ranks itself); the instance is ROW-SHARDED over the ranks (z-slabs / row
+blocks, NCCL collectives): strong scaling, value = K /
+max-over-ranks time.
 """
 from __future__ import annotations
 
@@ -154,35 +160,79 @@ def cpu_model() -> str:
     return "unknown"
 
 
-def cpu_reference_rate(inst, x0, budget_s: float = 15.0, threads: int = None, min_iters=1,
-                       max_iters=None):
-    """Time the reference CPU solve() on a bounded sample; returns (iters/s, info)."""
+# Per-iteration reference work is linear in n at fixed p (every term is O(np²)
+# or O(np)), so a configuration too large for the reference on one host is
+# timed on a z-slab of its own grid and scaled by n / n_slab.  Config 5 needs
+# ≈ 12 live n×p matrices in the reference's solve() — ≈ 190 GiB of host RAM
+# against the box's 196 GB — and ≈ 20–35 min per iteration, so its reference
+# sample is the 128×128×SLAB_NZ slab with p = 1024.
+SLAB_NZ = {"reference": 16, "cpu_baseline": 2}
+
+
+def cpu_reference_rate(inst, x0=None, budget_s: float = 15.0, threads: int = None, min_iters=1,
+                       max_iters=None, slab_nz: int = None):
+    """Time the reference CPU solve() on a bounded sample; returns (iters/s, info).
+
+    slab_nz: time the grid model on the nx×ny×slab_nz bottom slab of the same
+    grid (V = the slab's rows of the config's potential, the config's s, the
+    slab's own seeded QR start point) and scale the per-iteration time by
+    n / n_slab."""
     from oracle.oracle import Config, Model, MODEL_DENSE, MODEL_KOHN_SHAM, MODEL_STENCIL
     from oracle.oracle import Reference, Restatement, available_reference
     threads = threads or os.cpu_count() or 1
     R = Reference() if available_reference() else Restatement()
     kind = {"dense": MODEL_DENSE, "stencil": MODEL_STENCIL, "kohn_sham": MODEL_KOHN_SHAM}[inst.kind]
-    m = Model(kind, inst.n, inst.p, inst.s, a=inst.a, grid=inst.grid or (0, 0, 0), v=inst.v)
+    n, grid, v, scale = inst.n, inst.grid or (0, 0, 0), inst.v, 1.0
+    t_setup = time.perf_counter()
+    if slab_nz is not None and inst.kind == "stencil" and slab_nz < grid[2]:
+        grid = (grid[0], grid[1], slab_nz)
+        n = grid[0] * grid[1] * grid[2]
+        v = np.ascontiguousarray(inst.v[:n])
+        scale = inst.n / n
+        x0 = None
+    if x0 is None:  # the threaded C restatement of initial_point (bitwise the reference's)
+        x0 = Restatement().initial_point_qr(n, inst.p, inst.seed ^ INIT_SALT, threads=threads)
+    t_setup = time.perf_counter() - t_setup
+    m = Model(kind, n, inst.p, inst.s, a=inst.a, grid=grid, v=v)
+    t0 = time.perf_counter()
     # probe: one iteration, per-iteration time from the reference's own trace clock
     probe = R.solve(m, Config(tol_rel_kkt=TINY, max_iter=1, threads=threads, final_orth=False), x0)
     t_it = max(probe.trace[1, 6] - probe.trace[0, 6], 1e-6)
     iters = int(max(min_iters, min(inst.iters, max_iters or inst.iters, budget_s / t_it)))
-    rep = R.solve(m, Config(tol_rel_kkt=TINY, max_iter=iters, threads=threads, final_orth=False), x0)
-    per = (rep.trace[iters, 6] - rep.trace[0, 6]) / iters
+    if iters <= 1 and budget_s <= 2 * t_it:  # one iteration already spent the budget
+        rep, iters = probe, 1
+    else:
+        rep = R.solve(m, Config(tol_rel_kkt=TINY, max_iter=iters, threads=threads,
+                                final_orth=False), x0)
+    wall = time.perf_counter() - t0
+    per = (rep.trace[iters, 6] - rep.trace[0, 6]) / iters * scale
     what = "reference solve() (oracle/_ref)" if R.kind == "reference" else "C restatement (oracle)"
     if inst.kind != "dense":
         what += " driving the restated grid operator (no reference operator exists)"
+    where = (f"the {grid[0]}x{grid[1]}x{grid[2]} z-slab (n={n}) of config {inst.cfg}'s grid, "
+             f"p={inst.p}, per-iteration time x n/n_slab = {scale:g}" if scale != 1.0
+             else f"config {inst.cfg} (n={n}, p={inst.p})")
     info = {"kind": R.kind, "cores": threads, "iters": iters, "cpu_model": cpu_model(),
-            "sample": f"{what}: {iters} PCAL iteration(s) of config {inst.cfg} "
-                      f"(n={inst.n}, p={inst.p}), timed by its trace clock, setup excluded"}
+            "sample": f"{what}: {iters} PCAL iteration(s) of {where}, timed by its trace "
+                      f"clock, setup excluded",
+            "sample_n": n, "scale": scale, "setup_s": round(t_setup, 2), "solve_wall_s": round(wall, 2),
+            "host_rss_gib": round(peak_rss_gib(), 2)}
     return 1.0 / per, info
+
+
+def peak_rss_gib() -> float:
+    try:
+        import resource
+        return resource.getrusage(resource.RUSAGE_SELF).ru_maxrss / 2 ** 20
+    except Exception:
+        return float("nan")
 
 
 WORKLOADS = {1: "config 1: dense trace-min n=1000 p=20 (A=sym(randn), seed 1)",
              2: "config 2: dense trace-min n=16384 p=128 (A=sym(randn), seed 1)",
              3: "config 3: 7-pt periodic Laplacian + diag V, 64^3, p=256, seed 1",
              4: "config 4: Kohn-Sham-like 48^3, p=512, seed 1",
-             5: "config 5: 7-pt Laplacian + diag V, 128^3, p=1024, seed 1"}
+             5: "config 5: 7-pt Laplacian + diag V, 128^3, p=1024, seed 1 (scaling sweep)"}
 
 
 def run_reference_arm(args):
@@ -196,6 +246,7 @@ def run_reference_arm(args):
     O = Restatement()
     c = CONFIGS[args.config]
     th = os.cpu_count() or 8
+    slab = None
     if c["kind"] == "dense":
         m = O.dense_trace_min(c["n"], c["p"], 1, s=REFERENCE_S.get((c["n"], 1)), threads=th)
         inst = Instance(args.config, "dense", m.n, m.p, c["iters"], m.s, a=m.a)
@@ -205,9 +256,11 @@ def run_reference_arm(args):
         v = O.random_uniform(nn, 1) if c["kind"] == "stencil" else ks_potential(g, 1, O)
         s = 12.0 + float(v.max()) if c["kind"] == "stencil" else 6.0 + float(np.abs(v).max())
         inst = Instance(args.config, c["kind"], nn, c["p"], c["iters"], s, v=v, grid=g)
-    x0 = O.initial_point_qr(inst.n, inst.p, inst.seed ^ INIT_SALT, threads=th)
+        if args.config == 5:
+            slab = SLAB_NZ["reference"]
     budget = float(os.environ.get("PCAL_REF_BUDGET_S", "60"))
-    rate, info = cpu_reference_rate(inst, x0, budget_s=budget, min_iters=1, max_iters=args.steps)
+    rate, info = cpu_reference_rate(inst, None, budget_s=budget, min_iters=1, max_iters=args.steps,
+                                    slab_nz=slab)
     line = {"metric": "PCAL iterations/sec", "impl": "reference", "value": rate,
             "unit": "iterations/s", "n_gpus": args.gpus, "steps": info["iters"],
             "warmup": 1, "ms_per_step": 1e3 / rate, "higher_is_better": True,
@@ -216,47 +269,73 @@ def run_reference_arm(args):
                        "kind": inst.kind, "s": inst.s},
             "cpu_baseline": {"value": rate, "unit": "iterations/s", "cores": info["cores"],
                              "kind": info["kind"], "sample": info["sample"],
-                             "cpu_model": info["cpu_model"]},
+                             "cpu_model": info["cpu_model"], "sample_n": info["sample_n"],
+                             "scale": info["scale"], "setup_s": info["setup_s"],
+                             "solve_wall_s": info["solve_wall_s"],
+                             "host_rss_gib": info["host_rss_gib"]},
             "e2e": {"value": rate, "unit": "iterations/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
 
+def spawn_ranks(args) -> int:
+    """`bench.py --gpus N` without torchrun: launch N ranks (one per GPU) of this
+    same command through torch.distributed.run and return its exit code."""
+    import socket
+    import subprocess
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=5,
+                    help="BASELINE config (default 5: the 1/2/4/8-GPU sweep the metric names)")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-calls", type=int, default=3)
     ap.add_argument("--sharded", action="store_true",
                     help="use the NCCL row-sharded path even on one GPU (testing)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
 
     import torch
     import paper_1810_03930_b200 as P
     from paper_1810_03930_b200.problems import make_instance
 
     rank, world, local = dist_setup(args.gpus)
+    if args.gpus > 1 and world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     dev = local
     K, W = args.steps, max(args.warmup, 3)
     peaks = load_peaks()
     hostthreads = max(1, (os.cpu_count() or 8) // world)
 
-    # ---- setup (not timed): instance in pinned host memory, X0 on the device
+    # ---- setup (not timed): instance in pinned host memory; X0 = initial_point
+    # ({Qr}, seed) built by the library on the device (PCAL_X0_SEED) — sharded,
+    # each rank draws and orthonormalises only its own rows
+    t_setup = time.perf_counter()
     a_pin = None
     if args.config in (1, 2):
         n = {1: 1000, 2: 16384}[args.config]
         a_t, a_pin = pinned_f64(n, n)
     inst = make_instance(args.config, P, threads=hostthreads, a_out=a_pin, device=dev)
-    x0 = P.initial_point(inst.n, inst.p, inst.seed ^ INIT_SALT, device=dev)
-    prof_iters = 10
+    x0_seed = inst.seed ^ INIT_SALT
+    prof_iters = 10 if args.config < 5 else 4
     cfg = P.SolverConfig(tol_rel_kkt=TINY, max_iter=W + K + prof_iters + 2, final_orth=False,
                          device=dev)
     comm = None
@@ -269,7 +348,6 @@ def main():
         comm = P.Comm(world, rank, obj[0], dev)
         gm = inst.model(P)
         r0, nr = P.partition(gm, world, rank)
-        x0_loc = np.asfortranarray(x0[r0:r0 + nr])
         if inst.kind == "dense":
             a_loc = np.asfortranarray(inst.a[r0:r0 + nr, :])
             model = P.QuadraticModel(a_loc, inst.p, inst.s, n=inst.n)
@@ -277,10 +355,15 @@ def main():
             model = P.StencilModel(inst.grid, inst.v[r0:r0 + nr], inst.p, inst.s)
         else:
             model = P.KohnShamModel(inst.grid, inst.v[r0:r0 + nr], inst.p, inst.s)
-        ses = P.ShardedSession(model, cfg, x0_loc, comm, nr)
+        ses = P.ShardedSession(model, cfg, x0_seed, comm, nr)
     else:
         model = inst.model(P)
-        ses = P.Session(model, cfg, x0)
+        r0, nr = 0, inst.n
+        ses = P.Session(model, cfg, x0_seed)
+    # this rank's rows of X0 in pinned host memory: the e2e call's input
+    x0_t, x0h = pinned_f64(nr, inst.p)
+    ses.get_x(out=x0h)
+    t_setup = time.perf_counter() - t_setup
 
     # ---- value: device-resident iterations, CUDA events on the session stream
     stream = torch.cuda.ExternalStream(ses.stream, device=dev)
@@ -304,6 +387,7 @@ def main():
     phases = ses.profile(prof_iters)      # per-phase CUDA-event durations (same session)
     rep = ses.finish(want_x=False)
     ses.close()
+    del ses
     assert rep.status == "max_iter", rep.status
     ms_per = ms / K
     # sharded: the ranks advance ONE iteration of the problem together (strong
@@ -314,9 +398,11 @@ def main():
     n, p = inst.n, inst.p
     P64 = peaks["fp64_tflops"] * 1e12
     BW = peaks["hbm_gbs"] * 1e9
-    work = {"gradient": (inst.grad_flops(), "tensor") if inst.kind == "dense"
-            else ((16.0 * n * p + inst.op_bytes()), "hbm"),
-            "gram": (3.0 * n * p * p, "tensor"), "xm": (4.0 * n * p * p, "tensor")}
+    nl = nr  # this rank's rows: per-launch work of its kernels
+    gram_flops = (2.0 if inst.kind != "dense" else 3.0) * nl * p * p
+    work = {"gradient": (inst.grad_flops() * nl / n, "tensor") if inst.kind == "dense"
+            else ((16.0 * nl * p + inst.op_bytes() * nl / n), "hbm"),
+            "gram": (gram_flops, "tensor"), "xm": (4.0 * nl * p * p, "tensor")}
     dom = max(("gradient", "gram", "xm"), key=lambda k: phases[k])
     amount, bound = work[dom]
     t = phases[dom] * 1e-3
@@ -334,54 +420,64 @@ def main():
         pass
     F = 7.0 * n * p * p + inst.grad_flops()
     B = 80.0 * n * p + inst.op_bytes()
-    t_star = max(F / P64, B / BW)
+    t_star = max(F / P64, B / BW) / world
     roof = {"bound": bound, "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak,
-            "traffic": traffic, "kernel": dom, "kernel_ms": phases[dom], "peak_src": src}
+            "traffic": traffic, "kernel": dom, "kernel_ms": phases[dom], "peak_src": src,
+            "work_per_launch": amount,
+            "work_def": ("2np^2 (upper tiles of the symmetric G^TX + X^TX)" if dom == "gram"
+                         and inst.kind != "dense" else
+                         {"gram": "3np^2", "xm": "4np^2 (X·[W|C])", "gradient":
+                          "2n^2p" if inst.kind == "dense" else "16np+8n bytes"}[dom])}
     iter_roof = {"flops": F, "bytes": B, "t_star_ms": t_star * 1e3, "frac": t_star * 1e3 / ms_per,
                  "bound": "fp64" if F / P64 >= B / BW else "hbm",
+                 "def": "T* = max(7np^2+F_grad / P_fp64, (80np+B_op) / BW) / n_gpus",
                  "phase_ms": {k: round(v, 5) for k, v in phases.items()}}
 
     # ---- e2e: the public drop-in call with host buffers
     e2e = None
     if not args.no_e2e:
         iters = inst.iters
-        x0h = np.asfortranarray(x0)
         # one untimed 1-iteration call first: module loading and first-use setup
         # of the final-orthonormalisation kernels are not part of a steady call
         warm = P.SolverConfig(tol_rel_kkt=TINY, max_iter=1, device=dev)
+        emodel = model if comm is not None else inst.model(P, a=inst.a if inst.kind == "dense"
+                                                           else None)
         if comm is not None:
-            P.solve_sharded(model, warm, x0_loc, comm, nr)
+            P.solve_sharded(emodel, warm, x0h, comm, nr)
         else:
-            P.solve(inst.model(P, a=inst.a if inst.kind == "dense" else None), warm, x0h)
-        # three timed calls, the median reported: the host↔device copies of one
-        # call vary from run to run on this pool (measured 1.16–1.69 s for config 2)
+            P.solve(emodel, warm, x0h)
+        # timed calls, the median reported: the host↔device copies of one call
+        # vary from run to run on this pool (measured 1.16–1.69 s for config 2)
         walls = []
-        for _ in range(3):
+        for _ in range(max(1, args.e2e_calls)):
             barrier(world)
             t0 = time.perf_counter()
+            ecfg = P.SolverConfig(tol_rel_kkt=TINY, max_iter=iters, device=dev)
             if comm is not None:
-                r = P.solve_sharded(model, P.SolverConfig(tol_rel_kkt=TINY, max_iter=iters,
-                                                          device=dev), x0_loc, comm, nr)
+                r = P.solve_sharded(emodel, ecfg, x0h, comm, nr)
             else:
-                a_host = inst.a if inst.kind == "dense" else None
-                r = P.solve(inst.model(P, a=a_host),
-                            P.SolverConfig(tol_rel_kkt=TINY, max_iter=iters, device=dev), x0h)
+                r = P.solve(emodel, ecfg, x0h)
             walls.append(max_over_ranks(time.perf_counter() - t0, world))
+            post = r.final_post_orth.feas if r.final_post_orth else None
+            del r.final_x, r.stop_iterate
         wall = statistics.median(walls)
         h2d = inst.op_bytes() + 8 * n * p
         d2h = 8 * 2 * n * p + 8 * 7 * (iters + 1)
-        e2e = {"value": r.iterations / wall, "unit": "iterations/s",
-               "h2d_bytes_per_step": h2d / r.iterations, "d2h_bytes_per_step": d2h / r.iterations,
-               "iterations": r.iterations, "wall_s": wall, "walls_s": walls, "status": r.status,
-               "final_post_feas": r.final_post_orth.feas if r.final_post_orth else None,
-               "includes": "H2D A+X0 (pinned), all iterations, final CholeskyQR2, D2H trace+X; "
-                           "median of 3 calls after one untimed 1-iteration call"}
+        e2e = {"value": iters / wall, "unit": "iterations/s",
+               "h2d_bytes_per_step": h2d / iters, "d2h_bytes_per_step": d2h / iters,
+               "iterations": iters, "wall_s": wall, "walls_s": walls, "status": r.status,
+               "final_post_feas": post,
+               "includes": "H2D operator+X0 (pinned), all iterations, final CholeskyQR2, "
+                           "D2H trace + stop/final X; median of the timed calls after one "
+                           "untimed 1-iteration call"}
 
     # ---- CPU baseline (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            rate, info = cpu_reference_rate(inst, np.asfortranarray(x0), budget_s=15.0)
+            rate, info = cpu_reference_rate(
+                inst, np.asfortranarray(x0h) if args.config < 5 else None, budget_s=15.0,
+                slab_nz=SLAB_NZ["cpu_baseline"] if args.config == 5 else None)
             cpu = {"value": rate, "unit": "iterations/s", "cores": info["cores"],
                    "kind": info["kind"], "sample": info["sample"], "cpu_model": info["cpu_model"]}
         except Exception as e:  # reported, never silently substituted
@@ -396,13 +492,15 @@ def main():
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reference RNG stream, seed 1; no dataset)",
             "config": {"workload": wl, "n": n, "p": p, "kind": inst.kind, "s": inst.s,
+                       "iterations_per_solve": inst.iters,
                        "parallelism": "single-gpu" if comm is None
                        else f"row-sharded x{world} (NCCL: Gram/partials allreduce, "
                             f"{'X allgather' if inst.kind == 'dense' else 'z-halo planes'})",
                        "l2": ("inputs larger than L2: A = %.1f GiB streamed every iteration"
                               % (inst.op_bytes() / 2 ** 30)) if inst.kind == "dense"
-                       else "working set (X, P, X_prev, P_prev) larger than L2",
-                       "iteration_graph_kernels": kpi},
+                       else "inputs larger than L2: working set (X, P, X_prev, P_prev) = "
+                            "%.1f GiB" % (4 * 8 * n * p / world / 2 ** 30),
+                       "iteration_graph_kernels": kpi, "setup_s": round(t_setup, 2)},
             "roofline": roof, "iteration_roofline": iter_roof, "cpu_baseline": cpu,
             "e2e": e2e, "clocks": clk.summary(), "gpu_launches": launches,
         }

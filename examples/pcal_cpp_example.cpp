@@ -32,6 +32,16 @@ int main(int argc, char** argv) {
     if (rep.status != RunStatus::Converged || !rep.final_post_orth ||
         rep.final_post_orth->feas > 1e-12)
       return 1;
+    // ConfigEcho as the reference's solve() fills it (solver.cpp:333-342)
+    const ConfigEcho& ce = rep.config;
+    std::printf("echo: problem=%s solver=%s beta=%g eta_rule=%s n=%lld p=%lld threads=%d s=%.6f\n",
+                ce.problem.c_str(), ce.solver.c_str(), ce.beta, ce.eta_rule.c_str(),
+                static_cast<long long>(ce.n), static_cast<long long>(ce.p), ce.threads,
+                ce.curvature_scale);
+    if (ce.problem != "p2" || ce.solver != "pcal" || ce.beta != 1.0 || ce.eta_rule != "abb" ||
+        ce.n != n || ce.p != p || ce.max_iter != cfg.max_iter || ce.curvature_scale != s ||
+        ce.threads != cfg.threads)
+      return 6;
     // the P6 density model on the same operator (problems.cpp:276-285)
     {
       DensityModel p6(a, p, 2.0 * std::cbrt(3.0 / 3.14159265358979323846), ProblemKind::P6, s);

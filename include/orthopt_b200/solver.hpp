@@ -100,7 +100,9 @@ struct SolverConfig {
   MultiplierRule multiplier_rule = MultiplierRule::PcalFormula;
   double tol_rel_kkt = 1e-8;
   std::int64_t max_iter = 3000;
-  int device = 0;  // replaces the explicit thread count: an explicit GPU ordinal
+  int threads = 1;  // accepted for source compatibility (SolverConfig::threads); echoed,
+                    // not used: parallelism is the device's
+  int device = 0;   // the explicit GPU ordinal (never ambient)
   AlmOptions alm{};
   bool final_orth = true;
 };
@@ -117,7 +119,26 @@ struct FinalMetrics {
 struct CategoryTimers {
   double blas3 = 0, func = 0, orth = 0;
 };
+// ConfigEcho (report.hpp:35-49): what solve() ran with, filled like the
+// reference's iterate_main (solver.cpp:333-342); run_single-level fields
+// (seed, init, alpha…) stay at their defaults unless the caller's harness sets them.
+struct ConfigEcho {
+  std::string problem;
+  std::int64_t n = 0;
+  std::int64_t p = 0;
+  std::string solver;
+  double beta = 0.0;
+  std::string eta_rule;
+  double tol_rel_kkt = 0.0;
+  std::int64_t max_iter = 0;
+  int threads = 1;
+  std::string init;
+  std::uint64_t seed = 0;
+  double alpha = 0.0, kappa = 0.0, theta = 0.0, zeta = 0.0, xi = 0.0;
+  double curvature_scale = 0.0;
+};
 struct RunReport {
+  ConfigEcho config;
   std::vector<MetricSample> trace;
   FinalMetrics final_pre_orth;
   std::optional<FinalMetrics> final_post_orth;
@@ -133,23 +154,42 @@ struct RunReport {
 };
 
 // ---- models: device-evaluated descriptors of ObjectiveModel (problems.hpp:28-111)
+enum class ProblemKind { P1 = 1, P2 = 2, P3 = 3, P4 = 4, P6 = 6 };
+inline const char* problem_kind_name(ProblemKind k) {  // problems.cpp:114-123
+  switch (k) {
+    case ProblemKind::P1: return "p1";
+    case ProblemKind::P2: return "p2";
+    case ProblemKind::P3: return "p3";
+    case ProblemKind::P4: return "p4";
+    case ProblemKind::P6: return "p6";
+  }
+  return "?";
+}
+
 class ObjectiveModel {
  public:
   virtual ~ObjectiveModel() = default;
   std::int64_t n() const { return desc_.n; }
   std::int64_t p() const { return desc_.p; }
   double curvature_scale() const { return desc_.s; }
+  ProblemKind kind() const { return kind_; }
+  // ConfigEcho::problem: the reference's kind name; the models it does not
+  // have (grid, Kohn–Sham, caller-defined) echo their own names
+  virtual const char* problem_name() const { return problem_kind_name(kind_); }
   const pcal_model_desc& desc() const { return desc_; }
 
  protected:
   pcal_model_desc desc_{};
+  ProblemKind kind_ = ProblemKind::P2;  // make_quadratic's default (problems.hpp:141-142)
 };
 
 // f(X) = ½tr(XᵀAX) + tr(GᵀX); A and G are host matrices owned by the caller.
 class QuadraticModel : public ObjectiveModel {
  public:
-  QuadraticModel(const DenseMatrix& a, std::int64_t p, double s, const DenseMatrix* g = nullptr) {
+  QuadraticModel(const DenseMatrix& a, std::int64_t p, double s, const DenseMatrix* g = nullptr,
+                 ProblemKind kind = ProblemKind::P2) {
     if (a.rows() != a.cols()) throw dimension_error("QuadraticModel: A must be square");
+    kind_ = kind;
     if (g && (g->rows() != a.rows() || g->cols() != p))
       throw dimension_error("QuadraticModel: G row count must equal n");
     desc_.kind = PCAL_MODEL_DENSE;
@@ -179,6 +219,9 @@ class StencilModel : public ObjectiveModel {
     desc_.nz = nz;
     desc_.v = v.data();
   }
+  const char* problem_name() const override {
+    return desc_.kind == PCAL_MODEL_KOHN_SHAM ? "kohn_sham" : "stencil";
+  }
 };
 
 // f(X) = ½tr(XᵀAXB) (BilinearModel, problems.cpp:143-156; problem P4); A n×n and
@@ -188,6 +231,7 @@ class BilinearModel : public ObjectiveModel {
   BilinearModel(const DenseMatrix& a, const DenseMatrix& b, double s) {
     if (a.rows() != a.cols() || b.rows() != b.cols())
       throw dimension_error("BilinearModel: A and B must be square");
+    kind_ = ProblemKind::P4;
     desc_.kind = PCAL_MODEL_BILINEAR;
     desc_.location = PCAL_HOST;
     desc_.n = a.rows();
@@ -197,8 +241,6 @@ class BilinearModel : public ObjectiveModel {
     desc_.b = b.data();
   }
 };
-
-enum class ProblemKind { P1 = 1, P2 = 2, P3 = 3, P4 = 4, P6 = 6 };
 
 // DensityModel (problems.cpp:158-206): ½tr(XᵀLX) plus the density term of
 // ρ = rowsq(X) and h = L⁻¹ρ — P1: ¼·coeff·ρᵀh; P6: ½ρᵀh − ¾·coeff·Σρ^{4/3}.
@@ -215,6 +257,7 @@ class DensityModel : public ObjectiveModel {
       throw parameter_error("DensityModel: kind must be P1 or P6");
     if (pcal_density_inverse(l.data(), l.rows(), linv_.data(), 8) != PCAL_OK)
       throw generation_error("LinearSolver: matrix is numerically singular");
+    kind_ = kind;
     desc_.kind = PCAL_MODEL_DENSITY;
     desc_.location = PCAL_HOST;
     desc_.n = l.rows();
@@ -252,6 +295,7 @@ class DeviceModel : public ObjectiveModel {
   DeviceModel& operator=(const DeviceModel&) = delete;
   virtual int enqueue_gradient(const double* x, std::int64_t ld, double* g, double* f,
                                void* stream) const = 0;
+  const char* problem_name() const override { return "device"; }
 
  private:
   static int trampoline(const double* x, int64_t ld, int64_t n, int64_t p, double* g, double* f,
@@ -334,6 +378,27 @@ inline RunReport solve(const ObjectiveModel& model, const SolverConfig& config,
                : r.status == PCAL_STATUS_MAX_ITER ? RunStatus::MaxIter
                                                   : RunStatus::Diverged;
   rep.beta = r.beta;
+  // ConfigEcho as iterate_main fills it (solver.cpp:333-342)
+  static const char* const alg_names[] = {"plam", "pcal", "alm", "moptqr", "plam-da",
+                                          "pcal-da"};  // algorithm_name, diagnostics.cpp:9-19
+  rep.config.solver = alg_names[static_cast<int>(config.algorithm)];
+  rep.config.beta = r.beta;
+  switch (config.eta_rule.kind) {  // eta_rule_name (solver.cpp:41-50)
+    case StepsizeRule::Kind::Constant:
+      rep.config.eta_rule = "const:" + std::to_string(config.eta_rule.gamma);
+      break;
+    case StepsizeRule::Kind::Differential: rep.config.eta_rule = "diff"; break;
+    case StepsizeRule::Kind::Bb1: rep.config.eta_rule = "bb1"; break;
+    case StepsizeRule::Kind::Bb2: rep.config.eta_rule = "bb2"; break;
+    case StepsizeRule::Kind::Abb: rep.config.eta_rule = "abb"; break;
+  }
+  rep.config.tol_rel_kkt = config.tol_rel_kkt;
+  rep.config.max_iter = config.max_iter;
+  rep.config.threads = config.threads;
+  rep.config.n = model.n();
+  rep.config.p = model.p();
+  rep.config.problem = model.problem_name();
+  rep.config.curvature_scale = model.curvature_scale();
   return rep;
 }
 

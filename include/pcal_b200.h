@@ -74,6 +74,14 @@ typedef int (*pcal_gradient_fn)(const double* x, int64_t ld, int64_t n, int64_t 
 /* pointer location for model data / x0 */
 #define PCAL_HOST 0
 #define PCAL_DEVICE 1
+/* x0 only (session create / solve): x0 points to a uint64_t seed and the
+ * library builds initial_point({Qr}, seed) itself — orthonormalize(random_normal
+ * (n, p, Rng(seed))), solver.cpp:136-142 — on the device.  A sharded session
+ * draws only its own rows of the Gaussian (checkpointed reference stream) and
+ * orthonormalises them with the chunk-ordered Gram of the final CholeskyQR2,
+ * so no rank ever holds the global n×p start point and X0 is bitwise the same
+ * for every rank count. */
+#define PCAL_X0_SEED 2
 
 /* StepsizeRule::Kind (solver.hpp:13-20), same order */
 #define PCAL_ETA_CONSTANT 0
@@ -89,7 +97,7 @@ typedef int (*pcal_gradient_fn)(const double* x, int64_t ld, int64_t n, int64_t 
 /* Algorithm (diagnostics.hpp:10), reference enum order. */
 #define PCAL_ALG_PLAM 0
 #define PCAL_ALG_PCAL 1
-#define PCAL_ALG_ALM 2         /* alm_outer (solver.cpp:478-624); single GPU */
+#define PCAL_ALG_ALM 2         /* alm_outer (solver.cpp:478-624); single GPU and row-sharded */
 #define PCAL_ALG_MOPTQR 3
 #define PCAL_ALG_PLAMDA 4
 #define PCAL_ALG_PCALDA 5
@@ -291,6 +299,11 @@ int pcal_gen_dense_operator(int64_t n, uint64_t seed, double* a, int32_t threads
  * own substitution loops (linsolve.cpp:70-102).  PCAL_E_PARAMETER (the
  * reference's generation_error) when L is numerically singular. */
 int pcal_density_inverse(const double* l, int64_t n, double* linv, int32_t threads);
+/* Diagnostic: the branch of orthonormalize (kernels.cpp:250-261) the calling
+ * thread's last device orthonormalisation took — 0 CholeskyQR2; 1 / 2 MGS2
+ * after the first / second Cholesky pass hit the pivot floor 1e-14·‖XᵀX‖_F;
+ * -1 MGS2 failed too (rank_error). */
+int32_t pcal_last_orthonormalize_path(void);
 /* initial_point({Qr}, n, p) on the device: orthonormalize(random_normal(n,p,Rng(seed)))
  * (solver.cpp:136-142). */
 int pcal_initial_point_qr(int64_t n, int64_t p, uint64_t seed, double* x0, int32_t device);

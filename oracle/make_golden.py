@@ -227,6 +227,24 @@ def report_io_cases(R: Reference) -> None:
     print("wrote report/container fixtures")
 
 
+JSON_MAGNITUDES = [1e15, 1.5e15, 9.999e15, 1e16, 1e14, 999999999999999.9, 1234567890123456.0,
+                   -2.5e15, 123456.789, 1e-4, 1e-5, 1.5e-5, 0.1, 100.0, 1e300, 5e-324, -0.0,
+                   0.0, 1e21, 4.7429826849363259e-05, -418.65544567286281]
+
+
+def json_magnitudes_case(R: Reference) -> None:
+    """The reference's to_json number formatting over magnitudes where Python's
+    repr and nlohmann's dtoa disagree (1e15 ≤ |v| < 1e16) and their neighbours."""
+    import ctypes as C
+    L = R.lib
+    L.ref_report_json_values.argtypes = [C.c_void_p, C.c_int64, C.c_char_p, C.c_int64]
+    v = np.array(JSON_MAGNITUDES)
+    jb = C.create_string_buffer(1 << 20)
+    assert L.ref_report_json_values(v.ctypes.data, len(v), jb, len(jb)) == 0
+    open(os.path.join(OUT, "ref_report_magnitudes.json"), "w").write(jb.value.decode() + "\n")
+    print("wrote ref_report_magnitudes.json")
+
+
 def init_cases(R: Reference) -> None:
     """initial_point(InitialPointSpec) for the three InitMode values (solver.cpp:136-170)."""
     import ctypes as C
@@ -444,6 +462,7 @@ if __name__ == "__main__":
     grid_cases(R)
     algorithm_cases(R)
     report_io_cases(R)
+    json_magnitudes_case(R)
     init_cases(R)
     harness_cases(R)
     linsolve_cases(R)

@@ -135,45 +135,21 @@ void orc_sym_part(const double* m, int64_t n, double* out) { /* kernels.cpp:28-3
     }
 }
 
-/* matmul (kernels.cpp:105-122): c_j += b(k,j)·a_k for k in order.  Each output
- * element accumulates over k in index order, so splitting rows across threads
- * (in addition to the reference's column split) is bitwise neutral. */
+/* matmul (kernels.cpp:105-122), matmul_at_b (:124-137), gram (:139-153):
+ * the blocked restatements in orc_blas.c (same per-element operation order,
+ * bitwise equal to the reference). */
 void orc_matmul(const double* a, int64_t m, int64_t kdim, const double* b, int64_t ncols,
                 double* c, int threads) {
-  const int64_t rb = (threads > 1 && m >= 8192) ? 2048 : m;
-  const int64_t nrb = (m + rb - 1) / rb;
-  memset(c, 0, sizeof(double) * (size_t)(m * ncols));
-#pragma omp parallel for num_threads(threads > 0 ? threads : 1) collapse(2) schedule(static)
-  for (int64_t j = 0; j < ncols; ++j)
-    for (int64_t r = 0; r < nrb; ++r) {
-      double* cj = c + j * m;
-      const double* bj = b + j * kdim;
-      const int64_t i0 = r * rb, i1 = (i0 + rb < m) ? i0 + rb : m;
-      for (int64_t k = 0; k < kdim; ++k) {
-        const double s = bj[k];
-        const double* ak = a + k * m;
-        for (int64_t i = i0; i < i1; ++i) cj[i] += s * ak[i];
-      }
-    }
+  orc_blas_matmul(a, m, kdim, b, ncols, c, threads);
 }
 
-/* matmul_at_b (kernels.cpp:124-137): c(i,j) = dot(a_i, b_j). */
 void orc_matmul_at_b(const double* a, int64_t n, int64_t m, const double* b, int64_t ncols,
                      double* c, int threads) {
-#pragma omp parallel for num_threads(threads > 0 ? threads : 1) collapse(2) schedule(static)
-  for (int64_t j = 0; j < ncols; ++j)
-    for (int64_t i = 0; i < m; ++i) c[i + j * m] = orc_dot(a + i * n, b + j * n, n);
+  orc_blas_at_b(a, n, m, b, ncols, c, threads);
 }
 
-/* gram (kernels.cpp:139-153): upper triangle, mirrored. */
 void orc_gram(const double* x, int64_t n, int64_t p, double* g, int threads) {
-#pragma omp parallel for num_threads(threads > 0 ? threads : 1) schedule(dynamic)
-  for (int64_t j = 0; j < p; ++j)
-    for (int64_t i = 0; i <= j; ++i) {
-      const double v = orc_dot(x + i * n, x + j * n, n);
-      g[i + j * p] = v;
-      g[j + i * p] = v;
-    }
+  orc_blas_gram(x, n, p, g, threads);
 }
 
 /* cholesky_lower (kernels.cpp:159-175). */
@@ -194,18 +170,26 @@ static int cholesky_lower(const double* a, int64_t p, double floor_, double* l) 
   return 1;
 }
 
-/* solve_right_lt (kernels.cpp:178-195): Q·Lᵀ = X, column by column. */
-static void solve_right_lt(const double* x, int64_t n, int64_t p, const double* l, double* q) {
-  for (int64_t j = 0; j < p; ++j) {
-    double* qj = q + j * n;
-    memcpy(qj, x + j * n, sizeof(double) * (size_t)n);
-    for (int64_t k = 0; k < j; ++k) {
-      const double s = l[j + k * p];
-      const double* qk = q + k * n;
-      for (int64_t i = 0; i < n; ++i) qj[i] -= s * qk[i];
+/* solve_right_lt (kernels.cpp:178-195): Q·Lᵀ = X, column by column.  Each
+ * element q(i,j) = (x(i,j) − Σ_{k<j} l(j,k)·q(i,k), k ascending)·(1/l(j,j)) only
+ * depends on its own row, so row blocks run in parallel, bitwise neutral. */
+static void solve_right_lt(const double* x, int64_t n, int64_t p, const double* l, double* q,
+                           int threads) {
+  const int64_t rb = 512, nrb = (n + rb - 1) / rb;
+#pragma omp parallel for num_threads(threads > 0 ? threads : 1) schedule(dynamic, 1)
+  for (int64_t b = 0; b < nrb; ++b) {
+    const int64_t i0 = b * rb, i1 = (i0 + rb < n) ? i0 + rb : n;
+    for (int64_t j = 0; j < p; ++j) {
+      double* qj = q + j * n;
+      memcpy(qj + i0, x + j * n + i0, sizeof(double) * (size_t)(i1 - i0));
+      for (int64_t k = 0; k < j; ++k) {
+        const double s = l[j + k * p];
+        const double* qk = q + k * n;
+        for (int64_t i = i0; i < i1; ++i) qj[i] -= s * qk[i];
+      }
+      const double inv = 1.0 / l[j + j * p];
+      for (int64_t i = i0; i < i1; ++i) qj[i] *= inv;
     }
-    const double inv = 1.0 / l[j + j * p];
-    for (int64_t i = 0; i < n; ++i) qj[i] *= inv;
   }
 }
 
@@ -230,19 +214,23 @@ static int mgs2(const double* x, int64_t n, int64_t p, double floor_, double* q)
 
 /* orthonormalize_with_r (kernels.cpp:250-261). */
 int orc_orthonormalize(const double* x, int64_t n, int64_t p, double* q) {
+  return orc_orthonormalize_t(x, n, p, q, 1);
+}
+
+int orc_orthonormalize_t(const double* x, int64_t n, int64_t p, double* q, int threads) {
   double* b = (double*)malloc(sizeof(double) * (size_t)(p * p));
   double* l = (double*)malloc(sizeof(double) * (size_t)(p * p));
   double* q1 = (double*)malloc(sizeof(double) * (size_t)(n * p));
   int rc = ORC_OK;
-  orc_gram(x, n, p, b, 1);
+  orc_gram(x, n, p, b, threads);
   const double floor_ = 1e-14 * orc_frobenius_norm(b, p * p);
   if (!cholesky_lower(b, p, floor_, l)) {
     rc = mgs2(x, n, p, floor_, q);
   } else {
-    solve_right_lt(x, n, p, l, q1);
-    orc_gram(q1, n, p, b, 1);
+    solve_right_lt(x, n, p, l, q1, threads);
+    orc_gram(q1, n, p, b, threads);
     if (!cholesky_lower(b, p, floor_, l)) rc = mgs2(x, n, p, floor_, q);
-    else solve_right_lt(q1, n, p, l, q);
+    else solve_right_lt(q1, n, p, l, q, threads);
   }
   free(b);
   free(l);
@@ -825,7 +813,7 @@ int orc_solve(const orc_model* m, const orc_config* c, const double* x0, orc_rep
           if (!(eta > 0.0)) { rc = ORC_E_PARAM; goto done_error; }
           const double sc = -1.0 / eta;
           for (int64_t q = 0; q < np; ++q) tmp[q] = x[q] + sc * gl[q];
-          if (orc_orthonormalize(tmp, n, p, xn) != ORC_OK) { status = ORC_DIVERGED; rc = ORC_OK; break; }
+          if (orc_orthonormalize_t(tmp, n, p, xn, threads) != ORC_OK) { status = ORC_DIVERGED; rc = ORC_OK; break; }
         } else if (normalized) {                            /* :419-422 */
           rc = orc_pcal_step(x, gl, n, p, eta, xn, &deg, threads);
           if (rc == ORC_E_PARAM) goto done_error;
@@ -859,7 +847,7 @@ int orc_solve(const orc_model* m, const orc_config* c, const double* x0, orc_rep
       if (r->final_x) memcpy(r->final_x, x, sizeof(double) * (size_t)np);
       r->has_x = 1;
       if (c->final_orth) {                                                 /* :445-459 */
-        if (orc_orthonormalize(x, n, p, xn) == ORC_OK) {
+        if (orc_orthonormalize_t(x, n, p, xn, threads) == ORC_OK) {
           int erc = eval_iterate(m, xn, &d, tmp, threads);
           if (erc) {
             status = ORC_DIVERGED;

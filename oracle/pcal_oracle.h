@@ -51,6 +51,13 @@ double orc_frobenius_norm(const double* a, int64_t count);               /* :311
 /* orthonormalize (kernels.cpp:250-265): CholeskyQR2 with MGS2 fallback.
  * Returns 0, or ORC_E_RANK when the fallback hits the pivot floor. */
 int orc_orthonormalize(const double* x, int64_t n, int64_t p, double* q);
+int orc_orthonormalize_t(const double* x, int64_t n, int64_t p, double* q, int threads);
+/* blocked restatements (orc_blas.c), bitwise equal to the reference loops */
+void orc_blas_matmul(const double* a, int64_t m, int64_t kdim, const double* b, int64_t ncols,
+                     double* c, int threads);
+void orc_blas_at_b(const double* a, int64_t n, int64_t m, const double* b, int64_t ncols,
+                   double* c, int threads);
+void orc_blas_gram(const double* x, int64_t n, int64_t p, double* g, int threads);
 /* spectral_norm_estimate (kernels.cpp:267-293). */
 double orc_spectral_norm_estimate(const double* a, int64_t n, uint64_t seed, int threads);
 

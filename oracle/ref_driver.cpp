@@ -400,6 +400,31 @@ int ref_run_single_text(std::int64_t n, std::int64_t p, std::uint64_t seed, std:
   });
 }
 
+// to_json of a hand-built RunReport whose trace row k carries vals[k] in every
+// metric (iter = k): the reference's number formatting over any magnitudes.
+int ref_report_json_values(const double* vals, std::int64_t count, char* json_buf,
+                           std::int64_t json_cap) {
+  return guarded([&] {
+    RunReport rep;
+    rep.config.problem = "p3";
+    rep.config.n = 8;
+    rep.config.p = 2;
+    rep.config.solver = "pcal";
+    rep.config.curvature_scale = count > 0 ? vals[0] : 0.0;
+    for (std::int64_t k = 0; k < count; ++k)
+      rep.trace.push_back({k, vals[k], vals[k], vals[k], vals[k], vals[k], 0.0});
+    if (count > 0) {
+      rep.final_pre_orth = {vals[count - 1], vals[0], vals[0], vals[count - 1]};
+      rep.final_post_orth = FinalMetrics{vals[0], vals[count - 1], vals[0], vals[0]};
+    }
+    rep.iterations = count;
+    const std::string js = to_json(rep, false);
+    if ((std::int64_t)js.size() + 1 > json_cap) throw io_error("buffer too small");
+    std::memcpy(json_buf, js.c_str(), js.size() + 1);
+    return 0;
+  });
+}
+
 // run_single(ProblemSpec, SolverConfig{max_iter}, InitialPointSpec) as the
 // reference's JSON report (elapsed times zeroed); kind 1..6 = P1..P6 names.
 int ref_run_single_json(int kind, std::int64_t n, std::int64_t p, double alpha, double kappa,

@@ -43,7 +43,7 @@ OK, E_PARAMETER, E_DIMENSION, E_RANK, E_UNSUPPORTED, E_CUDA, E_STATE = 0, -1, -2
 E_DIVERGENCE, E_EVALUATION = -7, -8
 STATUS = {0: "converged", 1: "max_iter", 2: "diverged"}
 TRACE_COLS = 7
-HOST, DEVICE = 0, 1
+HOST, DEVICE, X0_SEED = 0, 1, 2
 MODEL_DENSE, MODEL_STENCIL, MODEL_KOHN_SHAM, MODEL_DEVICE_CALLBACK = 1, 2, 3, 4
 MODEL_BILINEAR, MODEL_DENSITY = 5, 6
 DENSITY_P1, DENSITY_P6 = 0, 1
@@ -497,22 +497,33 @@ def solve(model: _ModelBase, config: SolverConfig, x0,
     return _report_from(rep, trace, stop_x, final_x)
 
 
+def _x0_arg(x0) -> tuple:
+    """(pointer, location, keep-alive) of a start point: a host array, a device
+    tensor, or an int seed (PCAL_X0_SEED: initial_point({Qr}, seed) built by the
+    library on the device, solver.cpp:136-142)."""
+    if isinstance(x0, (int, np.integer)) and not isinstance(x0, bool):
+        seed = C.c_uint64(int(x0))
+        return C.cast(C.byref(seed), C.c_void_p).value, X0_SEED, seed
+    if hasattr(x0, "data_ptr") and not isinstance(x0, np.ndarray):
+        return _ptr(x0), DEVICE, x0
+    x0 = _f64(x0)
+    return _ptr(x0), HOST, x0
+
+
 class Session:
-    """Device-resident run split into create / run / finish (pcal_session_*)."""
+    """Device-resident run split into create / run / finish (pcal_session_*).
+    x0: host array, device tensor, or an int seed (library-built initial point)."""
 
     def __init__(self, model: _ModelBase, config: SolverConfig, x0):
         self._L = lib()
         self.model, self.config = model, config
         cm, self._keep = model._c()
         cc = config._c()
-        on_dev = hasattr(x0, "data_ptr") and not isinstance(x0, np.ndarray)
-        if not on_dev:
-            x0 = _f64(x0)
-        self._x0 = x0
+        ptr, loc, self._x0 = _x0_arg(x0)
         h = C.c_void_p()
-        _check(self._L.pcal_session_create(C.byref(cm), C.byref(cc), _ptr(x0),
-                                           DEVICE if on_dev else HOST, C.byref(h)))
+        _check(self._L.pcal_session_create(C.byref(cm), C.byref(cc), ptr, loc, C.byref(h)))
         self._h = h
+        self.n_local = model.n
 
     def run(self, iters: int) -> None:
         _check(self._L.pcal_session_run(self._h, iters))
@@ -529,8 +540,12 @@ class Session:
         xx = _f64(x)
         _check(self._L.pcal_session_set_state(self._h, _ptr(xp), _ptr(xx), k, eta_prev))
 
-    def get_x(self) -> tuple:
-        x = np.zeros((self.model.n, self.model.p), order="F")
+    def get_x(self, out=None) -> tuple:
+        """(X_k, η_{k−1}, k) of the current iterate (this rank's rows); `out`: an
+        optional preallocated Fortran-ordered host array (e.g. pinned memory)."""
+        x = np.zeros((self.n_local, self.model.p), order="F") if out is None else out
+        if x.shape != (self.n_local, self.model.p) or not x.flags.f_contiguous:
+            raise DimensionError("get_x: out must be a Fortran-ordered n_local x p array")
         eta = C.c_double()
         k = C.c_int64()
         _check(self._L.pcal_session_get_x(self._h, _ptr(x), C.byref(eta), C.byref(k)))
@@ -667,6 +682,15 @@ def spectral_norm_estimate(a, seed: int, device: int = 0) -> float:
 
 
 INIT_MODES = {"qr": 0, "a2-i": 1, "a2-ii": 2}  # InitMode (solver.hpp:47), harness names
+
+
+ORTH_PATHS = {0: "cholqr2", 1: "mgs2-after-first", 2: "mgs2-after-second", -1: "rank"}
+
+
+def last_orthonormalize_path() -> str:
+    """Branch of orthonormalize (kernels.cpp:250-261) this thread's last device
+    orthonormalisation took (diagnostic)."""
+    return ORTH_PATHS[lib().pcal_last_orthonormalize_path()]
 
 
 def initial_point(n: int, p: int, seed: int, device: int = 0, mode: str = "qr",
@@ -811,13 +835,9 @@ class ShardedSession(Session):
         self.n_local = n_local
         cm, self._keep = model._c()
         cc = config._c()
-        on_dev = hasattr(x0_local, "data_ptr") and not isinstance(x0_local, np.ndarray)
-        if not on_dev:
-            x0_local = _f64(x0_local)
-        self._x0 = x0_local
+        ptr, loc, self._x0 = _x0_arg(x0_local)
         h = C.c_void_p()
-        _check(self._L.pcal_session_create_sharded(C.byref(cm), C.byref(cc), _ptr(x0_local),
-                                                   DEVICE if on_dev else HOST, comm._h,
+        _check(self._L.pcal_session_create_sharded(C.byref(cm), C.byref(cc), ptr, loc, comm._h,
                                                    C.byref(h)))
         self._h = h
 

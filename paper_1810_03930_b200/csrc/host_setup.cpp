@@ -106,6 +106,49 @@ void host_random_normal(int64_t count, uint64_t seed, double* out, int threads) 
   for (auto& th : pool) th.join();
 }
 
+// Rows [row0, row0 + nrows) of random_normal(n, p, Rng(seed)) (column-major
+// fill, kernels.cpp:49-55): value (i, j) is draw k = i + j·n of the normal
+// stream, i.e. the cos (k even) or sin (k odd) half of Box–Muller pair ⌊k/2⌋.
+// One sequential pass of raw draws checkpoints the generator at each column's
+// first pair; the columns' Box–Muller work then runs on `threads` threads.
+// Bitwise the same values as the full fill, for any slab.
+void host_random_normal_rows(int64_t n, int64_t p, uint64_t seed, int64_t row0, int64_t nrows,
+                             double* out, int threads) {
+  if (nrows <= 0 || p <= 0) return;
+  Rng r(seed);
+  std::vector<Rng> cps;
+  cps.reserve(static_cast<size_t>(p));
+  int64_t pos = 0;  // Box–Muller pairs consumed so far
+  for (int64_t j = 0; j < p; ++j) {
+    const int64_t m0 = (j * n + row0) / 2;
+    for (int64_t q = 0; q < 2 * (m0 - pos); ++q) (void)r.next();
+    pos = m0;
+    cps.push_back(r);
+  }
+  auto column = [&](int64_t j) {
+    Rng g = cps[static_cast<size_t>(j)];
+    double* o = out + j * nrows;
+    int64_t i = 0;
+    double c, sn;
+    if ((j * n + row0) % 2 == 1) {  // the slab starts on a pair's sin half
+      g.pair(c, sn);
+      o[i++] = sn;
+    }
+    while (i < nrows) {
+      g.pair(c, sn);
+      o[i++] = c;
+      if (i < nrows) o[i++] = sn;
+    }
+  };
+  threads = std::max(1, threads);
+  std::vector<std::thread> pool;
+  for (int t = 0; t < threads; ++t)
+    pool.emplace_back([&, t] {
+      for (int64_t j = t; j < p; j += threads) column(j);
+    });
+  for (auto& th : pool) th.join();
+}
+
 void host_uniform_after_normals(int64_t nnormals, uint64_t seed, int64_t count, double* out) {
   Rng r(seed);
   const int64_t skip = 2 * ((nnormals + 1) / 2);

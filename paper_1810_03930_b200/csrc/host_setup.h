@@ -4,6 +4,9 @@
 
 namespace pcal {
 void host_random_normal(int64_t count, uint64_t seed, double* out, int threads);
+// rows [row0, row0+nrows) of random_normal(n, p, Rng(seed)), nrows × p column-major
+void host_random_normal_rows(int64_t n, int64_t p, uint64_t seed, int64_t row0, int64_t nrows,
+                             double* out, int threads);
 void host_random_uniform(int64_t count, uint64_t seed, double* out);
 // `count` uniforms of Rng(seed) drawn after `nnormals` normal() calls (each
 // Box–Muller pair consumes two raw draws; a cached spare does not).

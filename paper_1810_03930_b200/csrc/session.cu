@@ -39,6 +39,10 @@ namespace pcal {
 thread_local int64_t* g_launch_counter = nullptr;
 thread_local KernelProfiler* g_kprof = nullptr;
 thread_local std::string g_last_error;
+// which branch of orthonormalize (kernels.cpp:250-261) the calling thread's last
+// device orthonormalisation took: 0 CholeskyQR2, 1 / 2 MGS2 after the first /
+// second Cholesky pass hit the pivot floor, -1 rank-deficient (MGS2 failed too)
+thread_local int32_t g_orth_path = 0;
 
 // ------------------------------------------------------------------------------
 // small dense kernels of the final orthonormalization (kernels.cpp:159-195)
@@ -1793,6 +1797,8 @@ static void setup_small(pcal_session* s) {
   s->mega = true;
 }
 
+bool orthonormalize_dev(pcal_session* s, const double* x, double* q, double* scratch);
+
 void session_create(const pcal_model_desc* model, const pcal_config* config, const double* x0,
                     int32_t x0_loc, pcal_session** out, pcal_category_timers* timers,
                     Comm* comm = nullptr, cudaStream_t shared_stream = nullptr) {
@@ -1884,7 +1890,22 @@ void session_create(const pcal_model_desc* model, const pcal_config* config, con
   build_plans(s.get());
   setup_small(s.get());
   init_ctl(s.get());
-  upload_matrix(x0, x0_loc, s->n, s->p, Xof(s.get(), 0), s->ld, s->stream);
+  if (x0_loc == PCAL_X0_SEED) {  // initial_point({Qr}, seed) of this rank's rows
+    const uint64_t seed = *reinterpret_cast<const uint64_t*>(x0);
+    if (2 * s->p > s->n_glob)  // solver.cpp:137-138
+      throw Error(PCAL_E_PARAMETER, "initial_point: dimensions must satisfy 2p <= n");
+    double* h = nullptr;
+    PCAL_CUDA(cudaMallocHost(&h, sizeof(double) * (size_t)s->n * s->p));
+    std::unique_ptr<double, decltype(&cudaFreeHost)> hg(h, &cudaFreeHost);
+    host_random_normal_rows(s->n_glob, s->p, seed, s->row0, s->n, h,
+                            (int)std::max(1u, std::min(32u, std::thread::hardware_concurrency())));
+    upload_matrix(h, PCAL_HOST, s->n, s->p, Xof(s.get(), 1), s->ld, s->stream);
+    if (!orthonormalize_dev(s.get(), Xof(s.get(), 1), Xof(s.get(), 0), Pof(s.get(), 1)))
+      throw Error(PCAL_E_RANK, "initial_point: numerically rank-deficient Gaussian start");
+    PCAL_CUDA(cudaStreamSynchronize(s->stream));
+  } else {
+    upload_matrix(x0, x0_loc, s->n, s->p, Xof(s.get(), 0), s->ld, s->stream);
+  }
   k_set_t0<<<1, 1, 0, s->stream>>>(s->ctl);
   launched("k_set_t0");
   launch_eval(s.get(), 0, 1, s->ctl);  // eval_iterate(X0) + record(0) (solver.cpp:363-365)
@@ -2042,6 +2063,7 @@ bool orthonormalize_dev(pcal_session* s, const double* x, double* q, double* scr
   PCAL_CUDA(cudaMemcpyAsync(&ok, s->orth_status, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   PCAL_CUDA(cudaStreamSynchronize(st));
   bool chol_ok = ok != 0;
+  g_orth_path = chol_ok ? 0 : 1;
   if (chol_ok) {
     mul_t(x, scratch);  // Q1 = X·L1⁻ᵀ
     gram_of(scratch);
@@ -2050,6 +2072,7 @@ bool orthonormalize_dev(pcal_session* s, const double* x, double* q, double* scr
     PCAL_CUDA(cudaMemcpyAsync(&ok, s->orth_status, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     PCAL_CUDA(cudaStreamSynchronize(st));
     chol_ok = ok != 0;
+    if (!chol_ok) g_orth_path = 2;
     if (chol_ok) mul_t(scratch, q);  // Q = Q1·L2⁻ᵀ
   }
   if (!chol_ok) {  // mgs2(x) fallback (kernels.cpp:254,258)
@@ -2078,7 +2101,10 @@ bool orthonormalize_dev(pcal_session* s, const double* x, double* q, double* scr
     }
     PCAL_CUDA(cudaMemcpyAsync(&ok, s->orth_status, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     PCAL_CUDA(cudaStreamSynchronize(st));
-    if (!ok) return false;
+    if (!ok) {
+      g_orth_path = -1;
+      return false;
+    }
   }
   return true;
 }
@@ -2179,6 +2205,7 @@ void session_finish(pcal_session* s, pcal_report* r) {
 extern "C" {
 
 const char* pcal_last_error(void) { return g_last_error.c_str(); }
+int32_t pcal_last_orthonormalize_path(void) { return g_orth_path; }
 
 void pcal_config_default(pcal_config* c) {
   c->alm_inner_max = 500;  // AlmOptions (solver.hpp:24-28)

@@ -8,9 +8,10 @@
   ``%.17g`` (report_io.cpp:165-172); ``write_summary_header`` / ``_row``
   (report_io.cpp:174-194); ``same_numerics`` (report_io.cpp:259-283).
 * ``save_problem`` / ``load_problem`` — the ``OCPROB01`` binary container
-  (problems.cpp:327-416) for the dense quadratic family (kind tags 2, 3), the
-  models this library evaluates on the device.  Other tags (P1/P6 density,
-  P4 bilinear) are not device models and raise ``UnsupportedModel``.
+  (problems.cpp:327-416) for every reference family: the dense quadratic
+  (tags 2, 3), P4 bilinear (4) and the P1 / P6 density models (1, 6).  Only the
+  models the reference has no container for (grid, Kohn–Sham, caller-defined)
+  raise ``UnsupportedModel``.
 """
 from __future__ import annotations
 
@@ -79,6 +80,58 @@ def _num(v):
     return v
 
 
+def _nl_double(v: float) -> str:
+    """A finite double as nlohmann::json writes it (dtoa_impl::format_buffer with
+    min_exp = −4, max_exp = digits10 = 15): the shortest round-trip digits D
+    with v = 0.D·10ⁿ, positional for −4 < n ≤ 15 (integers get ".0"),
+    exponent form otherwise ("1e+15", "1.5e-05": sign and ≥ 2 exponent digits).
+    Python's repr differs exactly for 1e15 ≤ |v| < 1e16 (it stays positional
+    up to n = 16)."""
+    if v == 0.0:
+        return "-0.0" if math.copysign(1.0, v) < 0 else "0.0"
+    r = repr(v)
+    sign = "-" if r[0] == "-" else ""
+    r = r.lstrip("-")
+    mant, _, e = r.partition("e")
+    ip, _, fp = mant.partition(".")
+    digits = ip + fp
+    n = len(ip) + (int(e) if e else 0)
+    stripped = digits.lstrip("0")
+    n -= len(digits) - len(stripped)
+    d = stripped.rstrip("0")
+    k = len(d)
+    if k <= n <= 15:
+        body = d + "0" * (n - k) + ".0"
+    elif 0 < n <= 15:
+        body = d[:n] + "." + d[n:]
+    elif -4 < n <= 0:
+        body = "0." + "0" * (-n) + d
+    else:
+        x = n - 1
+        body = (d if k == 1 else d[0] + "." + d[1:]) + "e" + ("-" if x < 0 else "+") + \
+            f"{abs(x):02d}"
+    return sign + body
+
+
+def _dumps(obj, level: int = 0) -> str:
+    """json.dumps(obj, indent=2, sort_keys=True) with nlohmann's double format."""
+    pad, inner = "  " * level, "  " * (level + 1)
+    if isinstance(obj, dict):
+        if not obj:
+            return "{}"
+        items = [f"{inner}{json.dumps(str(k))}: {_dumps(obj[k], level + 1)}" for k in sorted(obj)]
+        return "{\n" + ",\n".join(items) + "\n" + pad + "}"
+    if isinstance(obj, (list, tuple)):
+        if not obj:
+            return "[]"
+        return "[\n" + ",\n".join(inner + _dumps(v, level + 1) for v in obj) + "\n" + pad + "]"
+    if isinstance(obj, bool) or obj is None or isinstance(obj, (int, str)):
+        return json.dumps(obj)
+    if isinstance(obj, float):
+        return _nl_double(obj) if math.isfinite(obj) else "null"
+    raise TypeError(f"not JSON-serialisable: {type(obj).__name__}")
+
+
 def _final(f) -> dict:
     return {"feas": _num(float(f.feas)), "fval": _num(float(f.fval)),
             "kkt_abs": _num(float(f.kkt_abs)), "kkt_rel": _num(float(f.kkt_rel))}
@@ -108,7 +161,7 @@ def to_json(report, echo: ConfigEcho, include_timing: bool = False,
         j["final"]["post_orth"] = _final(report.final_post_orth)
     if include_timing:
         j["wall_time"] = float(report.wall_time)
-    return json.dumps(j, indent=2, sort_keys=True)
+    return _dumps(j)
 
 
 def run_report_from_json(text: str) -> dict:

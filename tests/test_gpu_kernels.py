@@ -146,7 +146,8 @@ def test_stencil_gradient_bitwise(pcal, orc, grid, p):
     assert abs(f - f_ref) <= 1e-12 * abs(f_ref)
 
 
-@pytest.mark.parametrize("grid,p", [((6, 6, 6), 4), ((48, 48, 48), 3), ((8, 6, 10), 5)])
+@pytest.mark.parametrize("grid,p", [((6, 6, 6), 4), ((48, 48, 48), 3), ((8, 6, 10), 5),
+                                    ((96, 16, 5), 3), ((72, 8, 4), 2)])
 def test_kohn_sham_gradient(pcal, orc, grid, p):
     from oracle.oracle import Model, MODEL_KOHN_SHAM
     n = grid[0] * grid[1] * grid[2]
@@ -160,9 +161,13 @@ def test_kohn_sham_gradient(pcal, orc, grid, p):
 
 
 @pytest.mark.parametrize("grid,p", [((32, 8, 5), 3), ((48, 16, 7), 2), ((128, 16, 4), 2),
-                                    ((64, 64, 64), 2), ((40, 24, 3), 5)])
+                                    ((64, 64, 64), 2), ((40, 24, 3), 5),
+                                    ((96, 16, 5), 3), ((72, 8, 4), 2), ((100, 8, 3), 2)])
 def test_stencil_march_bitwise(pcal, orc, grid, p):
-    """z-marching kernel (nx ≤ 128, ny % 8 == 0): same bits as the oracle."""
+    """z-marching kernel (nx ≤ 128, ny % 8 == 0): same bits as the oracle.
+    (96,16,5) / (72,8,4) / (100,8,3) take the full-row march with 4 points per
+    lane and idle lanes (nx % 4 == 0, 64 < nx < 128: L = nx/4 < 32 — the x wrap
+    over the active lanes and the masked stores)."""
     from oracle.oracle import Model, MODEL_STENCIL
     n = grid[0] * grid[1] * grid[2]
     v = orc.random_uniform(n, 13)

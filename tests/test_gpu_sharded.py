@@ -65,6 +65,24 @@ def test_kohn_sham_sharded_matches_single_gpu(pcal, orc, R):
     check_pair(pcal.solve(m, cfg, x0), pcal.solve_emulated(m, cfg, x0, R))
 
 
+@pytest.mark.parametrize("kind,grid", [("stencil", (96, 16, 8)), ("kohn_sham", (72, 8, 6))])
+def test_row_march_with_idle_lanes_through_the_halo_path(pcal, orc, kind, grid):
+    """The 4-points-per-lane full-row stencil march with idle lanes (nx = 96, 72)
+    on sharded slabs: its hlo/hhi halo planes come from the neighbour ranks.
+    Rank counts 1 and 2 are bitwise identical, and both match the single GPU."""
+    n, p = grid[0] * grid[1] * grid[2], 5
+    v = orc.random_uniform(n, 4) if kind == "stencil" else -orc.random_uniform(n, 4)
+    x0 = orc.initial_point_qr(n, p, 11)
+    cls = pcal.StencilModel if kind == "stencil" else pcal.KohnShamModel
+    m = cls(grid, v, p, 12.0 + np.abs(v).max())
+    cfg = pcal.SolverConfig(tol_rel_kkt=TINY, max_iter=30)
+    r1 = pcal.solve_emulated(m, cfg, x0, 1)
+    r2 = pcal.solve_emulated(m, cfg, x0, 2)
+    assert np.array_equal(r1.trace[:, :6], r2.trace[:, :6])
+    assert np.array_equal(r1.final_x, r2.final_x)
+    check_pair(pcal.solve(m, cfg, x0), r2)
+
+
 def test_sharded_convergence_stops_every_rank_together(pcal, orc):
     r = orc.random_normal(40, 40, 24)
     a = np.asfortranarray(0.5 * (r + r.T))

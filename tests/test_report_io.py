@@ -28,6 +28,17 @@ def test_json_report_byte_identical_to_reference():
     assert R.to_json(rep, d["config"]) + "\n" == ref_text
 
 
+def test_json_number_format_matches_nlohmann_at_every_magnitude():
+    """nlohmann's dtoa switches to exponent form above 15 integer digits
+    (1e15 ≤ |v| < 1e16 is "1e+15", Python's repr says "1000000000000000.0"):
+    the reference's own to_json of a report holding those values, byte for byte
+    (ref_report_magnitudes.json, oracle/make_golden.py json_magnitudes_case)."""
+    ref_text = open(os.path.join(GOLD, "ref_report_magnitudes.json")).read()
+    assert '"fval": 1e+15,' in ref_text and '1.5e+15' in ref_text
+    rep, d = _report_from_reference_json(ref_text)
+    assert R.to_json(rep, d["config"]) + "\n" == ref_text
+
+
 def test_trace_csv_byte_identical_to_reference():
     ref_text = open(os.path.join(GOLD, "ref_trace_p1_n60.csv")).read()
     rep, _ = _report_from_reference_json(open(os.path.join(GOLD, "ref_report_p1_n60.json")).read())
