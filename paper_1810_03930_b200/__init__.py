@@ -462,10 +462,21 @@ def _report_from(rep: _Report, trace: np.ndarray, stop_x, final_x) -> RunReport:
                      outer_iterations=rep.outer_iterations, inner_cap_hits=rep.inner_cap_hits)
 
 
-def _new_report(n: int, p: int, max_iter: int, want_x: bool = True) -> tuple:
+def _out_matrix(buf, n: int, p: int) -> np.ndarray:
+    if buf is None:
+        return np.zeros((n, p), order="F")
+    if buf.shape != (n, p) or buf.dtype != np.float64 or not buf.flags.f_contiguous:
+        raise DimensionError("report output buffers must be Fortran-ordered float64 n x p")
+    return buf
+
+
+def _new_report(n: int, p: int, max_iter: int, want_x: bool = True, out=None) -> tuple:
+    """Report buffers; `out` = (stop_x, final_x): caller-owned host matrices
+    (e.g. pinned memory) that receive the iterates instead of fresh arrays."""
     trace = np.zeros((max_iter + 1, TRACE_COLS))
-    stop_x = np.zeros((n, p), order="F") if want_x else None
-    final_x = np.zeros((n, p), order="F") if want_x else None
+    o_stop, o_final = out if out is not None else (None, None)
+    stop_x = _out_matrix(o_stop, n, p) if want_x else None
+    final_x = _out_matrix(o_final, n, p) if want_x else None
     rep = _Report()
     rep.trace = trace.ctypes.data_as(_dp)
     rep.trace_capacity = max_iter + 1
@@ -475,8 +486,10 @@ def _new_report(n: int, p: int, max_iter: int, want_x: bool = True) -> tuple:
 
 
 def solve(model: _ModelBase, config: SolverConfig, x0,
-          timers: Optional[CategoryTimers] = None) -> RunReport:
-    """orthopt::solve for PCAL on the B200 (host buffers in, host report out)."""
+          timers: Optional[CategoryTimers] = None, out=None) -> RunReport:
+    """orthopt::solve for PCAL on the B200 (host buffers in, host report out).
+    out: optional (stop_x, final_x) host buffers the report's iterates are
+    written into (n×p, Fortran order; pinned memory makes the copy-out a DMA)."""
     L = lib()
     cm, keep = model._c()
     cc = config._c()
@@ -485,7 +498,7 @@ def solve(model: _ModelBase, config: SolverConfig, x0,
         x0 = _f64(x0)
     if tuple(x0.shape) != (model.n, model.p):
         raise DimensionError("solve: start point shape mismatch")
-    rep, trace, stop_x, final_x = _new_report(model.n, model.p, config.max_iter)
+    rep, trace, stop_x, final_x = _new_report(model.n, model.p, config.max_iter, out=out)
     tm = _Timers() if timers is not None else None
     _check(L.pcal_solve(C.byref(cm), C.byref(cc), _ptr(x0), DEVICE if on_dev else HOST,
                         C.byref(rep), C.byref(tm) if tm is not None else None))
@@ -785,12 +798,12 @@ def solve_emulated(model: _ModelBase, config: SolverConfig, x0, nranks: int,
 
 
 def solve_sharded(model: _ModelBase, config: SolverConfig, x0_local, comm: "Comm",
-                  n_local: int, timers: Optional[CategoryTimers] = None) -> RunReport:
+                  n_local: int, timers: Optional[CategoryTimers] = None, out=None) -> RunReport:
     """Row-sharded pcal_solve on this rank (host buffers: local slabs in, local rows out)."""
     cm, keep = model._c()
     cc = config._c()
     x0_local = _f64(x0_local)
-    rep, trace, stop_x, final_x = _new_report(n_local, model.p, config.max_iter)
+    rep, trace, stop_x, final_x = _new_report(n_local, model.p, config.max_iter, out=out)
     _timed_call(timers, lambda t: _check(lib().pcal_solve_sharded(
         C.byref(cm), C.byref(cc), _ptr(x0_local), HOST, comm._h, C.byref(rep), t)))
     return _report_from(rep, trace, stop_x, final_x)

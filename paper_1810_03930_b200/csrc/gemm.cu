@@ -1,4 +1,6 @@
 // gemm.cu — stream-K DMMA GEMM: configurations, schedules, launches.
+#include <cudaTypedefs.h>  // PFN_cuTensorMapEncodeTiled
+
 #include <algorithm>
 #include <cstdlib>
 #include <vector>
@@ -13,7 +15,7 @@ namespace pcal {
 // ------------------------------------------------------------------------------
 
 template <int AM>
-using CfgBig = GemmCfg<128, 128, 2, 4, 3, AM, 32>;  // BK = 32: 3 × 70 KB stages
+using CfgBig = GemmCfg<128, 128, 2, 4, 3, AM, 32>;  // BK = 32: 3 × 64 KB stages
 template <int AM>
 using CfgMid = GemmCfg<64, 64, 2, 2, 4, AM>;
 template <int AM>
@@ -173,27 +175,65 @@ void plan_gemm(GemmPlan& pl, int device, int size, int amode, int epi, int64_t M
   g.ws = pl.ws;
   g.qmax = qmax;
   g.force_ws = chunk_partials ? 1 : 0;
-  // long runs of k-iterations per CTA: split the copy stream over 4 producer
-  // warps; short tiles with heavy epilogues (X·[W|C]) keep a single producer
-  g.nprod = (ki >= 64 && units / std::max(grid, 1) >= 64) ? 4 : 1;
   g.segs = segs;
   pl.no_fixup = chunk_partials;
 }
 
+// ---- TMA descriptors ------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q{};
+    void* p = nullptr;
+    PCAL_CUDA(cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000,
+                                               cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !p)
+      throw Error(PCAL_E_CUDA, "cuTensorMapEncodeTiled unavailable in the driver");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 2-D FP64 tensor {inner, outer} with row pitch ld (elements), box
+// {16, box_outer}, 128-byte swizzle, zero fill outside the extents.
+static void encode_map(CUtensorMap* m, const double* base, int64_t inner, int64_t outer,
+                       int64_t ld, int box_outer) {
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || (ld * 8) % 16 || inner < 1 || outer < 1 ||
+      inner > ld)
+    throw Error(PCAL_E_STATE, "gemm: operand not TMA-addressable (16-byte aligned base / pitch)");
+  const cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  const cuuint64_t strides[1] = {(cuuint64_t)(ld * 8)};
+  const cuuint32_t box[2] = {16u, (cuuint32_t)box_outer};
+  const cuuint32_t estr[2] = {1u, 1u};
+  const CUresult r = tensor_map_encoder()(
+      m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, estr,
+      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw Error(PCAL_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+}
+
+template <class Cfg>
+static GemmMaps make_maps(const GemmArgs& g) {
+  GemmMaps m;
+  if (Cfg::AMODE == A_MCONTIG)
+    encode_map(&m.a, g.A, g.M, g.K, g.lda, Cfg::BK);   // A(m, k) = A[m + k·lda]
+  else
+    encode_map(&m.a, g.A, g.K, g.M, g.lda, Cfg::BM);   // A(m, k) = A[k + m·lda]
+  encode_map(&m.b, g.B, g.K, g.N, g.ldb, Cfg::BN);      // B(k, n) = B[k + n·ldb]
+  return m;
+}
+
 template <class Cfg, int EPI>
 static void launch_cfg(const GemmPlan& pl, cudaStream_t st) {
-  // separate instantiations per producer count keep the single-producer kernel
-  // (short-K tiles, heavy epilogues) free of the 4-producer code
-  auto kern = pl.args.nprod == 4 ? gemm_streamk<Cfg, EPI, 4> : gemm_streamk<Cfg, EPI, 1>;
   static bool attr_set = false;  // per (Cfg, EPI)
   if (!attr_set) {
-    PCAL_CUDA(cudaFuncSetAttribute(gemm_streamk<Cfg, EPI, 1>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
-    PCAL_CUDA(cudaFuncSetAttribute(gemm_streamk<Cfg, EPI, 4>,
+    PCAL_CUDA(cudaFuncSetAttribute(gemm_streamk<Cfg, EPI>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
     attr_set = true;
   }
-  kern<<<pl.args.grid, Cfg::THREADS + 128, Cfg::SMEM_BYTES, st>>>(pl.args);
+  const GemmMaps maps = make_maps<Cfg>(pl.args);
+  gemm_streamk<Cfg, EPI><<<pl.args.grid, Cfg::THREADS + 128, Cfg::SMEM_BYTES, st>>>(pl.args, maps);
   launched(EPI == EPI_GRAD ? "gemm_grad" : EPI == EPI_XM ? "gemm_xm" : Cfg::AMODE == A_KCONTIG ? "gemm_gram" : "gemm_store");
   PCAL_CUDA(cudaGetLastError());
   if (pl.ntasks && !pl.no_fixup) {
@@ -219,7 +259,8 @@ static void launch_xm_tmem(const GemmPlan& pl, cudaStream_t st) {
                                    smem));
     attr_set = true;
   }
-  gemm_xm_tmem<Cfg><<<pl.args.grid, Cfg::THREADS + 256, smem, st>>>(pl.args);
+  const GemmMaps maps = make_maps<Cfg>(pl.args);
+  gemm_xm_tmem<Cfg><<<pl.args.grid, Cfg::THREADS + 256, smem, st>>>(pl.args, maps);
   launched("gemm_xm");
   PCAL_CUDA(cudaGetLastError());
 }

@@ -4,8 +4,9 @@
 // Blackwell has no FP64 tcgen05 kind (ptxas rejects kind::f64),
 // so FP64 tensor math is the warp-level mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4,
 // measured 37.1 TFLOP/s peak on B200: profiles/fp64_peaks_r01.txt).  Tiles are
-// staged global→shared with 16-byte cp.async in a STAGES-deep ring; the
-// schedule is stream-K: the linearised (tile, k-iteration) space is cut into
+// staged global→shared by the Tensor Memory Accelerator (cp.async.bulk.tensor,
+// 128-byte swizzled boxes, mbarrier complete_tx) into a STAGES-deep ring that
+// ONE producer thread keeps full; the schedule is stream-K: the linearised (tile, k-iteration) space is cut into
 // `grid` equal contiguous ranges, one per CTA (grid = SM count), so the
 // tall-skinny contractions of PCAL (K = n up to 2M, M·N = p×p) and the dense
 // gradient (M = n, N = p, K = n) both fill all 148 SMs.  A tile completed by
@@ -20,40 +21,11 @@
 //   B        : B(k,n) = B[k + n·ldb]     (X, Y, or the p×2p multiplier block)
 #pragma once
 
+#include <cuda.h>  // CUtensorMap
+
 #include "gemm_types.h"
 
 namespace pcal {
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  const int sz = valid ? 16 : 0;
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
-}
-// Same with an L2 cache policy (createpolicy): the streamed dense operator is
-// marked evict-first so it does not push the reused X out of L2.
-__device__ __forceinline__ void cp_async16_pol(void* smem, const void* gmem, bool valid,
-                                               uint64_t pol) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  const int sz = valid ? 16 : 0;
-  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;\n" ::"r"(s),
-               "l"(gmem), "r"(sz), "l"(pol));
-}
-__device__ __forceinline__ uint64_t l2_evict_first_policy() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
-  return pol;
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
-
-__device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(c0), "+d"(c1)
-               : "d"(a), "d"(b));
-}
 
 template <int BM_, int BN_, int WARPS_M_, int WARPS_N_, int STAGES_, int AMODE_, int BK_ = 16>
 struct GemmCfg {
@@ -65,79 +37,107 @@ struct GemmCfg {
   static constexpr int WM = BM / WARPS_M, WN = BN / WARPS_N;  // warp tile
   static constexpr int MT = WM / 8, NT = WN / 8;              // 8×8 mma tiles per warp
   static constexpr int FRAG = MT * NT * 2;                    // accumulators per thread
-  // shared layouts (doubles); +4 padding makes the 16 lanes of a 64-bit
-  // fragment wavefront hit 16 distinct bank pairs
-  static constexpr int SA_M = BM + 4;       // A_MCONTIG: As[k][m]
-  static constexpr int SA_K = BK + 4;       // A_KCONTIG: As[m][k]
-  static constexpr int A_STAGE = AMODE == A_MCONTIG ? BK * SA_M : BM * SA_K;
-  static constexpr int SB_K = BK + 4;       // Bs[n][k]
-  static constexpr int B_STAGE = BN * SB_K;
-  static constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) * 8 + 2 * STAGES * 8;
-  static_assert(WM % 8 == 0 && WN % 8 == 0, "warp tile must be a multiple of 8");
+  // Shared layouts (TMA boxes, SWIZZLE_128B: 128-byte rows, the 16-byte chunk
+  // c of row R stored at chunk c ^ (R mod 8), every box 1024-byte aligned):
+  //   A_MCONTIG: BM/16 boxes {16 m, BK k}: rows = k, 16 consecutive m per row
+  //   A_KCONTIG and B: BK/16 boxes {16 k, BM or BN rows}: rows = m (n), 16 k per row
+  static constexpr int A_STAGE = BM * BK;   // doubles per stage
+  static constexpr int B_STAGE = BN * BK;
+  static constexpr int STAGE_BYTES = (A_STAGE + B_STAGE) * 8;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 2 * STAGES * 8 + 1024;  // + align slack
+  static_assert(WM % 16 == 0 && WN % 8 == 0, "warp tile: WM multiple of 16, WN of 8");
+  static_assert(BK % 16 == 0 && BM % 16 == 0, "TMA boxes are 16 doubles wide");
 };
 
-// ---- tile loads -------------------------------------------------------------
-template <class Cfg>
-__device__ __forceinline__ void load_stage(const GemmArgs& g, double* As, double* Bs, int tm,
-                                           int tn, int kk) {
-  constexpr int BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK, T = Cfg::THREADS;
-  const int64_t m0 = (int64_t)tm * BM, n0 = (int64_t)tn * BN, k0 = (int64_t)kk * BK;
-  if constexpr (Cfg::AMODE == A_MCONTIG) {
-    // BK columns of BM contiguous doubles; 16-byte chunks of 2 doubles
-    constexpr int CH = BK * BM / 2;
-#pragma unroll
-    for (int c = threadIdx.x; c < CH; c += T) {
-      const int kr = c / (BM / 2), mc = (c % (BM / 2)) * 2;
-      const int64_t m = m0 + mc;
-      const bool ok = m < g.M;
-      const double* src = g.A + (ok ? m + (k0 + kr) * g.lda : 0);
-      cp_async16(As + kr * Cfg::SA_M + mc, src, ok);
-    }
-  } else {
-    // BM rows (columns of the stored matrix) of BK contiguous doubles
-    constexpr int CH = BM * BK / 2;
-#pragma unroll
-    for (int c = threadIdx.x; c < CH; c += T) {
-      const int mr = c / (BK / 2), kc = (c % (BK / 2)) * 2;
-      const int64_t m = m0 + mr;
-      const bool ok = m < g.M;
-      const double* src = g.A + (ok ? (k0 + kc) + m * g.lda : 0);
-      cp_async16(As + mr * Cfg::SA_K + kc, src, ok);
-    }
-  }
-  {
-    constexpr int CH = BN * BK / 2;
-#pragma unroll
-    for (int c = threadIdx.x; c < CH; c += T) {
-      const int nr = c / (BK / 2), kc = (c % (BK / 2)) * 2;
-      const int64_t nn = n0 + nr;
-      const bool ok = nn < g.N;
-      const double* src = g.B + (ok ? (k0 + kc) + nn * g.ldb : 0);
-      cp_async16(Bs + nr * Cfg::SB_K + kc, src, ok);
-    }
-  }
+// Tensor maps of one launch (encoded on the host per launch, gemm.cu; kernel
+// parameter, so graph capture keeps the pointers of the captured launch).
+struct alignas(64) GemmMaps {
+  CUtensorMap a;  // A_MCONTIG: {M, K} box {16, BK};  A_KCONTIG: {K, M} box {16, BM}
+  CUtensorMap b;  // {K, N} box {16, BN}
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+// Same with an L2 cache policy: the streamed dense operator is marked
+// evict-first so it does not push the reused X out of L2.
+__device__ __forceinline__ void tma_load_2d_hint(void* dst, const CUtensorMap* map, int c0, int c1,
+                                                 uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
 }
 
-// ---- one BK slice of MMAs ------------------------------------------------------
+__device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// k-slice order inside one 16-k box.  DMMA.8x8x4 lane (r, q) holds A(m = r, k_q)
+// and B(k_q, n = r); which four k of the slice form k-step s is free as long as
+// A and B agree.  Step s of a box uses k = kq(q) ^ t(s) with kq = {0, 3, 12, 15}
+// and t = {0, 1, 4, 5}: the four sets partition 0..15, and under the 128-byte
+// swizzle each 16-lane half of a fragment load hits 16 distinct bank pairs
+//   * A_MCONTIG (rows = k): k mod 8 of the four q differ in bits 1–2, so the
+//     four rows' 32-byte segments land in four different chunk pairs;
+//   * rows = m / n (A_KCONTIG, B): two q per 8-byte half-chunk (k & 1), and
+//     within a half their chunks k >> 1 differ in bit 2, so rows r = 0..3
+//     (XOR r) never collide.
+__device__ __forceinline__ int kq_of(int q) { return (q & 1) * 3 + (q >> 1) * 12; }
+// ---- one BK slice of MMAs (swizzled TMA layout, permuted k order) ------------
 template <class Cfg>
-__device__ __forceinline__ void mma_stage(const double* As, const double* Bs, int wm, int wn,
-                                          int lane, double (&acc)[Cfg::MT][Cfg::NT][2]) {
+__device__ __forceinline__ void mma_stage(const char* As, const char* Bs, int wm, int wn, int lane,
+                                          double (&acc)[Cfg::MT][Cfg::NT][2]) {
   const int r = lane >> 2, q = lane & 3;
+  const int kq = kq_of(q);
 #pragma unroll
-  for (int k4 = 0; k4 < Cfg::BK; k4 += 4) {
+  for (int st = 0; st < Cfg::BK / 4; ++st) {
+    const int box = st >> 2;
+    const int kl = kq ^ ((st & 1) | ((st & 2) << 1));  // k within the box: kq ^ {0,1,4,5}
     double a[Cfg::MT], b[Cfg::NT];
+    if constexpr (Cfg::AMODE == A_MCONTIG) {
+      // element (m, k): box m/16, row k, chunk ((m & 15) >> 1) ^ (k & 7), half m & 1
+      const int k = box * 16 + kl;
+      const char* rowp = As + k * 128 + (r & 1) * 8;
+      const int ce = ((r >> 1) ^ (k & 7)) << 4;   // even mt (m & 15 < 8)
+      const int co = ce ^ 64;                      // odd mt: chunk ^ 4
 #pragma unroll
-    for (int mt = 0; mt < Cfg::MT; ++mt) {
-      const int m = wm * Cfg::WM + mt * 8 + r;
-      if constexpr (Cfg::AMODE == A_MCONTIG)
-        a[mt] = As[(k4 + q) * Cfg::SA_M + m];
-      else
-        a[mt] = As[m * Cfg::SA_K + k4 + q];
+      for (int mt = 0; mt < Cfg::MT; ++mt) {
+        const int mb = (wm * Cfg::WM + mt * 8) >> 4;
+        a[mt] = *reinterpret_cast<const double*>(rowp + mb * (Cfg::BK * 128) + ((mt & 1) ? co : ce));
+      }
+    } else {
+      // element (m, k): box k/16, row m, chunk ((k & 15) >> 1) ^ (m & 7), half k & 1
+      const char* bx = As + box * (Cfg::BM * 128) + (kl & 1) * 8 + ((((kl >> 1) ^ r)) << 4);
+#pragma unroll
+      for (int mt = 0; mt < Cfg::MT; ++mt) {
+        const int m = wm * Cfg::WM + mt * 8 + r;
+        a[mt] = *reinterpret_cast<const double*>(bx + m * 128);
+      }
     }
+    {
+      const char* bx = Bs + box * (Cfg::BN * 128) + (kl & 1) * 8 + ((((kl >> 1) ^ r)) << 4);
 #pragma unroll
-    for (int nt = 0; nt < Cfg::NT; ++nt) {
-      const int n = wn * Cfg::WN + nt * 8 + r;
-      b[nt] = Bs[n * Cfg::SB_K + k4 + q];
+      for (int nt = 0; nt < Cfg::NT; ++nt) {
+        const int n = wn * Cfg::WN + nt * 8 + r;
+        b[nt] = *reinterpret_cast<const double*>(bx + n * 128);
+      }
     }
 #pragma unroll
     for (int mt = 0; mt < Cfg::MT; ++mt)
@@ -281,9 +281,6 @@ __device__ __forceinline__ size_t frag_index(int warp, int mt, int nt, int x, in
 }
 
 // ---- mbarrier helpers ------------------------------------------------------------
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
 }
@@ -300,122 +297,83 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)));
 }
-// arrives on `bar` once all prior cp.async of this thread have landed
-__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)));
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
 }
 
-// ---- producers: NP warps of the producer warpgroup stream the CTA's unit
-// range into the smem ring, each 1/NP of every stage.  Long-K products use all
-// 4 (one per SM sub-partition, so no consumer pair shares its issue slots with
-// the whole copy stream); short-K tiles with heavy epilogues use one.
-// Per-lane source pointers are set up once per tile and advanced by one k-slice
-// per unit, so the copy loop is pure LDGSTS + pointer increments.
+// ---- producer: ONE thread streams the CTA's unit range into the smem ring.
+// Per stage it waits for the consumers to free the slot, announces the stage's
+// bytes on the slot's `full` barrier and issues the TMA box loads (A: BM/16
+// or BK/16 boxes, B: BK/16 boxes); the TMA unit completes the transaction
+// count, zero-filling every element outside the logical extents (edge tiles).
 constexpr int kProducerRegs = 40;  // per producer thread after setmaxnreg
-template <class Cfg, int PW, int NP>
-__device__ __forceinline__ void produce(const GemmArgs& g, double* As, double* Bs,
-                                        uint64_t* full, uint64_t* empty, int64_t u0, int64_t u1,
-                                        int lane) {
+template <class Cfg>
+__device__ __forceinline__ void produce_tma(const GemmArgs& g, const GemmMaps& maps, char* As,
+                                            char* Bs, uint64_t* full, uint64_t* empty, int64_t u0,
+                                            int64_t u1) {
   constexpr int BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK, S = Cfg::STAGES;
-  // A_MCONTIG: lane owns m-chunks {2·lane + 64·h}; A_KCONTIG / B: lane owns
-  // rows {lane/CPR + RPP·j} at k-chunk lane%CPR (CPR = BK/2 chunks per row).
-  // One base pointer per operand advances one k-slice per unit (the producer
-  // runs on 40 registers).
-  constexpr int CPR = BK / 2, RPP = 32 / CPR;
-  constexpr int AH = Cfg::AMODE == A_MCONTIG ? BM / 64 : BM / RPP;
-  constexpr int BJ = BN / RPP;
-  static_assert(Cfg::AMODE != A_MCONTIG || BM % 64 == 0, "MCONTIG producer needs BM % 64 == 0");
-  static_assert((BK == 16 || BK == 32) && AH <= 64 && BJ <= 64, "producer layout");
-  const double* pa = g.A;
-  const double* pb = g.B;
-  uint64_t amask = 0, bmask = 0;
-  int cur_tile = -1;
-  const int64_t a_step = Cfg::AMODE == A_MCONTIG ? (int64_t)BK * g.lda : BK;
-  const int64_t a_rows = Cfg::AMODE == A_MCONTIG ? 64 : RPP * g.lda;  // stride between lane chunks
-  const int64_t b_rows = RPP * g.ldb;
-  const int lr = lane / CPR, lc = 2 * (lane % CPR);
   const bool a_stream = Cfg::AMODE == A_MCONTIG && g.a_stream;
   const uint64_t pol = a_stream ? l2_evict_first_policy() : 0;
-  int t = (int)(u0 / g.ki), kk = (int)(u0 % g.ki);  // advanced incrementally
+  int t = (int)(u0 / g.ki), kk = (int)(u0 % g.ki);
+  int2 tc = g.tiles[t];
   int s = 0;
   unsigned ph = 0;
   for (int64_t u = u0; u < u1; ++u) {
-    if (t != cur_tile) {  // (re)base on this tile at k-iteration kk
-      cur_tile = t;
-      const int2 tc = g.tiles[t];
-      const int64_t m0 = (int64_t)tc.x * BM, n0 = (int64_t)tc.y * BN;
-      const int64_t k0 = (int64_t)kk * BK;
-      amask = 0;
-      bmask = 0;
-      if constexpr (Cfg::AMODE == A_MCONTIG) {
-        pa = g.A + (m0 + 2 * lane) + k0 * g.lda;
-#pragma unroll
-        for (int h = 0; h < AH; ++h)
-          if (m0 + 2 * lane + 64 * h < g.M) amask |= 1ull << h;
-      } else {
-        pa = g.A + (k0 + lc) + (m0 + lr) * g.lda;
-#pragma unroll
-        for (int h = 0; h < AH; ++h)
-          if (m0 + lr + RPP * h < g.M) amask |= 1ull << h;
-      }
-      pb = g.B + (k0 + lc) + (n0 + lr) * g.ldb;
-#pragma unroll
-      for (int j = 0; j < BJ; ++j)
-        if (n0 + lr + RPP * j < g.N) bmask |= 1ull << j;
-    }
     mbar_wait(&empty[s], ph ^ 1u);
-    double* as = As + s * Cfg::A_STAGE;
-    double* bs = Bs + s * Cfg::B_STAGE;
+    mbar_arrive_expect_tx(&full[s], Cfg::STAGE_BYTES);
+    char* as = As + s * (Cfg::A_STAGE * 8);
+    char* bs = Bs + s * (Cfg::B_STAGE * 8);
+    const int m0 = tc.x * BM, n0 = tc.y * BN, k0 = kk * BK;
     if constexpr (Cfg::AMODE == A_MCONTIG) {
 #pragma unroll
-      for (int h = 0; h < AH; ++h) {
-        const bool ok = (amask >> h) & 1ull;
-#pragma unroll
-        for (int kr = PW; kr < BK; kr += NP) {
-          double* dst = as + kr * Cfg::SA_M + 2 * lane + 64 * h;
-          const double* src = ok ? pa + h * a_rows + kr * g.lda : g.A;
-          if (a_stream) cp_async16_pol(dst, src, ok, pol);
-          else cp_async16(dst, src, ok);
-        }
+      for (int mb = 0; mb < BM / 16; ++mb) {
+        if (a_stream)
+          tma_load_2d_hint(as + mb * (BK * 128), &maps.a, m0 + 16 * mb, k0, &full[s], pol);
+        else
+          tma_load_2d(as + mb * (BK * 128), &maps.a, m0 + 16 * mb, k0, &full[s]);
       }
     } else {
 #pragma unroll
-      for (int h = PW; h < AH; h += NP) {
-        const bool ok = (amask >> h) & 1ull;
-        cp_async16(as + (lr + RPP * h) * Cfg::SA_K + lc, ok ? pa + h * a_rows : g.A, ok);
-      }
+      for (int kh = 0; kh < BK / 16; ++kh)
+        tma_load_2d(as + kh * (BM * 128), &maps.a, k0 + 16 * kh, m0, &full[s]);
     }
 #pragma unroll
-    for (int j = PW; j < BJ; j += NP) {
-      const bool ok = (bmask >> j) & 1ull;
-      cp_async16(bs + (lr + RPP * j) * Cfg::SB_K + lc, ok ? pb + j * b_rows : g.B, ok);
-    }
-    cp_async_mbar_arrive(&full[s]);
-    pa += a_step;
-    pb += BK;
+    for (int kh = 0; kh < BK / 16; ++kh)
+      tma_load_2d(bs + kh * (BN * 128), &maps.b, k0 + 16 * kh, n0, &full[s]);
     if (++s == S) {
       s = 0;
       ph ^= 1u;
     }
     if (++kk == g.ki) {
       kk = 0;
-      ++t;
+      if (u + 1 < u1) tc = g.tiles[++t];
     }
   }
+}
+
+// Smem carve-up shared by both kernels: 1024-byte aligned ring, then barriers.
+// (offset arithmetic on the __shared__ array itself, so the compiler keeps the
+// shared address space: LDS with 32-bit addresses, not generic loads)
+template <class Cfg>
+__device__ __forceinline__ char* smem_ring(char* raw) {
+  return raw + ((1024u - (smem_u32(raw) & 1023u)) & 1023u);
 }
 
 // ---- main kernel ----------------------------------------------------------------
 // Warp-specialized: warps [0, WARPS) consume (LDS + DMMA + epilogue), warp
 // WARPS produces (cp.async ring, one mbarrier pair per stage); the rest of
 // the producer warpgroup only donates its registers.
-template <class Cfg, int EPI, int NPROD>
-__global__ void __launch_bounds__(Cfg::THREADS + 128, 1) gemm_streamk(GemmArgs g) {
+template <class Cfg, int EPI>
+__global__ void __launch_bounds__(Cfg::THREADS + 128, 1)
+    gemm_streamk(GemmArgs g, const __grid_constant__ GemmMaps maps) {
   if (g.ctl && g.ctl->done) return;
   if (g.gate && !*g.gate) return;
-  extern __shared__ __align__(16) double smem[];
-  double* As = smem;
-  double* Bs = smem + Cfg::STAGES * Cfg::A_STAGE;
-  uint64_t* full = reinterpret_cast<uint64_t*>(Bs + Cfg::STAGES * Cfg::B_STAGE);
+  extern __shared__ __align__(1024) char smem_raw[];
+  char* As = smem_ring<Cfg>(smem_raw);
+  char* Bs = As + Cfg::STAGES * Cfg::A_STAGE * 8;
+  uint64_t* full = reinterpret_cast<uint64_t*>(Bs + Cfg::STAGES * Cfg::B_STAGE * 8);
   uint64_t* empty = full + Cfg::STAGES;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int32_t cta = blockIdx.x;
@@ -426,9 +384,10 @@ __global__ void __launch_bounds__(Cfg::THREADS + 128, 1) gemm_streamk(GemmArgs g
   if (u0 >= u1) return;
   if (threadIdx.x == 0) {
     for (int s = 0; s < Cfg::STAGES; ++s) {
-      mbar_init(&full[s], 32 * NPROD);
+      mbar_init(&full[s], 1);
       mbar_init(&empty[s], Cfg::WARPS);
     }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
   // The producer owns a whole warpgroup (setmaxnreg is warpgroup-collective):
@@ -436,18 +395,7 @@ __global__ void __launch_bounds__(Cfg::THREADS + 128, 1) gemm_streamk(GemmArgs g
   // group kProducerRegs = 40 (8·32·232 + 4·32·40 ≤ 64K).
   if (warp >= Cfg::WARPS) {
     if constexpr (Cfg::WARPS >= 8) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kProducerRegs));
-    const int pw = warp - Cfg::WARPS;
-    if constexpr (NPROD == 4) {
-      switch (pw) {
-        case 0: produce<Cfg, 0, 4>(g, As, Bs, full, empty, u0, u1, lane); break;
-        case 1: produce<Cfg, 1, 4>(g, As, Bs, full, empty, u0, u1, lane); break;
-        case 2: produce<Cfg, 2, 4>(g, As, Bs, full, empty, u0, u1, lane); break;
-        default: produce<Cfg, 3, 4>(g, As, Bs, full, empty, u0, u1, lane); break;
-      }
-    } else {
-      if (pw == 0) produce<Cfg, 0, 1>(g, As, Bs, full, empty, u0, u1, lane);
-    }
-    cp_async_wait<0>();
+    if (warp == Cfg::WARPS && lane == 0) produce_tma<Cfg>(g, maps, As, Bs, full, empty, u0, u1);
     return;
   }
   if constexpr (Cfg::WARPS >= 8) {
@@ -477,7 +425,8 @@ __global__ void __launch_bounds__(Cfg::THREADS + 128, 1) gemm_streamk(GemmArgs g
   unsigned phase = 0;
   for (int64_t u = u0; u < u1; ++u) {
     mbar_wait(&full[stage], phase);
-    mma_stage<Cfg>(As + stage * Cfg::A_STAGE, Bs + stage * Cfg::B_STAGE, wm, wn, lane, acc);
+    mma_stage<Cfg>(As + stage * (Cfg::A_STAGE * 8), Bs + stage * (Cfg::B_STAGE * 8), wm, wn, lane,
+                   acc);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[stage]);
     if (++stage == Cfg::STAGES) {
@@ -597,15 +546,16 @@ __device__ __forceinline__ void epilogue_xm_group(const GemmArgs& g, int tm, int
 
 constexpr int kTmemEpiRegs = 104;  // epilogue warpgroup after setmaxnreg
 template <class Cfg>
-__global__ void __launch_bounds__(Cfg::THREADS + 256, 1) gemm_xm_tmem(GemmArgs g) {
+__global__ void __launch_bounds__(Cfg::THREADS + 256, 1)
+    gemm_xm_tmem(GemmArgs g, const __grid_constant__ GemmMaps maps) {
   static_assert(Cfg::WARPS == 8 && Cfg::WARPS_N == 4 && Cfg::MT * Cfg::NT * 4 == 128,
                 "TMEM staging: 8 consumer warps (2 × 4), 64 doubles each");
   if (g.ctl && g.ctl->done) return;
-  extern __shared__ __align__(16) double smem[];
+  extern __shared__ __align__(1024) char smem_raw[];
   constexpr int S = Cfg::STAGES;
-  double* As = smem;
-  double* Bs = smem + S * Cfg::A_STAGE;
-  uint64_t* full = reinterpret_cast<uint64_t*>(Bs + S * Cfg::B_STAGE);
+  char* As = smem_ring<Cfg>(smem_raw);
+  char* Bs = As + S * Cfg::A_STAGE * 8;
+  uint64_t* full = reinterpret_cast<uint64_t*>(Bs + S * Cfg::B_STAGE * 8);
   uint64_t* empty = full + S;
   uint64_t* acc_full = empty + S;   // [2]
   uint64_t* acc_empty = acc_full + 2;  // [2]
@@ -616,13 +566,14 @@ __global__ void __launch_bounds__(Cfg::THREADS + 256, 1) gemm_xm_tmem(GemmArgs g
   if (t0 >= t1) return;  // uniform over the CTA, before any TMEM allocation
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
-      mbar_init(&full[i], 32 * 4);
+      mbar_init(&full[i], 1);
       mbar_init(&empty[i], Cfg::WARPS);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], Cfg::WARPS);
       mbar_init(&acc_empty[b], 4);
     }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 0) {  // all 512 columns: two 128 × (2 × 128) accumulator buffers
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n"
@@ -635,16 +586,8 @@ __global__ void __launch_bounds__(Cfg::THREADS + 256, 1) gemm_xm_tmem(GemmArgs g
   const uint32_t tbase = *tslot;
   if (warp >= Cfg::WARPS && warp < Cfg::WARPS + 4) {  // producer warpgroup
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kProducerRegs));
-    // all four warps copy: the consumers no longer pause for epilogues, so the
-    // ring must refill at the full DMMA rate
     const int64_t u0 = (int64_t)t0 * g.ki, u1 = (int64_t)t1 * g.ki;
-    switch (warp - Cfg::WARPS) {
-      case 0: produce<Cfg, 0, 4>(g, As, Bs, full, empty, u0, u1, lane); break;
-      case 1: produce<Cfg, 1, 4>(g, As, Bs, full, empty, u0, u1, lane); break;
-      case 2: produce<Cfg, 2, 4>(g, As, Bs, full, empty, u0, u1, lane); break;
-      default: produce<Cfg, 3, 4>(g, As, Bs, full, empty, u0, u1, lane); break;
-    }
-    cp_async_wait<0>();
+    if (warp == Cfg::WARPS && lane == 0) produce_tma<Cfg>(g, maps, As, Bs, full, empty, u0, u1);
     return;
   }
   const uint32_t quarter = (uint32_t)(warp & 3) * 32u;
@@ -715,7 +658,8 @@ __global__ void __launch_bounds__(Cfg::THREADS + 256, 1) gemm_xm_tmem(GemmArgs g
       for (int nt = 0; nt < Cfg::NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
     for (int kk = 0; kk < g.ki; ++kk) {
       mbar_wait(&full[stage], phase);
-      mma_stage<Cfg>(As + stage * Cfg::A_STAGE, Bs + stage * Cfg::B_STAGE, wm, wn, lane, acc);
+      mma_stage<Cfg>(As + stage * (Cfg::A_STAGE * 8), Bs + stage * (Cfg::B_STAGE * 8), wm, wn,
+                     lane, acc);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[stage]);
       if (++stage == S) {

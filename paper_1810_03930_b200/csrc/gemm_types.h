@@ -53,7 +53,6 @@ struct GemmArgs {
   int32_t force_ws;     // chunk-partial plans: every CTA stores its partial (no epilogue)
   int32_t segs;         // > 0: segmented schedule, S fixed K segments per tile (see below)
   int32_t a_stream;     // A is read exactly once (dense gradient): L2 evict-first loads
-  int32_t nprod;        // producer warps (1 or 4)
 };
 
 struct FixupTask {   // one split tile

@@ -44,11 +44,14 @@ def load(name):
     return np.load(path)
 
 
-def check_window(tr, ref, w, f_tol=1e-9):
+def check_window(tr, ref, w, f_tol=1e-9, feas_floor=1e-13):
+    """feas_floor: ‖XᵀX − I‖_F at the orthonormal X0 is pure rounding of the
+    Gram (≈1e-15 at p = 20, 3e-14 (reference) / 1.5e-13 (GPU) at p = 1024) —
+    an absolute floor under the post-orth bar of 1e-12."""
     assert np.array_equal(tr[:w, 0], ref[:w, 0])
     assert close(tr[:w, 1], ref[:w, 1], f_tol), np.max(np.abs(tr[:w, 1] / ref[:w, 1] - 1))
     assert close(tr[:w, 2], ref[:w, 2], 1e-9), np.max(np.abs(tr[:w, 2] / ref[:w, 2] - 1))
-    assert close(tr[:w, 4], ref[:w, 4], 1e-9, 1e-13)   # feas: ≈1e-15 rounding at X0
+    assert close(tr[:w, 4], ref[:w, 4], 1e-9, feas_floor)
     assert close(tr[:w, 5], ref[:w, 5], 1e-9)
 
 
@@ -86,7 +89,7 @@ def test_cfg5_shape_p1024_against_reference(pcal, orc, name, grid):
     rep = pcal.solve(pcal.StencilModel(grid, v, 1024, s),
                      pcal.SolverConfig(tol_rel_kkt=TINY, max_iter=tr_ref.shape[0] - 1), x0)
     assert rep.status == str(g[name + "_status"]) == "max_iter"
-    check_window(rep.trace, tr_ref, tr_ref.shape[0], f_tol=1e-11)
+    check_window(rep.trace, tr_ref, tr_ref.shape[0], f_tol=1e-11, feas_floor=1e-12)
     idx = g[name + "_row_idx"]
     assert np.abs(rep.stop_iterate[idx] - g[name + "_stop_x_rows"]).max() <= 1e-12
     fpre, fpost = g[name + "_final_pre"], g[name + "_final_post"]
@@ -154,7 +157,7 @@ def test_grid_configs_40_iteration_window(pcal, orc, name):
     rep = pcal.solve(cls(grid, v, p, s),
                      pcal.SolverConfig(tol_rel_kkt=TINY, max_iter=tr_ref.shape[0] - 1,
                                        final_orth=False), x0)
-    check_window(rep.trace, tr_ref, tr_ref.shape[0])
+    check_window(rep.trace, tr_ref, tr_ref.shape[0], feas_floor=1e-12)
     idx = g[name + "_row_idx"]
     assert np.abs(rep.stop_iterate[idx] - g[name + "_stop_x_rows"]).max() <= 1e-10
 
