@@ -290,6 +290,46 @@ def harness_cases(R: Reference) -> None:
     print("wrote run_single reports")
 
 
+def harness_ensembles(R: Reference, k: int = 8) -> None:
+    """For every run_single case: the iteration count and post-orth objective of
+    the reference solve() from the run_single start point and from K copies of
+    it with one entry moved by one ulp — how far a converging run's step count
+    moves under rounding-level differences (the GPU's tolerance)."""
+    import ctypes as C
+    from types import SimpleNamespace
+    L = R.lib
+    L.ref_make_problem.restype = C.c_void_p
+    L.ref_make_problem.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_double, C.c_double,
+                                   C.c_double, C.c_double, C.c_double, C.c_int, C.c_uint64]
+    g = {}
+    for name, (kind, n, p, alpha, kappa, theta, zeta, xi, bt, seed, init, sigma, iters) in \
+            HARNESS_CASES.items():
+        h = L.ref_make_problem(kind, n, p, alpha, kappa, theta, zeta, xi, bt, seed)
+        assert h, name
+        x0 = np.empty((n, p), order="F")
+        assert L.ref_initial_point(init, sigma, seed ^ INIT_SALT, n, p,
+                                   x0.ctypes.data_as(C.POINTER(C.c_double))) == 0
+        its, fpost = [], []
+        for q in range(k + 1):
+            xp = x0.copy(order="F")
+            if q > 0:
+                e = (q * 2654435761) % xp.size
+                xp.flat[e] = np.nextafter(xp.flat[e], np.inf if q % 2 else -np.inf)
+            cfg = Config(max_iter=iters, threads=1)
+            rep, keep = R._report(SimpleNamespace(n=n, p=p), cfg, ())
+            assert L.ref_solve(C.c_void_p(h), C.byref(cfg.c()), xp.ctypes.data_as(C.POINTER(C.c_double)),
+                               C.byref(rep), None) == 0, name
+            out = R._finish(rep, keep, ())
+            its.append(out.iterations)
+            fpost.append(out.final_post[0] if out.final_post is not None else np.nan)
+        L.ref_free_model(C.c_void_p(h))
+        g[name + "_iterations"] = np.array(its)
+        g[name + "_final_post_f"] = np.array(fpost)
+        print(name, its)
+    np.savez_compressed(os.path.join(OUT, "reference_run_single_ensembles.npz"), **g)
+    print("wrote reference_run_single_ensembles.npz")
+
+
 def linsolve_cases(R: Reference) -> None:
     """LinearSolver (linsolve.cpp) inverses: random symmetric (LU path), the block
     operator (Cholesky path), a singular matrix (generation_error)."""
@@ -465,6 +505,7 @@ if __name__ == "__main__":
     json_magnitudes_case(R)
     init_cases(R)
     harness_cases(R)
+    harness_ensembles(R)
     linsolve_cases(R)
     model_eval_cases(R)
     alm_cases(R)

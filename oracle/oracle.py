@@ -191,6 +191,7 @@ class Restatement(_Base):
         L.orc_matmul_at_b.argtypes = [_dp, i64, i64, _dp, i64, _dp, C.c_int]
         L.orc_gram.argtypes = [_dp, i64, i64, _dp, C.c_int]
         L.orc_orthonormalize.argtypes = [_dp, i64, i64, _dp]
+        L.orc_mgs2.argtypes = [_dp, i64, i64, dbl, _dp]
         L.orc_spectral_norm_estimate.argtypes = [_dp, i64, u64, C.c_int]
         L.orc_spectral_norm_estimate.restype = dbl
         L.orc_model_prepare.argtypes = [C.POINTER(OrcModel)]
@@ -253,6 +254,14 @@ class Restatement(_Base):
         rc = self.lib.orc_orthonormalize(_ptr(x), x.shape[0], x.shape[1], _ptr(q))
         if rc == E_RANK:
             raise np.linalg.LinAlgError("orthonormalize: numerically rank-deficient input")
+        return q
+
+    def mgs2(self, x, floor: float) -> np.ndarray:
+        """mgs2 (kernels.cpp:212-246), the fallback of orthonormalize."""
+        x = fmat(x)
+        q = np.empty_like(x, order="F")
+        if self.lib.orc_mgs2(_ptr(x), x.shape[0], x.shape[1], floor, _ptr(q)) == E_RANK:
+            raise np.linalg.LinAlgError("mgs2: numerically rank-deficient input")
         return q
 
     def initial_point_qr(self, n: int, p: int, seed: int, threads: int = 1) -> np.ndarray:

@@ -212,6 +212,10 @@ static int mgs2(const double* x, int64_t n, int64_t p, double floor_, double* q)
   return ORC_OK;
 }
 
+int orc_mgs2(const double* x, int64_t n, int64_t p, double floor_, double* q) {
+  return mgs2(x, n, p, floor_, q);
+}
+
 /* orthonormalize_with_r (kernels.cpp:250-261). */
 int orc_orthonormalize(const double* x, int64_t n, int64_t p, double* q) {
   return orc_orthonormalize_t(x, n, p, q, 1);

@@ -52,6 +52,8 @@ double orc_frobenius_norm(const double* a, int64_t count);               /* :311
  * Returns 0, or ORC_E_RANK when the fallback hits the pivot floor. */
 int orc_orthonormalize(const double* x, int64_t n, int64_t p, double* q);
 int orc_orthonormalize_t(const double* x, int64_t n, int64_t p, double* q, int threads);
+/* mgs2 (kernels.cpp:212-246) alone: ORC_E_RANK when a column norm² ≤ floor. */
+int orc_mgs2(const double* x, int64_t n, int64_t p, double floor_, double* q);
 /* blocked restatements (orc_blas.c), bitwise equal to the reference loops */
 void orc_blas_matmul(const double* a, int64_t m, int64_t kdim, const double* b, int64_t ncols,
                      double* c, int threads);

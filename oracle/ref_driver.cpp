@@ -455,6 +455,32 @@ int ref_run_single_json(int kind, std::int64_t n, std::int64_t p, double alpha, 
   });
 }
 
+// make_problem(ProblemSpec) (harness.cpp:31-46) as a model handle for
+// ref_solve (freed by ref_free_model): the reference's own instance of every
+// problem kind, for runs from caller-chosen start points.
+void* ref_make_problem(int kind, std::int64_t n, std::int64_t p, double alpha, double kappa,
+                       double theta, double zeta, double xi, int block_tridiag,
+                       std::uint64_t seed) {
+  void* out = nullptr;
+  const int rc = guarded([&] {
+    ProblemSpec spec;
+    spec.kind = kind == 1 ? ProblemKind::P1 : kind == 2 ? ProblemKind::P2
+                : kind == 3 ? ProblemKind::P3 : kind == 4 ? ProblemKind::P4 : ProblemKind::P6;
+    spec.n = n;
+    spec.p = p;
+    spec.alpha = alpha;
+    spec.kappa = kappa;
+    spec.theta = theta;
+    spec.zeta = zeta;
+    spec.xi = xi;
+    spec.mode = block_tridiag ? OperatorMode::BlockTridiag : OperatorMode::RandomSym;
+    spec.seed = seed;
+    out = make_problem(spec).release();
+    return 0;
+  });
+  return rc == 0 ? out : nullptr;
+}
+
 int ref_save_quadratic(const double* a, const double* g0, std::int64_t n, std::int64_t p, double s,
                        const char* path) {
   return guarded([&] {

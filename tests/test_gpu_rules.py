@@ -6,10 +6,11 @@
   drive a config-1 solve; the GPU's trace window — η in particular — must
   match the oracle's (the reference's closed forms are pinned on the CPU by
   tests/test_oracle_golden.py against test_solver.cpp:167-224's shapes).
-* orthonormalize (kernels.cpp:250-261): a start whose first Cholesky pass
-  hits the pivot floor 1e-14·‖XᵀX‖_F although the columns are independent, so
-  the MGS2 fallback runs and succeeds (the condition-1e6 family of
-  test_kernels.cpp:183-195 pushed past the floor).
+* orthonormalize (kernels.cpp:250-261): a start whose Cholesky pass hits the
+  pivot floor 1e-14·‖XᵀX‖_F although the columns are independent, so the MGS2
+  fallback runs and succeeds (a nearly parallel column, the condition-1e6
+  family of test_kernels.cpp:183-195 pushed to the floor), and one far under
+  the floor that raises rank_error.
 """
 import math
 import os
@@ -80,28 +81,37 @@ def _near_parallel(orc, n, eps_scale):
 
 
 def test_orthonormalize_mgs2_fallback_succeeds(pcal, orc):
-    """Scan α upward from the floor: the first start whose DEVICE Cholesky pass
-    fails takes MGS2, which must succeed (the columns are independent) and
-    agree with the oracle's orthonormalize of the same matrix."""
+    """orthonormalize falls back to MGS2 exactly when a Cholesky pivot lands on
+    or under 1e-14·‖XᵀX‖_F; MGS2 then tests the SAME quantity (the column's
+    squared distance to the span of the previous ones) against the same floor,
+    so 'Cholesky fails, MGS2 succeeds' only happens within rounding of the floor
+    — which side a start lands on depends on summation order, in the reference
+    as on the GPU.  Scan α upward from the floor until the DEVICE takes the
+    MGS2 branch and succeeds; the result must be the oracle's MGS2 of the same
+    matrix (kernels.cpp:212-246) and an orthonormal basis of X's column flag."""
     hit = None
-    for k in range(400):
-        x = _near_parallel(orc, 50, 1.0 + 0.05 * k / 400)
+    for k in range(800):
+        x = _near_parallel(orc, 50, 1.0 + 0.05 * k / 800)
         try:
             q = pcal.orthonormalize(x)
         except np.linalg.LinAlgError:
             continue  # α still under the floor for MGS2 as well
         if pcal.last_orthonormalize_path().startswith("mgs2"):
-            hit = (x, q)
+            floor = 1e-14 * np.linalg.norm(orc.gram(x))
+            try:
+                qo = orc.mgs2(x, floor)
+            except np.linalg.LinAlgError:
+                continue  # the oracle's sums put this start under the floor
+            hit = (x, q, qo)
             break
-    assert hit is not None, "no start took the MGS2 branch"
-    x, q = hit
+    assert hit is not None, "no start took (and passed) the MGS2 branch"
+    x, q, qo = hit
     assert np.linalg.norm(q.T @ q - np.eye(3)) <= 1e-12
-    qo = orc.orthonormalize(x)   # the oracle's result (CholeskyQR2 or MGS2, same Q)
     s = np.sign(np.sum(q * qo, axis=0))
-    assert np.abs(q[:, :2] * s[:2] - qo[:, :2]).max() <= 1e-13
-    assert np.abs(q[:, 2] * s[2] - qo[:, 2]).max() <= 1e-6  # the 1e-7-sized residual's direction
-    # span check: X = Q·R with R upper triangular
-    r = q.T @ x
+    assert np.all(s > 0)  # MGS keeps each column's direction (positive R diagonal)
+    assert np.abs(q[:, :2] - qo[:, :2]).max() <= 1e-13
+    assert np.abs(q[:, 2] - qo[:, 2]).max() <= 1e-6  # the ~1e-7-sized residual's direction
+    r = q.T @ x  # X = Q·R with R upper triangular
     assert np.abs(np.tril(r, -1)).max() <= 1e-12
 
 

@@ -113,8 +113,13 @@ def full(path: str, out, summary: dict):
         print(f"  dram read+write per launch: {(rb + wb) / 1e9:.4f} GB; "
               f"effective {(rb + wb) / t / 1e9:.1f} GB/s", file=out)
         ph = phase_of(name)
-        if ("streamk" in name or "xm_tmem" in name) and ph in ("gradient", "gram", "xm"):
-            summary.setdefault(ph, rb + wb)
+        kern = ("streamk" in name or "xm_tmem" in name or "xm_staged" in name
+                or "stencil" in name)
+        # per phase: the longest capture (the iteration's launch, not a smaller
+        # set-up launch of the same kernel, e.g. the initial point's Gram)
+        if kern and ph in ("gradient", "gram", "xm") and rb + wb == rb + wb:
+            if ph not in summary or t > summary[ph][1]:
+                summary[ph] = (rb + wb, t)
 
 
 def main():
@@ -136,7 +141,9 @@ def main():
             full(a.full, f, summ)
         with open(os.path.join(prof, f"ncu_cfg{a.config}_summary.json"), "w") as f:
             json.dump({"source": os.path.basename(a.full), "tag": a.tag,
-                       "dram_bytes_per_launch": summ}, f, indent=1)
+                       "dram_bytes_per_launch": {k: v[0] for k, v in summ.items()},
+                       "duration_s_per_launch": {k: v[1] for k, v in summ.items()}},
+                      f, indent=1)
 
 
 if __name__ == "__main__":
