@@ -16,6 +16,7 @@ namespace pcal {
 
 template <int AM>
 using CfgBig = GemmCfg<128, 128, 2, 4, 3, AM, 32>;  // BK = 32: 3 × 64 KB stages
+using CfgXms = GemmCfg<128, 64, 4, 2, 3, A_MCONTIG, 32>;  // staged X·[W|C]: 3 × 48 KB + 64 KB
 template <int AM>
 using CfgMid = GemmCfg<64, 64, 2, 2, 4, AM>;
 template <int AM>
@@ -31,6 +32,7 @@ CfgInfo cfg_info(int size) {
   switch (size) {
     case CFG_BIG:
     case CFG_XMT: return {128, 128, CfgBig<A_MCONTIG>::WM, CfgBig<A_MCONTIG>::BK};
+    case CFG_XMS: return {128, 64, CfgXms::WM, CfgXms::BK};
     case CFG_MID: return {64, 64, 32, CfgMid<A_MCONTIG>::BK};
     default: return {64, 32, 32, CfgSmall<A_MCONTIG>::BK};
   }
@@ -115,12 +117,14 @@ void plan_gemm(GemmPlan& pl, int device, int size, int amode, int epi, int64_t M
     const int64_t g0 = grid;
     const int64_t dp_cost = ceil_div(ntiles, g0) * ki;
     const int64_t sk_cost = ceil_div(units, g0) + 4;
-    if (size == CFG_XMT && (amode != A_MCONTIG || epi != EPI_XM))
-      throw Error(PCAL_E_STATE, "gemm: the TMEM-epilogue kernel is X·[W|C] only");
-    if (dp_cost <= sk_cost || size == CFG_XMT) {  // gemm_xm_tmem: whole tiles only
+    const bool xm_only = size == CFG_XMT || size == CFG_XMS;
+    if (xm_only && (amode != A_MCONTIG || epi != EPI_XM))
+      throw Error(PCAL_E_STATE, "gemm: the TMEM / staged-epilogue kernels are X·[W|C] only");
+    if (dp_cost <= sk_cost || xm_only) {  // gemm_xm_tmem / gemm_xm_staged: whole tiles only
       const int64_t w = ceil_div(ntiles, g0);
       upc = w * ki;
-      grid = (int)ceil_div(ntiles, w);
+      // gemm_xm_staged walks the tiles round-robin (one CTA per SM)
+      grid = size == CFG_XMS ? (int)std::min<int64_t>(ntiles, g0) : (int)ceil_div(ntiles, w);
     } else if (epi != EPI_STORE && grid > 4 * (int64_t)ntiles) {
       // fused epilogues are fixed up one tile per CTA: keep ≤ 4 partials per tile
       grid = (int)(4 * (int64_t)ntiles);
@@ -195,19 +199,21 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 }
 
 // 2-D FP64 tensor {inner, outer} with row pitch ld (elements), box
-// {16, box_outer}, 128-byte swizzle, zero fill outside the extents.
+// {box_inner, box_outer} (default {16, ·} with the 128-byte swizzle of the GEMM
+// rings), zero fill outside the extents.
 static void encode_map(CUtensorMap* m, const double* base, int64_t inner, int64_t outer,
-                       int64_t ld, int box_outer) {
+                       int64_t ld, int box_outer, int box_inner = 16,
+                       CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   if ((reinterpret_cast<uintptr_t>(base) & 15) || (ld * 8) % 16 || inner < 1 || outer < 1 ||
       inner > ld)
     throw Error(PCAL_E_STATE, "gemm: operand not TMA-addressable (16-byte aligned base / pitch)");
   const cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
   const cuuint64_t strides[1] = {(cuuint64_t)(ld * 8)};
-  const cuuint32_t box[2] = {16u, (cuuint32_t)box_outer};
+  const cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer};
   const cuuint32_t estr[2] = {1u, 1u};
   const CUresult r = tensor_map_encoder()(
       m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, estr,
-      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+      CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     throw Error(PCAL_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
@@ -265,11 +271,37 @@ static void launch_xm_tmem(const GemmPlan& pl, cudaStream_t st) {
   PCAL_CUDA(cudaGetLastError());
 }
 
+static void launch_xm_staged(const GemmPlan& pl, cudaStream_t st) {
+  using Cfg = CfgXms;
+  constexpr int kOut = Cfg::BN / 2;
+  constexpr int smem = Cfg::SMEM_BYTES + (2 * Cfg::BM * kOut + 2 * 8 * kOut) * 8 + 2 * 8;
+  static_assert(smem <= 232448, "staged XM: shared memory budget");
+  static bool attr_set = false;
+  if (!attr_set) {
+    PCAL_CUDA(cudaFuncSetAttribute(gemm_xm_staged<Cfg>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr_set = true;
+  }
+  const GemmArgs& g = pl.args;
+  XmMaps maps;
+  encode_map(&maps.a, g.A, g.M, g.K, g.lda, Cfg::BK);
+  encode_map(&maps.b, g.B, g.K, g.N, g.ldb, Cfg::BN);
+  encode_map(&maps.g, g.ep.G, g.ep.n, g.ep.p, g.ep.ld, kOut, Cfg::BM, CU_TENSOR_MAP_SWIZZLE_NONE);
+  encode_map(&maps.x, g.ep.X, g.ep.n, g.ep.p, g.ep.ld, kOut, Cfg::BM, CU_TENSOR_MAP_SWIZZLE_NONE);
+  gemm_xm_staged<Cfg><<<g.grid, Cfg::THREADS + 128, smem, st>>>(g, maps);
+  launched("gemm_xm");
+  PCAL_CUDA(cudaGetLastError());
+}
+
 template <int AM, int EPI>
 static void launch_sized(const GemmPlan& pl, cudaStream_t st) {
   if constexpr (AM == A_MCONTIG && EPI == EPI_XM) {
     if (pl.size == CFG_XMT) {
       launch_xm_tmem(pl, st);
+      return;
+    }
+    if (pl.size == CFG_XMS) {
+      launch_xm_staged(pl, st);
       return;
     }
   }

@@ -695,6 +695,174 @@ __global__ void __launch_bounds__(Cfg::THREADS + 256, 1)
   }
 }
 
+// ---- X·[W|C] with a fused epilogue whose operands are staged by TMA -------------
+// The epilogue of X·[W|C] needs, per output element, G and X (kkt = G − XW,
+// P = kkt + β·XC, column partials Σkkt², ΣX∘P).  Here the producer thread also
+// loads each tile's G and X blocks (128 rows × 32 output columns) into shared
+// memory with TMA while the tile is multiplied, so the consumers run the
+// epilogue straight after their last DMMA with every operand on chip: no
+// global-load latency, and the FP64 epilogue instructions run in one burst per
+// tile instead of being interleaved with (and starved by) the DMMA stream of a
+// separate epilogue warpgroup.  128 × 64 tiles (32 output columns) keep the
+// ring (3 × 48 KB) plus the staging (2 × 32 KB) inside 227 KB.
+// Column partials are reduced over the tile's 128 rows in a fixed order
+// (warp shuffles, then the four warp rows in order): one partial per
+// (128-row block, column).
+struct alignas(64) XmMaps {
+  CUtensorMap a;  // X  {n, K = pp}, box {16, BK}
+  CUtensorMap b;  // [W|C] interleaved {K = pp, 2pp}, box {16, BN}
+  CUtensorMap g;  // G  {n, p}, box {BM, BN/2} (no swizzle: [column][row])
+  CUtensorMap x;  // X  {n, p}, box {BM, BN/2}
+};
+
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS + 128, 1)
+    gemm_xm_staged(GemmArgs g, const __grid_constant__ XmMaps maps) {
+  constexpr int S = Cfg::STAGES, BM = Cfg::BM, BNO = Cfg::BN / 2;
+  static_assert(Cfg::WARPS == 8 && Cfg::WARPS_M == 4 && Cfg::WARPS_N == 2 && BM == 128 &&
+                    BNO == 32,
+                "staged XM: 128 × 64 tiles (32 output columns), 4 × 2 consumer warps");
+  if (g.ctl && g.ctl->done) return;
+  extern __shared__ __align__(1024) char smem_raw[];
+  char* As = smem_ring<Cfg>(smem_raw);
+  char* Bs = As + S * Cfg::A_STAGE * 8;
+  double* Gs = reinterpret_cast<double*>(Bs + S * Cfg::B_STAGE * 8);  // [col][row]
+  double* Xs = Gs + BM * BNO;
+  double* red = Xs + BM * BNO;                                        // [2][8][BNO]
+  uint64_t* full = reinterpret_cast<uint64_t*>(red + 2 * 8 * BNO);
+  uint64_t* empty = full + S;
+  uint64_t* efull = empty + S;
+  uint64_t* eempty = efull + 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // tiles round-robin over the CTAs: at any time the grid works on ~148
+  // consecutive (tm-major) tiles, so each 128-row block of X (the A operand,
+  // K = pp) is fetched from DRAM once and served from L2 to the CTAs of its
+  // 2pp/64 column tiles (a contiguous tile range per CTA keeps 148 different
+  // row blocks live — more than L2 holds at p = 1024)
+  if ((int)blockIdx.x >= g.ntiles) return;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], Cfg::WARPS);
+    }
+    mbar_init(efull, 1);
+    mbar_init(eempty, Cfg::WARPS);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (warp >= Cfg::WARPS) {  // producer warpgroup: one thread drives the TMA unit
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kProducerRegs));
+    if (warp != Cfg::WARPS || lane != 0) return;
+    const int kload = min(S, g.ki - 1);  // when the previous tile's epilogue is surely done
+    int s = 0;
+    unsigned ph = 0;
+    int it = 0;
+    for (int t = blockIdx.x; t < g.ntiles; t += gridDim.x, ++it) {
+      const int2 tc = g.tiles[t];
+      const int m0 = tc.x * BM, n0 = tc.y * Cfg::BN, j0 = tc.y * BNO;
+      for (int kk = 0; kk < g.ki; ++kk) {
+        if (kk == kload) {  // this tile's G / X blocks (after the previous tile's epilogue released them)
+          mbar_wait(eempty, (unsigned)(it & 1) ^ 1u);
+          mbar_arrive_expect_tx(efull, 2 * BM * BNO * 8);
+          tma_load_2d(Gs, &maps.g, m0, j0, efull);
+          tma_load_2d(Xs, &maps.x, m0, j0, efull);
+        }
+        mbar_wait(&empty[s], ph ^ 1u);
+        mbar_arrive_expect_tx(&full[s], Cfg::STAGE_BYTES);
+        char* as = As + s * (Cfg::A_STAGE * 8);
+        char* bs = Bs + s * (Cfg::B_STAGE * 8);
+        const int k0 = kk * Cfg::BK;
+#pragma unroll
+        for (int mb = 0; mb < BM / 16; ++mb)
+          tma_load_2d(as + mb * (Cfg::BK * 128), &maps.a, m0 + 16 * mb, k0, &full[s]);
+#pragma unroll
+        for (int kh = 0; kh < Cfg::BK / 16; ++kh)
+          tma_load_2d(bs + kh * (Cfg::BN * 128), &maps.b, k0 + 16 * kh, n0, &full[s]);
+        if (++s == S) {
+          s = 0;
+          ph ^= 1u;
+        }
+      }
+    }
+    return;
+  }
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(232));
+  const EpiParams& e = g.ep;
+  const int wm = warp / Cfg::WARPS_N, wn = warp % Cfg::WARPS_N;
+  const int r = lane >> 2, q = lane & 3;
+  double acc[Cfg::MT][Cfg::NT][2];
+  int stage = 0;
+  unsigned phase = 0;
+  int it = 0;
+  for (int t = blockIdx.x; t < g.ntiles; t += gridDim.x, ++it) {
+#pragma unroll
+    for (int mt = 0; mt < Cfg::MT; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < Cfg::NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+    for (int kk = 0; kk < g.ki; ++kk) {
+      mbar_wait(&full[stage], phase);
+      mma_stage<Cfg>(As + stage * (Cfg::A_STAGE * 8), Bs + stage * (Cfg::B_STAGE * 8), wm, wn,
+                     lane, acc);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (++stage == S) {
+        stage = 0;
+        phase ^= 1u;
+      }
+    }
+    // ---- epilogue: every operand in shared memory
+    const int2 tc = g.tiles[t];
+    const int64_t m0 = (int64_t)tc.x * BM;
+    const int64_t j0 = (int64_t)tc.y * BNO;
+    mbar_wait(efull, (unsigned)(it & 1));
+    double* rk = red + (it & 1) * (8 * BNO);  // per-tile double buffer: [k rows 0-3 | d rows 0-3]
+#pragma unroll
+    for (int nt = 0; nt < Cfg::NT; ++nt) {
+      const int jl = wn * (Cfg::WN / 2) + nt * 4 + q;  // output column within the tile
+      const int64_t j = j0 + jl;
+      double ks = 0.0, ds = 0.0;
+#pragma unroll
+      for (int mt = 0; mt < Cfg::MT; ++mt) {
+        const int rl = wm * Cfg::WM + mt * 8 + r;
+        const int64_t row = m0 + rl;
+        const double gv = Gs[jl * BM + rl];
+        const double xv = Xs[jl * BM + rl];
+        if (row < e.n && j < e.p) {
+          const double kkt = gv - acc[mt][nt][0];
+          const double pv = (e.p_from_g ? gv : kkt) + e.beta * acc[mt][nt][1];
+          e.G[row + j * e.ld] = pv;
+          ks += kkt * kkt;
+          ds += (e.d_sq ? pv : xv) * pv;
+        }
+      }
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1) {
+        ks += __shfl_xor_sync(0xffffffffu, ks, o);
+        ds += __shfl_xor_sync(0xffffffffu, ds, o);
+      }
+      if (r == 0) {
+        rk[wm * BNO + jl] = ks;
+        rk[(4 + wm) * BNO + jl] = ds;  // second half of the buffer: d partials
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(eempty);  // Gs / Xs of this tile are no longer read
+    // the four warp rows' partials of each column, summed in row order
+    asm volatile("bar.sync 1, %0;\n" ::"n"(Cfg::THREADS) : "memory");
+    if (warp == 0) {
+      const int jl = lane;  // BNO == 32 columns
+      const int64_t j = j0 + jl;
+      if (j < e.p) {
+        const double kv = ((rk[jl] + rk[BNO + jl]) + rk[2 * BNO + jl]) + rk[3 * BNO + jl];
+        const double dv = ((rk[4 * BNO + jl] + rk[5 * BNO + jl]) + rk[6 * BNO + jl]) +
+                          rk[7 * BNO + jl];
+        e.kpart[j * e.pstride + tc.x] = kv;
+        e.dpart[j * e.pstride + tc.x] = dv;
+      }
+    }
+  }
+}
+
 // Sums the partials of split tiles in CTA order (q = 0, 1, …) and applies the
 // epilogue with the consumer-warp geometry of the main kernel.  q-outer loop:
 // every partial contributes FRAG independent coalesced loads per thread.

@@ -1140,6 +1140,17 @@ static void launch_iteration(pcal_session* s, int b) {
   }
 }
 
+// GEMM configuration of X·[W|C] (its partial row-block is xm_row_block()).
+static int xm_config(const pcal_session* s) {
+  const int xsz = pick_size(2 * s->pp);
+  if (xsz != CFG_BIG || s->repro || getenv("PCAL_NO_TMEM_EPI")) return xsz;
+  return getenv("PCAL_XM_TMEM") ? (int)CFG_XMT : (int)CFG_XMS;
+}
+static int64_t xm_row_block(const pcal_session* s) {
+  const int c = xm_config(s);
+  return c == CFG_XMS ? cfg_info(c).BM : cfg_info(c).WM;  // staged: one partial per tile row
+}
+
 static void build_plans(pcal_session* s) {
   const int dev = s->device;
   const int64_t pp = s->pp, ld = s->ld, n = s->n;
@@ -1243,11 +1254,11 @@ static void build_plans(pcal_session* s) {
     // X·[W|C] with the PCAL epilogue: A = X (MCONTIG, K = pp), B = mcat (pp × 2pp)
     {
       GemmPlan& g = s->xm[b];
-      // wide outputs: the epilogue runs off the DMMA path from TMEM (gemm_xm_tmem,
-      // bitwise the same results)
-      const int xsz = pick_size(2 * pp);
-      const bool tmem = xsz == CFG_BIG && !s->repro && !getenv("PCAL_NO_TMEM_EPI");
-      plan_gemm(g, dev, tmem ? (int)CFG_XMT : xsz, A_MCONTIG, EPI_XM, n, 2 * pp, pp, -1, 0,
+      // wide outputs: 128 × 64 tiles whose fused epilogue reads TMA-staged G / X
+      // (gemm_xm_staged); PCAL_XM_TMEM=1 selects the TMEM-staged epilogue
+      // warpgroup instead (gemm_xm_tmem), PCAL_NO_TMEM_EPI=1 the plain fused one
+      const int xsz = xm_config(s);
+      plan_gemm(g, dev, xsz, A_MCONTIG, EPI_XM, n, 2 * pp, pp, -1, 0,
                 s->repro ? 1 : 0);  // reproducible: whole tiles, no K split
       g.args.A = Xof(s, b);
       g.args.lda = ld;
@@ -1391,7 +1402,7 @@ static void alloc_state(pcal_session* s) {
   s->mcat.zero(st);
   // partial arrays: row-block granularities
   const int64_t wm_grad = dense_family(s->model.kind) ? cfg_info(pick_size(pp)).WM : 0;
-  const int64_t wm_xm = cfg_info(pick_size(2 * pp)).WM;
+  const int64_t wm_xm = xm_row_block(s);
   s->st_chunk = 2048;
   s->st_nchunks = ceil_div(n, s->st_chunk);
   {
