@@ -286,8 +286,8 @@ static void launch_xm_staged(const GemmPlan& pl, cudaStream_t st) {
   XmMaps maps;
   encode_map(&maps.a, g.A, g.M, g.K, g.lda, Cfg::BK);
   encode_map(&maps.b, g.B, g.K, g.N, g.ldb, Cfg::BN);
-  encode_map(&maps.g, g.ep.G, g.ep.n, g.ep.p, g.ep.ld, kOut, Cfg::BM, CU_TENSOR_MAP_SWIZZLE_NONE);
-  encode_map(&maps.x, g.ep.X, g.ep.n, g.ep.p, g.ep.ld, kOut, Cfg::BM, CU_TENSOR_MAP_SWIZZLE_NONE);
+  encode_map(&maps.g, g.ep.G, g.ep.n, g.ep.p, g.ep.ld, kOut);
+  encode_map(&maps.x, g.ep.X, g.ep.n, g.ep.p, g.ep.ld, kOut);
   gemm_xm_staged<Cfg><<<g.grid, Cfg::THREADS + 128, smem, st>>>(g, maps);
   launched("gemm_xm");
   PCAL_CUDA(cudaGetLastError());

@@ -708,12 +708,22 @@ __global__ void __launch_bounds__(Cfg::THREADS + 256, 1)
 // Column partials are reduced over the tile's 128 rows in a fixed order
 // (warp shuffles, then the four warp rows in order): one partial per
 // (128-row block, column).
+// The staging boxes are {16 rows, 32 columns} with the 128-byte swizzle (box b
+// of rows [16b, 16b+16) at b·4 KB; "row" of the swizzle = the column): the
+// epilogue's lanes (r, q) read rows r(+8·mt) of four columns, and with the
+// columns of one 8-wide fragment chosen as {0, 1, 4, 5} + base (mcat column
+// order perm32, pcal_kernels.cuh xm_slot_of_col) two of them XOR into each
+// 64-byte half of the bank space: 2 wavefronts, the minimum for 256 bytes.
 struct alignas(64) XmMaps {
   CUtensorMap a;  // X  {n, K = pp}, box {16, BK}
-  CUtensorMap b;  // [W|C] interleaved {K = pp, 2pp}, box {16, BN}
-  CUtensorMap g;  // G  {n, p}, box {BM, BN/2} (no swizzle: [column][row])
-  CUtensorMap x;  // X  {n, p}, box {BM, BN/2}
+  CUtensorMap b;  // [W|C] interleaved (perm32 column order) {K = pp, 2pp}, box {16, BN}
+  CUtensorMap g;  // G  {n, p}, box {16, BN/2}, 128-byte swizzle
+  CUtensorMap x;  // X  {n, p}, box {16, BN/2}, 128-byte swizzle
 };
+// output column (within the tile) of fragment (wn, nt) lane column q
+__device__ __forceinline__ int xm_out_col(int wn, int nt, int q) {
+  return wn * 16 + 8 * (nt >> 1) + 2 * (nt & 1) + (q & 1) + 4 * (q >> 1);
+}
 
 template <class Cfg>
 __global__ void __launch_bounds__(Cfg::THREADS + 128, 1)
@@ -764,8 +774,11 @@ __global__ void __launch_bounds__(Cfg::THREADS + 128, 1)
         if (kk == kload) {  // this tile's G / X blocks (after the previous tile's epilogue released them)
           mbar_wait(eempty, (unsigned)(it & 1) ^ 1u);
           mbar_arrive_expect_tx(efull, 2 * BM * BNO * 8);
-          tma_load_2d(Gs, &maps.g, m0, j0, efull);
-          tma_load_2d(Xs, &maps.x, m0, j0, efull);
+#pragma unroll
+          for (int rb = 0; rb < BM / 16; ++rb) {
+            tma_load_2d(Gs + rb * 16 * BNO, &maps.g, m0 + 16 * rb, j0, efull);
+            tma_load_2d(Xs + rb * 16 * BNO, &maps.x, m0 + 16 * rb, j0, efull);
+          }
         }
         mbar_wait(&empty[s], ph ^ 1u);
         mbar_arrive_expect_tx(&full[s], Cfg::STAGE_BYTES);
@@ -816,17 +829,22 @@ __global__ void __launch_bounds__(Cfg::THREADS + 128, 1)
     const int64_t j0 = (int64_t)tc.y * BNO;
     mbar_wait(efull, (unsigned)(it & 1));
     double* rk = red + (it & 1) * (8 * BNO);  // per-tile double buffer: [k rows 0-3 | d rows 0-3]
+    const char* gsb = reinterpret_cast<const char*>(Gs);
+    const char* xsb = reinterpret_cast<const char*>(Xs);
 #pragma unroll
     for (int nt = 0; nt < Cfg::NT; ++nt) {
-      const int jl = wn * (Cfg::WN / 2) + nt * 4 + q;  // output column within the tile
+      const int jl = xm_out_col(wn, nt, q);  // output column within the tile
       const int64_t j = j0 + jl;
       double ks = 0.0, ds = 0.0;
 #pragma unroll
       for (int mt = 0; mt < Cfg::MT; ++mt) {
         const int rl = wm * Cfg::WM + mt * 8 + r;
         const int64_t row = m0 + rl;
-        const double gv = Gs[jl * BM + rl];
-        const double xv = Xs[jl * BM + rl];
+        // swizzled staging: box rl/16, swizzle row jl, chunk ((rl & 15) >> 1) ^ (jl & 7)
+        const int off = (rl >> 4) * (16 * BNO * 8) + jl * 128 +
+                        ((((rl & 15) >> 1) ^ (jl & 7)) << 4) + (rl & 1) * 8;
+        const double gv = *reinterpret_cast<const double*>(gsb + off);
+        const double xv = *reinterpret_cast<const double*>(xsb + off);
         if (row < e.n && j < e.p) {
           const double kkt = gv - acc[mt][nt][0];
           const double pv = (e.p_from_g ? gv : kkt) + e.beta * acc[mt][nt][1];

@@ -41,11 +41,21 @@ __global__ void __launch_bounds__(kStreamThreads) k_colsum3(ColSumArgs a, const 
 //   MOptQR      : M = −GᵀX (not symmetrised)   (epilogue: P = G + XM = G − X·GᵀX)
 // cpart[block] = Σ C² over the block (feasibility).
 // gr: (2·pp) × pp column-major; rows [0,pp) = GᵀX, rows [pp,2pp) = XᵀX.
+// perm32: the column order of gemm_xm_staged (gemm_dmma.cuh xm_out_col): within
+// each 32-column block, output column j sits at slot s = nt·4 + q of the
+// warp half wn, where t = j mod 16 = 8·(nt>>1) + 2·(nt&1) + (q&1) + 4·(q>>1) —
+// the order that makes the staged epilogue's swizzled G / X reads conflict-free.
+__host__ __device__ __forceinline__ int64_t xm_slot_of_col(int64_t j) {
+  const int64_t t = j & 15;
+  const int64_t nt = 2 * ((t >> 3) & 1) + ((t >> 1) & 1), q = 2 * ((t >> 2) & 1) + (t & 1);
+  return (j & ~int64_t(15)) + nt * 4 + q;
+}
+
 enum { MC_PCAL = 0, MC_DA = 1, MC_MOPTQR = 2 };
 __global__ void k_small_pxp(const double* __restrict__ gr, int64_t pp, int64_t p,
                             double* __restrict__ mcat, int64_t ldk, double* __restrict__ cpart,
                             int mode, double beta, double* __restrict__ lam, int lam_init,
-                            const Ctl* ctl, int gx_upper = 0) {
+                            const Ctl* ctl, int gx_upper = 0, int perm32 = 0) {
   if (ctl && ctl->done) return;
   __shared__ double sm[kStreamThreads / 32];
   const int64_t total = p * p;
@@ -74,8 +84,9 @@ __global__ void k_small_pxp(const double* __restrict__ gr, int64_t pp, int64_t p
     } else {
       m = -gr[k + j * ldg];
     }
-    mcat[k + (2 * j) * ldk] = w;
-    mcat[k + (2 * j + 1) * ldk] = m;
+    const int64_t slot = perm32 ? xm_slot_of_col(j) : j;
+    mcat[k + (2 * slot) * ldk] = w;
+    mcat[k + (2 * slot + 1) * ldk] = m;
     acc += c * c;
   }
   const double s = block_sum<kStreamThreads>(acc, sm);

@@ -930,7 +930,8 @@ static void launch_eval(pcal_session* s, int b, int mode, const Ctl* ctl_guard) 
     k_small_pxp<<<s->cp_blocks, kStreamThreads, 0, st>>>(s->gr.p, s->pp, s->p, s->mcat.p, s->pp,
                                                          s->cpart.p, mc, s->beta, s->lam.p,
                                                          lam_mode, ctl_guard,
-                                                         s->sym_gx ? 1 : 0);
+                                                         s->sym_gx ? 1 : 0,
+                                                         s->xm[b].size == CFG_XMS ? 1 : 0);
   }
   launched("k_small_pxp");
   mark(s, 3);
