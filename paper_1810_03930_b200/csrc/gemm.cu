@@ -198,6 +198,26 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   return fn;
 }
 
+void encode_tensor_map(CUtensorMap* m, const void* base, int rank, const int64_t* dims,
+                       const int64_t* pitches_bytes, const int* box) {
+  cuuint64_t d[5], st[4];
+  cuuint32_t bx[5], es[5];
+  for (int i = 0; i < rank; ++i) {
+    d[i] = (cuuint64_t)dims[i];
+    bx[i] = (cuuint32_t)box[i];
+    es[i] = 1u;
+    if (i + 1 < rank) st[i] = (cuuint64_t)pitches_bytes[i];
+  }
+  if (reinterpret_cast<uintptr_t>(base) & 15)
+    throw Error(PCAL_E_STATE, "tensor map: base not 16-byte aligned");
+  const CUresult r = tensor_map_encoder()(
+      m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, (cuuint32_t)rank, const_cast<void*>(base), d, st, bx, es,
+      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw Error(PCAL_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+}
+
 // 2-D FP64 tensor {inner, outer} with row pitch ld (elements), box
 // {box_inner, box_outer} (default {16, ·} with the 128-byte swizzle of the GEMM
 // rings), zero fill outside the extents.

@@ -1,6 +1,8 @@
 // gemm_types.h — host/device shared types of the stream-K DMMA GEMM.
 #pragma once
 
+#include <cuda.h>  // CUtensorMap
+
 #include "common.cuh"
 
 namespace pcal {
@@ -143,5 +145,9 @@ void launch_gemm_tree_local(const GemmPlan& pl, const int2* nodes, int nnodes, i
 void launch_gemm_tree_final(const GemmPlan& pl, const double* buf, const int32_t* cnt,
                             const int2* nodes, int R, int maxn, cudaStream_t st);
 int num_sms(int device);
+// A rank-`rank` FP64 TMA descriptor (no swizzle, zero fill): dims innermost
+// first, pitches (bytes) of dims 1…rank−1, box extents.
+void encode_tensor_map(CUtensorMap* m, const void* base, int rank, const int64_t* dims,
+                       const int64_t* pitches_bytes, const int* box);
 
 }  // namespace pcal

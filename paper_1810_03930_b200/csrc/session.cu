@@ -33,6 +33,7 @@
 #include "host_setup.h"
 #include "operators.cuh"
 #include "pcal_kernels.cuh"
+#include "stencil_tma.cuh"
 
 namespace pcal {
 
@@ -734,6 +735,43 @@ static void launch_colsums(pcal_session* s, const double* fp, int64_t nrb_f, con
 // Gradient of the model at X (pair b): G into P(b), f partials into fpart.
 // 7-point stencil part of the grid models: z-marching kernel when the grid
 // allows it (nx ≤ 128, ny % 8 == 0), else the generic element kernel.
+static void launch_stencil_tma(pcal_session* s, int b, const double* u, bool ks, const Ctl* ctl,
+                               int xp, const double* hlo, const double* hhi, dim3 grid) {
+  constexpr int TY = 8, NS = 4;
+  const auto& m = s->model;
+  const int64_t nx = m.nx, ny = m.ny, nz = s->gz, p = s->p;
+  StencilMaps mp;
+  {
+    const int64_t d4[4] = {nx, ny, nz, p}, pt4[3] = {nx * 8, nx * ny * 8, s->ld * 8};
+    const int bt[4] = {(int)nx, TY, 1, 1}, br[4] = {(int)nx, 1, 1, 1};
+    encode_tensor_map(&mp.x_tile, Xof(s, b), 4, d4, pt4, bt);
+    encode_tensor_map(&mp.x_row, Xof(s, b), 4, d4, pt4, br);
+    const int64_t d3[3] = {nx, ny, nz}, pt3[2] = {nx * 8, nx * ny * 8};
+    const int bu[3] = {(int)nx, TY, 1};
+    encode_tensor_map(&mp.u_tile, u, 3, d3, pt3, bu);
+    const int64_t dh[3] = {nx, ny, p}, pth[2] = {nx * 8, nx * ny * 8};
+    const int bht[3] = {(int)nx, TY, 1}, bhr[3] = {(int)nx, 1, 1};
+    const double* lo = hlo ? hlo : Xof(s, b);  // unused without halos: any valid map
+    const double* hi = hhi ? hhi : Xof(s, b);
+    encode_tensor_map(&mp.lo_tile, lo, 3, dh, pth, bht);
+    encode_tensor_map(&mp.lo_row, lo, 3, dh, pth, bhr);
+    encode_tensor_map(&mp.hi_tile, hi, 3, dh, pth, bht);
+    encode_tensor_map(&mp.hi_row, hi, 3, dh, pth, bhr);
+  }
+  const int smem = (int)(NS * ((TY + 2) * nx + TY * nx) * 8 + 2 * NS * 8);
+  const dim3 block(32 * (TY + 1));
+  const int sh = hlo ? 1 : 0;
+#define PCAL_TMA_ST(KSV, XPV)                                                                     do {                                                                                             auto kern = k_stencil_tma<KSV, XPV, TY, NS>;                                                   PCAL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));      kern<<<grid, block, smem, s->stream>>>(mp, Pof(s, b), (int)nx, (int)ny, (int)nz, s->ld,                                               (int)s->st_zchunk, s->fpart.p, s->pstride_f,                                                   s->bad, ctl, sh, (int)s->st_zpart);                   } while (0)
+  if (ks) {
+    if (xp == 2) PCAL_TMA_ST(true, 2); else PCAL_TMA_ST(true, 4);
+  } else {
+    if (xp == 2) PCAL_TMA_ST(false, 2); else PCAL_TMA_ST(false, 4);
+  }
+#undef PCAL_TMA_ST
+  launched("k_stencil_tma");
+  PCAL_CUDA(cudaGetLastError());
+}
+
 static void launch_stencil(pcal_session* s, int b, const double* u, bool ks, const Ctl* ctl) {
   const auto& m = s->model;
   const int64_t p = s->p;
@@ -764,8 +802,13 @@ static void launch_stencil(pcal_session* s, int b, const double* u, bool ks, con
       Xof(s, b), u, Pof(s, b), (int)m.nx, (int)m.ny, (int)s->gz, s->ld, (int)s->st_zchunk,     \
       s->fpart.p, s->pstride_f, s->bad, ctl, hlo, hhi, (int)s->st_zpart)
     // rows of an even number of points ≤ 64, or a multiple of 4 ≤ 128: the
-    // vectorised full-row kernel (XP consecutive points per lane)
+    // vectorised full-row kernel (XP consecutive points per lane); rows of a
+    // multiple of 16 points (128-byte TMA rows): its TMA-staged form
     const int rxp = m.nx % 2 == 0 && m.nx <= 64 ? 2 : m.nx % 4 == 0 && m.nx <= 128 ? 4 : 0;
+    if (rxp && m.nx % 16 == 0 && !getenv("PCAL_NO_TMA_STENCIL")) {
+      launch_stencil_tma(s, b, u, ks, ctl, rxp, hlo, hhi, grid);
+      return;
+    }
     if (rxp && !getenv("PCAL_NO_ROW_MARCH")) {
       if (ks) {
         if (rxp == 2) PCAL_MARCH_ROW(true, 2); else PCAL_MARCH_ROW(true, 4);

@@ -178,6 +178,31 @@ def test_stencil_march_bitwise(pcal, orc, grid, p):
     assert abs(f - f_ref) <= 1e-12 * abs(f_ref)
 
 
+@pytest.mark.parametrize("kind,grid,p", [("stencil", (64, 16, 6), 3), ("stencil", (128, 8, 5), 2),
+                                         ("stencil", (32, 16, 3), 4), ("kohn_sham", (48, 8, 6), 3),
+                                         ("kohn_sham", (96, 16, 4), 2)])
+def test_tma_stencil_is_bitwise_the_register_march(pcal, orc, kind, grid, p, monkeypatch):
+    """The TMA-staged stencil (k_stencil_tma, rows of a multiple of 16 points)
+    against the register-pipelined full-row march: same G bits, same f to
+    rounding; and both against the oracle's G."""
+    from oracle.oracle import Model, MODEL_STENCIL, MODEL_KOHN_SHAM
+    n = grid[0] * grid[1] * grid[2]
+    v = orc.random_uniform(n, 21) if kind == "stencil" else -orc.random_uniform(n, 21)
+    x = orc.random_normal(n, p, 22)
+    cls = pcal.StencilModel if kind == "stencil" else pcal.KohnShamModel
+    f1, g1 = pcal.evaluate(cls(grid, v, p, 13.0), x)
+    monkeypatch.setenv("PCAL_NO_TMA_STENCIL", "1")
+    f2, g2 = pcal.evaluate(cls(grid, v, p, 13.0), x)
+    assert np.array_equal(g1, g2)
+    assert abs(f1 - f2) <= 1e-13 * abs(f2)
+    mk = MODEL_STENCIL if kind == "stencil" else MODEL_KOHN_SHAM
+    f_ref, g_ref = orc.evaluate(Model(mk, n, p, 13.0, grid=grid, v=v), x)
+    if kind == "stencil":
+        assert np.array_equal(g1, g_ref)
+    else:
+        assert rel(g1, g_ref) <= 1e-14
+
+
 @pytest.mark.parametrize("name,mode", [("qr", "qr"), ("a2i", "a2-i"), ("a2ii", "a2-ii"),
                                        ("a2ii_p1", "a2-ii")])
 def test_initial_point_modes_match_reference(pcal, name, mode):
