@@ -180,8 +180,34 @@ def grids_full() -> None:
         save("long_grids_full.npz", g)
 
 
+def ensemble_grids(k: int = 4) -> None:
+    """Configs 3 and 4: K runs of the port from X0 with one entry moved by one
+    ulp (the spread the end of run must sit in), appended to long_grids_full.npz."""
+    O = Restatement()
+    path = os.path.join(OUT, "long_grids_full.npz")
+    g = dict(np.load(path))
+    for name, kind, grid, p, iters in [("cfg3", MODEL_STENCIL, (64, 64, 64), 256, 300),
+                                       ("cfg4", MODEL_KOHN_SHAM, (48, 48, 48), 512, 200)]:
+        n, v, s = grid_instance(O, kind, grid)
+        x0 = O.initial_point_qr(n, p, 1 ^ INIT_SALT, threads=TH)
+        for q in range(int(g.get(name + "_ens_done", 0)), k):
+            flat = x0.reshape(-1, order="F").copy()
+            e = (q * 2654435761) % flat.size
+            flat[e] = np.nextafter(flat[e], np.inf if q % 2 == 0 else -np.inf)
+            xp = flat.reshape(x0.shape, order="F")
+            t = time.time()
+            rep = O.solve(Model(kind, n, p, s, grid=grid, v=v),
+                          Config(tol_rel_kkt=TINY, max_iter=iters, threads=TH, final_orth=True), xp)
+            print(name, "ens", q, time.time() - t, rep.final_pre, rep.final_post, flush=True)
+            g[f"{name}_ens{q}_final_pre"] = rep.final_pre
+            g[f"{name}_ens{q}_final_post"] = rep.final_post
+            _, g[f"{name}_ens{q}_final_x_rows"] = rows_of(rep.final_x, 1024)
+            g[name + "_ens_done"] = q + 1
+            save("long_grids_full.npz", g)
+
+
 JOBS = {"cfg5s": cfg5_shape, "cfg2": cfg2_full, "grids40": grids40, "gridsfull": grids_full,
-        "ens2": ensemble2}
+        "ens2": ensemble2, "ensgrids": ensemble_grids}
 
 if __name__ == "__main__":
     for job in sys.argv[1:]:
