@@ -121,6 +121,7 @@ def dist_setup(ngpus: int):
     if world > 1:
         import torch
         import torch.distributed as dist
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # the log shows the real rank count
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return rank, world, local
@@ -279,6 +280,38 @@ def run_reference_arm(args):
     return 0
 
 
+def run_emulated(args) -> int:
+    """`--gpus N --emulate`: the row-sharded algorithm with N ranks emulated on
+    one GPU (host threads, loopback collectives) against the same
+    algorithm with one rank: the reports must be bitwise identical
+    (same_numerics, report_io.cpp:259-283).  A correctness check of the N-GPU
+    path on a one-GPU box, not a timing."""
+    import paper_1810_03930_b200 as P
+    from paper_1810_03930_b200 import report_io
+    from paper_1810_03930_b200.problems import make_instance
+    inst = make_instance(args.config, P, threads=os.cpu_count() or 8)
+    x0 = P.initial_point(inst.n, inst.p, inst.seed ^ INIT_SALT)
+    model = inst.model(P)
+    cfg = P.SolverConfig(tol_rel_kkt=TINY, max_iter=args.steps)
+    t0 = time.perf_counter()
+    r1 = P.solve_emulated(model, cfg, x0, 1)
+    t1 = time.perf_counter()
+    rn = P.solve_emulated(model, cfg, x0, args.gpus)
+    t2 = time.perf_counter()
+    rows = [P.partition(model, args.gpus, r)[1] for r in range(args.gpus)]
+    line = {"mode": "emulated", "config": {"workload": WORKLOADS[args.config], "n": inst.n,
+                                           "p": inst.p},
+            "n_ranks": args.gpus, "iterations": args.steps,
+            "same_numerics": bool(report_io.same_numerics(r1, rn)),
+            "rows_per_rank": rows,
+            "device_bytes_per_rank_nxp": [4 * 8 * r * inst.p for r in rows],
+            "wall_s": {"ranks_1": round(t1 - t0, 2), f"ranks_{args.gpus}": round(t2 - t1, 2)},
+            "final_post_f": [r1.final_post_orth.fval if r1.final_post_orth else None,
+                             rn.final_post_orth.fval if rn.final_post_orth else None]}
+    print(json.dumps(line), flush=True)
+    return 0 if line["same_numerics"] else 1
+
+
 def spawn_ranks(args) -> int:
     """`bench.py --gpus N` without torchrun: launch N ranks (one per GPU) of this
     same command through torch.distributed.run and return its exit code."""
@@ -306,10 +339,16 @@ def main():
     ap.add_argument("--e2e-calls", type=int, default=3)
     ap.add_argument("--sharded", action="store_true",
                     help="use the NCCL row-sharded path even on one GPU (testing)")
+    ap.add_argument("--emulate", action="store_true",
+                    help="with --gpus N: N ranks emulated on one GPU, same_numerics vs 1 rank")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
+    if args.emulate:
+        return run_emulated(args)
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # NCCL's own log shows the rank count the communicator really has
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
         return spawn_ranks(args)
 
     import torch

@@ -229,6 +229,147 @@ __global__ void k_update(const double* __restrict__ x, const double* __restrict_
   }
 }
 
+// ---- normalised step without a separate normalisation pass ----------------
+// pcal_step (solver.cpp:278-300) normalises z_j = x_j − (1/η)·gl_j by its
+// norm, which the reference takes from a second pass over z.  Here the
+// stepsize kernel, which reads X and P anyway, also sums per column
+//   a_j = Σ x²,  b_j = Σ x·gl,  c_j = Σ gl²     (gl = p − d_j·x),
+// so ‖z_j‖² = a_j + (1/η)·((1/η)·c_j − 2·b_j) is known before Z is formed and
+// k_update_norm writes X_{k+1} = z·(1/‖z_j‖) in the same pass that forms z
+// (16·n·p fewer bytes per iteration).  With the PCAL multiplier formula gl_j
+// is orthogonal to x_j up to ‖x_j‖² − 1, so the three terms add without
+// cancellation; a column whose expansion would cancel (terms / result > 1e6)
+// or that is near the degenerate threshold is flagged and takes the
+// reference's exact two-pass rule in k_normalize (fb mode).  The normalising
+// factor differs from the two-pass one by rounding only (the parity
+// tolerances of DESIGN.md §5).
+
+// Per (row chunk c, column j): colpart[(c·p + j)·6 + {ss, sy, yy, a, b, cc}].
+__global__ void k_bb_cols(const double* __restrict__ x, const double* __restrict__ pg,
+                          const double* __restrict__ xp, const double* __restrict__ pgp,
+                          const double* __restrict__ d, const double* __restrict__ dp, int64_t n,
+                          int64_t ld, int64_t p, int64_t chunk, double* __restrict__ colpart,
+                          const Ctl* ctl) {
+  if (ctl->done) return;
+  __shared__ double sm[kStreamThreads / 32];
+  const bool bb = ctl->iter != ctl->iter_base && ctl->have_prev;
+  const int64_t j = blockIdx.y;
+  const int64_t r0 = (int64_t)blockIdx.x * chunk;
+  const int64_t r1 = min(n, r0 + chunk);
+  const double dj = d[j], dpj = bb ? dp[j] : 0.0;
+  const double* xj = x + j * ld;
+  const double* pj = pg + j * ld;
+  double ss = 0.0, sy = 0.0, yy = 0.0, a = 0.0, b = 0.0, c = 0.0;
+  if (bb) {
+    const double* xpj = xp + j * ld;
+    const double* ppj = pgp + j * ld;
+    for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+      const double xv = xj[i], xpv = xpj[i];
+      const double gl = pj[i] - dj * xv;
+      const double sv = xv - xpv;
+      const double yv = gl - (ppj[i] - dpj * xpv);
+      ss += sv * sv;
+      sy += sv * yv;
+      yy += yv * yv;
+      a += xv * xv;
+      b += xv * gl;
+      c += gl * gl;
+    }
+  } else {
+    for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+      const double xv = xj[i];
+      const double gl = pj[i] - dj * xv;
+      a += xv * xv;
+      b += xv * gl;
+      c += gl * gl;
+    }
+  }
+  double v[6] = {ss, sy, yy, a, b, c};
+#pragma unroll
+  for (int q = 0; q < 6; ++q) {
+    const double t = block_sum<kStreamThreads>(v[q], sm);
+    if (threadIdx.x == 0) colpart[((int64_t)blockIdx.x * p + j) * 6 + q] = t;
+  }
+}
+
+// Sum of the (chunk, column) stepsize partials in a fixed order → the
+// k_eta input layout (one "block" slot holding the totals).
+__global__ void __launch_bounds__(kStreamThreads) k_bb_cols_sum(const double* __restrict__ colpart,
+                                                                int64_t nslots,
+                                                                double* __restrict__ part,
+                                                                const Ctl* ctl) {
+  if (ctl->done) return;
+  __shared__ double sm[kStreamThreads / 32];
+  double v[3] = {0.0, 0.0, 0.0};
+  for (int64_t i = threadIdx.x; i < nslots; i += blockDim.x)
+#pragma unroll
+    for (int q = 0; q < 3; ++q) v[q] += colpart[i * 6 + q];
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    const double t = block_sum<kStreamThreads>(v[q], sm);
+    if (threadIdx.x == 0) part[q] = t;
+  }
+}
+
+// 1/‖z_j‖ from the expansion (after k_eta), and the fallback flag.
+__global__ void k_colscale(const double* __restrict__ colpart, int64_t nchunks, int64_t p,
+                           double* __restrict__ inv, int32_t* __restrict__ fb, const Ctl* ctl) {
+  if (ctl->done) return;
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= p) return;
+  double a = 0.0, b = 0.0, c = 0.0;
+  for (int64_t k = 0; k < nchunks; ++k) {
+    const double* q = colpart + (k * p + j) * 6;
+    a += q[3];
+    b += q[4];
+    c += q[5];
+  }
+  const double ie = 1.0 / ctl->eta;
+  const double nz2 = a + ie * (ie * c - 2.0 * b);
+  const double mag = a + ie * (ie * c + 2.0 * fabs(b));
+  const bool exact = !(nz2 > 1e-20) || mag > 1e6 * nz2 || !isfinite(nz2);
+  fb[j] = exact ? 1 : 0;
+  inv[j] = exact ? 1.0 : 1.0 / sqrt(nz2);
+}
+
+// X_{k+1} = (x − (1/η)·gl)·inv_j in one pass (flagged columns: z unscaled for
+// k_normalize's exact rule); npart as k_update (the exact ‖z‖² partials).
+__global__ void k_update_norm(const double* __restrict__ x, const double* __restrict__ pg,
+                              const double* __restrict__ d, double* __restrict__ z, int64_t n,
+                              int64_t ld, int64_t p, int64_t chunk, double* __restrict__ npart,
+                              const double* __restrict__ inv, const int32_t* __restrict__ fb,
+                              Ctl* ctl) {
+  if (ctl->done) return;
+  __shared__ double sm[kStreamThreads / 32];
+  const int64_t j = blockIdx.y;
+  const int64_t r0 = (int64_t)blockIdx.x * chunk;
+  const int64_t r1 = min(n, r0 + chunk);
+  const double inv_eta = 1.0 / ctl->eta;
+  const double dj = d[j];
+  const bool exact = fb[j] != 0;
+  const double sc = inv[j];
+  const double* xj = x + j * ld;
+  const double* pj = pg + j * ld;
+  double* zj = z + j * ld;
+  double acc = 0.0;
+  bool bad = false;
+  for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+    const double xv = xj[i];
+    const double gl = pj[i] - dj * xv;
+    const double v = xv - inv_eta * gl;
+    acc += v * v;
+    const double w = exact ? v : v * sc;
+    zj[i] = w;
+    bad |= !isfinite(w);
+  }
+  const double s = block_sum<kStreamThreads>(acc, sm);
+  if (threadIdx.x == 0) npart[blockIdx.x * p + j] = s;
+  if (!exact && __syncthreads_or(bad) && threadIdx.x == 0) {
+    ctl->step_bad = 1;
+    ctl->done = 2;
+  }
+}
+
 // sharded: local column sums of the z² / x² chunk partials → nrm[0:p], nrm[p:2p]
 __global__ void k_norm_reduce(const double* __restrict__ npart, const double* __restrict__ xpart,
                               int64_t nchunks, int64_t p, double* __restrict__ nrm,
@@ -367,8 +508,10 @@ __device__ __forceinline__ bool scale_range(double* __restrict__ zj, int64_t r0,
 __global__ void k_normalize(const double* __restrict__ x, double* __restrict__ z, int64_t n,
                             int64_t ld, int64_t p, int64_t chunk, int64_t nchunks,
                             const double* __restrict__ npart, const double* __restrict__ nrm,
-                            int64_t row0, int64_t n_glob, int plain, Ctl* ctl) {
+                            int64_t row0, int64_t n_glob, int plain, Ctl* ctl,
+                            const int32_t* __restrict__ only_fb = nullptr) {
   if (ctl->done) return;
+  if (only_fb && !only_fb[blockIdx.y]) return;  // k_update_norm already normalised it
   if (plain) {  // plam_step (solver.cpp:253-262): no normalisation, only the finiteness check
     const int64_t j = blockIdx.y;
     const int64_t r0 = (int64_t)blockIdx.x * chunk;

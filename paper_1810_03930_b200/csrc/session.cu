@@ -555,6 +555,8 @@ struct pcal_session {
   // iteration state
   pcal::DevBuf pair[2];
   pcal::DevBuf gr, mcat, fpart, kpart, dpart, cpart, bbpart, npart, post;
+  pcal::DevBuf colpart, sinv;  // fused normalisation: (chunk, column) sums; 1/‖z_j‖
+  int32_t* sfb = nullptr;      // per column: take the exact two-pass normalisation
   pcal::DevBuf orth_b, orth_l, orth_t, orth_f2;
   int32_t* bad = nullptr;
   int32_t* orth_status = nullptr;
@@ -1142,6 +1144,31 @@ static void launch_iteration(pcal_session* s, int b) {
                                                s->chunk_rows, s->nch, s->cc.p, s->nrm.p, s->row0,
                                                s->n_glob, plain, s->ctl);
     launched("k_normalize");
+  } else if (!s->comm && !plain && !getenv("PCAL_TWO_PASS_NORMALIZE")) {
+    // normalised step in one pass over Z (pcal_kernels.cuh k_bb_cols): the
+    // stepsize kernel also sums x², x·gl, gl² per column, so ‖z_j‖ is known
+    // before z is formed; flagged columns fall back to the exact two-pass rule
+    dim3 gu((unsigned)s->up_nchunks, (unsigned)s->p);
+    k_bb_cols<<<gu, kStreamThreads, 0, st>>>(Xof(s, b), Pof(s, b), Xof(s, nb), Pof(s, nb),
+                                             Dvec(s, b), Dvec(s, nb), s->n, s->ld, s->p,
+                                             s->up_chunk, s->colpart.p, s->ctl);
+    launched("k_bb_cols");
+    k_bb_cols_sum<<<1, kStreamThreads, 0, st>>>(s->colpart.p, s->up_nchunks * s->p,
+                                                s->bbpart.p, s->ctl);
+    launched("k_bb_cols_sum");
+    k_eta<<<1, kStreamThreads, 0, st>>>(s->ctl, s->bbpart.p, 1);
+    launched("k_eta");
+    k_colscale<<<(unsigned)ceil_div(s->p, 128), 128, 0, st>>>(s->colpart.p, s->up_nchunks, s->p,
+                                                              s->sinv.p, s->sfb, s->ctl);
+    launched("k_colscale");
+    k_update_norm<<<gu, kStreamThreads, 0, st>>>(Xof(s, b), Pof(s, b), Dvec(s, b), Xof(s, nb),
+                                                 s->n, s->ld, s->p, s->up_chunk, s->npart.p,
+                                                 s->sinv.p, s->sfb, s->ctl);
+    launched("k_update_norm");
+    k_normalize<<<gu, kStreamThreads, 0, st>>>(Xof(s, b), Xof(s, nb), s->n, s->ld, s->p,
+                                               s->up_chunk, s->up_nchunks, s->npart.p, nullptr,
+                                               s->row0, s->n_glob, plain, s->ctl, s->sfb);
+    launched("k_normalize");
   } else {
     k_bb_partials<<<s->bb_blocks, kStreamThreads, 0, st>>>(Xof(s, b), Pof(s, b), Xof(s, nb),
                                                            Pof(s, nb), Dvec(s, b), Dvec(s, nb),
@@ -1514,6 +1541,10 @@ static void alloc_state(pcal_session* s) {
   s->up_chunk = std::min<int64_t>(s->up_chunk, round_up(n, 256));
   if (s->repro) s->up_chunk = s->chunk_rows;  // norm partials per row chunk
   s->up_nchunks = ceil_div(n, s->up_chunk);
+  s->colpart.alloc((size_t)s->up_nchunks * p * 6);
+  s->sinv.alloc((size_t)s->pp);
+  PCAL_CUDA(cudaMalloc(&s->sfb, sizeof(int32_t) * s->pp));
+  PCAL_CUDA(cudaMemsetAsync(s->sfb, 0, sizeof(int32_t) * s->pp, st));
   if (s->repro) {
     const int R = s->comm->size;
     s->cc.alloc((size_t)s->nch_max * 3 * p + 2);
@@ -1710,6 +1741,7 @@ pcal_session::~pcal_session() {
   for (auto& e : pev)
     if (e) cudaEventDestroy(e);
   if (bad) cudaFree(bad);
+  if (sfb) cudaFree(sfb);
   if (rank_nch_d) cudaFree(rank_nch_d);
   if (ctl) cudaFree(ctl);
   if (h_ctl) cudaFreeHost(h_ctl);
