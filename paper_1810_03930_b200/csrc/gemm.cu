@@ -40,6 +40,8 @@ CfgInfo cfg_info(int size) {
 
 void GemmPlan::release() {
   if (d_tiles) cudaFree(d_tiles);
+  if (d_tri) cudaFree(d_tri);
+  d_tri = nullptr;
   if (d_split) cudaFree(d_split);
   if (d_tasks) cudaFree(d_tasks);
   if (ws) cudaFree(ws);
@@ -154,6 +156,22 @@ void plan_gemm(GemmPlan& pl, int device, int size, int amode, int epi, int64_t M
   if (chunk_partials) qmax = std::max(qmax, qmax_min);
   PCAL_CUDA(cudaMalloc(&pl.d_tiles, sizeof(int2) * ntiles));
   PCAL_CUDA(cudaMemcpy(pl.d_tiles, tiles.data(), sizeof(int2) * ntiles, cudaMemcpyHostToDevice));
+  // diagonal tiles of the upper-triangle-only blocks: triangular work (mma_stage_tri)
+  std::vector<uint8_t> tri(ntiles, 0);
+  bool any_tri = false;
+  if (sym_row0 >= 0 && size == CFG_BIG && amode == A_KCONTIG && epi == EPI_STORE &&
+      ci.BM == ci.BN && !getenv("PCAL_NO_TRI_TILES")) {
+    for (int t = 0; t < ntiles; ++t) {
+      const int64_t r0 = (int64_t)tiles[t].x * ci.BM, c0 = (int64_t)tiles[t].y * ci.BN;
+      const bool d = r0 >= sym_row0 ? (r0 - sym_row0 == c0) : (sym_first && r0 == c0);
+      tri[t] = d ? 1 : 0;
+      any_tri |= d;
+    }
+  }
+  if (any_tri) {
+    PCAL_CUDA(cudaMalloc(&pl.d_tri, ntiles));
+    PCAL_CUDA(cudaMemcpy(pl.d_tri, tri.data(), ntiles, cudaMemcpyHostToDevice));
+  }
   PCAL_CUDA(cudaMalloc(&pl.d_split, sizeof(int32_t) * ntiles));
   PCAL_CUDA(cudaMemcpy(pl.d_split, split.data(), sizeof(int32_t) * ntiles, cudaMemcpyHostToDevice));
   pl.ntasks = (int)tasks.size();
@@ -170,6 +188,7 @@ void plan_gemm(GemmPlan& pl, int device, int size, int amode, int epi, int64_t M
   g.N = N;
   g.K = K;
   g.tiles = pl.d_tiles;
+  g.tile_tri = pl.d_tri;
   g.split_slot = pl.d_split;
   g.ntiles = ntiles;
   g.ki = ki;

@@ -146,6 +146,47 @@ __device__ __forceinline__ void mma_stage(const char* As, const char* Bs, int wm
   }
 }
 
+// ---- diagonal tiles of a symmetric Gram: only the upper triangle -------------
+// A 128 × 128 tile on the diagonal of a block whose upper triangle is all that
+// is needed (XᵀX; GᵀX of a symmetric operator) holds 136 of its 256 8×8
+// sub-blocks at or above the diagonal.  Warp w computes sub-block rows w and
+// 15 − w from the diagonal to the right edge — 16 − w and w + 1 sub-blocks,
+// 17 DMMAs per k-step for every warp (warps w and w + 4 share an SM
+// sub-partition: 34 each, balanced) instead of 32: the tile costs 136/256 of a
+// full one.  Sub-block (R, C) accumulates in acc[c/4 (+4 for row 15 − w)][c % 4],
+// the registers of the full tile, and is stored in the full tile's fragment
+// layout (frag_index of its owner in the full schedule), so partial tiles go
+// through the same fixup / tree reductions.  Same k order as mma_stage: the
+// computed elements are bitwise those of the full tile.
+template <class Cfg>
+__device__ __forceinline__ void mma_stage_tri(const char* As, const char* Bs, int warp, int lane,
+                                              double (&acc)[Cfg::MT][Cfg::NT][2]) {
+  static_assert(Cfg::AMODE == A_KCONTIG && Cfg::BM == 128 && Cfg::BN == 128 && Cfg::MT == 8 &&
+                    Cfg::NT == 4 && Cfg::WARPS == 8,
+                "triangular tiles: the 128 × 128 K-contiguous Gram configuration");
+  const int r = lane >> 2, q = lane & 3;
+  const int kq = kq_of(q);
+  const int R1 = warp, R2 = 15 - warp;
+#pragma unroll
+  for (int st = 0; st < Cfg::BK / 4; ++st) {
+    const int box = st >> 2;
+    const int kl = kq ^ ((st & 1) | ((st & 2) << 1));
+    const int sw = (kl & 1) * 8 + (((kl >> 1) ^ r) << 4);
+    const char* ax = As + box * (Cfg::BM * 128) + sw;
+    const char* bx = Bs + box * (Cfg::BN * 128) + sw;
+    const double a1 = *reinterpret_cast<const double*>(ax + (R1 * 8 + r) * 128);
+    const double a2 = *reinterpret_cast<const double*>(ax + (R2 * 8 + r) * 128);
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+      if (c >= R1) {  // warp-uniform
+        const double b = *reinterpret_cast<const double*>(bx + (c * 8 + r) * 128);
+        dmma_8x8x4(acc[c >> 2][c & 3][0], acc[c >> 2][c & 3][1], a1, b);
+        if (c >= R2) dmma_8x8x4(acc[4 + (c >> 2)][c & 3][0], acc[4 + (c >> 2)][c & 3][1], a2, b);
+      }
+    }
+  }
+}
+
 // ---- epilogues ---------------------------------------------------------------
 // Fragment (mt, nt, e) of lane `lane` in warp (wm, wn) is output element
 //   row = m0 + wm·WM + mt·8 + lane/4,   col = n0 + wn·WN + nt·8 + 2·(lane%4) + e.
@@ -361,6 +402,37 @@ __device__ __forceinline__ char* smem_ring(char* raw) {
   return raw + ((1024u - (smem_u32(raw) & 1023u)) & 1023u);
 }
 
+// Store the upper-triangle sub-blocks of a triangular tile (mma_stage_tri):
+// straight into C (whole tile) or into the partial slot w in the full tile's
+// fragment layout.
+template <class Cfg>
+__device__ __forceinline__ void flush_tri(const GemmArgs& g, int2 tc, bool whole, double* w,
+                                          int warp, int lane,
+                                          const double (&acc)[Cfg::MT][Cfg::NT][2]) {
+  const int r = lane >> 2, q = lane & 3;
+  const EpiParams& e = g.ep;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int R = h == 0 ? warp : 15 - warp;
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+      if (c < R) continue;
+#pragma unroll
+      for (int x = 0; x < 2; ++x) {
+        const double v = acc[4 * h + (c >> 2)][c & 3][x];
+        if (whole) {
+          const int64_t row = (int64_t)tc.x * Cfg::BM + R * 8 + r;
+          const int64_t col = (int64_t)tc.y * Cfg::BN + c * 8 + 2 * q + x;
+          if (row < e.m_store && col < e.n_store) e.C[row + col * e.ldc] = v;
+        } else {
+          const int owner = (R >> 3) * Cfg::WARPS_N + (c >> 2);  // full-schedule warp of (R, c)
+          w[frag_index<Cfg>(owner, R & 7, c & 3, x, lane)] = v;
+        }
+      }
+    }
+  }
+}
+
 // ---- main kernel ----------------------------------------------------------------
 // Warp-specialized: warps [0, WARPS) consume (LDS + DMMA + epilogue), warp
 // WARPS produces (cp.async ring, one mbarrier pair per stage); the rest of
@@ -423,10 +495,22 @@ __global__ void __launch_bounds__(Cfg::THREADS + 128, 1)
   bool tile_start = kk == 0;  // this CTA's current tile segment began at the tile's k = 0
   int stage = 0;
   unsigned phase = 0;
+  constexpr bool kTriCfg = Cfg::AMODE == A_KCONTIG && EPI == EPI_STORE && Cfg::BM == 128 &&
+                           Cfg::BN == 128 && Cfg::WARPS == 8;
+  bool tri = kTriCfg && g.tile_tri && g.tile_tri[t];
   for (int64_t u = u0; u < u1; ++u) {
     mbar_wait(&full[stage], phase);
-    mma_stage<Cfg>(As + stage * (Cfg::A_STAGE * 8), Bs + stage * (Cfg::B_STAGE * 8), wm, wn, lane,
-                   acc);
+    if constexpr (kTriCfg) {
+      if (tri)
+        mma_stage_tri<Cfg>(As + stage * (Cfg::A_STAGE * 8), Bs + stage * (Cfg::B_STAGE * 8), warp,
+                           lane, acc);
+      else
+        mma_stage<Cfg>(As + stage * (Cfg::A_STAGE * 8), Bs + stage * (Cfg::B_STAGE * 8), wm, wn,
+                       lane, acc);
+    } else {
+      mma_stage<Cfg>(As + stage * (Cfg::A_STAGE * 8), Bs + stage * (Cfg::B_STAGE * 8), wm, wn,
+                     lane, acc);
+    }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[stage]);
     if (++stage == Cfg::STAGES) {
@@ -439,7 +523,14 @@ __global__ void __launch_bounds__(Cfg::THREADS + 128, 1)
     if (tile_end || seg_end || u == u1 - 1) {
       const int2 tc = g.tiles[t];
       const bool whole = tile_start && tile_end && !g.force_ws && S <= 1;
-      if (whole) {
+      if (kTriCfg && tri) {
+        flush_tri<Cfg>(g, tc, whole, whole ? nullptr
+                       : g.ws + ((size_t)g.split_slot[t] * g.qmax +
+                                 (S ? cur_seg : cta - cta_of_unit((int64_t)t * g.ki, g.units,
+                                                                  g.grid))) *
+                                    (size_t)(Cfg::BM * Cfg::BN),
+                       warp, lane, acc);
+      } else if (whole) {
         epilogue<Cfg, EPI>(g, tc.x, tc.y, wm, wn, lane, acc);
       } else {
         const int slot = g.split_slot[t];
@@ -463,6 +554,7 @@ __global__ void __launch_bounds__(Cfg::THREADS + 128, 1)
       ++t;
       cur_seg = 0;
       seg_stop = S > 1 ? g.ki / S : g.ki;
+      if constexpr (kTriCfg) tri = g.tile_tri && u + 1 < u1 && g.tile_tri[t];
     } else {
       ++kk;
       if (seg_end) {

@@ -55,6 +55,7 @@ struct GemmArgs {
   int32_t force_ws;     // chunk-partial plans: every CTA stores its partial (no epilogue)
   int32_t segs;         // > 0: segmented schedule, S fixed K segments per tile (see below)
   int32_t a_stream;     // A is read exactly once (dense gradient): L2 evict-first loads
+  const uint8_t* tile_tri;  // per tile: 1 = diagonal tile of an upper-triangle-only block
 };
 
 struct FixupTask {   // one split tile
@@ -106,6 +107,7 @@ struct GemmPlan {
   int size = CFG_BIG, amode = A_MCONTIG, epi = EPI_STORE;
   GemmArgs args{};
   int2* d_tiles = nullptr;
+  uint8_t* d_tri = nullptr;   // triangular (diagonal) tiles of symmetric Grams
   int32_t* d_split = nullptr;
   FixupTask* d_tasks = nullptr;
   int ntasks = 0;

@@ -245,50 +245,60 @@ __global__ void k_update(const double* __restrict__ x, const double* __restrict_
 // tolerances of DESIGN.md §5).
 
 // Per (row chunk c, column j): colpart[(c·p + j)·6 + {ss, sy, yy, a, b, cc}].
-__global__ void k_bb_cols(const double* __restrict__ x, const double* __restrict__ pg,
-                          const double* __restrict__ xp, const double* __restrict__ pgp,
-                          const double* __restrict__ d, const double* __restrict__ dp, int64_t n,
-                          int64_t ld, int64_t p, int64_t chunk, double* __restrict__ colpart,
-                          const Ctl* ctl) {
+// 16-byte vector loads (chunks are multiples of 256 rows); the six block sums
+// share one shared-memory round (fixed order: lanes, then warps).
+__global__ void __launch_bounds__(kStreamThreads)
+    k_bb_cols(const double* __restrict__ x, const double* __restrict__ pg,
+              const double* __restrict__ xp, const double* __restrict__ pgp,
+              const double* __restrict__ d, const double* __restrict__ dp, int64_t n, int64_t ld,
+              int64_t p, int64_t chunk, double* __restrict__ colpart, const Ctl* ctl) {
   if (ctl->done) return;
-  __shared__ double sm[kStreamThreads / 32];
+  __shared__ double sm[6][kStreamThreads / 32];
   const bool bb = ctl->iter != ctl->iter_base && ctl->have_prev;
   const int64_t j = blockIdx.y;
   const int64_t r0 = (int64_t)blockIdx.x * chunk;
   const int64_t r1 = min(n, r0 + chunk);
   const double dj = d[j], dpj = bb ? dp[j] : 0.0;
-  const double* xj = x + j * ld;
-  const double* pj = pg + j * ld;
-  double ss = 0.0, sy = 0.0, yy = 0.0, a = 0.0, b = 0.0, c = 0.0;
-  if (bb) {
-    const double* xpj = xp + j * ld;
-    const double* ppj = pgp + j * ld;
-    for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
-      const double xv = xj[i], xpv = xpj[i];
-      const double gl = pj[i] - dj * xv;
-      const double sv = xv - xpv;
-      const double yv = gl - (ppj[i] - dpj * xpv);
-      ss += sv * sv;
-      sy += sv * yv;
-      yy += yv * yv;
-      a += xv * xv;
-      b += xv * gl;
-      c += gl * gl;
-    }
-  } else {
-    for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
-      const double xv = xj[i];
-      const double gl = pj[i] - dj * xv;
-      a += xv * xv;
-      b += xv * gl;
-      c += gl * gl;
+  const double2* xj = reinterpret_cast<const double2*>(x + j * ld);
+  const double2* pj = reinterpret_cast<const double2*>(pg + j * ld);
+  const double2* xpj = reinterpret_cast<const double2*>(xp + j * ld);
+  const double2* ppj = reinterpret_cast<const double2*>(pgp + j * ld);
+  double v[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};  // ss, sy, yy, a, b, c
+  // rows beyond n are zero padding (x = p = 0): they add nothing
+  const int64_t h0 = r0 / 2, h1 = (r1 + 1) / 2;  // an odd n ends on a zero padding row
+  for (int64_t h = h0 + threadIdx.x; h < h1; h += blockDim.x) {
+    const double2 xv = xj[h], pv = pj[h];
+    const double g0 = pv.x - dj * xv.x, g1 = pv.y - dj * xv.y;
+    v[3] += xv.x * xv.x;
+    v[4] += xv.x * g0;
+    v[5] += g0 * g0;
+    v[3] += xv.y * xv.y;
+    v[4] += xv.y * g1;
+    v[5] += g1 * g1;
+    if (bb) {
+      const double2 xpv = xpj[h], ppv = ppj[h];
+      const double s0 = xv.x - xpv.x, y0 = g0 - (ppv.x - dpj * xpv.x);
+      const double s1 = xv.y - xpv.y, y1 = g1 - (ppv.y - dpj * xpv.y);
+      v[0] += s0 * s0;
+      v[1] += s0 * y0;
+      v[2] += y0 * y0;
+      v[0] += s1 * s1;
+      v[1] += s1 * y1;
+      v[2] += y1 * y1;
     }
   }
-  double v[6] = {ss, sy, yy, a, b, c};
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
 #pragma unroll
   for (int q = 0; q < 6; ++q) {
-    const double t = block_sum<kStreamThreads>(v[q], sm);
-    if (threadIdx.x == 0) colpart[((int64_t)blockIdx.x * p + j) * 6 + q] = t;
+    const double t = warp_sum(v[q]);
+    if (l == 0) sm[q][w] = t;
+  }
+  __syncthreads();
+  if (threadIdx.x < 6) {
+    double t = 0.0;
+#pragma unroll
+    for (int i = 0; i < kStreamThreads / 32; ++i) t += sm[threadIdx.x][i];
+    colpart[((int64_t)blockIdx.x * p + j) * 6 + threadIdx.x] = t;
   }
 }
 
@@ -334,11 +344,11 @@ __global__ void k_colscale(const double* __restrict__ colpart, int64_t nchunks, 
 
 // X_{k+1} = (x − (1/η)·gl)·inv_j in one pass (flagged columns: z unscaled for
 // k_normalize's exact rule); npart as k_update (the exact ‖z‖² partials).
-__global__ void k_update_norm(const double* __restrict__ x, const double* __restrict__ pg,
-                              const double* __restrict__ d, double* __restrict__ z, int64_t n,
-                              int64_t ld, int64_t p, int64_t chunk, double* __restrict__ npart,
-                              const double* __restrict__ inv, const int32_t* __restrict__ fb,
-                              Ctl* ctl) {
+__global__ void __launch_bounds__(kStreamThreads)
+    k_update_norm(const double* __restrict__ x, const double* __restrict__ pg,
+                  const double* __restrict__ d, double* __restrict__ z, int64_t n, int64_t ld,
+                  int64_t p, int64_t chunk, double* __restrict__ npart,
+                  const double* __restrict__ inv, const int32_t* __restrict__ fb, Ctl* ctl) {
   if (ctl->done) return;
   __shared__ double sm[kStreamThreads / 32];
   const int64_t j = blockIdx.y;
@@ -347,20 +357,22 @@ __global__ void k_update_norm(const double* __restrict__ x, const double* __rest
   const double inv_eta = 1.0 / ctl->eta;
   const double dj = d[j];
   const bool exact = fb[j] != 0;
-  const double sc = inv[j];
-  const double* xj = x + j * ld;
-  const double* pj = pg + j * ld;
-  double* zj = z + j * ld;
+  const double sc = exact ? 1.0 : inv[j];  // v·1 = v: flagged columns stay z
+  const double2* xj = reinterpret_cast<const double2*>(x + j * ld);
+  const double2* pj = reinterpret_cast<const double2*>(pg + j * ld);
+  double2* zj = reinterpret_cast<double2*>(z + j * ld);
   double acc = 0.0;
   bool bad = false;
-  for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
-    const double xv = xj[i];
-    const double gl = pj[i] - dj * xv;
-    const double v = xv - inv_eta * gl;
-    acc += v * v;
-    const double w = exact ? v : v * sc;
-    zj[i] = w;
-    bad |= !isfinite(w);
+  const int64_t h0 = r0 / 2, h1 = (r1 + 1) / 2;  // an odd n ends on a zero padding row
+  for (int64_t h = h0 + threadIdx.x; h < h1; h += blockDim.x) {
+    const double2 xv = xj[h], pv = pj[h];
+    const double v0 = xv.x - inv_eta * (pv.x - dj * xv.x);
+    const double v1 = xv.y - inv_eta * (pv.y - dj * xv.y);
+    acc += v0 * v0;
+    acc += v1 * v1;
+    const double w0 = v0 * sc, w1 = v1 * sc;
+    zj[h] = make_double2(w0, w1);
+    bad |= !isfinite(w0) || !isfinite(w1);
   }
   const double s = block_sum<kStreamThreads>(acc, sm);
   if (threadIdx.x == 0) npart[blockIdx.x * p + j] = s;

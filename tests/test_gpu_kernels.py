@@ -203,6 +203,38 @@ def test_tma_stencil_is_bitwise_the_register_march(pcal, orc, kind, grid, p, mon
         assert rel(g1, g_ref) <= 1e-14
 
 
+@pytest.mark.parametrize("case", ["stencil", "dense", "sharded", "gram"])
+def test_triangular_diagonal_tiles_are_bitwise(pcal, orc, case, monkeypatch):
+    """The Gram's diagonal tiles compute only their upper-triangle sub-blocks
+    (mma_stage_tri, 17 instead of 32 DMMAs per warp and k-step): every value
+    that is used is bitwise the full tile's, so whole solves — the stencil's
+    symmetric GᵀX + XᵀX, the dense XᵀX, the sharded chunk-partial Gram — and
+    pcal_gram are identical with and without it (PCAL_NO_TRI_TILES=1)."""
+    from paper_1810_03930_b200 import report_io
+    if case == "gram":
+        x = orc.random_normal(5000, 300, 31)
+        g1 = pcal.gram(x)
+        monkeypatch.setenv("PCAL_NO_TRI_TILES", "1")
+        g2 = pcal.gram(x)
+        assert np.array_equal(g1, g2)
+        return
+    if case == "dense":
+        n, p = 2000, 256
+        m = pcal.QuadraticModel(pcal.gen_dense_operator(n, 5), p, 90.0)
+    else:
+        grid, p = (16, 16, 12), 256
+        n = 16 * 16 * 12
+        m = pcal.StencilModel(grid, orc.random_uniform(n, 6), p, 13.0)
+    x0 = orc.initial_point_qr(n, p, 7)
+    cfg = pcal.SolverConfig(tol_rel_kkt=1e-300, max_iter=12)
+    run = (lambda: pcal.solve_emulated(m, cfg, x0, 2)) if case == "sharded" else \
+        (lambda: pcal.solve(m, cfg, x0))
+    r1 = run()
+    monkeypatch.setenv("PCAL_NO_TRI_TILES", "1")
+    r2 = run()
+    assert report_io.same_numerics(r1, r2)
+
+
 @pytest.mark.parametrize("name,mode", [("qr", "qr"), ("a2i", "a2-i"), ("a2ii", "a2-ii"),
                                        ("a2ii_p1", "a2-ii")])
 def test_initial_point_modes_match_reference(pcal, name, mode):
