@@ -2,6 +2,7 @@
 #include <cudaTypedefs.h>  // PFN_cuTensorMapEncodeTiled
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <vector>
 
@@ -42,6 +43,10 @@ void GemmPlan::release() {
   if (d_tiles) cudaFree(d_tiles);
   if (d_tri) cudaFree(d_tri);
   d_tri = nullptr;
+  if (d_cta_begin) cudaFree(d_cta_begin);
+  if (d_tile_cta0) cudaFree(d_tile_cta0);
+  d_cta_begin = nullptr;
+  d_tile_cta0 = nullptr;
   if (d_split) cudaFree(d_split);
   if (d_tasks) cudaFree(d_tasks);
   if (ws) cudaFree(ws);
@@ -132,30 +137,6 @@ void plan_gemm(GemmPlan& pl, int device, int size, int amode, int epi, int64_t M
       grid = (int)(4 * (int64_t)ntiles);
     }
   }
-  std::vector<int32_t> split(ntiles, -1);
-  std::vector<FixupTask> tasks;
-  int qmax = 1;
-  if (segs > 0) {
-    if (segs > 1 || chunk_partials)
-      for (int t = 0; t < ntiles; ++t) {
-        split[t] = t;
-        tasks.push_back({t, t, segs});
-      }
-    qmax = segs;
-  } else {
-    for (int t = 0; t < ntiles && upc == 0; ++t) {
-      const int32_t cf = cta_of_unit((int64_t)t * ki, units, grid);
-      const int32_t cl = cta_of_unit((int64_t)(t + 1) * ki - 1, units, grid);
-      if (cf != cl || chunk_partials) {
-        split[t] = (int32_t)tasks.size();
-        tasks.push_back({t, (int32_t)tasks.size(), cl - cf + 1});
-        qmax = std::max(qmax, cl - cf + 1);
-      }
-    }
-  }
-  if (chunk_partials) qmax = std::max(qmax, qmax_min);
-  PCAL_CUDA(cudaMalloc(&pl.d_tiles, sizeof(int2) * ntiles));
-  PCAL_CUDA(cudaMemcpy(pl.d_tiles, tiles.data(), sizeof(int2) * ntiles, cudaMemcpyHostToDevice));
   // diagonal tiles of the upper-triangle-only blocks: triangular work (mma_stage_tri)
   std::vector<uint8_t> tri(ntiles, 0);
   bool any_tri = false;
@@ -168,9 +149,81 @@ void plan_gemm(GemmPlan& pl, int device, int size, int amode, int epi, int64_t M
       any_tri |= d;
     }
   }
+  // stream-K over tiles of unequal cost (triangular tiles ≈ 136/256 of a full
+  // one): the CTA ranges split the WEIGHTED unit sequence evenly, so no CTA
+  // waits on another's extra full tiles; explicit range starts replace ⌊c·U/G⌋
+  std::vector<int64_t> cta_begin;
+  if (segs == 0 && upc == 0 && any_tri) {
+    constexpr double kTriCost = 0.56;  // 17 of 32 DMMAs, a few more fragment loads
+    std::vector<double> cum(ntiles + 1, 0.0);
+    for (int t = 0; t < ntiles; ++t) cum[t + 1] = cum[t] + (tri[t] ? kTriCost : 1.0) * ki;
+    cta_begin.assign(grid + 1, units);
+    cta_begin[0] = 0;
+    int t = 0;
+    for (int c = 1; c < grid; ++c) {
+      const double target = cum[ntiles] * c / grid;
+      while (t < ntiles && cum[t + 1] <= target) ++t;
+      if (t >= ntiles) {
+        cta_begin[c] = units;
+        continue;
+      }
+      const double per = (tri[t] ? kTriCost : 1.0);
+      const int64_t within = std::min<int64_t>(ki, (int64_t)std::ceil((target - cum[t]) / per));
+      cta_begin[c] = std::max<int64_t>(cta_begin[c - 1], (int64_t)t * ki + within);
+    }
+    // every range non-empty (a partial slot per CTA of a split tile), else
+    // keep the plain equal split
+    for (int c = 0; c < grid; ++c)
+      if (cta_begin[c + 1] <= cta_begin[c]) {
+        cta_begin.clear();
+        break;
+      }
+  }
+  auto cta_of = [&](int64_t u) -> int32_t {  // CTA whose range contains unit u
+    if (cta_begin.empty()) return cta_of_unit(u, units, grid);
+    return (int32_t)(std::upper_bound(cta_begin.begin(), cta_begin.end() - 1, u) -
+                     cta_begin.begin() - 1);
+  };
+  std::vector<int32_t> tile_cta0;
+  if (!cta_begin.empty()) {
+    tile_cta0.resize(ntiles);
+    for (int t2 = 0; t2 < ntiles; ++t2) tile_cta0[t2] = cta_of((int64_t)t2 * ki);
+  }
+  std::vector<int32_t> split(ntiles, -1);
+  std::vector<FixupTask> tasks;
+  int qmax = 1;
+  if (segs > 0) {
+    if (segs > 1 || chunk_partials)
+      for (int t = 0; t < ntiles; ++t) {
+        split[t] = t;
+        tasks.push_back({t, t, segs});
+      }
+    qmax = segs;
+  } else {
+    for (int t = 0; t < ntiles && upc == 0; ++t) {
+      const int32_t cf = cta_of((int64_t)t * ki);
+      const int32_t cl = cta_of((int64_t)(t + 1) * ki - 1);
+      if (cf != cl || chunk_partials) {
+        split[t] = (int32_t)tasks.size();
+        tasks.push_back({t, (int32_t)tasks.size(), cl - cf + 1});
+        qmax = std::max(qmax, cl - cf + 1);
+      }
+    }
+  }
+  if (chunk_partials) qmax = std::max(qmax, qmax_min);
+  PCAL_CUDA(cudaMalloc(&pl.d_tiles, sizeof(int2) * ntiles));
+  PCAL_CUDA(cudaMemcpy(pl.d_tiles, tiles.data(), sizeof(int2) * ntiles, cudaMemcpyHostToDevice));
   if (any_tri) {
     PCAL_CUDA(cudaMalloc(&pl.d_tri, ntiles));
     PCAL_CUDA(cudaMemcpy(pl.d_tri, tri.data(), ntiles, cudaMemcpyHostToDevice));
+  }
+  if (!cta_begin.empty()) {
+    PCAL_CUDA(cudaMalloc(&pl.d_cta_begin, sizeof(int64_t) * cta_begin.size()));
+    PCAL_CUDA(cudaMemcpy(pl.d_cta_begin, cta_begin.data(), sizeof(int64_t) * cta_begin.size(),
+                         cudaMemcpyHostToDevice));
+    PCAL_CUDA(cudaMalloc(&pl.d_tile_cta0, sizeof(int32_t) * ntiles));
+    PCAL_CUDA(cudaMemcpy(pl.d_tile_cta0, tile_cta0.data(), sizeof(int32_t) * ntiles,
+                         cudaMemcpyHostToDevice));
   }
   PCAL_CUDA(cudaMalloc(&pl.d_split, sizeof(int32_t) * ntiles));
   PCAL_CUDA(cudaMemcpy(pl.d_split, split.data(), sizeof(int32_t) * ntiles, cudaMemcpyHostToDevice));
@@ -189,6 +242,8 @@ void plan_gemm(GemmPlan& pl, int device, int size, int amode, int epi, int64_t M
   g.K = K;
   g.tiles = pl.d_tiles;
   g.tile_tri = pl.d_tri;
+  g.cta_begin = pl.d_cta_begin;
+  g.tile_cta0 = pl.d_tile_cta0;
   g.split_slot = pl.d_split;
   g.ntiles = ntiles;
   g.ki = ki;

@@ -450,9 +450,11 @@ __global__ void __launch_bounds__(Cfg::THREADS + 128, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int32_t cta = blockIdx.x;
   const int64_t u0 = g.segs ? seg_unit_begin(cta, g.ntiles, g.ki, g.segs, g.grid)
-                            : cta_unit_begin(cta, g.units, g.grid, g.upc);
+                            : g.cta_begin ? g.cta_begin[cta]
+                                          : cta_unit_begin(cta, g.units, g.grid, g.upc);
   const int64_t u1 = g.segs ? seg_unit_begin(cta + 1, g.ntiles, g.ki, g.segs, g.grid)
-                            : cta_unit_begin(cta + 1, g.units, g.grid, g.upc);
+                            : g.cta_begin ? g.cta_begin[cta + 1]
+                                          : cta_unit_begin(cta + 1, g.units, g.grid, g.upc);
   if (u0 >= u1) return;
   if (threadIdx.x == 0) {
     for (int s = 0; s < Cfg::STAGES; ++s) {
@@ -526,15 +528,19 @@ __global__ void __launch_bounds__(Cfg::THREADS + 128, 1)
       if (kTriCfg && tri) {
         flush_tri<Cfg>(g, tc, whole, whole ? nullptr
                        : g.ws + ((size_t)g.split_slot[t] * g.qmax +
-                                 (S ? cur_seg : cta - cta_of_unit((int64_t)t * g.ki, g.units,
-                                                                  g.grid))) *
+                                 (S ? cur_seg
+                                    : cta - (g.tile_cta0 ? g.tile_cta0[t]
+                                                         : cta_of_unit((int64_t)t * g.ki, g.units,
+                                                                       g.grid)))) *
                                     (size_t)(Cfg::BM * Cfg::BN),
                        warp, lane, acc);
       } else if (whole) {
         epilogue<Cfg, EPI>(g, tc.x, tc.y, wm, wn, lane, acc);
       } else {
         const int slot = g.split_slot[t];
-        const int q = S ? cur_seg : cta - cta_of_unit((int64_t)t * g.ki, g.units, g.grid);
+        const int q = S ? cur_seg
+                        : cta - (g.tile_cta0 ? g.tile_cta0[t]
+                                             : cta_of_unit((int64_t)t * g.ki, g.units, g.grid));
         double* w = g.ws + ((size_t)slot * g.qmax + q) * (size_t)(Cfg::BM * Cfg::BN);
 #pragma unroll
         for (int mt = 0; mt < Cfg::MT; ++mt)

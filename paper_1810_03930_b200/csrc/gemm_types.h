@@ -56,6 +56,8 @@ struct GemmArgs {
   int32_t segs;         // > 0: segmented schedule, S fixed K segments per tile (see below)
   int32_t a_stream;     // A is read exactly once (dense gradient): L2 evict-first loads
   const uint8_t* tile_tri;  // per tile: 1 = diagonal tile of an upper-triangle-only block
+  const int64_t* cta_begin; // stream-K with weighted tiles: unit range start of each CTA (G+1)
+  const int32_t* tile_cta0; //   and the first CTA of each tile (its partial slot q = cta − cta0)
 };
 
 struct FixupTask {   // one split tile
@@ -108,6 +110,8 @@ struct GemmPlan {
   GemmArgs args{};
   int2* d_tiles = nullptr;
   uint8_t* d_tri = nullptr;   // triangular (diagonal) tiles of symmetric Grams
+  int64_t* d_cta_begin = nullptr;
+  int32_t* d_tile_cta0 = nullptr;
   int32_t* d_split = nullptr;
   FixupTask* d_tasks = nullptr;
   int ntasks = 0;
