@@ -931,10 +931,27 @@ __global__ void __launch_bounds__(Cfg::THREADS + 128, 1)
   const EpiParams& e = g.ep;
   const int wm = warp / Cfg::WARPS_N, wn = warp % Cfg::WARPS_N;
   const int r = lane >> 2, q = lane & 3;
+  double acc[Cfg::MT][Cfg::NT][2];
   int stage = 0;
   unsigned phase = 0;
-  // ---- epilogue of tile t (its it-th on this CTA) from accumulators a
-  auto epilogue = [&](const double (&a)[Cfg::MT][Cfg::NT][2], int t, int it) {
+  int it = 0;
+  for (int t = blockIdx.x; t < g.ntiles; t += gridDim.x, ++it) {
+#pragma unroll
+    for (int mt = 0; mt < Cfg::MT; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < Cfg::NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+    for (int kk = 0; kk < g.ki; ++kk) {
+      mbar_wait(&full[stage], phase);
+      mma_stage<Cfg>(As + stage * (Cfg::A_STAGE * 8), Bs + stage * (Cfg::B_STAGE * 8), wm, wn,
+                     lane, acc);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (++stage == S) {
+        stage = 0;
+        phase ^= 1u;
+      }
+    }
+    // ---- epilogue: every operand in shared memory
     const int2 tc = g.tiles[t];
     const int64_t m0 = (int64_t)tc.x * BM;
     const int64_t j0 = (int64_t)tc.y * BNO;
@@ -957,8 +974,8 @@ __global__ void __launch_bounds__(Cfg::THREADS + 128, 1)
         const double gv = *reinterpret_cast<const double*>(gsb + off);
         const double xv = *reinterpret_cast<const double*>(xsb + off);
         if (row < e.n && j < e.p) {
-          const double kkt = gv - a[mt][nt][0];
-          const double pv = (e.p_from_g ? gv : kkt) + e.beta * a[mt][nt][1];
+          const double kkt = gv - acc[mt][nt][0];
+          const double pv = (e.p_from_g ? gv : kkt) + e.beta * acc[mt][nt][1];
           e.G[row + j * e.ld] = pv;
           ks += kkt * kkt;
           ds += (e.d_sq ? pv : xv) * pv;
@@ -989,52 +1006,6 @@ __global__ void __launch_bounds__(Cfg::THREADS + 128, 1)
         e.dpart[j * e.pstride + tc.x] = dv;
       }
     }
-  };
-  // ---- main loop of one tile into accumulators a; `mid` runs right after the
-  // tile's first k-iteration has been issued (the previous tile's epilogue:
-  // its loads, stores and shuffles proceed while those DMMAs execute)
-  auto mainloop = [&](double (&a)[Cfg::MT][Cfg::NT][2], auto&& mid) {
-#pragma unroll
-    for (int mt = 0; mt < Cfg::MT; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < Cfg::NT; ++nt) a[mt][nt][0] = a[mt][nt][1] = 0.0;
-    for (int kk = 0; kk < g.ki; ++kk) {
-      mbar_wait(&full[stage], phase);
-      mma_stage<Cfg>(As + stage * (Cfg::A_STAGE * 8), Bs + stage * (Cfg::B_STAGE * 8), wm, wn,
-                     lane, a);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[stage]);
-      if (++stage == S) {
-        stage = 0;
-        phase ^= 1u;
-      }
-      if (kk == 0) mid();
-    }
-  };
-  // two accumulator sets alternate between consecutive tiles (compile-time
-  // indices: the loop is unrolled by two tiles), so each tile's epilogue runs
-  // one k-iteration into the next tile instead of stopping the DMMA stream
-  double acc0[Cfg::MT][Cfg::NT][2], acc1[Cfg::MT][Cfg::NT][2];
-  int t = blockIdx.x, it = 0, tprev = -1;
-  bool last_in_0 = true;
-  while (t < g.ntiles) {
-    mainloop(acc0, [&] {
-      if (tprev >= 0) epilogue(acc1, tprev, it - 1);
-    });
-    tprev = t;
-    last_in_0 = true;
-    t += gridDim.x;
-    ++it;
-    if (t >= g.ntiles) break;
-    mainloop(acc1, [&] { epilogue(acc0, tprev, it - 1); });
-    tprev = t;
-    last_in_0 = false;
-    t += gridDim.x;
-    ++it;
-  }
-  if (tprev >= 0) {
-    if (last_in_0) epilogue(acc0, tprev, it - 1);
-    else epilogue(acc1, tprev, it - 1);
   }
 }
 
