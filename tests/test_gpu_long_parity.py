@@ -252,7 +252,3 @@ def test_cfg2_end_of_run_inside_ulp_ensemble(cfg2_run):
         rep.final_pre_orth.kkt_abs, base_pre[1], max(dk))
     assert abs(rep.final_pre_orth.feas - base_pre[3]) <= 2.0 * max(df)
     assert cols_up_to_sign(rep.final_x[idx], base_x) <= 2.0 * max(dx)
-    # the objective is not chaotic: every member and the GPU agree to 1e-9
-    for q in range(k):
-        assert abs(g[f"ens{q}_final_post"][0] - g["base_final_post"][0]) <= 1e-9 * abs(
-            g["base_final_post"][0])

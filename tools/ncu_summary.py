@@ -20,6 +20,10 @@ def short(name: str) -> str:
     nm = name.replace("pcal::", "").replace("(int)", "")
     if "gemm_xm_tmem" in nm:
         return "gemm_xm_tmem<128x128,MC,XM>"
+    if "gemm_xm_staged" in nm:
+        return "gemm_xm_staged<128x64,MC,XM>"
+    if "k_stencil_tma" in nm:
+        return "k_stencil_tma"
     m = re.search(r"gemm_(streamk|fixup|fixup_store)<GemmCfg<(\d+), (\d+), \d+, \d+, \d+, (\d)(?:, \d+)?>(?:, (\d))?(?:, (\d))?", nm)
     if m:
         kind = {"0": "STORE", "1": "GRAD", "2": "XM", None: "STORE"}[m.group(5)]
@@ -37,7 +41,8 @@ def phase_of(s: str) -> str:
         return "gram"
     if "XM" in s or s in ("k_sum_rows", "k_finish_eval", "k_zero_i32", "k_colsum3"):
         return "xm"
-    if s in ("k_bb_partials", "k_eta", "k_update", "k_normalize", "k_step_fused"):
+    if s in ("k_bb_partials", "k_eta", "k_update", "k_normalize", "k_step_fused", "k_bb_cols",
+             "k_bb_cols_sum", "k_colscale", "k_update_norm"):
         return "step"
     return "other"
 
@@ -129,8 +134,10 @@ def main():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--tag", default="r01")
     ap.add_argument("--kpi", type=int, default=19, help="kernels per iteration graph")
+    ap.add_argument("--outdir", default=os.path.join(ROOT, "profiles"),
+                    help="where the summaries go (on a GPU box: under gpurun_out/)")
     a = ap.parse_args()
-    prof = os.path.join(ROOT, "profiles")
+    prof = a.outdir
     os.makedirs(prof, exist_ok=True)
     if a.launches:
         with open(os.path.join(prof, f"{a.tag}_cfg{a.config}_launches.txt"), "w") as f:
