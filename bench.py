@@ -424,6 +424,9 @@ def main():
     ms = max_over_ranks(ms, world)
     barrier(world)
     phases = ses.profile(prof_iters)      # per-phase CUDA-event durations (same session)
+    # X·[W|C] as one block (P = G − X·M1, 2np² flop) or two (4np²), and how
+    # often the kkt identity's gated fallback ran
+    xm_form, xm_fallbacks = ses.xm_mode() if hasattr(ses, "xm_mode") else ("two_block", 0)
     rep = ses.finish(want_x=False)
     ses.close()
     del ses
@@ -441,7 +444,8 @@ def main():
     gram_flops = (2.0 if inst.kind != "dense" else 3.0) * nl * p * p
     work = {"gradient": (inst.grad_flops() * nl / n, "tensor") if inst.kind == "dense"
             else ((16.0 * nl * p + inst.op_bytes() * nl / n), "hbm"),
-            "gram": (gram_flops, "tensor"), "xm": (4.0 * nl * p * p, "tensor")}
+            "gram": (gram_flops, "tensor"),
+            "xm": ((2.0 if xm_form == "single_block" else 4.0) * nl * p * p, "tensor")}
     dom = max(("gradient", "gram", "xm"), key=lambda k: phases[k])
     amount, bound = work[dom]
     t = phases[dom] * 1e-3
@@ -457,19 +461,28 @@ def main():
             traffic = json.load(f).get("dram_bytes_per_launch", {}).get(dom)
     except Exception:
         pass
-    F = 7.0 * n * p * p + inst.grad_flops()
+    # flops the iteration's GEMMs must do in the formulation executed: Gram
+    # (3np², grid models 2np²: symmetric GᵀX), X·M1 (2np²) or X·[W|C] (4np²)
+    F = (gram_flops + work["xm"][0]) * n / nl + inst.grad_flops()
+    F_two_block = 7.0 * n * p * p + inst.grad_flops()  # round-1 definition (3np² + 4np²)
     B = 80.0 * n * p + inst.op_bytes()
     t_star = max(F / P64, B / BW) / world
+    t_star_two = max(F_two_block / P64, B / BW) / world
     roof = {"bound": bound, "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak,
             "traffic": traffic, "kernel": dom, "kernel_ms": phases[dom], "peak_src": src,
             "work_per_launch": amount,
             "work_def": ("2np^2 (upper tiles of the symmetric G^TX + X^TX)" if dom == "gram"
                          and inst.kind != "dense" else
-                         {"gram": "3np^2", "xm": "4np^2 (X·[W|C])", "gradient":
+                         {"gram": "3np^2", "xm": "2np^2 (X·M1, M1 = W - beta C)"
+                          if xm_form == "single_block" else "4np^2 (X·[W|C])", "gradient":
                           "2n^2p" if inst.kind == "dense" else "16np+8n bytes"}[dom])}
     iter_roof = {"flops": F, "bytes": B, "t_star_ms": t_star * 1e3, "frac": t_star * 1e3 / ms_per,
                  "bound": "fp64" if F / P64 >= B / BW else "hbm",
-                 "def": "T* = max(7np^2+F_grad / P_fp64, (80np+B_op) / BW) / n_gpus",
+                 "def": "T* = max((F_gram + F_xm + F_grad) / P_fp64, (80np+B_op) / BW) / n_gpus; "
+                        "F_gram = 3np^2 (grid models 2np^2), F_xm = 2np^2 single block / 4np^2 two",
+                 "xm_form": xm_form, "xm_identity_fallbacks": xm_fallbacks,
+                 "t_star_two_block_ms": t_star_two * 1e3,
+                 "frac_vs_two_block": t_star_two * 1e3 / ms_per,
                  "phase_ms": {k: round(v, 5) for k, v in phases.items()}}
 
     # ---- e2e: the public drop-in call with host buffers

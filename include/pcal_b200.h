@@ -207,6 +207,11 @@ int pcal_session_profile(pcal_session* s, int64_t iters, double* ms_out);
 int pcal_session_profile_kernels(pcal_session* s, int64_t iters, char* buf, int64_t cap);
 /* Per-iteration launch count of the captured iteration graph. */
 int64_t pcal_session_kernels_per_iteration(pcal_session* s);
+/* Form of the X·[W|C] product of PCAL / PLAM: 1 = single block P = G − X·M1
+ * with M1 = W − βC and Σ kkt² from Σ P² by the identity (one GPU, p > 96),
+ * 0 = the two-block product.  *fallbacks (may be NULL) = evaluations so far in
+ * which the identity cancelled too much and the gated two-block product ran. */
+int pcal_session_xm_mode(pcal_session* s, int64_t* fallbacks);
 
 /* ---- row-sharded multi-GPU solve (one process per GPU, NCCL) -------------
  * Rows are split into fixed global row chunks (pcal_row_chunks: whole z-plane

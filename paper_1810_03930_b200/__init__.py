@@ -146,6 +146,8 @@ def lib() -> C.CDLL:
     L.pcal_session_profile_kernels.argtypes = [vp, i64, C.c_char_p, i64]
     L.pcal_session_kernels_per_iteration.argtypes = [vp]
     L.pcal_session_kernels_per_iteration.restype = i64
+    L.pcal_session_xm_mode.argtypes = [vp, C.POINTER(i64)]
+    L.pcal_session_xm_mode.restype = C.c_int
     L.pcal_matmul_at_b.argtypes = [vp, vp, i64, i64, i64, vp, i32]
     L.pcal_matmul.argtypes = [vp, vp, i64, i64, i64, vp, i32]
     L.pcal_gram.argtypes = [vp, i64, i64, vp, i32]
@@ -599,6 +601,13 @@ class Session:
     @property
     def kernels_per_iteration(self) -> int:
         return self._L.pcal_session_kernels_per_iteration(self._h)
+
+    def xm_mode(self) -> tuple:
+        """("single_block" | "two_block", gated fallbacks so far): the form of the
+        X·[W|C] product (pcal_session_xm_mode)."""
+        fb = C.c_int64(0)
+        m = self._L.pcal_session_xm_mode(self._h, C.byref(fb))
+        return ("single_block" if m else "two_block", int(fb.value))
 
     def close(self) -> None:
         if getattr(self, "_h", None):

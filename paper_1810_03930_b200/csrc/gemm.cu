@@ -18,6 +18,7 @@ namespace pcal {
 template <int AM>
 using CfgBig = GemmCfg<128, 128, 2, 4, 3, AM, 32>;  // BK = 32: 3 × 64 KB stages
 using CfgXms = GemmCfg<128, 64, 4, 2, 3, A_MCONTIG, 32>;  // staged X·[W|C]: 3 × 48 KB + 64 KB
+using CfgXm1 = GemmCfg<64, 64, 2, 4, 4, A_MCONTIG, 32>;   // staged X·M1: 4 × 32 KB + 64 KB
 template <int AM>
 using CfgMid = GemmCfg<64, 64, 2, 2, 4, AM>;
 template <int AM>
@@ -34,6 +35,7 @@ CfgInfo cfg_info(int size) {
     case CFG_BIG:
     case CFG_XMT: return {128, 128, CfgBig<A_MCONTIG>::WM, CfgBig<A_MCONTIG>::BK};
     case CFG_XMS: return {128, 64, CfgXms::WM, CfgXms::BK};
+    case CFG_XM1: return {64, 64, CfgXm1::WM, CfgXm1::BK};
     case CFG_MID: return {64, 64, 32, CfgMid<A_MCONTIG>::BK};
     default: return {64, 32, 32, CfgSmall<A_MCONTIG>::BK};
   }
@@ -124,17 +126,30 @@ void plan_gemm(GemmPlan& pl, int device, int size, int amode, int epi, int64_t M
     const int64_t g0 = grid;
     const int64_t dp_cost = ceil_div(ntiles, g0) * ki;
     const int64_t sk_cost = ceil_div(units, g0) + 4;
-    const bool xm_only = size == CFG_XMT || size == CFG_XMS;
+    const bool xm_only = size == CFG_XMT || size == CFG_XMS || size == CFG_XM1;
     if (xm_only && (amode != A_MCONTIG || epi != EPI_XM))
       throw Error(PCAL_E_STATE, "gemm: the TMEM / staged-epilogue kernels are X·[W|C] only");
     if (dp_cost <= sk_cost || xm_only) {  // gemm_xm_tmem / gemm_xm_staged: whole tiles only
       const int64_t w = ceil_div(ntiles, g0);
       upc = w * ki;
       // gemm_xm_staged walks the tiles round-robin (one CTA per SM)
-      grid = size == CFG_XMS ? (int)std::min<int64_t>(ntiles, g0) : (int)ceil_div(ntiles, w);
+      grid = (size == CFG_XMS || size == CFG_XM1) ? (int)std::min<int64_t>(ntiles, g0)
+                                                  : (int)ceil_div(ntiles, w);
     } else if (epi != EPI_STORE && grid > 4 * (int64_t)ntiles) {
       // fused epilogues are fixed up one tile per CTA: keep ≤ 4 partials per tile
       grid = (int)(4 * (int64_t)ntiles);
+    }
+    // Tall-skinny Grams (K = n, up to 2M rows at config 5): one CTA range would
+    // sum ≈ 1M rows in a single DMMA accumulator chain, whose rounding error
+    // (≈ eps·√chain on the unit diagonal of XᵀX) then dominates ‖XᵀX − I‖ and the
+    // CholeskyQR2 result.  Cap the chain at kGramChain k-iterations: more,
+    // shorter CTA ranges (whole waves of g0), their partials summed in CTA order
+    // by the fixup.  Cost: one partial tile store per range (< 0.3 % at config 5).
+    if (upc == 0 && amode == A_KCONTIG && epi == EPI_STORE) {
+      const char* ev = getenv("PCAL_GRAM_CHAIN");
+      const int64_t kmax = ev ? atoll(ev) : 2048;
+      if (kmax > 0 && ceil_div(units, (int64_t)grid) > kmax)
+        grid = (int)(ceil_div(ceil_div(units, kmax), g0) * g0);
     }
   }
   // diagonal tiles of the upper-triangle-only blocks: triangular work (mma_stage_tri)
@@ -397,6 +412,27 @@ static void launch_xm_staged(const GemmPlan& pl, cudaStream_t st) {
   PCAL_CUDA(cudaGetLastError());
 }
 
+static void launch_xm1_staged(const GemmPlan& pl, cudaStream_t st) {
+  using Cfg = CfgXm1;
+  constexpr int smem = Cfg::SMEM_BYTES + (2 * Cfg::BM * Cfg::BN + 2 * 4 * Cfg::BN) * 8 + 2 * 8;
+  static_assert(smem <= 232448, "XM1: shared memory budget");
+  static bool attr_set = false;
+  if (!attr_set) {
+    PCAL_CUDA(cudaFuncSetAttribute(gemm_xm1_staged<Cfg>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr_set = true;
+  }
+  const GemmArgs& g = pl.args;
+  XmMaps maps;
+  encode_map(&maps.a, g.A, g.M, g.K, g.lda, Cfg::BK);
+  encode_map(&maps.b, g.B, g.K, g.N, g.ldb, Cfg::BN);
+  encode_map(&maps.g, g.ep.G, g.ep.n, g.ep.p, g.ep.ld, Cfg::BN);
+  encode_map(&maps.x, g.ep.X, g.ep.n, g.ep.p, g.ep.ld, Cfg::BN);
+  gemm_xm1_staged<Cfg><<<g.grid, Cfg::THREADS + 128, smem, st>>>(g, maps);
+  launched("gemm_xm1");
+  PCAL_CUDA(cudaGetLastError());
+}
+
 template <int AM, int EPI>
 static void launch_sized(const GemmPlan& pl, cudaStream_t st) {
   if constexpr (AM == A_MCONTIG && EPI == EPI_XM) {
@@ -406,6 +442,10 @@ static void launch_sized(const GemmPlan& pl, cudaStream_t st) {
     }
     if (pl.size == CFG_XMS) {
       launch_xm_staged(pl, st);
+      return;
+    }
+    if (pl.size == CFG_XM1) {
+      launch_xm1_staged(pl, st);
       return;
     }
   }

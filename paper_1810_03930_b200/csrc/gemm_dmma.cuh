@@ -353,7 +353,8 @@ __device__ __forceinline__ size_t frag_index(int warp, int mt, int nt, int x, in
 
 // ---- mbarrier helpers ------------------------------------------------------------
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
   asm volatile(
@@ -363,10 +364,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
       "@!p bra WAIT_%=;\n"
       "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity));
+      "r"(parity)
+      : "memory");  // shared-memory reads of the stage must not move above the wait
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)));
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
@@ -620,6 +622,14 @@ __device__ __forceinline__ void tmem_ld32(uint32_t addr, uint32_t (&v)[32]) {
                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31]) : "r"(addr) : "memory");
 }
 
+// tcgen05.wait::ld with the loaded registers as operands: no use of them can be
+// scheduled before the wait.
+__device__ __forceinline__ void tmem_wait_ld(uint32_t (&v)[32]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n"
+               : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7]), "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]), "+r"(v[14]), "+r"(v[15]), "+r"(v[16]), "+r"(v[17]), "+r"(v[18]), "+r"(v[19]), "+r"(v[20]), "+r"(v[21]), "+r"(v[22]), "+r"(v[23]), "+r"(v[24]), "+r"(v[25]), "+r"(v[26]), "+r"(v[27]), "+r"(v[28]), "+r"(v[29]), "+r"(v[30]), "+r"(v[31])
+               :: "memory");
+}
+
 // XM epilogue of one 8-column group nt of warp tile (wm, wn): EPI_XM of
 // epilogue<> with NB = 1 (same element / partial / shuffle order).
 template <class Cfg>
@@ -708,9 +718,9 @@ __global__ void __launch_bounds__(Cfg::THREADS + 256, 1)
                  ::"r"(smem_u32(tslot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
-  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tbase = *tslot;
   if (warp >= Cfg::WARPS && warp < Cfg::WARPS + 4) {  // producer warpgroup
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kProducerRegs));
@@ -739,7 +749,7 @@ __global__ void __launch_bounds__(Cfg::THREADS + 256, 1)
         }
       }
       mbar_wait(&acc_full[buf], ph);
-      asm volatile("tcgen05.fence::after_thread_sync;\n");
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
       const int2 tc = g.tiles[t];
 #pragma unroll 1
       for (int wm = 0; wm < 2; ++wm)
@@ -747,7 +757,7 @@ __global__ void __launch_bounds__(Cfg::THREADS + 256, 1)
         for (int nt = 0; nt < Cfg::NT; ++nt) {
           uint32_t v[32];
           tmem_ld32(tbase + (quarter << 16) + (uint32_t)(buf * 256 + wm * 128 + nt * 32), v);
-          asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+          tmem_wait_ld(v);
           double a[Cfg::MT][2];
 #pragma unroll
           for (int mt = 0; mt < Cfg::MT; ++mt)
@@ -756,11 +766,11 @@ __global__ void __launch_bounds__(Cfg::THREADS + 256, 1)
               a[mt][x] = __hiloint2double((int)v[(mt * 2 + x) * 2 + 1], (int)v[(mt * 2 + x) * 2]);
           epilogue_xm_group<Cfg>(g, tc.x, tc.y, wm, wn, lane, nt, a);
         }
-      asm volatile("tcgen05.fence::before_thread_sync;\n");
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[buf]);
     }
-    asm volatile("bar.sync 1, %0;\n" ::"n"(Cfg::THREADS + 128));  // consumers + epilogue
+    asm volatile("bar.sync 1, %0;\n" ::"n"(Cfg::THREADS + 128) : "memory");  // consumers + epilogue
     return;
   }
   {  // consumers
@@ -798,7 +808,7 @@ __global__ void __launch_bounds__(Cfg::THREADS + 256, 1)
     const int buf = (t - t0) & 1;
     const unsigned ph = (unsigned)((t - t0) >> 1) & 1u;
     mbar_wait(&acc_empty[buf], ph ^ 1u);
-    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
 #pragma unroll
     for (int nt = 0; nt < Cfg::NT; ++nt) {
       uint32_t v[32];
@@ -812,13 +822,13 @@ __global__ void __launch_bounds__(Cfg::THREADS + 256, 1)
       tmem_st32(tbase + (quarter << 16) + (uint32_t)(buf * 256 + wm * 128 + nt * 32), v);
     }
     asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
-    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncwarp();
     if (lane == 0) mbar_arrive(&acc_full[buf]);
   }
-  asm volatile("bar.sync 1, %0;\n" ::"n"(Cfg::THREADS + 128));
+  asm volatile("bar.sync 1, %0;\n" ::"n"(Cfg::THREADS + 128) : "memory");
   if (warp == 0) {
-    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tbase));
   }
 }
@@ -1004,6 +1014,170 @@ __global__ void __launch_bounds__(Cfg::THREADS + 128, 1)
                           rk[7 * BNO + jl];
         e.kpart[j * e.pstride + tc.x] = kv;
         e.dpart[j * e.pstride + tc.x] = dv;
+      }
+    }
+  }
+}
+
+// ---- P = G − X·M1 with M1 = W − β·C: the single-block X·[W|C] -------------------
+// PCAL / PLAM need P = (G − XW) + β·XC and the column sums of kkt² with
+// kkt = G − XW.  Multiplying by the one p × p matrix M1 = W − β·C gives P with
+// half the flops of X·[W|C]; Σ kkt² then follows from Σ P² by the identity
+// (X has XᵀX = I + C, C and W symmetric):
+//   ‖G − XW‖² = ‖P‖² + 2β⟨W, C²⟩ − β²(‖C‖² + ⟨C, C²⟩)
+// (session.cu k_kkt_gate, with a gated fallback to the two-block product when
+// the correction cancels too much of ‖P‖²).  64 × 64 tiles, all 64 MMA
+// columns are output columns: the G / X staging (64 rows × 64 columns, 2 ×
+// 32 KB) fits beside a 4 × 32 KB ring.  Output column of (wn, nt, x, q):
+// wn·16 + 8·nt + 2·x + {0,1,4,5}[q] (M1 stored in that slot order,
+// pcal_kernels.cuh xm1_slot_of_col): each 8-lane row group of a fragment
+// column reads four columns whose (jl mod 8) are {b, b^1, b^4, b^5} — the
+// swizzled staging reads are conflict-free (2 wavefronts per 256 bytes).
+__device__ __forceinline__ int xm1_out_col(int wn, int nt, int x, int q) {
+  return wn * 16 + 8 * nt + 2 * x + (q & 1) + 4 * (q >> 1);
+}
+
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS + 128, 1)
+    gemm_xm1_staged(GemmArgs g, const __grid_constant__ XmMaps maps) {
+  constexpr int S = Cfg::STAGES, BM = Cfg::BM, BN = Cfg::BN;
+  static_assert(Cfg::WARPS == 8 && Cfg::WARPS_M == 2 && Cfg::WARPS_N == 4 && BM == 64 &&
+                    BN == 64 && Cfg::NT == 2 && Cfg::MT == 4,
+                "XM1: 64 × 64 tiles, 2 × 4 consumer warps");
+  if (g.ctl && g.ctl->done) return;
+  extern __shared__ __align__(1024) char smem_raw[];
+  char* As = smem_ring<Cfg>(smem_raw);
+  char* Bs = As + S * Cfg::A_STAGE * 8;
+  double* Gs = reinterpret_cast<double*>(Bs + S * Cfg::B_STAGE * 8);  // [col][row], swizzled
+  double* Xs = Gs + BM * BN;
+  double* red = Xs + BM * BN;  // [2 parity][k wm0, k wm1, d wm0, d wm1][BN]
+  uint64_t* full = reinterpret_cast<uint64_t*>(red + 2 * 4 * BN);
+  uint64_t* empty = full + S;
+  uint64_t* efull = empty + S;
+  uint64_t* eempty = efull + 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if ((int)blockIdx.x >= g.ntiles) return;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], Cfg::WARPS);
+    }
+    mbar_init(efull, 1);
+    mbar_init(eempty, Cfg::WARPS);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (warp >= Cfg::WARPS) {  // producer warpgroup: one thread drives the TMA unit
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kProducerRegs));
+    if (warp != Cfg::WARPS || lane != 0) return;
+    const int kload = min(S, g.ki - 1);
+    int s = 0;
+    unsigned ph = 0;
+    int it = 0;
+    for (int t = blockIdx.x; t < g.ntiles; t += gridDim.x, ++it) {
+      const int2 tc = g.tiles[t];
+      const int m0 = tc.x * BM, n0 = tc.y * BN;
+      for (int kk = 0; kk < g.ki; ++kk) {
+        if (kk == kload) {
+          mbar_wait(eempty, (unsigned)(it & 1) ^ 1u);
+          mbar_arrive_expect_tx(efull, 2 * BM * BN * 8);
+#pragma unroll
+          for (int rb = 0; rb < BM / 16; ++rb) {
+            tma_load_2d(Gs + rb * 16 * BN, &maps.g, m0 + 16 * rb, n0, efull);
+            tma_load_2d(Xs + rb * 16 * BN, &maps.x, m0 + 16 * rb, n0, efull);
+          }
+        }
+        mbar_wait(&empty[s], ph ^ 1u);
+        mbar_arrive_expect_tx(&full[s], Cfg::STAGE_BYTES);
+        char* as = As + s * (Cfg::A_STAGE * 8);
+        char* bs = Bs + s * (Cfg::B_STAGE * 8);
+        const int k0 = kk * Cfg::BK;
+#pragma unroll
+        for (int mb = 0; mb < BM / 16; ++mb)
+          tma_load_2d(as + mb * (Cfg::BK * 128), &maps.a, m0 + 16 * mb, k0, &full[s]);
+#pragma unroll
+        for (int kh = 0; kh < Cfg::BK / 16; ++kh)
+          tma_load_2d(bs + kh * (BN * 128), &maps.b, k0 + 16 * kh, n0, &full[s]);
+        if (++s == S) {
+          s = 0;
+          ph ^= 1u;
+        }
+      }
+    }
+    return;
+  }
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(232));
+  const EpiParams& e = g.ep;
+  const int wm = warp / Cfg::WARPS_N, wn = warp % Cfg::WARPS_N;
+  const int r = lane >> 2, q = lane & 3;
+  double acc[Cfg::MT][Cfg::NT][2];
+  int stage = 0;
+  unsigned phase = 0;
+  int it = 0;
+  for (int t = blockIdx.x; t < g.ntiles; t += gridDim.x, ++it) {
+#pragma unroll
+    for (int mt = 0; mt < Cfg::MT; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < Cfg::NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+    for (int kk = 0; kk < g.ki; ++kk) {
+      mbar_wait(&full[stage], phase);
+      mma_stage<Cfg>(As + stage * (Cfg::A_STAGE * 8), Bs + stage * (Cfg::B_STAGE * 8), wm, wn,
+                     lane, acc);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (++stage == S) {
+        stage = 0;
+        phase ^= 1u;
+      }
+    }
+    const int2 tc = g.tiles[t];
+    const int64_t m0 = (int64_t)tc.x * BM;
+    const int64_t j0 = (int64_t)tc.y * BN;
+    mbar_wait(efull, (unsigned)(it & 1));
+    double* rk = red + (it & 1) * (4 * BN);
+    const char* gsb = reinterpret_cast<const char*>(Gs);
+    const char* xsb = reinterpret_cast<const char*>(Xs);
+#pragma unroll
+    for (int nt = 0; nt < Cfg::NT; ++nt)
+#pragma unroll
+      for (int x = 0; x < 2; ++x) {
+        const int jl = xm1_out_col(wn, nt, x, q);
+        const int64_t j = j0 + jl;
+        double ks = 0.0, ds = 0.0;
+#pragma unroll
+        for (int mt = 0; mt < Cfg::MT; ++mt) {
+          const int rl = wm * Cfg::WM + mt * 8 + r;
+          const int64_t row = m0 + rl;
+          const int off = (rl >> 4) * (16 * BN * 8) + jl * 128 +
+                          ((((rl & 15) >> 1) ^ (jl & 7)) << 4) + (rl & 1) * 8;
+          const double gv = *reinterpret_cast<const double*>(gsb + off);
+          const double xv = *reinterpret_cast<const double*>(xsb + off);
+          if (row < e.n && j < e.p) {
+            const double pv = gv - acc[mt][nt][x];
+            e.G[row + j * e.ld] = pv;
+            ks += pv * pv;
+            ds += xv * pv;
+          }
+        }
+#pragma unroll
+        for (int o = 4; o < 32; o <<= 1) {
+          ks += __shfl_xor_sync(0xffffffffu, ks, o);
+          ds += __shfl_xor_sync(0xffffffffu, ds, o);
+        }
+        if (r == 0) {
+          rk[wm * BN + jl] = ks;
+          rk[(2 + wm) * BN + jl] = ds;
+        }
+      }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(eempty);  // Gs / Xs of this tile are no longer read
+    asm volatile("bar.sync 1, %0;\n" ::"n"(Cfg::THREADS) : "memory");
+    if (threadIdx.x < BN) {
+      const int jl = threadIdx.x;
+      const int64_t j = j0 + jl;
+      if (j < e.p) {
+        e.kpart[j * e.pstride + tc.x] = rk[jl] + rk[BN + jl];
+        e.dpart[j * e.pstride + tc.x] = rk[2 * BN + jl] + rk[3 * BN + jl];
       }
     }
   }

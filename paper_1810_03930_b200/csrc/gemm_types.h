@@ -95,8 +95,9 @@ __host__ __device__ inline int64_t seg_unit_begin(int32_t c, int32_t ntiles, int
 // CFG_XMT: the CFG_BIG tiles of X·[W|C] with the TMEM-staged epilogue
 // (gemm_xm_tmem; data-parallel whole tiles).  CFG_XMS: 128 × 64 tiles of
 // X·[W|C] with the fused epilogue reading TMA-staged G / X (gemm_xm_staged;
-// column partials per 128-row tile block).
-enum CfgSize { CFG_BIG = 0, CFG_MID = 1, CFG_SMALL = 2, CFG_XMT = 3, CFG_XMS = 4 };
+// column partials per 128-row tile block).  CFG_XM1: 64 × 64 tiles of the
+// single-block P = G − X·M1 (gemm_xm1_staged; column partials per 64-row block).
+enum CfgSize { CFG_BIG = 0, CFG_MID = 1, CFG_SMALL = 2, CFG_XMT = 3, CFG_XMS = 4, CFG_XM1 = 5 };
 
 struct CfgInfo {
   int BM, BN, WM, BK;

@@ -17,9 +17,11 @@ struct ColSumArgs {
   int64_t nrows[3];
   int64_t stride[3];
   double* out[3];
+  const int32_t* gate;  // non-null: run only when *gate != 0
 };
 __global__ void __launch_bounds__(kStreamThreads) k_colsum3(ColSumArgs a, const Ctl* ctl) {
   if (ctl && ctl->done) return;
+  if (a.gate && !*a.gate) return;
   __shared__ double sm[kStreamThreads / 32];
   const int which = blockIdx.y;
   if (!a.in[which]) return;
@@ -51,11 +53,31 @@ __host__ __device__ __forceinline__ int64_t xm_slot_of_col(int64_t j) {
   return (j & ~int64_t(15)) + nt * 4 + q;
 }
 
+// Column slot of output column j in M1 for gemm_xm1_staged (gemm_dmma.cuh
+// xm1_out_col): t = j mod 16 = 8·nt + 2·x + (q & 1) + 4·(q >> 1) sits at MMA
+// column 8·nt + 2·q + x.
+__host__ __device__ __forceinline__ int64_t xm1_slot_of_col(int64_t j) {
+  const int64_t t = j & 15;
+  const int64_t nt = (t >> 3) & 1, x = (t >> 1) & 1, q = (t & 1) + 2 * ((t >> 2) & 1);
+  return (j & ~int64_t(15)) + 8 * nt + 2 * q + x;
+}
+
+// XM1 mode (PCAL / PLAM, gemm_xm1_staged): besides the regular outputs the
+// kernel writes M1 = W − β·C in xm1 slot order into m1 (pp × pp), and W and C
+// in natural order into wm / cm (the ⟨W, C²⟩, ⟨C, C²⟩ terms of the kkt
+// identity), and mcat holds the fallback operand [β·C | C] interleaved.
+struct Xm1Out {
+  double* m1;
+  double* wm;
+  double* cm;
+};
+
 enum { MC_PCAL = 0, MC_DA = 1, MC_MOPTQR = 2 };
 __global__ void k_small_pxp(const double* __restrict__ gr, int64_t pp, int64_t p,
                             double* __restrict__ mcat, int64_t ldk, double* __restrict__ cpart,
                             int mode, double beta, double* __restrict__ lam, int lam_init,
-                            const Ctl* ctl, int gx_upper = 0, int perm32 = 0) {
+                            const Ctl* ctl, int gx_upper = 0, int perm32 = 0,
+                            Xm1Out xm1 = Xm1Out{nullptr, nullptr, nullptr}) {
   if (ctl && ctl->done) return;
   __shared__ double sm[kStreamThreads / 32];
   const int64_t total = p * p;
@@ -84,13 +106,78 @@ __global__ void k_small_pxp(const double* __restrict__ gr, int64_t pp, int64_t p
     } else {
       m = -gr[k + j * ldg];
     }
-    const int64_t slot = perm32 ? xm_slot_of_col(j) : j;
-    mcat[k + (2 * slot) * ldk] = w;
-    mcat[k + (2 * slot + 1) * ldk] = m;
+    if (xm1.m1) {
+      xm1.m1[k + xm1_slot_of_col(j) * ldk] = w + -beta * c;
+      xm1.wm[k + j * ldk] = w;
+      xm1.cm[k + j * ldk] = c;
+      mcat[k + (2 * j) * ldk] = beta * c;  // fallback: kkt = P − X·(βC), P = kkt + β·XC
+      mcat[k + (2 * j + 1) * ldk] = c;
+    } else {
+      const int64_t slot = perm32 ? xm_slot_of_col(j) : j;
+      mcat[k + (2 * slot) * ldk] = w;
+      mcat[k + (2 * slot + 1) * ldk] = m;
+    }
     acc += c * c;
   }
   const double s = block_sum<kStreamThreads>(acc, sm);
   if (threadIdx.x == 0) cpart[blockIdx.x] = s;
+}
+
+// The kkt identity's p × p inner products (XM1 mode):
+// part[block·3 + {0,1,2}] = partial {⟨W, C²⟩, ⟨C, C²⟩, ⟨C, C⟩}.
+__global__ void k_kkt_corr(const double* __restrict__ w, const double* __restrict__ c,
+                           const double* __restrict__ c2, int64_t ldk, int64_t p,
+                           double* __restrict__ part, const Ctl* ctl) {
+  if (ctl && ctl->done) return;
+  __shared__ double sm[kStreamThreads / 32];
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < p * p;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e % p + (e / p) * ldk;
+    const double cv = c[i], qv = c2[i];
+    a0 += w[i] * qv;
+    a1 += cv * qv;
+    a2 += cv * cv;
+  }
+  const double s0 = block_sum<kStreamThreads>(a0, sm);
+  const double s1 = block_sum<kStreamThreads>(a1, sm);
+  const double s2 = block_sum<kStreamThreads>(a2, sm);
+  if (threadIdx.x == 0) {
+    part[3 * blockIdx.x] = s0;
+    part[3 * blockIdx.x + 1] = s1;
+    part[3 * blockIdx.x + 2] = s2;
+  }
+}
+
+// Σ kkt² = Σ P² + 2β⟨W, C²⟩ − β²(‖C‖² + ⟨C, C²⟩) (gemm_dmma.cuh gemm_xm1_staged).
+// The identity is used while its terms cancel by less than a factor `gate_ratio`
+// ((Σ P² + |correction terms|) ≤ gate_ratio · result, i.e. the rounding of the
+// terms costs < gate_ratio ulps of Σ kkt²); otherwise *fb = 1 and the gated
+// two-block product recomputes kkt directly.  kk[0] = Σ kkt² (identity),
+// kk[1] counts fallbacks.
+__global__ void k_kkt_gate(const double* __restrict__ part, int nb, const double* __restrict__ kcol,
+                           int64_t p, double beta, double gate_ratio, int32_t* fb, double* kk,
+                           const Ctl* ctl) {
+  if (ctl && ctl->done) return;
+  __shared__ double sm[8];
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, ap = 0.0;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+    a0 += part[3 * i];
+    a1 += part[3 * i + 1];
+    a2 += part[3 * i + 2];
+  }
+  for (int64_t j = threadIdx.x; j < p; j += blockDim.x) ap += kcol[j];
+  const double wc2 = block_sum<256>(a0, sm);
+  const double cc2 = block_sum<256>(a1, sm);
+  const double cc = block_sum<256>(a2, sm);
+  const double pp2 = block_sum<256>(ap, sm);
+  if (threadIdx.x != 0) return;
+  const double k2 = pp2 + (2.0 * beta * wc2 - beta * beta * (cc + cc2));
+  const double mag = pp2 + 2.0 * fabs(beta * wc2) + beta * beta * (cc + fabs(cc2));
+  const bool fall = !(k2 > 0.0) || !isfinite(k2) || mag > gate_ratio * k2;
+  *fb = fall ? 1 : 0;
+  kk[0] = k2;
+  if (fall) kk[1] += 1.0;
 }
 
 // Stepsize inner products (stepsize_select, solver.cpp:218-222) with the

@@ -295,6 +295,8 @@ struct FinishArgs {
   double coeff;         // density models: α (P1) / γ (P6)
   int32_t p6;           // density models: the P6 term
   const double* glcol;  // ALM: Σ_i P_ij² per column (‖∇L‖² = their sum), else null
+  const double* k2_id;  // XM1 mode: Σ kkt² by the identity (k_kkt_gate) unless *k2_fb
+  const int32_t* k2_fb;
 };
 
 // ALM inner-loop bookkeeping for the iterate just evaluated (alm_outer,
@@ -452,7 +454,8 @@ __global__ void __launch_bounds__(256) k_finish_eval(FinishArgs a, Ctl* ctl,
       pe += a.spart[3 * i + 2];
     }
   const double f1 = block_sum<256>(pf, sm);
-  const double k2 = block_sum<256>(pk, sm);
+  const double k2s = block_sum<256>(pk, sm);
+  const double k2 = (a.k2_id && !*a.k2_fb) ? *a.k2_id : k2s;
   const double c2 = block_sum<256>(pc, sm);
   const double vr = block_sum<256>(pv, sm);
   const double rh = block_sum<256>(pr, sm);
@@ -557,6 +560,13 @@ struct pcal_session {
   pcal::DevBuf gr, mcat, fpart, kpart, dpart, cpart, bbpart, npart, post;
   pcal::DevBuf colpart, sinv;  // fused normalisation: (chunk, column) sums; 1/‖z_j‖
   int32_t* sfb = nullptr;      // per column: take the exact two-pass normalisation
+  // XM1 mode (PCAL / PLAM on one GPU): P = G − X·M1, Σ kkt² by the identity
+  // (pcal_kernels.cuh k_kkt_gate); M1 (slot order), W, C, C², the identity's
+  // partials, [Σ kkt², fallback count], the fallback flag
+  bool xm1 = false;
+  double xm1_gate = 1e4;
+  pcal::DevBuf m1, wmat, cmat, c2m, kcp, kk;
+  int32_t* kfb = nullptr;
   pcal::DevBuf orth_b, orth_l, orth_t, orth_f2;
   int32_t* bad = nullptr;
   int32_t* orth_status = nullptr;
@@ -566,6 +576,7 @@ struct pcal_session {
   int64_t trace_cap = 0;
   // plans
   pcal::GemmPlan grad[2], grad2[2], gram[2], xm[2], orth_gram, orth_mul;
+  pcal::GemmPlan c2plan, xmfb[2];  // XM1 mode: C² and the gated two-block fallback
   // MOptQR in-graph retraction (per parity): Gram of Z, Z·T → Q1, Gram of Q1, Q1·T → Q
   pcal::GemmPlan rq_gram_z[2], rq_mul1[2], rq_gram_q[2], rq_mul2[2];
   pcal::DevBuf lam;  // dual-ascent multiplier Λ (p×p, replicated)
@@ -709,8 +720,9 @@ static void tree_setup(pcal_session* s, int which, int m, int64_t ntiles) {
 // Column sums of the three partial arrays (f, kkt², d), one launch.
 static void launch_colsums(pcal_session* s, const double* fp, int64_t nrb_f, const double* kp,
                            const double* dp, int64_t nrb_kd, double* fcol, double* kcol,
-                           double* dcol, const Ctl* ctl) {
+                           double* dcol, const Ctl* ctl, const int32_t* gate = nullptr) {
   ColSumArgs a{};
+  a.gate = gate;
   a.in[0] = fp;
   a.nrows[0] = nrb_f;
   a.stride[0] = s->pstride_f;
@@ -972,16 +984,31 @@ static void launch_eval(pcal_session* s, int b, int mode, const Ctl* ctl_guard) 
     const int mc = (s->alg == PCAL_ALG_PLAMDA || s->alg == PCAL_ALG_PCALDA || alm) ? MC_DA
                    : s->alg == PCAL_ALG_MOPTQR                               ? MC_MOPTQR
                                                                              : MC_PCAL;
-    k_small_pxp<<<s->cp_blocks, kStreamThreads, 0, st>>>(s->gr.p, s->pp, s->p, s->mcat.p, s->pp,
-                                                         s->cpart.p, mc, s->beta, s->lam.p,
-                                                         lam_mode, ctl_guard,
-                                                         s->sym_gx ? 1 : 0,
-                                                         s->xm[b].size == CFG_XMS ? 1 : 0);
+    k_small_pxp<<<s->cp_blocks, kStreamThreads, 0, st>>>(
+        s->gr.p, s->pp, s->p, s->mcat.p, s->pp, s->cpart.p, mc, s->beta, s->lam.p, lam_mode,
+        ctl_guard, s->sym_gx ? 1 : 0, s->xm[b].size == CFG_XMS ? 1 : 0,
+        s->xm1 ? Xm1Out{s->m1.p, s->wmat.p, s->cmat.p} : Xm1Out{nullptr, nullptr, nullptr});
   }
   launched("k_small_pxp");
+  if (s->xm1) {  // C² and the identity's inner products
+    launch_gemm(s->c2plan, st);
+    k_kkt_corr<<<s->cp_blocks, kStreamThreads, 0, st>>>(s->wmat.p, s->cmat.p, s->c2m.p, s->pp,
+                                                        s->p, s->kcp.p, ctl_guard);
+    launched("k_kkt_corr");
+  }
   mark(s, 3);
   launch_gemm(s->xm[b], st);
-  if (s->repro) {  // C2: per-chunk column sums, gathered and summed in chunk order
+  if (s->xm1) {
+    launch_colsums(s, s->fpart.p, s->nrb_f, s->kpart.p, s->dpart.p, s->nrb_xm, Fcol(s, b),
+                   Kcol(s, b), Dvec(s, b), ctl_guard);
+    k_kkt_gate<<<1, 256, 0, st>>>(s->kcp.p, s->cp_blocks, Kcol(s, b), s->p, s->beta, s->xm1_gate,
+                                  s->kfb, s->kk.p, ctl_guard);
+    launched("k_kkt_gate");
+    // the identity cancelled too much: kkt = P − X·(βC) directly (gated: no-ops otherwise)
+    launch_gemm(s->xmfb[b], st);
+    launch_colsums(s, nullptr, 0, s->kpart.p, s->dpart.p, s->nrb_xm, nullptr, Kcol(s, b),
+                   Dvec(s, b), ctl_guard, s->kfb);
+  } else if (s->repro) {  // C2: per-chunk column sums, gathered and summed in chunk order
     const bool dform = s->alg == PCAL_ALG_PCAL && s->cfg.multiplier_rule == PCAL_MULT_PCAL_FORMULA;
     const int64_t wm_xm = cfg_info(pick_size(2 * s->pp)).WM;
     ChunkColArgs a{};
@@ -1034,6 +1061,8 @@ static void launch_eval(pcal_session* s, int b, int mode, const Ctl* ctl_guard) 
   fa.coeff = s->model.coeff;
   fa.p6 = s->model.density_variant == PCAL_DENSITY_P6;
   fa.glcol = s->alg == PCAL_ALG_ALM ? s->glcol.p : nullptr;
+  fa.k2_id = s->xm1 ? s->kk.p : nullptr;
+  fa.k2_fb = s->kfb;
   k_finish_eval<<<1, 256, 0, st>>>(fa, s->ctl, s->post.p);
   launched("k_finish_eval");
   mark(s, 4);
@@ -1212,14 +1241,23 @@ static void launch_iteration(pcal_session* s, int b) {
 }
 
 // GEMM configuration of X·[W|C] (its partial row-block is xm_row_block()).
+// XM1 (P = G − X·M1, half the flops): PCAL / PLAM on one GPU with p ≥ 128;
+// PCAL_XM_TWO_BLOCK=1 keeps the X·[W|C] product.
+static bool xm1_mode(const pcal_session* s) {
+  return (s->alg == PCAL_ALG_PCAL || s->alg == PCAL_ALG_PLAM) && !s->repro && !s->comm &&
+         pick_size(s->pp) == CFG_BIG && !getenv("PCAL_XM_TWO_BLOCK") &&
+         !getenv("PCAL_NO_TMEM_EPI") && !getenv("PCAL_XM_TMEM");
+}
 static int xm_config(const pcal_session* s) {
   const int xsz = pick_size(2 * s->pp);
   if (xsz != CFG_BIG || s->repro || getenv("PCAL_NO_TMEM_EPI")) return xsz;
+  if (xm1_mode(s)) return CFG_XM1;
   return getenv("PCAL_XM_TMEM") ? (int)CFG_XMT : (int)CFG_XMS;
 }
 static int64_t xm_row_block(const pcal_session* s) {
   const int c = xm_config(s);
-  return c == CFG_XMS ? cfg_info(c).BM : cfg_info(c).WM;  // staged: one partial per tile row
+  // staged: one partial per tile row (XM1: 64 rows = the fallback GEMM's warp rows)
+  return (c == CFG_XMS || c == CFG_XM1) ? cfg_info(c).BM : cfg_info(c).WM;
 }
 
 static void build_plans(pcal_session* s) {
@@ -1323,6 +1361,35 @@ static void build_plans(pcal_session* s) {
       g.args.ctl = s->ctl;
     }
     // X·[W|C] with the PCAL epilogue: A = X (MCONTIG, K = pp), B = mcat (pp × 2pp)
+    if (s->xm1) {  // P = G − X·M1 (B = M1, pp × pp), fallback X·[βC|C] gated by kfb
+      GemmPlan& g = s->xm[b];
+      plan_gemm(g, dev, CFG_XM1, A_MCONTIG, EPI_XM, n, pp, pp);
+      g.args.A = Xof(s, b);
+      g.args.lda = ld;
+      g.args.B = s->m1.p;
+      g.args.ldb = pp;
+      EpiParams& e = g.args.ep;
+      e.G = Pof(s, b);
+      e.X = Xof(s, b);
+      e.ld = ld;
+      e.kpart = s->kpart.p;
+      e.dpart = s->dpart.p;
+      e.pstride = s->pstride_xm;
+      e.n = n;
+      e.p = s->p;
+      g.args.ctl = s->ctl;
+      GemmPlan& f = s->xmfb[b];
+      plan_gemm(f, dev, CFG_BIG, A_MCONTIG, EPI_XM, n, 2 * pp, pp);
+      f.args.A = Xof(s, b);
+      f.args.lda = ld;
+      f.args.B = s->mcat.p;
+      f.args.ldb = pp;
+      f.args.ep = e;
+      f.args.ep.beta = s->beta;  // kkt = P − X·(βC); P = kkt + β·XC
+      f.args.ctl = s->ctl;
+      f.args.gate = s->kfb;
+      continue;
+    }
     {
       GemmPlan& g = s->xm[b];
       // wide outputs: 128 × 64 tiles whose fused epilogue reads TMA-staged G / X
@@ -1351,6 +1418,16 @@ static void build_plans(pcal_session* s) {
       e.p = s->p;
       g.args.ctl = s->ctl;
     }
+  }
+  if (s->xm1) {  // C² = C·C (C symmetric, pp × pp, zero padded)
+    plan_gemm(s->c2plan, dev, pick_size(pp), A_MCONTIG, EPI_STORE, pp, pp, pp);
+    GemmArgs& a = s->c2plan.args;
+    a.A = a.B = s->cmat.p;
+    a.lda = a.ldb = pp;
+    a.ep.C = s->c2m.p;
+    a.ep.ldc = pp;
+    a.ep.m_store = a.ep.n_store = pp;
+    a.ctl = s->ctl;
   }
   if (s->repro) tree_setup(s, 0, s->gram_sub, s->gram[0].ntasks);
 }
@@ -1471,6 +1548,18 @@ static void alloc_state(pcal_session* s) {
   s->gr.zero(st);
   s->mcat.alloc((size_t)pp * 2 * pp);
   s->mcat.zero(st);
+  s->xm1 = xm1_mode(s);
+  if (s->xm1) {
+    for (pcal::DevBuf* d : {&s->m1, &s->wmat, &s->cmat, &s->c2m}) {
+      d->alloc((size_t)pp * pp);
+      d->zero(st);
+    }
+    s->kk.alloc(2);
+    s->kk.zero(st);
+    PCAL_CUDA(cudaMalloc(&s->kfb, sizeof(int32_t)));
+    PCAL_CUDA(cudaMemsetAsync(s->kfb, 0, sizeof(int32_t), st));
+    if (const char* gr = getenv("PCAL_XM1_GATE")) s->xm1_gate = atof(gr);
+  }
   // partial arrays: row-block granularities
   const int64_t wm_grad = dense_family(s->model.kind) ? cfg_info(pick_size(pp)).WM : 0;
   const int64_t wm_xm = xm_row_block(s);
@@ -1526,6 +1615,7 @@ static void alloc_state(pcal_session* s) {
   s->dpart.zero(st);
   s->cp_blocks = (int)std::min<int64_t>(ceil_div(p * p, kStreamThreads), 256);
   s->cpart.alloc(s->cp_blocks);
+  if (s->xm1) s->kcp.alloc((size_t)3 * s->cp_blocks);
   s->bb_blocks = 4 * num_sms(s->device);
   {
     int per_sm = 0;
@@ -1742,6 +1832,7 @@ pcal_session::~pcal_session() {
     if (e) cudaEventDestroy(e);
   if (bad) cudaFree(bad);
   if (sfb) cudaFree(sfb);
+  if (kfb) cudaFree(kfb);
   if (rank_nch_d) cudaFree(rank_nch_d);
   if (ctl) cudaFree(ctl);
   if (h_ctl) cudaFreeHost(h_ctl);
@@ -2413,6 +2504,20 @@ int pcal_session_profile(pcal_session* s, int64_t iters, double* ms_out) {
   });
 }
 int64_t pcal_session_kernels_per_iteration(pcal_session* s) { return s ? s->kernels_per_iter : 0; }
+
+int pcal_session_xm_mode(pcal_session* s, int64_t* fallbacks) {
+  if (!s) return 0;
+  if (fallbacks) {
+    *fallbacks = 0;
+    if (s->xm1) {
+      double v[2] = {0, 0};
+      if (cudaSetDevice(s->device) == cudaSuccess && cudaStreamSynchronize(s->stream) == cudaSuccess &&
+          cudaMemcpy(v, s->kk.p, sizeof v, cudaMemcpyDeviceToHost) == cudaSuccess)
+        *fallbacks = (int64_t)v[1];
+    }
+  }
+  return s->xm1 ? 1 : 0;
+}
 
 int pcal_session_set_state(pcal_session* s, const double* x_prev, const double* x, int64_t k,
                            double eta_prev) {

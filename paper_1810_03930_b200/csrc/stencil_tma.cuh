@@ -57,10 +57,10 @@ __global__ void __launch_bounds__(32 * (TY + 1))
   if (threadIdx.x == 0) {
     for (int i = 0; i < NS; ++i) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(
-          (unsigned)__cvta_generic_to_shared(&full[i])));
+          (unsigned)__cvta_generic_to_shared(&full[i])) : "memory");
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(
                        (unsigned)__cvta_generic_to_shared(&empty[i])),
-                   "r"(TY));
+                   "r"(TY) : "memory");
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -70,7 +70,8 @@ __global__ void __launch_bounds__(32 * (TY + 1))
     asm volatile(
         "{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
         "@!p bra W_%=;\n}\n" ::"r"(bar_addr(b)),
-        "r"(par));
+        "r"(par)
+        : "memory");  // the slot's shared-memory reads must not move above the wait
   };
   if (warp == TY) {  // ---- producer: one lane drives the TMA unit
     if (lane != 0) return;
@@ -141,11 +142,13 @@ __global__ void __launch_bounds__(32 * (TY + 1))
   const int own = (ty + 1) * W + XP * ln;  // this lane's points in an X slot
   const int lsrc = ln == 0 ? L - 1 : ln - 1, rsrc = ln == L - 1 ? 0 : ln + 1;
   double below[XP], cur[XP], above[XP];
+  // A slot is released only after the values read from it have been consumed
+  // by the plane's arithmetic and stored: mbarrier.arrive does not wait for
+  // this warp's outstanding shared-memory loads, and a release straight after
+  // the loads let the producer's next TMA fill of the slot overtake them
+  // (observed: plane z0+3 read as plane z0−1 in a few rows at config 5).
   wait(&full[0], 0u);
   rd(xs + own, below);
-  __syncwarp();
-  if (lane == 0)
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar_addr(&empty[0])));
   wait(&full[1 % NS], (unsigned)(1 / NS) & 1u);
   rd(xs + (1 % NS) * XT + own, cur);
   double acc = 0.0;
@@ -181,13 +184,18 @@ __global__ void __launch_bounds__(32 * (TY + 1))
         if (KS) nonfinite |= !isfinite(gv[k]);
       }
     }
-    __syncwarp();  // every lane has read slot sc (plane z) for the last time
-    if (lane == 0)
-      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar_addr(&empty[sc])));
     if (act) {
       double2* gout = reinterpret_cast<double2*>(gj + (int64_t)z * nxy + (int64_t)y * nx + XP * ln);
 #pragma unroll
       for (int v = 0; v < V; ++v) gout[v] = make_double2(gv[2 * v], gv[2 * v + 1]);
+    }
+    // every lane has consumed what it read from slot sc (plane z) — and, at the
+    // first plane, from slot 0 (plane z0 − 1): the stores above depend on it
+    __syncwarp();
+    if (lane == 0) {
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar_addr(&empty[sc])) : "memory");
+      if (z == z0)
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar_addr(&empty[0])) : "memory");
     }
 #pragma unroll
     for (int k = 0; k < XP; ++k) {
@@ -217,7 +225,7 @@ __global__ void __launch_bounds__(32 * (TY + 1))
     const int il = z1 - z0 + 1;
     __syncwarp();
     if (lane == 0)
-      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar_addr(&empty[il % NS])));
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar_addr(&empty[il % NS])) : "memory");
   }
   if (__any_sync(0xffffffffu, nonfinite) && lane == 0) *bad = 1;
 }

@@ -203,6 +203,28 @@ def test_tma_stencil_is_bitwise_the_register_march(pcal, orc, kind, grid, p, mon
         assert rel(g1, g_ref) <= 1e-14
 
 
+def test_tma_stencil_slot_release_under_load(pcal, monkeypatch):
+    """Regression: the TMA stencil released its first ring slot (plane z0 − 1)
+    right after issuing the shared-memory loads, and under full load the next
+    TMA fill of that slot overtook them — a few rows of plane z0 took plane
+    z0 + 3's values (seen at config 5, p = 1024, a few rows per evaluation).
+    Slots are now released after the plane's arithmetic has consumed them.
+    A 128 × 128 × 16 grid with p = 512 (8192 blocks, the same XP = 4 kernel)
+    evaluated repeatedly must give the register march's G every time."""
+    grid, p = (128, 128, 16), 512
+    n = grid[0] * grid[1] * grid[2]
+    rng = np.random.default_rng(5)
+    v = rng.uniform(size=n)
+    x = np.asfortranarray(rng.standard_normal((n, p)))
+    m = pcal.StencilModel(grid, v, p, 13.0)
+    monkeypatch.setenv("PCAL_NO_TMA_STENCIL", "1")
+    f_ref, g_ref = pcal.evaluate(m, x)
+    monkeypatch.delenv("PCAL_NO_TMA_STENCIL")
+    for _ in range(8):  # the old release failed 2 of 3 runs of 4 evaluations
+        f, g = pcal.evaluate(m, x)
+        assert np.array_equal(g, g_ref)
+
+
 @pytest.mark.parametrize("case", ["stencil", "dense", "sharded", "gram"])
 def test_triangular_diagonal_tiles_are_bitwise(pcal, orc, case, monkeypatch):
     """The Gram's diagonal tiles compute only their upper-triangle sub-blocks

@@ -22,6 +22,8 @@ def short(name: str) -> str:
         return "gemm_xm_tmem<128x128,MC,XM>"
     if "gemm_xm_staged" in nm:
         return "gemm_xm_staged<128x64,MC,XM>"
+    if "gemm_xm1_staged" in nm:
+        return "gemm_xm1_staged<64x64,MC,XM>"
     if "k_stencil_tma" in nm:
         return "k_stencil_tma"
     m = re.search(r"gemm_(streamk|fixup|fixup_store)<GemmCfg<(\d+), (\d+), \d+, \d+, \d+, (\d)(?:, \d+)?>(?:, (\d))?(?:, (\d))?", nm)
@@ -39,7 +41,8 @@ def phase_of(s: str) -> str:
         return "gradient"
     if "KC,STORE" in s or s == "k_small_pxp":
         return "gram"
-    if "XM" in s or s in ("k_sum_rows", "k_finish_eval", "k_zero_i32", "k_colsum3"):
+    if "XM" in s or "MC,STORE" in s or s in ("k_sum_rows", "k_finish_eval", "k_zero_i32",
+                                               "k_colsum3", "k_kkt_corr", "k_kkt_gate"):
         return "xm"
     if s in ("k_bb_partials", "k_eta", "k_update", "k_normalize", "k_step_fused", "k_bb_cols",
              "k_bb_cols_sum", "k_colscale", "k_update_norm"):
@@ -118,7 +121,7 @@ def full(path: str, out, summary: dict):
         print(f"  dram read+write per launch: {(rb + wb) / 1e9:.4f} GB; "
               f"effective {(rb + wb) / t / 1e9:.1f} GB/s", file=out)
         ph = phase_of(name)
-        kern = ("streamk" in name or "xm_tmem" in name or "xm_staged" in name
+        kern = ("streamk" in name or "xm_tmem" in name or "xm_staged" in name or "xm1_staged" in name
                 or "stencil" in name)
         # per phase: the longest capture (the iteration's launch, not a smaller
         # set-up launch of the same kernel, e.g. the initial point's Gram)

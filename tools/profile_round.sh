@@ -18,7 +18,7 @@ for c in ${CONFIGS:-2 3 4}; do
       -o $OUT/full_c$c python bench.py $args > $OUT/ncu_full_c$c.log 2>&1
   python tools/ncu_summary.py --launches $OUT/launches_c$c.csv --full $OUT/full_c$c.ncu-rep \
       --config $c --tag $TAG --kpi $kpi --outdir $OUT > /dev/null 2>&1
-  for k in gemm_xm_staged "gemm_streamk<pcal::GemmCfg<(int)128, (int)128, (int)2, (int)4, (int)3, (int)1" k_stencil_tma gemm_streamk; do
+  for k in gemm_xm1_staged gemm_xm_staged "gemm_streamk<pcal::GemmCfg<(int)128, (int)128, (int)2, (int)4, (int)3, (int)1" k_stencil_tma gemm_streamk; do
     python tools/ncu_stalls.py $OUT/full_c$c.ncu-rep "$k" 20 > "$OUT/stalls_c${c}_$(echo $k | tr -c 'a-z0-9_' '_' | cut -c1-40).txt" 2>&1
   done
   rm -f $OUT/full_c$c.ncu-rep
