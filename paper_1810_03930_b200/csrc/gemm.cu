@@ -169,17 +169,12 @@ void plan_gemm(GemmPlan& pl, int device, int size, int amode, int epi, int64_t M
   // waits on another's extra full tiles; explicit range starts replace ⌊c·U/G⌋
   std::vector<int64_t> cta_begin;
   if (segs == 0 && upc == 0 && any_tri) {
-    // Compute cost: 17 of 32 DMMAs and a few more fragment loads (0.56).  A
-    // triangular tile still streams the full A and B panels, so when most
-    // CTAs sit on triangular tiles at once (config 3: 4 of 6 tiles) HBM caps
-    // their speed-up; measured best costs (tools/kernel_times.py with
-    // PCAL_TRI_COST): 0.56 at 22 % / 40 % triangular tiles (configs 5 / 4),
-    // 0.85 at 67 % (config 3).
-    int ntri = 0;
-    for (int t = 0; t < ntiles; ++t) ntri += tri[t];
-    const double kTriCost = getenv("PCAL_TRI_COST")   ? atof(getenv("PCAL_TRI_COST"))
-                            : 2 * ntri > ntiles        ? 0.85
-                                                       : 0.56;
+    // Cost of a triangular tile in units of a full one: 17 of 32 DMMAs, but
+    // the full A and B panels still stream in.  Measured best with the
+    // partially unrolled triangular k-loop (tools/kernel_times.py,
+    // PCAL_TRI_COST sweep 0.5 … 0.9): 0.6 for configs 3 (67 % triangular
+    // tiles), 4 (40 %) and 5 (22 %).
+    const double kTriCost = getenv("PCAL_TRI_COST") ? atof(getenv("PCAL_TRI_COST")) : 0.6;
     std::vector<double> cum(ntiles + 1, 0.0);
     for (int t = 0; t < ntiles; ++t) cum[t + 1] = cum[t] + (tri[t] ? kTriCost : 1.0) * ki;
     cta_begin.assign(grid + 1, units);

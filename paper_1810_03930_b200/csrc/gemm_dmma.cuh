@@ -167,6 +167,10 @@ __device__ __forceinline__ void mma_stage(const char* As, const char* Bs, int wm
 // layout (frag_index of its owner in the full schedule), so partial tiles go
 // through the same fixup / tree reductions.  Same k order as mma_stage: the
 // computed elements are bitwise those of the full tile.
+#ifndef PCAL_TRI_UNROLL
+#define PCAL_TRI_UNROLL 2
+#endif
+constexpr int kTriUnroll = PCAL_TRI_UNROLL;
 template <class Cfg, int W>
 __device__ __forceinline__ void mma_stage_tri_w(const char* As, const char* Bs, int lane,
                                                 double (&acc)[Cfg::MT][Cfg::NT][2]) {
@@ -176,7 +180,9 @@ __device__ __forceinline__ void mma_stage_tri_w(const char* As, const char* Bs, 
   constexpr int R1 = W, R2 = 15 - W;
   const int r = lane >> 2, q = lane & 3;
   const int kq = kq_of(q);
-#pragma unroll
+  // partially unrolled: eight specialised warp bodies fully unrolled over the
+  // k-steps overflow the instruction cache (stall_no_inst at config 3)
+#pragma unroll kTriUnroll
   for (int st = 0; st < Cfg::BK / 4; ++st) {
     const int box = st >> 2;
     const int kl = kq ^ ((st & 1) | ((st & 2) << 1));
