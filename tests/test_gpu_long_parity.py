@@ -191,6 +191,12 @@ def test_grid_configs_end_of_run(pcal, orc, name):
             pytest.skip(f"{name}: f differs by {abs(got - ref) / abs(ref):.2e} relative; the "
                         f"ulp ensemble that bounds it has {k} members so far")
         assert abs(got - ref) <= tol, (which, got, ref, tol)
+    # final KKT and pre-orth feasibility inside twice the ensemble's spread
+    fp = rep.final_pre_orth
+    for col, got in ((1, fp.kkt_abs), (3, fp.feas)):
+        ref = g[f"{name}_final_pre"][col]
+        spread = max(abs(g[f"{name}_ens{q}_final_pre"][col] - ref) for q in range(k))
+        assert abs(got - ref) <= 2.0 * spread, (col, got, ref, spread)
 
 
 # --------------------------------------------------------------------------- #
