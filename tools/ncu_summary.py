@@ -130,6 +130,39 @@ def full(path: str, out, summary: dict):
                 summary[ph] = (rb + wb, t)
 
 
+def app_csv(path: str, out, summary: dict):
+    """`ncu --replay-mode application --csv` output (one row per launch and
+    metric): config 5's 64 GiB working set defeats kernel replay."""
+    rows = [r for r in csv.reader(open(path)) if r]
+    hdr = next(i for i, r in enumerate(rows) if "Kernel Name" in r and "Metric Name" in r)
+    h = rows[hdr]
+    ii, ki, mi, ui, vi = (h.index(k) for k in ("ID", "Kernel Name", "Metric Name", "Metric Unit",
+                                                "Metric Value"))
+    launches = {}
+    for r in rows[hdr + 1:]:
+        if len(r) <= vi:
+            continue
+        d = launches.setdefault(r[ii], {"name": r[ki]})
+        d[r[mi]] = to_base(r[vi], r[ui]) if r[ui] not in ("%", "") else float(r[vi].replace(",", ""))
+    print(f"# ncu --replay-mode application --clock-control none ({os.path.basename(path)})",
+          file=out)
+    for lid in sorted(launches, key=int):
+        d = launches[lid]
+        name = short(d["name"])
+        t = d.get("gpu__time_duration.sum", float("nan"))
+        rb, wb = d.get("dram__bytes_read.sum", 0.0), d.get("dram__bytes_write.sum", 0.0)
+        pipe = d.get("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", float("nan"))
+        print(f"{lid:>4s} {name:45s} {t * 1e3:10.3f} ms  DRAM {(rb + wb) / 1e9:8.3f} GB "
+              f"({(rb + wb) / t / 1e9 if t == t and t > 0 else 0:7.1f} GB/s)  tensor pipe {pipe:5.1f} %",
+              file=out)
+        ph = phase_of(name)
+        kern = ("streamk" in d["name"] or "xm1_staged" in d["name"] or "xm_staged" in d["name"]
+                or "stencil" in d["name"])
+        if kern and ph in ("gradient", "gram", "xm") and t == t:
+            if ph not in summary or t > summary[ph][1]:
+                summary[ph] = (rb + wb, t)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--launches")
@@ -139,18 +172,22 @@ def main():
     ap.add_argument("--kpi", type=int, default=19, help="kernels per iteration graph")
     ap.add_argument("--outdir", default=os.path.join(ROOT, "profiles"),
                     help="where the summaries go (on a GPU box: under gpurun_out/)")
+    ap.add_argument("--app-csv", help="application-replay CSV (config 5)")
     a = ap.parse_args()
     prof = a.outdir
     os.makedirs(prof, exist_ok=True)
     if a.launches:
         with open(os.path.join(prof, f"{a.tag}_cfg{a.config}_launches.txt"), "w") as f:
             launches(a.launches, f, a.kpi)
-    if a.full:
+    if a.full or a.app_csv:
         summ = {}
         with open(os.path.join(prof, f"{a.tag}_cfg{a.config}_full.txt"), "w") as f:
-            full(a.full, f, summ)
+            if a.full:
+                full(a.full, f, summ)
+            else:
+                app_csv(a.app_csv, f, summ)
         with open(os.path.join(prof, f"ncu_cfg{a.config}_summary.json"), "w") as f:
-            json.dump({"source": os.path.basename(a.full), "tag": a.tag,
+            json.dump({"source": os.path.basename(a.full or a.app_csv), "tag": a.tag,
                        "dram_bytes_per_launch": {k: v[0] for k, v in summ.items()},
                        "duration_s_per_launch": {k: v[1] for k, v in summ.items()}},
                       f, indent=1)
