@@ -168,13 +168,39 @@ void plan_gemm(GemmPlan& pl, int device, int size, int amode, int epi, int64_t M
   // one): the CTA ranges split the WEIGHTED unit sequence evenly, so no CTA
   // waits on another's extra full tiles; explicit range starts replace ⌊c·U/G⌋
   std::vector<int64_t> cta_begin;
+  // Cost of a triangular tile in units of a full one: 17 of 32 DMMAs, but
+  // the full A and B panels still stream in.  Measured best with the
+  // partially unrolled triangular k-loop (tools/kernel_times.py,
+  // PCAL_TRI_COST sweep 0.5 … 0.9): 0.6 for configs 3 (67 % triangular
+  // tiles), 4 (40 %) and 5 (22 %).
+  const double kTriCost = getenv("PCAL_TRI_COST") ? atof(getenv("PCAL_TRI_COST")) : 0.6;
+  if (segs > 0 && any_tri && (int64_t)grid < (int64_t)ntiles * segs) {
+    // persistent CTAs over whole fixed segments (reproducible schedules): runs
+    // of equal WEIGHT, not equal count — with equal counts the CTAs on
+    // triangular tiles idle while the others finish (config 5 sharded: +10 %).
+    // Which CTA computes a segment never changes its value.
+    const int64_t nseg = (int64_t)ntiles * segs;
+    std::vector<double> cum(nseg + 1, 0.0);
+    for (int64_t sg = 0; sg < nseg; ++sg)
+      cum[sg + 1] = cum[sg] + (tri[sg / segs] ? kTriCost : 1.0);
+    cta_begin.assign(grid + 1, units);
+    cta_begin[0] = 0;
+    int64_t sg = 0;
+    for (int c = 1; c < grid; ++c) {
+      const double target = cum[nseg] * c / grid;
+      while (sg < nseg && cum[sg + 1] <= target) ++sg;
+      // the segment containing the target goes to whichever side holds more of it
+      int64_t b = sg;
+      if (sg < nseg && target - cum[sg] > 0.5 * (cum[sg + 1] - cum[sg])) b = sg + 1;
+      cta_begin[c] = b >= nseg ? units : (b / segs) * ki + (b % segs) * ki / segs;
+    }
+    for (int c = 0; c < grid; ++c)
+      if (cta_begin[c + 1] <= cta_begin[c]) {
+        cta_begin.clear();
+        break;
+      }
+  }
   if (segs == 0 && upc == 0 && any_tri) {
-    // Cost of a triangular tile in units of a full one: 17 of 32 DMMAs, but
-    // the full A and B panels still stream in.  Measured best with the
-    // partially unrolled triangular k-loop (tools/kernel_times.py,
-    // PCAL_TRI_COST sweep 0.5 … 0.9): 0.6 for configs 3 (67 % triangular
-    // tiles), 4 (40 %) and 5 (22 %).
-    const double kTriCost = getenv("PCAL_TRI_COST") ? atof(getenv("PCAL_TRI_COST")) : 0.6;
     std::vector<double> cum(ntiles + 1, 0.0);
     for (int t = 0; t < ntiles; ++t) cum[t + 1] = cum[t] + (tri[t] ? kTriCost : 1.0) * ki;
     cta_begin.assign(grid + 1, units);

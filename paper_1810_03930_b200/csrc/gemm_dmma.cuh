@@ -487,12 +487,13 @@ __global__ void __launch_bounds__(Cfg::THREADS + 128, 1)
   uint64_t* empty = full + Cfg::STAGES;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int32_t cta = blockIdx.x;
-  const int64_t u0 = g.segs ? seg_unit_begin(cta, g.ntiles, g.ki, g.segs, g.grid)
-                            : g.cta_begin ? g.cta_begin[cta]
-                                          : cta_unit_begin(cta, g.units, g.grid, g.upc);
-  const int64_t u1 = g.segs ? seg_unit_begin(cta + 1, g.ntiles, g.ki, g.segs, g.grid)
-                            : g.cta_begin ? g.cta_begin[cta + 1]
-                                          : cta_unit_begin(cta + 1, g.units, g.grid, g.upc);
+  // explicit (weighted) CTA ranges first: whole segments in segmented mode
+  const int64_t u0 = g.cta_begin ? g.cta_begin[cta]
+                     : g.segs    ? seg_unit_begin(cta, g.ntiles, g.ki, g.segs, g.grid)
+                                 : cta_unit_begin(cta, g.units, g.grid, g.upc);
+  const int64_t u1 = g.cta_begin ? g.cta_begin[cta + 1]
+                     : g.segs    ? seg_unit_begin(cta + 1, g.ntiles, g.ki, g.segs, g.grid)
+                                 : cta_unit_begin(cta + 1, g.units, g.grid, g.upc);
   if (u0 >= u1) return;
   if (threadIdx.x == 0) {
     for (int s = 0; s < Cfg::STAGES; ++s) {

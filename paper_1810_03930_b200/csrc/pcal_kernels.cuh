@@ -536,9 +536,11 @@ struct ChunkColArgs {
   double* out;
   int64_t p;
   int64_t nch;        // local chunks
+  const int32_t* gate;  // non-null: run only when *gate != 0
 };
 __global__ void __launch_bounds__(128) k_chunk_colsum3(ChunkColArgs a, const Ctl* ctl) {
   if (ctl && ctl->done) return;
+  if (a.gate && !*a.gate) return;
   const int which = blockIdx.y;
   const int64_t col = blockIdx.x;
   const double* src = a.in[which] ? a.in[which] + col * a.stride[which] : nullptr;

@@ -998,50 +998,59 @@ static void launch_eval(pcal_session* s, int b, int mode, const Ctl* ctl_guard) 
   }
   mark(s, 3);
   launch_gemm(s->xm[b], st);
+  // column sums of the f / kkt² (XM1: P²) / d partials; `gate` non-null: the
+  // gated recomputation after the XM1 fallback (collectives still run, so every
+  // rank issues the same sequence; the gated kernels keep the previous values)
+  auto colsums = [&](const int32_t* gate) {
+    if (s->repro) {  // C2: per-chunk column sums, gathered and summed in chunk order
+      const bool dform =
+          s->alg == PCAL_ALG_PCAL && s->cfg.multiplier_rule == PCAL_MULT_PCAL_FORMULA;
+      const int64_t wm_xm = cfg_info(pick_size(2 * s->pp)).WM;
+      ChunkColArgs a{};
+      a.in[0] = s->fpart.p;
+      a.nrows[0] = s->nrb_f;
+      a.stride[0] = s->pstride_f;
+      a.rpc[0] = dense_family(s->model.kind) ? s->chunk_rows / cfg_info(pick_size(s->pp)).WM
+                                             : s->model.ny / 8;
+      a.in[1] = s->kpart.p;
+      const bool alm = s->alg == PCAL_ALG_ALM;
+      a.in[2] = (dform || alm) ? s->dpart.p : nullptr;
+      for (int w = 1; w < 3; ++w) {
+        a.nrows[w] = s->nrb_xm;
+        a.stride[w] = s->pstride_xm;
+        a.rpc[w] = s->chunk_rows / wm_xm;
+      }
+      a.out = s->cc.p;
+      a.p = s->p;
+      a.nch = s->nch;
+      a.gate = gate;
+      k_chunk_colsum3<<<dim3((unsigned)s->p, 3), 128, 0, st>>>(a, ctl_guard);
+      launched("k_chunk_colsum3");
+      // + the ranks' failure flags in the same all-gather, so every rank stops
+      // together (exact counts)
+      if (!gate) {
+        k_flags<<<1, 1, 0, st>>>(s->ctl, s->bad, s->cc.p + s->nch_max * 3 * s->p);
+        launched("k_flags");
+      }
+      chunk_reduce(s, s->cc.p, 3 * s->p, s->fkd[b].p, ctl_guard, 2);
+      if (alm) {
+        k_alm_split<<<1, 256, 0, st>>>(Dvec(s, b), s->glcol.p, s->p, ctl_guard);
+        launched("k_alm_split");
+      }
+    } else {
+      launch_colsums(s, s->fpart.p, s->nrb_f, s->kpart.p, s->dpart.p,
+                     s->xm1 && !gate ? ceil_div(s->n, (int64_t)cfg_info(CFG_XM1).BM) : s->nrb_xm,
+                     Fcol(s, b), Kcol(s, b), Dvec(s, b), ctl_guard, gate);
+    }
+  };
+  colsums(nullptr);
   if (s->xm1) {
-    launch_colsums(s, s->fpart.p, s->nrb_f, s->kpart.p, s->dpart.p, s->nrb_xm, Fcol(s, b),
-                   Kcol(s, b), Dvec(s, b), ctl_guard);
     k_kkt_gate<<<1, 256, 0, st>>>(s->kcp.p, s->cp_blocks, Kcol(s, b), s->p, s->beta, s->xm1_gate,
                                   s->kfb, s->kk.p, ctl_guard);
     launched("k_kkt_gate");
     // the identity cancelled too much: kkt = P − X·(βC) directly (gated: no-ops otherwise)
     launch_gemm(s->xmfb[b], st);
-    launch_colsums(s, nullptr, 0, s->kpart.p, s->dpart.p, s->nrb_xm, nullptr, Kcol(s, b),
-                   Dvec(s, b), ctl_guard, s->kfb);
-  } else if (s->repro) {  // C2: per-chunk column sums, gathered and summed in chunk order
-    const bool dform = s->alg == PCAL_ALG_PCAL && s->cfg.multiplier_rule == PCAL_MULT_PCAL_FORMULA;
-    const int64_t wm_xm = cfg_info(pick_size(2 * s->pp)).WM;
-    ChunkColArgs a{};
-    a.in[0] = s->fpart.p;
-    a.nrows[0] = s->nrb_f;
-    a.stride[0] = s->pstride_f;
-    a.rpc[0] = dense_family(s->model.kind) ? s->chunk_rows / cfg_info(pick_size(s->pp)).WM
-                                                 : s->model.ny / 8;
-    a.in[1] = s->kpart.p;
-    const bool alm = s->alg == PCAL_ALG_ALM;
-    a.in[2] = (dform || alm) ? s->dpart.p : nullptr;
-    for (int w = 1; w < 3; ++w) {
-      a.nrows[w] = s->nrb_xm;
-      a.stride[w] = s->pstride_xm;
-      a.rpc[w] = s->chunk_rows / wm_xm;
-    }
-    a.out = s->cc.p;
-    a.p = s->p;
-    a.nch = s->nch;
-    k_chunk_colsum3<<<dim3((unsigned)s->p, 3), 128, 0, st>>>(a, ctl_guard);
-    launched("k_chunk_colsum3");
-    // + the ranks' failure flags in the same all-gather, so every rank stops
-    // together (exact counts)
-    k_flags<<<1, 1, 0, st>>>(s->ctl, s->bad, s->cc.p + s->nch_max * 3 * s->p);
-    launched("k_flags");
-    chunk_reduce(s, s->cc.p, 3 * s->p, s->fkd[b].p, ctl_guard, 2);
-    if (alm) {
-      k_alm_split<<<1, 256, 0, st>>>(Dvec(s, b), s->glcol.p, s->p, ctl_guard);
-      launched("k_alm_split");
-    }
-  } else {
-    launch_colsums(s, s->fpart.p, s->nrb_f, s->kpart.p, s->dpart.p, s->nrb_xm, Fcol(s, b),
-                   Kcol(s, b), Dvec(s, b), ctl_guard);
+    colsums(s->kfb);
   }
   FinishArgs fa{};
   fa.fcol = Fcol(s, b);
@@ -1244,14 +1253,13 @@ static void launch_iteration(pcal_session* s, int b) {
 // XM1 (P = G − X·M1, half the flops): PCAL / PLAM on one GPU with p ≥ 128;
 // PCAL_XM_TWO_BLOCK=1 keeps the X·[W|C] product.
 static bool xm1_mode(const pcal_session* s) {
-  return (s->alg == PCAL_ALG_PCAL || s->alg == PCAL_ALG_PLAM) && !s->repro && !s->comm &&
-         pick_size(s->pp) == CFG_BIG && !getenv("PCAL_XM_TWO_BLOCK") &&
-         !getenv("PCAL_NO_TMEM_EPI") && !getenv("PCAL_XM_TMEM");
+  return (s->alg == PCAL_ALG_PCAL || s->alg == PCAL_ALG_PLAM) && pick_size(s->pp) == CFG_BIG &&
+         !getenv("PCAL_XM_TWO_BLOCK") && !getenv("PCAL_NO_TMEM_EPI") && !getenv("PCAL_XM_TMEM");
 }
 static int xm_config(const pcal_session* s) {
   const int xsz = pick_size(2 * s->pp);
+  if (xm1_mode(s)) return CFG_XM1;  // whole 64-row tiles: reproducible as well
   if (xsz != CFG_BIG || s->repro || getenv("PCAL_NO_TMEM_EPI")) return xsz;
-  if (xm1_mode(s)) return CFG_XM1;
   return getenv("PCAL_XM_TMEM") ? (int)CFG_XMT : (int)CFG_XMS;
 }
 static int64_t xm_row_block(const pcal_session* s) {
@@ -1379,7 +1387,8 @@ static void build_plans(pcal_session* s) {
       e.p = s->p;
       g.args.ctl = s->ctl;
       GemmPlan& f = s->xmfb[b];
-      plan_gemm(f, dev, CFG_BIG, A_MCONTIG, EPI_XM, n, 2 * pp, pp);
+      plan_gemm(f, dev, CFG_BIG, A_MCONTIG, EPI_XM, n, 2 * pp, pp, -1, 0,
+                s->repro ? 1 : 0);  // reproducible: whole tiles, no K split
       f.args.A = Xof(s, b);
       f.args.lda = ld;
       f.args.B = s->mcat.p;

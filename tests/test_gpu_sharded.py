@@ -209,3 +209,36 @@ def test_run_scaling_nccl_process_per_gpu(pcal, orc):
     assert rep.identical_results and not rep.hardware_oversubscribed
     em = pcal.solve_emulated(m, cfg, x0, 1)
     assert report_io.same_numerics(rep.runs[0], em)
+
+
+@pytest.mark.parametrize("kind", ["dense", "stencil"])
+def test_sharded_single_block_xm_bitwise_across_gpu_counts(pcal, orc, kind, monkeypatch):
+    """X·M1 (p > 96) on the sharded path: P and the d / P² partials are row
+    local (64-row tiles inside the fixed chunks), the kkt identity's p × p
+    terms are replicated and the gate is taken from allreduced sums, so 1…4
+    ranks stay bitwise identical — also with the gated two-block fallback
+    forced on every evaluation (PCAL_XM1_GATE=0), which re-reduces the kkt
+    sums collectively; both agree with the single-GPU solve and with the
+    two-block product to the trace contract."""
+    from paper_1810_03930_b200 import report_io
+    if kind == "dense":
+        n, p = 2000, 128
+        m = pcal.QuadraticModel(pcal.gen_dense_operator(n, 2), p, 70.0)
+    else:
+        grid, p = (16, 16, 16), 128
+        n = 16 ** 3
+        v = orc.random_uniform(n, 3)
+        m = pcal.StencilModel(grid, v, p, 12.0 + v.max())
+    x0 = orc.initial_point_qr(n, p, 13)
+    cfg = pcal.SolverConfig(tol_rel_kkt=TINY, max_iter=30)
+    reps = [pcal.solve_emulated(m, cfg, x0, R) for R in (1, 2, 3, 4)]
+    for r in reps[1:]:
+        assert report_io.same_numerics(reps[0], r)
+    check_pair(pcal.solve(m, cfg, x0), reps[0], window=30)
+    monkeypatch.setenv("PCAL_XM1_GATE", "0")
+    fb = [pcal.solve_emulated(m, cfg, x0, R) for R in (1, 3)]
+    assert report_io.same_numerics(fb[0], fb[1])
+    check_pair(reps[0], fb[0], window=30)
+    monkeypatch.delenv("PCAL_XM1_GATE")
+    monkeypatch.setenv("PCAL_XM_TWO_BLOCK", "1")
+    check_pair(pcal.solve_emulated(m, cfg, x0, 2), reps[0], window=30)
