@@ -435,7 +435,8 @@ __global__ void __launch_bounds__(kStreamThreads)
     k_update_norm(const double* __restrict__ x, const double* __restrict__ pg,
                   const double* __restrict__ d, double* __restrict__ z, int64_t n, int64_t ld,
                   int64_t p, int64_t chunk, double* __restrict__ npart,
-                  const double* __restrict__ inv, const int32_t* __restrict__ fb, Ctl* ctl) {
+                  const double* __restrict__ inv, const int32_t* __restrict__ fb, Ctl* ctl,
+                  double* __restrict__ xpart = nullptr, int64_t cstride = 0) {
   if (ctl->done) return;
   __shared__ double sm[kStreamThreads / 32];
   const int64_t j = blockIdx.y;
@@ -448,7 +449,7 @@ __global__ void __launch_bounds__(kStreamThreads)
   const double2* xj = reinterpret_cast<const double2*>(x + j * ld);
   const double2* pj = reinterpret_cast<const double2*>(pg + j * ld);
   double2* zj = reinterpret_cast<double2*>(z + j * ld);
-  double acc = 0.0;
+  double acc = 0.0, xacc = 0.0;
   bool bad = false;
   const int64_t h0 = r0 / 2, h1 = (r1 + 1) / 2;  // an odd n ends on a zero padding row
   for (int64_t h = h0 + threadIdx.x; h < h1; h += blockDim.x) {
@@ -457,15 +458,22 @@ __global__ void __launch_bounds__(kStreamThreads)
     const double v1 = xv.y - inv_eta * (pv.y - dj * xv.y);
     acc += v0 * v0;
     acc += v1 * v1;
+    xacc += xv.x * xv.x;
+    xacc += xv.y * xv.y;
     const double w0 = v0 * sc, w1 = v1 * sc;
     zj[h] = make_double2(w0, w1);
     bad |= !isfinite(w0) || !isfinite(w1);
   }
+  const int64_t cs = cstride ? cstride : p;  // row stride of the chunk-partial arrays
   const double s = block_sum<kStreamThreads>(acc, sm);
-  if (threadIdx.x == 0) npart[blockIdx.x * p + j] = s;
+  if (threadIdx.x == 0) npart[blockIdx.x * cs + j] = s;
+  if (xpart) {  // sharded: ‖x_j‖² partials for the degenerate-column rule
+    const double t = block_sum<kStreamThreads>(xacc, sm);
+    if (threadIdx.x == 0) xpart[blockIdx.x * cs + j] = t;
+  }
   if (!exact && __syncthreads_or(bad) && threadIdx.x == 0) {
     ctl->step_bad = 1;
-    ctl->done = 2;
+    if (!xpart) ctl->done = 2;  // sharded (xpart given): decided collectively in k_finish_eval
   }
 }
 

@@ -1163,6 +1163,35 @@ static void launch_iteration(pcal_session* s, int b) {
     lc.numAttrs = 1;
     PCAL_CUDA(cudaLaunchKernelExC(&lc, (const void*)k_step_fused, args));
     launched("k_step_fused");
+  } else if (s->repro && !plain && !getenv("PCAL_TWO_PASS_NORMALIZE")) {
+    // C3 + C4 of the one-pass normalised step: the per-chunk stepsize AND
+    // column-norm expansion sums (a, b, c) in one all-gather; flagged columns
+    // take the exact rule with their chunk-reduced ‖z_j‖² (a second, tiny
+    // all-gather that every rank issues every iteration)
+    const unsigned nc = (unsigned)s->nch;
+    dim3 gu(nc, (unsigned)s->p);
+    k_bb_cols<<<gu, kStreamThreads, 0, st>>>(Xof(s, b), Pof(s, b), Xof(s, nb), Pof(s, nb),
+                                             Dvec(s, b), Dvec(s, nb), s->n, s->ld, s->p,
+                                             s->chunk_rows, s->colpart.p, s->ctl);
+    launched("k_bb_cols");
+    chunk_reduce(s, s->colpart.p, 6 * s->p, s->bbt.p, s->ctl);  // [j·6 + q], chunk order
+    k_bb_cols_sum<<<1, kStreamThreads, 0, st>>>(s->bbt.p, s->p, s->bbpart.p, s->ctl);
+    launched("k_bb_cols_sum");
+    k_eta<<<1, kStreamThreads, 0, st>>>(s->ctl, s->bbpart.p, 1);
+    launched("k_eta");
+    k_colscale<<<(unsigned)ceil_div(s->p, 128), 128, 0, st>>>(s->bbt.p, 1, s->p, s->sinv.p,
+                                                              s->sfb, s->ctl);
+    launched("k_colscale");
+    k_update_norm<<<gu, kStreamThreads, 0, st>>>(Xof(s, b), Pof(s, b), Dvec(s, b), Xof(s, nb),
+                                                 s->n, s->ld, s->p, s->chunk_rows, s->cc.p,
+                                                 s->sinv.p, s->sfb, s->ctl, s->cc.p + s->p,
+                                                 2 * s->p);
+    launched("k_update_norm");
+    chunk_reduce(s, s->cc.p, 2 * s->p, s->nrm.p, s->ctl);
+    k_normalize<<<gu, kStreamThreads, 0, st>>>(Xof(s, b), Xof(s, nb), s->n, s->ld, s->p,
+                                               s->chunk_rows, s->nch, s->cc.p, s->nrm.p, s->row0,
+                                               s->n_glob, plain, s->ctl, s->sfb);
+    launched("k_normalize");
   } else if (s->repro) {  // C3/C4 with chunked, rank-count invariant reductions
     const unsigned nc = (unsigned)s->nch;
     k_bb_chunk<<<dim3(nc, (unsigned)s->p), kStreamThreads, 0, st>>>(
@@ -1640,7 +1669,9 @@ static void alloc_state(pcal_session* s) {
   s->up_chunk = std::min<int64_t>(s->up_chunk, round_up(n, 256));
   if (s->repro) s->up_chunk = s->chunk_rows;  // norm partials per row chunk
   s->up_nchunks = ceil_div(n, s->up_chunk);
-  s->colpart.alloc((size_t)s->up_nchunks * p * 6);
+  // (sharded: the all-gathered per-chunk stepsize / norm sums, nch_max rows)
+  s->colpart.alloc((size_t)std::max<int64_t>(s->up_nchunks, s->nch_max) * p * 6);
+  s->colpart.zero(st);
   s->sinv.alloc((size_t)s->pp);
   PCAL_CUDA(cudaMalloc(&s->sfb, sizeof(int32_t) * s->pp));
   PCAL_CUDA(cudaMemsetAsync(s->sfb, 0, sizeof(int32_t) * s->pp, st));
@@ -1648,8 +1679,8 @@ static void alloc_state(pcal_session* s) {
     const int R = s->comm->size;
     s->cc.alloc((size_t)s->nch_max * 3 * p + 2);
     s->cc.zero(st);
-    s->ccg.alloc((size_t)R * (s->nch_max * 3 * p + 2));
-    s->bbt.alloc((size_t)3 * p);
+    s->ccg.alloc((size_t)R * (s->nch_max * 6 * p + 2));
+    s->bbt.alloc((size_t)6 * p);
     s->spt.alloc(3);
     s->spt.zero(st);
   }
