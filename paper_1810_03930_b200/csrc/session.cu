@@ -470,6 +470,7 @@ __global__ void __launch_bounds__(256) k_finish_eval(FinishArgs a, Ctl* ctl,
 
 }  // namespace pcal
 #include "small.cuh"
+#include "small_rows.cuh"
 namespace pcal {
 
 // check_finite (problems.cpp:27-30) of a caller-computed gradient.
@@ -592,6 +593,9 @@ struct pcal_session {
   int mega_grid = 0;
   int64_t mega_lda_s = 0;   // > 0: k_iter_small keeps each CTA's 8 rows of A in shared memory
   pcal::DevBuf at, mpart, mz, mnpb, mbb;  // Aᵀ, Z and the CTA partials of k_iter_small
+  bool rows = false;        // n ≤ 8·SMs: k_iter_rows (own rows in registers, 4 barriers)
+  int rows_nent = 0, rows_ngroups = 0, rows_csize = 1;
+  pcal::DevBuf rgpart, rgtot, rgcnt, rcpart;  // k_iter_rows partials / group sums / counters
   int64_t st_zchunk = 0, st_nzc = 0, st_zpart = 0;  // march z-chunk, count, planes per f partial
   // graphs
   cudaGraphExec_t graph[2] = {nullptr, nullptr};
@@ -1900,8 +1904,107 @@ int guarded(F&& f) {
   }
 }
 
+// k_iter_rows over `iters` iterations (cooperative, one CTA per 8 rows).
+static void launch_rows(pcal_session* s, int iters) {
+  RowsArgs a{};
+  for (int b = 0; b < 2; ++b) {
+    a.pair[b] = s->pair[b].p;
+    a.fkd[b] = s->fkd[b].p;
+  }
+  a.at = s->at.p;
+  a.ldat = s->ld;
+  a.g0 = s->g0.p;
+  a.lam = s->lam.p;
+  a.z = s->mz.p;
+  a.gpart = s->rgpart.p;
+  a.gtot = s->rgtot.p;
+  a.gcnt = reinterpret_cast<unsigned*>(s->rgcnt.p);
+  a.cpart = s->rcpart.p;
+  a.bbpart = s->mbb.p;
+  a.n = s->n;
+  a.ld = s->ld;
+  a.p = s->p;
+  a.pp = s->pp;
+  a.nent = s->rows_nent;
+  a.plain = !(s->alg == PCAL_ALG_PCAL || s->alg == PCAL_ALG_PCALDA);
+  const bool da = s->alg == PCAL_ALG_PLAMDA || s->alg == PCAL_ALG_PCALDA;
+  a.mc_mode = da ? MC_DA : MC_PCAL;
+  a.p_from_g = da;
+  a.dform = s->alg == PCAL_ALG_PCAL && s->cfg.multiplier_rule == PCAL_MULT_PCAL_FORMULA;
+  a.beta = s->beta;
+  a.beta_epi = da ? 1.0 : s->beta;
+  a.fa.model = s->model.kind;
+  a.fa.p = s->p;
+  a.fa.mode = 0;
+  a.fa.trace = s->trace.p;
+  a.fa.bad = s->bad;
+  a.fa.c_xc = s->c_xc;
+  Ctl* c = s->ctl;
+  void* args[] = {&a, &c, &iters};
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3((unsigned)s->mega_grid);
+  lc.blockDim = dim3(kRowsThreads);
+  a.zld = rows_zld(s->n);
+  lc.dynamicSmemBytes = rows_smem_bytes(s->p, a.zld);
+  lc.stream = s->stream;
+  cudaLaunchAttribute attr[2]{};
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = (unsigned)s->rows_csize;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  lc.attrs = attr;
+  lc.numAttrs = s->rows_csize > 1 ? 2 : 1;
+  a.csize = s->rows_csize;
+  // PCAL_SMALL_PROF=1: per-phase %globaltimer stamps of CTA 0, printed per batch
+  static const bool prof = getenv("PCAL_SMALL_PROF") && getenv("PCAL_SMALL_PROF")[0] == '1';
+  uint64_t* dprof = nullptr;
+  if (prof) {
+    PCAL_CUDA(cudaMalloc(&dprof, sizeof(uint64_t) * 16 * iters));
+    PCAL_CUDA(cudaMemsetAsync(dprof, 0, sizeof(uint64_t) * 16 * iters, s->stream));
+    a.prof = dprof;
+  }
+  PCAL_CUDA(cudaLaunchKernelExC(&lc, (const void*)k_iter_rows, args));
+  launched("k_iter_rows");
+  if (prof) {
+    std::vector<uint64_t> h((size_t)16 * iters);
+    PCAL_CUDA(cudaMemcpyAsync(h.data(), dprof, sizeof(uint64_t) * h.size(), cudaMemcpyDeviceToHost,
+                              s->stream));
+    PCAL_CUDA(cudaStreamSynchronize(s->stream));
+    double acc[16] = {};
+    int cnt = 0;
+    for (int it = 0; it + 1 < iters; ++it) {
+      const uint64_t* r = &h[(size_t)16 * it];
+      if (!r[4] || !h[(size_t)16 * (it + 1)]) break;
+      for (int q = 0; q < 4; ++q) acc[q] += (double)(r[q + 1] - r[q]);
+      acc[4] += (double)(h[(size_t)16 * (it + 1)] - r[4]);
+      acc[5] += (double)(r[6] - r[1]);  // phase 2: Y staged
+      acc[6] += (double)(r[7] - r[6]);  //          DMMA loop
+      acc[7] += (double)(r[5] - r[7]);  //          warp reduction
+      for (int q = 8; q <= 13; ++q) acc[q] += (double)(r[q] - r[q == 8 ? 2 : q == 11 ? 3 : q - 1]);
+      ++cnt;
+    }
+    if (cnt)
+      fprintf(stderr,
+              "k_iter_rows us/iter: 1 eta+Z %.2f  2 A.Z+Gram partials %.2f  3 P epilogue %.2f  "
+              "4 sums+record+bb %.2f  (loop %.2f)  [2: stage Y %.2f, DMMA %.2f, reduce %.2f] "
+              "grid %d cluster %d\n  3: totals %.2f WCM %.2f rows %.2f | 4: col totals %.2f "
+              "record %.2f bb %.2f\n",
+              acc[0] / cnt / 1e3, acc[1] / cnt / 1e3, acc[2] / cnt / 1e3, acc[3] / cnt / 1e3,
+              acc[4] / cnt / 1e3, acc[5] / cnt / 1e3, acc[6] / cnt / 1e3, acc[7] / cnt / 1e3,
+              s->mega_grid, s->rows_csize, acc[8] / cnt / 1e3, acc[9] / cnt / 1e3,
+              acc[10] / cnt / 1e3, acc[11] / cnt / 1e3, acc[12] / cnt / 1e3, acc[13] / cnt / 1e3);
+    cudaFree(dprof);
+  }
+}
+
 // k_iter_small over `iters` iterations (cooperative, one CTA per SM).
 static void launch_small(pcal_session* s, int iters) {
+  if (s->rows) {
+    launch_rows(s, iters);
+    return;
+  }
   SmallArgs a{};
   for (int b = 0; b < 2; ++b) {
     a.pair[b] = s->pair[b].p;
@@ -1989,7 +2092,79 @@ static void setup_small(pcal_session* s) {
     return;
   int coop = 0, per_sm = 0;
   PCAL_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, s->device));
-  s->mega_grid = num_sms(s->device);
+  const int nsm = num_sms(s->device);
+  {  // n ≤ 8·SMs (and ≤ 8·4·kRowsKS): one CTA per 8 rows, k_iter_rows
+    int64_t g = ceil_div(s->n, 8);
+    const char* v1 = getenv("PCAL_SMALL_V1");
+    const size_t smem = rows_smem_bytes(s->p, rows_zld(s->n));
+    cudaFuncAttributes fa{};
+    PCAL_CUDA(cudaFuncGetAttributes(&fa, k_iter_rows));
+    int optin = 0;
+    PCAL_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, s->device));
+    if (!(v1 && v1[0] == '1') && coop && g <= nsm && g <= kRowsMaxGrid &&
+        ceil_div(ceil_div(s->n, 4), 8) <= kRowsKS && smem + fa.sharedSizeBytes <= (size_t)optin) {
+      PCAL_CUDA(cudaFuncSetAttribute(k_iter_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+      PCAL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_iter_rows, kRowsThreads,
+                                                              smem));
+      // clusters of up to 8 CTAs share one L2 read of Y (multicast); the
+      // cluster size must divide the grid and every cluster must fit at once
+      // (measured at config 1: multicast saves 0.3 us of staging but the
+      // rounded-up grid costs as much in the totals; default off)
+      int cs = 1;
+      const char* ce = getenv("PCAL_ROWS_CLUSTER");
+      if (ce) cs = std::max(1, std::min(8, atoi(ce)));
+      int64_t gg = g;
+      for (; cs > 1; cs /= 2) {
+        gg = round_up(g, cs);
+        if (gg > nsm || gg > kRowsMaxGrid) continue;
+        cudaLaunchConfig_t lc{};
+        lc.gridDim = dim3((unsigned)gg);
+        lc.blockDim = dim3(kRowsThreads);
+        lc.dynamicSmemBytes = smem;
+        cudaLaunchAttribute at{};
+        at.id = cudaLaunchAttributeClusterDimension;
+        at.val.clusterDim.x = (unsigned)cs;
+        at.val.clusterDim.y = at.val.clusterDim.z = 1;
+        lc.attrs = &at;
+        lc.numAttrs = 1;
+        int ncl = 0;
+        if (cudaOccupancyMaxActiveClusters(&ncl, (const void*)k_iter_rows, &lc) == cudaSuccess &&
+            (int64_t)ncl * cs >= gg)
+          break;
+        cudaGetLastError();
+      }
+      if (cs <= 1) {
+        cs = 1;
+        gg = g;
+      }
+      if (per_sm >= 1) {
+        s->rows_csize = cs;
+        g = gg;
+        s->mega_grid = (int)g;
+        const int64_t p = s->p, np2 = p * (p + 1) / 2;
+        s->rows_nent = (int)(2 * np2 + (s->g0.p ? p * p : 0));
+        s->rows_ngroups = (int)ceil_div(g, kRowsGroup);
+        s->at.alloc((size_t)s->ld * s->n);
+        s->at.zero(s->stream);
+        dim3 tg((unsigned)ceil_div(s->n, 32), (unsigned)ceil_div(s->n, 32));
+        k_transpose<<<tg, dim3(32, 8), 0, s->stream>>>(s->A.p, s->ldA, s->n, s->at.p, s->ld);
+        launched("k_transpose");
+        s->rgpart.alloc((size_t)g * s->rows_nent);
+        s->rgtot.alloc((size_t)s->rows_ngroups * s->rows_nent);
+        s->rgcnt.alloc((size_t)s->rows_ngroups);
+        s->rgcnt.zero(s->stream);
+        s->rcpart.alloc((size_t)g * 2 * 32);
+        s->mbb.alloc((size_t)g * 3);
+        s->mz.alloc((size_t)s->ld * s->pp);
+        s->mz.zero(s->stream);
+        s->rows = true;
+        s->mega = true;
+        return;
+      }
+    }
+  }
+  s->mega_grid = nsm;
   // one 8-row gradient tile per CTA: keep those rows of A resident in shared
   // memory (row stride ≡ 4 mod 16 doubles: conflict-free DMMA fragment loads)
   const int64_t lda_s = round_up(s->n, 16) + 4;
