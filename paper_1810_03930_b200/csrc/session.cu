@@ -2539,7 +2539,31 @@ void session_finish(pcal_session* s, pcal_report* r) {
     r->final_pre[2] = c.rel;
     r->final_pre[3] = c.feas;
     r->has_x = 1;
-    if (r->stop_x) copy_out(s, Xof(s, b), r->stop_x);
+    cudaStream_t cs = nullptr;  // the stop iterate's D2H overlaps the final CholeskyQR2
+    if (r->stop_x) {
+      if (s->cfg.final_orth) {
+        cudaEvent_t ev;
+        PCAL_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        PCAL_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        PCAL_CUDA(cudaEventRecord(ev, s->stream));
+        PCAL_CUDA(cudaStreamWaitEvent(cs, ev, 0));
+        PCAL_CUDA(cudaEventDestroy(ev));
+        PCAL_CUDA(cudaMemcpy2DAsync(r->stop_x, sizeof(double) * s->n, Xof(s, b),
+                                    sizeof(double) * s->ld, sizeof(double) * s->n, s->p,
+                                    cudaMemcpyDeviceToHost, cs));
+      } else {
+        copy_out(s, Xof(s, b), r->stop_x);
+      }
+    }
+    struct StreamJoin {  // the side copy completes before the report is returned
+      cudaStream_t st;
+      ~StreamJoin() {
+        if (st) {
+          cudaStreamSynchronize(st);
+          cudaStreamDestroy(st);
+        }
+      }
+    } join{cs};
     bool final_is_q = false;  // final_x = Q after a successful final orthonormalization
     if (s->cfg.final_orth) {  // solver.cpp:445-459
       auto t0 = std::chrono::steady_clock::now();
