@@ -2539,31 +2539,32 @@ void session_finish(pcal_session* s, pcal_report* r) {
     r->final_pre[2] = c.rel;
     r->final_pre[3] = c.feas;
     r->has_x = 1;
-    cudaStream_t cs = nullptr;  // the stop iterate's D2H overlaps the final CholeskyQR2
-    if (r->stop_x) {
-      if (s->cfg.final_orth) {
-        cudaEvent_t ev;
-        PCAL_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-        PCAL_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-        PCAL_CUDA(cudaEventRecord(ev, s->stream));
-        PCAL_CUDA(cudaStreamWaitEvent(cs, ev, 0));
-        PCAL_CUDA(cudaEventDestroy(ev));
-        PCAL_CUDA(cudaMemcpy2DAsync(r->stop_x, sizeof(double) * s->n, Xof(s, b),
-                                    sizeof(double) * s->ld, sizeof(double) * s->n, s->p,
-                                    cudaMemcpyDeviceToHost, cs));
-      } else {
-        copy_out(s, Xof(s, b), r->stop_x);
-      }
-    }
-    struct StreamJoin {  // the side copy completes before the report is returned
-      cudaStream_t st;
+    // D2H on a side stream: the stop iterate under the final CholeskyQR2, Q
+    // under the post-orth evaluation (which only reads it)
+    cudaStream_t cs = nullptr;
+    auto side_copy = [&](const double* dsrc, double* host) {
+      cudaEvent_t ev;
+      if (!cs) PCAL_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+      PCAL_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      PCAL_CUDA(cudaEventRecord(ev, s->stream));
+      PCAL_CUDA(cudaStreamWaitEvent(cs, ev, 0));
+      PCAL_CUDA(cudaEventDestroy(ev));
+      PCAL_CUDA(cudaMemcpy2DAsync(host, sizeof(double) * s->n, dsrc, sizeof(double) * s->ld,
+                                  sizeof(double) * s->n, s->p, cudaMemcpyDeviceToHost, cs));
+    };
+    struct StreamJoin {  // the side copies complete before the report is returned
+      cudaStream_t* st;
       ~StreamJoin() {
-        if (st) {
-          cudaStreamSynchronize(st);
-          cudaStreamDestroy(st);
+        if (*st) {
+          cudaStreamSynchronize(*st);
+          cudaStreamDestroy(*st);
         }
       }
-    } join{cs};
+    } join{&cs};
+    if (r->stop_x) {
+      if (s->cfg.final_orth) side_copy(Xof(s, b), r->stop_x);
+      else copy_out(s, Xof(s, b), r->stop_x);
+    }
     bool final_is_q = false;  // final_x = Q after a successful final orthonormalization
     if (s->cfg.final_orth) {  // solver.cpp:445-459
       auto t0 = std::chrono::steady_clock::now();
@@ -2573,6 +2574,7 @@ void session_finish(pcal_session* s, pcal_report* r) {
         s->timers->orth +=
             std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
       if (ok) {
+        if (r->final_x) side_copy(Xof(s, nb), r->final_x);  // Q, unless the post-eval fails
         // the iteration kernels skip work once `done` is set: clear it for the
         // post-orth evaluation (solver.cpp:452) and restore it afterwards
         const int32_t zero = 0;
@@ -2587,10 +2589,10 @@ void session_finish(pcal_session* s, pcal_report* r) {
         PCAL_CUDA(cudaStreamSynchronize(s->stream));
         if (post[4] != 0.0) {
           status = PCAL_STATUS_DIVERGED;  // evaluation_error in the post-eval
+          if (r->final_x) PCAL_CUDA(cudaStreamSynchronize(cs));  // before final_x is rewritten
         } else {
           for (int i = 0; i < 4; ++i) r->final_post[i] = post[i];
           r->has_post = 1;
-          if (r->final_x) copy_out(s, Xof(s, nb), r->final_x);
           final_is_q = true;
         }
       }
