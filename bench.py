@@ -58,10 +58,10 @@ def load_peaks() -> dict:
     except Exception:
         pass
     try:
-        with open(os.path.join(ROOT, "profiles", "fp64_peaks_r01.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "fp64_peaks_r02.json")) as f:
             m = json.load(f)
         peaks["fp64_tflops"] = float(m["dmma_tflops"])
-        peaks["fp64_src"] = "measured DMMA.8x8x4 peak, profiles/fp64_peaks_r01.json"
+        peaks["fp64_src"] = "measured DMMA.8x8x4 peak at 1965 MHz, profiles/fp64_peaks_r02.json"
     except Exception:
         pass
     return peaks
