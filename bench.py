@@ -17,7 +17,7 @@ the largest configuration that fits one GPU).
           full iteration count + final orthonormalization, wall clock.
   roofline : dominant kernel, achieved = algorithmic flops (or bytes) per launch
           ÷ its mean CUDA-event duration measured in this run; peak = measured
-          FP64 DMMA rate (profiles/fp64_peaks_r01.json; MEASURED_PEAKS.json has
+          FP64 DMMA rate (profiles/fp64_peaks_r02.json; MEASURED_PEAKS.json has
           no FP64 entry) or MEASURED_PEAKS.json hbm_gbs for HBM-bound kernels.
   cpu_baseline : the UNMODIFIED reference solve() (oracle/_ref) on the host
           cores, per-iteration time from its own trace clock, bounded sample
