@@ -517,6 +517,10 @@ struct pcal_session {
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = true;
+  // sharded grid models (NCCL): the halo exchange runs on hstream while the
+  // interior planes of the stencil run on `stream` (ev_x: X ready, ev_h: halos in)
+  cudaStream_t hstream = nullptr;
+  cudaEvent_t ev_x = nullptr, ev_h = nullptr;
   // row sharding (null comm: the whole problem on this GPU)
   pcal::Comm* comm = nullptr;
   // reproducible reductions (every sharded session): fixed global row chunks
@@ -754,7 +758,8 @@ static void launch_colsums(pcal_session* s, const double* fp, int64_t nrb_f, con
 // 7-point stencil part of the grid models: z-marching kernel when the grid
 // allows it (nx ≤ 128, ny % 8 == 0), else the generic element kernel.
 static void launch_stencil_tma(pcal_session* s, int b, const double* u, bool ks, const Ctl* ctl,
-                               int xp, const double* hlo, const double* hhi, dim3 grid) {
+                               int xp, const double* hlo, const double* hhi, dim3 grid,
+                               int zmode = 0) {
   constexpr int TY = 8, NS = 4;
   const auto& m = s->model;
   const int64_t nx = m.nx, ny = m.ny, nz = s->gz, p = s->p;
@@ -779,7 +784,7 @@ static void launch_stencil_tma(pcal_session* s, int b, const double* u, bool ks,
   const int smem = (int)(NS * ((TY + 2) * nx + TY * nx) * 8 + 2 * NS * 8);
   const dim3 block(32 * (TY + 1));
   const int sh = hlo ? 1 : 0;
-#define PCAL_TMA_ST(KSV, XPV)                                                                     do {                                                                                             auto kern = k_stencil_tma<KSV, XPV, TY, NS>;                                                   PCAL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));      kern<<<grid, block, smem, s->stream>>>(mp, Pof(s, b), (int)nx, (int)ny, (int)nz, s->ld,                                               (int)s->st_zchunk, s->fpart.p, s->pstride_f,                                                   s->bad, ctl, sh, (int)s->st_zpart);                   } while (0)
+#define PCAL_TMA_ST(KSV, XPV)                                                                     do {                                                                                             auto kern = k_stencil_tma<KSV, XPV, TY, NS>;                                                   PCAL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));      kern<<<grid, block, smem, s->stream>>>(mp, Pof(s, b), (int)nx, (int)ny, (int)nz, s->ld,                                               (int)s->st_zchunk, s->fpart.p, s->pstride_f,                                                   s->bad, ctl, sh, (int)s->st_zpart, zmode);            } while (0)
   if (ks) {
     if (xp == 2) PCAL_TMA_ST(true, 2); else PCAL_TMA_ST(true, 4);
   } else {
@@ -797,20 +802,54 @@ static void launch_stencil(pcal_session* s, int b, const double* u, bool ks, con
     const int TY = 8;
     const double* hlo = nullptr;
     const double* hhi = nullptr;
+    dim3 grid((unsigned)(m.ny / TY), (unsigned)s->st_nzc, (unsigned)p);
+    dim3 block(32, TY);
+    const int xp = (int)ceil_div(m.nx, 32);
+    const int rxp0 = m.nx % 2 == 0 && m.nx <= 64 ? 2 : m.nx % 4 == 0 && m.nx <= 128 ? 4 : 0;
+    const bool tma = rxp0 && m.nx % 16 == 0 && !getenv("PCAL_NO_TMA_STENCIL");
     if (s->comm) {  // C5: exchange the boundary planes with the slab neighbours
       const int64_t nxy = m.nx * m.ny;
       double* h = s->halo.p;
       const size_t cnt = (size_t)p * nxy;
+      hlo = h + 2 * cnt;
+      hhi = h + 3 * cnt;
+      const int64_t zp = s->st_zpart;
+      // TMA stencil: the interior planes (no halo read) first, the two boundary
+      // row chunks after the exchange — with NCCL the exchange runs on a side
+      // stream under the interior planes; emulated ranks keep one stream
+      if (tma && s->gz > 2 * zp && !getenv("PCAL_NO_HALO_OVERLAP")) {
+        const bool side = s->hstream != nullptr;
+        cudaStream_t hs = side ? s->hstream : s->stream;
+        if (side) {
+          PCAL_CUDA(cudaEventRecord(s->ev_x, s->stream));
+          PCAL_CUDA(cudaStreamWaitEvent(hs, s->ev_x, 0));
+        }
+        const auto pack_and_exchange = [&]() {
+          k_pack_planes<<<dim3((unsigned)ceil_div(nxy, 256), (unsigned)p), 256, 0, hs>>>(
+              Xof(s, b), s->ld, nxy, s->gz, h, h + cnt, ctl);
+          launched("k_pack_planes");
+          s->comm->halo(h, h + cnt, h + 2 * cnt, h + 3 * cnt, cnt, hs);
+        };
+        if (side) pack_and_exchange();
+        dim3 gi = grid;
+        gi.y = (unsigned)ceil_div(s->gz - 2 * zp, s->st_zchunk);
+        launch_stencil_tma(s, b, u, ks, ctl, rxp0, hlo, hhi, gi, 1);
+        if (side) {
+          PCAL_CUDA(cudaEventRecord(s->ev_h, hs));
+          PCAL_CUDA(cudaStreamWaitEvent(s->stream, s->ev_h, 0));
+        } else {
+          pack_and_exchange();
+        }
+        dim3 gb = grid;
+        gb.y = 2;
+        launch_stencil_tma(s, b, u, ks, ctl, rxp0, hlo, hhi, gb, 2);
+        return;
+      }
       k_pack_planes<<<dim3((unsigned)ceil_div(nxy, 256), (unsigned)p), 256, 0, s->stream>>>(
           Xof(s, b), s->ld, nxy, s->gz, h, h + cnt, ctl);
       launched("k_pack_planes");
       s->comm->halo(h, h + cnt, h + 2 * cnt, h + 3 * cnt, cnt, s->stream);
-      hlo = h + 2 * cnt;
-      hhi = h + 3 * cnt;
     }
-    dim3 grid((unsigned)(m.ny / TY), (unsigned)s->st_nzc, (unsigned)p);
-    dim3 block(32, TY);
-    const int xp = (int)ceil_div(m.nx, 32);
 #define PCAL_MARCH(KSV, XPV)                                                                   \
   k_stencil_march<KSV, XPV, 8><<<grid, block, 0, s->stream>>>(                               \
       Xof(s, b), u, Pof(s, b), (int)m.nx, (int)m.ny, (int)s->gz, s->ld, (int)s->st_zchunk,     \
@@ -1632,6 +1671,11 @@ static void alloc_state(pcal_session* s) {
       s->xfull.zero(st);
     } else {  // C5: z-halo planes [send_lo | send_hi | recv_lo | recv_hi], p·nx·ny each
       s->halo.alloc((size_t)4 * p * m.nx * m.ny);
+      if (!s->comm->emulated()) {  // exchange overlapped with the interior planes
+        PCAL_CUDA(cudaStreamCreateWithFlags(&s->hstream, cudaStreamNonBlocking));
+        PCAL_CUDA(cudaEventCreateWithFlags(&s->ev_x, cudaEventDisableTiming));
+        PCAL_CUDA(cudaEventCreateWithFlags(&s->ev_h, cudaEventDisableTiming));
+      }
       if (m.kind == PCAL_MODEL_KOHN_SHAM) s->rho_gath.alloc((size_t)R * ld);
     }
     std::vector<int64_t> rr(2 * R);
@@ -1881,6 +1925,9 @@ pcal_session::~pcal_session() {
   if (ctl) cudaFree(ctl);
   if (h_ctl) cudaFreeHost(h_ctl);
   if (stream && own_stream) cudaStreamDestroy(stream);
+  if (hstream) cudaStreamDestroy(hstream);
+  if (ev_x) cudaEventDestroy(ev_x);
+  if (ev_h) cudaEventDestroy(ev_h);
 }
 
 using namespace pcal;

@@ -36,7 +36,7 @@ template <bool KS, int XP, int TY, int NS>
 __global__ void __launch_bounds__(32 * (TY + 1))
     k_stencil_tma(const __grid_constant__ StencilMaps maps, double* __restrict__ g, int nx, int ny,
                   int nz, int64_t ld, int zchunk, double* __restrict__ fpart, int64_t pstride,
-                  int32_t* bad, const Ctl* ctl, int sharded, int zpart) {
+                  int32_t* bad, const Ctl* ctl, int sharded, int zpart, int zmode) {
   static_assert(XP % 2 == 0, "full-row march: XP even (16-byte vectors)");
   constexpr int V = XP / 2;
   if (ctl && ctl->done) return;
@@ -50,8 +50,22 @@ __global__ void __launch_bounds__(32 * (TY + 1))
   __shared__ double sm[TY];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int y0 = blockIdx.x * TY;
-  const int z0 = blockIdx.y * zchunk;
-  const int z1 = min(nz, z0 + zchunk);
+  // zmode 0: z-chunks of the whole slab; 1: the interior planes [zpart, nz − zpart)
+  // (no halo plane read — they run while the halo exchange is in flight);
+  // 2: the two boundary row chunks [0, zpart) and [nz − zpart, nz).  Chunks
+  // start on multiples of zpart, so every f partial (zpart planes) is summed
+  // inside one CTA exactly as in mode 0.
+  int z0, z1;
+  if (zmode == 0) {
+    z0 = blockIdx.y * zchunk;
+    z1 = min(nz, z0 + zchunk);
+  } else if (zmode == 1) {
+    z0 = zpart + blockIdx.y * zchunk;
+    z1 = min(nz - zpart, z0 + zchunk);
+  } else {
+    z0 = blockIdx.y ? nz - zpart : 0;
+    z1 = z0 + zpart;
+  }
   const int j = blockIdx.z;
   const int nplanes = z1 - z0 + 2;  // planes z0 − 1 … z1
   if (threadIdx.x == 0) {

@@ -140,6 +140,22 @@ def test_nccl_single_rank_session(pcal, orc, kind):
     check_pair(r1, rs, window=40)
 
 
+@pytest.mark.parametrize("kind", ["stencil", "ks"])
+def test_halo_overlap_split_is_bitwise(pcal, orc, kind, monkeypatch):
+    """The sharded TMA stencil split into the interior planes (run while the
+    halo exchange is in flight) and the two boundary row chunks (after it) is
+    bitwise the one-launch march after the exchange (PCAL_NO_HALO_OVERLAP=1):
+    every f partial is summed inside one CTA in both."""
+    from paper_1810_03930_b200 import report_io
+    m, x0 = _scaling_case(pcal, orc, kind)
+    cfg = pcal.SolverConfig(tol_rel_kkt=TINY, max_iter=30)
+    split = [pcal.solve_emulated(m, cfg, x0, R) for R in (2, 3)]
+    monkeypatch.setenv("PCAL_NO_HALO_OVERLAP", "1")
+    whole = [pcal.solve_emulated(m, cfg, x0, R) for R in (2, 3)]
+    for a, b in zip(split, whole):
+        assert report_io.same_numerics(a, b)
+
+
 def _scaling_case(pcal, orc, kind):
     if kind == "dense":
         n, p = 1000, 20
