@@ -1759,6 +1759,13 @@ static void alloc_state(pcal_session* s) {
 
 static void upload_matrix(const double* src, int32_t loc, int64_t rows, int64_t cols, double* dst,
                           int64_t ld, cudaStream_t st) {
+  if (ld == rows) {  // contiguous: one linear copy (the DMA engines' full rate)
+    PCAL_CUDA(cudaMemcpyAsync(dst, src, sizeof(double) * rows * cols,
+                              loc == PCAL_DEVICE ? cudaMemcpyDeviceToDevice
+                                                 : cudaMemcpyHostToDevice,
+                              st));
+    return;
+  }
   PCAL_CUDA(cudaMemcpy2DAsync(dst, sizeof(double) * ld, src, sizeof(double) * rows,
                               sizeof(double) * rows, cols,
                               loc == PCAL_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
@@ -2549,9 +2556,18 @@ bool orthonormalize_dev(pcal_session* s, const double* x, double* q, double* scr
   return true;
 }
 
+// D2H of an n×p iterate (ld) into a column-major host array; a contiguous
+// layout (ld = n) is one linear copy
+static void d2h_matrix(const pcal_session* s, const double* dsrc, double* host, cudaStream_t st) {
+  if (s->ld == s->n)
+    PCAL_CUDA(cudaMemcpyAsync(host, dsrc, sizeof(double) * s->n * s->p, cudaMemcpyDeviceToHost, st));
+  else
+    PCAL_CUDA(cudaMemcpy2DAsync(host, sizeof(double) * s->n, dsrc, sizeof(double) * s->ld,
+                                sizeof(double) * s->n, s->p, cudaMemcpyDeviceToHost, st));
+}
+
 void copy_out(pcal_session* s, const double* dsrc, double* host) {
-  PCAL_CUDA(cudaMemcpy2DAsync(host, sizeof(double) * s->n, dsrc, sizeof(double) * s->ld,
-                              sizeof(double) * s->n, s->p, cudaMemcpyDeviceToHost, s->stream));
+  d2h_matrix(s, dsrc, host, s->stream);
 }
 
 void session_finish(pcal_session* s, pcal_report* r) {
@@ -2596,8 +2612,7 @@ void session_finish(pcal_session* s, pcal_report* r) {
       PCAL_CUDA(cudaEventRecord(ev, s->stream));
       PCAL_CUDA(cudaStreamWaitEvent(cs, ev, 0));
       PCAL_CUDA(cudaEventDestroy(ev));
-      PCAL_CUDA(cudaMemcpy2DAsync(host, sizeof(double) * s->n, dsrc, sizeof(double) * s->ld,
-                                  sizeof(double) * s->n, s->p, cudaMemcpyDeviceToHost, cs));
+      d2h_matrix(s, dsrc, host, cs);
     };
     struct StreamJoin {  // the side copies complete before the report is returned
       cudaStream_t* st;
