@@ -194,6 +194,92 @@ __global__ void __launch_bounds__(1024) k_chol_trinv_small(const double* __restr
   }
 }
 
+// Cholesky for kCholSmemP < p ≤ kCholWideP (L does not fit in shared memory):
+// the left-looking recurrence of k_cholesky with the factor stored TRANSPOSED,
+// u[k + i·ldu] = L(i, k), so every dot Σ_k L(i,k)·L(j,k) reads two contiguous
+// rows — one warp per row, lanes over k, fixed-order warp sums — and row j of L
+// staged in shared memory for the column's updates.  Same pivot floor.
+// (k_cholesky's thread-0 recurrence took ≈ 75 ms at p = 1024.)
+constexpr int kCholWideP = 2048;
+__global__ void __launch_bounds__(1024) k_cholesky_wide(const double* __restrict__ b,
+                                                        int64_t ldb, int p,
+                                                        const double* fro2_first,
+                                                        double* __restrict__ u, int64_t ldu,
+                                                        int32_t* status, const int32_t* prev_ok,
+                                                        const Ctl* ctl) {
+  __shared__ double s_row[kCholWideP];  // row j of L (k < j)
+  __shared__ double s_ljj;
+  __shared__ int s_ok;
+  if (ctl && ctl->done) return;
+  if (prev_ok && !*prev_ok) {
+    if (threadIdx.x == 0) *status = 0;
+    return;
+  }
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
+  const double floor_ = 1e-14 * sqrt(*fro2_first);
+  if (tid == 0) s_ok = 1;
+  for (int j = 0; j < p; ++j) {
+    // row j of L (written by the earlier columns) into shared memory
+    for (int k = tid; k < j; k += blockDim.x) s_row[k] = u[k + (int64_t)j * ldu];
+    __syncthreads();
+    if (warp == 0) {
+      double d = 0.0;
+      for (int k = lane; k < j; k += 32) d += s_row[k] * s_row[k];
+      d = warp_sum(d);
+      if (lane == 0) {
+        d = b[j + (int64_t)j * ldb] - d;
+        if (!(d > floor_)) s_ok = 0;
+        s_ljj = sqrt(d);
+        u[j + (int64_t)j * ldu] = s_ljj;
+      }
+    }
+    __syncthreads();
+    if (!s_ok) break;
+    const double ljj = s_ljj;
+    for (int i = j + 1 + warp; i < p; i += nw) {
+      const double* ui = u + (int64_t)i * ldu;
+      double acc = 0.0;
+      for (int k = lane; k < j; k += 32) acc += ui[k] * s_row[k];
+      acc = warp_sum(acc);
+      if (lane == 0) u[j + (int64_t)i * ldu] = (b[j + (int64_t)i * ldb] - acc) / ljj;  // B(j,i), upper
+    }
+    __syncthreads();
+  }
+  if (tid == 0) *status = s_ok;
+}
+
+// T = (L⁻¹)ᵀ from the transposed factor of k_cholesky_wide: one warp per column c
+// of L⁻¹ (forward substitution, lanes hold x_k for k ≡ lane mod 32, rows of L
+// read contiguously), T(c, i) = x_i.
+template <int NQ>  // p ≤ 32·NQ
+__global__ void __launch_bounds__(256) k_trinv_wide(const double* __restrict__ u, int64_t ldu,
+                                                    int p, double* __restrict__ t, int64_t ldt,
+                                                    const int32_t* status) {
+  if (!*status) return;
+  const int lane = threadIdx.x & 31;
+  const int c = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  if (c >= p) return;
+  double x[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) x[q] = 0.0;
+  for (int i = lane; i < c; i += 32) t[c + (int64_t)i * ldt] = 0.0;
+  for (int i = c; i < p; ++i) {
+    const double* ui = u + (int64_t)i * ldu;
+    double acc = 0.0;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int k = lane + 32 * q;
+      if (k >= c && k < i) acc += ui[k] * x[q];
+    }
+    acc = warp_sum(acc);
+    const double v = (((i == c) ? 1.0 : 0.0) - acc) / ui[i];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q)
+      if (lane + 32 * q == i) x[q] = v;
+    if (lane == (i & 31)) t[c + (int64_t)i * ldt] = v;
+  }
+}
+
 // mgs2 (kernels.cpp:212-246) fallback: one block, in place on q (= copy of X).
 __global__ void k_mgs2(double* __restrict__ q, int64_t n, int64_t ld, int64_t p,
                        const double* fro2_first, int32_t* status) {
@@ -1149,6 +1235,17 @@ static void launch_chol_trinv(cudaStream_t st, const double* b, int64_t ldb, int
     }
     k_chol_trinv_small<<<1, 1024, smem, st>>>(b, ldb, (int)p, f2, t, ldt, status, prev_ok, ctl);
     launched("k_chol_trinv_small");
+    return;
+  }
+  if (p <= kCholWideP) {  // l holds Lᵀ here (rows of L contiguous)
+    k_cholesky_wide<<<1, 1024, 0, st>>>(b, ldb, (int)p, f2, l, ldl, status, prev_ok, ctl);
+    launched("k_cholesky_wide");
+    const unsigned g = (unsigned)ceil_div(p, 8);
+    if (p <= 256) k_trinv_wide<8><<<g, 256, 0, st>>>(l, ldl, (int)p, t, ldt, status);
+    else if (p <= 512) k_trinv_wide<16><<<g, 256, 0, st>>>(l, ldl, (int)p, t, ldt, status);
+    else if (p <= 1024) k_trinv_wide<32><<<g, 256, 0, st>>>(l, ldl, (int)p, t, ldt, status);
+    else k_trinv_wide<kCholWideP / 32><<<g, 256, 0, st>>>(l, ldl, (int)p, t, ldt, status);
+    launched("k_trinv_wide");
     return;
   }
   k_cholesky<<<1, 1024, 0, st>>>(b, ldb, p, f2, l, ldl, status, prev_ok, ctl);
