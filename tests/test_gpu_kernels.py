@@ -68,6 +68,21 @@ def test_orthonormalize(pcal, orc, gold):
     assert np.abs(np.tril(r, -1)).max() <= 1e-10 * np.abs(r).max()
 
 
+@pytest.mark.parametrize("n,p", [(3000, 129), (4000, 300), (6000, 777), (4096, 1024)])
+def test_orthonormalize_wide_p(pcal, orc, n, p):
+    """CholeskyQR2 for 128 < p ≤ 2048 (k_cholesky_wide + k_trinv_wide: transposed
+    factor, warp-per-row dots; warp-per-column inverse) against the oracle's
+    orthonormalize (kernels.cpp:250-265) and the acceptance feasibility bar, for
+    p off and on the 32-column grid."""
+    x = orc.random_normal(n, p, 43)
+    q = pcal.orthonormalize(x)
+    assert pcal.last_orthonormalize_path() == "cholqr2"  # no MGS2 fallback
+    assert np.linalg.norm(q.T @ q - np.eye(p)) <= 1e-12  # acceptance_main.cpp:101
+    assert rel(q, orc.orthonormalize(x)) <= 1e-11
+    r = q.T @ x
+    assert np.abs(np.tril(r, -1)).max() <= 1e-10 * np.abs(r).max()
+
+
 def test_orthonormalize_rank_deficient(pcal, orc):
     x = orc.random_normal(40, 4, 42)
     x[:, 3] = x[:, 0] + x[:, 1]  # exactly dependent column (test_kernels.cpp:150-181)
