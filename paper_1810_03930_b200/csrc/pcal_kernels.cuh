@@ -429,6 +429,17 @@ __global__ void k_colscale(const double* __restrict__ colpart, int64_t nchunks, 
   inv[j] = exact ? 1.0 : 1.0 / sqrt(nz2);
 }
 
+// One element of the normalised step: z = x − (1/η)·(p − d_j·x) and z·(1/‖z_j‖),
+// with explicit roundings so k_update_norm and the fused stencil
+// (stencil_tma.cuh, FUSE) produce bitwise the same X_{k+1}.
+__device__ __forceinline__ double step_z(double x, double p, double dj, double inv_eta) {
+  return __fma_rn(-inv_eta, __fma_rn(-dj, x, p), x);
+}
+__device__ __forceinline__ double step_value(double x, double p, double dj, double inv_eta,
+                                             double sc) {
+  return __dmul_rn(step_z(x, p, dj, inv_eta), sc);
+}
+
 // X_{k+1} = (x − (1/η)·gl)·inv_j in one pass (flagged columns: z unscaled for
 // k_normalize's exact rule); npart as k_update (the exact ‖z‖² partials).
 __global__ void __launch_bounds__(kStreamThreads)
@@ -436,8 +447,9 @@ __global__ void __launch_bounds__(kStreamThreads)
                   const double* __restrict__ d, double* __restrict__ z, int64_t n, int64_t ld,
                   int64_t p, int64_t chunk, double* __restrict__ npart,
                   const double* __restrict__ inv, const int32_t* __restrict__ fb, Ctl* ctl,
-                  double* __restrict__ xpart = nullptr, int64_t cstride = 0) {
+                  double* __restrict__ xpart = nullptr, int64_t cstride = 0, int only_fb = 0) {
   if (ctl->done) return;
+  if (only_fb && !fb[blockIdx.y]) return;  // the fused stencil wrote this column
   __shared__ double sm[kStreamThreads / 32];
   const int64_t j = blockIdx.y;
   const int64_t r0 = (int64_t)blockIdx.x * chunk;
@@ -454,13 +466,13 @@ __global__ void __launch_bounds__(kStreamThreads)
   const int64_t h0 = r0 / 2, h1 = (r1 + 1) / 2;  // an odd n ends on a zero padding row
   for (int64_t h = h0 + threadIdx.x; h < h1; h += blockDim.x) {
     const double2 xv = xj[h], pv = pj[h];
-    const double v0 = xv.x - inv_eta * (pv.x - dj * xv.x);
-    const double v1 = xv.y - inv_eta * (pv.y - dj * xv.y);
+    const double v0 = step_z(xv.x, pv.x, dj, inv_eta);
+    const double v1 = step_z(xv.y, pv.y, dj, inv_eta);
     acc += v0 * v0;
     acc += v1 * v1;
     xacc += xv.x * xv.x;
     xacc += xv.y * xv.y;
-    const double w0 = v0 * sc, w1 = v1 * sc;
+    const double w0 = __dmul_rn(v0, sc), w1 = __dmul_rn(v1, sc);
     zj[h] = make_double2(w0, w1);
     bad |= !isfinite(w0) || !isfinite(w1);
   }

@@ -679,6 +679,10 @@ struct pcal_session {
   int64_t st_chunk = 0, st_nchunks = 0;
   bool st_march = false;
   bool fused_step = false;  // cooperative k_step_fused fits co-resident on the device
+  // stencil model, one GPU: the normalised step's X_{k+1} formed inside the
+  // TMA stencil (stencil_tma.cuh FUSE); grad_fused marks an iteration whose
+  // gradient already exists except for the exact-rule columns
+  bool step_stencil = false, grad_fused = false;
   bool mega = false;        // small dense problem: k_iter_small runs whole batches of iterations
   int mega_grid = 0;
   int64_t mega_lda_s = 0;   // > 0: k_iter_small keeps each CTA's 8 rows of A in shared memory
@@ -845,36 +849,54 @@ static void launch_colsums(pcal_session* s, const double* fp, int64_t nrb_f, con
 // allows it (nx ≤ 128, ny % 8 == 0), else the generic element kernel.
 static void launch_stencil_tma(pcal_session* s, int b, const double* u, bool ks, const Ctl* ctl,
                                int xp, const double* hlo, const double* hhi, dim3 grid,
-                               int zmode = 0) {
+                               int zmode = 0, const int32_t* only_fb = nullptr,
+                               const StepFuse* fuse = nullptr) {
   constexpr int TY = 8, NS = 4;
   const auto& m = s->model;
   const int64_t nx = m.nx, ny = m.ny, nz = s->gz, p = s->p;
+  // X operand: X of pair b, or (fused step) X_k of pair b with P_k beside it;
+  // output G into P of pair b, or (fused) P of the other pair
+  const double* xsrc = Xof(s, b);
+  double* gout = fuse ? Pof(s, 1 - b) : Pof(s, b);
   StencilMaps mp;
   {
     const int64_t d4[4] = {nx, ny, nz, p}, pt4[3] = {nx * 8, nx * ny * 8, s->ld * 8};
     const int bt[4] = {(int)nx, TY, 1, 1}, br[4] = {(int)nx, 1, 1, 1};
-    encode_tensor_map(&mp.x_tile, Xof(s, b), 4, d4, pt4, bt);
-    encode_tensor_map(&mp.x_row, Xof(s, b), 4, d4, pt4, br);
+    encode_tensor_map(&mp.x_tile, xsrc, 4, d4, pt4, bt);
+    encode_tensor_map(&mp.x_row, xsrc, 4, d4, pt4, br);
+    const double* psrc = fuse ? Pof(s, b) : xsrc;  // unused unless fused: any valid map
+    encode_tensor_map(&mp.p_tile, psrc, 4, d4, pt4, bt);
+    encode_tensor_map(&mp.p_row, psrc, 4, d4, pt4, br);
     const int64_t d3[3] = {nx, ny, nz}, pt3[2] = {nx * 8, nx * ny * 8};
     const int bu[3] = {(int)nx, TY, 1};
     encode_tensor_map(&mp.u_tile, u, 3, d3, pt3, bu);
     const int64_t dh[3] = {nx, ny, p}, pth[2] = {nx * 8, nx * ny * 8};
     const int bht[3] = {(int)nx, TY, 1}, bhr[3] = {(int)nx, 1, 1};
-    const double* lo = hlo ? hlo : Xof(s, b);  // unused without halos: any valid map
-    const double* hi = hhi ? hhi : Xof(s, b);
+    const double* lo = hlo ? hlo : xsrc;  // unused without halos: any valid map
+    const double* hi = hhi ? hhi : xsrc;
     encode_tensor_map(&mp.lo_tile, lo, 3, dh, pth, bht);
     encode_tensor_map(&mp.lo_row, lo, 3, dh, pth, bhr);
     encode_tensor_map(&mp.hi_tile, hi, 3, dh, pth, bht);
     encode_tensor_map(&mp.hi_row, hi, 3, dh, pth, bhr);
   }
-  const int smem = (int)(NS * ((TY + 2) * nx + TY * nx) * 8 + 2 * NS * 8);
+  const int smem = (int)(NS * ((TY + 2) * nx * (fuse ? 2 : 1) + TY * nx) * 8 + 2 * NS * 8);
   const dim3 block(32 * (TY + 1));
   const int sh = hlo ? 1 : 0;
-#define PCAL_TMA_ST(KSV, XPV)                                                                     do {                                                                                             auto kern = k_stencil_tma<KSV, XPV, TY, NS>;                                                   PCAL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));      kern<<<grid, block, smem, s->stream>>>(mp, Pof(s, b), (int)nx, (int)ny, (int)nz, s->ld,                                               (int)s->st_zchunk, s->fpart.p, s->pstride_f,                                                   s->bad, ctl, sh, (int)s->st_zpart, zmode);            } while (0)
-  if (ks) {
-    if (xp == 2) PCAL_TMA_ST(true, 2); else PCAL_TMA_ST(true, 4);
+  const StepFuse sf = fuse ? *fuse : StepFuse{};
+#define PCAL_TMA_ST(KSV, XPV, FV)                                                                 \
+  do {                                                                                            \
+    auto kern = k_stencil_tma<KSV, XPV, TY, NS, FV>;                                             \
+    PCAL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));    \
+    kern<<<grid, block, smem, s->stream>>>(mp, gout, (int)nx, (int)ny, (int)nz, s->ld,           \
+                                           (int)s->st_zchunk, s->fpart.p, s->pstride_f, s->bad,  \
+                                           ctl, sh, (int)s->st_zpart, zmode, only_fb, sf);       \
+  } while (0)
+  if (fuse) {  // the stencil model only (Kohn–Sham needs ρ of all of X_{k+1} first)
+    if (xp == 2) PCAL_TMA_ST(false, 2, true); else PCAL_TMA_ST(false, 4, true);
+  } else if (ks) {
+    if (xp == 2) PCAL_TMA_ST(true, 2, false); else PCAL_TMA_ST(true, 4, false);
   } else {
-    if (xp == 2) PCAL_TMA_ST(false, 2); else PCAL_TMA_ST(false, 4);
+    if (xp == 2) PCAL_TMA_ST(false, 2, false); else PCAL_TMA_ST(false, 4, false);
   }
 #undef PCAL_TMA_ST
   launched("k_stencil_tma");
@@ -949,7 +971,9 @@ static void launch_stencil(pcal_session* s, int b, const double* u, bool ks, con
     // multiple of 16 points (128-byte TMA rows): its TMA-staged form
     const int rxp = m.nx % 2 == 0 && m.nx <= 64 ? 2 : m.nx % 4 == 0 && m.nx <= 128 ? 4 : 0;
     if (rxp && m.nx % 16 == 0 && !getenv("PCAL_NO_TMA_STENCIL")) {
-      launch_stencil_tma(s, b, u, ks, ctl, rxp, hlo, hhi, grid);
+      // after the fused step only the exact-rule columns are left
+      launch_stencil_tma(s, b, u, ks, ctl, rxp, hlo, hhi, grid, 0, s->grad_fused ? s->sfb : nullptr);
+      s->grad_fused = false;
       return;
     }
     if (rxp && !getenv("PCAL_NO_ROW_MARCH")) {
@@ -1368,9 +1392,19 @@ static void launch_iteration(pcal_session* s, int b) {
     k_colscale<<<(unsigned)ceil_div(s->p, 128), 128, 0, st>>>(s->colpart.p, s->up_nchunks, s->p,
                                                               s->sinv.p, s->sfb, s->ctl);
     launched("k_colscale");
+    if (s->step_stencil) {  // X_{k+1} and G_{k+1} in one pass; flagged columns below
+      const auto& m = s->model;
+      const StepFuse sf{Xof(s, nb), Dvec(s, b), s->sinv.p, s->sfb, s->ctl};
+      dim3 grid((unsigned)(m.ny / 8), (unsigned)s->st_nzc, (unsigned)s->p);
+      const int rxp = m.nx % 2 == 0 && m.nx <= 64 ? 2 : 4;
+      launch_stencil_tma(s, b, s->V.p, false, s->ctl, rxp, nullptr, nullptr, grid, 0, nullptr,
+                         &sf);
+      s->grad_fused = true;
+    }
     k_update_norm<<<gu, kStreamThreads, 0, st>>>(Xof(s, b), Pof(s, b), Dvec(s, b), Xof(s, nb),
                                                  s->n, s->ld, s->p, s->up_chunk, s->npart.p,
-                                                 s->sinv.p, s->sfb, s->ctl);
+                                                 s->sinv.p, s->sfb, s->ctl, nullptr, 0,
+                                                 s->step_stencil ? 1 : 0);
     launched("k_update_norm");
     k_normalize<<<gu, kStreamThreads, 0, st>>>(Xof(s, b), Xof(s, nb), s->n, s->ld, s->p,
                                                s->up_chunk, s->up_nchunks, s->npart.p, nullptr,
@@ -1808,6 +1842,14 @@ static void alloc_state(pcal_session* s) {
     // the cooperative kernel wins while launch gaps dominate (≤ 8M elements);
     // beyond that the separate kernels stream better
     s->fused_step = coop && per_sm >= 4 && n * p <= (int64_t)8 << 20;
+  }
+  {
+    const auto& m = s->model;
+    const int rxp = m.nx % 2 == 0 && m.nx <= 64 ? 2 : m.nx % 4 == 0 && m.nx <= 128 ? 4 : 0;
+    s->step_stencil = !s->comm && !s->fused_step && m.kind == PCAL_MODEL_STENCIL && s->st_march &&
+                      rxp && m.nx % 16 == 0 && s->alg == PCAL_ALG_PCAL &&
+                      !getenv("PCAL_NO_TMA_STENCIL") && !getenv("PCAL_TWO_PASS_NORMALIZE") &&
+                      !getenv("PCAL_NO_FUSED_STEP");
   }
   s->bbpart.alloc((size_t)3 * s->bb_blocks);
   s->up_chunk = std::max<int64_t>(1024, round_up(ceil_div(n * p, 8 * 148 * 4), 256));

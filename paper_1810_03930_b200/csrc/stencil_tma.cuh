@@ -30,22 +30,44 @@ struct alignas(64) StencilMaps {
   CUtensorMap lo_tile, lo_row;  // plane −1 of the slab (sharded), box {nx, TY, 1} / {nx, 1, 1}
   CUtensorMap hi_tile, hi_row;  // plane nz
   CUtensorMap u_tile;           // box {nx, TY, 1}
+  CUtensorMap p_tile, p_row;    // STEP: P_k as X (the fused normalised step)
 };
 
-template <bool KS, int XP, int TY, int NS>
+// The fused normalised step (FUSE): the kernel reads X_k and P_k instead of
+// X_{k+1} and forms every X_{k+1} value it uses as k_update_norm does,
+// x⁺ = (x − (1/η)·(p − d_j·x))·(1/‖z_j‖) — one expression shared by both
+// kernels, so X_{k+1} and G are bitwise the unfused path's — writing X_{k+1}
+// of its own rows beside G: the step's write of X_{k+1} and the stencil's
+// re-read of it become one pass (16np instead of 24np + 16np bytes).  Columns
+// flagged for the exact two-pass rule (k_colscale) are skipped here and take
+// k_update_norm → k_normalize → the plain stencil.
+struct StepFuse {
+  double* xplus;        // X_{k+1} (ld)
+  const double* d;      // d_j of X_k
+  const double* inv;    // 1/‖z_j‖
+  const int32_t* fb;    // exact-rule flags (skipped columns)
+  Ctl* ctl;             // η; step_bad / done on a non-finite X_{k+1}
+};
+
+template <bool KS, int XP, int TY, int NS, bool FUSE = false>
 __global__ void __launch_bounds__(32 * (TY + 1))
     k_stencil_tma(const __grid_constant__ StencilMaps maps, double* __restrict__ g, int nx, int ny,
                   int nz, int64_t ld, int zchunk, double* __restrict__ fpart, int64_t pstride,
-                  int32_t* bad, const Ctl* ctl, int sharded, int zpart, int zmode) {
+                  int32_t* bad, const Ctl* ctl, int sharded, int zpart, int zmode,
+                  const int32_t* only_fb, StepFuse sf) {
   static_assert(XP % 2 == 0, "full-row march: XP even (16-byte vectors)");
   constexpr int V = XP / 2;
   if (ctl && ctl->done) return;
+  const int j = blockIdx.z;
+  if (only_fb && !only_fb[j]) return;  // the fused step already produced this column
+  if (FUSE && sf.fb[j]) return;        // exact-rule column: the unfused path
   extern __shared__ __align__(128) double st_smem[];
   const int W = nx;                              // doubles per row
   const int XT = (TY + 2) * W, UT = TY * W;      // slot sizes (doubles)
   double* xs = st_smem;                          // [NS][TY + 2][nx]
   double* us = xs + NS * XT;                     // [NS][TY][nx]
-  uint64_t* full = reinterpret_cast<uint64_t*>(us + NS * UT);
+  double* ps = us + NS * UT;                     // FUSE: [NS][TY + 2][nx] of P_k
+  uint64_t* full = reinterpret_cast<uint64_t*>(FUSE ? ps + NS * XT : us + NS * UT);
   uint64_t* empty = full + NS;
   __shared__ double sm[TY];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -66,7 +88,6 @@ __global__ void __launch_bounds__(32 * (TY + 1))
     z0 = blockIdx.y ? nz - zpart : 0;
     z1 = z0 + zpart;
   }
-  const int j = blockIdx.z;
   const int nplanes = z1 - z0 + 2;  // planes z0 − 1 … z1
   if (threadIdx.x == 0) {
     for (int i = 0; i < NS; ++i) {
@@ -90,7 +111,7 @@ __global__ void __launch_bounds__(32 * (TY + 1))
   if (warp == TY) {  // ---- producer: one lane drives the TMA unit
     if (lane != 0) return;
     const int yl = y0 == 0 ? ny - 1 : y0 - 1, yh = y0 + TY == ny ? 0 : y0 + TY;
-    const unsigned bytes = (unsigned)((XT + UT) * 8);
+    const unsigned bytes = (unsigned)((XT + UT + (FUSE ? XT : 0)) * 8);
     for (int i = 0; i < nplanes; ++i) {
       const int s = i % NS;
       wait(&empty[s], ((unsigned)(i / NS) & 1u) ^ 1u);
@@ -129,6 +150,12 @@ __global__ void __launch_bounds__(32 * (TY + 1))
         ld4(xd + W, &maps.x_tile, 0, y0, zz, j);
         ld4(xd, &maps.x_row, 0, yl, zz, j);
         ld4(xd + (TY + 1) * W, &maps.x_row, 0, yh, zz, j);
+        if (FUSE) {
+          double* pd = ps + s * XT;
+          ld4(pd + W, &maps.p_tile, 0, y0, zz, j);
+          ld4(pd, &maps.p_row, 0, yl, zz, j);
+          ld4(pd + (TY + 1) * W, &maps.p_row, 0, yh, zz, j);
+        }
       }
       // u of plane z (needed for z0 … z1−1; the two end planes load a valid
       // plane so every slot carries the same byte count)
@@ -145,7 +172,29 @@ __global__ void __launch_bounds__(32 * (TY + 1))
   const int y = y0 + ty;
   const int64_t nxy = (int64_t)nx * ny;
   double* gj = g + (int64_t)j * ld;
+  // FUSE: the step's scalars of column j
+  double f_ie = 0.0, f_dj = 0.0, f_sc = 1.0;
+  if (FUSE) {
+    f_ie = 1.0 / sf.ctl->eta;
+    f_dj = sf.d[j];
+    f_sc = sf.inv[j];
+  }
+  // X values of a slot (FUSE: X_{k+1} formed from the X_k and P_k slots)
   auto rd = [&](const double* p, double (&d)[XP]) {
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const double2 t = reinterpret_cast<const double2*>(p)[v];
+      if (FUSE) {
+        const double2 q = reinterpret_cast<const double2*>(p + (ps - xs))[v];
+        d[2 * v] = step_value(t.x, q.x, f_dj, f_ie, f_sc);
+        d[2 * v + 1] = step_value(t.y, q.y, f_dj, f_ie, f_sc);
+      } else {
+        d[2 * v] = t.x;
+        d[2 * v + 1] = t.y;
+      }
+    }
+  };
+  auto rdu = [&](const double* p, double (&d)[XP]) {  // potential (never transformed)
 #pragma unroll
     for (int v = 0; v < V; ++v) {
       const double2 t = reinterpret_cast<const double2*>(p)[v];
@@ -166,7 +215,7 @@ __global__ void __launch_bounds__(32 * (TY + 1))
   wait(&full[1 % NS], (unsigned)(1 / NS) & 1u);
   rd(xs + (1 % NS) * XT + own, cur);
   double acc = 0.0;
-  bool nonfinite = false;
+  bool nonfinite = false, xbad = false;
   int zp_cnt = z0 % zpart, zp_idx = z0 / zpart;
   for (int z = z0; z < z1; ++z) {
     const int ic = z - z0 + 1, ia = ic + 1;  // slots of planes z and z + 1
@@ -177,7 +226,7 @@ __global__ void __launch_bounds__(32 * (TY + 1))
     double dn[XP], up[XP], uc[XP];
     rd(xc + ty * W + XP * ln, dn);
     rd(xc + (ty + 2) * W + XP * ln, up);
-    rd(us + sc * UT + ty * W + XP * ln, uc);
+    rdu(us + sc * UT + ty * W + XP * ln, uc);
     const double left = __shfl_sync(0xffffffffu, cur[XP - 1], lsrc);
     const double right = __shfl_sync(0xffffffffu, cur[0], rsrc);
     double gv[XP];
@@ -202,6 +251,15 @@ __global__ void __launch_bounds__(32 * (TY + 1))
       double2* gout = reinterpret_cast<double2*>(gj + (int64_t)z * nxy + (int64_t)y * nx + XP * ln);
 #pragma unroll
       for (int v = 0; v < V; ++v) gout[v] = make_double2(gv[2 * v], gv[2 * v + 1]);
+      if (FUSE) {  // X_{k+1} of the own points (k_update_norm's store)
+        double2* xout = reinterpret_cast<double2*>(sf.xplus + (int64_t)j * ld + (int64_t)z * nxy +
+                                                   (int64_t)y * nx + XP * ln);
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          xout[v] = make_double2(cur[2 * v], cur[2 * v + 1]);
+          xbad |= !isfinite(cur[2 * v]) || !isfinite(cur[2 * v + 1]);
+        }
+      }
     }
     // every lane has consumed what it read from slot sc (plane z) — and, at the
     // first plane, from slot 0 (plane z0 − 1): the stores above depend on it
@@ -242,6 +300,10 @@ __global__ void __launch_bounds__(32 * (TY + 1))
       asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar_addr(&empty[il % NS])) : "memory");
   }
   if (__any_sync(0xffffffffu, nonfinite) && lane == 0) *bad = 1;
+  if (FUSE && __any_sync(0xffffffffu, xbad) && lane == 0) {  // k_update_norm's divergence rule
+    sf.ctl->step_bad = 1;
+    sf.ctl->done = 2;
+  }
 }
 
 }  // namespace pcal
